@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the filtered PIM matrix exponential (arXiv 2110.04493) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 5] [--plan-norm one|fro] [--eps-tol 1e-16]
+
+One step = one whole e^H through the C ABI: sexpm_plan (validation, device norm,
+Eq. 4.20 plan, H0 = H 2^-N) + sexpm_run (filtered Taylor phase, N filtered squarings,
+E = I + T^_N) + sexpm_destroy, with H resident in HBM.  Workload: BASELINE.json config 5
+(n = 1449^2 2D Dirichlet heat, r = 0.5, the configuration the north-star target names),
+synthetic and seeded.  N > 1: torchrun, one rank per GPU, contiguous row blocks with an
+NCCL halo exchange per squaring (strong scaling: the job is one e^H).
+
+Prints ONE JSON line on rank 0.  `value` = e^H per second for the whole job (K / max over
+ranks of the device time of the K timed steps).  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "e^H wall time & squarings/s; achieved HBM GB/s vs peak, 1/2/4/8 B200"
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # derived: SMs x fp64 FMA lanes x 2 x max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--plan-norm", default="one", choices=["one", "fro"])
+    ap.add_argument("--eps-tol", type=float, default=1e-16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-grid", type=int, default=0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------------------
+def cpu_oracle_sample(args, target_seconds=12.0, grid=0):
+    """The oracle as it stands (OpenMP over rows, all host cores) on a bounded sample of
+    the workload: the same law (config 5: uniform 2D Dirichlet heat, r = 0.5, same plan
+    options) on a g x g grid; scaled to config 5's size by rows (interior rows carry the
+    same work).  Returns (e^H/s scaled, cores, sample description, seconds)."""
+    import oracle as O
+    from synth import make_config
+    cores = os.cpu_count() or 1
+    n_full = make_config_n(args.config)
+    g = grid or 48
+    while True:
+        H = make_config(args.config, scale_down=g)
+        t0 = time.perf_counter()
+        O.expm(H, args.eps_tol, plan_norm=args.plan_norm, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if dt >= target_seconds / 4 or grid or g >= 400:
+            break
+        g = int(g * 1.6)
+    rows_per_s = H.n / dt
+    value = rows_per_s / n_full  # e^H per second at full size
+    return value, cores, f"config {args.config} law on a {g}x{g} grid (n={H.n}), scaled by rows to n={n_full}", dt
+
+
+def make_config_n(cid):
+    from synth.configs import CONFIGS
+    return CONFIGS[cid]["n"]
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return  # other ranks exit without work
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, cores, sample, dt = cpu_oracle_sample(args, grid=args.cpu_sample_grid or 64)
+        if i >= args.warmup:
+            vals.append(v)
+    value = sum(vals) / len(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "e^H/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {args.config}", "eps_tol": args.eps_tol,
+                       "plan_norm": args.plan_norm},
+            "cpu_baseline": {"value": value, "unit": "e^H/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "e^H/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2110_04493_b200 import binding as B
+    from paper_2110_04493_b200.build import build
+    if rank == 0:
+        build()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    B.lib()
+    from synth import make_config
+    H = make_config(args.config)
+    n = H.n
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        uid = [B.sexpm_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = B.sexpm_nccl_comm_init(rank, world, uid[0])
+        # contiguous row blocks balanced by a squaring-work proxy (row nnz^2)
+        w = np.diff(H.rowptr).astype(np.float64) ** 2
+        bounds = B.sexpm_partition_rows(n, w, world)
+    else:
+        bounds = np.array([0, n], np.int64)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    Hl = H.rows(r0, r1)
+    rp = torch.from_numpy(Hl.rowptr).to(dev)
+    ci = torch.from_numpy(Hl.col).to(dev)
+    va = torch.from_numpy(Hl.val).to(dev)
+    stream = torch.cuda.current_stream()
+    opts = dict(plan_norm=args.plan_norm)
+    l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_step():
+        p = B.Plan(n, rp, ci, va, args.eps_tol, row_begin=r0, row_end=r1, nccl_comm=comm,
+                   stream=stream, **opts)
+        out = p.run_only()
+        st = p.stats()
+        p.close()
+        return out, st
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    launches0 = B.sexpm_kernel_launches()
+    times = []
+    stats = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            l2_flush.zero_()  # flush L2 between timed steps (outside the timed span)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out, st = one_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            stats.append(st)
+        barrier()
+    launches = B.sexpm_kernel_launches() - launches0
+    total_ms = sum(times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = 1000.0 / ms_per_step
+    st = stats[-1]
+    N = int(st["N"])
+
+    # ---------------- end to end through the C ABI with HOST buffers ----------------
+    e2e = None
+    est_out_bytes = int(st["nnz_out"]) * 12 + (r1 - r0 + 1) * 8
+    try:
+        avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+    except Exception:
+        avail = 0
+    if est_out_bytes > 0.25 * avail:
+        e2e = {"value": None, "unit": "e^H/s", "skipped": f"pinned result buffer {est_out_bytes/1e9:.1f} GB > 25% of host MemAvailable {avail/1e9:.1f} GB"}
+    elif not args.no_e2e:
+        hrp = torch.from_numpy(Hl.rowptr).pin_memory().numpy()
+        hci = torch.from_numpy(Hl.col).pin_memory().numpy()
+        hva = torch.from_numpy(Hl.val).pin_memory().numpy()
+        nnz_out = int(st["nnz_out"]) if world == 1 else None
+        outbufs = None
+        e2e_times = []
+        h2d = hrp.nbytes + hci.nbytes + hva.nbytes
+        d2h = 0
+        for it in range(2 if world == 1 else 0):
+            barrier()
+            t0 = time.perf_counter()
+            o = B.sexpm_options_init(plan_norm=args.plan_norm)
+            o.stream = stream.cuda_stream
+            Hin = B._csr_in(n, hrp, hci, hva, r0, r1, host=True)
+            h = B.sexpm_plan_host(Hin, args.eps_tol, o)
+            E = B.sexpm_run(h)
+            if outbufs is None or outbufs[1].numel() < E.nnz:
+                outbufs = (torch.empty(r1 - r0 + 1, dtype=torch.int64).pin_memory(),
+                           torch.empty(max(E.nnz, 1), dtype=torch.int32).pin_memory(),
+                           torch.empty(max(E.nnz, 1), dtype=torch.float64).pin_memory())
+                if it == 0:
+                    B.sexpm_destroy(h)
+                    continue  # first pass only sizes the pinned buffers
+            B.sexpm_result_copy(h, outbufs[0].data_ptr(), outbufs[1].data_ptr(), outbufs[2].data_ptr())
+            B.sexpm_destroy(h)
+            torch.cuda.synchronize()
+            e2e_times.append(time.perf_counter() - t0)
+            d2h = (r1 - r0 + 1) * 8 + E.nnz * 12
+        if e2e_times:
+            e2e = {"value": 1.0 / min(e2e_times), "unit": "e^H/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h),
+                   "note": "sexpm_plan_host (H2D of H from pinned memory) + sexpm_run + "
+                           "sexpm_result_copy (D2H of E into pinned memory), wall clock"}
+
+    # ---------------- roofline of the dominant kernel ----------------
+    import math
+    sq_ms = [float(st["sq_numeric_ms"][i]) for i in range(1, N + 1)]
+    sq_fl = [2.0 * float(st["sq_fmas"][i]) for i in range(1, N + 1)]
+    ty_idx = [i for i in range(2, int(st["M"]) + 1) if st["taylor_numeric_ms"][i] > 0]
+    ty_ms = [float(st["taylor_numeric_ms"][i]) for i in ty_idx]
+    ty_by = [float(st["taylor_numeric_bytes"][i]) for i in ty_idx]
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    if sum(sq_ms) >= sum(ty_ms) and sq_ms:
+        dur = sum(sq_ms) / len(sq_ms) / 1e3
+        ach = sum(sq_fl) / len(sq_fl) / dur / 1e12
+        roof = {"kernel": "k_numeric (squaring SpGEMM + 2T + filter classify)", "bound": "alu",
+                "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "derived fp64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)",
+                "launches_per_step": len(sq_ms), "avg_launch_ms": dur * 1e3,
+                "hbm_gbs_compulsory": sum(float(st["sq_numeric_bytes"][i]) for i in range(1, N + 1)) / len(sq_ms) / dur / 1e9}
+    elif ty_ms:
+        dur = sum(ty_ms) / len(ty_ms) / 1e3
+        ach = sum(ty_by) / len(ty_by) / dur / 1e9
+        roof = {"kernel": "k_numeric (Taylor term S H0 / i + filter classify)", "bound": "hbm",
+                "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "launches_per_step": len(ty_ms), "avg_launch_ms": dur * 1e3}
+    else:
+        roof = None
+
+    sq_total_ms = float(sum(st["sq_ms"][1:N + 1]))
+    line = {
+        "metric": METRIC, "value": value, "unit": "e^H/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE.json config law)",
+        "config": {"workload": f"BASELINE config {args.config}: 2D Dirichlet heat 1449x1449 r=0.5"
+                   if args.config == 5 else f"BASELINE config {args.config}",
+                   "n": n, "nnz_H": int(H.nnz), "eps_tol": args.eps_tol, "plan_norm": args.plan_norm,
+                   "M": int(st["M"]), "N": N, "M_eff": int(st["M_eff"]), "nnz_E": int(st["nnz_out"]),
+                   "parallelism": f"rows{world}", "l2": "flushed (256 MB write) between timed steps; working set >> L2"},
+        "expm_wall_s": ms_per_step / 1e3,
+        "squarings_per_s": (N / (sq_total_ms / 1e3)) if N and sq_total_ms > 0 else None,
+        "phase_ms": {"plan": float(st["ms_plan"]), "taylor": float(st["ms_taylor"]),
+                     "squaring": float(st["ms_squaring"]), "finalize": float(st["ms_finalize"])},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+    }
+    if rank == 0:
+        line["clocks"] = clk.summary()
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, sample, dt = cpu_oracle_sample(args, grid=args.cpu_sample_grid)
+            line["cpu_baseline"] = {"value": v, "unit": "e^H/s", "cores": cores, "kind": "oracle",
+                                    "sample": sample, "sample_seconds": dt}
+        print(json.dumps(line, default=lambda o: float(o) if hasattr(o, "__float__") else str(o)),
+              flush=True)
+    if comm is not None:
+        B.sexpm_nccl_comm_destroy(comm)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,205 @@
+/*
+ * sexpm.h — C ABI of libsexpm: the filtered precise-integration (PIM)
+ * scaling-and-squaring matrix exponential of arXiv 2110.04493 on B200 (sm_100a).
+ *
+ * PAPER.md citations are P:<line> (Wu, Zhang, Zhu, Hu, "High-performance
+ * computation of large sparse matrix exponential").
+ *
+ * What the library computes (Algorithm 4.2):
+ *   1. (M, N) from Eq. (4.20) with the plan norm (1-norm by default;
+ *      Frobenius as in the paper's experiments);
+ *   2. a = 1/(N+1) if H is normal else min(1, 1/||H||) (Eq. 4.19);
+ *   3. filtered Taylor phase on H0 = H 2^-N: S^_1 = H0, S~_i = S^_{i-1} H0 / i,
+ *      S^_i = Alg4.1(S~_i, eps_g^(0)), T^_0 = sum S^_i, eps_g^(0) = a r0/(M e^{2||H0||})
+ *      (Eq. 4.10-4.14);
+ *   4. N filtered squarings T~_i = 2 T^_{i-1} + T^_{i-1}^2, T^_i = Alg4.1(T~_i, eps_g^(i))
+ *      (Eq. 2.7, Eq. 4.15), eps_g^(i) = a r_i ||I + T^_{i-1}||_F
+ *      (reading R4 of DESIGN.md; option ABS gives a r_i as printed at P:422);
+ *   5. e^H = I + T^_N.
+ * Algorithm 4.1 is the adaptive drop filter of P:360-380 (strict '>' keep).
+ * All arithmetic is IEEE fp64.
+ *
+ * Memory / ownership conventions
+ *   - Every pointer inside sexpm_csr_in / sexpm_csr_out is a CUDA DEVICE pointer on the
+ *     caller's current device, except in sexpm_plan_host (HOST pointers) and
+ *     sexpm_result_copy (host or device pointers).
+ *   - CSR: int64 rowptr (row_end - row_begin + 1 entries, rowptr[0] == 0), int32 column
+ *     indices (global, strictly increasing within a row), fp64 values (finite, nonzero).
+ *   - Inputs are borrowed: the library copies what it needs during sexpm_plan*; the caller
+ *     may free them when the call returns.
+ *   - Outputs (sexpm_csr_out) are owned by the plan and stay valid until the next
+ *     sexpm_run on the same plan or sexpm_destroy.
+ *   - A plan is bound to one device and one CUDA stream and is not thread-safe.
+ *   - With world > 1 (an NCCL communicator in the options), sexpm_plan / sexpm_run are
+ *     collective: every rank passes its own contiguous row block and gets its row block
+ *     of e^H back.
+ *
+ * Errors: every entry point returns an sexpm_status; no exception crosses the ABI;
+ * sexpm_last_error() returns a thread-local message for the last non-OK status.
+ * Sticky CUDA errors map to SEXPM_ECUDA.
+ */
+#ifndef SEXPM_H
+#define SEXPM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SEXPM_OK = 0,
+  SEXPM_EINVAL = 1,        /* bad argument / malformed CSR / n == 0 */
+  SEXPM_ENONFINITE = 2,    /* H holds a NaN or Inf */
+  SEXPM_ETOL = 3,          /* eps_tol below the unit roundoff reading (R13: eps_tol >= 1e-16) */
+  SEXPM_EINFEASIBLE = 4,   /* Eq. (4.20) has no solution with M <= m_cap in the N window */
+  SEXPM_ENOMEM = 5,        /* device allocation failed */
+  SEXPM_ECUDA = 6,         /* CUDA runtime error */
+  SEXPM_ENCCL = 7,         /* NCCL error / NCCL unavailable */
+  SEXPM_ESTATE = 8,        /* call out of order (e.g. stats before run) */
+  SEXPM_EINTERNAL = 9      /* invariant violated (e.g. Algorithm 4.1 pass cap) */
+} sexpm_status;
+
+typedef struct sexpm_plan_s *sexpm_plan_t;
+
+typedef struct {
+  int64_t n;                  /* global dimension (n >= 1) */
+  int64_t row_begin, row_end; /* rows held by this rank; [0, n) on one GPU */
+  int64_t nnz;                /* entries in this row block */
+  const int64_t *rowptr;      /* row_end - row_begin + 1 entries, rowptr[0] == 0 */
+  const int32_t *colidx;      /* global columns, strictly increasing within a row */
+  const double *vals;         /* finite; explicit zeros are allowed and ignored */
+} sexpm_csr_in;
+
+typedef struct {
+  int64_t n, row_begin, row_end, nnz;
+  const int64_t *rowptr; /* device, plan-owned */
+  const int32_t *colidx;
+  const double *vals;
+} sexpm_csr_out;
+
+typedef struct {
+  uint32_t struct_size;   /* = sizeof(sexpm_options) (ABI check) */
+  int32_t plan_norm;      /* 0 = 1-norm (default, BASELINE north star), 1 = Frobenius */
+  int32_t normal;         /* -1 auto: bit-exact symmetric or skew-symmetric => normal; 0 no; 1 yes */
+  int32_t threshold_mode; /* 0 = a r_i ||I+T^_{i-1}||_F (default, R4); 1 = a r_i (P:422 as printed) */
+  int32_t filter;         /* 1 = paper's filter (default); 0 = unfiltered PIM (all eps_g = 0) */
+  int32_t m_cap;          /* max Taylor order in Eq. (4.20) enumeration (default 120) */
+  int32_t n_window;       /* N in [N0, N0 + n_window] (default 50) */
+  int32_t force_M;        /* -1 = from Eq. (4.20) */
+  int32_t force_N;        /* -1 = from Eq. (4.20) */
+  int32_t output_T;       /* 0 = return E = I + T^_N (default); 1 = return T^_N */
+  int32_t window_cols;    /* dense accumulator window in columns (0 = default 8192) */
+  double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
+  void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
+  void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */
+} sexpm_options;
+
+#define SEXPM_MAXSTEP 160
+
+typedef struct {
+  uint32_t struct_size;
+  int32_t M, N, M_eff, normal, world, rank;
+  double norm, a, r0, eps_g0;
+  /* Taylor terms i = 2..M at index i */
+  int64_t taylor_nnz_unf[SEXPM_MAXSTEP]; /* distinct nonzeros of S~_i */
+  int64_t taylor_nnz[SEXPM_MAXSTEP];     /* nnz of S^_i after Algorithm 4.1 */
+  int32_t taylor_passes[SEXPM_MAXSTEP];
+  double taylor_tau[SEXPM_MAXSTEP];      /* final Algorithm 4.1 threshold */
+  double taylor_ms[SEXPM_MAXSTEP];
+  double taylor_numeric_ms[SEXPM_MAXSTEP];    /* device time of the term's SpGEMM kernel */
+  double taylor_numeric_bytes[SEXPM_MAXSTEP]; /* its compulsory bytes: A + B + staged writes */
+  double taylor_fmas_i[SEXPM_MAXSTEP];        /* its products */
+  /* squarings i = 1..N at index i; index 0 describes T^_0 */
+  int64_t sq_nnz_unf[SEXPM_MAXSTEP];
+  int64_t sq_nnz[SEXPM_MAXSTEP];
+  int64_t sq_staged[SEXPM_MAXSTEP];      /* entries above the floor eps_g/sqrt(K) */
+  int32_t sq_passes[SEXPM_MAXSTEP];
+  double sq_eps_g[SEXPM_MAXSTEP];
+  double sq_tau[SEXPM_MAXSTEP];
+  double sq_normIT[SEXPM_MAXSTEP];       /* ||I + T^_i||_F */
+  int64_t sq_l1[SEXPM_MAXSTEP], sq_l2[SEXPM_MAXSTEP]; /* Eq. (3.1) bandwidths of T^_i */
+  double sq_fmas[SEXPM_MAXSTEP];         /* sum_r sum_{k in row r} nnz(row k) (+ 2T adds) */
+  double sq_ms[SEXPM_MAXSTEP];           /* device time of the whole step */
+  double sq_numeric_ms[SEXPM_MAXSTEP];   /* device time of the SpGEMM kernel alone */
+  double sq_bytes[SEXPM_MAXSTEP];        /* compulsory HBM bytes of the step: 12 nnz(T^_{i-1}) + 12 nnz(T^_i) + 16 rows */
+  double sq_numeric_bytes[SEXPM_MAXSTEP];/* compulsory bytes of the SpGEMM kernel: A + B + staged writes */
+  double ms_plan, ms_taylor, ms_squaring, ms_finalize, ms_total;
+  double taylor_bytes, taylor_fmas;
+  int64_t nnz_out;
+  int32_t gpu_launches;                  /* kernels launched by the last sexpm_run */
+  int32_t retries;                       /* steps re-run after a staging-pool overflow */
+} sexpm_stats;
+
+/* sizes[0..3] = sizeof(sexpm_options), sizeof(sexpm_stats), sizeof(sexpm_csr_in),
+ * sizeof(sexpm_csr_out): lets bindings verify their struct layouts (host only). */
+int sexpm_abi_sizes(uint32_t *sizes);
+
+/* Kernels enqueued by this library since it was loaded (all plans, all threads). */
+int sexpm_kernel_launches(int64_t *count);
+
+/* Fill defaults (see field comments). */
+int sexpm_options_init(sexpm_options *o);
+
+/* NCCL bootstrap: rank 0 calls sexpm_nccl_unique_id and ships the 128 bytes to all ranks
+ * (e.g. torch.distributed broadcast); every rank then calls sexpm_nccl_comm_init with its
+ * own CUDA device current.  The communicator is destroyed with sexpm_nccl_comm_destroy. */
+int sexpm_nccl_unique_id(void *id128);
+int sexpm_nccl_comm_init(int rank, int world, const void *id128, void **comm);
+int sexpm_nccl_comm_destroy(void *comm);
+
+/* Step 1-3 set-up: validate H (device CSR), compute ||H|| on the device, solve Eq. (4.20),
+ * choose a, r0, eps_g^(0), scale H0 = H 2^-N.  eps_tol: target relative error bound r_N. */
+int sexpm_plan(const sexpm_csr_in *H, double eps_tol, const sexpm_options *o, sexpm_plan_t *out);
+
+/* Same as sexpm_plan but H's arrays are HOST pointers; the library copies them in. */
+int sexpm_plan_host(const sexpm_csr_in *H_host, double eps_tol, const sexpm_options *o,
+                    sexpm_plan_t *out);
+
+/* Steps 3-5: Taylor phase, N filtered squarings, E = I + T^_N.  Synchronises the plan's
+ * stream before returning.  E (device, plan-owned) may be NULL. */
+int sexpm_run(sexpm_plan_t p, sexpm_csr_out *E);
+
+/* Copy the last result (rows+1 rowptr, nnz cols, nnz vals) into caller-owned arrays,
+ * HOST (D2H, pinned or pageable) or DEVICE (D2D) pointers alike; synchronises the stream. */
+int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *vals);
+
+/* Plan scalars, per-step trace and CUDA-event timings of the last run. */
+int sexpm_stats_get(sexpm_plan_t p, sexpm_stats *s);
+
+int sexpm_destroy(sexpm_plan_t p);
+
+const char *sexpm_last_error(void);
+
+/* ----- component entry points (used by the parity tests; same kernels as sexpm_run) ----- */
+
+/* One filtered product on the plan's device/stream (single GPU):
+ *   C~ = (self_coef * A + A * B) / divisor,  C^ = Alg4.1(C~, eps_g, e_r).
+ * self_coef = 2, divisor = 1 is a squaring step (Eq. 4.15); self_coef = 0, divisor = i is
+ * a Taylor term (Eq. 4.11).  A and B are device CSR over all n rows.  The result is
+ * plan-owned (valid until the next call on the plan); *passes / *tau report Algorithm 4.1;
+ * *nnz_unf the distinct nonzeros of C~. */
+int sexpm_filtered_product(sexpm_plan_t p, const sexpm_csr_in *A, const sexpm_csr_in *B,
+                           double self_coef, double divisor, double eps_g, sexpm_csr_out *C,
+                           int32_t *passes, double *tau, int64_t *nnz_unf);
+
+/* Algorithm 4.1 over a device array of cnt values: returns the number of passes, the final
+ * threshold tau (entries kept are exactly |x| > tau; +inf if the loop never ran; 0 when
+ * eps_g == 0) and the dropped Frobenius norm. */
+int sexpm_alg41(sexpm_plan_t p, const double *x, int64_t cnt, double eps_g, double e_r,
+                int32_t *passes, double *tau, double *dropped);
+
+/* Host-side halo planner for the row-partitioned multi-GPU squaring (Lemma 3.1):
+ * rank g owns rows [bounds[g], bounds[g+1]); with T^_{i-1} of bandwidths (l1, l2) the
+ * product rows of rank g need B rows [max(0, b_g - l2), min(n, b_{g+1} + l1)).  Writes, for
+ * every peer h, the row range [lo, hi) rank g must receive from h (lo == hi when none). */
+int sexpm_halo_ranges(int world, int rank, const int64_t *bounds, int64_t n, int64_t l1,
+                      int64_t l2, int64_t *recv_lo, int64_t *recv_hi);
+
+/* Row partition balanced by a per-row work estimate (contiguous blocks). */
+int sexpm_partition_rows(int64_t n, const double *work, int world, int64_t *bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEXPM_H */

@@ -1,0 +1,1388 @@
+// driver.cu — host driver and C ABI of libsexpm (see include/sexpm.h).
+//
+// Algorithm 4.2 on one or more B200s.  Host work is scalar only
+// (Eq. 4.20 enumeration, Algorithm 4.1's threshold recurrence); every matrix step runs
+// in the kernels of kernels.cu.  Multi-GPU: contiguous row blocks, NCCL halo exchange of
+// the rows of T^_{i-1} within its bandwidth (Lemma 3.1) and tiny scalar
+// all-gathers summed in rank order (identical thresholds on every rank).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/sexpm.h"
+#include "kernels.cuh"
+
+using namespace sx;
+
+// ------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+struct SxError {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw SxError{e_ == cudaErrorMemoryAllocation ? SEXPM_ENOMEM : SEXPM_ECUDA,       \
+                    std::string(#x) + ": " + cudaGetErrorString(e_)};                   \
+  } while (0)
+
+#define REQUIRE(cond, code, msg)                \
+  do {                                          \
+    if (!(cond)) throw SxError{(code), (msg)};  \
+  } while (0)
+
+// ------------------------------------------------------------------------------------
+// NCCL, loaded at run time (the library works on one GPU without NCCL present)
+// ------------------------------------------------------------------------------------
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Bcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
+                        cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*ErrStr)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+
+static NcclApi &nccl() {
+  if (!g_nccl.tried) {
+    g_nccl.tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+#define NS(f, s) g_nccl.f = reinterpret_cast<decltype(g_nccl.f)>(dlsym(h, s))
+      NS(GetUniqueId, "ncclGetUniqueId");
+      NS(CommInitRank, "ncclCommInitRank");
+      NS(CommDestroy, "ncclCommDestroy");
+      NS(AllGather, "ncclAllGather");
+      NS(Send, "ncclSend");
+      NS(Recv, "ncclRecv");
+      NS(Bcast, "ncclBroadcast");
+      NS(GroupStart, "ncclGroupStart");
+      NS(GroupEnd, "ncclGroupEnd");
+      NS(ErrStr, "ncclGetErrorString");
+#undef NS
+      g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllGather &&
+                  g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd &&
+                  g_nccl.Bcast;
+    }
+  }
+  REQUIRE(g_nccl.ok, SEXPM_ENCCL, "libnccl.so.2 could not be loaded");
+  return g_nccl;
+}
+
+#define NK(x)                                                                            \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess)                                                               \
+      throw SxError{SEXPM_ENCCL, std::string(#x) + ": " +                                \
+                                     (g_nccl.ErrStr ? g_nccl.ErrStr(r_) : "nccl error")}; \
+  } while (0)
+
+// ------------------------------------------------------------------------------------
+// device buffers (stream-ordered allocator)
+// ------------------------------------------------------------------------------------
+template <typename T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaStream_t st = nullptr;
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t cnt, cudaStream_t s) {
+    release();
+    st = s;
+    if (cnt == 0) cnt = 1;
+    CK(cudaMallocAsync(reinterpret_cast<void **>(&p), cnt * sizeof(T), s));
+    n = cnt;
+  }
+  void ensure(size_t cnt, cudaStream_t s) {
+    if (cnt > n || !p) alloc(std::max<size_t>(cnt, 1), s);
+  }
+  DBuf() = default;
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept { *this = std::move(o); }
+  DBuf &operator=(DBuf &&o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      st = o.st;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+};
+
+struct DCsr {
+  int64_t nrows = 0, row0 = 0, nnz = 0;
+  DBuf<int64_t> rp;
+  DBuf<int32_t> col;
+  DBuf<double> val;
+  CsrView view() const {
+    CsrView v;
+    v.nrows = nrows;
+    v.row0 = row0;
+    v.nnz = nnz;
+    v.rp = rp.p;
+    v.col = col.p;
+    v.val = val.p;
+    return v;
+  }
+};
+
+static CsrView view_of(const sexpm_csr_in *H, int64_t row0_override = -1) {
+  CsrView v;
+  v.nrows = H->row_end - H->row_begin;
+  v.row0 = row0_override >= 0 ? row0_override : H->row_begin;
+  v.nnz = H->nnz;
+  v.rp = H->rowptr;
+  v.col = H->colidx;
+  v.val = H->vals;
+  return v;
+}
+
+// ------------------------------------------------------------------------------------
+// plan
+// ------------------------------------------------------------------------------------
+struct StepReport {
+  int32_t passes = 0;
+  double tau = 0.0, fsum = 0.0;
+  int64_t nnz_unf = 0, staged = 0, nnz = 0;
+  double normIT2 = 0.0;
+  int64_t l1 = 0, l2 = 0;
+  double fmas = 0.0;
+  float numeric_ms = 0.f;
+  double numeric_bytes = 0.0;
+};
+
+struct Workspace {
+  DBuf<int32_t> lo, hi, order, bin_cnt, bin_off;
+  DBuf<int64_t> prod, bound, row_off, row_cnt, row_nnz, cnt, scan_tmp, l1r, l2r, i64tmp;
+  DBuf<double> row_fsum, rs, partial, scal;
+  DBuf<int64_t> cursor;
+  DBuf<int32_t> scr_col, pool_col;
+  DBuf<double> scr_val, pool_val;
+  DBuf<unsigned long long> pool_used;
+  DBuf<int> row_counter, flags;
+  int64_t pool_cap_hint = 0;
+};
+
+struct sexpm_plan_s {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  sexpm_options o{};
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  int64_t n = 0, row_begin = 0, row_end = 0;
+  std::vector<int64_t> bounds;  // world + 1 row bounds
+  double eps_tol = 0.0;
+  DCsr H0full;  // H0 = H 2^-N, all n rows (replicated)
+  DCsr T, E;
+  bool have_result = false;
+  int M = 0, N = 0, normal = 0, M_eff = 0;
+  double norm = 0.0, a = 0.0, eps_g0 = 0.0;
+  long double r0 = 0.0L;
+  Workspace ws;
+  sexpm_stats stats{};
+  int sm_count = 148;
+  int numeric_blocks_per_sm = 2;
+  float plan_ms = 0.f;
+};
+
+// ------------------------------------------------------------------------------------
+// collectives on scalars: all-gather, then sum / max in rank order (identical everywhere)
+// ------------------------------------------------------------------------------------
+static void gather_doubles(sexpm_plan_s &P, const double *local, int cnt, std::vector<double> &all) {
+  all.assign((size_t)cnt * P.world, 0.0);
+  if (P.world == 1) {
+    std::copy(local, local + cnt, all.begin());
+    return;
+  }
+  DBuf<double> d;
+  d.alloc((size_t)cnt * (P.world + 1), P.st);
+  CK(cudaMemcpyAsync(d.p, local, cnt * sizeof(double), cudaMemcpyHostToDevice, P.st));
+  NK(nccl().AllGather(d.p, d.p + cnt, cnt, ncclDouble, P.comm, P.st));
+  CK(cudaMemcpyAsync(all.data(), d.p + cnt, (size_t)cnt * P.world * sizeof(double),
+                     cudaMemcpyDeviceToHost, P.st));
+  CK(cudaStreamSynchronize(P.st));
+}
+static double allsum(sexpm_plan_s &P, double v) {
+  if (P.world == 1) return v;
+  std::vector<double> all;
+  gather_doubles(P, &v, 1, all);
+  double s = 0.0;
+  for (double x : all) s += x;
+  return s;
+}
+static double allmax(sexpm_plan_s &P, double v) {
+  if (P.world == 1) return v;
+  std::vector<double> all;
+  gather_doubles(P, &v, 1, all);
+  double s = all[0];
+  for (double x : all) s = std::max(s, x);
+  return s;
+}
+
+template <typename T>
+static T d2h(const T *dptr, cudaStream_t st) {
+  T v;
+  CK(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return v;
+}
+
+// ------------------------------------------------------------------------------------
+// filtered product: C^ = Alg4.1((self*A + A*B)/div, eps_g)   [K1, K2, K3, K6, K4]
+// A: local rows; B: rows covering every column of A.  C gets A's rows.
+// ------------------------------------------------------------------------------------
+static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
+                            double div, double eps_g, DCsr &C, StepReport &rep) {
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  const int64_t nr = A.nrows;
+  const size_t nr1 = (size_t)std::max<int64_t>(nr, 1);
+  w.lo.ensure(nr1, st);
+  w.hi.ensure(nr1, st);
+  w.order.ensure(nr1, st);
+  w.prod.ensure(nr1, st);
+  w.bound.ensure(nr1, st);
+  w.row_off.ensure(nr1, st);
+  w.row_cnt.ensure(nr1, st);
+  w.row_nnz.ensure(nr1, st);
+  w.row_fsum.ensure(nr1, st);
+  w.cnt.ensure(nr1, st);
+  w.rs.ensure(nr1, st);
+  w.l1r.ensure(nr1, st);
+  w.l2r.ensure(nr1, st);
+  w.scan_tmp.ensure((size_t)scan_tmp_elems(nr) + 1, st);
+  w.bin_cnt.ensure(64, st);
+  w.bin_off.ensure(64, st);
+  w.partial.ensure(1024, st);
+  w.scal.ensure(8, st);
+  w.i64tmp.ensure(8, st);
+  w.pool_used.ensure(1, st);
+  w.row_counter.ensure(1, st);
+  w.flags.ensure(1, st);
+
+  // K1 symbolic bounds
+  launch_symbolic(A, B, self != 0.0 ? 1 : 0, w.lo.p, w.hi.p, w.prod.p, w.bound.p, st);
+  launch_reduce_sum_i64(w.bound.p, nr, w.i64tmp.p + 0, st);
+  launch_reduce_max_i64(w.bound.p, nr, w.i64tmp.p + 1, st);
+  launch_reduce_sum_i64(w.prod.p, nr, w.i64tmp.p + 2, st);
+  // longest A row (cursor scratch size)
+  launch_row_lengths(A.rp, nr, w.cnt.p, st);
+  launch_reduce_max_i64(w.cnt.p, nr, w.i64tmp.p + 6, st);
+  int64_t hstat[8];
+  CK(cudaMemcpyAsync(hstat, w.i64tmp.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int64_t maxk = hstat[6];
+  const double Kglob = allsum(P, (double)hstat[0]);
+  const int64_t maxb = hstat[1];
+  rep.fmas = (double)hstat[2];
+  const double floor_tau = (eps_g > 0.0 && Kglob > 0.0) ? eps_g / sqrt(Kglob) : 0.0;
+
+  // K2 binning (longest rows first)
+  launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
+
+  // K3 numeric
+  NumericArgs na;
+  na.A = A;
+  na.B = B;
+  na.self_coef = self;
+  na.divisor = div;
+  na.floor_tau = floor_tau;
+  na.lo = w.lo.p;
+  na.hi = w.hi.p;
+  na.order = w.order.p;
+  na.window = P.o.window_cols > 0 ? P.o.window_cols : 8192;
+  na.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.numeric_blocks_per_sm));
+  na.cursor_cap = std::max<int64_t>(maxk, 1);
+  na.scr_cap = std::max<int64_t>(maxb, 1);
+  w.cursor.ensure((size_t)na.grid * na.cursor_cap, st);
+  w.scr_col.ensure((size_t)na.grid * na.scr_cap, st);
+  w.scr_val.ensure((size_t)na.grid * na.scr_cap, st);
+  int64_t cap = std::max<int64_t>(w.pool_cap_hint, (self != 0.0 ? 3 : 2) * A.nnz + 2 * nr + 1024);
+  double sum_bound = 0;  // exact upper bound
+  sum_bound = (double)hstat[0];
+  if ((double)cap > sum_bound) cap = (int64_t)sum_bound + 1;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  unsigned long long used = 0;
+  for (int attempt = 0;; attempt++) {
+    w.pool_col.ensure((size_t)cap, st);
+    w.pool_val.ensure((size_t)cap, st);
+    na.pool_col = w.pool_col.p;
+    na.pool_val = w.pool_val.p;
+    na.pool_cap = (int64_t)w.pool_col.n;
+    na.cursor = w.cursor.p;
+    na.scr_col = w.scr_col.p;
+    na.scr_val = w.scr_val.p;
+    na.pool_used = w.pool_used.p;
+    na.row_off = w.row_off.p;
+    na.row_cnt = w.row_cnt.p;
+    na.row_fsum = w.row_fsum.p;
+    na.row_nnz = w.row_nnz.p;
+    na.row_counter = w.row_counter.p;
+    na.flags = w.flags.p;
+    CK(cudaMemsetAsync(w.pool_used.p, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+    CK(cudaEventRecord(e0, st));
+    launch_numeric(na, st);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, st));
+    int flags = 0;
+    CK(cudaMemcpyAsync(&flags, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&used, w.pool_used.p, sizeof(used), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    REQUIRE(!(flags & 2), SEXPM_EINTERNAL, "numeric: per-CTA staging overflow");
+    if (!(flags & 1)) break;
+    REQUIRE(attempt < 8, SEXPM_EINTERNAL, "numeric: staging pool keeps overflowing");
+    cap = std::max<int64_t>(2 * cap, (int64_t)(1.25 * (double)used) + 1024);
+    P.stats.retries++;
+  }
+  CK(cudaEventElapsedTime(&rep.numeric_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  w.pool_cap_hint = std::max<int64_t>(w.pool_cap_hint, (int64_t)(1.2 * (double)used));
+  rep.staged = (int64_t)used;
+  // compulsory bytes of K3: A (rowptr + entries), the B rows it reads (whole B: each row once;
+  // when B is A itself it is read once), staged writes (col + val) and per-row outputs.
+  {
+    const bool same = (B.rp == A.rp);
+    rep.numeric_bytes = 8.0 * (nr + 1) + 12.0 * (double)A.nnz +
+                        (same ? 0.0 : 8.0 * (B.nrows + 1) + 12.0 * (double)B.nnz) +
+                        12.0 * (double)used + 32.0 * (double)nr;
+  }
+
+  // Algorithm 4.1: scalar recurrence on the host, sums on the device
+  launch_reduce_sum(w.row_fsum.p, nr, w.partial.p, w.scal.p + 0, st);
+  launch_reduce_sum_i64(w.row_nnz.p, nr, w.i64tmp.p + 3, st);
+  double Floc = d2h(w.scal.p + 0, st);
+  rep.nnz_unf = (int64_t)allsum(P, (double)d2h(w.i64tmp.p + 3, st));
+  const double F = allsum(P, Floc);
+  rep.fsum = F;
+  double tau;
+  int passes = 0;
+  if (eps_g == 0.0) {
+    tau = 0.0;  // reading R3: no filtering
+  } else {
+    long double m = 1.0L, b = 1.0L;  // m_0 = 1, b_0 = 1 (reading R1)
+    const long double eg = eps_g;
+    const long double lim = eg * (1.0L + (long double)P.o.e_r);
+    long double epsf = INFINITY;
+    while (b > lim) {
+      epsf = eg / m;
+      const double tau_d = (double)epsf;
+      launch_alg41_pass(w.pool_val.p, (int64_t)used, tau_d, w.partial.p, w.scal.p + 1, st);
+      const double S = allsum(P, d2h(w.scal.p + 1, st));
+      b = sqrtl((long double)F + (long double)S);
+      m = b / epsf;
+      passes++;
+      REQUIRE(passes < 256, SEXPM_EINTERNAL, "Algorithm 4.1 pass cap reached (Theorem 4.1)");
+    }
+    tau = passes == 0 ? INFINITY : (double)epsf;  // loop never ran: A~ = 0 (reading R1)
+  }
+  rep.passes = passes;
+  rep.tau = tau;
+
+  // K4 compaction + fused row statistics
+  launch_compact_count(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau, w.cnt.p, st);
+  DCsr out;
+  out.nrows = nr;
+  out.row0 = A.row0;
+  out.rp.alloc((size_t)nr + 1, st);
+  launch_exclusive_scan(w.cnt.p, nr, out.rp.p, w.scan_tmp.p, st);
+  out.nnz = d2h(out.rp.p + nr, st);
+  out.col.alloc((size_t)out.nnz, st);
+  out.val.alloc((size_t)out.nnz, st);
+  launch_compact_write(nr, A.row0, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
+                       out.rp.p, out.col.p, out.val.p, w.rs.p, w.l1r.p, w.l2r.p, st);
+  launch_reduce_sum(w.rs.p, nr, w.partial.p, w.scal.p + 2, st);
+  launch_reduce_max_i64(w.l1r.p, nr, w.i64tmp.p + 4, st);
+  launch_reduce_max_i64(w.l2r.p, nr, w.i64tmp.p + 5, st);
+  rep.normIT2 = allsum(P, d2h(w.scal.p + 2, st));
+  rep.l1 = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 4, st));
+  rep.l2 = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 5, st));
+  rep.nnz = (int64_t)allsum(P, (double)out.nnz);
+  C = std::move(out);
+}
+
+// C = A + B (same rows)
+static void merge_add(sexpm_plan_s &P, const CsrView &A, const CsrView &B, DCsr &C) {
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  const int64_t nr = A.nrows;
+  w.cnt.ensure((size_t)std::max<int64_t>(nr, 1), st);
+  w.scan_tmp.ensure((size_t)scan_tmp_elems(nr) + 1, st);
+  launch_merge_count(A, B, w.cnt.p, st);
+  DCsr out;
+  out.nrows = nr;
+  out.row0 = A.row0;
+  out.rp.alloc((size_t)nr + 1, st);
+  launch_exclusive_scan(w.cnt.p, nr, out.rp.p, w.scan_tmp.p, st);
+  out.nnz = d2h(out.rp.p + nr, st);
+  out.col.alloc((size_t)out.nnz, st);
+  out.val.alloc((size_t)out.nnz, st);
+  launch_merge_write(A, B, out.rp.p, out.col.p, out.val.p, st);
+  C = std::move(out);
+}
+
+static void copy_csr(sexpm_plan_s &P, const CsrView &A, DCsr &C) {
+  cudaStream_t st = P.st;
+  C.nrows = A.nrows;
+  C.row0 = A.row0;
+  C.nnz = A.nnz;
+  C.rp.alloc((size_t)A.nrows + 1, st);
+  C.col.alloc((size_t)A.nnz, st);
+  C.val.alloc((size_t)A.nnz, st);
+  CK(cudaMemcpyAsync(C.rp.p, A.rp, ((size_t)A.nrows + 1) * sizeof(int64_t),
+                     cudaMemcpyDeviceToDevice, st));
+  if (A.nnz) {
+    CK(cudaMemcpyAsync(C.col.p, A.col, A.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(C.val.p, A.val, A.nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+// local row block [row_begin, row_end) of a full-row CSR (rows re-based)
+static void slice_rows(sexpm_plan_s &P, const DCsr &F, int64_t r0, int64_t r1, DCsr &C) {
+  cudaStream_t st = P.st;
+  int64_t a = 0, b = 0;
+  CK(cudaMemcpyAsync(&a, F.rp.p + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&b, F.rp.p + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  C.nrows = r1 - r0;
+  C.row0 = r0;
+  C.nnz = b - a;
+  C.rp.alloc((size_t)C.nrows + 1, st);
+  C.col.alloc((size_t)C.nnz, st);
+  C.val.alloc((size_t)C.nnz, st);
+  launch_rebase_rowptr(F.rp.p + r0, C.nrows, 0, C.rp.p, st);
+  if (C.nnz) {
+    CK(cudaMemcpyAsync(C.col.p, F.col.p + a, C.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(C.val.p, F.val.p + a, C.nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// multi-GPU: all-gather full H, halo exchange
+// ------------------------------------------------------------------------------------
+static void allgather_rows(sexpm_plan_s &P, const CsrView &L, DCsr &F) {
+  // every rank broadcasts its block (rowptr deltas, col, val); F holds all n rows
+  cudaStream_t st = P.st;
+  std::vector<double> meta;
+  double mine[2] = {(double)L.nrows, (double)L.nnz};
+  gather_doubles(P, mine, 2, meta);
+  std::vector<int64_t> rows(P.world), nnzs(P.world), roff(P.world + 1, 0), noff(P.world + 1, 0);
+  for (int g = 0; g < P.world; g++) {
+    rows[g] = (int64_t)meta[2 * g];
+    nnzs[g] = (int64_t)meta[2 * g + 1];
+    roff[g + 1] = roff[g] + rows[g];
+    noff[g + 1] = noff[g] + nnzs[g];
+  }
+  REQUIRE(roff[P.world] == P.n, SEXPM_EINVAL, "row blocks do not cover [0, n)");
+  DBuf<int64_t> rp_parts;  // per rank: its rowptr (rows+1) stored at roff[g] + g
+  rp_parts.alloc((size_t)P.n + P.world, st);
+  F.nrows = P.n;
+  F.row0 = 0;
+  F.nnz = noff[P.world];
+  F.col.alloc((size_t)F.nnz, st);
+  F.val.alloc((size_t)F.nnz, st);
+  F.rp.alloc((size_t)P.n + 1, st);
+  NK(nccl().GroupStart());
+  for (int g = 0; g < P.world; g++) {
+    const bool me = g == P.rank;
+    NK(nccl().Bcast(me ? (const void *)L.rp : nullptr, rp_parts.p + roff[g] + g, rows[g] + 1,
+                    ncclInt64, g, P.comm, st));
+    if (nnzs[g]) {
+      NK(nccl().Bcast(me ? (const void *)L.col : nullptr, F.col.p + noff[g], nnzs[g], ncclInt32,
+                      g, P.comm, st));
+      NK(nccl().Bcast(me ? (const void *)L.val : nullptr, F.val.p + noff[g], nnzs[g], ncclDouble,
+                      g, P.comm, st));
+    }
+  }
+  NK(nccl().GroupEnd());
+  for (int g = 0; g < P.world; g++)
+    launch_rebase_rowptr(rp_parts.p + roff[g] + g, rows[g], noff[g], F.rp.p + roff[g], st);
+  CK(cudaStreamSynchronize(st));
+}
+
+static void halo_ranges_host(int world, int rank, const int64_t *bounds, int64_t n, int64_t l1,
+                             int64_t l2, int64_t *lo, int64_t *hi) {
+  const int64_t need_lo = std::max<int64_t>(0, bounds[rank] - l2);
+  const int64_t need_hi = std::min<int64_t>(n, bounds[rank + 1] + l1);
+  for (int h = 0; h < world; h++) {
+    int64_t a = std::max(need_lo, bounds[h]), b = std::min(need_hi, bounds[h + 1]);
+    if (h == rank || a >= b) a = b = 0;
+    lo[h] = a;
+    hi[h] = b;
+  }
+}
+
+// B = rows [need_lo, need_hi) of T^ assembled from the local block and the peers' halos
+static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2, DCsr &B) {
+  cudaStream_t st = P.st;
+  const int W = P.world, R = P.rank;
+  std::vector<int64_t> rlo(W), rhi(W);
+  halo_ranges_host(W, R, P.bounds.data(), P.n, l1, l2, rlo.data(), rhi.data());
+  // what each peer h needs from me: symmetric computation with h's bounds
+  std::vector<int64_t> slo(W), shi(W);
+  for (int h = 0; h < W; h++) {
+    std::vector<int64_t> lo(W), hi(W);
+    halo_ranges_host(W, h, P.bounds.data(), P.n, l1, l2, lo.data(), hi.data());
+    slo[h] = lo[R];
+    shi[h] = hi[R];
+  }
+  // host copy of my rowptr (needed to size sends)
+  std::vector<int64_t> rp((size_t)T.nrows + 1);
+  CK(cudaMemcpyAsync(rp.data(), T.rp.p, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // exchange nnz counts of the pieces
+  std::vector<double> cnt_send(W, 0.0), all;
+  for (int h = 0; h < W; h++)
+    if (shi[h] > slo[h])
+      cnt_send[h] = (double)(rp[shi[h] - T.row0] - rp[slo[h] - T.row0]);
+  gather_doubles(P, cnt_send.data(), W, all);  // all[g*W + h] = nnz g sends to h
+  const int64_t need_lo = std::max<int64_t>(0, P.bounds[R] - l2);
+  const int64_t need_hi = std::min<int64_t>(P.n, P.bounds[R + 1] + l1);
+  // pieces in row order: peers below, me, peers above
+  std::vector<int64_t> piece_rows(W, 0), piece_nnz(W, 0);
+  for (int h = 0; h < W; h++) {
+    if (h == R) {
+      piece_rows[h] = T.nrows;
+      piece_nnz[h] = T.nnz;
+    } else if (rhi[h] > rlo[h]) {
+      piece_rows[h] = rhi[h] - rlo[h];
+      piece_nnz[h] = (int64_t)all[(size_t)h * W + R];
+    }
+  }
+  B.nrows = need_hi - need_lo;
+  B.row0 = need_lo;
+  B.nnz = 0;
+  for (int h = 0; h < W; h++) B.nnz += piece_nnz[h];
+  B.rp.alloc((size_t)B.nrows + 1, st);
+  B.col.alloc((size_t)B.nnz, st);
+  B.val.alloc((size_t)B.nnz, st);
+  DBuf<int64_t> rp_tmp;
+  rp_tmp.alloc((size_t)B.nrows + W + 1, st);
+  std::vector<int64_t> row_at(W), nnz_at(W), tmp_at(W);
+  int64_t ro = 0, no = 0, to = 0;
+  for (int h = 0; h < W; h++) {
+    row_at[h] = ro;
+    nnz_at[h] = no;
+    tmp_at[h] = to;
+    ro += piece_rows[h];
+    no += piece_nnz[h];
+    to += piece_rows[h] ? piece_rows[h] + 1 : 0;
+  }
+  REQUIRE(ro == B.nrows, SEXPM_EINTERNAL, "halo rows do not tile the needed range");
+  NK(nccl().GroupStart());
+  for (int h = 0; h < W; h++) {
+    if (h == R) continue;
+    if (shi[h] > slo[h]) {
+      int64_t a = slo[h] - T.row0, b = shi[h] - T.row0;
+      NK(nccl().Send(T.rp.p + a, b - a + 1, ncclInt64, h, P.comm, st));
+      int64_t na = rp[a], nb = rp[b];
+      if (nb > na) {
+        NK(nccl().Send(T.col.p + na, nb - na, ncclInt32, h, P.comm, st));
+        NK(nccl().Send(T.val.p + na, nb - na, ncclDouble, h, P.comm, st));
+      }
+    }
+    if (piece_rows[h]) {
+      NK(nccl().Recv(rp_tmp.p + tmp_at[h], piece_rows[h] + 1, ncclInt64, h, P.comm, st));
+      if (piece_nnz[h]) {
+        NK(nccl().Recv(B.col.p + nnz_at[h], piece_nnz[h], ncclInt32, h, P.comm, st));
+        NK(nccl().Recv(B.val.p + nnz_at[h], piece_nnz[h], ncclDouble, h, P.comm, st));
+      }
+    }
+  }
+  NK(nccl().GroupEnd());
+  // my own rows
+  CK(cudaMemcpyAsync(rp_tmp.p + tmp_at[R], T.rp.p, (T.nrows + 1) * sizeof(int64_t),
+                     cudaMemcpyDeviceToDevice, st));
+  if (T.nnz) {
+    CK(cudaMemcpyAsync(B.col.p + nnz_at[R], T.col.p, T.nnz * sizeof(int32_t),
+                       cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(B.val.p + nnz_at[R], T.val.p, T.nnz * sizeof(double),
+                       cudaMemcpyDeviceToDevice, st));
+  }
+  for (int h = 0; h < W; h++)
+    if (piece_rows[h])
+      launch_rebase_rowptr(rp_tmp.p + tmp_at[h], piece_rows[h], nnz_at[h], B.rp.p + row_at[h], st);
+  CK(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------------------------------------
+// plan
+// ------------------------------------------------------------------------------------
+static long double r0_series(long double x, int M) {  // Eq. (4.5)
+  if (x <= 0.0L) return 0.0L;
+  long double t = 1.0L;
+  for (int s = 1; s <= M; s++) t *= x / (long double)s;
+  t *= x / (long double)(M + 1);
+  long double sum = 0.0L;
+  for (int i = 0; i < 100000; i++) {
+    long double ns = sum + t;
+    if (ns == sum) break;
+    sum = ns;
+    t = t * x * (long double)(i + M + 1) / ((long double)(i + 1) * (long double)(i + M + 2));
+  }
+  return sum;
+}
+
+static bool plan_MN(double norm, double eps_tol, int m_cap, int n_window, int &M, int &N) {
+  // Eq. (4.20): min M 2^N s.t. ||H 2^-N|| <= 1, 2^N r0 <= eps_tol
+  if (norm == 0.0) {
+    M = N = 0;
+    return true;
+  }
+  int N0 = (int)ceil(log2(norm));
+  if (N0 < 0) N0 = 0;
+  while (ldexp(norm, -N0) > 1.0) N0++;
+  long double best = -1.0L;
+  int bM = -1, bN = -1;
+  for (int n = N0; n <= N0 + n_window; n++) {
+    long double x = (long double)ldexp(norm, -n);
+    for (int m = 0; m <= m_cap; m++) {
+      if (ldexpl(r0_series(x, m), n) <= (long double)eps_tol) {
+        long double cost = (long double)m * ldexpl(1.0L, n);
+        if (best < 0.0L || cost < best) {
+          best = cost;
+          bM = m;
+          bN = n;
+        }
+        break;
+      }
+    }
+  }
+  if (bM < 0) return false;
+  M = bM;
+  N = bN;
+  return true;
+}
+
+static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
+  cudaStream_t st = P.st;
+  REQUIRE(H->n >= 1, SEXPM_EINVAL, "n must be >= 1");
+  REQUIRE(H->row_begin >= 0 && H->row_end <= H->n && H->row_begin <= H->row_end, SEXPM_EINVAL,
+          "bad row range");
+  REQUIRE(H->n < INT32_MAX, SEXPM_EINVAL, "n must fit int32 column indices");
+  REQUIRE(H->nnz >= 0 && (H->nnz == 0 || (H->colidx && H->vals)) && H->rowptr, SEXPM_EINVAL,
+          "null CSR arrays");
+  REQUIRE(isfinite(eps_tol) && eps_tol >= 1e-16, SEXPM_ETOL,
+          "eps_tol must be >= 1e-16 (unit roundoff, reading R13)");
+  REQUIRE(P.o.e_r > 0.0, SEXPM_EINVAL, "e_r must be > 0");
+  P.n = H->n;
+  P.row_begin = H->row_begin;
+  P.row_end = H->row_end;
+  P.eps_tol = eps_tol;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  Workspace &w = P.ws;
+  w.flags.ensure(1, st);
+  w.partial.ensure(1024, st);
+  w.scal.ensure(8, st);
+  // validate the local block
+  CsrView L = view_of(H);
+  CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+  int64_t rp01[2];
+  CK(cudaMemcpyAsync(&rp01[0], L.rp, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&rp01[1], L.rp + L.nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  REQUIRE(rp01[0] == 0 && rp01[1] == L.nnz, SEXPM_EINVAL, "rowptr[0] must be 0 and rowptr[rows] == nnz");
+  launch_validate(L, P.n, w.flags.p, st);
+  int vf = d2h(w.flags.p, st);
+  vf = (int)allmax(P, (double)vf);
+  REQUIRE(!(vf & 8), SEXPM_ENONFINITE, "H holds a non-finite value");
+  REQUIRE(!(vf & 7), SEXPM_EINVAL, "malformed CSR (rowptr / column range / column order)");
+  // rank partition
+  std::vector<double> rb;
+  double mine[2] = {(double)P.row_begin, (double)P.row_end};
+  gather_doubles(P, mine, 2, rb);
+  P.bounds.assign(P.world + 1, 0);
+  for (int g = 0; g < P.world; g++) {
+    REQUIRE((int64_t)rb[2 * g] == (g == 0 ? 0 : (int64_t)rb[2 * g - 1]), SEXPM_EINVAL,
+            "row blocks must be contiguous in rank order");
+    P.bounds[g + 1] = (int64_t)rb[2 * g + 1];
+  }
+  REQUIRE(P.bounds[P.world] == P.n, SEXPM_EINVAL, "row blocks must cover [0, n)");
+  // full H on every rank (explicit zeros purged: compaction with tau = 0)
+  DCsr Hraw;
+  if (P.world == 1) {
+    copy_csr(P, L, Hraw);
+  } else {
+    allgather_rows(P, L, Hraw);
+  }
+  {
+    w.row_off.ensure((size_t)P.n, st);
+    w.row_cnt.ensure((size_t)P.n, st);
+    w.cnt.ensure((size_t)P.n, st);
+    w.scan_tmp.ensure((size_t)scan_tmp_elems(P.n) + 1, st);
+    // row_off = rp[0..n), row_cnt = rp diff
+    launch_copy_i64_offset(Hraw.rp.p, P.n, 0, w.row_off.p, st);
+    std::vector<int64_t> hrp((size_t)P.n + 1);
+    CK(cudaMemcpyAsync(hrp.data(), Hraw.rp.p, hrp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> hc((size_t)P.n);
+    for (int64_t r = 0; r < P.n; r++) hc[r] = hrp[r + 1] - hrp[r];
+    CK(cudaMemcpyAsync(w.row_cnt.p, hc.data(), hc.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    launch_compact_count(P.n, w.row_off.p, w.row_cnt.p, Hraw.val.p, 0.0, w.cnt.p, st);
+    DCsr Hc;
+    Hc.nrows = P.n;
+    Hc.row0 = 0;
+    Hc.rp.alloc((size_t)P.n + 1, st);
+    launch_exclusive_scan(w.cnt.p, P.n, Hc.rp.p, w.scan_tmp.p, st);
+    Hc.nnz = d2h(Hc.rp.p + P.n, st);
+    Hc.col.alloc((size_t)Hc.nnz, st);
+    Hc.val.alloc((size_t)Hc.nnz, st);
+    launch_compact_write(P.n, 0, w.row_off.p, w.row_cnt.p, Hraw.col.p, Hraw.val.p, 0.0, Hc.rp.p,
+                         Hc.col.p, Hc.val.p, nullptr, nullptr, nullptr, st);
+    P.H0full = std::move(Hc);
+  }
+  DCsr &Hf = P.H0full;
+  // K8 norms on the device
+  double norm = 0.0;
+  int symflags = 3;
+  {
+    DBuf<int32_t> ccnt;
+    ccnt.alloc((size_t)P.n, st);
+    CK(cudaMemsetAsync(ccnt.p, 0, P.n * sizeof(int32_t), st));
+    launch_col_count(Hf.view(), ccnt.p, st);
+    DBuf<int64_t> cnt64, cp, cursor;
+    cnt64.alloc((size_t)P.n, st);
+    // widen counts (int32 -> int64) through the scan input
+    std::vector<int32_t> hc32((size_t)P.n);
+    CK(cudaMemcpyAsync(hc32.data(), ccnt.p, P.n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> hc64(hc32.begin(), hc32.end());
+    CK(cudaMemcpyAsync(cnt64.p, hc64.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    cp.alloc((size_t)P.n + 1, st);
+    w.scan_tmp.ensure((size_t)scan_tmp_elems(P.n) + 1, st);
+    launch_exclusive_scan(cnt64.p, P.n, cp.p, w.scan_tmp.p, st);
+    cursor.alloc((size_t)P.n, st);
+    CK(cudaMemcpyAsync(cursor.p, cp.p, P.n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    DBuf<int32_t> trow;
+    DBuf<double> tval, colsum;
+    trow.alloc((size_t)Hf.nnz, st);
+    tval.alloc((size_t)Hf.nnz, st);
+    launch_transpose_fill(Hf.view(), cursor.p, trow.p, tval.p, st);
+    launch_sort_columns(P.n, cp.p, trow.p, tval.p, st);
+    if (P.o.plan_norm == 0) {
+      colsum.alloc((size_t)P.n, st);
+      launch_col_abs_sum(P.n, cp.p, tval.p, colsum.p, st);
+      launch_reduce_max(colsum.p, P.n, w.partial.p, w.scal.p, st);
+    } else {
+      launch_reduce_sumsq(Hf.val.p, Hf.nnz, w.partial.p, w.scal.p, st);
+    }
+    CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+    launch_compare_transpose(Hf.view(), cp.p, trow.p, tval.p, w.flags.p, st);
+    double s = d2h(w.scal.p, st);
+    norm = P.o.plan_norm == 0 ? s : sqrt(s);
+    if (Hf.nnz == 0) norm = 0.0;
+    symflags = d2h(w.flags.p, st);
+  }
+  P.norm = norm;
+  int M, N;
+  REQUIRE(plan_MN(norm, eps_tol, P.o.m_cap, P.o.n_window, M, N), SEXPM_EINFEASIBLE,
+          "Eq. (4.20) infeasible within m_cap / n_window");
+  if (P.o.force_M >= 0) M = P.o.force_M;
+  if (P.o.force_N >= 0) N = P.o.force_N;
+  P.M = M;
+  P.N = N;
+  int normal = P.o.normal;
+  if (normal < 0) normal = ((symflags & 1) == 0) || ((symflags & 2) == 0);
+  P.normal = normal;
+  P.a = normal ? 1.0 / (1.0 + (double)N) : (norm > 1.0 ? 1.0 / norm : 1.0);  // P:404, R8
+  const double normH0 = ldexp(norm, -N);
+  P.r0 = r0_series((long double)normH0, M);
+  P.eps_g0 = 0.0;
+  if (M >= 1)
+    P.eps_g0 = (double)((long double)P.a * P.r0 / ((long double)M * expl(2.0L * (long double)normH0)));
+  if (!P.o.filter) P.eps_g0 = 0.0;
+  // H0 = H 2^-N (exact)
+  launch_scale_pow2(Hf.val.p, Hf.nnz, -N, st);
+  CK(cudaEventRecord(e1, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaEventElapsedTime(&P.plan_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+// ------------------------------------------------------------------------------------
+// run: Taylor phase, squarings, finish
+// ------------------------------------------------------------------------------------
+static void do_run(sexpm_plan_s &P) {
+  cudaStream_t st = P.st;
+  sexpm_stats &S = P.stats;
+  const long long launches0 = g_kernel_launches;
+  memset(&S, 0, sizeof(S));
+  S.struct_size = sizeof(sexpm_stats);
+  S.M = P.M;
+  S.N = P.N;
+  S.normal = P.normal;
+  S.world = P.world;
+  S.rank = P.rank;
+  S.norm = P.norm;
+  S.a = P.a;
+  S.r0 = (double)P.r0;
+  S.eps_g0 = P.eps_g0;
+  S.ms_plan = P.plan_ms;
+  cudaEvent_t ev_start, ev_taylor, ev_sq, ev_end;
+  CK(cudaEventCreate(&ev_start));
+  CK(cudaEventCreate(&ev_taylor));
+  CK(cudaEventCreate(&ev_sq));
+  CK(cudaEventCreate(&ev_end));
+  CK(cudaEventRecord(ev_start, st));
+  const int64_t nl = P.row_end - P.row_begin;
+  DCsr H0loc;
+  slice_rows(P, P.H0full, P.row_begin, P.row_end, H0loc);
+  // ---- Taylor phase ----
+  DCsr T;
+  int M_eff = 0;
+  if (P.M == 0) {  // reading R9: T^_0 = 0
+    T.nrows = nl;
+    T.row0 = P.row_begin;
+    T.nnz = 0;
+    T.rp.alloc((size_t)nl + 1, st);
+    CK(cudaMemsetAsync(T.rp.p, 0, (nl + 1) * sizeof(int64_t), st));
+    T.col.alloc(1, st);
+    T.val.alloc(1, st);
+  } else {
+    copy_csr(P, H0loc.view(), T);  // T^_0^(1) = S_1 = H0
+    DCsr Sc;
+    copy_csr(P, H0loc.view(), Sc);
+    M_eff = 1;
+    for (int i = 2; i <= P.M; i++) {
+      cudaEvent_t a0, a1;
+      CK(cudaEventCreate(&a0));
+      CK(cudaEventCreate(&a1));
+      CK(cudaEventRecord(a0, st));
+      StepReport rep;
+      DCsr Sn;
+      filtered_product(P, Sc.view(), P.H0full.view(), 0.0, (double)i, P.eps_g0, Sn, rep);
+      if (i < SEXPM_MAXSTEP) {
+        S.taylor_nnz_unf[i] = rep.nnz_unf;
+        S.taylor_nnz[i] = rep.nnz;
+        S.taylor_passes[i] = rep.passes;
+        S.taylor_tau[i] = rep.tau;
+        S.taylor_numeric_ms[i] = rep.numeric_ms;
+        S.taylor_numeric_bytes[i] = rep.numeric_bytes;
+        S.taylor_fmas_i[i] = rep.fmas;
+      }
+      S.taylor_fmas += rep.fmas;
+      S.taylor_bytes += 12.0 * (double)Sc.nnz + 12.0 * (double)Sn.nnz + 16.0 * (double)nl;
+      if (rep.nnz == 0) {  // S^_i = 0: all later terms vanish
+        CK(cudaEventRecord(a1, st));
+        CK(cudaStreamSynchronize(st));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a0, a1));
+        if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = ms;
+        cudaEventDestroy(a0);
+        cudaEventDestroy(a1);
+        break;
+      }
+      M_eff = i;
+      DCsr Tn;
+      merge_add(P, T.view(), Sn.view(), Tn);  // T^_0^(i) = T^_0^(i-1) + S^_i
+      S.taylor_bytes += 12.0 * ((double)T.nnz + (double)Sn.nnz + (double)Tn.nnz);
+      T = std::move(Tn);
+      Sc = std::move(Sn);
+      CK(cudaEventRecord(a1, st));
+      CK(cudaStreamSynchronize(st));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a0, a1));
+      if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = ms;
+      cudaEventDestroy(a0);
+      cudaEventDestroy(a1);
+    }
+  }
+  P.M_eff = M_eff;
+  S.M_eff = M_eff;
+  CK(cudaEventRecord(ev_taylor, st));
+  // stats of T^_0
+  {
+    Workspace &w = P.ws;
+    w.rs.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    w.l1r.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    w.l2r.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    w.partial.ensure(1024, st);
+    w.scal.ensure(8, st);
+    w.i64tmp.ensure(8, st);
+    launch_row_stats(T.view(), w.rs.p, w.l1r.p, w.l2r.p, st);
+    launch_reduce_sum(w.rs.p, nl, w.partial.p, w.scal.p, st);
+    launch_reduce_max_i64(w.l1r.p, nl, w.i64tmp.p + 0, st);
+    launch_reduce_max_i64(w.l2r.p, nl, w.i64tmp.p + 1, st);
+    S.sq_normIT[0] = sqrt(allsum(P, d2h(w.scal.p, st)));
+    S.sq_l1[0] = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 0, st));
+    S.sq_l2[0] = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 1, st));
+    S.sq_nnz[0] = (int64_t)allsum(P, (double)T.nnz);
+  }
+  // ---- squarings ----
+  long double ri = P.r0;
+  double normIT = S.sq_normIT[0];
+  int64_t l1 = S.sq_l1[0], l2 = S.sq_l2[0];
+  for (int i = 1; i <= P.N; i++) {
+    cudaEvent_t a0, a1;
+    CK(cudaEventCreate(&a0));
+    CK(cudaEventCreate(&a1));
+    CK(cudaEventRecord(a0, st));
+    ri = 2.0L * ri;  // r_i = 2 r_{i-1}
+    double eps_g = P.o.threshold_mode == 1 ? (double)((long double)P.a * ri)
+                                           : (double)((long double)P.a * ri * (long double)normIT);
+    if (!P.o.filter) eps_g = 0.0;
+    StepReport rep;
+    DCsr Tn;
+    if (P.world == 1) {
+      filtered_product(P, T.view(), T.view(), 2.0, 1.0, eps_g, Tn, rep);
+    } else {
+      DCsr B;
+      exchange_halo(P, T, l1, l2, B);
+      filtered_product(P, T.view(), B.view(), 2.0, 1.0, eps_g, Tn, rep);
+    }
+    CK(cudaEventRecord(a1, st));
+    CK(cudaStreamSynchronize(st));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a0, a1));
+    cudaEventDestroy(a0);
+    cudaEventDestroy(a1);
+    if (i < SEXPM_MAXSTEP) {
+      S.sq_nnz_unf[i] = rep.nnz_unf;
+      S.sq_nnz[i] = rep.nnz;
+      S.sq_staged[i] = (int64_t)allsum(P, (double)rep.staged);
+      S.sq_passes[i] = rep.passes;
+      S.sq_eps_g[i] = eps_g;
+      S.sq_tau[i] = rep.tau;
+      S.sq_normIT[i] = sqrt(rep.normIT2);
+      S.sq_l1[i] = rep.l1;
+      S.sq_l2[i] = rep.l2;
+      S.sq_fmas[i] = allsum(P, rep.fmas);
+      S.sq_ms[i] = ms;
+      S.sq_numeric_ms[i] = rep.numeric_ms;
+      S.sq_numeric_bytes[i] = rep.numeric_bytes;
+      S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)Tn.nnz + 16.0 * (double)nl;
+    }
+    normIT = sqrt(rep.normIT2);
+    l1 = rep.l1;
+    l2 = rep.l2;
+    T = std::move(Tn);
+  }
+  CK(cudaEventRecord(ev_sq, st));
+  // ---- e^H = I + T^_N ----
+  if (P.o.output_T) {
+    P.E = std::move(T);
+  } else {
+    DCsr I;
+    I.nrows = nl;
+    I.row0 = P.row_begin;
+    I.nnz = nl;
+    I.rp.alloc((size_t)nl + 1, st);
+    I.col.alloc((size_t)nl, st);
+    I.val.alloc((size_t)nl, st);
+    launch_identity(nl, P.row_begin, I.rp.p, I.col.p, I.val.p, st);
+    DCsr E;
+    merge_add(P, T.view(), I.view(), E);
+    P.E = std::move(E);
+  }
+  CK(cudaEventRecord(ev_end, st));
+  CK(cudaStreamSynchronize(st));
+  float t1, t2, t3, t4;
+  CK(cudaEventElapsedTime(&t1, ev_start, ev_taylor));
+  CK(cudaEventElapsedTime(&t2, ev_taylor, ev_sq));
+  CK(cudaEventElapsedTime(&t3, ev_sq, ev_end));
+  CK(cudaEventElapsedTime(&t4, ev_start, ev_end));
+  S.ms_taylor = t1;
+  S.ms_squaring = t2;
+  S.ms_finalize = t3;
+  S.ms_total = t4;
+  S.nnz_out = P.E.nnz;
+  S.gpu_launches = (int32_t)(g_kernel_launches - launches0);
+  cudaEventDestroy(ev_start);
+  cudaEventDestroy(ev_taylor);
+  cudaEventDestroy(ev_sq);
+  cudaEventDestroy(ev_end);
+  P.have_result = true;
+}
+
+// ------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------
+#define ABI_BEGIN try {
+#define ABI_END                                                  \
+  }                                                              \
+  catch (const SxError &e) {                                     \
+    g_err = e.msg;                                               \
+    return e.code;                                               \
+  }                                                              \
+  catch (const std::exception &e) {                              \
+    g_err = e.what();                                            \
+    return SEXPM_EINTERNAL;                                      \
+  }                                                              \
+  catch (...) {                                                  \
+    g_err = "unknown exception";                                 \
+    return SEXPM_EINTERNAL;                                      \
+  }                                                              \
+  return SEXPM_OK;
+
+extern "C" {
+
+const char *sexpm_last_error(void) { return g_err.c_str(); }
+
+int sexpm_kernel_launches(int64_t *count) {
+  if (!count) return SEXPM_EINVAL;
+  *count = (int64_t)g_kernel_launches;
+  return SEXPM_OK;
+}
+
+int sexpm_abi_sizes(uint32_t *sizes) {
+  if (!sizes) return SEXPM_EINVAL;
+  sizes[0] = sizeof(sexpm_options);
+  sizes[1] = sizeof(sexpm_stats);
+  sizes[2] = sizeof(sexpm_csr_in);
+  sizes[3] = sizeof(sexpm_csr_out);
+  return SEXPM_OK;
+}
+
+int sexpm_options_init(sexpm_options *o) {
+  if (!o) return SEXPM_EINVAL;
+  memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(sexpm_options);
+  o->plan_norm = 0;
+  o->normal = -1;
+  o->threshold_mode = 0;
+  o->filter = 1;
+  o->m_cap = 120;
+  o->n_window = 50;
+  o->force_M = -1;
+  o->force_N = -1;
+  o->output_T = 0;
+  o->window_cols = 0;
+  o->e_r = 0.1;
+  o->stream = nullptr;
+  o->nccl_comm = nullptr;
+  return SEXPM_OK;
+}
+
+int sexpm_nccl_unique_id(void *id128) {
+  ABI_BEGIN
+  REQUIRE(id128, SEXPM_EINVAL, "null id");
+  ncclUniqueId id;
+  NK(nccl().GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(id128, &id, sizeof(id));
+  ABI_END
+}
+
+int sexpm_nccl_comm_init(int rank, int world, const void *id128, void **comm) {
+  ABI_BEGIN
+  REQUIRE(id128 && comm && world >= 1 && rank >= 0 && rank < world, SEXPM_EINVAL, "bad args");
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  ncclComm_t c;
+  NK(nccl().CommInitRank(&c, world, id, rank));
+  *comm = c;
+  ABI_END
+}
+
+int sexpm_nccl_comm_destroy(void *comm) {
+  ABI_BEGIN
+  if (comm) NK(nccl().CommDestroy((ncclComm_t)comm));
+  ABI_END
+}
+
+static sexpm_plan_s *new_plan(const sexpm_options *o) {
+  sexpm_plan_s *P = new sexpm_plan_s();
+  if (o) {
+    REQUIRE(o->struct_size == sizeof(sexpm_options), SEXPM_EINVAL, "sexpm_options ABI mismatch");
+    P->o = *o;
+  } else {
+    sexpm_options_init(&P->o);
+  }
+  CK(cudaGetDevice(&P->dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, P->dev));
+  P->sm_count = prop.multiProcessorCount;
+  int window = P->o.window_cols > 0 ? P->o.window_cols : 8192;
+  int smem = numeric_smem_bytes(window);
+  REQUIRE(smem <= (int)prop.sharedMemPerBlockOptin - 2048, SEXPM_EINVAL, "window too large");
+  P->numeric_blocks_per_sm = std::max(1, std::min(4, (int)(prop.sharedMemPerMultiprocessor / (smem + 4096))));
+  if (P->o.stream) {
+    P->st = (cudaStream_t)P->o.stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
+    P->own_stream = true;
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, P->dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (P->o.nccl_comm) {
+    P->comm = (ncclComm_t)P->o.nccl_comm;
+    int r = 0, w = 1;
+    auto &api = nccl();
+    (void)api;
+    ncclResult_t (*CountF)(const ncclComm_t, int *) =
+        reinterpret_cast<ncclResult_t (*)(const ncclComm_t, int *)>(dlsym(RTLD_DEFAULT, "ncclCommCount"));
+    ncclResult_t (*RankF)(const ncclComm_t, int *) =
+        reinterpret_cast<ncclResult_t (*)(const ncclComm_t, int *)>(dlsym(RTLD_DEFAULT, "ncclCommUserRank"));
+    REQUIRE(CountF && RankF, SEXPM_ENCCL, "ncclCommCount / ncclCommUserRank missing");
+    NK(CountF(P->comm, &w));
+    NK(RankF(P->comm, &r));
+    P->world = w;
+    P->rank = r;
+  }
+  return P;
+}
+
+static int plan_common(const sexpm_csr_in *H, double eps_tol, const sexpm_options *o,
+                       sexpm_plan_t *out, bool host) {
+  if (!out || !H) {
+    g_err = "null argument";
+    return SEXPM_EINVAL;
+  }
+  *out = nullptr;
+  sexpm_plan_s *P = nullptr;
+  try {
+    P = new_plan(o);
+    if (host) {
+      // copy the host CSR in (H2D inside the call, for end-to-end timing)
+      sexpm_csr_in D = *H;
+      const int64_t rows = H->row_end - H->row_begin;
+      REQUIRE(rows >= 0 && H->rowptr, SEXPM_EINVAL, "bad host CSR");
+      DCsr tmp;
+      tmp.rp.alloc((size_t)rows + 1, P->st);
+      tmp.col.alloc((size_t)std::max<int64_t>(H->nnz, 1), P->st);
+      tmp.val.alloc((size_t)std::max<int64_t>(H->nnz, 1), P->st);
+      CK(cudaMemcpyAsync(tmp.rp.p, H->rowptr, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, P->st));
+      if (H->nnz) {
+        CK(cudaMemcpyAsync(tmp.col.p, H->colidx, H->nnz * sizeof(int32_t), cudaMemcpyHostToDevice, P->st));
+        CK(cudaMemcpyAsync(tmp.val.p, H->vals, H->nnz * sizeof(double), cudaMemcpyHostToDevice, P->st));
+      }
+      D.rowptr = tmp.rp.p;
+      D.colidx = tmp.col.p;
+      D.vals = tmp.val.p;
+      do_plan(*P, &D, eps_tol);
+    } else {
+      do_plan(*P, H, eps_tol);
+    }
+    *out = P;
+    return SEXPM_OK;
+  } catch (const SxError &e) {
+    g_err = e.msg;
+    if (P) {
+      if (P->own_stream) cudaStreamSynchronize(P->st);
+      delete P;
+    }
+    return e.code;
+  } catch (...) {
+    g_err = "unknown exception in sexpm_plan";
+    delete P;
+    return SEXPM_EINTERNAL;
+  }
+}
+
+int sexpm_plan(const sexpm_csr_in *H, double eps_tol, const sexpm_options *o, sexpm_plan_t *out) {
+  return plan_common(H, eps_tol, o, out, false);
+}
+
+int sexpm_plan_host(const sexpm_csr_in *H, double eps_tol, const sexpm_options *o,
+                    sexpm_plan_t *out) {
+  return plan_common(H, eps_tol, o, out, true);
+}
+
+int sexpm_run(sexpm_plan_t p, sexpm_csr_out *E) {
+  ABI_BEGIN
+  REQUIRE(p, SEXPM_EINVAL, "null plan");
+  do_run(*p);
+  if (E) {
+    E->n = p->n;
+    E->row_begin = p->row_begin;
+    E->row_end = p->row_end;
+    E->nnz = p->E.nnz;
+    E->rowptr = p->E.rp.p;
+    E->colidx = p->E.col.p;
+    E->vals = p->E.val.p;
+  }
+  ABI_END
+}
+
+int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *vals) {
+  ABI_BEGIN
+  REQUIRE(p && p->have_result, SEXPM_ESTATE, "no result: call sexpm_run first");
+  REQUIRE(rowptr && (p->E.nnz == 0 || (colidx && vals)), SEXPM_EINVAL, "null host arrays");
+  CK(cudaMemcpyAsync(rowptr, p->E.rp.p, (p->E.nrows + 1) * sizeof(int64_t), cudaMemcpyDefault, p->st));
+  if (p->E.nnz) {
+    CK(cudaMemcpyAsync(colidx, p->E.col.p, p->E.nnz * sizeof(int32_t), cudaMemcpyDefault, p->st));
+    CK(cudaMemcpyAsync(vals, p->E.val.p, p->E.nnz * sizeof(double), cudaMemcpyDefault, p->st));
+  }
+  CK(cudaStreamSynchronize(p->st));
+  ABI_END
+}
+
+int sexpm_stats_get(sexpm_plan_t p, sexpm_stats *s) {
+  ABI_BEGIN
+  REQUIRE(p && s, SEXPM_EINVAL, "null argument");
+  REQUIRE(s->struct_size == sizeof(sexpm_stats), SEXPM_EINVAL, "sexpm_stats ABI mismatch");
+  if (!p->have_result || p->stats.struct_size != sizeof(sexpm_stats)) {
+    memset(s, 0, sizeof(*s));
+    s->struct_size = sizeof(sexpm_stats);
+    s->M = p->M;
+    s->N = p->N;
+    s->normal = p->normal;
+    s->norm = p->norm;
+    s->a = p->a;
+    s->r0 = (double)p->r0;
+    s->eps_g0 = p->eps_g0;
+    s->ms_plan = p->plan_ms;
+    s->world = p->world;
+    s->rank = p->rank;
+  } else {
+    *s = p->stats;
+  }
+  ABI_END
+}
+
+int sexpm_destroy(sexpm_plan_t p) {
+  ABI_BEGIN
+  if (!p) return SEXPM_OK;
+  cudaStreamSynchronize(p->st);
+  cudaStream_t st = p->st;
+  bool own = p->own_stream;
+  delete p;
+  cudaStreamSynchronize(st);
+  if (own) cudaStreamDestroy(st);
+  ABI_END
+}
+
+int sexpm_filtered_product(sexpm_plan_t p, const sexpm_csr_in *A, const sexpm_csr_in *B,
+                           double self_coef, double divisor, double eps_g, sexpm_csr_out *C,
+                           int32_t *passes, double *tau, int64_t *nnz_unf) {
+  ABI_BEGIN
+  REQUIRE(p && A && B && C, SEXPM_EINVAL, "null argument");
+  REQUIRE(p->world == 1, SEXPM_EINVAL, "component entry points are single-GPU");
+  REQUIRE(divisor != 0.0 && isfinite(eps_g) && eps_g >= 0.0, SEXPM_EINVAL, "bad scalars");
+  CsrView Av = view_of(A), Bv = view_of(B);
+  StepReport rep;
+  DCsr out;
+  filtered_product(*p, Av, Bv, self_coef, divisor, eps_g, out, rep);
+  p->E = std::move(out);
+  p->have_result = true;  // sexpm_result_copy reads it; sexpm_stats_get is not updated
+  C->n = A->n;
+  C->row_begin = A->row_begin;
+  C->row_end = A->row_end;
+  C->nnz = p->E.nnz;
+  C->rowptr = p->E.rp.p;
+  C->colidx = p->E.col.p;
+  C->vals = p->E.val.p;
+  if (passes) *passes = rep.passes;
+  if (tau) *tau = rep.tau;
+  if (nnz_unf) *nnz_unf = rep.nnz_unf;
+  ABI_END
+}
+
+int sexpm_alg41(sexpm_plan_t p, const double *x, int64_t cnt, double eps_g, double e_r,
+                int32_t *passes, double *tau, double *dropped) {
+  ABI_BEGIN
+  REQUIRE(p && (x || cnt == 0) && cnt >= 0 && e_r > 0.0 && eps_g >= 0.0, SEXPM_EINVAL, "bad args");
+  Workspace &w = p->ws;
+  w.partial.ensure(1024, p->st);
+  w.scal.ensure(8, p->st);
+  int np = 0;
+  double t = 0.0;
+  if (eps_g == 0.0) {
+    t = 0.0;
+  } else {
+    long double m = 1.0L, b = 1.0L, epsf = INFINITY;
+    const long double eg = eps_g, lim = eg * (1.0L + (long double)e_r);
+    while (b > lim) {
+      epsf = eg / m;
+      launch_alg41_pass(x, cnt, (double)epsf, w.partial.p, w.scal.p, p->st);
+      double S = d2h(w.scal.p, p->st);
+      b = sqrtl((long double)S);
+      m = b / epsf;
+      np++;
+      REQUIRE(np < 256, SEXPM_EINTERNAL, "Algorithm 4.1 pass cap");
+    }
+    t = np == 0 ? INFINITY : (double)epsf;
+  }
+  // dropped norm: everything <= t (or all, when the loop never ran)
+  launch_alg41_pass(x, cnt, np == 0 && eps_g != 0.0 ? INFINITY : t, w.partial.p, w.scal.p, p->st);
+  double d = sqrt(d2h(w.scal.p, p->st));
+  if (eps_g == 0.0) d = 0.0;
+  if (passes) *passes = np;
+  if (tau) *tau = t;
+  if (dropped) *dropped = d;
+  ABI_END
+}
+
+int sexpm_halo_ranges(int world, int rank, const int64_t *bounds, int64_t n, int64_t l1,
+                      int64_t l2, int64_t *recv_lo, int64_t *recv_hi) {
+  ABI_BEGIN
+  REQUIRE(world >= 1 && rank >= 0 && rank < world && bounds && recv_lo && recv_hi && l1 >= 0 &&
+              l2 >= 0,
+          SEXPM_EINVAL, "bad args");
+  for (int g = 0; g < world; g++)
+    REQUIRE(bounds[g] <= bounds[g + 1], SEXPM_EINVAL, "bounds must be non-decreasing");
+  REQUIRE(bounds[0] == 0 && bounds[world] == n, SEXPM_EINVAL, "bounds must cover [0, n)");
+  halo_ranges_host(world, rank, bounds, n, l1, l2, recv_lo, recv_hi);
+  ABI_END
+}
+
+int sexpm_partition_rows(int64_t n, const double *work, int world, int64_t *bounds) {
+  ABI_BEGIN
+  REQUIRE(n >= 0 && world >= 1 && bounds, SEXPM_EINVAL, "bad args");
+  double total = 0.0;
+  if (work)
+    for (int64_t i = 0; i < n; i++) total += work[i];
+  else
+    total = (double)n;
+  bounds[0] = 0;
+  double acc = 0.0;
+  int g = 1;
+  for (int64_t i = 0; i < n && g < world; i++) {
+    acc += work ? work[i] : 1.0;
+    while (g < world && acc >= total * (double)g / (double)world) {
+      bounds[g++] = i + 1;
+    }
+  }
+  while (g < world) bounds[g++] = n;
+  bounds[world] = n;
+  for (int k = 1; k <= world; k++)
+    if (bounds[k] < bounds[k - 1]) bounds[k] = bounds[k - 1];
+  ABI_END
+}
+
+}  // extern "C"

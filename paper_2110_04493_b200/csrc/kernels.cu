@@ -1,0 +1,948 @@
+// kernels.cu — sm_100a kernels of libsexpm (fp64 CUDA cores; no tensor cores: the
+// work is a sparse Gustavson product, not a dense contraction).
+//
+// PAPER.md citations: P:<line>.  Kernel ids follow SURVEY.md §2.3 / DESIGN.md:
+//   K8 norms/validation (plan, P:392 needs ||H||), K1 symbolic row bound (Lemma 3.1,
+//   P:96-128), K2 binning, K3 numeric SpGEMM + fused 2T add + filter classification
+//   (Eq. 2.7, Eq. 4.15, Eq. 4.11), K6 Algorithm 4.1 pass,
+//   K4 compaction ("A~ = A - b_n"), merge T^_0 += S^_i and I + T.
+#include <math.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+
+namespace sx {
+
+long long g_kernel_launches = 0;  // kernels enqueued (reported as gpu_launches)
+#define KL (++g_kernel_launches)
+
+#define FULL_MASK 0xffffffffu
+
+static inline int grid_for(int64_t items, int per_block, int cap = 1 << 30) {
+  int64_t g = (items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL_MASK, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_down_sync(FULL_MASK, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_down_sync(FULL_MASK, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------------------------
+// K8: validation and transpose-based norm / symmetry (plan time)
+// ------------------------------------------------------------------------------------
+// flags[0] bits: 1 bad rowptr, 2 column out of range, 4 columns not strictly increasing,
+// 8 non-finite value.
+__global__ void k_validate(CsrView A, int64_t n, int *flags) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= A.nrows) return;
+  int64_t p0 = A.rp[w], p1 = A.rp[w + 1];
+  int f = 0;
+  if (p1 < p0 || p0 < 0 || p1 > A.nnz) f |= 1;
+  else {
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+      int32_t c = A.col[p];
+      if (c < 0 || c >= n) f |= 2;
+      if (p > p0 && A.col[p - 1] >= c) f |= 4;
+      if (!isfinite(A.val[p])) f |= 8;
+    }
+  }
+  f = __reduce_or_sync(FULL_MASK, f);
+  if (lane == 0 && f) atomicOr(flags, f);
+}
+void launch_validate(const CsrView &A, int64_t n, int *flags, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_validate<<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, n, flags);
+}
+
+__global__ void k_col_count(CsrView A, int32_t *cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < A.nnz; i += stride) atomicAdd(&cnt[A.col[i]], 1);
+}
+void launch_col_count(const CsrView &A, int32_t *cnt, cudaStream_t st) {
+  if (A.nnz == 0) return;
+  KL;
+  k_col_count<<<grid_for(A.nnz, kThreads, 148 * 16), kThreads, 0, st>>>(A, cnt);
+}
+
+__global__ void k_transpose_fill(CsrView A, unsigned long long *cursor, int32_t *trow,
+                                 double *tval) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= A.nrows) return;
+  for (int64_t p = A.rp[w] + lane; p < A.rp[w + 1]; p += 32) {
+    unsigned long long pos = atomicAdd(&cursor[A.col[p]], 1ull);
+    trow[pos] = (int32_t)(A.row0 + w);
+    tval[pos] = A.val[p];
+  }
+}
+void launch_transpose_fill(const CsrView &A, int64_t *cursor, int32_t *trow, double *tval,
+                           cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_transpose_fill<<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(
+      A, reinterpret_cast<unsigned long long *>(cursor), trow, tval);
+}
+
+// insertion sort of each column segment by row (columns of sparse H are short)
+__global__ void k_sort_columns(int64_t ncols, const int64_t *cp, int32_t *trow, double *tval) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  int64_t a = cp[j], b = cp[j + 1];
+  for (int64_t p = a + 1; p < b; p++) {
+    int32_t r = trow[p];
+    double v = tval[p];
+    int64_t q = p - 1;
+    while (q >= a && trow[q] > r) {
+      trow[q + 1] = trow[q];
+      tval[q + 1] = tval[q];
+      q--;
+    }
+    trow[q + 1] = r;
+    tval[q + 1] = v;
+  }
+}
+void launch_sort_columns(int64_t ncols, const int64_t *cp, int32_t *trow, double *tval,
+                         cudaStream_t st) {
+  if (ncols == 0) return;
+  KL;
+  k_sort_columns<<<grid_for(ncols, kThreads), kThreads, 0, st>>>(ncols, cp, trow, tval);
+}
+
+// column j: sum_i |h_ij| in ascending row order (the row-major order of the definition)
+__global__ void k_col_abs_sum(int64_t ncols, const int64_t *cp, const double *tval,
+                              double *out) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  double s = 0.0;
+  for (int64_t p = cp[j]; p < cp[j + 1]; p++) s = s + fabs(tval[p]);
+  out[j] = s;
+}
+void launch_col_abs_sum(int64_t ncols, const int64_t *cp, const double *tval, double *out,
+                        cudaStream_t st) {
+  if (ncols == 0) return;
+  KL;
+  k_col_abs_sum<<<grid_for(ncols, kThreads), kThreads, 0, st>>>(ncols, cp, tval, out);
+}
+
+// flags bit 1: H != H^T, bit 2: H != -H^T (bit-exact; A must hold all rows)
+__global__ void k_compare_transpose(CsrView A, const int64_t *cp, const int32_t *trow,
+                                    const double *tval, int *flags) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= A.nrows) return;
+  int64_t r = A.row0 + w;
+  int64_t p0 = A.rp[w], p1 = A.rp[w + 1];
+  int64_t q0 = cp[r], q1 = cp[r + 1];
+  int f = 0;
+  if (p1 - p0 != q1 - q0) f = 3;
+  else {
+    for (int64_t t = lane; t < p1 - p0; t += 32) {
+      if (A.col[p0 + t] != trow[q0 + t]) f |= 3;
+      if (A.val[p0 + t] != tval[q0 + t]) f |= 1;
+      if (A.val[p0 + t] != -tval[q0 + t]) f |= 2;
+    }
+  }
+  f = __reduce_or_sync(FULL_MASK, f);
+  if (lane == 0 && f) atomicOr(flags, f);
+}
+void launch_compare_transpose(const CsrView &A, const int64_t *cp, const int32_t *trow,
+                              const double *tval, int *flags, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_compare_transpose<<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, cp, trow,
+                                                                             tval, flags);
+}
+
+// ------------------------------------------------------------------------------------
+// Deterministic reductions: fixed grid of kRedBlocks CTAs over contiguous chunks, a
+// fixed thread-stride order inside each chunk, a fixed tree, then one CTA over partials.
+// ------------------------------------------------------------------------------------
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+
+enum RedOp { RED_SUM = 0, RED_SUMSQ = 1, RED_MAX = 2, RED_SUMSQ_LE = 3 };
+
+template <int OP>
+__device__ __forceinline__ double red_map(double x, double tau) {
+  if (OP == RED_SUMSQ) return x * x;
+  if (OP == RED_SUMSQ_LE) return fabs(x) <= tau ? x * x : 0.0;
+  return x;
+}
+template <int OP>
+__device__ __forceinline__ double red_comb(double a, double b) {
+  return OP == RED_MAX ? (a > b ? a : b) : a + b;
+}
+
+template <int OP>
+__device__ double block_reduce(double v) {
+  __shared__ double s[kWarps];
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = red_comb<OP>(v, __shfl_down_sync(FULL_MASK, v, o));
+  if (lane == 0) s[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    r = s[0];
+    for (int w = 1; w < kWarps; w++) r = red_comb<OP>(r, s[w]);
+  }
+  __syncthreads();
+  return r;
+}
+
+template <int OP>
+__global__ void k_reduce_partial(const double *x, int64_t cnt, double tau, double *partial) {
+  int64_t chunk = (cnt + gridDim.x - 1) / gridDim.x;
+  int64_t a = (int64_t)blockIdx.x * chunk;
+  int64_t b = a + chunk < cnt ? a + chunk : cnt;
+  double v = OP == RED_MAX ? -INFINITY : 0.0;
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x)
+    v = red_comb<OP>(v, red_map<OP>(x[i], tau));
+  double r = block_reduce<OP>(v);
+  if (threadIdx.x == 0) partial[blockIdx.x] = r;
+}
+template <int OP>
+__global__ void k_reduce_final(const double *partial, int np, double *out) {
+  double v = OP == RED_MAX ? -INFINITY : 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) v = red_comb<OP>(v, partial[i]);
+  double r = block_reduce<OP == RED_MAX ? RED_MAX : RED_SUM>(v);
+  if (threadIdx.x == 0) out[0] = (OP == RED_MAX && np == 0) ? 0.0 : r;
+}
+template <int OP>
+static void reduce_impl(const double *x, int64_t cnt, double tau, double *partial, double *out,
+                        cudaStream_t st) {
+  KL;
+  k_reduce_partial<OP><<<kRedBlocks, kThreads, 0, st>>>(x, cnt, tau, partial);
+  KL;
+  k_reduce_final<OP><<<1, kThreads, 0, st>>>(partial, kRedBlocks, out);
+}
+void launch_reduce_max(const double *x, int64_t cnt, double *partial, double *out,
+                       cudaStream_t st) {
+  reduce_impl<RED_MAX>(x, cnt, 0.0, partial, out, st);
+}
+void launch_reduce_sumsq(const double *x, int64_t cnt, double *partial, double *out,
+                         cudaStream_t st) {
+  reduce_impl<RED_SUMSQ>(x, cnt, 0.0, partial, out, st);
+}
+void launch_reduce_sum(const double *x, int64_t cnt, double *partial, double *out,
+                       cudaStream_t st) {
+  reduce_impl<RED_SUM>(x, cnt, 0.0, partial, out, st);
+}
+// K6: one pass of Algorithm 4.1 over the staged values: sum of x^2 with |x| <= tau
+void launch_alg41_pass(const double *x, int64_t cnt, double tau, double *partial, double *out,
+                       cudaStream_t st) {
+  reduce_impl<RED_SUMSQ_LE>(x, cnt, tau, partial, out, st);
+}
+
+__global__ void k_reduce_i64(const int64_t *x, int64_t cnt, int64_t *out, int is_max) {
+  __shared__ long long s[kWarps];
+  long long v = 0;
+  for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    long long y = x[i];
+    v = is_max ? (y > v ? y : v) : v + y;
+  }
+  v = is_max ? warp_max(v) : warp_sum(v);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long r = 0;
+    for (int w = 0; w < kWarps; w++) r = is_max ? (s[w] > r ? s[w] : r) : r + s[w];
+    out[0] = r;
+  }
+}
+void launch_reduce_max_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st) {
+  KL;
+  k_reduce_i64<<<1, kThreads, 0, st>>>(x, cnt, out, 1);
+}
+void launch_reduce_sum_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st) {
+  KL;
+  k_reduce_i64<<<1, kThreads, 0, st>>>(x, cnt, out, 0);
+}
+
+__global__ void k_scale_pow2(double *v, int64_t cnt, int e) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < cnt; i += stride) v[i] = ldexp(v[i], e);
+}
+void launch_scale_pow2(double *v, int64_t cnt, int e, cudaStream_t st) {
+  if (cnt == 0 || e == 0) return;
+  KL;
+  k_scale_pow2<<<grid_for(cnt, kThreads, 148 * 16), kThreads, 0, st>>>(v, cnt, e);
+}
+
+__global__ void k_row_lengths(const int64_t *rp, int64_t nrows, int64_t *out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) out[i] = rp[i + 1] - rp[i];
+}
+void launch_row_lengths(const int64_t *rp, int64_t nrows, int64_t *out, cudaStream_t st) {
+  if (nrows == 0) return;
+  KL;
+  k_row_lengths<<<grid_for(nrows, kThreads), kThreads, 0, st>>>(rp, nrows, out);
+}
+
+__global__ void k_copy_i64_offset(const int64_t *src, int64_t cnt, int64_t off, int64_t *dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) dst[i] = src[i] + off;
+}
+void launch_copy_i64_offset(const int64_t *src, int64_t cnt, int64_t off, int64_t *dst,
+                            cudaStream_t st) {
+  if (cnt == 0) return;
+  KL;
+  k_copy_i64_offset<<<grid_for(cnt, kThreads), kThreads, 0, st>>>(src, cnt, off, dst);
+}
+
+// ------------------------------------------------------------------------------------
+// Exclusive scan (reduce-then-scan, 3 kernels)
+// ------------------------------------------------------------------------------------
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kThreads * kScanItems;
+
+int64_t scan_tmp_elems(int64_t cnt) { return (cnt + kScanTile - 1) / kScanTile + 1; }
+
+__device__ long long block_excl_scan(long long v, long long *total) {
+  __shared__ long long s[kWarps];
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(FULL_MASK, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s[warp] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int w = 0; w < kWarps; w++) {
+      long long t = s[w];
+      s[w] = acc;
+      acc += t;
+    }
+    *total = acc;
+  }
+  __syncthreads();
+  long long r = x - v + s[warp];
+  __syncthreads();
+  return r;
+}
+
+__global__ void k_scan_tiles(const int64_t *in, int64_t cnt, int64_t *tile_sum) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+  long long v = 0;
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = base + (int64_t)k * kThreads + threadIdx.x;
+    if (i < cnt) v += in[i];
+  }
+  v = warp_sum(v);
+  __shared__ long long s[kWarps];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < kWarps; w++) t += s[w];
+    tile_sum[blockIdx.x] = t;
+  }
+}
+__global__ void k_scan_tile_sums(int64_t *tile_sum, int64_t ntiles) {
+  __shared__ long long total;
+  long long carry = 0;
+  for (int64_t b = 0; b < ntiles; b += kThreads) {
+    int64_t i = b + threadIdx.x;
+    long long v = i < ntiles ? tile_sum[i] : 0;
+    long long e = block_excl_scan(v, &total);
+    if (i < ntiles) tile_sum[i] = e + carry;
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_sum[ntiles] = carry;
+}
+__global__ void k_scan_apply(const int64_t *in, int64_t cnt, const int64_t *tile_sum,
+                             int64_t *out) {
+  __shared__ long long total;
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  long long loc[kScanItems];
+  long long s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = base + k;
+    loc[k] = i < cnt ? in[i] : 0;
+    s += loc[k];
+  }
+  long long e = block_excl_scan(s, &total) + tile_sum[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = base + k;
+    if (i < cnt) out[i] = e;
+    e += loc[k];
+  }
+}
+__global__ void k_scan_total(const int64_t *tile_sum, int64_t ntiles, int64_t cnt, int64_t *out) {
+  out[cnt] = tile_sum[ntiles];
+}
+void launch_exclusive_scan(const int64_t *in, int64_t cnt, int64_t *out, int64_t *tmp,
+                           cudaStream_t st) {
+  int64_t ntiles = (cnt + kScanTile - 1) / kScanTile;
+  if (ntiles > 0) {
+    KL;
+    k_scan_tiles<<<(int)ntiles, kThreads, 0, st>>>(in, cnt, tmp);
+    KL;
+    k_scan_tile_sums<<<1, kThreads, 0, st>>>(tmp, ntiles);
+    KL;
+    k_scan_apply<<<(int)ntiles, kThreads, 0, st>>>(in, cnt, tmp, out);
+    KL;
+    k_scan_total<<<1, 1, 0, st>>>(tmp, ntiles, cnt, out);
+  } else {
+    cudaMemsetAsync(out, 0, sizeof(int64_t), st);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K1 symbolic row bound (warp per output row).  Lemma 3.1: the nonzeros of
+// row r of A*B lie in [min_k first(B_k), max_k last(B_k)] for k in row r of A.
+// ------------------------------------------------------------------------------------
+__global__ void k_symbolic(CsrView A, CsrView B, int self, int32_t *lo, int32_t *hi,
+                           int64_t *prod, int64_t *bound) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= A.nrows) return;
+  int64_t p0 = A.rp[w], p1 = A.rp[w + 1];
+  int32_t l = INT32_MAX, h = -1;
+  long long pr = 0;
+  for (int64_t p = p0 + lane; p < p1; p += 32) {
+    int64_t k = (int64_t)A.col[p] - B.row0;
+    if (k < 0 || k >= B.nrows) continue;  // caller guarantees coverage (halo)
+    int64_t s = B.rp[k], e = B.rp[k + 1];
+    if (e > s) {
+      int32_t f = B.col[s], g = B.col[e - 1];
+      l = f < l ? f : l;
+      h = g > h ? g : h;
+      pr += e - s;
+    }
+  }
+  if (self && p1 > p0) {
+    if (lane == 0) {
+      int32_t f = A.col[p0], g = A.col[p1 - 1];
+      l = f < l ? f : l;
+      h = g > h ? g : h;
+      pr += p1 - p0;
+    }
+  }
+  l = warp_min(l);
+  h = warp_max(h);
+  pr = warp_sum(pr);
+  if (lane == 0) {
+    lo[w] = l;
+    hi[w] = h;
+    prod[w] = pr;
+    long long span = h >= l ? (long long)h - l + 1 : 0;
+    bound[w] = span < pr ? span : pr;
+  }
+}
+void launch_symbolic(const CsrView &A, const CsrView &B, int self, int32_t *lo, int32_t *hi,
+                     int64_t *prod, int64_t *bound, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_symbolic<<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, B, self, lo, hi, prod,
+                                                                    bound);
+}
+
+// ------------------------------------------------------------------------------------
+// K2 binning: rows ordered by descending work class (longest-processing-time first) so
+// the dynamic row scheduler of K3 ends with short rows.
+// ------------------------------------------------------------------------------------
+constexpr int kBins = 64;
+__device__ __forceinline__ int work_bin(long long w) {
+  return 63 - (w > 0 ? (63 - __clzll((unsigned long long)w)) : 0);  // heavy -> small bin id
+}
+__global__ void k_bin_count(int64_t nrows, const int64_t *work, int32_t *bin_cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) atomicAdd(&bin_cnt[work_bin(work[i])], 1);
+}
+__global__ void k_bin_offsets(int32_t *bin_cnt, int32_t *bin_off) {
+  if (threadIdx.x == 0) {
+    int32_t s = 0;
+    for (int b = 0; b < kBins; b++) {
+      bin_off[b] = s;
+      s += bin_cnt[b];
+      bin_cnt[b] = 0;
+    }
+  }
+}
+__global__ void k_bin_scatter(int64_t nrows, const int64_t *work, int32_t *bin_cnt,
+                              const int32_t *bin_off, int32_t *order) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) {
+    int b = work_bin(work[i]);
+    int32_t pos = bin_off[b] + atomicAdd(&bin_cnt[b], 1);
+    order[pos] = (int32_t)i;
+  }
+}
+void launch_bin_rows(int64_t nrows, const int64_t *work, int32_t *bin_cnt, int32_t *bin_off,
+                     int32_t *order, cudaStream_t st) {
+  if (nrows == 0) return;
+  cudaMemsetAsync(bin_cnt, 0, kBins * sizeof(int32_t), st);
+  KL;
+  k_bin_count<<<grid_for(nrows, kThreads), kThreads, 0, st>>>(nrows, work, bin_cnt);
+  KL;
+  k_bin_offsets<<<1, 32, 0, st>>>(bin_cnt, bin_off);
+  KL;
+  k_bin_scatter<<<grid_for(nrows, kThreads), kThreads, 0, st>>>(nrows, work, bin_cnt, bin_off,
+                                                               order);
+}
+
+// ------------------------------------------------------------------------------------
+// K3 numeric filtered SpGEMM (one CTA per output row, dynamic row scheduler).
+//
+//   C~(r,:) = (self_coef * A(r,:) + sum_{k in row r of A} a_rk * B(k,:)) / divisor
+//
+// Squaring (Eq. 2.7 P:76 / Eq. 4.15): A = B = T^_{i-1}, self_coef = 2, divisor = 1.
+// Taylor term (Eq. 4.11, Alg. 4.2): A = S^_{i-1}, B = H0, self 0, divisor i.
+//
+// Accumulator: a dense shared-memory window over the row's reachable column span
+// [lo, hi] (K1), processed in chunks of `window` columns; B rows are sorted, so each
+// k keeps a cursor that only moves forward across chunks.  The 2T term is stored first
+// (no other writer in that phase), products are added with shared-memory atomics
+// (warps work on different k), and the flush fuses the filter classification of
+// Algorithm 4.1: entries with |x| <= floor_tau = eps_g / sqrt(K) can never be kept
+// (every threshold the algorithm visits is >= eps_g / sqrt(K), K >= #entries; see
+// DESIGN.md "floor lemma"), so only their x^2 is kept (per-row partial sums); the
+// others are staged (col, val) in column order for the passes (K6) and compaction (K4).
+// ------------------------------------------------------------------------------------
+int numeric_smem_bytes(int window) { return window * (int)sizeof(double); }
+
+__global__ void __launch_bounds__(kThreads) k_numeric(NumericArgs a) {
+  extern __shared__ double win[];
+  __shared__ int s_row;
+  __shared__ long long s_wcnt[kWarps];
+  __shared__ long long s_base[kWarps + 1];
+  __shared__ long long s_selfcur;
+  __shared__ unsigned long long s_off;
+  __shared__ double s_fs[kWarps];
+  __shared__ long long s_nz[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = a.window;
+  for (int i = tid; i < W; i += kThreads) win[i] = 0.0;
+  int64_t *cur = a.cursor + (int64_t)blockIdx.x * a.cursor_cap;
+  int32_t *sc = a.scr_col + (int64_t)blockIdx.x * a.scr_cap;
+  double *sv = a.scr_val + (int64_t)blockIdx.x * a.scr_cap;
+  const double inv_div_flag = a.divisor;  // division (not reciprocal multiply), reading R7
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int idx = s_row;
+    if (idx >= a.A.nrows) break;
+    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
+    const int32_t lo = a.lo[r], hi = a.hi[r];
+    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
+    const int64_t nk = pa1 - pa0;
+    if (hi < lo) {
+      if (tid == 0) {
+        a.row_off[r] = 0;
+        a.row_cnt[r] = 0;
+        a.row_fsum[r] = 0.0;
+        a.row_nnz[r] = 0;
+      }
+      continue;
+    }
+    for (int64_t q = tid; q < nk; q += kThreads) {
+      int64_t k = (int64_t)a.A.col[pa0 + q] - a.B.row0;
+      cur[q] = (k >= 0 && k < a.B.nrows) ? a.B.rp[k] : -1;
+    }
+    if (tid == 0) s_selfcur = pa0;
+    long long nst = 0;
+    double fs = 0.0;
+    long long nnzu = 0;
+    __syncthreads();
+    for (int64_t c0 = lo; c0 <= hi; c0 += W) {
+      const int64_t c1 = (c0 + W < (int64_t)hi + 1) ? c0 + W : (int64_t)hi + 1;
+      const int wlen = (int)(c1 - c0);
+      if (a.self_coef != 0.0) {
+        const long long sc0 = s_selfcur;
+        long long done = 0;
+        for (long long p = sc0 + tid;; p += kThreads) {
+          bool v = p < pa1 && (int64_t)a.A.col[p] < c1;
+          if (v) win[a.A.col[p] - c0] = a.self_coef * a.A.val[p];
+          int cnt = __syncthreads_count(v);
+          done += cnt;
+          if (cnt < kThreads) break;
+        }
+        if (tid == 0) s_selfcur = sc0 + done;
+        __syncthreads();
+      }
+      for (int64_t q = warp; q < nk; q += kWarps) {
+        long long pos = cur[q];
+        if (pos < 0) continue;
+        const int64_t k = (int64_t)a.A.col[pa0 + q] - a.B.row0;
+        const long long end = a.B.rp[k + 1];
+        const double av = a.A.val[pa0 + q];
+        for (;;) {
+          long long p = pos + lane;
+          bool v = false;
+          int32_t c = 0;
+          if (p < end) {
+            c = a.B.col[p];
+            v = (int64_t)c < c1;
+          }
+          if (v) {
+            double prod = av * a.B.val[p];
+            atomicAdd(&win[c - c0], prod);
+          }
+          int cnt = __popc(__ballot_sync(FULL_MASK, v));
+          pos += cnt;
+          if (cnt < 32) break;
+        }
+        if (lane == 0) cur[q] = pos;
+      }
+      __syncthreads();
+      // flush, pass 1: staged count per warp sub-range
+      const int per = (((wlen + kWarps - 1) / kWarps) + 31) & ~31;
+      const int w0 = warp * per;
+      const int w1 = (w0 + per < wlen) ? w0 + per : wlen;
+      long long wc = 0;
+      for (int base = w0; base < w1; base += 32) {
+        int i = base + lane;
+        bool st = false;
+        if (i < w1) {
+          double x = win[i] / inv_div_flag;
+          st = (x != 0.0) && (fabs(x) > a.floor_tau);
+        }
+        wc += __popc(__ballot_sync(FULL_MASK, st));
+      }
+      if (lane == 0) s_wcnt[warp] = wc;
+      __syncthreads();
+      if (tid == 0) {
+        long long s = 0;
+        for (int w = 0; w < kWarps; w++) {
+          s_base[w] = s;
+          s += s_wcnt[w];
+        }
+        s_base[kWarps] = s;
+      }
+      __syncthreads();
+      // pass 2: classify, stage in column order, reset the window
+      long long o = nst + s_base[warp];
+      for (int base = w0; base < w1; base += 32) {
+        int i = base + lane;
+        bool st = false;
+        double x = 0.0;
+        if (i < w1) {
+          x = win[i] / inv_div_flag;
+          win[i] = 0.0;
+          if (x != 0.0) {
+            nnzu++;
+            st = fabs(x) > a.floor_tau;
+            if (!st) fs += x * x;
+          }
+        }
+        unsigned m = __ballot_sync(FULL_MASK, st);
+        if (st) {
+          long long pp = o + __popc(m & lanemask_lt());
+          if (pp < a.scr_cap) {
+            sc[pp] = (int32_t)(c0 + i);
+            sv[pp] = x;
+          }
+        }
+        o += __popc(m);
+      }
+      nst += s_base[kWarps];
+      __syncthreads();
+    }
+    // per-row partials (deterministic tree)
+    fs = warp_sum(fs);
+    nnzu = warp_sum(nnzu);
+    if (lane == 0) {
+      s_fs[warp] = fs;
+      s_nz[warp] = nnzu;
+    }
+    if (tid == 0) s_off = atomicAdd(a.pool_used, (unsigned long long)nst);
+    __syncthreads();
+    const unsigned long long off = s_off;
+    const bool ok = (long long)off + nst <= a.pool_cap && nst <= a.scr_cap;
+    if (ok) {
+      for (long long t = tid; t < nst; t += kThreads) {
+        a.pool_col[off + t] = sc[t];
+        a.pool_val[off + t] = sv[t];
+      }
+    }
+    if (tid == 0) {
+      double f = 0.0;
+      long long z = 0;
+      for (int w = 0; w < kWarps; w++) {
+        f += s_fs[w];
+        z += s_nz[w];
+      }
+      if (!ok) atomicOr(a.flags, nst > a.scr_cap ? 2 : 1);
+      a.row_off[r] = (int64_t)off;
+      a.row_cnt[r] = nst;
+      a.row_fsum[r] = f;
+      a.row_nnz[r] = z;
+    }
+  }
+}
+
+void launch_numeric(const NumericArgs &a, cudaStream_t st) {
+  if (a.A.nrows == 0) return;
+  int smem = numeric_smem_bytes(a.window);
+  cudaFuncSetAttribute(k_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric<<<a.grid, kThreads, smem, st>>>(a);
+}
+
+// ------------------------------------------------------------------------------------
+// K4 compaction: keep staged entries with |x| > tau (Alg. 4.1 step 3).
+// ------------------------------------------------------------------------------------
+__global__ void k_compact_count(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
+                                const double *pool_val, double tau, int64_t *cnt) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= nrows) return;
+  int64_t o = row_off[w], c = row_cnt[w];
+  long long k = 0;
+  for (int64_t t = lane; t < c; t += 32) k += fabs(pool_val[o + t]) > tau;
+  k = warp_sum(k);
+  if (lane == 0) cnt[w] = k;
+}
+void launch_compact_count(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
+                          const double *pool_val, double tau, int64_t *cnt, cudaStream_t st) {
+  if (nrows == 0) return;
+  KL;
+  k_compact_count<<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(nrows, row_off, row_cnt,
+                                                                       pool_val, tau, cnt);
+}
+
+__device__ __forceinline__ void row_stat_accum(int64_t grow, int32_t c, double x, double &s,
+                                               int &have_diag, long long &l1, long long &l2) {
+  long long d = (long long)c - grow;
+  if (d == 0) {
+    double y = x + 1.0;
+    s += y * y;
+    have_diag = 1;
+  } else {
+    s += x * x;
+  }
+  if (d > l1) l1 = d;
+  if (-d > l2) l2 = -d;
+}
+__device__ __forceinline__ void row_stat_finish(int lane, int64_t w, double s, int have_diag,
+                                                long long l1, long long l2, double *rs,
+                                                int64_t *l1r, int64_t *l2r) {
+  s = warp_sum(s);
+  have_diag = __reduce_or_sync(FULL_MASK, have_diag);
+  l1 = warp_max(l1);
+  l2 = warp_max(l2);
+  if (lane == 0) {
+    if (rs) rs[w] = s + (have_diag ? 0.0 : 1.0);
+    if (l1r) l1r[w] = l1;
+    if (l2r) l2r[w] = l2;
+  }
+}
+
+__global__ void k_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
+                                const int64_t *row_cnt, const int32_t *pool_col,
+                                const double *pool_val, double tau, const int64_t *rp_out,
+                                int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
+                                int64_t *l2r) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= nrows) return;
+  int64_t o = row_off[w], c = row_cnt[w];
+  int64_t dst = rp_out[w];
+  const int64_t grow = row0 + w;
+  double s = 0.0;
+  int have_diag = 0;
+  long long l1 = 0, l2 = 0;
+  for (int64_t base = 0; base < c; base += 32) {
+    int64_t t = base + lane;
+    bool k = false;
+    double x = 0.0;
+    int32_t cc = 0;
+    if (t < c) {
+      x = pool_val[o + t];
+      cc = pool_col[o + t];
+      k = fabs(x) > tau;
+    }
+    unsigned m = __ballot_sync(FULL_MASK, k);
+    if (k) {
+      int64_t q = dst + __popc(m & lanemask_lt());
+      col_out[q] = cc;
+      val_out[q] = x;
+      row_stat_accum(grow, cc, x, s, have_diag, l1, l2);
+    }
+    dst += __popc(m);
+  }
+  row_stat_finish(lane, w, s, have_diag, l1, l2, rs, l1r, l2r);
+}
+void launch_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
+                          const int64_t *row_cnt, const int32_t *pool_col,
+                          const double *pool_val, double tau, const int64_t *rp_out,
+                          int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
+                          int64_t *l2r, cudaStream_t st) {
+  if (nrows == 0) return;
+  KL;
+  k_compact_write<<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(
+      nrows, row0, row_off, row_cnt, pool_col, pool_val, tau, rp_out, col_out, val_out, rs, l1r,
+      l2r);
+}
+
+__global__ void k_row_stats(CsrView C, double *rs, int64_t *l1r, int64_t *l2r) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= C.nrows) return;
+  const int64_t grow = C.row0 + w;
+  double s = 0.0;
+  int have_diag = 0;
+  long long l1 = 0, l2 = 0;
+  for (int64_t p = C.rp[w] + lane; p < C.rp[w + 1]; p += 32)
+    row_stat_accum(grow, C.col[p], C.val[p], s, have_diag, l1, l2);
+  row_stat_finish(lane, w, s, have_diag, l1, l2, rs, l1r, l2r);
+}
+void launch_row_stats(const CsrView &C, double *rs, int64_t *l1r, int64_t *l2r,
+                      cudaStream_t st) {
+  if (C.nrows == 0) return;
+  KL;
+  k_row_stats<<<grid_for(C.nrows * 32, kThreads), kThreads, 0, st>>>(C, rs, l1r, l2r);
+}
+
+// ------------------------------------------------------------------------------------
+// Merge C = A + B of two row-sorted CSRs over the same rows (warp per row).
+// Equal columns are summed as a + b (T^_0 + S^_i; T^_N + I); sums that
+// are exactly zero are purged.  Each round takes up to 32 entries of each list and
+// emits every entry with column <= min(last loaded column of a side that has more).
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int lower_bound32(const int32_t *s, int32_t key) {
+  int lo = 0, hi = 32;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (s[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <bool WRITE>
+__global__ void k_merge(CsrView A, CsrView B, const int64_t *rp_out, int64_t *cnt,
+                        int32_t *col_out, double *val_out) {
+  __shared__ int32_t sA[kWarps][32], sB[kWarps][32];
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  if (w >= A.nrows) return;
+  int64_t a0 = A.rp[w], na = A.rp[w + 1] - a0;
+  int64_t b0 = B.rp[w], nb = B.rp[w + 1] - b0;
+  int64_t i = 0, j = 0, out = WRITE ? rp_out[w] : 0;
+  while (i < na || j < nb) {
+    bool ina = i + lane < na, inb = j + lane < nb;
+    int32_t ca = ina ? A.col[a0 + i + lane] : INT32_MAX;
+    int32_t cb = inb ? B.col[b0 + j + lane] : INT32_MAX;
+    double va = ina ? A.val[a0 + i + lane] : 0.0;
+    double vb = inb ? B.val[b0 + j + lane] : 0.0;
+    int32_t limA = (na - i > 32) ? __shfl_sync(FULL_MASK, ca, 31) : INT32_MAX;
+    int32_t limB = (nb - j > 32) ? __shfl_sync(FULL_MASK, cb, 31) : INT32_MAX;
+    int32_t lim = limA < limB ? limA : limB;
+    bool oka = ina && ca <= lim, okb = inb && cb <= lim;
+    sA[wi][lane] = ca;
+    sB[wi][lane] = cb;
+    __syncwarp();
+    int posB = lower_bound32(sB[wi], ca);
+    int posA = lower_bound32(sA[wi], cb);
+    bool dupA = oka && posB < 32 && sB[wi][posB] == ca;
+    bool dupB = okb && posA < 32 && sA[wi][posA] == cb;
+    double vbm = __shfl_sync(FULL_MASK, vb, posB & 31);
+    double sum = dupA ? va + vbm : va;
+    bool keepA = oka && sum != 0.0;
+    bool uB = okb && !dupB && vb != 0.0;
+    unsigned bKA = __ballot_sync(FULL_MASK, keepA);
+    unsigned bUB = __ballot_sync(FULL_MASK, uB);
+    if (WRITE) {
+      unsigned mB = posB >= 32 ? FULL_MASK : ((1u << posB) - 1u);
+      unsigned mA = posA >= 32 ? FULL_MASK : ((1u << posA) - 1u);
+      if (keepA) {
+        int64_t q = out + __popc(bKA & lanemask_lt()) + __popc(bUB & mB);
+        col_out[q] = ca;
+        val_out[q] = sum;
+      }
+      if (uB) {
+        int64_t q = out + __popc(bKA & mA) + __popc(bUB & lanemask_lt());
+        col_out[q] = cb;
+        val_out[q] = vb;
+      }
+    }
+    out += __popc(bKA) + __popc(bUB);
+    i += __popc(__ballot_sync(FULL_MASK, oka));
+    j += __popc(__ballot_sync(FULL_MASK, okb));
+    __syncwarp();
+  }
+  if (!WRITE && lane == 0) cnt[w] = out;
+}
+void launch_merge_count(const CsrView &A, const CsrView &B, int64_t *cnt, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_merge<false><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, B, nullptr, cnt,
+                                                                        nullptr, nullptr);
+}
+void launch_merge_write(const CsrView &A, const CsrView &B, const int64_t *rp_out,
+                        int32_t *col_out, double *val_out, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_merge<true><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, B, rp_out, nullptr,
+                                                                       col_out, val_out);
+}
+
+__global__ void k_identity(int64_t nrows, int64_t row0, int64_t *rp, int32_t *col, double *val) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) {
+    rp[i] = i;
+    col[i] = (int32_t)(row0 + i);
+    val[i] = 1.0;
+  }
+  if (i == 0) rp[nrows] = nrows;
+}
+void launch_identity(int64_t nrows, int64_t row0, int64_t *rp, int32_t *col, double *val,
+                     cudaStream_t st) {
+  KL;
+  k_identity<<<grid_for(nrows + 1, kThreads), kThreads, 0, st>>>(nrows, row0, rp, col, val);
+}
+
+__global__ void k_rebase(const int64_t *src, int64_t cnt, int64_t base, int64_t *dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= cnt) dst[i] = src[i] - src[0] + base;
+}
+void launch_rebase_rowptr(const int64_t *src, int64_t cnt, int64_t base, int64_t *dst,
+                          cudaStream_t st) {
+  KL;
+  k_rebase<<<grid_for(cnt + 1, kThreads), kThreads, 0, st>>>(src, cnt, base, dst);
+}
+
+}  // namespace sx

@@ -1,0 +1,128 @@
+// kernels.cuh — internal launchers of the sm_100a kernels of libsexpm.
+// Each launcher enqueues on `st` and never synchronises.  See kernels.cu for the
+// paper passage every kernel implements.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sx {
+
+extern long long g_kernel_launches;  // incremented by every launcher
+
+constexpr int kThreads = 256;                 // row kernels: 8 warps per CTA
+constexpr int kWarps = kThreads / 32;
+
+// Device CSR view over a contiguous block of rows. Row r of the view is global row
+// row0 + r; columns are global.
+struct CsrView {
+  int64_t nrows = 0;
+  int64_t row0 = 0;
+  int64_t nnz = 0;
+  const int64_t *rp = nullptr;
+  const int32_t *col = nullptr;
+  const double *val = nullptr;
+};
+
+// --- K8: norms, validation, transpose-based checks (plan time) --------------------
+void launch_validate(const CsrView &A, int64_t n, int *flags, cudaStream_t st);
+void launch_col_count(const CsrView &A, int32_t *cnt, cudaStream_t st);
+void launch_transpose_fill(const CsrView &A, int64_t *cursor, int32_t *trow, double *tval,
+                           cudaStream_t st);
+void launch_sort_columns(int64_t ncols, const int64_t *cp, int32_t *trow, double *tval,
+                         cudaStream_t st);
+void launch_col_abs_sum(int64_t ncols, const int64_t *cp, const double *tval, double *out,
+                        cudaStream_t st);
+void launch_compare_transpose(const CsrView &A, const int64_t *cp, const int32_t *trow,
+                              const double *tval, int *flags, cudaStream_t st);
+// deterministic reductions into out[0] (fixed grid, fixed order)
+void launch_reduce_max(const double *x, int64_t cnt, double *partial, double *out,
+                       cudaStream_t st);
+void launch_reduce_sumsq(const double *x, int64_t cnt, double *partial, double *out,
+                         cudaStream_t st);
+void launch_reduce_sum(const double *x, int64_t cnt, double *partial, double *out,
+                       cudaStream_t st);
+void launch_reduce_max_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st);
+void launch_reduce_sum_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st);
+void launch_scale_pow2(double *v, int64_t cnt, int e, cudaStream_t st);
+void launch_row_lengths(const int64_t *rp, int64_t nrows, int64_t *out, cudaStream_t st);
+void launch_copy_i64_offset(const int64_t *src, int64_t cnt, int64_t off, int64_t *dst,
+                            cudaStream_t st);
+
+// --- scan ------------------------------------------------------------------------
+// exclusive scan of cnt int64 values into out[0..cnt]; out[cnt] = total.
+// tmp needs scan_tmp_elems(cnt) int64s.
+int64_t scan_tmp_elems(int64_t cnt);
+void launch_exclusive_scan(const int64_t *in, int64_t cnt, int64_t *out, int64_t *tmp,
+                           cudaStream_t st);
+
+// --- K1 symbolic bound -----------------------------------------------------------
+// For each row r of A: lo/hi = min/max column reachable (B rows of A's columns and, if
+// self, A's own row), prod = sum of nnz(B row k) (+ nnz(A row)), bound = min(span, prod).
+void launch_symbolic(const CsrView &A, const CsrView &B, int self, int32_t *lo, int32_t *hi,
+                     int64_t *prod, int64_t *bound, cudaStream_t st);
+
+// --- K2 binning ------------------------------------------------------------------
+// order = row ids sorted by descending work (counting sort on floor(log2(work+1))).
+void launch_bin_rows(int64_t nrows, const int64_t *work, int32_t *bin_cnt, int32_t *bin_off,
+                     int32_t *order, cudaStream_t st);
+
+// --- K3 numeric filtered SpGEMM with fused 2T add + classification ---------------
+struct NumericArgs {
+  CsrView A, B;
+  double self_coef = 0.0;   // 2 for squaring (Eq. 4.15), 0 for Taylor (Eq. 4.11)
+  double divisor = 1.0;     // i for Taylor terms, 1 otherwise
+  double floor_tau = 0.0;   // entries with 0 < |x| <= floor_tau are dropped, x^2 summed
+  const int32_t *lo = nullptr, *hi = nullptr;
+  const int32_t *order = nullptr;
+  int window = 8192;
+  int64_t *cursor = nullptr;      // per-CTA scratch [grid][cursor_cap]
+  int64_t cursor_cap = 0;
+  int32_t *scr_col = nullptr;     // per-CTA staging [grid][scr_cap]
+  double *scr_val = nullptr;
+  int64_t scr_cap = 0;
+  int32_t *pool_col = nullptr;    // global staging pool
+  double *pool_val = nullptr;
+  int64_t pool_cap = 0;
+  unsigned long long *pool_used = nullptr;
+  int64_t *row_off = nullptr;     // per row: offset in pool
+  int64_t *row_cnt = nullptr;     // per row: staged count
+  double *row_fsum = nullptr;     // per row: sum of x^2 below the floor
+  int64_t *row_nnz = nullptr;     // per row: distinct nonzeros of C~
+  int *row_counter = nullptr;     // dynamic scheduler
+  int *flags = nullptr;           // flags[0] |= 1 on pool overflow, 2 on scratch overflow
+  int grid = 0;
+};
+int numeric_smem_bytes(int window);
+void launch_numeric(const NumericArgs &a, cudaStream_t st);
+
+// --- K6 Algorithm 4.1 pass -------------------------------------------------------
+// out[0] = sum over x[0..cnt) of x^2 for |x| <= tau (deterministic order for fixed layout)
+void launch_alg41_pass(const double *x, int64_t cnt, double tau, double *partial,
+                       double *out, cudaStream_t st);
+
+// --- K4 compaction -----------------------------------------------------------------
+void launch_compact_count(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
+                          const double *pool_val, double tau, int64_t *cnt, cudaStream_t st);
+// writes C rows; per-row stats: rs = ||row of (I + C)||^2 (identity on global row),
+// l1r/l2r = max(col - row) / max(row - col) clamped at 0.
+void launch_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
+                          const int64_t *row_cnt, const int32_t *pool_col,
+                          const double *pool_val, double tau, const int64_t *rp_out,
+                          int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
+                          int64_t *l2r, cudaStream_t st);
+// per-row ||row of (I + C)||^2 and bandwidth stats for an existing CSR
+void launch_row_stats(const CsrView &C, double *rs, int64_t *l1r, int64_t *l2r,
+                      cudaStream_t st);
+
+// --- merge C = A + B (exact, zero sums purged): count then write ---------------------
+void launch_merge_count(const CsrView &A, const CsrView &B, int64_t *cnt, cudaStream_t st);
+void launch_merge_write(const CsrView &A, const CsrView &B, const int64_t *rp_out,
+                        int32_t *col_out, double *val_out, cudaStream_t st);
+// identity rows for rows [row0, row0+nrows)
+void launch_identity(int64_t nrows, int64_t row0, int64_t *rp, int32_t *col, double *val,
+                     cudaStream_t st);
+// rowptr fix-up: dst[i] = src[i] - src[0] + base for i in [0, cnt]
+void launch_rebase_rowptr(const int64_t *src, int64_t cnt, int64_t base, int64_t *dst,
+                          cudaStream_t st);
+
+}  // namespace sx

@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same seeded
+inputs (BASELINE.json north-star criteria, see gpu_helpers.parity)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import (csr_to_dense, dense_to_csr, diagonal, laplacian_2d, make_config,
+                   neumann_laplacian_2d, random_banded, random_skew, tridiag)
+
+from gpu_helpers import NTHREADS, from_dev, last_tau, parity, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2110_04493_b200 import binding
+    from paper_2110_04493_b200.build import build
+    build()
+    binding.lib()
+    return binding
+
+
+def run_gpu(B, H, eps_tol=1e-16, **opts):
+    rp, ci, va = to_dev(H)
+    (erp, eci, eva), st = B.expm(H.n, rp, ci, va, eps_tol, **opts)
+    return from_dev(H.n, erp, eci, eva), st
+
+
+def run_both(B, H, eps_tol=1e-16, **opts):
+    Eg, st = run_gpu(B, H, eps_tol, **opts)
+    oo = {k: v for k, v in opts.items() if k != "window_cols"}
+    Eo, tr = O.expm(H, eps_tol, nthreads=NTHREADS, **oo)
+    return Eg, st, Eo, tr
+
+
+def assert_plan_equal(st, tr):
+    assert (st["M"], st["N"]) == (tr["M"], tr["N"])
+    assert st["normal"] == tr["normal"]
+    assert st["norm"] == pytest.approx(tr["norm"], rel=1e-14)
+    assert st["a"] == pytest.approx(tr["a"], rel=1e-15)
+    assert st["eps_g0"] == pytest.approx(tr["eps_g0"], rel=1e-13, abs=0)
+
+
+def assert_parity(Eg, st, Eo, tr):
+    ok, res = parity(Eg, Eo, last_tau(tr, st))
+    assert ok, res
+    return res
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_baseline_configs_one_norm(B, cid):
+    H = make_config(cid)
+    Eg, st, Eo, tr = run_both(B, H)
+    assert_plan_equal(st, tr)
+    assert_parity(Eg, st, Eo, tr)
+    assert st["M_eff"] == tr["M_eff"]
+    for i in range(1, tr["N"] + 1):  # per-squaring pattern sizes agree within flips
+        assert abs(st["sq_nnz"][i] - tr["sq_nnz"][i]) <= 1e-3 * tr["sq_nnz"][i] + 2
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_baseline_configs_fro_norm(B, cid):
+    H = make_config(cid)
+    Eg, st, Eo, tr = run_both(B, H, plan_norm="fro")
+    assert_plan_equal(st, tr)
+    assert_parity(Eg, st, Eo, tr)
+
+
+def test_paper_tables_2_3_on_gpu(B):
+    """Tables 2-3 reproduced by the CUDA path itself."""
+    H = tridiag(10_000, 1.0, -2.0, 1.0)
+    Eg, st = run_gpu(B, H, plan_norm="fro")
+    assert (st["M"], st["N"]) == (20, 8)
+    lam = [int(st["sq_l1"][i] + st["sq_l2"][i]) for i in range(1, 9)]
+    assert lam == [14, 16, 18, 20, 22, 26, 32, 38]
+    assert st["M_eff"] == 9 and st["taylor_nnz"][10] == 0
+
+
+SMALL = {
+    "heat2d_pm10_20": lambda: make_config(2, scale_down=20),
+    "structural_24": lambda: make_config(3, scale_down=24),
+    "heat3d_9": lambda: make_config(4, scale_down=9),
+    "heat2d_uniform_33": lambda: make_config(5, scale_down=33),
+    "neumann_15x13": lambda: neumann_laplacian_2d(15, 13, 0.7, seed=3),
+    "banded_nonsym": lambda: random_banded(150, 5, 0.6, 1.5, seed=21),
+    "banded_sym": lambda: random_banded(170, 4, 0.7, 2.0, seed=22, symmetric=True),
+    "skew": lambda: random_skew(120, 3, 0.7, 1.5, seed=23),
+    "diagonal": lambda: diagonal(np.linspace(-3, 2.5, 37)),
+    "n1": lambda: diagonal([0.75]),
+    "tridiag_ragged_997": lambda: tridiag(997, 0.3, -0.9, 0.6),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+@pytest.mark.parametrize("tol", [1e-16, 1e-10])
+def test_small_cases(B, name, tol):
+    H = SMALL[name]()
+    Eg, st, Eo, tr = run_both(B, H, tol)
+    assert_plan_equal(st, tr)
+    assert_parity(Eg, st, Eo, tr)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_table1_matrices(B, k):
+    import refs
+    A = refs.table1_matrices()[k]
+    H = dense_to_csr(A)
+    Eg, st, Eo, tr = run_both(B, H, plan_norm="fro")
+    assert_plan_equal(st, tr)
+    assert_parity(Eg, st, Eo, tr)
+    Ex = refs.table1_exact(k)
+    assert np.linalg.norm(csr_to_dense(Eg) - Ex) / np.linalg.norm(Ex) < 1e-13
+
+
+@pytest.mark.parametrize("window", [32, 96, 1000])
+def test_window_chunking_and_ragged_tail(B, window):
+    """Force many accumulator chunks (and a ragged last chunk) per row."""
+    H = make_config(2, scale_down=24)
+    Eg, st, Eo, tr = run_both(B, H, window_cols=window)
+    assert_parity(Eg, st, Eo, tr)
+
+
+def test_zero_matrix_gives_identity(B):
+    import scipy.sparse as sps
+    n = 50
+    H = dense_to_csr(np.zeros((n, n)))
+    Eg, st = run_gpu(B, H)
+    assert (st["M"], st["N"]) == (0, 0)
+    assert np.array_equal(csr_to_dense(Eg), np.eye(n))
+
+
+def test_unfiltered_matches_oracle(B):
+    H = random_banded(90, 3, 0.8, 1.0, seed=31)
+    Eg, st, Eo, tr = run_both(B, H, filter=False)
+    assert_parity(Eg, st, Eo, tr)
+    assert all(st["sq_passes"][: st["N"] + 1] == 0)
+
+
+def test_abs_threshold_mode(B):
+    H = make_config(2, scale_down=16)
+    Eg, st, Eo, tr = run_both(B, H, threshold_mode="abs")
+    assert_parity(Eg, st, Eo, tr)
+
+
+def test_output_T(B):
+    H = make_config(1, scale_down=200)
+    Eg, st, Eo, tr = run_both(B, H, output_T=True)
+    assert_parity(Eg, st, Eo, tr)
+
+
+def test_errors(B):
+    import torch
+    H = tridiag(10, 1.0, -2.0, 1.0)
+    rp, ci, va = to_dev(H)
+    bad = va.clone()
+    bad[3] = float("nan")
+    with pytest.raises(B.SexpmError) as e:
+        B.expm(H.n, rp, ci, bad)
+    assert e.value.code == 2
+    with pytest.raises(B.SexpmError) as e:
+        B.expm(H.n, rp, ci, va, 1e-17)
+    assert e.value.code == 3
+    ci2 = ci.clone()
+    ci2[1], ci2[2] = ci[2], ci[1]
+    with pytest.raises(B.SexpmError) as e:
+        B.expm(H.n, rp, ci2, va)
+    assert e.value.code == 1
+
+
+def test_explicit_zeros_ignored(B):
+    H = tridiag(300, 0.4, -0.8, 0.4)
+    Hz = tridiag(300, 0.4, -0.8, 0.4)
+    Hz.val[::7] = 0.0  # explicit zeros in the input are ignored by the library
+    Hc = dense_to_csr(csr_to_dense(Hz))
+    rp, ci, va = to_dev(Hz)
+    (a, b, c), st = B.expm(Hz.n, rp, ci, va)
+    Eo, tr = O.expm(Hc, 1e-16)
+    ok, res = parity(from_dev(Hz.n, a, b, c), Eo, last_tau(tr, st))
+    assert ok, res
+
+
+def test_host_entry_point_matches_device(B):
+    H = make_config(2, scale_down=30)
+    (hrp, hci, hva), st_h = B.expm_host(H.n, H.rowptr, H.col, H.val)
+    Eg, st = run_gpu(B, H)
+    Eh = type(Eg)(H.n, hrp, hci, hva)
+    ok, res = parity(Eh, Eg, last_tau({"N": st["N"], "M": st["M"], "M_eff": st["M_eff"],
+                                         "sq_tau": st["sq_tau"], "taylor_tau": st["taylor_tau"]}))
+    assert ok, res
+
+
+# ---------------------------- component entry points ----------------------------------
+
+def _rand_csr(n, bw, dens, seed, empty_rows=()):
+    A = csr_to_dense(random_banded(n, bw, dens, 1.0, seed))
+    for r in empty_rows:
+        A[r, :] = 0
+    return dense_to_csr(A)
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("self_coef,divisor", [(2.0, 1.0), (0.0, 3.0), (0.0, 1.0)])
+def test_filtered_product_vs_oracle(B, seed, self_coef, divisor):
+    n = 257
+    A = _rand_csr(n, 6, 0.5, 100 + seed, empty_rows=(0, 5, 128, 256))
+    Bm = A if self_coef else _rand_csr(n, 3, 0.6, 200 + seed, empty_rows=(7,))
+    eps_g = [0.0, 1e-4, 1e-2, 0.3, 2.0, 10.0][seed]
+    (rp, ci, va), passes, tau, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(Bm),
+                                                                  self_coef, divisor, eps_g)
+    Ct = O.spgemm(A, Bm, self_coef, divisor)
+    keep, tau_o, passes_o, _, _ = O.alg41(Ct.val, eps_g, 0.1)
+    assert nnz_unf == Ct.nnz
+    assert passes == passes_o
+    if np.isfinite(tau_o):
+        assert tau == pytest.approx(tau_o, rel=1e-12)
+    G = csr_to_dense(from_dev(n, rp, ci, va))
+    Cd = csr_to_dense(Ct)
+    rows = np.repeat(np.arange(n), np.diff(Ct.rowptr))
+    ref = np.zeros((n, n))
+    ref[rows[keep], Ct.col[keep]] = Ct.val[keep]
+    # kept sets equal except entries within rounding of tau
+    diff = np.abs(G - ref)
+    assert diff.max() <= 1e-13 * max(np.abs(Cd).max(), 1e-300) + 10 * (tau if np.isfinite(tau) else 0)
+
+
+HAND = [
+    ([1.0] * 4 + [1e-3] * 100, 5e-3, 0.01, 4, 6.25e-4),
+    ([1.0, 1e-20], 1e-10, 0.1, 1, 1e-10),
+    ([1.0] * 4, 1e-12, 0.1, 1, 1e-12),
+    ([1.0] + [1e-4] * 16, 1e-3, 0.1, 1, 1e-3),
+    ([1.0] * 2 + [4e-4] * 25 + [1e-4] * 100, 1e-3, 0.1, 3, 2e-4),
+    ([5.0, 0.5], 1.0, 0.1, 0, float("inf")),
+]
+
+
+@pytest.mark.parametrize("case", range(len(HAND)))
+def test_alg41_hand_traces_gpu(B, case):
+    import torch
+    vals, eps_g, e_r, passes, tau = HAND[case]
+    x = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    p, t, d = B.sexpm_alg41(x, eps_g, e_r)
+    assert p == passes
+    assert t == pytest.approx(tau, rel=1e-14)
+
+
+def test_alg41_random_vs_oracle(B):
+    import torch
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        n = int(rng.integers(1, 5000))
+        x = 10.0 ** rng.uniform(-22, 0, n) * rng.choice([-1.0, 1.0], n)
+        eps_g = 10.0 ** rng.uniform(-20, -2)
+        keep, tau_o, passes_o, dropped_o, _ = O.alg41(x, eps_g, 0.1)
+        p, t, d = B.sexpm_alg41(torch.from_numpy(x).cuda(), eps_g, 0.1)
+        assert p == passes_o
+        assert t == pytest.approx(tau_o, rel=1e-12)
+        assert d == pytest.approx(dropped_o, rel=1e-10, abs=1e-300)
