@@ -121,8 +121,10 @@ struct DBuf {
     CK(cudaMallocAsync(reinterpret_cast<void **>(&p), cnt * sizeof(T), s));
     n = cnt;
   }
+  // grow-only: reuse the buffer when it is large enough, else grow by 1.25x (fewer
+  // stream-ordered re-allocations as the iterates fill in)
   void ensure(size_t cnt, cudaStream_t s) {
-    if (cnt > n || !p) alloc(std::max<size_t>(cnt, 1), s);
+    if (cnt > n || !p) alloc(std::max<size_t>(cnt + cnt / 4, 1), s);
   }
   DBuf() = default;
   DBuf(const DBuf &) = delete;
@@ -182,6 +184,7 @@ struct StepReport {
   double fmas = 0.0;
   float numeric_ms = 0.f;
   double numeric_bytes = 0.0;
+  int64_t window_rows = 0;
 };
 
 struct Workspace {
@@ -192,7 +195,8 @@ struct Workspace {
   DBuf<int32_t> scr_col, pool_col;
   DBuf<double> scr_val, pool_val;
   DBuf<unsigned long long> pool_used;
-  DBuf<int> row_counter, flags;
+  DBuf<int> row_counter, flags, fail_count;
+  DBuf<int32_t> fail_rows;
   int64_t pool_cap_hint = 0;
 };
 
@@ -207,7 +211,10 @@ struct sexpm_plan_s {
   std::vector<int64_t> bounds;  // world + 1 row bounds
   double eps_tol = 0.0;
   DCsr H0full;  // H0 = H 2^-N, all n rows (replicated)
-  DCsr T, E;
+  DCsr H0loc;   // this rank's rows of H0
+  DCsr T, Tn, S, Sn, Bhalo, Ibuf, E;  // persistent (grow-only) iterates
+  int32_t retries = 0;
+  DBuf<int32_t> proc_order;  // K3 row processing order (cluster order of H's graph)
   bool have_result = false;
   int M = 0, N = 0, normal = 0, M_eff = 0;
   double norm = 0.0, a = 0.0, eps_g0 = 0.0;
@@ -216,6 +223,10 @@ struct sexpm_plan_s {
   sexpm_stats stats{};
   int sm_count = 148;
   int numeric_blocks_per_sm = 2;
+  int hash_blocks_per_sm = 4;
+  int warp_blocks_per_sm = 4;
+  int paged_blocks_per_sm = 3;
+  int warp_window = 1024;
   float plan_ms = 0.f;
 };
 
@@ -311,8 +322,11 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   rep.fmas = (double)hstat[2];
   const double floor_tau = (eps_g > 0.0 && Kglob > 0.0) ? eps_g / sqrt(Kglob) : 0.0;
 
-  // K2 binning (longest rows first)
-  launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
+  // K2 scheduling order: the plan's locality (cluster) order when it covers these rows,
+  // else longest-processing-time-first bins
+  const bool use_cluster = P.proc_order.p && (int64_t)P.proc_order.n >= nr && A.row0 == P.row_begin &&
+                           nr == P.row_end - P.row_begin;
+  if (!use_cluster) launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
 
   // K3 numeric
   NumericArgs na;
@@ -323,14 +337,11 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   na.floor_tau = floor_tau;
   na.lo = w.lo.p;
   na.hi = w.hi.p;
-  na.order = w.order.p;
+  na.order = use_cluster ? P.proc_order.p : w.order.p;
   na.window = P.o.window_cols > 0 ? P.o.window_cols : 8192;
   na.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.numeric_blocks_per_sm));
   na.cursor_cap = std::max<int64_t>(maxk, 1);
   na.scr_cap = std::max<int64_t>(maxb, 1);
-  w.cursor.ensure((size_t)na.grid * na.cursor_cap, st);
-  w.scr_col.ensure((size_t)na.grid * na.scr_cap, st);
-  w.scr_val.ensure((size_t)na.grid * na.scr_cap, st);
   int64_t cap = std::max<int64_t>(w.pool_cap_hint, (self != 0.0 ? 3 : 2) * A.nnz + 2 * nr + 1024);
   double sum_bound = 0;  // exact upper bound
   sum_bound = (double)hstat[0];
@@ -339,15 +350,18 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   unsigned long long used = 0;
+  w.fail_rows.ensure(nr1, st);
+  w.fail_count.ensure(1, st);
+  const int hash_grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.hash_blocks_per_sm));
+  const int paged_grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged_blocks_per_sm));
   for (int attempt = 0;; attempt++) {
     w.pool_col.ensure((size_t)cap, st);
     w.pool_val.ensure((size_t)cap, st);
     na.pool_col = w.pool_col.p;
     na.pool_val = w.pool_val.p;
     na.pool_cap = (int64_t)w.pool_col.n;
-    na.cursor = w.cursor.p;
-    na.scr_col = w.scr_col.p;
-    na.scr_val = w.scr_val.p;
     na.pool_used = w.pool_used.p;
     na.row_off = w.row_off.p;
     na.row_cnt = w.row_cnt.p;
@@ -358,9 +372,57 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     CK(cudaMemsetAsync(w.pool_used.p, 0, sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
     CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(w.fail_count.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
-    launch_numeric(na, st);
-    CK(cudaGetLastError());
+    int kern = P.o.kernel;
+    if (kern == 0) kern = self != 0.0 ? 5 : 1;
+    int nfail = 0;
+    if (kern == 2) {  // warp-per-row conflict-free window
+      const int64_t gw = (int64_t)P.sm_count * P.warp_blocks_per_sm * kWarpRowWarpsPerCta;
+      const int64_t grid_w = std::max<int64_t>(1, std::min<int64_t>((nr + kWarpRowWarpsPerCta - 1) / kWarpRowWarpsPerCta,
+                                                                    gw / kWarpRowWarpsPerCta));
+      const int64_t nwarps = grid_w * kWarpRowWarpsPerCta;
+      w.cursor.ensure((size_t)nwarps * 2 * na.cursor_cap, st);
+      w.scr_col.ensure((size_t)nwarps * na.scr_cap, st);
+      w.scr_val.ensure((size_t)nwarps * na.scr_cap, st);
+      NumericArgs nw = na;
+      nw.window = P.warp_window;
+      nw.cursor = w.cursor.p;
+      nw.scr_col = w.scr_col.p;
+      nw.scr_val = w.scr_val.p;
+      nw.nlist = nr;
+      nw.grid = (int)grid_w;
+      launch_numeric_warp(nw, st);
+      CK(cudaGetLastError());
+    } else {
+      if (kern == 1 || kern == 4 || kern == 5) {  // shared-memory accumulator over all rows
+        NumericArgs nh = na;
+        nh.grid = kern == 5 ? paged_grid : hash_grid;
+        nh.nlist = nr;
+        if (kern == 1) launch_numeric_hash(nh, w.fail_rows.p, w.fail_count.p, st);
+        else if (kern == 4) launch_numeric_ksync(nh, w.fail_rows.p, w.fail_count.p, st);
+        else launch_numeric_paged(nh, w.fail_rows.p, w.fail_count.p, st);
+        CK(cudaGetLastError());
+        nfail = d2h(w.fail_count.p, st);
+      }
+      const bool all_window = kern == 3;
+      if (nfail > 0 || all_window) {  // block-window kernel (hash overflow rows, or all)
+        w.cursor.ensure((size_t)na.grid * na.cursor_cap, st);
+        w.scr_col.ensure((size_t)na.grid * na.scr_cap, st);
+        w.scr_val.ensure((size_t)na.grid * na.scr_cap, st);
+        NumericArgs nw = na;
+        nw.cursor = w.cursor.p;
+        nw.scr_col = w.scr_col.p;
+        nw.scr_val = w.scr_val.p;
+        nw.order = all_window ? na.order : w.fail_rows.p;
+        nw.nlist = all_window ? nr : nfail;
+        nw.grid = (int)std::min<int64_t>(na.grid, nw.nlist);
+        CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
+        launch_numeric(nw, st);
+        CK(cudaGetLastError());
+      }
+    }
+    rep.window_rows = nfail;
     CK(cudaEventRecord(e1, st));
     int flags = 0;
     CK(cudaMemcpyAsync(&flags, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -370,7 +432,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     if (!(flags & 1)) break;
     REQUIRE(attempt < 8, SEXPM_EINTERNAL, "numeric: staging pool keeps overflowing");
     cap = std::max<int64_t>(2 * cap, (int64_t)(1.25 * (double)used) + 1024);
-    P.stats.retries++;
+    P.retries++;
   }
   CK(cudaEventElapsedTime(&rep.numeric_ms, e0, e1));
   cudaEventDestroy(e0);
@@ -419,14 +481,14 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
 
   // K4 compaction + fused row statistics
   launch_compact_count(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau, w.cnt.p, st);
-  DCsr out;
+  DCsr &out = C;  // must not alias A or B
   out.nrows = nr;
   out.row0 = A.row0;
-  out.rp.alloc((size_t)nr + 1, st);
+  out.rp.ensure((size_t)nr + 1, st);
   launch_exclusive_scan(w.cnt.p, nr, out.rp.p, w.scan_tmp.p, st);
   out.nnz = d2h(out.rp.p + nr, st);
-  out.col.alloc((size_t)out.nnz, st);
-  out.val.alloc((size_t)out.nnz, st);
+  out.col.ensure((size_t)out.nnz, st);
+  out.val.ensure((size_t)out.nnz, st);
   launch_compact_write(nr, A.row0, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
                        out.rp.p, out.col.p, out.val.p, w.rs.p, w.l1r.p, w.l2r.p, st);
   launch_reduce_sum(w.rs.p, nr, w.partial.p, w.scal.p + 2, st);
@@ -436,7 +498,6 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   rep.l1 = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 4, st));
   rep.l2 = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 5, st));
   rep.nnz = (int64_t)allsum(P, (double)out.nnz);
-  C = std::move(out);
 }
 
 // C = A + B (same rows)
@@ -447,16 +508,15 @@ static void merge_add(sexpm_plan_s &P, const CsrView &A, const CsrView &B, DCsr 
   w.cnt.ensure((size_t)std::max<int64_t>(nr, 1), st);
   w.scan_tmp.ensure((size_t)scan_tmp_elems(nr) + 1, st);
   launch_merge_count(A, B, w.cnt.p, st);
-  DCsr out;
+  DCsr &out = C;  // must not alias A or B
   out.nrows = nr;
   out.row0 = A.row0;
-  out.rp.alloc((size_t)nr + 1, st);
+  out.rp.ensure((size_t)nr + 1, st);
   launch_exclusive_scan(w.cnt.p, nr, out.rp.p, w.scan_tmp.p, st);
   out.nnz = d2h(out.rp.p + nr, st);
-  out.col.alloc((size_t)out.nnz, st);
-  out.val.alloc((size_t)out.nnz, st);
+  out.col.ensure((size_t)out.nnz, st);
+  out.val.ensure((size_t)out.nnz, st);
   launch_merge_write(A, B, out.rp.p, out.col.p, out.val.p, st);
-  C = std::move(out);
 }
 
 static void copy_csr(sexpm_plan_s &P, const CsrView &A, DCsr &C) {
@@ -464,9 +524,9 @@ static void copy_csr(sexpm_plan_s &P, const CsrView &A, DCsr &C) {
   C.nrows = A.nrows;
   C.row0 = A.row0;
   C.nnz = A.nnz;
-  C.rp.alloc((size_t)A.nrows + 1, st);
-  C.col.alloc((size_t)A.nnz, st);
-  C.val.alloc((size_t)A.nnz, st);
+  C.rp.ensure((size_t)A.nrows + 1, st);
+  C.col.ensure((size_t)A.nnz, st);
+  C.val.ensure((size_t)A.nnz, st);
   CK(cudaMemcpyAsync(C.rp.p, A.rp, ((size_t)A.nrows + 1) * sizeof(int64_t),
                      cudaMemcpyDeviceToDevice, st));
   if (A.nnz) {
@@ -641,6 +701,59 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
     if (piece_rows[h])
       launch_rebase_rowptr(rp_tmp.p + tmp_at[h], piece_rows[h], nnz_at[h], B.rp.p + row_at[h], st);
   CK(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------------------------------------
+// processing order with L2 locality (plan time, host): rows are visited cluster by
+// cluster, each cluster a BFS ball of ~kCluster rows of H's graph, clusters taken in a
+// global BFS sweep.  The dynamic row scheduler of K3 hands consecutive rows of this
+// order to the CTAs in flight, so the B rows they gather (the ball dilated by the
+// bandwidth of T^, Lemma 3.1) stay L2-resident (126 MB) instead of the whole band of
+// lexicographically consecutive rows (~2R grid lines for a 2D stencil).
+// ------------------------------------------------------------------------------------
+static void cluster_order(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
+                          int64_t r0, int64_t r1, int cluster, std::vector<int32_t> &order) {
+  const int64_t nl = r1 - r0;
+  order.clear();
+  order.reserve((size_t)nl);
+  std::vector<int32_t> gorder;
+  gorder.reserve((size_t)nl);
+  std::vector<uint8_t> seen((size_t)nl, 0), assigned((size_t)nl, 0);
+  for (int64_t s = 0; s < nl; s++) {
+    if (seen[s]) continue;
+    size_t head = gorder.size();
+    gorder.push_back((int32_t)s);
+    seen[s] = 1;
+    while (head < gorder.size()) {
+      int64_t v = gorder[head++];
+      for (int64_t p = rp[v + r0]; p < rp[v + r0 + 1]; p++) {
+        int64_t u = (int64_t)col[p] - r0;
+        if (u >= 0 && u < nl && !seen[u]) {
+          seen[u] = 1;
+          gorder.push_back((int32_t)u);
+        }
+      }
+    }
+  }
+  std::vector<int32_t> q;
+  for (int32_t s : gorder) {
+    if (assigned[s]) continue;
+    q.clear();
+    q.push_back(s);
+    assigned[s] = 1;
+    size_t head = 0;
+    while (head < q.size() && (int)q.size() < cluster) {
+      int64_t v = q[head++];
+      for (int64_t p = rp[v + r0]; p < rp[v + r0 + 1] && (int)q.size() < cluster; p++) {
+        int64_t u = (int64_t)col[p] - r0;
+        if (u >= 0 && u < nl && !assigned[u]) {
+          assigned[u] = 1;
+          q.push_back((int32_t)u);
+        }
+      }
+    }
+    order.insert(order.end(), q.begin(), q.end());
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -834,6 +947,21 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   if (!P.o.filter) P.eps_g0 = 0.0;
   // H0 = H 2^-N (exact)
   launch_scale_pow2(Hf.val.p, Hf.nnz, -N, st);
+  slice_rows(P, Hf, P.row_begin, P.row_end, P.H0loc);
+  {
+    std::vector<int64_t> hrp((size_t)P.n + 1);
+    std::vector<int32_t> hcol((size_t)std::max<int64_t>(Hf.nnz, 1));
+    CK(cudaMemcpyAsync(hrp.data(), Hf.rp.p, hrp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (Hf.nnz)
+      CK(cudaMemcpyAsync(hcol.data(), Hf.col.p, Hf.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int32_t> ord;
+    cluster_order(hrp, hcol, P.row_begin, P.row_end, 1024, ord);
+    P.proc_order.ensure(std::max<size_t>(ord.size(), 1), st);
+    if (!ord.empty())
+      CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
   CK(cudaEventRecord(e1, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaEventElapsedTime(&P.plan_ms, e0, e1));
@@ -844,6 +972,12 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
 // ------------------------------------------------------------------------------------
 // run: Taylor phase, squarings, finish
 // ------------------------------------------------------------------------------------
+static void swap_csr(DCsr &a, DCsr &b) {
+  DCsr t = std::move(a);
+  a = std::move(b);
+  b = std::move(t);
+}
+
 static void do_run(sexpm_plan_s &P) {
   cudaStream_t st = P.st;
   sexpm_stats &S = P.stats;
@@ -860,38 +994,41 @@ static void do_run(sexpm_plan_s &P) {
   S.r0 = (double)P.r0;
   S.eps_g0 = P.eps_g0;
   S.ms_plan = P.plan_ms;
-  cudaEvent_t ev_start, ev_taylor, ev_sq, ev_end;
+  cudaEvent_t ev_start, ev_taylor, ev_sq, ev_end, a0, a1;
   CK(cudaEventCreate(&ev_start));
   CK(cudaEventCreate(&ev_taylor));
   CK(cudaEventCreate(&ev_sq));
   CK(cudaEventCreate(&ev_end));
+  CK(cudaEventCreate(&a0));
+  CK(cudaEventCreate(&a1));
+  auto step_ms = [&]() {
+    CK(cudaEventRecord(a1, st));
+    CK(cudaEventSynchronize(a1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a0, a1));
+    return (double)ms;
+  };
   CK(cudaEventRecord(ev_start, st));
   const int64_t nl = P.row_end - P.row_begin;
-  DCsr H0loc;
-  slice_rows(P, P.H0full, P.row_begin, P.row_end, H0loc);
+  DCsr &H0loc = P.H0loc;
+  DCsr &T = P.T, &Tn = P.Tn, &Sc = P.S, &Sn = P.Sn;
   // ---- Taylor phase ----
-  DCsr T;
   int M_eff = 0;
   if (P.M == 0) {  // reading R9: T^_0 = 0
     T.nrows = nl;
     T.row0 = P.row_begin;
     T.nnz = 0;
-    T.rp.alloc((size_t)nl + 1, st);
+    T.rp.ensure((size_t)nl + 1, st);
     CK(cudaMemsetAsync(T.rp.p, 0, (nl + 1) * sizeof(int64_t), st));
-    T.col.alloc(1, st);
-    T.val.alloc(1, st);
+    T.col.ensure(1, st);
+    T.val.ensure(1, st);
   } else {
     copy_csr(P, H0loc.view(), T);  // T^_0^(1) = S_1 = H0
-    DCsr Sc;
     copy_csr(P, H0loc.view(), Sc);
     M_eff = 1;
     for (int i = 2; i <= P.M; i++) {
-      cudaEvent_t a0, a1;
-      CK(cudaEventCreate(&a0));
-      CK(cudaEventCreate(&a1));
       CK(cudaEventRecord(a0, st));
       StepReport rep;
-      DCsr Sn;
       filtered_product(P, Sc.view(), P.H0full.view(), 0.0, (double)i, P.eps_g0, Sn, rep);
       if (i < SEXPM_MAXSTEP) {
         S.taylor_nnz_unf[i] = rep.nnz_unf;
@@ -905,28 +1042,15 @@ static void do_run(sexpm_plan_s &P) {
       S.taylor_fmas += rep.fmas;
       S.taylor_bytes += 12.0 * (double)Sc.nnz + 12.0 * (double)Sn.nnz + 16.0 * (double)nl;
       if (rep.nnz == 0) {  // S^_i = 0: all later terms vanish
-        CK(cudaEventRecord(a1, st));
-        CK(cudaStreamSynchronize(st));
-        float ms;
-        CK(cudaEventElapsedTime(&ms, a0, a1));
-        if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = ms;
-        cudaEventDestroy(a0);
-        cudaEventDestroy(a1);
+        if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();
         break;
       }
       M_eff = i;
-      DCsr Tn;
       merge_add(P, T.view(), Sn.view(), Tn);  // T^_0^(i) = T^_0^(i-1) + S^_i
       S.taylor_bytes += 12.0 * ((double)T.nnz + (double)Sn.nnz + (double)Tn.nnz);
-      T = std::move(Tn);
-      Sc = std::move(Sn);
-      CK(cudaEventRecord(a1, st));
-      CK(cudaStreamSynchronize(st));
-      float ms;
-      CK(cudaEventElapsedTime(&ms, a0, a1));
-      if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = ms;
-      cudaEventDestroy(a0);
-      cudaEventDestroy(a1);
+      swap_csr(T, Tn);
+      swap_csr(Sc, Sn);
+      if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();
     }
   }
   P.M_eff = M_eff;
@@ -955,29 +1079,19 @@ static void do_run(sexpm_plan_s &P) {
   double normIT = S.sq_normIT[0];
   int64_t l1 = S.sq_l1[0], l2 = S.sq_l2[0];
   for (int i = 1; i <= P.N; i++) {
-    cudaEvent_t a0, a1;
-    CK(cudaEventCreate(&a0));
-    CK(cudaEventCreate(&a1));
     CK(cudaEventRecord(a0, st));
     ri = 2.0L * ri;  // r_i = 2 r_{i-1}
     double eps_g = P.o.threshold_mode == 1 ? (double)((long double)P.a * ri)
                                            : (double)((long double)P.a * ri * (long double)normIT);
     if (!P.o.filter) eps_g = 0.0;
     StepReport rep;
-    DCsr Tn;
     if (P.world == 1) {
       filtered_product(P, T.view(), T.view(), 2.0, 1.0, eps_g, Tn, rep);
     } else {
-      DCsr B;
-      exchange_halo(P, T, l1, l2, B);
-      filtered_product(P, T.view(), B.view(), 2.0, 1.0, eps_g, Tn, rep);
+      exchange_halo(P, T, l1, l2, P.Bhalo);
+      filtered_product(P, T.view(), P.Bhalo.view(), 2.0, 1.0, eps_g, Tn, rep);
     }
-    CK(cudaEventRecord(a1, st));
-    CK(cudaStreamSynchronize(st));
-    float ms;
-    CK(cudaEventElapsedTime(&ms, a0, a1));
-    cudaEventDestroy(a0);
-    cudaEventDestroy(a1);
+    const double ms = step_ms();
     if (i < SEXPM_MAXSTEP) {
       S.sq_nnz_unf[i] = rep.nnz_unf;
       S.sq_nnz[i] = rep.nnz;
@@ -997,24 +1111,22 @@ static void do_run(sexpm_plan_s &P) {
     normIT = sqrt(rep.normIT2);
     l1 = rep.l1;
     l2 = rep.l2;
-    T = std::move(Tn);
+    swap_csr(T, Tn);
   }
   CK(cudaEventRecord(ev_sq, st));
   // ---- e^H = I + T^_N ----
   if (P.o.output_T) {
-    P.E = std::move(T);
+    copy_csr(P, T.view(), P.E);
   } else {
-    DCsr I;
+    DCsr &I = P.Ibuf;
     I.nrows = nl;
     I.row0 = P.row_begin;
     I.nnz = nl;
-    I.rp.alloc((size_t)nl + 1, st);
-    I.col.alloc((size_t)nl, st);
-    I.val.alloc((size_t)nl, st);
+    I.rp.ensure((size_t)nl + 1, st);
+    I.col.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    I.val.ensure((size_t)std::max<int64_t>(nl, 1), st);
     launch_identity(nl, P.row_begin, I.rp.p, I.col.p, I.val.p, st);
-    DCsr E;
-    merge_add(P, T.view(), I.view(), E);
-    P.E = std::move(E);
+    merge_add(P, T.view(), I.view(), P.E);
   }
   CK(cudaEventRecord(ev_end, st));
   CK(cudaStreamSynchronize(st));
@@ -1029,10 +1141,9 @@ static void do_run(sexpm_plan_s &P) {
   S.ms_total = t4;
   S.nnz_out = P.E.nnz;
   S.gpu_launches = (int32_t)(g_kernel_launches - launches0);
-  cudaEventDestroy(ev_start);
-  cudaEventDestroy(ev_taylor);
-  cudaEventDestroy(ev_sq);
-  cudaEventDestroy(ev_end);
+  S.retries = P.retries;
+  P.retries = 0;
+  for (cudaEvent_t e : {ev_start, ev_taylor, ev_sq, ev_end, a0, a1}) cudaEventDestroy(e);
   P.have_result = true;
 }
 
@@ -1089,6 +1200,7 @@ int sexpm_options_init(sexpm_options *o) {
   o->force_N = -1;
   o->output_T = 0;
   o->window_cols = 0;
+  o->kernel = 0;
   o->e_r = 0.1;
   o->stream = nullptr;
   o->nccl_comm = nullptr;
@@ -1138,6 +1250,10 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
   int smem = numeric_smem_bytes(window);
   REQUIRE(smem <= (int)prop.sharedMemPerBlockOptin - 2048, SEXPM_EINVAL, "window too large");
   P->numeric_blocks_per_sm = std::max(1, std::min(4, (int)(prop.sharedMemPerMultiprocessor / (smem + 4096))));
+  P->hash_blocks_per_sm = std::max(1, std::min(8, (int)(prop.sharedMemPerMultiprocessor / (hash_smem_bytes() + 2048))));
+  P->paged_blocks_per_sm = std::max(1, std::min(8, (int)(prop.sharedMemPerMultiprocessor / (paged_smem_bytes() + 8192))));
+  P->warp_blocks_per_sm = std::max(1, std::min(16, (int)(prop.sharedMemPerMultiprocessor /
+                                                         (warp_numeric_smem_bytes(P->warp_window) + 1024))));
   if (P->o.stream) {
     P->st = (cudaStream_t)P->o.stream;
   } else {

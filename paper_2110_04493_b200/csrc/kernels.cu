@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kThreads) k_numeric(NumericArgs a) {
     if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
     __syncthreads();
     const int idx = s_row;
-    if (idx >= a.A.nrows) break;
+    if (idx >= a.nlist) break;
     const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
     const int32_t lo = a.lo[r], hi = a.hi[r];
     const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
@@ -714,11 +714,1100 @@ __global__ void __launch_bounds__(kThreads) k_numeric(NumericArgs a) {
 }
 
 void launch_numeric(const NumericArgs &a, cudaStream_t st) {
-  if (a.A.nrows == 0) return;
+  if (a.A.nrows == 0 || a.nlist == 0) return;
   int smem = numeric_smem_bytes(a.window);
   cudaFuncSetAttribute(k_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
   k_numeric<<<a.grid, kThreads, smem, st>>>(a);
+}
+
+// ------------------------------------------------------------------------------------
+// K3h numeric filtered SpGEMM with a shared-memory hash accumulator (one CTA per row).
+//
+// Same contract as k_numeric (the 2T term first, products a_rk * b_kj accumulated, then
+// the fused Algorithm 4.1 classification at the flush), but the accumulator is an
+// open-addressing table of kHashCap (column, value) slots keyed by a multiplicative hash,
+// so the cost no longer depends on the row's column span (a 2D stencil's rows span
+// ~2R*sqrt(n) columns for only ~2R^2 distinct ones).  At the flush the entries above the
+// floor are compacted, bitonic-sorted by column in shared memory (canonical CSR rows) and
+// appended to the staging pool.  A row whose table passes kHashMaxFill entries is handed
+// to the window kernel (fail list); nothing is lost.
+// ------------------------------------------------------------------------------------
+constexpr int kHashCap = 4096;
+constexpr int kHashMaxFill = 3072;
+constexpr int kHashPerThread = kHashCap / kThreads;
+constexpr int32_t kEmpty = -1;
+
+int hash_smem_bytes() { return kHashCap * (int)(sizeof(double) + sizeof(int32_t)); }
+
+__device__ __forceinline__ unsigned hslot(int32_t c) {
+  return ((unsigned)c * 2654435761u) >> (32 - 12);  // log2(kHashCap) = 12
+}
+
+// find or insert column c; returns the slot or -1 when the table is over-full
+__device__ __forceinline__ int hash_slot(volatile int32_t *keys, int32_t c, int *count) {
+  unsigned h = hslot(c);
+#pragma unroll 1
+  for (int probe = 0; probe < kHashCap; probe++) {
+    int32_t k = keys[h];
+    if (k == c) return (int)h;
+    if (k == kEmpty) {
+      int32_t old = atomicCAS((int32_t *)&keys[h], kEmpty, c);
+      if (old == kEmpty) {
+        int n = atomicAdd(count, 1);
+        return n < kHashMaxFill ? (int)h : -1;
+      }
+      if (old == c) return (int)h;
+    }
+    h = (h + 1) & (kHashCap - 1);
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kThreads) k_numeric_hash(NumericArgs a, int32_t *fail_rows,
+                                                           int *fail_count) {
+  extern __shared__ double hsm[];
+  double *vals = hsm;
+  int32_t *keys = reinterpret_cast<int32_t *>(hsm + kHashCap);
+  __shared__ int s_row;
+  __shared__ int s_count;
+  __shared__ int s_fail;
+  __shared__ unsigned long long s_off;
+  __shared__ long long s_base[kWarps + 1];
+  __shared__ double s_fs[kWarps];
+  __shared__ long long s_nz[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kHashCap; i += kThreads) {
+    keys[i] = kEmpty;
+    vals[i] = 0.0;
+  }
+  if (tid == 0) {
+    s_count = 0;
+    s_fail = 0;
+  }
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int idx = s_row;
+    if (idx >= a.nlist) break;
+    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
+    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
+    const int64_t nk = pa1 - pa0;
+    if (a.hi[r] < a.lo[r]) {
+      if (tid == 0) {
+        a.row_off[r] = 0;
+        a.row_cnt[r] = 0;
+        a.row_fsum[r] = 0.0;
+        a.row_nnz[r] = 0;
+      }
+      continue;
+    }
+    if (nk > kHashMaxFill) {  // C~ row has at least ~nk columns: straight to the window kernel
+      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+      continue;
+    }
+    // 2T term (Eq. 2.7): distinct columns, one writer per slot
+    if (a.self_coef != 0.0) {
+      for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
+        int h = hash_slot(keys, a.A.col[p], &s_count);
+        if (h >= 0) vals[h] = a.self_coef * a.A.val[p];
+        else s_fail = 1;
+      }
+      __syncthreads();
+    }
+    // products: each warp takes 32 consecutive k's (lane l loads k_l).  Long B rows: the
+    // warp walks them one k at a time, lanes over the entries.  Short B rows (a Taylor
+    // term's H0 rows have ~5 entries): the batch's products are flattened so all 32
+    // lanes work (segment found by a 5-step shuffle search over the exclusive scan).
+    for (int64_t q0 = (int64_t)warp * 32; q0 < nk; q0 += (int64_t)kWarps * 32) {
+      const int64_t q = q0 + lane;
+      long long b0 = 0;
+      int len = 0;
+      double av = 0.0;
+      if (q < nk) {
+        const int64_t k = (int64_t)a.A.col[pa0 + q] - a.B.row0;
+        if (k >= 0 && k < a.B.nrows) {
+          b0 = a.B.rp[k];
+          len = (int)(a.B.rp[k + 1] - b0);
+          av = a.A.val[pa0 + q];
+        }
+      }
+      int inc = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL_MASK, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int total = __shfl_sync(FULL_MASK, inc, 31);
+      const int excl = inc - len;
+      if (total > 32 * 24) {
+        for (int j = 0; j < 32; j++) {
+          const long long kb0 = __shfl_sync(FULL_MASK, b0, j);
+          const int klen = __shfl_sync(FULL_MASK, len, j);
+          const double kav = __shfl_sync(FULL_MASK, av, j);
+          for (int t = lane; t < klen; t += 32) {
+            const int32_t c = a.B.col[kb0 + t];
+            const double prod = kav * a.B.val[kb0 + t];
+            int h = hash_slot(keys, c, &s_count);
+            if (h >= 0) atomicAdd(&vals[h], prod);
+            else s_fail = 1;
+          }
+          if (*(volatile int *)&s_fail) break;
+        }
+      } else {
+        for (int base = 0; base < total; base += 32) {
+          const int t = base + lane;
+          int seg = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            int e = __shfl_sync(FULL_MASK, excl, seg + step);
+            if (e <= t) seg += step;
+          }
+          const long long sb0 = __shfl_sync(FULL_MASK, b0, seg);
+          const int sex = __shfl_sync(FULL_MASK, excl, seg);
+          const double sav = __shfl_sync(FULL_MASK, av, seg);
+          if (t < total) {
+            const long long p = sb0 + (t - sex);
+            const int32_t c = a.B.col[p];
+            const double prod = sav * a.B.val[p];
+            int h = hash_slot(keys, c, &s_count);
+            if (h >= 0) atomicAdd(&vals[h], prod);
+            else s_fail = 1;
+          }
+        }
+      }
+      if (*(volatile int *)&s_fail) break;
+    }
+    __syncthreads();
+    if (s_fail) {  // hand the row to the window kernel
+      if (tid == 0) {
+        int f = atomicAdd(fail_count, 1);
+        fail_rows[f] = (int32_t)r;
+      }
+      for (int i = tid; i < kHashCap; i += kThreads) {
+        keys[i] = kEmpty;
+        vals[i] = 0.0;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_count = 0;
+        s_fail = 0;
+      }
+      continue;
+    }
+    // flush: read this thread's slots, classify, reset the table
+    int32_t rk[kHashPerThread];
+    double rv[kHashPerThread];
+    int nst = 0;
+    double fs = 0.0;
+    long long nnzu = 0;
+#pragma unroll
+    for (int j = 0; j < kHashPerThread; j++) {
+      const int i = tid + j * kThreads;
+      int32_t c = keys[i];
+      double x = 0.0;
+      bool st = false;
+      if (c != kEmpty) {
+        x = vals[i] / a.divisor;
+        if (x != 0.0) {
+          nnzu++;
+          st = fabs(x) > a.floor_tau;
+          if (!st) fs += x * x;
+        }
+      }
+      rk[j] = st ? c : kEmpty;
+      rv[j] = x;
+      nst += st;
+    }
+    __syncthreads();
+    // block exclusive scan of nst
+    {
+      int v = nst;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL_MASK, v, o);
+        if (lane >= o) v += y;
+      }
+      if (lane == 31) s_base[warp] = v;
+      fs = warp_sum(fs);
+      nnzu = warp_sum(nnzu);
+      if (lane == 0) {
+        s_fs[warp] = fs;
+        s_nz[warp] = nnzu;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        long long acc = 0;
+        for (int w = 0; w < kWarps; w++) {
+          long long t = s_base[w];
+          s_base[w] = acc;
+          acc += t;
+        }
+        s_base[kWarps] = acc;
+      }
+      __syncthreads();
+      int pos = (int)s_base[warp] + v - nst;
+#pragma unroll
+      for (int j = 0; j < kHashPerThread; j++) {
+        if (rk[j] != kEmpty) {
+          keys[pos] = rk[j];
+          vals[pos] = rv[j];
+          pos++;
+        }
+      }
+    }
+    const int total = (int)s_base[kWarps];
+    int P = 1;
+    while (P < total) P <<= 1;
+    for (int i = total + tid; i < P; i += kThreads) keys[i] = INT32_MAX;
+    __syncthreads();
+    // bitonic sort of (keys, vals)[0..P) by column
+    for (int k2 = 2; k2 <= P; k2 <<= 1) {
+      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+        for (int i = tid; i < P; i += kThreads) {
+          int ixj = i ^ j2;
+          if (ixj > i) {
+            int32_t ki = keys[i], kj = keys[ixj];
+            bool up = (i & k2) == 0;
+            if ((ki > kj) == up) {
+              keys[i] = kj;
+              keys[ixj] = ki;
+              double t = vals[i];
+              vals[i] = vals[ixj];
+              vals[ixj] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid == 0) s_off = atomicAdd(a.pool_used, (unsigned long long)total);
+    __syncthreads();
+    const unsigned long long off = s_off;
+    const bool ok = (long long)off + total <= a.pool_cap;
+    if (ok) {
+      for (int i = tid; i < total; i += kThreads) {
+        a.pool_col[off + i] = keys[i];
+        a.pool_val[off + i] = vals[i];
+      }
+    }
+    if (tid == 0) {
+      double f = 0.0;
+      long long z = 0;
+      for (int w = 0; w < kWarps; w++) {
+        f += s_fs[w];
+        z += s_nz[w];
+      }
+      if (!ok) atomicOr(a.flags, 1);
+      a.row_off[r] = (int64_t)off;
+      a.row_cnt[r] = total;
+      a.row_fsum[r] = f;
+      a.row_nnz[r] = z;
+      s_count = 0;
+    }
+    __syncthreads();
+    for (int i = tid; i < kHashCap; i += kThreads) {
+      keys[i] = kEmpty;
+      vals[i] = 0.0;
+    }
+  }
+}
+
+void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                         cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  int smem = hash_smem_bytes();
+  cudaFuncSetAttribute(k_numeric_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_hash<<<a.grid, kThreads, smem, st>>>(a, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
+// K3k numeric filtered SpGEMM, one CTA per output row, k-synchronous hash accumulator.
+//
+// The CTA adds the B rows of row r ONE k AT A TIME, in ascending k, its 256 threads
+// over that row's entries (distinct columns), with a barrier between consecutive k.  So
+// no two threads ever update the same slot concurrently: plain shared-memory
+// read-add-write (the fp64 shared atomic is a CAS loop on sm_100a), and
+// each entry is accumulated exactly like the oracle: acc = self*a_rj, then
+// acc = acc + (a_rk * b_kj) for ascending k, then acc / divisor, with _rn intrinsics
+// (no FMA contraction) -- C~ is bit-identical to the oracle.  The next k's entries are
+// prefetched into registers while the current k is added.  Flush as k_numeric_hash.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int hash_find_insert(volatile int32_t *keys, int32_t c, int *count) {
+  unsigned h = hslot(c);
+#pragma unroll 1
+  for (int probe = 0; probe < kHashCap; probe++) {
+    int32_t k = keys[h];
+    if (k == c) return (int)h;
+    if (k == kEmpty) {
+      int32_t old = atomicCAS((int32_t *)&keys[h], kEmpty, c);
+      if (old == kEmpty) {
+        int n = atomicAdd(count, 1);
+        return n < kHashMaxFill ? (int)h : -1;
+      }
+      if (old == c) return (int)h;
+    }
+    h = (h + 1) & (kHashCap - 1);
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kThreads) k_numeric_ksync(NumericArgs a, int32_t *fail_rows,
+                                                            int *fail_count) {
+  extern __shared__ double hsm[];
+  double *vals = hsm;
+  int32_t *keys = reinterpret_cast<int32_t *>(hsm + kHashCap);
+  __shared__ long long s_start[kThreads];
+  __shared__ int s_len[kThreads];
+  __shared__ double s_av[kThreads];
+  __shared__ int s_row;
+  __shared__ int s_count;
+  __shared__ int s_fail;
+  __shared__ unsigned long long s_off;
+  __shared__ long long s_base[kWarps + 1];
+  __shared__ double s_fs[kWarps];
+  __shared__ long long s_nz[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kHashCap; i += kThreads) {
+    keys[i] = kEmpty;
+    vals[i] = 0.0;
+  }
+  if (tid == 0) {
+    s_count = 0;
+    s_fail = 0;
+  }
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int idx = s_row;
+    if (idx >= a.nlist) break;
+    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
+    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
+    const int nk = (int)(pa1 - pa0);
+    if (a.hi[r] < a.lo[r]) {
+      if (tid == 0) {
+        a.row_off[r] = 0;
+        a.row_cnt[r] = 0;
+        a.row_fsum[r] = 0.0;
+        a.row_nnz[r] = 0;
+      }
+      continue;
+    }
+    if (nk > kHashMaxFill) {
+      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+      continue;
+    }
+    if (a.self_coef != 0.0) {  // 2T term first (Eq. 2.7)
+      for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
+        int h = hash_find_insert(keys, a.A.col[p], &s_count);
+        if (h >= 0) vals[h] = __dmul_rn(a.self_coef, a.A.val[p]);
+        else s_fail = 1;
+      }
+    }
+    for (int kc = 0; kc < nk; kc += kThreads) {
+      __syncthreads();
+      if (s_fail) break;
+      {
+        const int j = kc + tid;
+        long long st0 = 0;
+        int ln = 0;
+        double av = 0.0;
+        if (j < nk) {
+          const int64_t k = (int64_t)a.A.col[pa0 + j] - a.B.row0;
+          if (k >= 0 && k < a.B.nrows) {
+            st0 = a.B.rp[k];
+            ln = (int)(a.B.rp[k + 1] - st0);
+            av = a.A.val[pa0 + j];
+          }
+        }
+        s_start[tid] = st0;
+        s_len[tid] = ln;
+        s_av[tid] = av;
+      }
+      __syncthreads();
+      const int cn = nk - kc < kThreads ? nk - kc : kThreads;
+      // prefetch the first entry of k = kc for this thread
+      int32_t pc = 0;
+      double pv = 0.0;
+      if (tid < s_len[0]) {
+        pc = a.B.col[s_start[0] + tid];
+        pv = a.B.val[s_start[0] + tid];
+      }
+      for (int kk = 0; kk < cn; kk++) {
+        const long long st0 = s_start[kk];
+        const int ln = s_len[kk];
+        const double av = s_av[kk];
+        const int32_t cc = pc;
+        const double cv = pv;
+        if (kk + 1 < cn) {  // prefetch next k
+          const int nl = s_len[kk + 1];
+          if (tid < nl) {
+            const long long ns = s_start[kk + 1];
+            pc = a.B.col[ns + tid];
+            pv = a.B.val[ns + tid];
+          }
+        }
+        if (tid < ln) {
+          int h = hash_find_insert(keys, cc, &s_count);
+          if (h >= 0) vals[h] = __dadd_rn(vals[h], __dmul_rn(av, cv));
+          else s_fail = 1;
+          for (int e = tid + kThreads; e < ln; e += kThreads) {
+            const int32_t c = a.B.col[st0 + e];
+            const double v = a.B.val[st0 + e];
+            h = hash_find_insert(keys, c, &s_count);
+            if (h >= 0) vals[h] = __dadd_rn(vals[h], __dmul_rn(av, v));
+            else s_fail = 1;
+          }
+        }
+        __syncthreads();  // k -> k+1: one writer per slot at any time
+      }
+    }
+    __syncthreads();
+    if (s_fail) {
+      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+      for (int i = tid; i < kHashCap; i += kThreads) {
+        keys[i] = kEmpty;
+        vals[i] = 0.0;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_count = 0;
+        s_fail = 0;
+      }
+      continue;
+    }
+    // flush: identical to k_numeric_hash
+    int32_t rk[kHashPerThread];
+    double rv[kHashPerThread];
+    int nst = 0;
+    double fs = 0.0;
+    long long nnzu = 0;
+#pragma unroll
+    for (int j = 0; j < kHashPerThread; j++) {
+      const int i = tid + j * kThreads;
+      int32_t c = keys[i];
+      double x = 0.0;
+      bool st = false;
+      if (c != kEmpty) {
+        x = vals[i] / a.divisor;
+        if (x != 0.0) {
+          nnzu++;
+          st = fabs(x) > a.floor_tau;
+          if (!st) fs += x * x;
+        }
+      }
+      rk[j] = st ? c : kEmpty;
+      rv[j] = x;
+      nst += st;
+    }
+    __syncthreads();
+    {
+      int v = nst;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL_MASK, v, o);
+        if (lane >= o) v += y;
+      }
+      if (lane == 31) s_base[warp] = v;
+      fs = warp_sum(fs);
+      nnzu = warp_sum(nnzu);
+      if (lane == 0) {
+        s_fs[warp] = fs;
+        s_nz[warp] = nnzu;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        long long acc = 0;
+        for (int w = 0; w < kWarps; w++) {
+          long long t = s_base[w];
+          s_base[w] = acc;
+          acc += t;
+        }
+        s_base[kWarps] = acc;
+      }
+      __syncthreads();
+      int pos = (int)s_base[warp] + v - nst;
+#pragma unroll
+      for (int j = 0; j < kHashPerThread; j++) {
+        if (rk[j] != kEmpty) {
+          keys[pos] = rk[j];
+          vals[pos] = rv[j];
+          pos++;
+        }
+      }
+    }
+    const int total = (int)s_base[kWarps];
+    int P = 1;
+    while (P < total) P <<= 1;
+    for (int i = total + tid; i < P; i += kThreads) keys[i] = INT32_MAX;
+    __syncthreads();
+    for (int k2 = 2; k2 <= P; k2 <<= 1) {
+      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+        for (int i = tid; i < P; i += kThreads) {
+          int ixj = i ^ j2;
+          if (ixj > i) {
+            int32_t ki = keys[i], kj = keys[ixj];
+            bool up = (i & k2) == 0;
+            if ((ki > kj) == up) {
+              keys[i] = kj;
+              keys[ixj] = ki;
+              double t = vals[i];
+              vals[i] = vals[ixj];
+              vals[ixj] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid == 0) s_off = atomicAdd(a.pool_used, (unsigned long long)total);
+    __syncthreads();
+    const unsigned long long off = s_off;
+    const bool ok = (long long)off + total <= a.pool_cap;
+    if (ok) {
+      for (int i = tid; i < total; i += kThreads) {
+        a.pool_col[off + i] = keys[i];
+        a.pool_val[off + i] = vals[i];
+      }
+    }
+    if (tid == 0) {
+      double f = 0.0;
+      long long z = 0;
+      for (int w = 0; w < kWarps; w++) {
+        f += s_fs[w];
+        z += s_nz[w];
+      }
+      if (!ok) atomicOr(a.flags, 1);
+      a.row_off[r] = (int64_t)off;
+      a.row_cnt[r] = total;
+      a.row_fsum[r] = f;
+      a.row_nnz[r] = z;
+      s_count = 0;
+    }
+    __syncthreads();
+    for (int i = tid; i < kHashCap; i += kThreads) {
+      keys[i] = kEmpty;
+      vals[i] = 0.0;
+    }
+  }
+}
+
+void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                          cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  int smem = hash_smem_bytes();
+  cudaFuncSetAttribute(k_numeric_ksync, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_ksync<<<a.grid, kThreads, smem, st>>>(a, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
+// K3p numeric filtered SpGEMM: one CTA per output row, k-synchronous, PAGED accumulator.
+//
+// Accumulator: the row's reachable column span [lo, hi] (K1) is cut into pages of 2^s
+// columns (s chosen so the span has <= kPages pages); a page gets 2^s value slots the
+// first time any product lands in it (page-table CAS, rare), so a column maps to its slot
+// with one shared-memory load and a shift -- no probing.  Pages are allocated in the
+// order products arrive, but the flush walks the page table in column order, so the
+// staged row comes out sorted without any sort.  Like K3k, the B rows are added one k at
+// a time in ascending k with a barrier between k (one writer per slot, no atomics on
+// values, exact oracle order with _rn intrinsics: C~ bit-identical to the oracle).
+// Rows whose span needs pages wider than 64 columns or whose pages overflow kSlots are
+// handed to the block-window kernel.
+// ------------------------------------------------------------------------------------
+constexpr int kPages = 4096;
+constexpr int kSlots = 4096;
+constexpr int kMaxPageShift = 6;
+
+int paged_smem_bytes() { return kSlots * 8 + kPages * 4 * 2; }
+
+__device__ __forceinline__ int page_slot(volatile int32_t *ptab, int pg, int psize, int *slot_count) {
+  int b = ptab[pg];
+  if (b >= 0) return b;
+  if (b == -1) {
+    int old = atomicCAS((int32_t *)&ptab[pg], -1, -2);
+    if (old == -1) {
+      int nb = atomicAdd(slot_count, psize);
+      if (nb + psize > kSlots) nb = -3;  // overflow marker
+      __threadfence_block();
+      ptab[pg] = nb;
+      return nb;
+    }
+  }
+  while ((b = ptab[pg]) == -2) {
+  }
+  return b;  // >= 0 or -3 (overflow)
+}
+
+__global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32_t *fail_rows,
+                                                            int *fail_count) {
+  extern __shared__ double psm[];
+  double *vals = psm;                                              // kSlots
+  int32_t *ptab = reinterpret_cast<int32_t *>(psm + kSlots);       // kPages
+  int32_t *plist = ptab + kPages;                                  // kPages (flush)
+  __shared__ long long s_start[kThreads];
+  __shared__ int s_len[kThreads];
+  __shared__ double s_av[kThreads];
+  __shared__ int s_row, s_slots, s_fail, s_npl;
+  __shared__ unsigned long long s_off;
+  __shared__ long long s_wsum[kWarps + 1];
+  __shared__ double s_fs[kWarps];
+  __shared__ long long s_nz[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kSlots; i += kThreads) vals[i] = 0.0;
+  for (int i = tid; i < kPages; i += kThreads) ptab[i] = -1;
+  if (tid == 0) {
+    s_slots = 0;
+    s_fail = 0;
+  }
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int idx = s_row;
+    if (idx >= a.nlist) break;
+    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
+    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
+    const int nk = (int)(pa1 - pa0);
+    const int32_t lo = a.lo[r], hi = a.hi[r];
+    if (hi < lo) {
+      if (tid == 0) {
+        a.row_off[r] = 0;
+        a.row_cnt[r] = 0;
+        a.row_fsum[r] = 0.0;
+        a.row_nnz[r] = 0;
+      }
+      continue;
+    }
+    const int64_t span = (int64_t)hi - lo + 1;
+    int sh = 4;
+    while ((span >> sh) >= kPages) sh++;
+    if (sh > kMaxPageShift || nk > kSlots) {
+      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+      continue;
+    }
+    const int psize = 1 << sh;
+    const int npages = (int)((span - 1) >> sh) + 1;
+    if (a.self_coef != 0.0) {  // 2T term first (Eq. 2.7)
+      for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
+        const int rel = a.A.col[p] - lo;
+        const int b = page_slot(ptab, rel >> sh, psize, &s_slots);
+        if (b >= 0) vals[b + (rel & (psize - 1))] = __dmul_rn(a.self_coef, a.A.val[p]);
+        else s_fail = 1;
+      }
+    }
+    for (int kc = 0; kc < nk; kc += kThreads) {
+      __syncthreads();
+      if (s_fail) break;
+      {
+        const int j = kc + tid;
+        long long st0 = 0;
+        int ln = 0;
+        double av = 0.0;
+        if (j < nk) {
+          const int64_t k = (int64_t)a.A.col[pa0 + j] - a.B.row0;
+          if (k >= 0 && k < a.B.nrows) {
+            st0 = a.B.rp[k];
+            ln = (int)(a.B.rp[k + 1] - st0);
+            av = a.A.val[pa0 + j];
+          }
+        }
+        s_start[tid] = st0;
+        s_len[tid] = ln;
+        s_av[tid] = av;
+      }
+      __syncthreads();
+      const int cn = nk - kc < kThreads ? nk - kc : kThreads;
+      int32_t pc = 0;
+      double pv = 0.0;
+      if (tid < s_len[0]) {
+        pc = a.B.col[s_start[0] + tid];
+        pv = a.B.val[s_start[0] + tid];
+      }
+      for (int kk = 0; kk < cn; kk++) {
+        const long long st0 = s_start[kk];
+        const int ln = s_len[kk];
+        const double av = s_av[kk];
+        const int32_t cc = pc;
+        const double cv = pv;
+        if (kk + 1 < cn) {
+          const int nl = s_len[kk + 1];
+          if (tid < nl) {
+            const long long ns = s_start[kk + 1];
+            pc = a.B.col[ns + tid];
+            pv = a.B.val[ns + tid];
+          }
+        }
+        if (tid < ln) {
+          int rel = cc - lo;
+          int b = page_slot(ptab, rel >> sh, psize, &s_slots);
+          if (b >= 0) {
+            const int o = b + (rel & (psize - 1));
+            vals[o] = __dadd_rn(vals[o], __dmul_rn(av, cv));
+          } else {
+            s_fail = 1;
+          }
+          for (int e = tid + kThreads; e < ln; e += kThreads) {
+            rel = a.B.col[st0 + e] - lo;
+            const double v = a.B.val[st0 + e];
+            b = page_slot(ptab, rel >> sh, psize, &s_slots);
+            if (b >= 0) {
+              const int o = b + (rel & (psize - 1));
+              vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v));
+            } else {
+              s_fail = 1;
+            }
+          }
+        }
+        __syncthreads();  // one writer per slot at any time (k -> k+1)
+      }
+    }
+    __syncthreads();
+    const bool failed = s_fail != 0;
+    // ---- flush: allocated pages in column order ----
+    // (a) ordered list of allocated pages
+    if (tid == 0) s_npl = 0;
+    __syncthreads();
+    for (int t0 = 0; t0 < npages; t0 += kThreads) {
+      const int i = t0 + tid;
+      const bool f = !failed && i < npages && ptab[i] >= 0;
+      const unsigned m = __ballot_sync(FULL_MASK, f);
+      if (lane == 0) s_wsum[warp] = __popc(m);
+      __syncthreads();
+      if (tid == 0) {
+        long long acc = s_npl;
+        for (int w = 0; w < kWarps; w++) {
+          long long t = s_wsum[w];
+          s_wsum[w] = acc;
+          acc += t;
+        }
+        s_npl = (int)acc;
+      }
+      __syncthreads();
+      if (f) plist[s_wsum[warp] + __popc(m & lanemask_lt())] = i;
+      __syncthreads();
+    }
+    const int npl = s_npl;
+    // (b) per-thread contiguous range of slots in page order: thread handles list
+    //     positions [q0, q1) of the concatenated (page, offset) sequence
+    const int total_slots = npl * psize;
+    const int per = (total_slots + kThreads - 1) / kThreads;
+    const int q0 = tid * per < total_slots ? tid * per : total_slots;
+    const int q1 = q0 + per < total_slots ? q0 + per : total_slots;
+    int nst = 0;
+    double fs = 0.0;
+    long long nnzu = 0;
+    for (int q = q0; q < q1; q++) {
+      const int pgi = plist[q >> sh];
+      const int o = ptab[pgi] + (q & (psize - 1));
+      const double x = vals[o] / a.divisor;
+      if (x != 0.0) {
+        nnzu++;
+        if (fabs(x) > a.floor_tau) nst++;
+        else fs += x * x;
+      }
+    }
+    // exclusive scan of nst over threads (thread order == column order)
+    int v = nst;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULL_MASK, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) s_wsum[warp] = v;
+    fs = warp_sum(fs);
+    nnzu = warp_sum(nnzu);
+    if (lane == 0) {
+      s_fs[warp] = fs;
+      s_nz[warp] = nnzu;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long acc = 0;
+      for (int w = 0; w < kWarps; w++) {
+        long long t = s_wsum[w];
+        s_wsum[w] = acc;
+        acc += t;
+      }
+      s_wsum[kWarps] = acc;
+      s_off = failed ? 0ull : atomicAdd(a.pool_used, (unsigned long long)acc);
+    }
+    __syncthreads();
+    const long long total = s_wsum[kWarps];
+    const unsigned long long off = s_off;
+    const bool ok = !failed && (long long)off + total <= a.pool_cap;
+    if (ok) {
+      long long pos = (long long)off + s_wsum[warp] + v - nst;
+      for (int q = q0; q < q1; q++) {
+        const int pgi = plist[q >> sh];
+        const int o = ptab[pgi] + (q & (psize - 1));
+        const double x = vals[o] / a.divisor;
+        if (x != 0.0 && fabs(x) > a.floor_tau) {
+          a.pool_col[pos] = lo + (pgi << sh) + (q & (psize - 1));
+          a.pool_val[pos] = x;
+          pos++;
+        }
+      }
+    }
+    __syncthreads();
+    // (c) reset the touched pages
+    if (failed) {
+      for (int i = tid; i < kSlots; i += kThreads) vals[i] = 0.0;
+      for (int i = tid; i < npages; i += kThreads) ptab[i] = -1;
+    } else {
+      for (int q = tid; q < total_slots; q += kThreads) {
+        const int pgi = plist[q >> sh];
+        vals[ptab[pgi] + (q & (psize - 1))] = 0.0;
+      }
+      __syncthreads();
+      for (int i = tid; i < npl; i += kThreads) ptab[plist[i]] = -1;
+    }
+    if (tid == 0) {
+      if (failed) {
+        fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+      } else {
+        double f = 0.0;
+        long long z = 0;
+        for (int w = 0; w < kWarps; w++) {
+          f += s_fs[w];
+          z += s_nz[w];
+        }
+        if (!ok) atomicOr(a.flags, 1);
+        a.row_off[r] = (int64_t)off;
+        a.row_cnt[r] = total;
+        a.row_fsum[r] = f;
+        a.row_nnz[r] = z;
+      }
+      s_slots = 0;
+      s_fail = 0;
+    }
+  }
+}
+
+void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                          cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  int smem = paged_smem_bytes();
+  cudaFuncSetAttribute(k_numeric_paged, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_paged<<<a.grid, kThreads, smem, st>>>(a, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
+// K3w numeric filtered SpGEMM, one WARP per output row, conflict-free dense window.
+//
+// Row r of C~ = self_coef * A(r,:) + sum_k a_rk B(k,:) is built in column passes: a pass
+// starts at the smallest column any remaining entry of row r's sources reaches (B rows
+// are sorted, every k keeps a cursor that only moves forward) and covers `window`
+// columns of a private shared-memory window.  Inside a pass the warp adds the self term
+// first, then the B rows one k at a time in ascending k, lanes over a row's entries
+// (distinct columns), so no two lanes ever touch the same slot: no atomics, no barriers,
+// and every entry is accumulated exactly as the oracle does it --
+// acc = self*a_rj; acc = acc + (a_rk * b_kj) for ascending k, then acc / divisor -- with
+// explicit _rn intrinsics (no FMA contraction), i.e. bit-identical values of C~.
+// The flush scans only the touched span of the window, classifies (Algorithm 4.1 floor,
+// see k_numeric) and stages entries in column order: rows come out sorted.
+// ------------------------------------------------------------------------------------
+constexpr int kWarpRowWarps = 4;        // warps per CTA
+constexpr int kWarpRowCursors = 512;    // cursors kept in shared memory per warp
+
+int warp_numeric_smem_bytes(int window) {
+  return kWarpRowWarps * (window * (int)sizeof(double) + kWarpRowCursors * 12);
+}
+
+__global__ void __launch_bounds__(kWarpRowWarps * 32) k_numeric_warp(NumericArgs a) {
+  extern __shared__ double wsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int W = a.window;
+  double *win = wsm + (size_t)wib * (W + (kWarpRowCursors * 12) / 8);
+  int64_t *scur = reinterpret_cast<int64_t *>(win + W);
+  int32_t *slen = reinterpret_cast<int32_t *>(scur + kWarpRowCursors);
+  const int64_t gw = (int64_t)blockIdx.x * kWarpRowWarps + wib;
+  int64_t *gcur = a.cursor + gw * 2 * a.cursor_cap;
+  int32_t *sc = a.scr_col + gw * a.scr_cap;
+  double *sv = a.scr_val + gw * a.scr_cap;
+  for (int i = lane; i < W; i += 32) win[i] = 0.0;
+  __syncwarp();
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(a.row_counter, 1);
+    idx = __shfl_sync(FULL_MASK, idx, 0);
+    if (idx >= a.nlist) break;
+    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
+    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
+    const int nk = (int)(pa1 - pa0);
+    // per-k cursor (absolute position in B) and entries left; shared memory when they
+    // fit, else this warp's global scratch
+    int64_t *cur = nk <= kWarpRowCursors ? scur : gcur;
+    int32_t *rem_end = nk <= kWarpRowCursors ? slen : reinterpret_cast<int32_t *>(gcur + a.cursor_cap);
+    for (int j = lane; j < nk; j += 32) {
+      const int64_t k = (int64_t)a.A.col[pa0 + j] - a.B.row0;
+      int64_t b0 = 0, b1 = 0;
+      if (k >= 0 && k < a.B.nrows) {
+        b0 = a.B.rp[k];
+        b1 = a.B.rp[k + 1];
+      }
+      cur[j] = b0;
+      rem_end[j] = (int32_t)(b1 - b0);
+    }
+    __syncwarp();
+    long long self_pos = pa0;
+    long long nst = 0;
+    double fs = 0.0;
+    long long nnzu = 0;
+    for (;;) {
+      // next column reached by any remaining source
+      int32_t nxt = INT32_MAX;
+      for (int j = lane; j < nk; j += 32) {
+        if (rem_end[j] > 0) {
+          int32_t c = a.B.col[cur[j]];
+          nxt = c < nxt ? c : nxt;
+        }
+      }
+      if (a.self_coef != 0.0 && lane == 0 && self_pos < pa1) {
+        int32_t c = a.A.col[self_pos];
+        nxt = c < nxt ? c : nxt;
+      }
+      nxt = warp_min(nxt);
+      nxt = __shfl_sync(FULL_MASK, nxt, 0);
+      if (nxt == INT32_MAX) break;
+      const int64_t c0 = nxt;
+      const int64_t c1 = c0 + W;
+      int tmin = INT32_MAX, tmax = -1;
+      // self term (the 2T of Eq. 2.7), stored first
+      if (a.self_coef != 0.0) {
+        for (;;) {
+          const long long p = self_pos + lane;
+          bool v = false;
+          if (p < pa1) {
+            const int32_t c = a.A.col[p];
+            v = (int64_t)c < c1;
+            if (v) {
+              const int o = (int)(c - c0);
+              win[o] = __dmul_rn(a.self_coef, a.A.val[p]);
+              tmin = o < tmin ? o : tmin;
+              tmax = o > tmax ? o : tmax;
+            }
+          }
+          const int cnt = __popc(__ballot_sync(FULL_MASK, v));
+          self_pos += cnt;
+          if (cnt < 32) break;
+        }
+      }
+      // products, ascending k
+      for (int j0 = 0; j0 < nk; j0 += 32) {
+        const int j = j0 + lane;
+        long long mypos = 0;
+        int myrem = 0;
+        bool act = false;
+        if (j < nk) {
+          myrem = rem_end[j];
+          if (myrem > 0) {
+            mypos = cur[j];
+            act = (int64_t)a.B.col[mypos] < c1;
+          }
+        }
+        unsigned mask = __ballot_sync(FULL_MASK, act);
+        while (mask) {
+          const int jj = __ffs(mask) - 1;
+          mask &= mask - 1;
+          long long pos = __shfl_sync(FULL_MASK, mypos, jj);
+          const int rem = __shfl_sync(FULL_MASK, myrem, jj);
+          const long long end = pos + rem;
+          const double av = a.A.val[pa0 + j0 + jj];
+          for (;;) {
+            const long long p = pos + lane;
+            bool v = false;
+            if (p < end) {
+              const int32_t c = a.B.col[p];
+              v = (int64_t)c < c1;
+              if (v) {
+                const int o = (int)(c - c0);
+                win[o] = __dadd_rn(win[o], __dmul_rn(av, a.B.val[p]));
+                tmin = o < tmin ? o : tmin;
+                tmax = o > tmax ? o : tmax;
+              }
+            }
+            const int cnt = __popc(__ballot_sync(FULL_MASK, v));
+            pos += cnt;
+            if (cnt < 32 || pos >= end) break;
+          }
+          if (lane == jj) {
+            myrem -= (int)(pos - mypos);
+            mypos = pos;
+          }
+        }
+        if (j < nk && act) {
+          cur[j] = mypos;
+          rem_end[j] = myrem;
+        }
+      }
+      __syncwarp();
+      // flush the touched span [tmin, tmax] in column order
+      tmin = warp_min(tmin);
+      tmax = warp_max(tmax);
+      tmin = __shfl_sync(FULL_MASK, tmin, 0);
+      tmax = __shfl_sync(FULL_MASK, tmax, 0);
+      for (int base = tmin; base <= tmax; base += 32) {
+        const int o = base + lane;
+        bool st = false;
+        double x = 0.0;
+        if (o <= tmax) {
+          x = win[o] / a.divisor;
+          win[o] = 0.0;
+          if (x != 0.0) {
+            nnzu++;
+            st = fabs(x) > a.floor_tau;
+            if (!st) fs += x * x;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL_MASK, st);
+        if (st) {
+          const long long pp = nst + __popc(m & lanemask_lt());
+          if (pp < a.scr_cap) {
+            sc[pp] = (int32_t)(c0 + o);
+            sv[pp] = x;
+          }
+        }
+        nst += __popc(m);
+      }
+      __syncwarp();
+    }
+    fs = warp_sum(fs);
+    nnzu = warp_sum(nnzu);
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)nst);
+    off = __shfl_sync(FULL_MASK, off, 0);
+    const bool ok = (long long)off + nst <= a.pool_cap && nst <= a.scr_cap;
+    if (ok) {
+      for (long long t = lane; t < nst; t += 32) {
+        a.pool_col[off + t] = sc[t];
+        a.pool_val[off + t] = sv[t];
+      }
+    }
+    if (lane == 0) {
+      if (!ok) atomicOr(a.flags, nst > a.scr_cap ? 2 : 1);
+      a.row_off[r] = (int64_t)off;
+      a.row_cnt[r] = nst;
+      a.row_fsum[r] = fs;
+      a.row_nnz[r] = nnzu;
+    }
+    __syncwarp();
+  }
+}
+
+void launch_numeric_warp(const NumericArgs &a, cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  int smem = warp_numeric_smem_bytes(a.window);
+  cudaFuncSetAttribute(k_numeric_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_warp<<<a.grid, kWarpRowWarps * 32, smem, st>>>(a);
 }
 
 // ------------------------------------------------------------------------------------

@@ -91,9 +91,25 @@ struct NumericArgs {
   int *row_counter = nullptr;     // dynamic scheduler
   int *flags = nullptr;           // flags[0] |= 1 on pool overflow, 2 on scratch overflow
   int grid = 0;
+  int64_t nlist = 0;              // rows to process: order[0..nlist) (or 0..nlist)
 };
 int numeric_smem_bytes(int window);
 void launch_numeric(const NumericArgs &a, cudaStream_t st);
+// warp-per-row conflict-free window variant (bit-identical accumulation order)
+constexpr int kWarpRowWarpsPerCta = 4;
+int warp_numeric_smem_bytes(int window);
+void launch_numeric_warp(const NumericArgs &a, cudaStream_t st);
+// k-synchronous hash variant (no atomics on values, bit-identical accumulation order)
+void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                          cudaStream_t st);
+// k-synchronous paged variant (no probing, sorted flush, bit-identical order)
+int paged_smem_bytes();
+void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                          cudaStream_t st);
+// hash-accumulator variant; rows whose table over-fills are appended to fail_rows
+int hash_smem_bytes();
+void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                         cudaStream_t st);
 
 // --- K6 Algorithm 4.1 pass -------------------------------------------------------
 // out[0] = sum over x[0..cnt) of x^2 for |x| <= tau (deterministic order for fixed layout)

@@ -31,7 +31,7 @@ def run_gpu(B, H, eps_tol=1e-16, **opts):
 
 def run_both(B, H, eps_tol=1e-16, **opts):
     Eg, st = run_gpu(B, H, eps_tol, **opts)
-    oo = {k: v for k, v in opts.items() if k != "window_cols"}
+    oo = {k: v for k, v in opts.items() if k not in ("window_cols", "kernel")}
     Eo, tr = O.expm(H, eps_tol, nthreads=NTHREADS, **oo)
     return Eg, st, Eo, tr
 
@@ -258,3 +258,29 @@ def test_alg41_random_vs_oracle(B):
         assert p == passes_o
         assert t == pytest.approx(tau_o, rel=1e-12)
         assert d == pytest.approx(dropped_o, rel=1e-10, abs=1e-300)
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("name", ["heat2d_pm10_20", "structural_24", "heat3d_9", "banded_nonsym"])
+def test_accumulator_variants(B, kernel, name):
+    """Every K3 accumulator (hash, warp-window, block-window) meets parity."""
+    H = SMALL[name]()
+    Eg, st, Eo, tr = run_both(B, H, kernel=kernel)
+    assert_parity(Eg, st, Eo, tr)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_warp_window_bit_exact_products(B, seed):
+    """The warp-window kernel accumulates self term first, then ascending k with
+    round-to-nearest products and sums (no FMA): C~ is bit-identical to the oracle."""
+    import torch
+    n = 300
+    A = _rand_csr(n, 9, 0.6, 300 + seed, empty_rows=(3, 200))
+    old = B._ctx
+    B._ctx = None
+    h = B._context()
+    (rp, ci, va), passes, tau, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(A), 2.0, 1.0, 0.0)
+    Ct = O.spgemm(A, A, 2.0, 1.0)
+    G = from_dev(n, rp, ci, va)
+    assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
+    assert np.array_equal(G.val, Ct.val)  # bit-exact
