@@ -90,10 +90,12 @@ typedef struct {
   int32_t force_N;        /* -1 = from Eq. (4.20) */
   int32_t output_T;       /* 0 = return E = I + T^_N (default); 1 = return T^_N */
   int32_t window_cols;    /* dense accumulator window of the block-window kernel (0 = 8192) */
-  int32_t kernel;         /* K3 accumulator: 0 auto (k-sync paged for squarings, atomic hash for
-                             Taylor terms), 1 atomic hash, 2 warp-window, 3 block-window,
-                             4 k-synchronous hash, 5 k-synchronous paged; all meet parity;
-                             2, 4 and 5 reproduce the oracle's C~ bit for bit */
+  int32_t kernel;         /* K3 accumulator: 0 auto (k-sync paged for squarings, pull over H0^T
+                             for Taylor terms), 1 atomic hash, 2 warp-window, 3 block-window,
+                             4 k-synchronous hash, 5 k-synchronous paged, 6 Taylor pull (Taylor
+                             terms only; else 1).  All meet parity; 2, 4, 5 and 6 reproduce the
+                             oracle's C~ bit for bit.  Rows a kernel cannot hold fall through
+                             6 -> 1 -> 3 and 1/4/5 -> 3. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */

@@ -196,7 +196,7 @@ struct Workspace {
   DBuf<double> scr_val, pool_val;
   DBuf<unsigned long long> pool_used;
   DBuf<int> row_counter, flags, fail_count;
-  DBuf<int32_t> fail_rows;
+  DBuf<int32_t> fail_rows, fail_rows2;
   int64_t pool_cap_hint = 0;
 };
 
@@ -212,6 +212,7 @@ struct sexpm_plan_s {
   double eps_tol = 0.0;
   DCsr H0full;  // H0 = H 2^-N, all n rows (replicated)
   DCsr H0loc;   // this rank's rows of H0
+  DCsr H0T;     // H0^T (CSC of H0, columns sorted by row) for the Taylor pull kernel
   DCsr T, Tn, S, Sn, Bhalo, Ibuf, E;  // persistent (grow-only) iterates
   int32_t retries = 0;
   DBuf<int32_t> proc_order;  // K3 row processing order (cluster order of H's graph)
@@ -272,12 +273,42 @@ static T d2h(const T *dptr, cudaStream_t st) {
   return v;
 }
 
+// B^T as CSR (= CSC of B) with every row sorted by column: count, scan, scatter, sort.
+static void build_transpose(sexpm_plan_s &P, const CsrView &Bv, int64_t ncols, DCsr &BT) {
+  cudaStream_t st = P.st;
+  Workspace &w = P.ws;
+  DBuf<int32_t> ccnt;
+  ccnt.alloc((size_t)std::max<int64_t>(ncols, 1), st);
+  CK(cudaMemsetAsync(ccnt.p, 0, ncols * sizeof(int32_t), st));
+  launch_col_count(Bv, ccnt.p, st);
+  DBuf<int64_t> cnt64, cursor;
+  cnt64.alloc((size_t)std::max<int64_t>(ncols, 1), st);
+  std::vector<int32_t> hc32((size_t)ncols);
+  CK(cudaMemcpyAsync(hc32.data(), ccnt.p, ncols * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> hc64(hc32.begin(), hc32.end());
+  CK(cudaMemcpyAsync(cnt64.p, hc64.data(), ncols * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  BT.nrows = ncols;
+  BT.row0 = 0;
+  BT.nnz = Bv.nnz;
+  BT.rp.alloc((size_t)ncols + 1, st);
+  w.scan_tmp.ensure((size_t)scan_tmp_elems(ncols) + 1, st);
+  launch_exclusive_scan(cnt64.p, ncols, BT.rp.p, w.scan_tmp.p, st);
+  cursor.alloc((size_t)std::max<int64_t>(ncols, 1), st);
+  CK(cudaMemcpyAsync(cursor.p, BT.rp.p, ncols * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  BT.col.alloc((size_t)std::max<int64_t>(Bv.nnz, 1), st);
+  BT.val.alloc((size_t)std::max<int64_t>(Bv.nnz, 1), st);
+  launch_transpose_fill(Bv, cursor.p, BT.col.p, BT.val.p, st);
+  launch_sort_columns(ncols, BT.rp.p, BT.col.p, BT.val.p, st);
+}
+
 // ------------------------------------------------------------------------------------
 // filtered product: C^ = Alg4.1((self*A + A*B)/div, eps_g)   [K1, K2, K3, K6, K4]
 // A: local rows; B: rows covering every column of A.  C gets A's rows.
 // ------------------------------------------------------------------------------------
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
-                            double div, double eps_g, DCsr &C, StepReport &rep) {
+                            double div, double eps_g, DCsr &C, StepReport &rep,
+                            const DCsr *BT = nullptr) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   const int64_t nr = A.nrows;
@@ -351,6 +382,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   CK(cudaEventCreate(&e1));
   unsigned long long used = 0;
   w.fail_rows.ensure(nr1, st);
+  w.fail_rows2.ensure(nr1, st);
   w.fail_count.ensure(1, st);
   const int hash_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.hash_blocks_per_sm));
@@ -375,7 +407,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     CK(cudaMemsetAsync(w.fail_count.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
     int kern = P.o.kernel;
-    if (kern == 0) kern = self != 0.0 ? 5 : 1;
+    const bool taylor_pull_ok = self == 0.0 && BT != nullptr && BT->rp.p != nullptr;
+    if (kern == 0) kern = self != 0.0 ? 5 : (taylor_pull_ok ? 6 : 1);
+    if (kern == 6 && !taylor_pull_ok) kern = 1;
     int nfail = 0;
     if (kern == 2) {  // warp-per-row conflict-free window
       const int64_t gw = (int64_t)P.sm_count * P.warp_blocks_per_sm * kWarpRowWarpsPerCta;
@@ -395,31 +429,52 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       launch_numeric_warp(nw, st);
       CK(cudaGetLastError());
     } else {
-      if (kern == 1 || kern == 4 || kern == 5) {  // shared-memory accumulator over all rows
+      // staged chain: the chosen shared-memory kernel over all rows, rows it cannot hold
+      // go to the next one (pull -> hash -> block window; paged / k-sync / hash -> window)
+      const int32_t *list = na.order;
+      int64_t nlist = nr;
+      int32_t *fbuf[2] = {w.fail_rows.p, w.fail_rows2.p};
+      int fb = 0;
+      int stage = kern;
+      while (nlist > 0) {
         NumericArgs nh = na;
-        nh.grid = kern == 5 ? paged_grid : hash_grid;
-        nh.nlist = nr;
-        if (kern == 1) launch_numeric_hash(nh, w.fail_rows.p, w.fail_count.p, st);
-        else if (kern == 4) launch_numeric_ksync(nh, w.fail_rows.p, w.fail_count.p, st);
-        else launch_numeric_paged(nh, w.fail_rows.p, w.fail_count.p, st);
-        CK(cudaGetLastError());
-        nfail = d2h(w.fail_count.p, st);
-      }
-      const bool all_window = kern == 3;
-      if (nfail > 0 || all_window) {  // block-window kernel (hash overflow rows, or all)
-        w.cursor.ensure((size_t)na.grid * na.cursor_cap, st);
-        w.scr_col.ensure((size_t)na.grid * na.scr_cap, st);
-        w.scr_val.ensure((size_t)na.grid * na.scr_cap, st);
-        NumericArgs nw = na;
-        nw.cursor = w.cursor.p;
-        nw.scr_col = w.scr_col.p;
-        nw.scr_val = w.scr_val.p;
-        nw.order = all_window ? na.order : w.fail_rows.p;
-        nw.nlist = all_window ? nr : nfail;
-        nw.grid = (int)std::min<int64_t>(na.grid, nw.nlist);
+        nh.order = list;
+        nh.nlist = nlist;
         CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
-        launch_numeric(nw, st);
+        CK(cudaMemsetAsync(w.fail_count.p, 0, sizeof(int), st));
+        if (stage == 3) {
+          w.cursor.ensure((size_t)na.grid * na.cursor_cap, st);
+          w.scr_col.ensure((size_t)na.grid * na.scr_cap, st);
+          w.scr_val.ensure((size_t)na.grid * na.scr_cap, st);
+          nh.cursor = w.cursor.p;
+          nh.scr_col = w.scr_col.p;
+          nh.scr_val = w.scr_val.p;
+          nh.grid = (int)std::min<int64_t>(na.grid, nlist);
+          launch_numeric(nh, st);
+          CK(cudaGetLastError());
+          break;
+        }
+        int32_t *fout = fbuf[fb];
+        if (stage == 1) {
+          nh.grid = hash_grid;
+          launch_numeric_hash(nh, fout, w.fail_count.p, st);
+        } else if (stage == 4) {
+          nh.grid = hash_grid;
+          launch_numeric_ksync(nh, fout, w.fail_count.p, st);
+        } else if (stage == 5) {
+          nh.grid = paged_grid;
+          launch_numeric_paged(nh, fout, w.fail_count.p, st);
+        } else {  // 6
+          nh.grid = paged_grid;
+          launch_taylor_pull(nh, BT->view(), fout, w.fail_count.p, st);
+        }
         CK(cudaGetLastError());
+        const int nf = d2h(w.fail_count.p, st);
+        nfail += nf;
+        list = fout;
+        nlist = nf;
+        fb ^= 1;
+        stage = stage == 6 ? 1 : 3;
       }
     }
     rep.window_rows = nfail;
@@ -890,29 +945,12 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   double norm = 0.0;
   int symflags = 3;
   {
-    DBuf<int32_t> ccnt;
-    ccnt.alloc((size_t)P.n, st);
-    CK(cudaMemsetAsync(ccnt.p, 0, P.n * sizeof(int32_t), st));
-    launch_col_count(Hf.view(), ccnt.p, st);
-    DBuf<int64_t> cnt64, cp, cursor;
-    cnt64.alloc((size_t)P.n, st);
-    // widen counts (int32 -> int64) through the scan input
-    std::vector<int32_t> hc32((size_t)P.n);
-    CK(cudaMemcpyAsync(hc32.data(), ccnt.p, P.n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::vector<int64_t> hc64(hc32.begin(), hc32.end());
-    CK(cudaMemcpyAsync(cnt64.p, hc64.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    cp.alloc((size_t)P.n + 1, st);
-    w.scan_tmp.ensure((size_t)scan_tmp_elems(P.n) + 1, st);
-    launch_exclusive_scan(cnt64.p, P.n, cp.p, w.scan_tmp.p, st);
-    cursor.alloc((size_t)P.n, st);
-    CK(cudaMemcpyAsync(cursor.p, cp.p, P.n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    DBuf<int32_t> trow;
-    DBuf<double> tval, colsum;
-    trow.alloc((size_t)Hf.nnz, st);
-    tval.alloc((size_t)Hf.nnz, st);
-    launch_transpose_fill(Hf.view(), cursor.p, trow.p, tval.p, st);
-    launch_sort_columns(P.n, cp.p, trow.p, tval.p, st);
+    DCsr HT;
+    build_transpose(P, Hf.view(), P.n, HT);
+    DBuf<int64_t> &cp = HT.rp;
+    DBuf<int32_t> &trow = HT.col;
+    DBuf<double> &tval = HT.val;
+    DBuf<double> colsum;
     if (P.o.plan_norm == 0) {
       colsum.alloc((size_t)P.n, st);
       launch_col_abs_sum(P.n, cp.p, tval.p, colsum.p, st);
@@ -926,6 +964,8 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     norm = P.o.plan_norm == 0 ? s : sqrt(s);
     if (Hf.nnz == 0) norm = 0.0;
     symflags = d2h(w.flags.p, st);
+    // keep the transpose: H0^T (scaled below) feeds the Taylor pull kernel
+    P.H0T = std::move(HT);
   }
   P.norm = norm;
   int M, N;
@@ -947,6 +987,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   if (!P.o.filter) P.eps_g0 = 0.0;
   // H0 = H 2^-N (exact)
   launch_scale_pow2(Hf.val.p, Hf.nnz, -N, st);
+  launch_scale_pow2(P.H0T.val.p, P.H0T.nnz, -N, st);
   slice_rows(P, Hf, P.row_begin, P.row_end, P.H0loc);
   {
     std::vector<int64_t> hrp((size_t)P.n + 1);
@@ -1029,7 +1070,7 @@ static void do_run(sexpm_plan_s &P) {
     for (int i = 2; i <= P.M; i++) {
       CK(cudaEventRecord(a0, st));
       StepReport rep;
-      filtered_product(P, Sc.view(), P.H0full.view(), 0.0, (double)i, P.eps_g0, Sn, rep);
+      filtered_product(P, Sc.view(), P.H0full.view(), 0.0, (double)i, P.eps_g0, Sn, rep, &P.H0T);
       if (i < SEXPM_MAXSTEP) {
         S.taylor_nnz_unf[i] = rep.nnz_unf;
         S.taylor_nnz[i] = rep.nnz;
@@ -1413,7 +1454,10 @@ int sexpm_filtered_product(sexpm_plan_t p, const sexpm_csr_in *A, const sexpm_cs
   CsrView Av = view_of(A), Bv = view_of(B);
   StepReport rep;
   DCsr out;
-  filtered_product(*p, Av, Bv, self_coef, divisor, eps_g, out, rep);
+  DCsr BT;
+  const bool want_pull = self_coef == 0.0 && (p->o.kernel == 0 || p->o.kernel == 6);
+  if (want_pull) build_transpose(*p, Bv, A->n, BT);
+  filtered_product(*p, Av, Bv, self_coef, divisor, eps_g, out, rep, want_pull ? &BT : nullptr);
   p->E = std::move(out);
   p->have_result = true;  // sexpm_result_copy reads it; sexpm_stats_get is not updated
   C->n = A->n;

@@ -1323,6 +1323,7 @@ void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_co
 constexpr int kPages = 4096;
 constexpr int kSlots = 4096;
 constexpr int kMaxPageShift = 6;
+constexpr int kPF = 8;  // k-steps of B entries prefetched into registers
 
 int paged_smem_bytes() { return kSlots * 8 + kPages * 4 * 2; }
 
@@ -1424,48 +1425,81 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
       }
       __syncthreads();
       const int cn = nk - kc < kThreads ? nk - kc : kThreads;
-      int32_t pc = 0;
-      double pv = 0.0;
-      if (tid < s_len[0]) {
-        pc = a.B.col[s_start[0] + tid];
-        pv = a.B.val[s_start[0] + tid];
-      }
-      for (int kk = 0; kk < cn; kk++) {
-        const long long st0 = s_start[kk];
-        const int ln = s_len[kk];
-        const double av = s_av[kk];
-        const int32_t cc = pc;
-        const double cv = pv;
-        if (kk + 1 < cn) {
-          const int nl = s_len[kk + 1];
-          if (tid < nl) {
-            const long long ns = s_start[kk + 1];
-            pc = a.B.col[ns + tid];
-            pv = a.B.val[ns + tid];
-          }
-        }
-        if (tid < ln) {
-          int rel = cc - lo;
-          int b = page_slot(ptab, rel >> sh, psize, &s_slots);
-          if (b >= 0) {
-            const int o = b + (rel & (psize - 1));
-            vals[o] = __dadd_rn(vals[o], __dmul_rn(av, cv));
-          } else {
-            s_fail = 1;
-          }
-          for (int e = tid + kThreads; e < ln; e += kThreads) {
-            rel = a.B.col[st0 + e] - lo;
-            const double v = a.B.val[st0 + e];
-            b = page_slot(ptab, rel >> sh, psize, &s_slots);
-            if (b >= 0) {
-              const int o = b + (rel & (psize - 1));
-              vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v));
-            } else {
-              s_fail = 1;
+      // register ring: the first two entries (tid, tid + 256) of the next kPF k's
+      int32_t pc[kPF][2];
+      double pv[kPF][2];
+#pragma unroll
+      for (int d = 0; d < kPF; d++) {
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          pc[d][u] = 0;
+          pv[d][u] = 0.0;
+          if (d < cn) {
+            const int e = tid + u * kThreads;
+            if (e < s_len[d]) {
+              pc[d][u] = a.B.col[s_start[d] + e];
+              pv[d][u] = a.B.val[s_start[d] + e];
             }
           }
         }
-        __syncthreads();  // one writer per slot at any time (k -> k+1)
+      }
+      for (int kk0 = 0; kk0 < cn; kk0 += kPF) {
+#pragma unroll
+        for (int d = 0; d < kPF; d++) {
+          const int kk = kk0 + d;
+          if (kk < cn) {
+            const long long st0 = s_start[kk];
+            const int ln = s_len[kk];
+            const double av = s_av[kk];
+            const int32_t c0 = pc[d][0], c1 = pc[d][1];
+            const double v0 = pv[d][0], v1 = pv[d][1];
+            const int kn = kk + kPF;  // refill this ring slot
+            if (kn < cn) {
+              const int nl = s_len[kn];
+              const long long ns = s_start[kn];
+              if (tid < nl) {
+                pc[d][0] = a.B.col[ns + tid];
+                pv[d][0] = a.B.val[ns + tid];
+              }
+              if (tid + kThreads < nl) {
+                pc[d][1] = a.B.col[ns + tid + kThreads];
+                pv[d][1] = a.B.val[ns + tid + kThreads];
+              }
+            }
+            if (tid < ln) {
+              int rel = c0 - lo;
+              int b = page_slot(ptab, rel >> sh, psize, &s_slots);
+              if (b >= 0) {
+                const int o = b + (rel & (psize - 1));
+                vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v0));
+              } else {
+                s_fail = 1;
+              }
+              if (tid + kThreads < ln) {
+                rel = c1 - lo;
+                b = page_slot(ptab, rel >> sh, psize, &s_slots);
+                if (b >= 0) {
+                  const int o = b + (rel & (psize - 1));
+                  vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v1));
+                } else {
+                  s_fail = 1;
+                }
+              }
+              for (int e = tid + 2 * kThreads; e < ln; e += kThreads) {
+                rel = a.B.col[st0 + e] - lo;
+                const double v = a.B.val[st0 + e];
+                b = page_slot(ptab, rel >> sh, psize, &s_slots);
+                if (b >= 0) {
+                  const int o = b + (rel & (psize - 1));
+                  vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v));
+                } else {
+                  s_fail = 1;
+                }
+              }
+            }
+            __syncthreads();  // one writer per slot at any time (k -> k+1)
+          }
+        }
       }
     }
     __syncthreads();
@@ -1597,6 +1631,245 @@ void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_co
   cudaFuncSetAttribute(k_numeric_paged, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
   k_numeric_paged<<<a.grid, kThreads, smem, st>>>(a, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
+// K5p Taylor term by PULL: S~(r, j) = (sum_{k} s_rk h0_kj) / i  (Eq. 4.11).
+//
+// H0 rows are short (a few entries), so pushing them through an accumulator leaves most
+// lanes idle.  Instead the CTA (1) maps row r of S^ into a paged shared-memory table
+// (k -> s_rk), marking in a bitmap every column j reachable through H0's rows; (2) reads
+// the bitmap in column order to list the candidate columns (sorted, no sort needed);
+// (3) gives each candidate to one thread, which walks column j of H0 (the CSC copy H0^T
+// built at plan time, ascending k) and accumulates acc = acc + (s_rk * h0_kj) over the k
+// present in row r -- exactly the oracle's order, with _rn intrinsics: S~ is bit-identical
+// to the oracle's, and no two threads ever write the same value.  Rows that do not fit
+// the tables go to the push kernels (fail list).
+// ------------------------------------------------------------------------------------
+constexpr int kTPages = 4096;
+constexpr int kTSlots = 2048;
+constexpr int kTBitWords = 4096;
+constexpr int kTCand = 2048;
+
+int taylor_pull_smem_bytes() {
+  return kTSlots * 8 + kTCand * 8 + kTPages * 4 + kTBitWords * 4 + kTCand * 4;
+}
+
+__global__ void __launch_bounds__(kThreads) k_taylor_pull(NumericArgs a, CsrView BT,
+                                                          int32_t *fail_rows, int *fail_count) {
+  extern __shared__ double tsm[];
+  double *vals = tsm;                                                   // kTSlots
+  double *xval = vals + kTSlots;                                        // kTCand
+  int32_t *ptab = reinterpret_cast<int32_t *>(xval + kTCand);           // kTPages
+  unsigned *bits = reinterpret_cast<unsigned *>(ptab + kTPages);        // kTBitWords
+  int32_t *cand = reinterpret_cast<int32_t *>(bits + kTBitWords);       // kTCand
+  __shared__ int s_row, s_slots, s_fail;
+  __shared__ unsigned long long s_off;
+  __shared__ long long s_wsum[kWarps + 1];
+  __shared__ double s_fs[kWarps];
+  __shared__ long long s_nz[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kTSlots; i += kThreads) vals[i] = 0.0;
+  for (int i = tid; i < kTPages; i += kThreads) ptab[i] = -1;
+  for (int i = tid; i < kTBitWords; i += kThreads) bits[i] = 0u;
+  if (tid == 0) {
+    s_slots = 0;
+    s_fail = 0;
+  }
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int idx = s_row;
+    if (idx >= a.nlist) break;
+    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
+    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
+    const int32_t lo = a.lo[r], hi = a.hi[r];
+    if (hi < lo) {
+      if (tid == 0) {
+        a.row_off[r] = 0;
+        a.row_cnt[r] = 0;
+        a.row_fsum[r] = 0.0;
+        a.row_nnz[r] = 0;
+      }
+      continue;
+    }
+    const int32_t alo = a.A.col[pa0], ahi = a.A.col[pa1 - 1];
+    int sh = 4;
+    while ((((int64_t)ahi - alo) >> sh) >= kTPages) sh++;
+    const int nw = (int)(((int64_t)hi - lo) >> 5) + 1;
+    if (sh > kMaxPageShift || nw > kTBitWords) {
+      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+      continue;
+    }
+    const int psize = 1 << sh;
+    // (1) row r of S^ into the paged table; mark reachable columns
+    for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
+      const int32_t k = a.A.col[p];
+      const int rel = k - alo;
+      const int b = page_slot(ptab, rel >> sh, psize, &s_slots);
+      if (b >= 0 && b + psize <= kTSlots) vals[b + (rel & (psize - 1))] = a.A.val[p];
+      else s_fail = 1;
+      const int64_t kb = (int64_t)k - a.B.row0;
+      if (kb >= 0 && kb < a.B.nrows) {
+        for (int64_t q = a.B.rp[kb]; q < a.B.rp[kb + 1]; q++) {
+          const int jr = a.B.col[q] - lo;
+          atomicOr(&bits[jr >> 5], 1u << (jr & 31));
+        }
+      }
+    }
+    __syncthreads();
+    bool failed = s_fail != 0;
+    // (2) candidates in column order (contiguous word range per thread)
+    const int per = (nw + kThreads - 1) / kThreads;
+    const int w0 = tid * per < nw ? tid * per : nw;
+    const int w1 = w0 + per < nw ? w0 + per : nw;
+    int cnt = 0;
+    for (int i = w0; i < w1; i++) cnt += __popc(bits[i]);
+    int v = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULL_MASK, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) s_wsum[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      long long acc = 0;
+      for (int w = 0; w < kWarps; w++) {
+        long long t = s_wsum[w];
+        s_wsum[w] = acc;
+        acc += t;
+      }
+      s_wsum[kWarps] = acc;
+    }
+    __syncthreads();
+    const int ncand = (int)s_wsum[kWarps];
+    if (ncand > kTCand) failed = true;
+    {
+      int pos = (int)s_wsum[warp] + v - cnt;
+      for (int i = w0; i < w1; i++) {
+        unsigned m = bits[i];
+        bits[i] = 0u;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          if (!failed) cand[pos] = (i << 5) + b;
+          pos++;
+        }
+      }
+    }
+    __syncthreads();
+    // (3) pull: one thread per candidate column, ascending k along column j of H0
+    int nst_t = 0;
+    double fs = 0.0;
+    long long nnzu = 0;
+    if (!failed) {
+      for (int c = tid; c < ncand; c += kThreads) {
+        const int64_t j = (int64_t)lo + cand[c];
+        double acc = 0.0;
+        for (int64_t q = BT.rp[j]; q < BT.rp[j + 1]; q++) {
+          const int32_t k = BT.col[q];
+          if (k < alo || k > ahi) continue;
+          const int rel = k - alo;
+          const int b = ptab[rel >> sh];
+          if (b < 0) continue;
+          const double sv = vals[b + (rel & (psize - 1))];
+          if (sv == 0.0) continue;  // k not in row r: the oracle has no such product
+          acc = __dadd_rn(acc, __dmul_rn(sv, BT.val[q]));
+        }
+        const double x = acc / a.divisor;
+        xval[c] = x;
+        if (x != 0.0) {
+          nnzu++;
+          if (fabs(x) > a.floor_tau) nst_t++;
+          else fs += x * x;
+        }
+      }
+    }
+    // staged count: candidates are strided over threads, so count per 256-chunk in order
+    fs = warp_sum(fs);
+    nnzu = warp_sum(nnzu);
+    int nst_w = __reduce_add_sync(FULL_MASK, nst_t);
+    if (lane == 0) {
+      s_fs[warp] = fs;
+      s_nz[warp] = nnzu;
+      s_wsum[warp] = nst_w;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long tot = 0;
+      double f = 0.0;
+      long long z = 0;
+      for (int w = 0; w < kWarps; w++) {
+        tot += s_wsum[w];
+        f += s_fs[w];
+        z += s_nz[w];
+      }
+      s_wsum[kWarps] = tot;
+      s_fs[0] = f;
+      s_nz[0] = z;
+      s_off = failed ? 0ull : atomicAdd(a.pool_used, (unsigned long long)tot);
+    }
+    __syncthreads();
+    const long long total = s_wsum[kWarps];
+    const unsigned long long off = s_off;
+    const bool ok = !failed && (long long)off + total <= a.pool_cap;
+    if (ok) {  // ordered write: chunks of kThreads candidates, block-wide ballot scan
+      long long base = 0;
+      for (int c0 = 0; c0 < ncand; c0 += kThreads) {
+        const int c = c0 + tid;
+        const double x = c < ncand ? xval[c] : 0.0;
+        const bool st = c < ncand && x != 0.0 && fabs(x) > a.floor_tau;
+        const unsigned m = __ballot_sync(FULL_MASK, st);
+        __syncthreads();
+        if (lane == 0) s_wsum[warp] = __popc(m);
+        __syncthreads();
+        long long pre = 0, tot = 0;
+        for (int w = 0; w < kWarps; w++) {
+          if (w < warp) pre += s_wsum[w];
+          tot += s_wsum[w];
+        }
+        if (st) {
+          const long long q = (long long)off + base + pre + __popc(m & lanemask_lt());
+          a.pool_col[q] = lo + cand[c];
+          a.pool_val[q] = x;
+        }
+        base += tot;
+      }
+    }
+    __syncthreads();
+    // reset the paged table (slots of row r's k, then the page entries)
+    for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
+      const int rel = a.A.col[p] - alo;
+      const int b = ptab[rel >> sh];
+      if (b >= 0 && b + psize <= kTSlots) vals[b + (rel & (psize - 1))] = 0.0;
+    }
+    __syncthreads();
+    for (int64_t p = pa0 + tid; p < pa1; p += kThreads) ptab[(a.A.col[p] - alo) >> sh] = -1;
+    if (tid == 0) {
+      if (failed) {
+        fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+      } else {
+        if (!ok) atomicOr(a.flags, 1);
+        a.row_off[r] = (int64_t)off;
+        a.row_cnt[r] = total;
+        a.row_fsum[r] = s_fs[0];
+        a.row_nnz[r] = s_nz[0];
+      }
+      s_slots = 0;
+      s_fail = 0;
+    }
+  }
+}
+
+void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_rows,
+                        int *fail_count, cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  int smem = taylor_pull_smem_bytes();
+  cudaFuncSetAttribute(k_taylor_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_taylor_pull<<<a.grid, kThreads, smem, st>>>(a, BT, fail_rows, fail_count);
 }
 
 // ------------------------------------------------------------------------------------

@@ -106,6 +106,10 @@ void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_co
 int paged_smem_bytes();
 void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
                           cudaStream_t st);
+// Taylor term by pull over H0^T (bit-identical order); BT = CSC of B (= B^T as CSR)
+int taylor_pull_smem_bytes();
+void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_rows,
+                        int *fail_count, cudaStream_t st);
 // hash-accumulator variant; rows whose table over-fills are appended to fail_rows
 int hash_smem_bytes();
 void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,

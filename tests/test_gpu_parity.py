@@ -260,7 +260,7 @@ def test_alg41_random_vs_oracle(B):
         assert d == pytest.approx(dropped_o, rel=1e-10, abs=1e-300)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("name", ["heat2d_pm10_20", "structural_24", "heat3d_9", "banded_nonsym"])
 def test_accumulator_variants(B, kernel, name):
     """Every K3 accumulator (hash, warp-window, block-window) meets parity."""
@@ -284,3 +284,19 @@ def test_warp_window_bit_exact_products(B, seed):
     G = from_dev(n, rp, ci, va)
     assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
     assert np.array_equal(G.val, Ct.val)  # bit-exact
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_taylor_pull_bit_exact(B, seed):
+    """A Taylor term S~ = S^ H0 / i through the pull kernel equals the oracle bit for bit
+    (ascending k along H0's columns, _rn products and sums, then / i)."""
+    import torch
+    from synth import laplacian_2d
+    H = laplacian_2d(30, 30, 0.4, "pm10", seed=seed)
+    S = O.spgemm(H, H, 0.0, 2.0)  # a realistic S^_2
+    (g_rp, g_ci, g_va), passes, tau, nu = B.sexpm_filtered_product(H.n, to_dev(S), to_dev(H),
+                                                                   0.0, 3.0, 0.0)
+    G = from_dev(H.n, g_rp, g_ci, g_va)
+    Ct = O.spgemm(S, H, 0.0, 3.0)
+    assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
+    assert np.array_equal(G.val, Ct.val)
