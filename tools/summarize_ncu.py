@@ -76,7 +76,8 @@ def launches(path):
     for r in rows[hdr + 1:]:
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
-        scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[ui], 1.0)
+        scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
+                 "msecond": 1.0, "s": 1e3, "second": 1e3}.get(r[ui].strip(), 1.0)
         name = r[ki].split("(")[0]
         tot[name] += float(r[vi].replace(",", "")) * scale
         cnt[name] += 1
