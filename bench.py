@@ -270,9 +270,12 @@ def main():
             h = B.sexpm_plan_host(Hin, args.eps_tol, o)
             E = B.sexpm_run(h)
             if outbufs is None or outbufs[1].numel() < E.nnz:
+                if it > 0:  # never copy into a buffer that is too small
+                    e2e_times = []
+                cap = int(E.nnz * 1.01) + 1024
                 outbufs = (torch.empty(r1 - r0 + 1, dtype=torch.int64).pin_memory(),
-                           torch.empty(max(E.nnz, 1), dtype=torch.int32).pin_memory(),
-                           torch.empty(max(E.nnz, 1), dtype=torch.float64).pin_memory())
+                           torch.empty(cap, dtype=torch.int32).pin_memory(),
+                           torch.empty(cap, dtype=torch.float64).pin_memory())
                 if it == 0:
                     B.sexpm_destroy(h)
                     continue  # first pass only sizes the pinned buffers
@@ -332,6 +335,13 @@ def main():
         "phase_ms": {"plan": float(st["ms_plan"]), "taylor": float(st["ms_taylor"]),
                      "squaring": float(st["ms_squaring"]), "finalize": float(st["ms_finalize"])},
         "roofline": roof,
+        "steps_detail": [{"ms": times[j], "retries": int(stats[j]["retries"]),
+                          "taylor_ms": float(stats[j]["ms_taylor"]),
+                          "sq_numeric_ms": [float(x) for x in stats[j]["sq_numeric_ms"][1:N + 1]],
+                          "sq_first_ms": [float(x) for x in stats[j]["sq_first_ms"][1:N + 1]],
+                          "sq_fallback_rows": [int(x) for x in stats[j]["sq_fallback_rows"][1:N + 1]],
+                          "cache_misses": int(stats[j]["cache_misses"])}
+                         for j in range(len(stats))],
         "gpu_launches": int(launches),
         "e2e": e2e,
     }

@@ -25,7 +25,7 @@ EXPORTED = [
     "sexpm_nccl_comm_destroy", "sexpm_plan", "sexpm_plan_host", "sexpm_run",
     "sexpm_result_copy", "sexpm_stats_get", "sexpm_destroy", "sexpm_last_error",
     "sexpm_filtered_product", "sexpm_alg41", "sexpm_halo_ranges", "sexpm_partition_rows",
-    "sexpm_abi_sizes", "sexpm_kernel_launches",
+    "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache",
 ]
 
 
@@ -76,7 +76,12 @@ class Stats(C.Structure):
                 ("ms_plan", C.c_double), ("ms_taylor", C.c_double), ("ms_squaring", C.c_double),
                 ("ms_finalize", C.c_double), ("ms_total", C.c_double),
                 ("taylor_bytes", C.c_double), ("taylor_fmas", C.c_double),
-                ("nnz_out", C.c_int64), ("gpu_launches", C.c_int32), ("retries", C.c_int32)]
+                ("nnz_out", C.c_int64), ("gpu_launches", C.c_int32), ("retries", C.c_int32),
+                ("taylor_fallback_rows", _I64), ("sq_fallback_rows", _I64), ("sq_first_ms", _F64),
+                ("sq_group_prof", C.c_double * 8 * MAXSTEP),
+                ("cache_hits", C.c_int64), ("cache_misses", C.c_int64),
+                ("cache_releases", C.c_int64), ("cache_bytes_cached", C.c_double),
+                ("cache_bytes_allocated", C.c_double)]
 
 
 _lib = None
@@ -184,7 +189,7 @@ def sexpm_stats_get(h) -> dict:
     d = {}
     for k, _ in Stats._fields_:
         v = getattr(s, k)
-        d[k] = np.array(v[:]) if hasattr(v, "_length_") else v
+        d[k] = np.ctypeslib.as_array(v).copy() if hasattr(v, "_length_") else v
     return d
 
 
@@ -197,6 +202,10 @@ def sexpm_kernel_launches() -> int:
 def sexpm_destroy(h):
     if h:
         _check(lib().sexpm_destroy(h))
+
+
+def sexpm_release_cache():
+    _check(lib().sexpm_release_cache())
 
 
 def sexpm_nccl_unique_id() -> bytes:
@@ -316,6 +325,8 @@ def expm_host(n, rowptr: np.ndarray, col: np.ndarray, val: np.ndarray, eps_tol=1
         if out is None:
             out = (np.empty(rows + 1, np.int64), np.empty(max(E.nnz, 1), np.int32),
                    np.empty(max(E.nnz, 1), np.float64))
+        if out[0].size < rows + 1 or out[1].size < E.nnz or out[2].size < E.nnz:
+            raise ValueError(f"output buffers too small for nnz(E) = {E.nnz}")
         sexpm_result_copy(h, out[0].ctypes.data, out[1].ctypes.data, out[2].ctypes.data)
         st = sexpm_stats_get(h)
         return (out[0], out[1][:E.nnz], out[2][:E.nnz]), st
@@ -324,28 +335,37 @@ def expm_host(n, rowptr: np.ndarray, col: np.ndarray, val: np.ndarray, eps_tol=1
 
 
 _ctx = None
+_ctx_kernel = {}
 
 
-def _context():
-    """A plan on a 1x1 zero matrix: the device/stream context of the component entry points."""
+def _context(kernel=0):
+    """A plan on a 1x1 zero matrix: the device/stream context of the component entry points
+    (one per accumulator choice `kernel`, see sexpm_options.kernel)."""
     global _ctx
     torch = _torch()
-    if _ctx is None:
-        dev = torch.device("cuda", torch.cuda.current_device())
-        rp = torch.zeros(2, dtype=torch.int64, device=dev)
-        ci = torch.zeros(1, dtype=torch.int32, device=dev)
-        va = torch.zeros(1, dtype=torch.float64, device=dev)
-        o = sexpm_options_init()
-        o.stream = torch.cuda.current_stream().cuda_stream
-        _ctx = sexpm_plan(_csr_in(1, rp, ci, va), 1e-16, o)
-    return _ctx
+    if kernel == 0 and _ctx is not None:
+        return _ctx
+    if kernel in _ctx_kernel:
+        return _ctx_kernel[kernel]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rp = torch.zeros(2, dtype=torch.int64, device=dev)
+    ci = torch.zeros(1, dtype=torch.int32, device=dev)
+    va = torch.zeros(1, dtype=torch.float64, device=dev)
+    o = sexpm_options_init(kernel=kernel)
+    o.stream = torch.cuda.current_stream().cuda_stream
+    h = sexpm_plan(_csr_in(1, rp, ci, va), 1e-16, o)
+    if kernel == 0:
+        _ctx = h
+    else:
+        _ctx_kernel[kernel] = h
+    return h
 
 
-def sexpm_filtered_product(n, A, B, self_coef, divisor, eps_g):
+def sexpm_filtered_product(n, A, B, self_coef, divisor, eps_g, kernel=0):
     """One filtered product (K1-K4) on the GPU. A, B = (rowptr, col, val) device tensors.
     Returns ((rowptr, col, val) tensors, passes, tau, nnz_unf)."""
     torch = _torch()
-    h = _context()
+    h = _context(kernel)
     Ai = _csr_in(n, *A)
     Bi = _csr_in(n, *B)
     out = CsrOut()

@@ -14,6 +14,10 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -104,22 +108,146 @@ static NcclApi &nccl() {
 // ------------------------------------------------------------------------------------
 // device buffers (stream-ordered allocator)
 // ------------------------------------------------------------------------------------
+// Process-wide cache of device blocks.  Every plan grows its iterates and staging pool
+// as the terms fill in, and a new plan starts empty; mapping fresh memory through the
+// stream-ordered pool costs ~20-30 ms per GB, so freed blocks are kept here and handed
+// to later requests (best fit within 2x).  A block freed while its stream still has work
+// queued is reused only on that stream (stream order makes that safe); blocks freed after
+// a synchronize (sexpm_destroy) are idle and reusable on any stream.
+namespace cache {
+struct Block {
+  void *p;
+  size_t bytes;
+  cudaStream_t st;  // nullptr: idle (no pending work)
+  int dev;
+};
+static std::mutex mu;
+static std::multimap<size_t, Block> free_blocks;
+static long long hits = 0, misses = 0, releases = 0;
+static double bytes_cached = 0.0, bytes_allocated = 0.0;
+static size_t budget = 0;  // cap on bytes_allocated: 90% of the device memory
+static thread_local bool freeing_idle = false;
+// size each role-tagged buffer (iterates, staging pool) reached in the latest plan: a new
+// plan asks for that size first, so repeated e^H of similar matrices never grow in steps
+constexpr int kRoles = 32;
+static size_t role_hint[kRoles] = {0};
+static size_t round_bytes(size_t b) {
+  const size_t g = b >= ((size_t)1 << 24) ? ((size_t)1 << 21) : 512;
+  return (b + g - 1) / g * g;
+}
+static void free_block(const Block &b, cudaStream_t fallback) {  // mu held
+  cudaFreeAsync(b.p, b.st ? b.st : fallback);
+  bytes_allocated -= (double)b.bytes;
+  bytes_cached -= (double)b.bytes;
+}
+static void release_all() {
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &kv : free_blocks) {
+    if (kv.second.st) cudaFreeAsync(kv.second.p, kv.second.st);
+    else cudaFree(kv.second.p);
+    bytes_allocated -= (double)kv.first;
+  }
+  free_blocks.clear();
+  bytes_cached = 0.0;
+  releases++;
+}
+// blocks whose stream has just been synchronized carry no pending work
+static void mark_idle(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &kv : free_blocks)
+    if (kv.second.st == st) kv.second.st = nullptr;
+}
+static bool take(size_t lo, size_t hi, cudaStream_t st, int dev, void **p, size_t *got) {
+  for (auto it = free_blocks.lower_bound(lo); it != free_blocks.end() && it->first <= hi; ++it) {
+    if (it->second.dev == dev && (it->second.st == st || it->second.st == nullptr)) {
+      *p = it->second.p;
+      *got = it->first;
+      bytes_cached -= (double)it->first;
+      free_blocks.erase(it);
+      hits++;
+      return true;
+    }
+  }
+  return false;
+}
+static void *alloc(size_t bytes, cudaStream_t st, size_t *got, size_t hint) {
+  bytes = round_bytes(bytes);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  void *p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (budget == 0) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      budget = (size_t)(0.90 * (double)tot);
+    }
+    if (hint > bytes) {
+      hint = round_bytes(hint);
+      if (take(hint, 2 * hint + ((size_t)1 << 21), st, dev, &p, got)) return p;
+    }
+    if (take(bytes, 2 * bytes + ((size_t)1 << 21), st, dev, &p, got)) return p;
+    // miss: make room under the budget by returning the largest cached blocks to the pool
+    while (!free_blocks.empty() && bytes_allocated + (double)bytes > (double)budget) {
+      auto it = std::prev(free_blocks.end());
+      free_block(it->second, st);
+      free_blocks.erase(it);
+    }
+  }
+  cudaError_t e = cudaMallocAsync(&p, bytes, st);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    cudaStreamSynchronize(st);
+    release_all();
+    cudaDeviceSynchronize();
+    e = cudaMallocAsync(&p, bytes, st);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw SxError{e == cudaErrorMemoryAllocation ? SEXPM_ENOMEM : SEXPM_ECUDA,
+                  std::string("device allocation of ") + std::to_string(bytes) + " bytes: " +
+                      cudaGetErrorString(e)};
+  }
+  *got = bytes;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    misses++;
+    bytes_allocated += (double)bytes;
+  }
+  return p;
+}
+static void free(void *p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  free_blocks.emplace(bytes, Block{p, bytes, freeing_idle ? nullptr : st, dev});
+  bytes_cached += (double)bytes;
+}
+}  // namespace cache
+
 template <typename T>
 struct DBuf {
   T *p = nullptr;
   size_t n = 0;
+  size_t bytes = 0;
   cudaStream_t st = nullptr;
+  int role = -1;      // cache::role_hint slot (large growing buffers), -1 none
+  bool grown = false;  // allocated at least once in this plan
   void release() {
-    if (p) cudaFreeAsync(p, st);
+    if (p) cache::free(p, bytes, st);
     p = nullptr;
     n = 0;
+    bytes = 0;
   }
   void alloc(size_t cnt, cudaStream_t s) {
     release();
     st = s;
     if (cnt == 0) cnt = 1;
-    CK(cudaMallocAsync(reinterpret_cast<void **>(&p), cnt * sizeof(T), s));
-    n = cnt;
+    const size_t hint = (role >= 0 && !grown) ? cache::role_hint[role] : 0;
+    p = reinterpret_cast<T *>(cache::alloc(cnt * sizeof(T), s, &bytes, hint));
+    n = bytes / sizeof(T);
+    grown = true;
+    if (role >= 0) cache::role_hint[role] = bytes;
   }
   // grow-only: reuse the buffer when it is large enough, else grow by 1.25x (fewer
   // stream-ordered re-allocations as the iterates fill in)
@@ -135,9 +263,12 @@ struct DBuf {
       release();
       p = o.p;
       n = o.n;
+      bytes = o.bytes;
       st = o.st;
+      grown = o.grown;  // role stays with the slot (swap_csr keeps roles per slot)
       o.p = nullptr;
       o.n = 0;
+      o.bytes = 0;
     }
     return *this;
   }
@@ -185,18 +316,22 @@ struct StepReport {
   float numeric_ms = 0.f;
   double numeric_bytes = 0.0;
   int64_t window_rows = 0;
+  float first_ms = 0.f;  // the first kernel of the fallback chain alone
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // grouped kernel phase clocks
 };
 
 struct Workspace {
   DBuf<int32_t> lo, hi, order, bin_cnt, bin_off;
   DBuf<int64_t> prod, bound, row_off, row_cnt, row_nnz, cnt, scan_tmp, l1r, l2r, i64tmp;
-  DBuf<double> row_fsum, rs, partial, scal;
+  DBuf<double> row_fsum, rs, partial, scal, passrow;
   DBuf<int64_t> cursor;
   DBuf<int32_t> scr_col, pool_col;
   DBuf<double> scr_val, pool_val;
   DBuf<unsigned long long> pool_used;
   DBuf<int> row_counter, flags, fail_count;
   DBuf<int32_t> fail_rows, fail_rows2;
+  DBuf<int8_t> ident;
+  DBuf<unsigned long long> prof;
   int64_t pool_cap_hint = 0;
 };
 
@@ -213,6 +348,15 @@ struct sexpm_plan_s {
   DCsr H0full;  // H0 = H 2^-N, all n rows (replicated)
   DCsr H0loc;   // this rank's rows of H0
   DCsr H0T;     // H0^T (CSC of H0, columns sorted by row) for the Taylor pull kernel
+  // H0 as diagonals (when it has at most kDiaMax distinct offsets) for the Taylor push kernel
+  int dia_nd = 0;
+  int32_t dia_dmin = 0, dia_dmax = 0;
+  DBuf<int32_t> dia_off;
+  DBuf<double> dia_val;
+  DBuf<unsigned long long> dia_prod;
+  int dia_slots = 1152;
+  int group_slots = 4096;
+  long long cache0[3] = {0, 0, 0};  // cache counters when the plan was created
   DCsr T, Tn, S, Sn, Bhalo, Ibuf, E;  // persistent (grow-only) iterates
   int32_t retries = 0;
   DBuf<int32_t> proc_order;  // K3 row processing order (cluster order of H's graph)
@@ -223,6 +367,7 @@ struct sexpm_plan_s {
   Workspace ws;
   sexpm_stats stats{};
   int sm_count = 148;
+  size_t smem_per_sm = 233472;
   int numeric_blocks_per_sm = 2;
   int hash_blocks_per_sm = 4;
   int warp_blocks_per_sm = 4;
@@ -308,7 +453,7 @@ static void build_transpose(sexpm_plan_s &P, const CsrView &Bv, int64_t ncols, D
 // ------------------------------------------------------------------------------------
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
                             double div, double eps_g, DCsr &C, StepReport &rep,
-                            const DCsr *BT = nullptr) {
+                            const DCsr *BT = nullptr, bool add_identity = false) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   const int64_t nr = A.nrows;
@@ -322,6 +467,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   w.row_cnt.ensure(nr1, st);
   w.row_nnz.ensure(nr1, st);
   w.row_fsum.ensure(nr1, st);
+  w.passrow.ensure(nr1, st);
   w.cnt.ensure(nr1, st);
   w.rs.ensure(nr1, st);
   w.l1r.ensure(nr1, st);
@@ -336,20 +482,32 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   w.row_counter.ensure(1, st);
   w.flags.ensure(1, st);
 
-  // K1 symbolic bounds
-  launch_symbolic(A, B, self != 0.0 ? 1 : 0, w.lo.p, w.hi.p, w.prod.p, w.bound.p, st);
-  launch_reduce_sum_i64(w.bound.p, nr, w.i64tmp.p + 0, st);
-  launch_reduce_max_i64(w.bound.p, nr, w.i64tmp.p + 1, st);
-  launch_reduce_sum_i64(w.prod.p, nr, w.i64tmp.p + 2, st);
-  // longest A row (cursor scratch size)
-  launch_row_lengths(A.rp, nr, w.cnt.p, st);
-  launch_reduce_max_i64(w.cnt.p, nr, w.i64tmp.p + 6, st);
-  int64_t hstat[8];
-  CK(cudaMemcpyAsync(hstat, w.i64tmp.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  const int64_t maxk = hstat[6];
-  const double Kglob = allsum(P, (double)hstat[0]);
-  const int64_t maxb = hstat[1];
+  // Taylor term with a diagonal H0: the push kernel K5d needs no symbolic pass; every
+  // product count is bounded by ndiag * nnz(A), a valid K for the floor lemma
+  const bool dia_path = self == 0.0 && P.dia_nd > 0 && B.rp == P.H0full.rp.p &&
+                        (P.o.kernel == 0 || P.o.kernel == 7);
+  int64_t hstat[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool have_symbolic = false;
+  auto run_symbolic = [&]() {  // K1 symbolic bounds
+    launch_symbolic(A, B, self != 0.0 ? 1 : 0, w.lo.p, w.hi.p, w.prod.p, w.bound.p, st);
+    launch_reduce_sum_i64(w.bound.p, nr, w.i64tmp.p + 0, st);
+    launch_reduce_max_i64(w.bound.p, nr, w.i64tmp.p + 1, st);
+    launch_reduce_sum_i64(w.prod.p, nr, w.i64tmp.p + 2, st);
+    // longest A row (cursor scratch size)
+    launch_row_lengths(A.rp, nr, w.cnt.p, st);
+    launch_reduce_max_i64(w.cnt.p, nr, w.i64tmp.p + 6, st);
+    CK(cudaMemcpyAsync(hstat, w.i64tmp.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    have_symbolic = true;
+  };
+  double Kglob;
+  if (dia_path) {
+    hstat[0] = (int64_t)P.dia_nd * A.nnz;
+    Kglob = allsum(P, (double)hstat[0]);
+  } else {
+    run_symbolic();
+    Kglob = allsum(P, (double)hstat[0]);
+  }
   rep.fmas = (double)hstat[2];
   const double floor_tau = (eps_g > 0.0 && Kglob > 0.0) ? eps_g / sqrt(Kglob) : 0.0;
 
@@ -357,7 +515,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   // else longest-processing-time-first bins
   const bool use_cluster = P.proc_order.p && (int64_t)P.proc_order.n >= nr && A.row0 == P.row_begin &&
                            nr == P.row_end - P.row_begin;
-  if (!use_cluster) launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
+  if (!use_cluster && have_symbolic)
+    launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
 
   // K3 numeric
   NumericArgs na;
@@ -368,18 +527,20 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   na.floor_tau = floor_tau;
   na.lo = w.lo.p;
   na.hi = w.hi.p;
-  na.order = use_cluster ? P.proc_order.p : w.order.p;
+  na.order = use_cluster ? P.proc_order.p : (have_symbolic ? w.order.p : nullptr);
   na.window = P.o.window_cols > 0 ? P.o.window_cols : 8192;
   na.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.numeric_blocks_per_sm));
-  na.cursor_cap = std::max<int64_t>(maxk, 1);
-  na.scr_cap = std::max<int64_t>(maxb, 1);
+  na.cursor_cap = std::max<int64_t>(hstat[6], 1);
+  na.scr_cap = std::max<int64_t>(hstat[1], 1);
   int64_t cap = std::max<int64_t>(w.pool_cap_hint, (self != 0.0 ? 3 : 2) * A.nnz + 2 * nr + 1024);
   double sum_bound = 0;  // exact upper bound
   sum_bound = (double)hstat[0];
   if ((double)cap > sum_bound) cap = (int64_t)sum_bound + 1;
-  cudaEvent_t e0, e1;
+  cudaEvent_t e0, e1, e_first;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e_first));
+  bool have_first = false;
   unsigned long long used = 0;
   w.fail_rows.ensure(nr1, st);
   w.fail_rows2.ensure(nr1, st);
@@ -393,7 +554,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     w.pool_val.ensure((size_t)cap, st);
     na.pool_col = w.pool_col.p;
     na.pool_val = w.pool_val.p;
-    na.pool_cap = (int64_t)w.pool_col.n;
+    na.pool_cap = (int64_t)std::min(w.pool_col.n, w.pool_val.n);
     na.pool_used = w.pool_used.p;
     na.row_off = w.row_off.p;
     na.row_cnt = w.row_cnt.p;
@@ -408,8 +569,13 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     CK(cudaEventRecord(e0, st));
     int kern = P.o.kernel;
     const bool taylor_pull_ok = self == 0.0 && BT != nullptr && BT->rp.p != nullptr;
-    if (kern == 0) kern = self != 0.0 ? 5 : (taylor_pull_ok ? 6 : 1);
+    // the grouped kernel stages B rows with TMA bulk copies: 16-byte aligned B arrays
+    const bool group_ok = ((uintptr_t)B.col % 16 == 0) && ((uintptr_t)B.val % 16 == 0);
+    if (kern == 0) kern = self != 0.0 ? (group_ok ? 8 : 5) : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
+    if (kern == 8 && !group_ok) kern = 5;
+    if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 1;
     if (kern == 6 && !taylor_pull_ok) kern = 1;
+    if (kern == 7) CK(cudaMemsetAsync(P.dia_prod.p, 0, sizeof(unsigned long long), st));
     int nfail = 0;
     if (kern == 2) {  // warp-per-row conflict-free window
       const int64_t gw = (int64_t)P.sm_count * P.warp_blocks_per_sm * kWarpRowWarpsPerCta;
@@ -436,7 +602,13 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       int32_t *fbuf[2] = {w.fail_rows.p, w.fail_rows2.p};
       int fb = 0;
       int stage = kern;
+      bool first = true;
       while (nlist > 0) {
+        if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
+          run_symbolic();
+          na.cursor_cap = std::max<int64_t>(hstat[6], 1);
+          na.scr_cap = std::max<int64_t>(hstat[1], 1);
+        }
         NumericArgs nh = na;
         nh.order = list;
         nh.nlist = nlist;
@@ -464,17 +636,44 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         } else if (stage == 5) {
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
+        } else if (stage == 8) {
+          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kGroupRows - 1) / kGroupRows,
+                                                                (int64_t)P.sm_count));
+          w.prof.ensure(8, st);
+          CK(cudaMemsetAsync(w.prof.p, 0, 8 * sizeof(unsigned long long), st));
+          nh.prof = w.prof.p;
+          if (const char *e = getenv("SEXPM_DEBUG_GROUP")) nh.dbg = atoi(e);
+          launch_numeric_group(nh, P.group_slots, fout, w.fail_count.p, st);
+          CK(cudaMemcpyAsync(rep.prof, w.prof.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        } else if (stage == 7) {
+          DiaView D;
+          D.ndiag = P.dia_nd;
+          D.off = P.dia_off.p;
+          D.val = P.dia_val.p;
+          D.n = P.n;
+          D.dmin = P.dia_dmin;
+          D.dmax = P.dia_dmax;
+          D.prod_count = P.dia_prod.p;
+          const int per_sm = std::max(1, std::min(16, (int)(P.smem_per_sm / (taylor_dia_smem_bytes(P.dia_slots) + 1024))));
+          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kDiaWarpsPerCta - 1) / kDiaWarpsPerCta,
+                                                                (int64_t)P.sm_count * per_sm));
+          launch_taylor_dia(nh, D, P.dia_slots, fout, w.fail_count.p, st);
         } else {  // 6
           nh.grid = paged_grid;
           launch_taylor_pull(nh, BT->view(), fout, w.fail_count.p, st);
         }
         CK(cudaGetLastError());
+        if (first) {
+          CK(cudaEventRecord(e_first, st));
+          first = false;
+          have_first = true;
+        }
         const int nf = d2h(w.fail_count.p, st);
         nfail += nf;
         list = fout;
         nlist = nf;
         fb ^= 1;
-        stage = stage == 6 ? 1 : 3;
+        stage = stage == 7 ? (taylor_pull_ok ? 6 : 1) : (stage == 6 ? 1 : (stage == 8 ? 5 : 3));
       }
     }
     rep.window_rows = nfail;
@@ -490,6 +689,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     P.retries++;
   }
   CK(cudaEventElapsedTime(&rep.numeric_ms, e0, e1));
+  rep.first_ms = rep.numeric_ms;
+  if (have_first) CK(cudaEventElapsedTime(&rep.first_ms, e0, e_first));
+  cudaEventDestroy(e_first);
+  if (dia_path && !have_symbolic && rep.window_rows == 0) rep.fmas = (double)d2h(P.dia_prod.p, st);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   w.pool_cap_hint = std::max<int64_t>(w.pool_cap_hint, (int64_t)(1.2 * (double)used));
@@ -522,7 +725,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     while (b > lim) {
       epsf = eg / m;
       const double tau_d = (double)epsf;
-      launch_alg41_pass(w.pool_val.p, (int64_t)used, tau_d, w.partial.p, w.scal.p + 1, st);
+      launch_alg41_pass_rows(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p,
+                             w.partial.p, w.scal.p + 1, st);
       const double S = allsum(P, d2h(w.scal.p + 1, st));
       b = sqrtl((long double)F + (long double)S);
       m = b / epsf;
@@ -534,8 +738,15 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   rep.passes = passes;
   rep.tau = tau;
 
-  // K4 compaction + fused row statistics
-  launch_compact_count(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau, w.cnt.p, st);
+  // K4 compaction + fused row statistics (+ E = I + T^_N on the last squaring)
+  if (add_identity) {
+    w.ident.ensure(nr1, st);
+    launch_compact_count_ident(nr, A.row0, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p,
+                               tau, w.cnt.p, w.ident.p, st);
+    launch_count_ident(w.ident.p, nr, w.i64tmp.p + 6, st);
+  } else {
+    launch_compact_count(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau, w.cnt.p, st);
+  }
   DCsr &out = C;  // must not alias A or B
   out.nrows = nr;
   out.row0 = A.row0;
@@ -545,14 +756,22 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   out.col.ensure((size_t)out.nnz, st);
   out.val.ensure((size_t)out.nnz, st);
   launch_compact_write(nr, A.row0, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
-                       out.rp.p, out.col.p, out.val.p, w.rs.p, w.l1r.p, w.l2r.p, st);
+                       out.rp.p, out.col.p, out.val.p, w.rs.p, w.l1r.p, w.l2r.p, st,
+                       add_identity ? w.ident.p : nullptr);
   launch_reduce_sum(w.rs.p, nr, w.partial.p, w.scal.p + 2, st);
   launch_reduce_max_i64(w.l1r.p, nr, w.i64tmp.p + 4, st);
   launch_reduce_max_i64(w.l2r.p, nr, w.i64tmp.p + 5, st);
   rep.normIT2 = allsum(P, d2h(w.scal.p + 2, st));
   rep.l1 = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 4, st));
   rep.l2 = (int64_t)allmax(P, (double)d2h(w.i64tmp.p + 5, st));
-  rep.nnz = (int64_t)allsum(P, (double)out.nnz);
+  int64_t nnz_T = out.nnz;  // nnz of the filtered iterate itself
+  if (add_identity) {
+    int64_t ins_pur[2];
+    CK(cudaMemcpyAsync(ins_pur, w.i64tmp.p + 6, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    nnz_T = out.nnz - ins_pur[0] + ins_pur[1];
+  }
+  rep.nnz = (int64_t)allsum(P, (double)nnz_T);
 }
 
 // C = A + B (same rows)
@@ -807,6 +1026,9 @@ static void cluster_order(const std::vector<int64_t> &rp, const std::vector<int3
         }
       }
     }
+    // rows of a cluster in index order: neighbours in the processing order are then mostly
+    // neighbours in the matrix (the grouped kernel shares their B rows)
+    std::sort(q.begin(), q.end());
     order.insert(order.end(), q.begin(), q.end());
   }
 }
@@ -858,6 +1080,44 @@ static bool plan_MN(double norm, double eps_tol, int m_cap, int n_window, int &M
   M = bM;
   N = bN;
   return true;
+}
+
+// Diagonal offsets of H0 (d = j - k over all entries); when there are at most kDiaMax of
+// them the Taylor terms use the diagonal push kernel K5d (grid stencils have 3 / 5 / 7).
+static void build_diagonals(sexpm_plan_s &P) {
+  cudaStream_t st = P.st;
+  P.dia_nd = 0;
+  const DCsr &Hf = P.H0full;
+  if (Hf.nnz == 0 || P.o.kernel != 0 && P.o.kernel != 7) return;
+  const int64_t nbits = 2 * P.n - 1, nwords = (nbits + 31) / 32;
+  DBuf<unsigned> bits;
+  bits.alloc((size_t)nwords, st);
+  CK(cudaMemsetAsync(bits.p, 0, nwords * sizeof(unsigned), st));
+  launch_mark_offsets(Hf.view(), bits.p, P.n, st);
+  std::vector<unsigned> hb((size_t)nwords);
+  CK(cudaMemcpyAsync(hb.data(), bits.p, nwords * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int32_t> offs;
+  for (int64_t w = 0; w < nwords && (int)offs.size() <= kDiaMax; w++) {
+    unsigned m = hb[w];
+    while (m) {
+      const int b = __builtin_ctz(m);
+      m &= m - 1;
+      offs.push_back((int32_t)(w * 32 + b - (P.n - 1)));
+    }
+  }
+  if (offs.empty() || (int)offs.size() > kDiaMax) return;
+  std::sort(offs.begin(), offs.end(), std::greater<int32_t>());  // descending: k ascending per column
+  P.dia_nd = (int)offs.size();
+  P.dia_dmax = offs.front();
+  P.dia_dmin = offs.back();
+  P.dia_off.alloc(offs.size(), st);
+  CK(cudaMemcpyAsync(P.dia_off.p, offs.data(), offs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  P.dia_val.alloc((size_t)P.dia_nd * P.n, st);
+  CK(cudaMemsetAsync(P.dia_val.p, 0, (size_t)P.dia_nd * P.n * sizeof(double), st));
+  launch_fill_dia(Hf.view(), offs.data(), P.dia_nd, P.dia_val.p, P.n, st);
+  P.dia_prod.alloc(1, st);
+  CK(cudaStreamSynchronize(st));  // offs (host) is captured by value in the launch
 }
 
 static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
@@ -988,6 +1248,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   // H0 = H 2^-N (exact)
   launch_scale_pow2(Hf.val.p, Hf.nnz, -N, st);
   launch_scale_pow2(P.H0T.val.p, P.H0T.nnz, -N, st);
+  build_diagonals(P);
   slice_rows(P, Hf, P.row_begin, P.row_end, P.H0loc);
   {
     std::vector<int64_t> hrp((size_t)P.n + 1);
@@ -1079,6 +1340,7 @@ static void do_run(sexpm_plan_s &P) {
         S.taylor_numeric_ms[i] = rep.numeric_ms;
         S.taylor_numeric_bytes[i] = rep.numeric_bytes;
         S.taylor_fmas_i[i] = rep.fmas;
+        S.taylor_fallback_rows[i] = rep.window_rows;
       }
       S.taylor_fmas += rep.fmas;
       S.taylor_bytes += 12.0 * (double)Sc.nnz + 12.0 * (double)Sn.nnz + 16.0 * (double)nl;
@@ -1126,11 +1388,14 @@ static void do_run(sexpm_plan_s &P) {
                                            : (double)((long double)P.a * ri * (long double)normIT);
     if (!P.o.filter) eps_g = 0.0;
     StepReport rep;
+    // last squaring: E = I + T^_N is written by its compaction, no separate merge
+    const bool fuse_I = (i == P.N) && !P.o.output_T;
+    DCsr &dst = fuse_I ? P.E : Tn;
     if (P.world == 1) {
-      filtered_product(P, T.view(), T.view(), 2.0, 1.0, eps_g, Tn, rep);
+      filtered_product(P, T.view(), T.view(), 2.0, 1.0, eps_g, dst, rep, nullptr, fuse_I);
     } else {
       exchange_halo(P, T, l1, l2, P.Bhalo);
-      filtered_product(P, T.view(), P.Bhalo.view(), 2.0, 1.0, eps_g, Tn, rep);
+      filtered_product(P, T.view(), P.Bhalo.view(), 2.0, 1.0, eps_g, dst, rep, nullptr, fuse_I);
     }
     const double ms = step_ms();
     if (i < SEXPM_MAXSTEP) {
@@ -1147,16 +1412,21 @@ static void do_run(sexpm_plan_s &P) {
       S.sq_ms[i] = ms;
       S.sq_numeric_ms[i] = rep.numeric_ms;
       S.sq_numeric_bytes[i] = rep.numeric_bytes;
-      S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)Tn.nnz + 16.0 * (double)nl;
+      S.sq_fallback_rows[i] = rep.window_rows;
+      S.sq_first_ms[i] = rep.first_ms;
+      for (int q = 0; q < 8; q++) S.sq_group_prof[i][q] = (double)rep.prof[q];
+      S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)dst.nnz + 16.0 * (double)nl;
     }
     normIT = sqrt(rep.normIT2);
     l1 = rep.l1;
     l2 = rep.l2;
-    swap_csr(T, Tn);
+    if (!fuse_I) swap_csr(T, Tn);
   }
   CK(cudaEventRecord(ev_sq, st));
   // ---- e^H = I + T^_N ----
-  if (P.o.output_T) {
+  if (P.N >= 1 && !P.o.output_T) {
+    // already written by the last squaring's compaction
+  } else if (P.o.output_T) {
     copy_csr(P, T.view(), P.E);
   } else {
     DCsr &I = P.Ibuf;
@@ -1184,6 +1454,14 @@ static void do_run(sexpm_plan_s &P) {
   S.gpu_launches = (int32_t)(g_kernel_launches - launches0);
   S.retries = P.retries;
   P.retries = 0;
+  {
+    std::lock_guard<std::mutex> lk(cache::mu);
+    S.cache_hits = cache::hits - P.cache0[0];
+    S.cache_misses = cache::misses - P.cache0[1];
+    S.cache_releases = cache::releases - P.cache0[2];
+    S.cache_bytes_cached = cache::bytes_cached;
+    S.cache_bytes_allocated = cache::bytes_allocated;
+  }
   for (cudaEvent_t e : {ev_start, ev_taylor, ev_sq, ev_end, a0, a1}) cudaEventDestroy(e);
   P.have_result = true;
 }
@@ -1287,6 +1565,25 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, P->dev));
   P->sm_count = prop.multiProcessorCount;
+  P->smem_per_sm = prop.sharedMemPerMultiprocessor;
+  {
+    int role = 0;
+    for (DCsr *c : {&P->T, &P->Tn, &P->S, &P->Sn, &P->E, &P->Bhalo}) {
+      c->rp.role = role++;
+      c->col.role = role++;
+      c->val.role = role++;
+    }
+    P->ws.pool_col.role = role++;
+    P->ws.pool_val.role = role++;
+  }
+  {
+    std::lock_guard<std::mutex> lk(cache::mu);
+    P->cache0[0] = cache::hits;
+    P->cache0[1] = cache::misses;
+    P->cache0[2] = cache::releases;
+  }
+  while (P->group_slots > 512 && group_smem_bytes(P->group_slots) > (int)prop.sharedMemPerBlockOptin - 4096)
+    P->group_slots -= 512;
   int window = P->o.window_cols > 0 ? P->o.window_cols : 8192;
   int smem = numeric_smem_bytes(window);
   REQUIRE(smem <= (int)prop.sharedMemPerBlockOptin - 2048, SEXPM_EINVAL, "window too large");
@@ -1438,9 +1735,18 @@ int sexpm_destroy(sexpm_plan_t p) {
   cudaStreamSynchronize(p->st);
   cudaStream_t st = p->st;
   bool own = p->own_stream;
+  cache::freeing_idle = true;  // the stream is drained: the plan's blocks are idle
   delete p;
-  cudaStreamSynchronize(st);
+  cache::freeing_idle = false;
+  cache::mark_idle(st);
   if (own) cudaStreamDestroy(st);
+  ABI_END
+}
+
+int sexpm_release_cache(void) {
+  ABI_BEGIN
+  cudaDeviceSynchronize();
+  cache::release_all();
   ABI_END
 }
 

@@ -265,10 +265,44 @@ void launch_alg41_pass(const double *x, int64_t cnt, double tau, double *partial
   reduce_impl<RED_SUMSQ_LE>(x, cnt, tau, partial, out, st);
 }
 
+// integer sum / max (max over non-negative values, 0 for an empty range): grid-stride,
+// one 64-bit atomic per CTA (integer arithmetic: exact in any order)
+// K6 by rows: per-row sum of x^2 over the row's staged values with |x| <= tau (lanes in a
+// fixed stride, fixed warp tree), then a fixed-order reduction over rows.  The staged
+// rows are in column order whatever order the product kernel processed them in, so the
+// pass sums -- and Algorithm 4.1's thresholds -- are identical from run to run.
+__global__ void k_alg41_rows(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
+                             const double *pool_val, double tau, double *out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nrows) return;
+  const int64_t o = row_off[w], c = row_cnt[w];
+  double s = 0.0;
+  for (int64_t t = lane; t < c; t += 32) {
+    const double x = pool_val[o + t];
+    if (fabs(x) <= tau) s += x * x;
+  }
+  s = warp_sum(s);
+  if (lane == 0) out[w] = s;
+}
+void launch_alg41_pass_rows(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
+                            const double *pool_val, double tau, double *rowsum, double *partial,
+                            double *out, cudaStream_t st) {
+  if (nrows == 0) {
+    cudaMemsetAsync(out, 0, sizeof(double), st);
+    return;
+  }
+  KL;
+  k_alg41_rows<<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(nrows, row_off, row_cnt,
+                                                                     pool_val, tau, rowsum);
+  reduce_impl<RED_SUM>(rowsum, nrows, 0.0, partial, out, st);
+}
+
 __global__ void k_reduce_i64(const int64_t *x, int64_t cnt, int64_t *out, int is_max) {
   __shared__ long long s[kWarps];
   long long v = 0;
-  for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
     long long y = x[i];
     v = is_max ? (y > v ? y : v) : v + y;
   }
@@ -278,16 +312,21 @@ __global__ void k_reduce_i64(const int64_t *x, int64_t cnt, int64_t *out, int is
   if (threadIdx.x == 0) {
     long long r = 0;
     for (int w = 0; w < kWarps; w++) r = is_max ? (s[w] > r ? s[w] : r) : r + s[w];
-    out[0] = r;
+    if (is_max) atomicMax(reinterpret_cast<unsigned long long *>(out), (unsigned long long)r);
+    else atomicAdd(reinterpret_cast<unsigned long long *>(out), (unsigned long long)r);
   }
 }
-void launch_reduce_max_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st) {
+static void reduce_i64(const int64_t *x, int64_t cnt, int64_t *out, int is_max, cudaStream_t st) {
+  cudaMemsetAsync(out, 0, sizeof(int64_t), st);
+  if (cnt <= 0) return;
   KL;
-  k_reduce_i64<<<1, kThreads, 0, st>>>(x, cnt, out, 1);
+  k_reduce_i64<<<grid_for(cnt, kThreads * 8, kRedBlocks), kThreads, 0, st>>>(x, cnt, out, is_max);
+}
+void launch_reduce_max_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st) {
+  reduce_i64(x, cnt, out, 1, st);
 }
 void launch_reduce_sum_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st) {
-  KL;
-  k_reduce_i64<<<1, kThreads, 0, st>>>(x, cnt, out, 0);
+  reduce_i64(x, cnt, out, 0, st);
 }
 
 __global__ void k_scale_pow2(double *v, int64_t cnt, int e) {
@@ -1873,6 +1912,790 @@ void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_r
 }
 
 // ------------------------------------------------------------------------------------
+// K3g numeric filtered SpGEMM over GROUPS of kGG rows (the squaring, Eq. 2.7 P:76 /
+// Eq. 4.15; also any A*B):
+//
+//   C~(r_g,:) = self_coef * A(r_g,:) + sum_k a_{r_g k} B(k,:),   g = 0..kGG-1.
+//
+// Rows that are close in the processing order (locality clusters of H's graph) share most
+// of their k's (|union| ~ 1.3x one row's count for a 2D stencil, vs kGG x).  The CTA walks
+// the UNION of the group's k's in ascending order, gathers each B row k from L2 once and
+// applies it to all kGG rows: acc[slot(j)][g] += a_gk * b_kj (the 4 cells of a column are
+// contiguous, two 16-byte shared-memory accesses).  Rows without k add 0 * b_kj, which
+// leaves every cell unchanged bit for bit.  One barrier per k keeps every cell
+// single-writer, and each cell sees the self term first, then ascending k, with _rn
+// products and sums: C~ is bit-identical to the oracle's.
+//
+// Accumulator: pages of 2^sh columns of the group's output span, claimed on first touch
+// (allocated-page bitmap + page table), so the flush walks the claimed pages in column
+// order: rows come out sorted.  The union of k's is a bitmap over the group's k span,
+// numbered by a popcount scan (coefficients a_gk land at the k's rank).  The flush
+// classifies against the Algorithm 4.1 floor (see k_numeric) and stages each row's entries
+// contiguously in the pool.  Groups that do not fit (span, union size or slot capacity)
+// hand their rows to the fail list (paged / window kernels).
+// ------------------------------------------------------------------------------------
+constexpr int kGG = 4;
+constexpr int kGThreads = 256;
+constexpr int kGWarps = kGThreads / 32;
+constexpr int kGPages = 12288;     // direct page table over the group's output span
+constexpr int kGKWords = 1536;     // union-k bitmap words (k span <= 49152)
+constexpr int kGKCap = 1024;       // union k's per group
+constexpr int kGRing = 4;          // B rows in flight (TMA bulk copies)
+constexpr int kGRowCap = 768;      // longest B row staged in the ring (longer: global loads)
+constexpr int kGRingCols = kGRowCap + 8, kGRingVals = kGRowCap + 4;
+constexpr uint16_t kGNone = 0xFFFF, kGOver = 0xFFFE;
+
+int group_smem_bytes(int slots) {
+  return slots * kGG * 8 + kGRing * (kGRingVals * 8 + kGRingCols * 4) + kGKCap * kGG * 8 +
+         kGKCap * 8 + kGKCap * 4 + kGPages * 2 + (kGPages / 32) * 4 + kGKWords * 4 +
+         kGKWords * 2 + (slots >> 3) * 2 + kGRing * 8 + 64;
+}
+
+// mbarrier + TMA bulk copy helpers (sm_90+ PTX, here sm_100a)
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int group_slot(volatile uint16_t *ptab, unsigned *pbits, int *nblk,
+                                          int blk_cap, int pg) {
+  uint16_t b = ptab[pg];
+  if (b < kGOver) return b;
+  if (b == kGOver) return -1;
+  const unsigned bit = 1u << (pg & 31);
+  const unsigned old = atomicOr(&pbits[pg >> 5], bit);
+  if (!(old & bit)) {
+    int nb = atomicAdd(nblk, 1);
+    const uint16_t v = nb < blk_cap ? (uint16_t)nb : kGOver;
+    __threadfence_block();
+    ptab[pg] = v;
+    return nb < blk_cap ? nb : -1;
+  }
+  while ((b = ptab[pg]) == kGNone) {
+  }
+  return b == kGOver ? -1 : (int)b;
+}
+
+// exclusive scan of kGG values over the CTA's threads (thread order): v[] becomes the
+// exclusive prefix, tot[] the totals
+template <typename T>
+__device__ __forceinline__ void gblock_scan4(T (&v)[kGG], T (&tot)[kGG], T *sbuf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T incl[kGG];
+#pragma unroll
+  for (int g = 0; g < kGG; g++) {
+    T x = v[g];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(FULL_MASK, x, o);
+      if (lane >= o) x += y;
+    }
+    incl[g] = x;
+    if (lane == 31) sbuf[warp * kGG + g] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < kGG; g++) {
+    T pre = 0, t = 0;
+    for (int w = 0; w < kGWarps; w++) {
+      const T y = sbuf[w * kGG + g];
+      if (w < warp) pre += y;
+      t += y;
+    }
+    tot[g] = t;
+    v[g] = pre + incl[g] - v[g];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, int slots,
+                                                                int32_t *fail_rows,
+                                                                int *fail_count) {
+  extern __shared__ double gsm[];
+  double *acc = gsm;                                                     // kGG * slots (row-major)
+  double *rval = acc + (size_t)slots * kGG;                              // kGRing * kGRingVals
+  double *coef = rval + kGRing * kGRingVals;                             // kGKCap * kGG
+  long long *kst = reinterpret_cast<long long *>(coef + kGKCap * kGG);   // kGKCap
+  uint64_t *bars = reinterpret_cast<uint64_t *>(kst + kGKCap);           // kGRing
+  int32_t *kln = reinterpret_cast<int32_t *>(bars + kGRing);             // kGKCap
+  int32_t *rcol = kln + kGKCap;                                          // kGRing * kGRingCols
+  uint16_t *ptab = reinterpret_cast<uint16_t *>(rcol + kGRing * kGRingCols);  // kGPages
+  unsigned *pbits = reinterpret_cast<unsigned *>(ptab + kGPages);        // kGPages / 32
+  unsigned *kbits = pbits + kGPages / 32;                                // kGKWords
+  uint16_t *kpref = reinterpret_cast<uint16_t *>(kbits + kGKWords);      // kGKWords
+  uint16_t *plist = kpref + kGKWords;                                    // slots >> 3
+  __shared__ int s_grp, s_nblk, s_fail, s_nk;
+  __shared__ long long s_p0[kGG], s_p1[kGG];
+  __shared__ int64_t s_r[kGG];
+  __shared__ int s_ng, s_kmin, s_kmax, s_lo, s_hi;
+  __shared__ long long s_scan[kGWarps * kGG];
+  __shared__ double s_fs[kGWarps * kGG];
+  __shared__ unsigned long long s_off[kGG];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
+  for (int i = tid; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
+  for (int i = tid; i < kGPages; i += kGThreads) ptab[i] = kGNone;
+  for (int i = tid; i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
+  for (int i = tid; i < kGKWords; i += kGThreads) kbits[i] = 0u;
+  if (tid == 0) {
+    for (int d = 0; d < kGRing; d++) mbar_init(&bars[d], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  unsigned phase = 0;  // bit d: parity of ring slot d's next completion (uniform)
+  const int64_t ngroups = (a.nlist + kGG - 1) / kGG;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_grp = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int64_t grp = s_grp;
+    if (grp >= ngroups) break;
+    long long t_0 = clock64();
+    // ---- group rows, spans ----
+    if (tid < kGG) {
+      const int64_t idx = grp * kGG + tid;
+      int64_t r = -1;
+      long long p0 = 0, p1 = 0;
+      if (idx < a.nlist) {
+        r = a.order ? (int64_t)a.order[idx] : idx;
+        p0 = a.A.rp[r];
+        p1 = a.A.rp[r + 1];
+      }
+      s_r[tid] = r;
+      s_p0[tid] = p0;
+      s_p1[tid] = p1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int ng = 0, lo = INT32_MAX, hi = -1, kmin = INT32_MAX, kmax = -1;
+      for (int g = 0; g < kGG; g++) {
+        if (s_r[g] < 0) continue;
+        ng = g + 1;
+        const int64_t r = s_r[g];
+        if (a.hi[r] >= a.lo[r]) {
+          lo = min(lo, a.lo[r]);
+          hi = max(hi, a.hi[r]);
+        }
+        if (s_p1[g] > s_p0[g]) {
+          kmin = min(kmin, a.A.col[s_p0[g]]);
+          kmax = max(kmax, a.A.col[s_p1[g] - 1]);
+        }
+      }
+      s_ng = ng;
+      s_lo = lo;
+      s_hi = hi;
+      s_kmin = kmin;
+      s_kmax = kmax;
+      s_nblk = 0;
+      s_nk = 0;
+      int fail = 0;  // 1: k span, 2: output span, 3: union size, 4: slots
+      if (kmax >= kmin && (int64_t)kmax - kmin + 1 > (int64_t)kGKWords * 32) fail = 1;
+      if (hi >= lo && (((int64_t)hi >> 6) - ((int64_t)lo >> 6) + 1) > kGPages) fail = 2;
+      s_fail = fail;
+    }
+    __syncthreads();
+    const int ng = s_ng;
+    if (s_hi < s_lo) {  // every row of the group is empty
+      if (tid < ng) {
+        const int64_t r = s_r[tid];
+        a.row_off[r] = 0;
+        a.row_cnt[r] = 0;
+        a.row_fsum[r] = 0.0;
+        a.row_nnz[r] = 0;
+      }
+      continue;
+    }
+    int sh = 3;
+    {
+      const int64_t lo = s_lo, hi = s_hi;
+      while (sh < 6 && ((hi >> sh) - (lo >> sh) + 1) > kGPages) sh++;
+    }
+    const int pmask = (1 << sh) - 1;
+    const int64_t pg0 = (int64_t)s_lo >> sh;
+    const int npg = (int)(((int64_t)s_hi >> sh) - pg0 + 1);
+    const int bcap = slots >> sh;  // page blocks of this size that fit
+    const int kmin = s_kmin;
+    // ---- union of k: bitmap, ranks, coefficients, B-row extents ----
+    if (!s_fail) {
+      for (int g = 0; g < ng; g++) {
+        for (long long p = s_p0[g] + tid; p < s_p1[g]; p += kGThreads) {
+          const int kb = a.A.col[p] - kmin;
+          atomicOr(&kbits[kb >> 5], 1u << (kb & 31));
+        }
+      }
+    }
+    __syncthreads();
+    const int nkw = s_fail ? 0 : ((s_kmax - kmin) >> 5) + 1;
+    {
+      const int per = (nkw + kGThreads - 1) / kGThreads;
+      const int w0 = min(tid * per, nkw), w1 = min(w0 + per, nkw);
+      long long c[kGG] = {0, 0, 0, 0}, tot[kGG];
+      for (int w = w0; w < w1; w++) c[0] += __popc(kbits[w]);
+      gblock_scan4<long long>(c, tot, s_scan);
+      int run = (int)c[0];
+      for (int w = w0; w < w1; w++) {
+        kpref[w] = (uint16_t)run;
+        run += __popc(kbits[w]);
+      }
+      if (tid == 0) {
+        s_nk = (int)tot[0];
+        if (!s_fail && tot[0] > kGKCap) s_fail = 3;
+      }
+    }
+    __syncthreads();
+    const int nk = s_fail ? 0 : s_nk;
+    if (!s_fail) {
+      for (int g = 0; g < ng; g++) {
+        for (long long p = s_p0[g] + tid; p < s_p1[g]; p += kGThreads) {
+          const int k = a.A.col[p];
+          const int kb = k - kmin;
+          const int rk = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
+          coef[rk * kGG + g] = a.A.val[p];
+          const int64_t kr = (int64_t)k - a.B.row0;
+          long long b0 = 0;
+          int ln = 0;
+          if (kr >= 0 && kr < a.B.nrows) {
+            b0 = a.B.rp[kr];
+            ln = (int)(a.B.rp[kr + 1] - b0);
+          }
+          kst[rk] = b0;
+          kln[rk] = ln;
+        }
+      }
+    }
+    __syncthreads();
+    // ring: union row q is staged in slot q % kGRing with two bulk copies (cols and values,
+    // widened to 16-byte boundaries) issued by lane 0 of warp q % kGWarps (spread over the
+    // warps, so no warp is late at every barrier)
+    auto issue = [&](int q) {
+      if (a.dbg == 4) return;
+      if (q < nk && kln[q] <= kGRowCap) {
+        const int d = q % kGRing;
+        const long long b0 = kst[q];
+        const int ln = kln[q];
+        const long long ca = b0 & ~3LL, va = b0 & ~1LL;
+        const unsigned cb = (unsigned)(((b0 + ln + 3) & ~3LL) - ca) * 4u;
+        const unsigned vb = (unsigned)(((b0 + ln + 1) & ~1LL) - va) * 8u;
+        mbar_expect_tx(&bars[d], cb + vb);
+        if (cb) tma_bulk_g2s(rcol + d * kGRingCols, a.B.col + ca, cb, &bars[d]);
+        if (vb) tma_bulk_g2s(rval + d * kGRingVals, a.B.val + va, vb, &bars[d]);
+      }
+    };
+    if (lane == 0 && warp < kGRing)
+      for (int q = warp; q < kGRing; q += kGWarps) issue(q);
+    // ---- self term (the 2T of Eq. 2.7), before any product ----
+    if (!s_fail && a.self_coef != 0.0) {
+      for (int g = 0; g < ng; g++) {
+        for (long long p = s_p0[g] + tid; p < s_p1[g]; p += kGThreads) {
+          const int rel = (int)(a.A.col[p] - (pg0 << sh));
+          const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
+          if (b >= 0) acc[(size_t)g * slots + (b << sh) + (rel & pmask)] = __dmul_rn(a.self_coef, a.A.val[p]);
+          else s_fail = 4;
+        }
+      }
+    }
+    long long t_1 = clock64();
+    // ---- products: union k ascending, one barrier per k ----
+    // Every union row k is applied to all kGG rows (a row without k adds 0 * b_kj, which
+    // leaves its cells bit-identical); entries tid and tid + kGThreads per thread.
+    const int cbase = (int)(pg0 << sh);
+    __syncthreads();
+    for (int kk = 0; kk < nk; kk++) {
+      const int d = kk % kGRing;
+      const int ln = kln[kk];
+      const long long b0 = kst[kk];
+      const bool staged = ln <= kGRowCap;
+      if (staged && a.dbg != 4) {
+        mbar_wait(&bars[d], (phase >> d) & 1u);
+        phase ^= 1u << d;
+      }
+      if (!s_fail) {
+        const double2 c01 = *reinterpret_cast<const double2 *>(&coef[kk * kGG]);
+        const double2 c23 = *reinterpret_cast<const double2 *>(&coef[kk * kGG + 2]);
+        // one entry: slot lookup (page claimed on first touch), then the kGG cells of the
+        // group's rows, loads before stores
+        auto apply = [&](int32_t c, double v) {
+          const int rel = c - cbase;
+          if (a.dbg == 1 || a.dbg == 4) return;
+          const int b = a.dbg == 2 ? (int)ptab[rel >> sh] : group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
+          if (a.dbg == 3) {
+            if (b >= 0) acc[(b << sh) + (rel & pmask)] += v;
+            return;
+          }
+          if (b < 0) {
+            s_fail = 4;
+            return;
+          }
+          const int o = (b << sh) + (rel & pmask);
+          const double x0 = acc[o], x1 = acc[slots + o], x2 = acc[2 * slots + o], x3 = acc[3 * slots + o];
+          acc[o] = __dadd_rn(x0, __dmul_rn(c01.x, v));
+          acc[slots + o] = __dadd_rn(x1, __dmul_rn(c01.y, v));
+          acc[2 * slots + o] = __dadd_rn(x2, __dmul_rn(c23.x, v));
+          acc[3 * slots + o] = __dadd_rn(x3, __dmul_rn(c23.y, v));
+        };
+        if (staged) {  // entries from the shared-memory ring
+          const int cb = d * kGRingCols + (int)(b0 & 3), vb = d * kGRingVals + (int)(b0 & 1);
+          if (tid < ln) {
+            const int32_t c0 = rcol[cb + tid];
+            const double v0 = rval[vb + tid];
+            if (tid + kGThreads < ln) {
+              const int32_t c1 = rcol[cb + tid + kGThreads];
+              const double v1 = rval[vb + tid + kGThreads];
+              apply(c0, v0);
+              apply(c1, v1);
+            } else {
+              apply(c0, v0);
+            }
+            for (int e = tid + 2 * kGThreads; e < ln; e += kGThreads) apply(rcol[cb + e], rval[vb + e]);
+          }
+        } else {  // rows longer than the ring slot: straight from global memory
+          for (int e = tid; e < ln; e += kGThreads) apply(a.B.col[b0 + e], a.B.val[b0 + e]);
+        }
+      }
+      __syncthreads();  // one writer per cell (k -> next k); ring slot d free again
+      if (lane == 0 && warp == (kk + kGRing) % kGWarps) issue(kk + kGRing);
+    }
+    __syncthreads();
+    long long t_2 = clock64();
+    const int failed = s_fail;
+    // ---- flush: claimed pages in column order ----
+    int npl = 0;
+    {
+      const int nw = failed ? 0 : (npg + 31) >> 5;
+      const int per = (nw + kGThreads - 1) / kGThreads;
+      const int w0 = min(tid * per, nw), w1 = min(w0 + per, nw);
+      long long c[kGG] = {0, 0, 0, 0}, tot[kGG];
+      for (int w = w0; w < w1; w++) c[0] += __popc(pbits[w]);
+      gblock_scan4<long long>(c, tot, s_scan);
+      int run = (int)c[0];
+      for (int w = w0; w < w1; w++) {
+        unsigned m = pbits[w];
+        while (m) {
+          const int bb = __ffs(m) - 1;
+          m &= m - 1;
+          plist[run++] = (uint16_t)(w * 32 + bb);
+        }
+      }
+      npl = (int)tot[0];
+    }
+    __syncthreads();
+    const int total = npl << sh;
+    const int per = (total + kGThreads - 1) / kGThreads;
+    const int q0 = min(tid * per, total), q1 = min(q0 + per, total);
+    long long nst[kGG] = {0, 0, 0, 0}, nnzu[kGG] = {0, 0, 0, 0}, tot[kGG];
+    double fs[kGG] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = q0; q < q1; q++) {
+      const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
+#pragma unroll
+      for (int g = 0; g < kGG; g++) {
+        double x = acc[(size_t)g * slots + o];
+        if (x != 0.0) {
+          if (a.divisor != 1.0) x = x / a.divisor;
+          if (x != 0.0) {
+            nnzu[g]++;
+            if (fabs(x) > a.floor_tau) nst[g]++;
+            else fs[g] += x * x;
+          }
+        }
+      }
+    }
+    gblock_scan4<long long>(nst, tot, s_scan);
+    // per-row floor sums and distinct counts (fixed order: lanes, then warps)
+#pragma unroll
+    for (int g = 0; g < kGG; g++) {
+      const double f = warp_sum(fs[g]);
+      const long long z = warp_sum(nnzu[g]);
+      if (lane == 0) {
+        s_fs[warp * kGG + g] = f;
+        s_scan[warp * kGG + g] = z;
+      }
+    }
+    __syncthreads();
+    if (tid < kGG) {
+      const int g = tid;
+      double f = 0.0;
+      long long z = 0;
+      for (int w = 0; w < kGWarps; w++) {
+        f += s_fs[w * kGG + g];
+        z += s_scan[w * kGG + g];
+      }
+      s_off[g] = (!failed && g < ng) ? atomicAdd(a.pool_used, (unsigned long long)tot[g]) : 0ull;
+      if (!failed && g < ng) {
+        const int64_t r = s_r[g];
+        const bool ok = (long long)s_off[g] + tot[g] <= a.pool_cap;
+        if (!ok) atomicOr(a.flags, 1);
+        a.row_off[r] = (int64_t)s_off[g];
+        a.row_cnt[r] = tot[g];
+        a.row_fsum[r] = f;
+        a.row_nnz[r] = z;
+      }
+    }
+    __syncthreads();
+    if (!failed) {
+      long long pos[kGG];
+      bool okg[kGG];
+#pragma unroll
+      for (int g = 0; g < kGG; g++) {
+        pos[g] = (long long)s_off[g] + nst[g];
+        okg[g] = g < ng && (long long)s_off[g] + tot[g] <= a.pool_cap;
+      }
+      for (int q = q0; q < q1; q++) {
+        const int pgi = plist[q >> sh];
+        const int o = ((int)ptab[pgi] << sh) + (q & pmask);
+        const int32_t col = (int32_t)(((pg0 + pgi) << sh) + (q & pmask));
+#pragma unroll
+        for (int g = 0; g < kGG; g++) {
+          double x = acc[(size_t)g * slots + o];
+          if (x != 0.0) {
+            if (a.divisor != 1.0) x = x / a.divisor;
+            if (x != 0.0 && fabs(x) > a.floor_tau) {
+              if (okg[g]) {
+                a.pool_col[pos[g]] = col;
+                a.pool_val[pos[g]] = x;
+              }
+              pos[g]++;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- reset the group's state ----
+    if (!failed) {
+      for (int q = tid; q < total; q += kGThreads) {
+        const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
+#pragma unroll
+        for (int g = 0; g < kGG; g++) acc[(size_t)g * slots + o] = 0.0;
+      }
+      __syncthreads();
+      for (int i = tid; i < npl; i += kGThreads) ptab[plist[i]] = kGNone;
+      for (int i = tid; i < nk * kGG; i += kGThreads) coef[i] = 0.0;
+    } else {
+      for (int i = tid; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
+      for (int i = tid; i < kGPages; i += kGThreads) ptab[i] = kGNone;
+      for (int i = tid; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
+    }
+    for (int i = tid; i < ((npg + 31) >> 5) && i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
+    for (int i = tid; i < kGKWords; i += kGThreads) kbits[i] = 0u;
+    if (failed && tid < ng) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)s_r[tid];
+    if (a.prof && tid == 0) {
+      const long long t_3 = clock64();
+      atomicAdd(&a.prof[0], (unsigned long long)(t_1 - t_0));
+      atomicAdd(&a.prof[1], (unsigned long long)(t_2 - t_1));
+      atomicAdd(&a.prof[2], (unsigned long long)(t_3 - t_2));
+      atomicAdd(&a.prof[3], 1ull);
+      atomicAdd(&a.prof[4], (unsigned long long)s_nk);
+      if (failed) atomicAdd(&a.prof[5], 1ull);
+      if (failed == 3) atomicAdd(&a.prof[6], 1ull);
+      if (failed == 4) atomicAdd(&a.prof[7], 1ull);
+    }
+  }
+}
+
+void launch_numeric_group(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
+                          cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  const int smem = group_smem_bytes(slots);
+  cudaFuncSetAttribute(k_numeric_group, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_group<<<a.grid, kGThreads, smem, st>>>(a, slots, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
+// Diagonal structure of H0 (plan time): offsets d = j - k present anywhere in H0, as a
+// bitmap over [-(n-1), n-1]; then the diagonals h_d[k] = H0(k, k + d).
+// ------------------------------------------------------------------------------------
+__global__ void k_mark_offsets(CsrView H, unsigned *bits, int64_t n) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= H.nrows) return;
+  const int64_t row = H.row0 + w;
+  for (int64_t p = H.rp[w] + lane; p < H.rp[w + 1]; p += 32) {
+    const int64_t b = (int64_t)H.col[p] - row + (n - 1);
+    atomicOr(&bits[b >> 5], 1u << (b & 31));
+  }
+}
+void launch_mark_offsets(const CsrView &H, unsigned *bits, int64_t n, cudaStream_t st) {
+  if (H.nrows == 0) return;
+  KL;
+  k_mark_offsets<<<grid_for(H.nrows * 32, kThreads), kThreads, 0, st>>>(H, bits, n);
+}
+struct DiaOffsets {
+  int32_t off[kDiaMax];
+  int nd;
+};
+__global__ void k_fill_dia(CsrView H, DiaOffsets O, double *dia, int64_t n) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= H.nrows) return;
+  const int64_t row = H.row0 + w;
+  for (int64_t p = H.rp[w] + lane; p < H.rp[w + 1]; p += 32) {
+    const int64_t d = (int64_t)H.col[p] - row;
+    for (int i = 0; i < O.nd; i++)
+      if (O.off[i] == d) dia[(int64_t)i * n + row] = H.val[p];
+  }
+}
+void launch_fill_dia(const CsrView &H, const int32_t *off_host, int nd, double *dia, int64_t n,
+                     cudaStream_t st) {
+  if (H.nrows == 0 || nd == 0) return;
+  DiaOffsets O;
+  for (int i = 0; i < kDiaMax; i++) O.off[i] = i < nd ? off_host[i] : 0;
+  O.nd = nd;
+  KL;
+  k_fill_dia<<<grid_for(H.nrows * 32, kThreads), kThreads, 0, st>>>(H, O, dia, n);
+}
+
+// ------------------------------------------------------------------------------------
+// K5d Taylor term by DIAGONAL PUSH: S~(r, j) = (sum_k s_rk h0_kj) / i  (Eq. 4.11, P:306,
+// Alg. 4.2 step 3 P:412), for an H0 with few distinct diagonal offsets d = j - k (grid
+// stencils: 3 in 1D, 5 in 2D, 7 in 3D).  H0 is held as diagonals h_d[k] = H0(k, k + d)
+// (zero where absent), offsets sorted DESCENDING.
+//
+// One warp per row r of S^.  Lanes take 32 consecutive entries (k, s_rk) of the row; for
+// each offset d in turn every lane adds s_rk * h_d[k] into column j = k + d.  Lanes hold
+// distinct k, so within one offset they write distinct columns (no atomics, no conflicts;
+// __syncwarp between offsets orders the shared-memory updates).  For a fixed column j the
+// contributions arrive with k = j - d ascending (offsets descending inside a chunk, chunks
+// ascending), i.e. exactly the oracle's order: acc = acc + (s_rk * h_kj) with _rn
+// intrinsics, then / i -- S~ is bit-identical to the oracle's.
+//
+// Accumulator: pages of 2^sh columns aligned to absolute multiples of 2^sh.  A first pass
+// marks the pages the row can reach in a bitmap over the row's span; a popcount scan of
+// the bitmap numbers the marked pages in column order, so slot(j) = 2^sh * rank(page(j)) +
+// (j mod 2^sh) with two shared-memory loads and a popc, and the flush walks the slots in
+// column order (rows come out sorted).  The flush divides by i, classifies against the
+// Algorithm 4.1 floor (see k_numeric) and stages (col, val) in the pool.  Rows that do not
+// fit (span or slot capacity) go to the fail list (pull kernel).
+// ------------------------------------------------------------------------------------
+constexpr int kDWarps = 4;            // warps per CTA
+constexpr int kDPageWords = 256;      // page bitmap: 8192 pages per row
+constexpr int kDMaxDiag = kDiaMax;
+
+int taylor_dia_smem_bytes(int slots) {
+  return kDWarps * (slots * 8 + kDPageWords * 4 + kDPageWords * 2 + (slots >> 3) * 2 + 16);
+}
+
+__global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaView D, int slots,
+                                                             int32_t *fail_rows, int *fail_count) {
+  extern __shared__ double dsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int max_pages = slots >> 3;
+  const size_t wbytes = (size_t)slots * 8 + kDPageWords * 4 + kDPageWords * 2 + (size_t)max_pages * 2 + 16;
+  char *base = reinterpret_cast<char *>(dsm) + wbytes * wib;
+  double *acc = reinterpret_cast<double *>(base);
+  unsigned *pbits = reinterpret_cast<unsigned *>(acc + slots);
+  uint16_t *pref = reinterpret_cast<uint16_t *>(pbits + kDPageWords);
+  uint16_t *plist = pref + kDPageWords;
+  __shared__ int32_t s_doff[kDMaxDiag];
+  if (threadIdx.x < kDMaxDiag) s_doff[threadIdx.x] = threadIdx.x < D.ndiag ? D.off[threadIdx.x] : 0;
+  for (int i = lane; i < slots; i += 32) acc[i] = 0.0;
+  for (int i = lane; i < kDPageWords; i += 32) pbits[i] = 0u;
+  __syncthreads();
+  const int nd = D.ndiag;
+  const int32_t dmin = D.dmin, dmax = D.dmax;
+  const int64_t n = D.n;
+  unsigned long long prods = 0;
+  constexpr int kBatch = 4;  // rows taken per scheduler atomic
+  for (;;) {
+    int idx0 = 0;
+    if (lane == 0) idx0 = atomicAdd(a.row_counter, kBatch);
+    idx0 = __shfl_sync(FULL_MASK, idx0, 0);
+    if (idx0 >= a.nlist) break;
+    const int idx1 = idx0 + kBatch < a.nlist ? idx0 + kBatch : (int)a.nlist;
+    for (int idx = idx0; idx < idx1; idx++) {
+      const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
+      const int64_t p0 = a.A.rp[r], p1 = a.A.rp[r + 1];
+      const int nx = (int)(p1 - p0);
+      if (nx == 0) {
+        if (lane == 0) {
+          a.row_off[r] = 0;
+          a.row_cnt[r] = 0;
+          a.row_fsum[r] = 0.0;
+          a.row_nnz[r] = 0;
+        }
+        continue;
+      }
+      int64_t lo = (int64_t)a.A.col[p0] + dmin, hi = (int64_t)a.A.col[p1 - 1] + dmax;
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > n - 1 ? n - 1 : hi;
+      int sh = 3;
+      while (sh < 7 && ((hi >> sh) - (lo >> sh)) >= (int64_t)kDPageWords * 32) sh++;
+      const int64_t pg0 = lo >> sh;
+      const int npg = (int)((hi >> sh) - pg0 + 1);
+      bool fail = sh >= 7;
+      // (1) mark reachable pages
+      if (!fail) {
+        for (int c0 = 0; c0 < nx; c0 += 32) {
+          const int t = c0 + lane;
+          const bool in = t < nx;
+          const int64_t k = in ? (int64_t)a.A.col[p0 + t] : 0;
+          for (int di = 0; di < nd; di++) {
+            const int64_t j = k + s_doff[di];
+            const bool v = in && j >= 0 && j < n;
+            const int pg = v ? (int)((j >> sh) - pg0) : -1;
+            const unsigned act = __ballot_sync(FULL_MASK, v);
+            if (v) {
+              const unsigned peers = __match_any_sync(act, pg);
+              if (lane == __ffs(peers) - 1) atomicOr(&pbits[pg >> 5], 1u << (pg & 31));
+            }
+          }
+        }
+        __syncwarp();
+      }
+      // (2) number the marked pages in column order
+      const int nwords = (npg + 31) >> 5;
+      int npages = 0;
+      if (!fail) {
+        int cnt = 0;
+        for (int w = lane * 8; w < lane * 8 + 8; w++) cnt += w < nwords ? __popc(pbits[w]) : 0;
+        int v = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(FULL_MASK, v, o);
+          if (lane >= o) v += y;
+        }
+        npages = __shfl_sync(FULL_MASK, v, 31);
+        if ((npages << sh) > slots) {
+          fail = true;
+        } else {
+          int run = v - cnt;
+          for (int w = lane * 8; w < lane * 8 + 8; w++) {
+            if (w < nwords) {
+              pref[w] = (uint16_t)run;
+              unsigned m = pbits[w];
+              while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                plist[run++] = (uint16_t)(w * 32 + b);
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (fail) {
+        for (int w = lane; w < nwords; w += 32) pbits[w] = 0u;
+        if (lane == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+        __syncwarp();
+        continue;
+      }
+      // (3) products, offsets descending inside each chunk of 32 entries
+      const int pmask = (1 << sh) - 1;
+      for (int c0 = 0; c0 < nx; c0 += 32) {
+        const int t = c0 + lane;
+        const bool in = t < nx;
+        const int64_t k = in ? (int64_t)a.A.col[p0 + t] : 0;
+        const double sv = in ? a.A.val[p0 + t] : 0.0;
+        double h[kDMaxDiag];
+#pragma unroll
+        for (int di = 0; di < kDMaxDiag; di++) {
+          h[di] = 0.0;
+          if (di < nd && in) h[di] = D.val[(int64_t)di * n + k];
+        }
+#pragma unroll
+        for (int di = 0; di < kDMaxDiag; di++) {
+          if (di < nd) {
+            if (h[di] != 0.0) {
+              const int64_t j = k + s_doff[di];
+              const int pg = (int)((j >> sh) - pg0);
+              const unsigned wd = pbits[pg >> 5];
+              const int rank = pref[pg >> 5] + __popc(wd & ((1u << (pg & 31)) - 1u));
+              const int o = (rank << sh) + (int)(j & pmask);
+              acc[o] = __dadd_rn(acc[o], __dmul_rn(sv, h[di]));
+              prods++;
+            }
+            __syncwarp();
+          }
+        }
+      }
+      // (4) flush in column order: divide, classify, count
+      const int total = npages << sh;
+      int nst = 0;
+      double fs = 0.0;
+      long long nnzu = 0;
+      for (int s0 = lane; s0 < total; s0 += 32) {
+        double x = acc[s0];
+        if (x != 0.0) {
+          x = x / a.divisor;
+          acc[s0] = x;
+          if (x != 0.0) {
+            nnzu++;
+            if (fabs(x) > a.floor_tau) nst++;
+            else fs += x * x;
+          }
+        }
+      }
+      nst = __reduce_add_sync(FULL_MASK, nst);
+      fs = warp_sum(fs);
+      nnzu = warp_sum(nnzu);
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)nst);
+      off = __shfl_sync(FULL_MASK, off, 0);
+      const bool ok = (long long)off + nst <= a.pool_cap;
+      long long pos = (long long)off;
+      for (int b0 = 0; b0 < total; b0 += 32) {
+        const int s0 = b0 + lane;
+        double x = 0.0;
+        if (s0 < total) {
+          x = acc[s0];
+          acc[s0] = 0.0;
+        }
+        const bool st = x != 0.0 && fabs(x) > a.floor_tau;
+        const unsigned m = __ballot_sync(FULL_MASK, st);
+        if (st && ok) {
+          const long long q = pos + __popc(m & lanemask_lt());
+          a.pool_col[q] = (int32_t)(((pg0 + plist[s0 >> sh]) << sh) + (s0 & pmask));
+          a.pool_val[q] = x;
+        }
+        pos += __popc(m);
+      }
+      for (int w = lane; w < nwords; w += 32) pbits[w] = 0u;
+      if (lane == 0) {
+        if (!ok) atomicOr(a.flags, 1);
+        a.row_off[r] = (int64_t)off;
+        a.row_cnt[r] = nst;
+        a.row_fsum[r] = fs;
+        a.row_nnz[r] = nnzu;
+      }
+      __syncwarp();
+    }
+  }
+  prods = warp_sum(prods);
+  if (lane == 0 && prods) atomicAdd(D.prod_count, prods);
+}
+
+void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_t *fail_rows,
+                       int *fail_count, cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  const int smem = taylor_dia_smem_bytes(slots);
+  cudaFuncSetAttribute(k_taylor_dia, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_taylor_dia<<<a.grid, kDWarps * 32, smem, st>>>(a, D, slots, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
 // K3w numeric filtered SpGEMM, one WARP per output row, conflict-free dense window.
 //
 // Row r of C~ = self_coef * A(r,:) + sum_k a_rk B(k,:) is built in column passes: a pass
@@ -2086,23 +2909,51 @@ void launch_numeric_warp(const NumericArgs &a, cudaStream_t st) {
 // ------------------------------------------------------------------------------------
 // K4 compaction: keep staged entries with |x| > tau (Alg. 4.1 step 3).
 // ------------------------------------------------------------------------------------
-__global__ void k_compact_count(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
-                                const double *pool_val, double tau, int64_t *cnt) {
+// ident != nullptr (E = I + T^_N fused into the last compaction): per row,
+// ident[w] = 0 no kept diagonal (insert 1.0), 1 kept diagonal t (write 1 + t), 2 kept
+// diagonal with 1 + t == 0 (purged, reading R11); cnt counts the entries of E's row.
+__global__ void k_compact_count(int64_t nrows, int64_t row0, const int64_t *row_off,
+                                const int64_t *row_cnt, const int32_t *pool_col,
+                                const double *pool_val, double tau, int64_t *cnt,
+                                int8_t *ident) {
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (w >= nrows) return;
   int64_t o = row_off[w], c = row_cnt[w];
+  const int64_t grow = row0 + w;
   long long k = 0;
-  for (int64_t t = lane; t < c; t += 32) k += fabs(pool_val[o + t]) > tau;
+  int diag = 0;  // 1: kept diagonal, 2: kept diagonal with 1 + t == 0
+  for (int64_t t = lane; t < c; t += 32) {
+    const double x = pool_val[o + t];
+    const bool kept = fabs(x) > tau;
+    k += kept;
+    if (ident && kept && pool_col[o + t] == grow) diag = (1.0 + x == 0.0) ? 2 : 1;
+  }
   k = warp_sum(k);
-  if (lane == 0) cnt[w] = k;
+  if (ident) diag = __reduce_max_sync(FULL_MASK, diag);
+  if (lane == 0) {
+    if (ident) {
+      ident[w] = (int8_t)diag;
+      k += diag == 0 ? 1 : (diag == 2 ? -1 : 0);
+    }
+    cnt[w] = k;
+  }
 }
 void launch_compact_count(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
                           const double *pool_val, double tau, int64_t *cnt, cudaStream_t st) {
   if (nrows == 0) return;
   KL;
-  k_compact_count<<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(nrows, row_off, row_cnt,
-                                                                       pool_val, tau, cnt);
+  k_compact_count<<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(
+      nrows, 0, row_off, row_cnt, nullptr, pool_val, tau, cnt, nullptr);
+}
+void launch_compact_count_ident(int64_t nrows, int64_t row0, const int64_t *row_off,
+                                const int64_t *row_cnt, const int32_t *pool_col,
+                                const double *pool_val, double tau, int64_t *cnt, int8_t *ident,
+                                cudaStream_t st) {
+  if (nrows == 0) return;
+  KL;
+  k_compact_count<<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(
+      nrows, row0, row_off, row_cnt, pool_col, pool_val, tau, cnt, ident);
 }
 
 __device__ __forceinline__ void row_stat_accum(int64_t grow, int32_t c, double x, double &s,
@@ -2136,16 +2987,19 @@ __global__ void k_compact_write(int64_t nrows, int64_t row0, const int64_t *row_
                                 const int64_t *row_cnt, const int32_t *pool_col,
                                 const double *pool_val, double tau, const int64_t *rp_out,
                                 int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
-                                int64_t *l2r) {
+                                int64_t *l2r, const int8_t *ident) {
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (w >= nrows) return;
   int64_t o = row_off[w], c = row_cnt[w];
-  int64_t dst = rp_out[w];
+  const int64_t dst0 = rp_out[w];
+  int64_t dst = dst0;
   const int64_t grow = row0 + w;
+  const int idg = ident ? ident[w] : -1;  // -1: plain compaction of T^
   double s = 0.0;
   int have_diag = 0;
   long long l1 = 0, l2 = 0;
+  long long nlt = 0;  // kept entries left of the diagonal (insert position, idg == 0)
   for (int64_t base = 0; base < c; base += 32) {
     int64_t t = base + lane;
     bool k = false;
@@ -2156,14 +3010,22 @@ __global__ void k_compact_write(int64_t nrows, int64_t row0, const int64_t *row_
       cc = pool_col[o + t];
       k = fabs(x) > tau;
     }
-    unsigned m = __ballot_sync(FULL_MASK, k);
-    if (k) {
+    if (k) row_stat_accum(grow, cc, x, s, have_diag, l1, l2);  // statistics of T^ itself
+    const bool isd = k && cc == grow;
+    const bool wr = k && !(isd && idg == 2);
+    unsigned m = __ballot_sync(FULL_MASK, wr);
+    if (wr) {
       int64_t q = dst + __popc(m & lanemask_lt());
+      if (idg == 0 && cc > grow) q += 1;  // room for the inserted diagonal
       col_out[q] = cc;
-      val_out[q] = x;
-      row_stat_accum(grow, cc, x, s, have_diag, l1, l2);
+      val_out[q] = (isd && idg == 1) ? 1.0 + x : x;
     }
     dst += __popc(m);
+    if (idg == 0) nlt += __popc(__ballot_sync(FULL_MASK, k && cc < grow));
+  }
+  if (idg == 0 && lane == 0) {
+    col_out[dst0 + nlt] = (int32_t)grow;
+    val_out[dst0 + nlt] = 1.0;
   }
   row_stat_finish(lane, w, s, have_diag, l1, l2, rs, l1r, l2r);
 }
@@ -2171,12 +3033,35 @@ void launch_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
                           const int64_t *row_cnt, const int32_t *pool_col,
                           const double *pool_val, double tau, const int64_t *rp_out,
                           int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
-                          int64_t *l2r, cudaStream_t st) {
+                          int64_t *l2r, cudaStream_t st, const int8_t *ident) {
   if (nrows == 0) return;
   KL;
   k_compact_write<<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(
       nrows, row0, row_off, row_cnt, pool_col, pool_val, tau, rp_out, col_out, val_out, rs, l1r,
-      l2r);
+      l2r, ident);
+}
+
+// out[0] += rows with ident == 0 (inserted diagonals), out[1] += rows with ident == 2
+__global__ void k_count_ident(const int8_t *ident, int64_t nrows, unsigned long long *out) {
+  unsigned long long a = 0, b = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    a += ident[i] == 0;
+    b += ident[i] == 2;
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(&out[0], a);
+    if (b) atomicAdd(&out[1], b);
+  }
+}
+void launch_count_ident(const int8_t *ident, int64_t nrows, int64_t *out2, cudaStream_t st) {
+  cudaMemsetAsync(out2, 0, 2 * sizeof(int64_t), st);
+  if (nrows == 0) return;
+  KL;
+  k_count_ident<<<grid_for(nrows, kThreads * 8, kRedBlocks), kThreads, 0, st>>>(
+      ident, nrows, reinterpret_cast<unsigned long long *>(out2));
 }
 
 __global__ void k_row_stats(CsrView C, double *rs, int64_t *l1r, int64_t *l2r) {

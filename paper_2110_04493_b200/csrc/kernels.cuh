@@ -92,6 +92,9 @@ struct NumericArgs {
   int *flags = nullptr;           // flags[0] |= 1 on pool overflow, 2 on scratch overflow
   int grid = 0;
   int64_t nlist = 0;              // rows to process: order[0..nlist) (or 0..nlist)
+  int dbg = 0;                         // experiments (grouped kernel), 0 in production
+  unsigned long long *prof = nullptr;  // optional phase clocks (grouped kernel): setup,
+                                       // products, flush, groups, union k's, failed groups
 };
 int numeric_smem_bytes(int window);
 void launch_numeric(const NumericArgs &a, cudaStream_t st);
@@ -110,6 +113,31 @@ void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_co
 int taylor_pull_smem_bytes();
 void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_rows,
                         int *fail_count, cudaStream_t st);
+// H0 as diagonals: val[di * n + k] = H0(k, k + off[di]) (0 where absent), off descending
+struct DiaView {
+  int ndiag = 0;
+  const int32_t *off = nullptr;   // device, ndiag offsets, descending
+  const double *val = nullptr;    // device, ndiag * n
+  int64_t n = 0;
+  int32_t dmin = 0, dmax = 0;
+  unsigned long long *prod_count = nullptr;  // += products (a_rk h_kj pairs) computed
+};
+constexpr int kDiaMax = 16;       // most offsets the diagonal kernel handles
+constexpr int kDiaWarpsPerCta = 4;
+// plan time: bitmap over offsets j - k + (n - 1) present in H; diagonals from offsets
+void launch_mark_offsets(const CsrView &H, unsigned *bits, int64_t n, cudaStream_t st);
+void launch_fill_dia(const CsrView &H, const int32_t *off_host, int nd, double *dia, int64_t n,
+                     cudaStream_t st);
+int taylor_dia_smem_bytes(int slots);
+// Taylor term by diagonal push (bit-identical order); rows that do not fit -> fail_rows
+void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_t *fail_rows,
+                       int *fail_count, cudaStream_t st);
+// grouped-row variant (kGroupRows rows per CTA share the B-row gathers; bit-identical
+// order); rows of groups that do not fit -> fail_rows
+constexpr int kGroupRows = 4;
+int group_smem_bytes(int slots);
+void launch_numeric_group(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
+                          cudaStream_t st);
 // hash-accumulator variant; rows whose table over-fills are appended to fail_rows
 int hash_smem_bytes();
 void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
@@ -120,6 +148,12 @@ void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_cou
 void launch_alg41_pass(const double *x, int64_t cnt, double tau, double *partial,
                        double *out, cudaStream_t st);
 
+// the same pass summed per staged row (column order) then over rows in row order:
+// independent of the order the product kernel staged rows in (run-to-run deterministic)
+void launch_alg41_pass_rows(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
+                            const double *pool_val, double tau, double *rowsum, double *partial,
+                            double *out, cudaStream_t st);
+
 // --- K4 compaction -----------------------------------------------------------------
 void launch_compact_count(int64_t nrows, const int64_t *row_off, const int64_t *row_cnt,
                           const double *pool_val, double tau, int64_t *cnt, cudaStream_t st);
@@ -129,7 +163,15 @@ void launch_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
                           const int64_t *row_cnt, const int32_t *pool_col,
                           const double *pool_val, double tau, const int64_t *rp_out,
                           int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
-                          int64_t *l2r, cudaStream_t st);
+                          int64_t *l2r, cudaStream_t st, const int8_t *ident = nullptr);
+// E = I + T^_N fused into the last compaction: counts E's rows and records per-row
+// diagonal status (0 insert 1.0, 1 write 1 + t, 2 purge) for launch_compact_write(ident).
+void launch_compact_count_ident(int64_t nrows, int64_t row0, const int64_t *row_off,
+                                const int64_t *row_cnt, const int32_t *pool_col,
+                                const double *pool_val, double tau, int64_t *cnt, int8_t *ident,
+                                cudaStream_t st);
+// out2[0] = rows whose diagonal was inserted, out2[1] = rows whose diagonal was purged
+void launch_count_ident(const int8_t *ident, int64_t nrows, int64_t *out2, cudaStream_t st);
 // per-row ||row of (I + C)||^2 and bandwidth stats for an existing CSR
 void launch_row_stats(const CsrView &C, double *rs, int64_t *l1r, int64_t *l2r,
                       cudaStream_t st);

@@ -260,7 +260,7 @@ def test_alg41_random_vs_oracle(B):
         assert d == pytest.approx(dropped_o, rel=1e-10, abs=1e-300)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("name", ["heat2d_pm10_20", "structural_24", "heat3d_9", "banded_nonsym"])
 def test_accumulator_variants(B, kernel, name):
     """Every K3 accumulator (hash, warp-window, block-window) meets parity."""
@@ -269,17 +269,17 @@ def test_accumulator_variants(B, kernel, name):
     assert_parity(Eg, st, Eo, tr)
 
 
+@pytest.mark.parametrize("kernel", [2, 4, 5, 8])
 @pytest.mark.parametrize("seed", range(4))
-def test_warp_window_bit_exact_products(B, seed):
-    """The warp-window kernel accumulates self term first, then ascending k with
-    round-to-nearest products and sums (no FMA): C~ is bit-identical to the oracle."""
+def test_bit_exact_products(B, seed, kernel):
+    """The warp-window, k-sync hash, paged and grouped kernels accumulate the self term
+    first, then ascending k with round-to-nearest products and sums (no FMA): C~ is
+    bit-identical to the oracle."""
     import torch
     n = 300
     A = _rand_csr(n, 9, 0.6, 300 + seed, empty_rows=(3, 200))
-    old = B._ctx
-    B._ctx = None
-    h = B._context()
-    (rp, ci, va), passes, tau, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(A), 2.0, 1.0, 0.0)
+    (rp, ci, va), passes, tau, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(A), 2.0, 1.0,
+                                                                  0.0, kernel=kernel)
     Ct = O.spgemm(A, A, 2.0, 1.0)
     G = from_dev(n, rp, ci, va)
     assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
@@ -298,5 +298,85 @@ def test_taylor_pull_bit_exact(B, seed):
                                                                    0.0, 3.0, 0.0)
     G = from_dev(H.n, g_rp, g_ci, g_va)
     Ct = O.spgemm(S, H, 0.0, 3.0)
+    assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
+    assert np.array_equal(G.val, Ct.val)
+
+
+@pytest.mark.parametrize("name", ["heat2d", "structural", "heat3d"])
+def test_taylor_dia_bit_exact(B, name):
+    """Unfiltered Taylor phase (filter off, N = 0) through the diagonal push kernel K5d:
+    every term S~ = S^ H0 / i accumulates k ascending with _rn products and sums, the
+    merges add exactly, so E = I + sum S^_i equals the oracle's bit for bit."""
+    from synth import structural_state_space, laplacian_3d
+    if name == "heat2d":
+        H = laplacian_2d(40, 40, 0.6, "pm10", seed=3)
+    elif name == "structural":
+        H = structural_state_space(12, 10, 0.5, seed=4)
+    else:
+        H = laplacian_3d(8, 7, 6, 0.25, "u0812", seed=5)
+    opts = dict(filter=0, force_N=0, force_M=9)
+    Eg, st = run_gpu(B, H, kernel=7, **opts)
+    Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS, **opts)
+    assert np.array_equal(Eg.rowptr, Eo.rowptr) and np.array_equal(Eg.col, Eo.col)
+    assert np.array_equal(Eg.val, Eo.val)
+    assert st["taylor_fmas"] > 0
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_taylor_dia_default_matches_pull(B, cid):
+    """Filtered runs through K5d (default) and the pull kernel (kernel=6) give the same
+    Taylor-phase patterns (both reproduce the oracle's S~ bit for bit)."""
+    H = make_config(cid)
+    _, s7 = run_gpu(B, H)
+    _, s6 = run_gpu(B, H, kernel=6)
+    M = s7["M_eff"]
+    assert M == s6["M_eff"]
+    for i in range(2, M + 1):
+        assert s7["taylor_nnz"][i] == s6["taylor_nnz"][i]
+        # the two kernels stage rows in different pool orders, so the pass sums may differ
+        # in the last bits
+        assert s7["taylor_tau"][i] == pytest.approx(s6["taylor_tau"][i], rel=1e-12)
+
+
+def _coo(n, rows, cols, vals):
+    """CSR from COO triplets, duplicate (row, col) pairs dropped (first kept)."""
+    from synth.configs import coo_to_csr
+    rows, cols = np.asarray(rows, np.int64), np.asarray(cols, np.int64)
+    _, first = np.unique(rows * n + cols, return_index=True)
+    return coo_to_csr(n, rows[first], cols[first], np.asarray(vals, np.float64)[first])
+
+
+@pytest.mark.parametrize("kernel", [8, 0])
+def test_group_kernel_long_b_rows(B, kernel):
+    """B rows longer than the grouped kernel's CTA (> 512 entries): the extra entries loop;
+    A x B + 2A is still bit-identical to the oracle."""
+    n = 3000
+    rng = np.random.default_rng(11)
+    Bm = random_banded(n, 450, 0.85, 1.0, 12)
+    rows = np.repeat(np.arange(n), 4)
+    cols = np.clip(rows + rng.integers(-40, 41, rows.size), 0, n - 1)
+    A = _coo(n, rows, cols, rng.uniform(-1, 1, rows.size))
+    assert np.diff(Bm.rowptr).max() > 512
+    (rp, ci, va), _, _, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(Bm), 2.0, 1.0, 0.0,
+                                                           kernel=kernel)
+    Ct = O.spgemm(A, Bm, 2.0, 1.0)
+    G = from_dev(n, rp, ci, va)
+    assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
+    assert np.array_equal(G.val, Ct.val)
+
+
+def test_group_kernel_fallback_wide_rows(B):
+    """Rows whose k span exceeds the grouped kernel's union bitmap fall through to the paged
+    kernel; the result is unchanged (bit-identical to the oracle)."""
+    n = 150_000
+    rng = np.random.default_rng(13)
+    rows = np.repeat(np.arange(n), 3)
+    cols = rng.integers(0, n, rows.size)
+    cols[::3] = rows[::3]
+    A = _coo(n, rows, cols, rng.uniform(-1, 1, rows.size))
+    (rp, ci, va), _, _, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(A), 2.0, 1.0, 0.0,
+                                                           kernel=8)
+    Ct = O.spgemm(A, A, 2.0, 1.0)
+    G = from_dev(n, rp, ci, va)
     assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
     assert np.array_equal(G.val, Ct.val)

@@ -24,11 +24,26 @@ def main():
     H = make_config(args.config, scale_down=args.scale or None)
     dev = torch.device("cuda", 0)
     rp, ci, va = (torch.from_numpy(x).to(dev) for x in (H.rowptr, H.col, H.val))
-    for _ in range(args.repeat):
+    for rep in range(args.repeat):
         p = B.Plan(H.n, rp, ci, va, args.eps_tol, plan_norm=args.plan_norm)
         p.run_only()
         st = p.stats()
         p.close()
+        N = int(st["N"])
+        sys.stderr.write(
+            f"repeat {rep}: plan {st['ms_plan']:.1f} taylor {st['ms_taylor']:.1f} (numeric "
+            f"{sum(st['taylor_numeric_ms']):.1f}) squaring {st['ms_squaring']:.1f} sq_numeric "
+            f"{[round(float(x), 1) for x in st['sq_numeric_ms'][1:N + 1]]} sq_first "
+            f"{[round(float(x), 1) for x in st['sq_first_ms'][1:N + 1]]} sq_fallback "
+            f"{[int(x) for x in st['sq_fallback_rows'][1:N + 1]]} cache hits/misses/releases "
+            f"{st['cache_hits']}/{st['cache_misses']}/{st['cache_releases']} cached "
+            f"{st['cache_bytes_cached'] / 1e9:.1f} GB allocated {st['cache_bytes_allocated'] / 1e9:.1f} GB\n")
+        for i in range(1, N + 1):
+            g = st["sq_group_prof"][i]
+            if g[3] > 0:
+                sys.stderr.write(f"  sq{i} group: setup {g[0] / g[3]:.0f} products {g[1] / g[3]:.0f} "
+                                 f"flush {g[2] / g[3]:.0f} clk/group, groups {g[3]:.0f}, "
+                                 f"union k/group {g[4] / g[3]:.1f}, failed {g[5]:.0f} (union {g[6]:.0f}, slots {g[7]:.0f})\n")
     M, N = int(st["M"]), int(st["N"])
     out = {k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in st.items()}
     for k, v in list(out.items()):
