@@ -90,15 +90,16 @@ typedef struct {
   int32_t force_N;        /* -1 = from Eq. (4.20) */
   int32_t output_T;       /* 0 = return E = I + T^_N (default); 1 = return T^_N */
   int32_t window_cols;    /* dense accumulator window of the block-window kernel (0 = 8192) */
-  int32_t kernel;         /* K3 accumulator: 0 auto (grouped rows for squarings; for Taylor
+  int32_t kernel;         /* K3 accumulator: 0 auto (k-sync paged for squarings; for Taylor
                              terms the diagonal push kernel when H0 has <= 16 distinct
                              diagonal offsets, else the pull over H0^T), 1 atomic hash,
                              2 warp-window, 3 block-window, 4 k-synchronous hash, 5 k-synchronous
                              paged, 6 Taylor pull (Taylor terms only; else 1), 7 Taylor diagonal
                              push (Taylor terms only; else as 0), 8 grouped rows (4 rows per
-                             CTA share each B-row gather).  All meet parity; 2, 4, 5, 6, 7 and 8
+                             CTA share each B-row gather, TMA-staged), 9 one warp per row (8
+                             rows per CTA share a page table).  All meet parity; 2 and 4-9
                              reproduce the oracle's C~ bit for bit.  Rows a kernel cannot hold
-                             fall through 8 -> 5 -> 3, 7 -> 6 -> 1 -> 3 and 1/4/5 -> 3. */
+                             fall through 8/9 -> 5 -> 3, 7 -> 6 -> 1 -> 3 and 1/4/5 -> 3. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */
@@ -143,8 +144,9 @@ typedef struct {
   double sq_first_ms[SEXPM_MAXSTEP];           /* device time of the squaring's first kernel */
   /* grouped kernel (kernel 8) per squaring: summed SM clocks of its setup / product / flush
    * phases over all groups, groups processed, union k's, groups handed on (all causes, union
-   * too large, slots full) */
-  double sq_group_prof[SEXPM_MAXSTEP][8];
+   * too large, slots full), then thread-0 clocks of the product loop: ring wait, rest of
+   * stage A, stage B, barrier */
+  double sq_group_prof[SEXPM_MAXSTEP][12];
   /* the library's device-block cache during the last sexpm_plan + sexpm_run (process-wide) */
   int64_t cache_hits, cache_misses, cache_releases;
   double cache_bytes_cached, cache_bytes_allocated;

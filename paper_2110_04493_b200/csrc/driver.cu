@@ -317,7 +317,7 @@ struct StepReport {
   double numeric_bytes = 0.0;
   int64_t window_rows = 0;
   float first_ms = 0.f;  // the first kernel of the fallback chain alone
-  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // grouped kernel phase clocks
+  unsigned long long prof[12] = {0};  // grouped kernel phase clocks
 };
 
 struct Workspace {
@@ -356,10 +356,13 @@ struct sexpm_plan_s {
   DBuf<unsigned long long> dia_prod;
   int dia_slots = 1152;
   int group_slots = 4096;
+  int rowwarp_slots = 3072;
   long long cache0[3] = {0, 0, 0};  // cache counters when the plan was created
   DCsr T, Tn, S, Sn, Bhalo, Ibuf, E;  // persistent (grow-only) iterates
   int32_t retries = 0;
   DBuf<int32_t> proc_order;  // K3 row processing order (cluster order of H's graph)
+  DBuf<int32_t> group_start;  // grouped kernel: group boundaries in proc_order
+  int64_t ngroups = 0;
   bool have_result = false;
   int M = 0, N = 0, normal = 0, M_eff = 0;
   double norm = 0.0, a = 0.0, eps_g0 = 0.0;
@@ -571,7 +574,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     const bool taylor_pull_ok = self == 0.0 && BT != nullptr && BT->rp.p != nullptr;
     // the grouped kernel stages B rows with TMA bulk copies: 16-byte aligned B arrays
     const bool group_ok = ((uintptr_t)B.col % 16 == 0) && ((uintptr_t)B.val % 16 == 0);
-    if (kern == 0) kern = self != 0.0 ? (group_ok ? 8 : 5) : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
+    // squarings: the k-synchronous paged kernel (measured fastest on configs 2, 3 and 5;
+    // the grouped kernels 8 / 9 are options)
+    if (kern == 0) kern = self != 0.0 ? 5 : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
     if (kern == 8 && !group_ok) kern = 5;
     if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 1;
     if (kern == 6 && !taylor_pull_ok) kern = 1;
@@ -636,15 +641,26 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         } else if (stage == 5) {
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
-        } else if (stage == 8) {
-          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kGroupRows - 1) / kGroupRows,
+        } else if (stage == 9) {
+          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kRowWarpRows - 1) / kRowWarpRows,
                                                                 (int64_t)P.sm_count));
           w.prof.ensure(8, st);
           CK(cudaMemsetAsync(w.prof.p, 0, 8 * sizeof(unsigned long long), st));
           nh.prof = w.prof.p;
-          if (const char *e = getenv("SEXPM_DEBUG_GROUP")) nh.dbg = atoi(e);
-          launch_numeric_group(nh, P.group_slots, fout, w.fail_count.p, st);
+          launch_numeric_rowwarp(nh, P.rowwarp_slots, fout, w.fail_count.p, st);
           CK(cudaMemcpyAsync(rep.prof, w.prof.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        } else if (stage == 8) {
+          if (use_cluster && list == P.proc_order.p && nlist == nr) {
+            nh.gstart = P.group_start.p;
+            nh.ngroups = P.ngroups;
+          }
+          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kGroupRows - 1) / kGroupRows,
+                                                                (int64_t)P.sm_count));
+          w.prof.ensure(16, st);
+          CK(cudaMemsetAsync(w.prof.p, 0, 16 * sizeof(unsigned long long), st));
+          nh.prof = w.prof.p;
+          launch_numeric_group(nh, P.group_slots, fout, w.fail_count.p, st);
+          CK(cudaMemcpyAsync(rep.prof, w.prof.p, 12 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         } else if (stage == 7) {
           DiaView D;
           D.ndiag = P.dia_nd;
@@ -673,7 +689,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         list = fout;
         nlist = nf;
         fb ^= 1;
-        stage = stage == 7 ? (taylor_pull_ok ? 6 : 1) : (stage == 6 ? 1 : (stage == 8 ? 5 : 3));
+        stage = stage == 7 ? (taylor_pull_ok ? 6 : 1) : (stage == 6 ? 1 : ((stage == 8 || stage == 9) ? 5 : 3));
       }
     }
     rep.window_rows = nfail;
@@ -1262,6 +1278,18 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     P.proc_order.ensure(std::max<size_t>(ord.size(), 1), st);
     if (!ord.empty())
       CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    // groups of the grouped kernel: up to kGroupRows consecutive entries of the order, cut
+    // where the row index jumps (rows far apart share few B rows and overflow the union)
+    std::vector<int32_t> gs;
+    for (size_t j = 0; j < ord.size(); j++) {
+      const bool cut = j == 0 || (int)(j - (size_t)gs.back()) >= kGroupRows ||
+                       std::abs((long long)ord[j] - (long long)ord[j - 1]) > 2;
+      if (cut) gs.push_back((int32_t)j);
+    }
+    P.ngroups = (int64_t)gs.size();
+    gs.push_back((int32_t)ord.size());
+    P.group_start.ensure(gs.size(), st);
+    CK(cudaMemcpyAsync(P.group_start.p, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
   }
   CK(cudaEventRecord(e1, st));
@@ -1414,7 +1442,7 @@ static void do_run(sexpm_plan_s &P) {
       S.sq_numeric_bytes[i] = rep.numeric_bytes;
       S.sq_fallback_rows[i] = rep.window_rows;
       S.sq_first_ms[i] = rep.first_ms;
-      for (int q = 0; q < 8; q++) S.sq_group_prof[i][q] = (double)rep.prof[q];
+      for (int q = 0; q < 12; q++) S.sq_group_prof[i][q] = (double)rep.prof[q];
       S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)dst.nnz + 16.0 * (double)nl;
     }
     normIT = sqrt(rep.normIT2);
@@ -1584,6 +1612,8 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
   }
   while (P->group_slots > 512 && group_smem_bytes(P->group_slots) > (int)prop.sharedMemPerBlockOptin - 4096)
     P->group_slots -= 512;
+  while (P->rowwarp_slots > 512 && rowwarp_smem_bytes(P->rowwarp_slots) > (int)prop.sharedMemPerBlockOptin - 4096)
+    P->rowwarp_slots -= 256;
   int window = P->o.window_cols > 0 ? P->o.window_cols : 8192;
   int smem = numeric_smem_bytes(window);
   REQUIRE(smem <= (int)prop.sharedMemPerBlockOptin - 2048, SEXPM_EINVAL, "window too large");

@@ -1937,18 +1937,18 @@ void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_r
 constexpr int kGG = 4;
 constexpr int kGThreads = 256;
 constexpr int kGWarps = kGThreads / 32;
-constexpr int kGPages = 12288;     // direct page table over the group's output span
+constexpr int kGPages = 6144;      // direct page table over the group's output span
 constexpr int kGKWords = 1536;     // union-k bitmap words (k span <= 49152)
 constexpr int kGKCap = 1024;       // union k's per group
-constexpr int kGRing = 4;          // B rows in flight (TMA bulk copies)
-constexpr int kGRowCap = 768;      // longest B row staged in the ring (longer: global loads)
+constexpr int kGRing = 8;          // B rows in flight (TMA bulk copies)
+constexpr int kGRowCap = 512;      // longest B row staged in the ring (longer: global loads)
 constexpr int kGRingCols = kGRowCap + 8, kGRingVals = kGRowCap + 4;
 constexpr uint16_t kGNone = 0xFFFF, kGOver = 0xFFFE;
 
 int group_smem_bytes(int slots) {
   return slots * kGG * 8 + kGRing * (kGRingVals * 8 + kGRingCols * 4) + kGKCap * kGG * 8 +
          kGKCap * 8 + kGKCap * 4 + kGPages * 2 + (kGPages / 32) * 4 + kGKWords * 4 +
-         kGKWords * 2 + (slots >> 3) * 2 + kGRing * 8 + 64;
+         kGKWords * 2 + (slots >> 3) * 2 + 2 * kGRing * 8 + 64;
 }
 
 // mbarrier + TMA bulk copy helpers (sm_90+ PTX, here sm_100a)
@@ -2030,16 +2030,31 @@ __device__ __forceinline__ void gblock_scan4(T (&v)[kGG], T (&tot)[kGG], T *sbuf
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, int slots,
-                                                                int32_t *fail_rows,
-                                                                int *fail_count) {
+// consumer-only barrier (named barrier 1: the kGThreads consumer threads; the producer
+// warp never takes part)
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kGThreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// kGWarps consumer warps + 1 producer warp.  The producer (lane 0 of the last warp) stages
+// the union's B rows into the ring (TMA bulk copies, `full` mbarriers) as slots are
+// released (`empty` mbarriers); the consumers never wait on global memory latency inside a
+// product step.  Setup and flush run on the consumers; the producer only joins the CTA
+// barriers around them (ct = its "thread index" for work loops, out of range).
+__global__ void __launch_bounds__(kGThreads + 32, 1) k_numeric_group(NumericArgs a, int slots,
+                                                                     int32_t *fail_rows,
+                                                                     int *fail_count) {
   extern __shared__ double gsm[];
   double *acc = gsm;                                                     // kGG * slots (row-major)
   double *rval = acc + (size_t)slots * kGG;                              // kGRing * kGRingVals
   double *coef = rval + kGRing * kGRingVals;                             // kGKCap * kGG
   long long *kst = reinterpret_cast<long long *>(coef + kGKCap * kGG);   // kGKCap
-  uint64_t *bars = reinterpret_cast<uint64_t *>(kst + kGKCap);           // kGRing
-  int32_t *kln = reinterpret_cast<int32_t *>(bars + kGRing);             // kGKCap
+  uint64_t *fullb = reinterpret_cast<uint64_t *>(kst + kGKCap);          // kGRing
+  uint64_t *emptyb = fullb + kGRing;                                     // kGRing
+  int32_t *kln = reinterpret_cast<int32_t *>(emptyb + kGRing);           // kGKCap
   int32_t *rcol = kln + kGKCap;                                          // kGRing * kGRingCols
   uint16_t *ptab = reinterpret_cast<uint16_t *>(rcol + kGRing * kGRingCols);  // kGPages
   unsigned *pbits = reinterpret_cast<unsigned *>(ptab + kGPages);        // kGPages / 32
@@ -2050,22 +2065,27 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
   __shared__ long long s_p0[kGG], s_p1[kGG];
   __shared__ int64_t s_r[kGG];
   __shared__ int s_ng, s_kmin, s_kmax, s_lo, s_hi;
-  __shared__ long long s_scan[kGWarps * kGG];
+  __shared__ long long s_scan[(kGWarps + 1) * kGG];
   __shared__ double s_fs[kGWarps * kGG];
   __shared__ unsigned long long s_off[kGG];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
-  for (int i = tid; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
-  for (int i = tid; i < kGPages; i += kGThreads) ptab[i] = kGNone;
-  for (int i = tid; i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
-  for (int i = tid; i < kGKWords; i += kGThreads) kbits[i] = 0u;
+  const bool producer = warp == kGWarps;
+  const int ct = producer ? (1 << 28) : tid;  // consumer thread index for work loops
+  for (int i = ct; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
+  for (int i = ct; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
+  for (int i = ct; i < kGPages; i += kGThreads) ptab[i] = kGNone;
+  for (int i = ct; i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
+  for (int i = ct; i < kGKWords; i += kGThreads) kbits[i] = 0u;
   if (tid == 0) {
-    for (int d = 0; d < kGRing; d++) mbar_init(&bars[d], 1);
+    for (int d = 0; d < kGRing; d++) {
+      mbar_init(&fullb[d], 1);
+      mbar_init(&emptyb[d], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  unsigned phase = 0;  // bit d: parity of ring slot d's next completion (uniform)
-  const int64_t ngroups = (a.nlist + kGG - 1) / kGG;
+  unsigned long long used = 0;  // ring uses so far (slot = used % kGRing), uniform per role
+  const int64_t ngroups = a.gstart ? a.ngroups : (a.nlist + kGG - 1) / kGG;
   for (;;) {
     __syncthreads();
     if (tid == 0) s_grp = atomicAdd(a.row_counter, 1);
@@ -2073,12 +2093,16 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
     const int64_t grp = s_grp;
     if (grp >= ngroups) break;
     long long t_0 = clock64();
-    // ---- group rows, spans ----
+    // ---- group rows (plan-time group boundaries, else kGG consecutive list entries) ----
     if (tid < kGG) {
-      const int64_t idx = grp * kGG + tid;
+      int64_t idx = grp * kGG + tid, iend = a.nlist;
+      if (a.gstart) {
+        idx = (int64_t)a.gstart[grp] + tid;
+        iend = a.gstart[grp + 1];
+      }
       int64_t r = -1;
       long long p0 = 0, p1 = 0;
-      if (idx < a.nlist) {
+      if (idx < iend) {
         r = a.order ? (int64_t)a.order[idx] : idx;
         p0 = a.A.rp[r];
         p1 = a.A.rp[r + 1];
@@ -2112,7 +2136,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
       s_nk = 0;
       int fail = 0;  // 1: k span, 2: output span, 3: union size, 4: slots
       if (kmax >= kmin && (int64_t)kmax - kmin + 1 > (int64_t)kGKWords * 32) fail = 1;
-      if (hi >= lo && (((int64_t)hi >> 6) - ((int64_t)lo >> 6) + 1) > kGPages) fail = 2;
+      if (hi >= lo && (((int64_t)hi >> 7) - ((int64_t)lo >> 7) + 1) > kGPages) fail = 2;
       s_fail = fail;
     }
     __syncthreads();
@@ -2127,20 +2151,21 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
       }
       continue;
     }
-    int sh = 3;
+    // pages of >= 16 columns: the cells of consecutive columns fall in distinct banks
+    int sh = 4;
     {
       const int64_t lo = s_lo, hi = s_hi;
-      while (sh < 6 && ((hi >> sh) - (lo >> sh) + 1) > kGPages) sh++;
+      while (sh < 7 && ((hi >> sh) - (lo >> sh) + 1) > kGPages) sh++;
     }
     const int pmask = (1 << sh) - 1;
     const int64_t pg0 = (int64_t)s_lo >> sh;
     const int npg = (int)(((int64_t)s_hi >> sh) - pg0 + 1);
-    const int bcap = slots >> sh;  // page blocks of this size that fit
+    const int bcap = (slots - 32) >> sh;  // page blocks that fit (dummy cells after)
     const int kmin = s_kmin;
     // ---- union of k: bitmap, ranks, coefficients, B-row extents ----
     if (!s_fail) {
       for (int g = 0; g < ng; g++) {
-        for (long long p = s_p0[g] + tid; p < s_p1[g]; p += kGThreads) {
+        for (long long p = s_p0[g] + ct; p < s_p1[g]; p += kGThreads) {
           const int kb = a.A.col[p] - kmin;
           atomicOr(&kbits[kb >> 5], 1u << (kb & 31));
         }
@@ -2150,7 +2175,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
     const int nkw = s_fail ? 0 : ((s_kmax - kmin) >> 5) + 1;
     {
       const int per = (nkw + kGThreads - 1) / kGThreads;
-      const int w0 = min(tid * per, nkw), w1 = min(w0 + per, nkw);
+      const int w0 = producer ? nkw : min(tid * per, nkw), w1 = min(w0 + per, nkw);
       long long c[kGG] = {0, 0, 0, 0}, tot[kGG];
       for (int w = w0; w < w1; w++) c[0] += __popc(kbits[w]);
       gblock_scan4<long long>(c, tot, s_scan);
@@ -2168,7 +2193,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
     const int nk = s_fail ? 0 : s_nk;
     if (!s_fail) {
       for (int g = 0; g < ng; g++) {
-        for (long long p = s_p0[g] + tid; p < s_p1[g]; p += kGThreads) {
+        for (long long p = s_p0[g] + ct; p < s_p1[g]; p += kGThreads) {
           const int k = a.A.col[p];
           const int kb = k - kmin;
           const int rk = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
@@ -2185,30 +2210,10 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
         }
       }
     }
-    __syncthreads();
-    // ring: union row q is staged in slot q % kGRing with two bulk copies (cols and values,
-    // widened to 16-byte boundaries) issued by lane 0 of warp q % kGWarps (spread over the
-    // warps, so no warp is late at every barrier)
-    auto issue = [&](int q) {
-      if (a.dbg == 4) return;
-      if (q < nk && kln[q] <= kGRowCap) {
-        const int d = q % kGRing;
-        const long long b0 = kst[q];
-        const int ln = kln[q];
-        const long long ca = b0 & ~3LL, va = b0 & ~1LL;
-        const unsigned cb = (unsigned)(((b0 + ln + 3) & ~3LL) - ca) * 4u;
-        const unsigned vb = (unsigned)(((b0 + ln + 1) & ~1LL) - va) * 8u;
-        mbar_expect_tx(&bars[d], cb + vb);
-        if (cb) tma_bulk_g2s(rcol + d * kGRingCols, a.B.col + ca, cb, &bars[d]);
-        if (vb) tma_bulk_g2s(rval + d * kGRingVals, a.B.val + va, vb, &bars[d]);
-      }
-    };
-    if (lane == 0 && warp < kGRing)
-      for (int q = warp; q < kGRing; q += kGWarps) issue(q);
     // ---- self term (the 2T of Eq. 2.7), before any product ----
     if (!s_fail && a.self_coef != 0.0) {
       for (int g = 0; g < ng; g++) {
-        for (long long p = s_p0[g] + tid; p < s_p1[g]; p += kGThreads) {
+        for (long long p = s_p0[g] + ct; p < s_p1[g]; p += kGThreads) {
           const int rel = (int)(a.A.col[p] - (pg0 << sh));
           const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
           if (b >= 0) acc[(size_t)g * slots + (b << sh) + (rel & pmask)] = __dmul_rn(a.self_coef, a.A.val[p]);
@@ -2216,67 +2221,173 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
         }
       }
     }
+    __syncthreads();  // kst / kln / coef / self term ready
     long long t_1 = clock64();
-    // ---- products: union k ascending, one barrier per k ----
-    // Every union row k is applied to all kGG rows (a row without k adds 0 * b_kj, which
-    // leaves its cells bit-identical); entries tid and tid + kGThreads per thread.
-    const int cbase = (int)(pg0 << sh);
-    __syncthreads();
-    for (int kk = 0; kk < nk; kk++) {
-      const int d = kk % kGRing;
-      const int ln = kln[kk];
-      const long long b0 = kst[kk];
-      const bool staged = ln <= kGRowCap;
-      if (staged && a.dbg != 4) {
-        mbar_wait(&bars[d], (phase >> d) & 1u);
-        phase ^= 1u << d;
-      }
-      if (!s_fail) {
-        const double2 c01 = *reinterpret_cast<const double2 *>(&coef[kk * kGG]);
-        const double2 c23 = *reinterpret_cast<const double2 *>(&coef[kk * kGG + 2]);
-        // one entry: slot lookup (page claimed on first touch), then the kGG cells of the
-        // group's rows, loads before stores
-        auto apply = [&](int32_t c, double v) {
-          const int rel = c - cbase;
-          if (a.dbg == 1 || a.dbg == 4) return;
-          const int b = a.dbg == 2 ? (int)ptab[rel >> sh] : group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
-          if (a.dbg == 3) {
-            if (b >= 0) acc[(b << sh) + (rel & pmask)] += v;
-            return;
+    if (producer) {
+      // ---- producer: stage union row q in slot (used + q) % kGRing (two bulk copies, cols
+      // and values widened to 16-byte boundaries; rows longer than a slot only complete
+      // the phase and are read from global memory by the consumers) ----
+      if (lane == 0) {
+        for (int q = 0; q < nk; q++) {
+          const unsigned long long u = used + q;
+          const int d = (int)(u % kGRing);
+          if (u >= kGRing) mbar_wait(&emptyb[d], (unsigned)((u / kGRing - 1) & 1));
+          const int ln = kln[q];
+          if (ln <= kGRowCap && ln > 0) {
+            const long long b0 = kst[q];
+            const long long ca = b0 & ~3LL, va = b0 & ~1LL;
+            const unsigned cb = (unsigned)(((b0 + ln + 3) & ~3LL) - ca) * 4u;
+            const unsigned vb = (unsigned)(((b0 + ln + 1) & ~1LL) - va) * 8u;
+            mbar_expect_tx(&fullb[d], cb + vb);
+            tma_bulk_g2s(rcol + d * kGRingCols, a.B.col + ca, cb, &fullb[d]);
+            tma_bulk_g2s(rval + d * kGRingVals, a.B.val + va, vb, &fullb[d]);
+          } else {
+            mbar_arrive(&fullb[d]);
           }
-          if (b < 0) {
-            s_fail = 4;
-            return;
-          }
-          const int o = (b << sh) + (rel & pmask);
-          const double x0 = acc[o], x1 = acc[slots + o], x2 = acc[2 * slots + o], x3 = acc[3 * slots + o];
-          acc[o] = __dadd_rn(x0, __dmul_rn(c01.x, v));
-          acc[slots + o] = __dadd_rn(x1, __dmul_rn(c01.y, v));
-          acc[2 * slots + o] = __dadd_rn(x2, __dmul_rn(c23.x, v));
-          acc[3 * slots + o] = __dadd_rn(x3, __dmul_rn(c23.y, v));
-        };
-        if (staged) {  // entries from the shared-memory ring
-          const int cb = d * kGRingCols + (int)(b0 & 3), vb = d * kGRingVals + (int)(b0 & 1);
-          if (tid < ln) {
-            const int32_t c0 = rcol[cb + tid];
-            const double v0 = rval[vb + tid];
-            if (tid + kGThreads < ln) {
-              const int32_t c1 = rcol[cb + tid + kGThreads];
-              const double v1 = rval[vb + tid + kGThreads];
-              apply(c0, v0);
-              apply(c1, v1);
-            } else {
-              apply(c0, v0);
-            }
-            for (int e = tid + 2 * kGThreads; e < ln; e += kGThreads) apply(rcol[cb + e], rval[vb + e]);
-          }
-        } else {  // rows longer than the ring slot: straight from global memory
-          for (int e = tid; e < ln; e += kGThreads) apply(a.B.col[b0 + e], a.B.val[b0 + e]);
         }
       }
-      __syncthreads();  // one writer per cell (k -> next k); ring slot d free again
-      if (lane == 0 && warp == (kk + kGRing) % kGWarps) issue(kk + kGRing);
+    } else {
+      // ---- consumers: union k ascending, one (consumer) barrier per k.  Every union row
+      // k is applied to all kGG rows (a row without k adds 0 * b_kj, which leaves its cells
+      // bit-identical).  Thread t takes entries t and t + kGThreads of B row k (longer rows:
+      // the rest from global memory).  A step is interleaved by hand (warps issue in
+      // order): the next row's metadata, this row's cell loads, the next row's entries, this
+      // row's multiply-adds and stores, the next row's slot lookups (the branchy part).
+      // Cells of inactive entries go to a lane-private dummy cell past the claimable slots
+      // (never flushed) with value 0, and the first-touch page claim is a warp-uniform slow
+      // path, so the common path has no per-lane branches.
+      const int cbase = (int)(pg0 << sh);
+      long long pw = 0, pa = 0, pbar = 0;  // thread-0 clocks: ring wait, steps, barrier
+      const int dummy = slots - 32;
+      double *acc1 = acc + slots, *acc2 = acc + 2 * slots, *acc3 = acc + 3 * slots;
+      struct Step {
+        int o0, o1;
+        double v0, v1;
+        double2 k01, k23;
+      };
+      auto slot_of = [&](int32_t c, bool on, int dflt) -> int {
+        const int rel = c - cbase;
+        int b = on ? (int)ptab[rel >> sh] : 0;
+        const bool need = on && b >= (int)kGOver;
+        if (__any_sync(FULL_MASK, need)) {
+          if (need) b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
+          if (on && b < 0) s_fail = 4;
+        }
+        return (on && b >= 0) ? (b << sh) + (rel & pmask) : dflt;
+      };
+      auto rmw = [&](int o, double v, const double2 &k01, const double2 &k23) {
+        const double x0 = acc[o], x1 = acc1[o], x2 = acc2[o], x3 = acc3[o];
+        acc[o] = __dadd_rn(x0, __dmul_rn(k01.x, v));
+        acc1[o] = __dadd_rn(x1, __dmul_rn(k01.y, v));
+        acc2[o] = __dadd_rn(x2, __dmul_rn(k23.x, v));
+        acc3[o] = __dadd_rn(x3, __dmul_rn(k23.y, v));
+      };
+      // stage A of row q: wait for the staged row, read its entries and a_gk, look up slots
+      auto stage_a = [&](int q, Step &S) {
+        const int ln = kln[q];
+        const long long b0 = kst[q];
+        S.k01 = *reinterpret_cast<const double2 *>(&coef[q * kGG]);
+        S.k23 = *reinterpret_cast<const double2 *>(&coef[q * kGG + 2]);
+        const bool h0 = tid < ln, h1 = tid + kGThreads < ln;
+        int32_t ca = cbase, cb = cbase;
+        S.v0 = 0.0;
+        S.v1 = 0.0;
+        const unsigned long long u = used + q;
+        const int d = (int)(u % kGRing);
+        const long long tw0 = clock64();
+        mbar_wait(&fullb[d], (unsigned)((u / kGRing) & 1));
+        pw += clock64() - tw0;
+        if (ln <= kGRowCap) {
+          const int cbo = d * kGRingCols + (int)(b0 & 3), vbo = d * kGRingVals + (int)(b0 & 1);
+          if (h0) {
+            ca = rcol[cbo + tid];
+            S.v0 = rval[vbo + tid];
+          }
+          if (h1) {
+            cb = rcol[cbo + tid + kGThreads];
+            S.v1 = rval[vbo + tid + kGThreads];
+          }
+        } else {
+          if (h0) {
+            ca = a.B.col[b0 + tid];
+            S.v0 = a.B.val[b0 + tid];
+          }
+          if (h1) {
+            cb = a.B.col[b0 + tid + kGThreads];
+            S.v1 = a.B.val[b0 + tid + kGThreads];
+          }
+        }
+        S.o0 = __any_sync(FULL_MASK, h0) ? slot_of(ca, h0, dummy + lane) : -1;
+        S.o1 = __any_sync(FULL_MASK, h1) ? slot_of(cb, h1, dummy + lane) : -1;
+      };
+      auto step = [&](int k, Step &C, Step &Nx) {
+        double x00 = 0.0, x01 = 0.0, x02 = 0.0, x03 = 0.0, x10 = 0.0, x11 = 0.0, x12 = 0.0, x13 = 0.0;
+        if (C.o0 >= 0) {
+          x00 = acc[C.o0];
+          x01 = acc1[C.o0];
+          x02 = acc2[C.o0];
+          x03 = acc3[C.o0];
+        }
+        if (C.o1 >= 0) {
+          x10 = acc[C.o1];
+          x11 = acc1[C.o1];
+          x12 = acc2[C.o1];
+          x13 = acc3[C.o1];
+        }
+        if (k + 1 < nk) stage_a(k + 1, Nx);
+        if (C.o0 >= 0) {
+          acc[C.o0] = __dadd_rn(x00, __dmul_rn(C.k01.x, C.v0));
+          acc1[C.o0] = __dadd_rn(x01, __dmul_rn(C.k01.y, C.v0));
+          acc2[C.o0] = __dadd_rn(x02, __dmul_rn(C.k23.x, C.v0));
+          acc3[C.o0] = __dadd_rn(x03, __dmul_rn(C.k23.y, C.v0));
+        }
+        if (C.o1 >= 0) {
+          acc[C.o1] = __dadd_rn(x10, __dmul_rn(C.k01.x, C.v1));
+          acc1[C.o1] = __dadd_rn(x11, __dmul_rn(C.k01.y, C.v1));
+          acc2[C.o1] = __dadd_rn(x12, __dmul_rn(C.k23.x, C.v1));
+          acc3[C.o1] = __dadd_rn(x13, __dmul_rn(C.k23.y, C.v1));
+        }
+        const int ln = kln[k];
+        if (ln > 2 * kGThreads) {  // rows longer than 2 x CTA: the rest from global memory
+          const long long b0 = kst[k];
+          for (int e = tid + 2 * kGThreads; e < ln; e += kGThreads) {
+            const int rel = a.B.col[b0 + e] - cbase;
+            const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
+            if (b >= 0) rmw((b << sh) + (rel & pmask), a.B.val[b0 + e], C.k01, C.k23);
+            else s_fail = 4;
+          }
+        }
+      };
+      // the slot of row q is free once every consumer passed the barrier after its stage A
+      auto release = [&](int q) {
+        if (tid == 0) mbar_arrive(&emptyb[(int)((used + q) % kGRing)]);
+      };
+      Step X, Y;
+      X.o0 = X.o1 = Y.o0 = Y.o1 = -1;
+      X.v0 = X.v1 = Y.v0 = Y.v1 = 0.0;
+      if (nk > 0) stage_a(0, X);
+      long long tc = clock64(), tn;
+      for (int kk = 0; kk < nk; kk += 2) {
+        step(kk, X, Y);
+        tn = clock64(); pa += tn - tc; tc = tn;
+        consumer_sync();  // one writer per cell (k -> next k)
+        if (kk == 0) release(0);
+        if (kk + 1 < nk) release(kk + 1);
+        tn = clock64(); pbar += tn - tc; tc = tn;
+        if (kk + 1 >= nk) break;
+        step(kk + 1, Y, X);
+        tn = clock64(); pa += tn - tc; tc = tn;
+        consumer_sync();
+        if (kk + 2 < nk) release(kk + 2);
+        tn = clock64(); pbar += tn - tc; tc = tn;
+      }
+      if (a.prof && tid == 0) {
+        atomicAdd(&a.prof[8], (unsigned long long)pw);
+        atomicAdd(&a.prof[9], (unsigned long long)(pa - pw));
+        atomicAdd(&a.prof[11], (unsigned long long)pbar);
+      }
     }
+    used += nk;
     __syncthreads();
     long long t_2 = clock64();
     const int failed = s_fail;
@@ -2285,7 +2396,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
     {
       const int nw = failed ? 0 : (npg + 31) >> 5;
       const int per = (nw + kGThreads - 1) / kGThreads;
-      const int w0 = min(tid * per, nw), w1 = min(w0 + per, nw);
+      const int w0 = producer ? nw : min(tid * per, nw), w1 = min(w0 + per, nw);
       long long c[kGG] = {0, 0, 0, 0}, tot[kGG];
       for (int w = w0; w < w1; w++) c[0] += __popc(pbits[w]);
       gblock_scan4<long long>(c, tot, s_scan);
@@ -2303,7 +2414,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
     __syncthreads();
     const int total = npl << sh;
     const int per = (total + kGThreads - 1) / kGThreads;
-    const int q0 = min(tid * per, total), q1 = min(q0 + per, total);
+    const int q0 = producer ? total : min(tid * per, total), q1 = min(q0 + per, total);
     long long nst[kGG] = {0, 0, 0, 0}, nnzu[kGG] = {0, 0, 0, 0}, tot[kGG];
     double fs[kGG] = {0.0, 0.0, 0.0, 0.0};
     for (int q = q0; q < q1; q++) {
@@ -2327,7 +2438,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
     for (int g = 0; g < kGG; g++) {
       const double f = warp_sum(fs[g]);
       const long long z = warp_sum(nnzu[g]);
-      if (lane == 0) {
+      if (lane == 0 && !producer) {
         s_fs[warp * kGG + g] = f;
         s_scan[warp * kGG + g] = z;
       }
@@ -2384,21 +2495,21 @@ __global__ void __launch_bounds__(kGThreads, 1) k_numeric_group(NumericArgs a, i
     __syncthreads();
     // ---- reset the group's state ----
     if (!failed) {
-      for (int q = tid; q < total; q += kGThreads) {
+      for (int q = ct; q < total; q += kGThreads) {
         const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
 #pragma unroll
         for (int g = 0; g < kGG; g++) acc[(size_t)g * slots + o] = 0.0;
       }
       __syncthreads();
-      for (int i = tid; i < npl; i += kGThreads) ptab[plist[i]] = kGNone;
-      for (int i = tid; i < nk * kGG; i += kGThreads) coef[i] = 0.0;
+      for (int i = ct; i < npl; i += kGThreads) ptab[plist[i]] = kGNone;
+      for (int i = ct; i < nk * kGG; i += kGThreads) coef[i] = 0.0;
     } else {
-      for (int i = tid; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
-      for (int i = tid; i < kGPages; i += kGThreads) ptab[i] = kGNone;
-      for (int i = tid; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
+      for (int i = ct; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
+      for (int i = ct; i < kGPages; i += kGThreads) ptab[i] = kGNone;
+      for (int i = ct; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
     }
-    for (int i = tid; i < ((npg + 31) >> 5) && i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
-    for (int i = tid; i < kGKWords; i += kGThreads) kbits[i] = 0u;
+    for (int i = ct; i < ((npg + 31) >> 5) && i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
+    for (int i = ct; i < kGKWords; i += kGThreads) kbits[i] = 0u;
     if (failed && tid < ng) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)s_r[tid];
     if (a.prof && tid == 0) {
       const long long t_3 = clock64();
@@ -2420,7 +2531,375 @@ void launch_numeric_group(const NumericArgs &a, int slots, int32_t *fail_rows, i
   const int smem = group_smem_bytes(slots);
   cudaFuncSetAttribute(k_numeric_group, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
-  k_numeric_group<<<a.grid, kGThreads, smem, st>>>(a, slots, fail_rows, fail_count);
+  k_numeric_group<<<a.grid, kGThreads + 32, smem, st>>>(a, slots, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
+// K3r numeric filtered SpGEMM, ONE WARP PER ROW, kRG rows per CTA sharing a page table:
+//
+//   C~(r,:) = self_coef * A(r,:) + sum_k a_rk B(k,:)    (Eq. 2.7 P:76 / Eq. 4.15)
+//
+// Warp g owns row r_g of a group of kRG rows that are close in the processing order, and
+// its cells acc[g][slot] (single writer: no atomics on values, no CTA barrier per k).  The
+// warp walks its own k ascending; for each k the lanes take the B row's entries in passes
+// of 32 x kRChunks, issuing all loads of a pass, then all slot lookups, then all cell
+// reads, then the _rn multiply-adds, then all stores (entries of one B row have distinct
+// columns, so the chains overlap); __syncwarp orders consecutive k.  Each cell sees the
+// self term first, then ascending k: C~ is bit-identical to the oracle's.
+// The kRG warps walk similar k sets at similar pace; a CTA barrier every kRSync k keeps
+// them close, so the B rows one warp gathers from L2 are still in L1 for the others.
+// Pages of 2^sh columns of the group's output span are claimed on first touch (shared
+// page table); the flush walks the claimed pages in column order (rows come out sorted),
+// classifies against the Algorithm 4.1 floor and stages each row contiguously.
+// ------------------------------------------------------------------------------------
+constexpr int kRG = 8;
+constexpr int kRThreads = kRG * 32;
+constexpr int kRPages = 12288;
+constexpr int kRSync = 4;
+constexpr int kRChunks = 8;
+
+int rowwarp_smem_bytes(int slots) {
+  return slots * kRG * 8 + kRPages * 2 + (kRPages / 32) * 4 + (slots >> 3) * 2 + 64;
+}
+
+template <int G, int NW, typename T>
+__device__ __forceinline__ void block_scan_g(T (&v)[G], T (&tot)[G], T *sbuf /* [NW][G] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T incl[G];
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    T x = v[g];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(FULL_MASK, x, o);
+      if (lane >= o) x += y;
+    }
+    incl[g] = x;
+    if (lane == 31) sbuf[warp * G + g] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    T pre = 0, t = 0;
+    for (int w = 0; w < NW; w++) {
+      const T y = sbuf[w * G + g];
+      if (w < warp) pre += y;
+      t += y;
+    }
+    tot[g] = t;
+    v[g] = pre + incl[g] - v[g];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kRThreads, 1) k_numeric_rowwarp(NumericArgs a, int slots,
+                                                                  int32_t *fail_rows,
+                                                                  int *fail_count) {
+  extern __shared__ double rsm[];
+  double *acc = rsm;                                                   // kRG * slots
+  uint16_t *ptab = reinterpret_cast<uint16_t *>(acc + (size_t)slots * kRG);  // kRPages
+  unsigned *pbits = reinterpret_cast<unsigned *>(ptab + kRPages);      // kRPages / 32
+  uint16_t *plist = reinterpret_cast<uint16_t *>(pbits + kRPages / 32);  // slots >> 3
+  __shared__ int s_grp, s_nblk, s_fail, s_ng, s_lo, s_hi, s_maxk;
+  __shared__ long long s_p0[kRG], s_p1[kRG];
+  __shared__ int64_t s_r[kRG];
+  __shared__ long long s_scan[kRG * kRG];
+  __shared__ double s_fs[kRG * kRG];
+  __shared__ unsigned long long s_off[kRG];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < slots * kRG; i += kRThreads) acc[i] = 0.0;
+  for (int i = tid; i < kRPages; i += kRThreads) ptab[i] = kGNone;
+  for (int i = tid; i < kRPages / 32; i += kRThreads) pbits[i] = 0u;
+  const int64_t ngroups = (a.nlist + kRG - 1) / kRG;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_grp = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int64_t grp = s_grp;
+    if (grp >= ngroups) break;
+    long long t_0 = clock64();
+    if (tid < kRG) {
+      const int64_t idx = grp * kRG + tid;
+      int64_t r = -1;
+      long long p0 = 0, p1 = 0;
+      if (idx < a.nlist) {
+        r = a.order ? (int64_t)a.order[idx] : idx;
+        p0 = a.A.rp[r];
+        p1 = a.A.rp[r + 1];
+      }
+      s_r[tid] = r;
+      s_p0[tid] = p0;
+      s_p1[tid] = p1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int ng = 0, lo = INT32_MAX, hi = -1, mk = 0;
+      for (int g = 0; g < kRG; g++) {
+        if (s_r[g] < 0) continue;
+        ng = g + 1;
+        const int64_t r = s_r[g];
+        if (a.hi[r] >= a.lo[r]) {
+          lo = min(lo, a.lo[r]);
+          hi = max(hi, a.hi[r]);
+        }
+        mk = max(mk, (int)(s_p1[g] - s_p0[g]));
+      }
+      s_ng = ng;
+      s_lo = lo;
+      s_hi = hi;
+      s_maxk = mk;
+      s_nblk = 0;
+      s_fail = (hi >= lo && (((int64_t)hi >> 6) - ((int64_t)lo >> 6) + 1) > kRPages) ? 2 : 0;
+    }
+    __syncthreads();
+    const int ng = s_ng;
+    if (s_hi < s_lo) {
+      if (tid < ng) {
+        const int64_t r = s_r[tid];
+        a.row_off[r] = 0;
+        a.row_cnt[r] = 0;
+        a.row_fsum[r] = 0.0;
+        a.row_nnz[r] = 0;
+      }
+      continue;
+    }
+    int sh = 3;
+    {
+      const int64_t lo = s_lo, hi = s_hi;
+      while (sh < 6 && ((hi >> sh) - (lo >> sh) + 1) > kRPages) sh++;
+    }
+    const int pmask = (1 << sh) - 1;
+    const int64_t pg0 = (int64_t)s_lo >> sh;
+    const int npg = (int)(((int64_t)s_hi >> sh) - pg0 + 1);
+    const int bcap = slots >> sh;
+    const int cbase = (int)(pg0 << sh);
+    const bool mine = warp < ng && !s_fail;
+    const long long p0 = s_p0[warp < kRG ? warp : 0], p1 = s_p1[warp < kRG ? warp : 0];
+    const int nkw = mine ? (int)(p1 - p0) : 0;
+    double *accw = acc + (size_t)warp * slots;
+    // ---- self term (the 2T of Eq. 2.7), first in every cell of the row ----
+    if (mine && a.self_coef != 0.0) {
+      for (long long p = p0 + lane; p < p1; p += 32) {
+        const int rel = a.A.col[p] - cbase;
+        const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
+        if (b >= 0) accw[(b << sh) + (rel & pmask)] = __dmul_rn(a.self_coef, a.A.val[p]);
+        else s_fail = 4;
+      }
+      __syncwarp();
+    }
+    long long t_1 = clock64();
+    // ---- products: own k ascending; CTA barrier every kRSync k ----
+    const int maxk = s_maxk;
+    int32_t kk_l = 0;     // lane l holds entry (j0 + l) of the A row: k, a_rk, B row extent
+    double ak_l = 0.0;
+    long long kb_l = 0;
+    int kn_l = 0;
+    for (int j0 = 0; j0 < maxk; j0 += kRSync) {
+      if ((j0 & 31) == 0 && j0 < nkw) {
+        const int j = j0 + lane;
+        kk_l = 0;
+        ak_l = 0.0;
+        kb_l = 0;
+        kn_l = 0;
+        if (j < nkw) {
+          kk_l = a.A.col[p0 + j];
+          ak_l = a.A.val[p0 + j];
+          const int64_t kr = (int64_t)kk_l - a.B.row0;
+          if (kr >= 0 && kr < a.B.nrows) {
+            kb_l = a.B.rp[kr];
+            kn_l = (int)(a.B.rp[kr + 1] - kb_l);
+          }
+        }
+      }
+#pragma unroll 1
+      for (int j = j0; j < j0 + kRSync && j < nkw; j++) {
+        const int src = j & 31;
+        const double av = __shfl_sync(FULL_MASK, ak_l, src);
+        const long long b0 = __shfl_sync(FULL_MASK, kb_l, src);
+        const int ln = __shfl_sync(FULL_MASK, kn_l, src);
+        for (int e0 = 0; e0 < ln; e0 += 32 * kRChunks) {
+          int32_t c[kRChunks];
+          double v[kRChunks];
+          int o[kRChunks];
+          double x[kRChunks];
+#pragma unroll
+          for (int i = 0; i < kRChunks; i++) {
+            const int e = e0 + i * 32 + lane;
+            c[i] = -1;
+            v[i] = 0.0;
+            if (e < ln) {
+              c[i] = a.B.col[b0 + e];
+              v[i] = a.B.val[b0 + e];
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < kRChunks; i++) {
+            o[i] = -1;
+            if (c[i] >= 0) {
+              const int rel = c[i] - cbase;
+              const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
+              if (b >= 0) o[i] = (b << sh) + (rel & pmask);
+              else s_fail = 4;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < kRChunks; i++) x[i] = o[i] >= 0 ? accw[o[i]] : 0.0;
+#pragma unroll
+          for (int i = 0; i < kRChunks; i++) x[i] = __dadd_rn(x[i], __dmul_rn(av, v[i]));
+#pragma unroll
+          for (int i = 0; i < kRChunks; i++)
+            if (o[i] >= 0) accw[o[i]] = x[i];
+        }
+        __syncwarp();  // next k may hit the same cells from other lanes
+      }
+      __syncthreads();  // keep the warps' B-row walks close (L1 sharing)
+    }
+    long long t_2 = clock64();
+    const int failed = s_fail;
+    // ---- flush: claimed pages in column order ----
+    int npl = 0;
+    {
+      const int nw = failed ? 0 : (npg + 31) >> 5;
+      const int per = (nw + kRThreads - 1) / kRThreads;
+      const int w0 = min(tid * per, nw), w1 = min(w0 + per, nw);
+      long long c[1] = {0}, tot[1];
+      for (int w = w0; w < w1; w++) c[0] += __popc(pbits[w]);
+      block_scan_g<1, kRG>(c, tot, s_scan);
+      int run = (int)c[0];
+      for (int w = w0; w < w1; w++) {
+        unsigned m = pbits[w];
+        while (m) {
+          const int bb = __ffs(m) - 1;
+          m &= m - 1;
+          plist[run++] = (uint16_t)(w * 32 + bb);
+        }
+      }
+      npl = (int)tot[0];
+    }
+    __syncthreads();
+    const int total = npl << sh;
+    const int per = (total + kRThreads - 1) / kRThreads;
+    const int q0 = min(tid * per, total), q1 = min(q0 + per, total);
+    long long nst[kRG], nnzu[kRG], tot[kRG];
+    double fs[kRG];
+#pragma unroll
+    for (int g = 0; g < kRG; g++) {
+      nst[g] = 0;
+      nnzu[g] = 0;
+      fs[g] = 0.0;
+    }
+    for (int q = q0; q < q1; q++) {
+      const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
+#pragma unroll
+      for (int g = 0; g < kRG; g++) {
+        double x = acc[(size_t)g * slots + o];
+        if (x != 0.0) {
+          if (a.divisor != 1.0) x = x / a.divisor;
+          if (x != 0.0) {
+            nnzu[g]++;
+            if (fabs(x) > a.floor_tau) nst[g]++;
+            else fs[g] += x * x;
+          }
+        }
+      }
+    }
+    block_scan_g<kRG, kRG>(nst, tot, s_scan);
+#pragma unroll
+    for (int g = 0; g < kRG; g++) {
+      const double f = warp_sum(fs[g]);
+      const long long z = warp_sum(nnzu[g]);
+      if (lane == 0) {
+        s_fs[warp * kRG + g] = f;
+        s_scan[warp * kRG + g] = z;
+      }
+    }
+    __syncthreads();
+    if (tid < kRG) {
+      const int g = tid;
+      double f = 0.0;
+      long long z = 0;
+      for (int w = 0; w < kRG; w++) {
+        f += s_fs[w * kRG + g];
+        z += s_scan[w * kRG + g];
+      }
+      s_off[g] = (!failed && g < ng) ? atomicAdd(a.pool_used, (unsigned long long)tot[g]) : 0ull;
+      if (!failed && g < ng) {
+        const int64_t r = s_r[g];
+        const bool ok = (long long)s_off[g] + tot[g] <= a.pool_cap;
+        if (!ok) atomicOr(a.flags, 1);
+        a.row_off[r] = (int64_t)s_off[g];
+        a.row_cnt[r] = tot[g];
+        a.row_fsum[r] = f;
+        a.row_nnz[r] = z;
+      }
+    }
+    __syncthreads();
+    if (!failed) {
+      long long pos[kRG];
+      bool okg[kRG];
+#pragma unroll
+      for (int g = 0; g < kRG; g++) {
+        pos[g] = (long long)s_off[g] + nst[g];
+        okg[g] = g < ng && (long long)s_off[g] + tot[g] <= a.pool_cap;
+      }
+      for (int q = q0; q < q1; q++) {
+        const int pgi = plist[q >> sh];
+        const int o = ((int)ptab[pgi] << sh) + (q & pmask);
+        const int32_t col = (int32_t)(((pg0 + pgi) << sh) + (q & pmask));
+#pragma unroll
+        for (int g = 0; g < kRG; g++) {
+          double x = acc[(size_t)g * slots + o];
+          if (x != 0.0) {
+            if (a.divisor != 1.0) x = x / a.divisor;
+            if (x != 0.0 && fabs(x) > a.floor_tau) {
+              if (okg[g]) {
+                a.pool_col[pos[g]] = col;
+                a.pool_val[pos[g]] = x;
+              }
+              pos[g]++;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- reset ----
+    if (!failed) {
+      for (int q = tid; q < total; q += kRThreads) {
+        const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
+#pragma unroll
+        for (int g = 0; g < kRG; g++) acc[(size_t)g * slots + o] = 0.0;
+      }
+      __syncthreads();
+      for (int i = tid; i < npl; i += kRThreads) ptab[plist[i]] = kGNone;
+    } else {
+      for (int i = tid; i < slots * kRG; i += kRThreads) acc[i] = 0.0;
+      for (int i = tid; i < kRPages; i += kRThreads) ptab[i] = kGNone;
+    }
+    for (int i = tid; i < ((npg + 31) >> 5) && i < kRPages / 32; i += kRThreads) pbits[i] = 0u;
+    if (failed && tid < ng) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)s_r[tid];
+    if (a.prof && tid == 0) {
+      const long long t_3 = clock64();
+      atomicAdd(&a.prof[0], (unsigned long long)(t_1 - t_0));
+      atomicAdd(&a.prof[1], (unsigned long long)(t_2 - t_1));
+      atomicAdd(&a.prof[2], (unsigned long long)(t_3 - t_2));
+      atomicAdd(&a.prof[3], 1ull);
+      atomicAdd(&a.prof[4], (unsigned long long)maxk);
+      if (failed) atomicAdd(&a.prof[5], 1ull);
+      if (failed == 2) atomicAdd(&a.prof[6], 1ull);
+      if (failed == 4) atomicAdd(&a.prof[7], 1ull);
+    }
+  }
+}
+
+void launch_numeric_rowwarp(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
+                            cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  const int smem = rowwarp_smem_bytes(slots);
+  cudaFuncSetAttribute(k_numeric_rowwarp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_rowwarp<<<a.grid, kRThreads, smem, st>>>(a, slots, fail_rows, fail_count);
 }
 
 // ------------------------------------------------------------------------------------

@@ -92,7 +92,8 @@ struct NumericArgs {
   int *flags = nullptr;           // flags[0] |= 1 on pool overflow, 2 on scratch overflow
   int grid = 0;
   int64_t nlist = 0;              // rows to process: order[0..nlist) (or 0..nlist)
-  int dbg = 0;                         // experiments (grouped kernel), 0 in production
+  const int32_t *gstart = nullptr;     // grouped kernels: group g = order[gstart[g], gstart[g+1])
+  int64_t ngroups = 0;
   unsigned long long *prof = nullptr;  // optional phase clocks (grouped kernel): setup,
                                        // products, flush, groups, union k's, failed groups
 };
@@ -138,6 +139,12 @@ constexpr int kGroupRows = 4;
 int group_smem_bytes(int slots);
 void launch_numeric_group(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
                           cudaStream_t st);
+// one-warp-per-row variant (kRowWarpRows rows per CTA share a page table; no barrier per
+// k; bit-identical order); rows of groups that do not fit -> fail_rows
+constexpr int kRowWarpRows = 8;
+int rowwarp_smem_bytes(int slots);
+void launch_numeric_rowwarp(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
+                            cudaStream_t st);
 // hash-accumulator variant; rows whose table over-fills are appended to fail_rows
 int hash_smem_bytes();
 void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,

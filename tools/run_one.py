@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--plan-norm", default="one")
     ap.add_argument("--eps-tol", type=float, default=1e-16)
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--kernel", type=int, default=0)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -25,7 +26,7 @@ def main():
     dev = torch.device("cuda", 0)
     rp, ci, va = (torch.from_numpy(x).to(dev) for x in (H.rowptr, H.col, H.val))
     for rep in range(args.repeat):
-        p = B.Plan(H.n, rp, ci, va, args.eps_tol, plan_norm=args.plan_norm)
+        p = B.Plan(H.n, rp, ci, va, args.eps_tol, plan_norm=args.plan_norm, kernel=args.kernel)
         p.run_only()
         st = p.stats()
         p.close()
@@ -43,7 +44,8 @@ def main():
             if g[3] > 0:
                 sys.stderr.write(f"  sq{i} group: setup {g[0] / g[3]:.0f} products {g[1] / g[3]:.0f} "
                                  f"flush {g[2] / g[3]:.0f} clk/group, groups {g[3]:.0f}, "
-                                 f"union k/group {g[4] / g[3]:.1f}, failed {g[5]:.0f} (union {g[6]:.0f}, slots {g[7]:.0f})\n")
+                                 f"union k/group {g[4] / g[3]:.1f}, failed {g[5]:.0f} (union {g[6]:.0f}, slots {g[7]:.0f}); "
+                                 f"per k: wait {g[8] / g[4]:.0f} A {g[9] / g[4]:.0f} B {g[10] / g[4]:.0f} bar {g[11] / g[4]:.0f}\n")
     M, N = int(st["M"]), int(st["N"])
     out = {k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in st.items()}
     for k, v in list(out.items()):
