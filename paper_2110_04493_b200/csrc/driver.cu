@@ -116,10 +116,10 @@ static NcclApi &nccl() {
 // a synchronize (sexpm_destroy) are idle and reusable on any stream.
 namespace cache {
 struct Block {
-  void *p;
-  size_t bytes;
-  cudaStream_t st;  // nullptr: idle (no pending work)
-  int dev;
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st = nullptr;  // nullptr: idle (no pending work)
+  int dev = 0;
 };
 static std::mutex mu;
 static std::multimap<size_t, Block> free_blocks;
@@ -127,10 +127,12 @@ static long long hits = 0, misses = 0, releases = 0;
 static double bytes_cached = 0.0, bytes_allocated = 0.0;
 static size_t budget = 0;  // cap on bytes_allocated: 90% of the device memory
 static thread_local bool freeing_idle = false;
-// size each role-tagged buffer (iterates, staging pool) reached in the latest plan: a new
-// plan asks for that size first, so repeated e^H of similar matrices never grow in steps
+// Role parking: the final block of each role-tagged buffer (iterates, staging pool, E) of a
+// destroyed plan is kept for the same role of the next plan, which takes it whenever it is
+// large enough for its first request: a plan on a matrix like the previous one gets its
+// final-size buffers at once, with no cross-role fragmentation.
 constexpr int kRoles = 32;
-static size_t role_hint[kRoles] = {0};
+static Block parked[kRoles];
 static size_t round_bytes(size_t b) {
   const size_t g = b >= ((size_t)1 << 24) ? ((size_t)1 << 21) : 512;
   return (b + g - 1) / g * g;
@@ -148,6 +150,13 @@ static void release_all() {
     bytes_allocated -= (double)kv.first;
   }
   free_blocks.clear();
+  for (Block &b : parked) {
+    if (b.p) {
+      cudaFree(b.p);
+      bytes_allocated -= (double)b.bytes;
+    }
+    b = Block{};
+  }
   bytes_cached = 0.0;
   releases++;
 }
@@ -170,7 +179,7 @@ static bool take(size_t lo, size_t hi, cudaStream_t st, int dev, void **p, size_
   }
   return false;
 }
-static void *alloc(size_t bytes, cudaStream_t st, size_t *got, size_t hint) {
+static void *alloc(size_t bytes, cudaStream_t st, size_t *got) {
   bytes = round_bytes(bytes);
   int dev = 0;
   cudaGetDevice(&dev);
@@ -181,10 +190,6 @@ static void *alloc(size_t bytes, cudaStream_t st, size_t *got, size_t hint) {
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
       budget = (size_t)(0.90 * (double)tot);
-    }
-    if (hint > bytes) {
-      hint = round_bytes(hint);
-      if (take(hint, 2 * hint + ((size_t)1 << 21), st, dev, &p, got)) return p;
     }
     if (take(bytes, 2 * bytes + ((size_t)1 << 21), st, dev, &p, got)) return p;
     // miss: make room under the budget by returning the largest cached blocks to the pool
@@ -214,6 +219,9 @@ static void *alloc(size_t bytes, cudaStream_t st, size_t *got, size_t hint) {
     misses++;
     bytes_allocated += (double)bytes;
   }
+  if (getenv("SEXPM_CACHE_LOG"))
+    fprintf(stderr, "[sexpm cache] miss: %zu bytes, allocated %.1f GB, cached %.1f GB\n", bytes,
+            bytes_allocated / 1e9, bytes_cached / 1e9);
   return p;
 }
 static void free(void *p, size_t bytes, cudaStream_t st) {
@@ -223,6 +231,32 @@ static void free(void *p, size_t bytes, cudaStream_t st) {
   free_blocks.emplace(bytes, Block{p, bytes, freeing_idle ? nullptr : st, dev});
   bytes_cached += (double)bytes;
 }
+static void park(int role, void *p, size_t bytes) {  // idle blocks only (plan destroyed)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  Block &b = parked[role];
+  Block other{p, bytes, nullptr, dev};
+  if (!b.p || (b.bytes < bytes && b.dev == dev)) std::swap(b, other);  // keep the larger one
+  if (other.p) {
+    free_blocks.emplace(other.bytes, other);
+    bytes_cached += (double)other.bytes;
+  }
+}
+static void *unpark(int role, size_t bytes, size_t *got) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  Block &b = parked[role];
+  if (b.p && b.dev == dev && b.bytes >= round_bytes(bytes)) {
+    void *p = b.p;
+    *got = b.bytes;
+    b = Block{};
+    hits++;
+    return p;
+  }
+  return nullptr;
+}
 }  // namespace cache
 
 template <typename T>
@@ -231,10 +265,13 @@ struct DBuf {
   size_t n = 0;
   size_t bytes = 0;
   cudaStream_t st = nullptr;
-  int role = -1;      // cache::role_hint slot (large growing buffers), -1 none
+  int role = -1;      // cache::parked slot (large growing buffers), -1 none
   bool grown = false;  // allocated at least once in this plan
   void release() {
-    if (p) cache::free(p, bytes, st);
+    if (p) {
+      if (role >= 0 && cache::freeing_idle) cache::park(role, p, bytes);  // plan destroyed
+      else cache::free(p, bytes, st);
+    }
     p = nullptr;
     n = 0;
     bytes = 0;
@@ -243,14 +280,15 @@ struct DBuf {
     release();
     st = s;
     if (cnt == 0) cnt = 1;
-    const size_t hint = (role >= 0 && !grown) ? cache::role_hint[role] : 0;
-    p = reinterpret_cast<T *>(cache::alloc(cnt * sizeof(T), s, &bytes, hint));
+    p = nullptr;
+    if (role >= 0 && !grown) p = reinterpret_cast<T *>(cache::unpark(role, cnt * sizeof(T), &bytes));
+    if (!p) p = reinterpret_cast<T *>(cache::alloc(cnt * sizeof(T), s, &bytes));
     n = bytes / sizeof(T);
     grown = true;
-    if (role >= 0) cache::role_hint[role] = bytes;
   }
-  // grow-only: reuse the buffer when it is large enough, else grow by 1.25x (fewer
-  // stream-ordered re-allocations as the iterates fill in)
+  // grow-only: reuse the buffer when it is large enough, else grow by 1.25x; the large
+  // role-tagged buffers (iterates, staging pool), which fill in term after term, at least
+  // double, so a cold plan re-allocates them a few times rather than at every step
   void ensure(size_t cnt, cudaStream_t s) {
     if (cnt > n || !p) alloc(std::max<size_t>(cnt + cnt / 4, 1), s);
   }
@@ -323,7 +361,8 @@ struct StepReport {
 struct Workspace {
   DBuf<int32_t> lo, hi, order, bin_cnt, bin_off;
   DBuf<int64_t> prod, bound, row_off, row_cnt, row_nnz, cnt, scan_tmp, l1r, l2r, i64tmp;
-  DBuf<double> row_fsum, rs, partial, scal, passrow;
+  DBuf<double> row_fsum, rs, partial, scal, passrow, row_p1;
+  DBuf<int64_t> row_c1;
   DBuf<int64_t> cursor;
   DBuf<int32_t> scr_col, pool_col;
   DBuf<double> scr_val, pool_val;
@@ -545,6 +584,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   CK(cudaEventCreate(&e_first));
   bool have_first = false;
   unsigned long long used = 0;
+  bool fused_p1 = false;
+  w.row_p1.ensure(nr1, st);
+  w.row_c1.ensure(nr1, st);
   w.fail_rows.ensure(nr1, st);
   w.fail_rows2.ensure(nr1, st);
   w.fail_count.ensure(1, st);
@@ -608,6 +650,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       int fb = 0;
       int stage = kern;
       bool first = true;
+      // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
+      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7);
       while (nlist > 0) {
         if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
           run_symbolic();
@@ -617,6 +661,11 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         NumericArgs nh = na;
         nh.order = list;
         nh.nlist = nlist;
+        if (first && fused_p1) {
+          nh.row_p1 = w.row_p1.p;
+          nh.row_c1 = w.row_c1.p;
+          nh.eps_g = eps_g;
+        }
         CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
         CK(cudaMemsetAsync(w.fail_count.p, 0, sizeof(int), st));
         if (stage == 3) {
@@ -693,6 +742,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       }
     }
     rep.window_rows = nfail;
+    if (nfail > 0) fused_p1 = false;  // rows handled by kernels without the fused pass
     CK(cudaEventRecord(e1, st));
     int flags = 0;
     CK(cudaMemcpyAsync(&flags, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -722,11 +772,18 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
                         12.0 * (double)used + 32.0 * (double)nr;
   }
 
-  // Algorithm 4.1: scalar recurrence on the host, sums on the device
+  // Algorithm 4.1: scalar recurrence on the host, sums on the device (one
+  // read-back for the floor sum, the distinct count and the fused first pass)
   launch_reduce_sum(w.row_fsum.p, nr, w.partial.p, w.scal.p + 0, st);
   launch_reduce_sum_i64(w.row_nnz.p, nr, w.i64tmp.p + 3, st);
-  double Floc = d2h(w.scal.p + 0, st);
-  rep.nnz_unf = (int64_t)allsum(P, (double)d2h(w.i64tmp.p + 3, st));
+  if (fused_p1) launch_reduce_sum(w.row_p1.p, nr, w.partial.p, w.scal.p + 3, st);
+  double hs[4];
+  int64_t hnz = 0;
+  CK(cudaMemcpyAsync(hs, w.scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&hnz, w.i64tmp.p + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double Floc = hs[0];
+  rep.nnz_unf = (int64_t)allsum(P, (double)hnz);
   const double F = allsum(P, Floc);
   rep.fsum = F;
   double tau;
@@ -741,9 +798,14 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     while (b > lim) {
       epsf = eg / m;
       const double tau_d = (double)epsf;
-      launch_alg41_pass_rows(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p,
-                             w.partial.p, w.scal.p + 1, st);
-      const double S = allsum(P, d2h(w.scal.p + 1, st));
+      double S;
+      if (passes == 0 && fused_p1 && tau_d == eps_g) {
+        S = allsum(P, hs[3]);  // tau_1 = eps_g: summed in the product kernel's flush
+      } else {
+        launch_alg41_pass_rows(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p,
+                               w.partial.p, w.scal.p + 1, st);
+        S = allsum(P, d2h(w.scal.p + 1, st));
+      }
       b = sqrtl((long double)F + (long double)S);
       m = b / epsf;
       passes++;
@@ -760,6 +822,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     launch_compact_count_ident(nr, A.row0, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p,
                                tau, w.cnt.p, w.ident.p, st);
     launch_count_ident(w.ident.p, nr, w.i64tmp.p + 6, st);
+  } else if (fused_p1 && passes == 1 && tau == eps_g) {
+    launch_copy_i64_offset(w.row_c1.p, nr, 0, w.cnt.p, st);  // kept = staged |x| > eps_g
   } else {
     launch_compact_count(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau, w.cnt.p, st);
   }

@@ -1396,8 +1396,8 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
   __shared__ int s_row, s_slots, s_fail, s_npl;
   __shared__ unsigned long long s_off;
   __shared__ long long s_wsum[kWarps + 1];
-  __shared__ double s_fs[kWarps];
-  __shared__ long long s_nz[kWarps];
+  __shared__ double s_fs[kWarps], s_p1[kWarps];
+  __shared__ long long s_nz[kWarps], s_c1[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < kSlots; i += kThreads) vals[i] = 0.0;
@@ -1422,6 +1422,10 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
         a.row_cnt[r] = 0;
         a.row_fsum[r] = 0.0;
         a.row_nnz[r] = 0;
+        if (a.row_p1) {
+          a.row_p1[r] = 0.0;
+          a.row_c1[r] = 0;
+        }
       }
       continue;
     }
@@ -1574,16 +1578,29 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
     const int q0 = tid * per < total_slots ? tid * per : total_slots;
     const int q1 = q0 + per < total_slots ? q0 + per : total_slots;
     int nst = 0;
-    double fs = 0.0;
-    long long nnzu = 0;
+    double fs = 0.0, p1 = 0.0;
+    long long nnzu = 0, c1 = 0;
     for (int q = q0; q < q1; q++) {
       const int pgi = plist[q >> sh];
       const int o = ptab[pgi] + (q & (psize - 1));
       const double x = vals[o] / a.divisor;
       if (x != 0.0) {
         nnzu++;
-        if (fabs(x) > a.floor_tau) nst++;
-        else fs += x * x;
+        if (fabs(x) > a.floor_tau) {
+          nst++;
+          if (fabs(x) <= a.eps_g) p1 += x * x;
+          else c1++;
+        } else {
+          fs += x * x;
+        }
+      }
+    }
+    if (a.row_p1) {  // fused first pass of Algorithm 4.1 (fixed order: threads, then warps)
+      p1 = warp_sum(p1);
+      c1 = warp_sum(c1);
+      if (lane == 0) {
+        s_p1[warp] = p1;
+        s_c1[warp] = c1;
       }
     }
     // exclusive scan of nst over threads (thread order == column order)
@@ -1656,6 +1673,16 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
         a.row_cnt[r] = total;
         a.row_fsum[r] = f;
         a.row_nnz[r] = z;
+        if (a.row_p1) {
+          double pp = 0.0;
+          long long cc = 0;
+          for (int w = 0; w < kWarps; w++) {
+            pp += s_p1[w];
+            cc += s_c1[w];
+          }
+          a.row_p1[r] = pp;
+          a.row_c1[r] = cc;
+        }
       }
       s_slots = 0;
       s_fail = 0;
@@ -2976,6 +3003,7 @@ int taylor_dia_smem_bytes(int slots) {
   return kDWarps * (slots * 8 + kDPageWords * 4 + kDPageWords * 2 + (slots >> 3) * 2 + 16);
 }
 
+template <int MAXD>  // compile-time bound on the number of diagonals (>= D.ndiag)
 __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaView D, int slots,
                                                              int32_t *fail_rows, int *fail_count) {
   extern __shared__ double dsm[];
@@ -3013,6 +3041,10 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
           a.row_cnt[r] = 0;
           a.row_fsum[r] = 0.0;
           a.row_nnz[r] = 0;
+          if (a.row_p1) {
+            a.row_p1[r] = 0.0;
+            a.row_c1[r] = 0;
+          }
         }
         continue;
       }
@@ -3025,19 +3057,21 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
       const int npg = (int)((hi >> sh) - pg0 + 1);
       bool fail = sh >= 7;
       // (1) mark reachable pages
+      // lanes hold ascending k, so equal pages are adjacent lanes: a lane marks its page only
+      // if the lane below holds a different one (one atomic per page run)
       if (!fail) {
+        int64_t kn = lane < nx ? (int64_t)a.A.col[p0 + lane] : -1;
         for (int c0 = 0; c0 < nx; c0 += 32) {
-          const int t = c0 + lane;
-          const bool in = t < nx;
-          const int64_t k = in ? (int64_t)a.A.col[p0 + t] : 0;
-          for (int di = 0; di < nd; di++) {
-            const int64_t j = k + s_doff[di];
-            const bool v = in && j >= 0 && j < n;
-            const int pg = v ? (int)((j >> sh) - pg0) : -1;
-            const unsigned act = __ballot_sync(FULL_MASK, v);
-            if (v) {
-              const unsigned peers = __match_any_sync(act, pg);
-              if (lane == __ffs(peers) - 1) atomicOr(&pbits[pg >> 5], 1u << (pg & 31));
+          const int64_t k = kn;
+          kn = c0 + 32 + lane < nx ? (int64_t)a.A.col[p0 + c0 + 32 + lane] : -1;
+#pragma unroll
+          for (int di = 0; di < MAXD; di++) {
+            if (di < nd) {
+              const int64_t j = k + s_doff[di];
+              const bool v = k >= 0 && j >= 0 && j < n;
+              const int pg = v ? (int)((j >> sh) - pg0) : -1;
+              const int pgl = __shfl_up_sync(FULL_MASK, pg, 1);
+              if (v && (lane == 0 || pgl != pg)) atomicOr(&pbits[pg >> 5], 1u << (pg & 31));
             }
           }
         }
@@ -3080,40 +3114,51 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
         __syncwarp();
         continue;
       }
-      // (3) products, offsets descending inside each chunk of 32 entries
+      // (3) products, offsets descending inside each chunk of 32 entries; the next chunk's
+      // entries and diagonal values are loaded while this chunk is accumulated
       const int pmask = (1 << sh) - 1;
-      for (int c0 = 0; c0 < nx; c0 += 32) {
+      int64_t kc = -1;
+      double sc = 0.0, hc[MAXD];
+      auto load_chunk = [&](int c0, int64_t &k, double &sv, double (&h)[MAXD]) {
         const int t = c0 + lane;
         const bool in = t < nx;
-        const int64_t k = in ? (int64_t)a.A.col[p0 + t] : 0;
-        const double sv = in ? a.A.val[p0 + t] : 0.0;
-        double h[kDMaxDiag];
+        k = in ? (int64_t)a.A.col[p0 + t] : -1;
+        sv = in ? a.A.val[p0 + t] : 0.0;
 #pragma unroll
-        for (int di = 0; di < kDMaxDiag; di++) {
-          h[di] = 0.0;
-          if (di < nd && in) h[di] = D.val[(int64_t)di * n + k];
-        }
+        for (int di = 0; di < MAXD; di++) h[di] = (di < nd && in) ? D.val[(int64_t)di * n + k] : 0.0;
+      };
+      load_chunk(0, kc, sc, hc);
+      for (int c0 = 0; c0 < nx; c0 += 32) {
+        int64_t kn;
+        double sn, hn[MAXD];
+        if (c0 + 32 < nx) load_chunk(c0 + 32, kn, sn, hn);
 #pragma unroll
-        for (int di = 0; di < kDMaxDiag; di++) {
+        for (int di = 0; di < MAXD; di++) {
           if (di < nd) {
-            if (h[di] != 0.0) {
-              const int64_t j = k + s_doff[di];
+            if (hc[di] != 0.0) {
+              const int64_t j = kc + s_doff[di];
               const int pg = (int)((j >> sh) - pg0);
               const unsigned wd = pbits[pg >> 5];
               const int rank = pref[pg >> 5] + __popc(wd & ((1u << (pg & 31)) - 1u));
               const int o = (rank << sh) + (int)(j & pmask);
-              acc[o] = __dadd_rn(acc[o], __dmul_rn(sv, h[di]));
+              acc[o] = __dadd_rn(acc[o], __dmul_rn(sc, hc[di]));
               prods++;
             }
             __syncwarp();
           }
         }
+        if (c0 + 32 < nx) {
+          kc = kn;
+          sc = sn;
+#pragma unroll
+          for (int di = 0; di < MAXD; di++) hc[di] = hn[di];
+        }
       }
       // (4) flush in column order: divide, classify, count
       const int total = npages << sh;
       int nst = 0;
-      double fs = 0.0;
-      long long nnzu = 0;
+      double fs = 0.0, q1 = 0.0;
+      long long nnzu = 0, c1 = 0;
       for (int s0 = lane; s0 < total; s0 += 32) {
         double x = acc[s0];
         if (x != 0.0) {
@@ -3121,14 +3166,21 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
           acc[s0] = x;
           if (x != 0.0) {
             nnzu++;
-            if (fabs(x) > a.floor_tau) nst++;
-            else fs += x * x;
+            if (fabs(x) > a.floor_tau) {
+              nst++;
+              if (fabs(x) <= a.eps_g) q1 += x * x;
+              else c1++;
+            } else {
+              fs += x * x;
+            }
           }
         }
       }
       nst = __reduce_add_sync(FULL_MASK, nst);
       fs = warp_sum(fs);
       nnzu = warp_sum(nnzu);
+      q1 = warp_sum(q1);
+      c1 = warp_sum(c1);
       unsigned long long off = 0;
       if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)nst);
       off = __shfl_sync(FULL_MASK, off, 0);
@@ -3157,6 +3209,10 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
         a.row_cnt[r] = nst;
         a.row_fsum[r] = fs;
         a.row_nnz[r] = nnzu;
+        if (a.row_p1) {
+          a.row_p1[r] = q1;
+          a.row_c1[r] = c1;
+        }
       }
       __syncwarp();
     }
@@ -3169,9 +3225,10 @@ void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_
                        int *fail_count, cudaStream_t st) {
   if (a.A.nrows == 0 || a.nlist == 0) return;
   const int smem = taylor_dia_smem_bytes(slots);
-  cudaFuncSetAttribute(k_taylor_dia, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto kf = D.ndiag <= 4 ? k_taylor_dia<4> : (D.ndiag <= 8 ? k_taylor_dia<8> : k_taylor_dia<16>);
+  cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
-  k_taylor_dia<<<a.grid, kDWarps * 32, smem, st>>>(a, D, slots, fail_rows, fail_count);
+  kf<<<a.grid, kDWarps * 32, smem, st>>>(a, D, slots, fail_rows, fail_count);
 }
 
 // ------------------------------------------------------------------------------------

@@ -92,6 +92,11 @@ struct NumericArgs {
   int *flags = nullptr;           // flags[0] |= 1 on pool overflow, 2 on scratch overflow
   int grid = 0;
   int64_t nlist = 0;              // rows to process: order[0..nlist) (or 0..nlist)
+  // first Algorithm 4.1 pass fused into the flush (kernels 5 and 7): per row, the sum of
+  // x^2 over staged |x| <= eps_g (tau_1 = eps_g) and the count of staged |x| > eps_g
+  double *row_p1 = nullptr;
+  int64_t *row_c1 = nullptr;
+  double eps_g = 0.0;
   const int32_t *gstart = nullptr;     // grouped kernels: group g = order[gstart[g], gstart[g+1])
   int64_t ngroups = 0;
   unsigned long long *prof = nullptr;  // optional phase clocks (grouped kernel): setup,
