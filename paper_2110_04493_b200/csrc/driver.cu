@@ -13,12 +13,14 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/sexpm.h"
@@ -402,6 +404,20 @@ struct sexpm_plan_s {
   DBuf<int32_t> proc_order;  // K3 row processing order (cluster order of H's graph)
   DBuf<int32_t> group_start;  // grouped kernel: group boundaries in proc_order
   int64_t ngroups = 0;
+  // background computation of proc_order / group_start (overlaps the Taylor phase)
+  std::thread bg;
+  cudaStream_t bg_st = nullptr;
+  cudaEvent_t ev_pattern = nullptr, ev_order = nullptr;
+  bool order_pending = false;
+  std::string bg_err;
+  std::vector<int32_t> h_order, h_groups;
+  ~sexpm_plan_s() {
+    if (bg.joinable()) bg.join();
+    if (bg_st) cudaStreamSynchronize(bg_st);
+    if (ev_pattern) cudaEventDestroy(ev_pattern);
+    if (ev_order) cudaEventDestroy(ev_order);
+    if (bg_st) cudaStreamDestroy(bg_st);
+  }
   bool have_result = false;
   int M = 0, N = 0, normal = 0, M_eff = 0;
   double norm = 0.0, a = 0.0, eps_g0 = 0.0;
@@ -493,6 +509,15 @@ static void build_transpose(sexpm_plan_s &P, const CsrView &Bv, int64_t ncols, D
 // filtered product: C^ = Alg4.1((self*A + A*B)/div, eps_g)   [K1, K2, K3, K6, K4]
 // A: local rows; B: rows covering every column of A.  C gets A's rows.
 // ------------------------------------------------------------------------------------
+// join the background order thread (once) and order the plan's stream after its upload
+static void wait_order(sexpm_plan_s &P) {
+  if (!P.order_pending) return;
+  if (P.bg.joinable()) P.bg.join();
+  P.order_pending = false;
+  REQUIRE(P.bg_err.empty(), SEXPM_ECUDA, P.bg_err);
+  CK(cudaStreamWaitEvent(P.st, P.ev_order, 0));
+}
+
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
                             double div, double eps_g, DCsr &C, StepReport &rep,
                             const DCsr *BT = nullptr, bool add_identity = false) {
@@ -555,8 +580,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
 
   // K2 scheduling order: the plan's locality (cluster) order when it covers these rows,
   // else longest-processing-time-first bins
-  const bool use_cluster = P.proc_order.p && (int64_t)P.proc_order.n >= nr && A.row0 == P.row_begin &&
-                           nr == P.row_end - P.row_begin;
+  // the locality order serves the squarings (Taylor terms stream their rows in index order)
+  const bool use_cluster = self != 0.0 && P.proc_order.p && (int64_t)P.proc_order.n >= nr &&
+                           A.row0 == P.row_begin && nr == P.row_end - P.row_begin;
+  if (use_cluster) wait_order(P);
   if (!use_cluster && have_symbolic)
     launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
 
@@ -1219,6 +1246,16 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, st));
+  const bool plog = getenv("SEXPM_PLAN_LOG") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto mark = [&](const char *what) {  // SEXPM_PLAN_LOG: host-side phase times of the plan
+    if (!plog) return;
+    CK(cudaStreamSynchronize(st));
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[sexpm plan] %-28s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - tprev).count());
+    tprev = t;
+  };
   Workspace &w = P.ws;
   w.flags.ensure(1, st);
   w.partial.ensure(1024, st);
@@ -1236,6 +1273,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   vf = (int)allmax(P, (double)vf);
   REQUIRE(!(vf & 8), SEXPM_ENONFINITE, "H holds a non-finite value");
   REQUIRE(!(vf & 7), SEXPM_EINVAL, "malformed CSR (rowptr / column range / column order)");
+  mark("validate");
   // rank partition
   std::vector<double> rb;
   double mine[2] = {(double)P.row_begin, (double)P.row_end};
@@ -1281,6 +1319,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     P.H0full = std::move(Hc);
   }
   DCsr &Hf = P.H0full;
+  mark("gather + purge zeros");
   // K8 norms on the device
   double norm = 0.0;
   int symflags = 3;
@@ -1307,6 +1346,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     // keep the transpose: H0^T (scaled below) feeds the Taylor pull kernel
     P.H0T = std::move(HT);
   }
+  mark("transpose + norm + symmetry");
   P.norm = norm;
   int M, N;
   REQUIRE(plan_MN(norm, eps_tol, P.o.m_cap, P.o.n_window, M, N), SEXPM_EINFEASIBLE,
@@ -1328,34 +1368,58 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   // H0 = H 2^-N (exact)
   launch_scale_pow2(Hf.val.p, Hf.nnz, -N, st);
   launch_scale_pow2(P.H0T.val.p, P.H0T.nnz, -N, st);
+  mark("plan (M,N) + scale");
   build_diagonals(P);
+  mark("diagonals");
   slice_rows(P, Hf, P.row_begin, P.row_end, P.H0loc);
+  // The squarings' processing order (locality clusters of H's graph, host BFS) is computed
+  // on a background host thread with its own stream, overlapping the Taylor phase on the
+  // GPU; sexpm_run waits for it (event) before the first squaring.
   {
-    std::vector<int64_t> hrp((size_t)P.n + 1);
-    std::vector<int32_t> hcol((size_t)std::max<int64_t>(Hf.nnz, 1));
-    CK(cudaMemcpyAsync(hrp.data(), Hf.rp.p, hrp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    if (Hf.nnz)
-      CK(cudaMemcpyAsync(hcol.data(), Hf.col.p, Hf.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::vector<int32_t> ord;
-    cluster_order(hrp, hcol, P.row_begin, P.row_end, 1024, ord);
-    P.proc_order.ensure(std::max<size_t>(ord.size(), 1), st);
-    if (!ord.empty())
-      CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    // groups of the grouped kernel: up to kGroupRows consecutive entries of the order, cut
-    // where the row index jumps (rows far apart share few B rows and overflow the union)
-    std::vector<int32_t> gs;
-    for (size_t j = 0; j < ord.size(); j++) {
-      const bool cut = j == 0 || (int)(j - (size_t)gs.back()) >= kGroupRows ||
-                       std::abs((long long)ord[j] - (long long)ord[j - 1]) > 2;
-      if (cut) gs.push_back((int32_t)j);
-    }
-    P.ngroups = (int64_t)gs.size();
-    gs.push_back((int32_t)ord.size());
-    P.group_start.ensure(gs.size(), st);
-    CK(cudaMemcpyAsync(P.group_start.p, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
+    const int64_t nl = P.row_end - P.row_begin;
+    P.proc_order.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    P.group_start.ensure((size_t)nl + 2, st);
+    CK(cudaEventCreateWithFlags(&P.ev_pattern, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&P.ev_order, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&P.bg_st, cudaStreamNonBlocking));
+    CK(cudaEventRecord(P.ev_pattern, st));
+    P.order_pending = true;
+    P.bg = std::thread([&P]() {
+      try {
+        CK(cudaSetDevice(P.dev));
+        CK(cudaStreamWaitEvent(P.bg_st, P.ev_pattern, 0));
+        const DCsr &F = P.H0full;
+        std::vector<int64_t> hrp((size_t)P.n + 1);
+        std::vector<int32_t> hcol((size_t)std::max<int64_t>(F.nnz, 1));
+        CK(cudaMemcpyAsync(hrp.data(), F.rp.p, hrp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, P.bg_st));
+        if (F.nnz)
+          CK(cudaMemcpyAsync(hcol.data(), F.col.p, F.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, P.bg_st));
+        CK(cudaStreamSynchronize(P.bg_st));
+        std::vector<int32_t> &ord = P.h_order;
+        cluster_order(hrp, hcol, P.row_begin, P.row_end, 1024, ord);
+        // groups of the grouped kernel: up to kGroupRows consecutive entries of the order,
+        // cut where the row index jumps (rows far apart share few B rows)
+        std::vector<int32_t> &gs = P.h_groups;
+        gs.clear();
+        for (size_t j = 0; j < ord.size(); j++) {
+          const bool cut = j == 0 || (int)(j - (size_t)gs.back()) >= kGroupRows ||
+                           std::abs((long long)ord[j] - (long long)ord[j - 1]) > 2;
+          if (cut) gs.push_back((int32_t)j);
+        }
+        P.ngroups = (int64_t)gs.size();
+        gs.push_back((int32_t)ord.size());
+        if (!ord.empty())
+          CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
+        CK(cudaMemcpyAsync(P.group_start.p, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
+        CK(cudaEventRecord(P.ev_order, P.bg_st));
+      } catch (const SxError &e) {
+        P.bg_err = e.msg.empty() ? "order thread failed" : e.msg;
+      } catch (...) {
+        P.bg_err = "order thread failed";
+      }
+    });
   }
+  mark("groups + upload");
   CK(cudaEventRecord(e1, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaEventElapsedTime(&P.plan_ms, e0, e1));
