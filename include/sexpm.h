@@ -97,9 +97,10 @@ typedef struct {
                              paged, 6 Taylor pull (Taylor terms only; else 1), 7 Taylor diagonal
                              push (Taylor terms only; else as 0), 8 grouped rows (4 rows per
                              CTA share each B-row gather, TMA-staged), 9 one warp per row (8
-                             rows per CTA share a page table).  All meet parity; 2 and 4-9
-                             reproduce the oracle's C~ bit for bit.  Rows a kernel cannot hold
-                             fall through 8/9 -> 5 -> 3, 7 -> 6 -> 1 -> 3 and 1/4/5 -> 3. */
+                             rows per CTA share a page table), 10 k-sync paged with 128
+                             threads per row.  All meet parity; 2 and 4-10 reproduce the
+                             oracle's C~ bit for bit.  Rows a kernel cannot hold fall through
+                             8/9/10 -> 5 -> 3, 7 -> 6 -> 1 -> 3 and 1/4/5 -> 3. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */

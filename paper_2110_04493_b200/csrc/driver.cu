@@ -430,6 +430,7 @@ struct sexpm_plan_s {
   int hash_blocks_per_sm = 4;
   int warp_blocks_per_sm = 4;
   int paged_blocks_per_sm = 3;
+  int paged2_blocks_per_sm = 5;
   int warp_window = 1024;
   float plan_ms = 0.f;
 };
@@ -678,7 +679,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       int stage = kern;
       bool first = true;
       // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
-      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7);
+      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10);
       while (nlist > 0) {
         if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
           run_symbolic();
@@ -717,6 +718,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         } else if (stage == 5) {
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
+        } else if (stage == 10) {
+          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged2_blocks_per_sm));
+          launch_numeric_paged2(nh, fout, w.fail_count.p, st);
         } else if (stage == 9) {
           nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kRowWarpRows - 1) / kRowWarpRows,
                                                                 (int64_t)P.sm_count));
@@ -765,7 +769,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         list = fout;
         nlist = nf;
         fb ^= 1;
-        stage = stage == 7 ? (taylor_pull_ok ? 6 : 1) : (stage == 6 ? 1 : ((stage == 8 || stage == 9) ? 5 : 3));
+        stage = stage == 7 ? (taylor_pull_ok ? 6 : 1)
+                           : (stage == 6 ? 1 : ((stage >= 8 && stage <= 10) ? 5 : 3));
       }
     }
     rep.window_rows = nfail;
@@ -1747,7 +1752,9 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
   REQUIRE(smem <= (int)prop.sharedMemPerBlockOptin - 2048, SEXPM_EINVAL, "window too large");
   P->numeric_blocks_per_sm = std::max(1, std::min(4, (int)(prop.sharedMemPerMultiprocessor / (smem + 4096))));
   P->hash_blocks_per_sm = std::max(1, std::min(8, (int)(prop.sharedMemPerMultiprocessor / (hash_smem_bytes() + 2048))));
-  P->paged_blocks_per_sm = std::max(1, std::min(8, (int)(prop.sharedMemPerMultiprocessor / (paged_smem_bytes() + 8192))));
+  // CTAs per SM from shared memory: dynamic + static (< 6 KB) + the 1 KB per-CTA reserve
+  P->paged_blocks_per_sm = std::max(1, std::min(8, (int)(prop.sharedMemPerMultiprocessor / (paged_smem_bytes() + 7168))));
+  P->paged2_blocks_per_sm = std::max(1, std::min(16, (int)(prop.sharedMemPerMultiprocessor / (paged2_smem_bytes() + 4096))));
   P->warp_blocks_per_sm = std::max(1, std::min(16, (int)(prop.sharedMemPerMultiprocessor /
                                                          (warp_numeric_smem_bytes(P->warp_window) + 1024))));
   if (P->o.stream) {

@@ -1359,21 +1359,34 @@ void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_co
 // Rows whose span needs pages wider than 64 columns or whose pages overflow kSlots are
 // handed to the block-window kernel.
 // ------------------------------------------------------------------------------------
-constexpr int kPages = 4096;
-constexpr int kSlots = 4096;
 constexpr int kMaxPageShift = 6;
-constexpr int kPF = 8;  // k-steps of B entries prefetched into registers
+// two configurations: (threads, entries per thread per k held in the prefetch ring, ring
+// depth in k, slots, pages).  v1: 256 threads; v2: 128 threads with 4 entries each (the
+// per-k bookkeeping is amortized over twice the entries) and a smaller footprint (more
+// CTAs per SM).
+template <int T, int NE, int PF, int SLOTS, int PAGES, typename PT = int32_t, int MINSH = 4>
+struct PagedCfg {
+  static constexpr int kT = T, kW = T / 32, kNE = NE, kPF = PF, kSlots = SLOTS, kPages = PAGES;
+  static constexpr int kMinShift = MINSH;
+  using PageT = PT;  // page-table entry: slot base, -1 free, -2 being claimed, -3 overflow
+  static constexpr int smem() {
+    return SLOTS * 8 + ((PAGES * (int)sizeof(PT) + 7) / 8) * 8 + (SLOTS >> MINSH) * 4;
+  }
+};
+using PagedV1 = PagedCfg<256, 2, 8, 4096, 4096>;
+using PagedV2 = PagedCfg<128, 4, 4, 4096, 4096>;
+int paged_smem_bytes() { return PagedV1::smem(); }
+int paged2_smem_bytes() { return PagedV2::smem(); }
 
-int paged_smem_bytes() { return kSlots * 8 + kPages * 4 * 2; }
-
-__device__ __forceinline__ int page_slot(volatile int32_t *ptab, int pg, int psize, int *slot_count) {
+__device__ __forceinline__ int page_slot(volatile int32_t *ptab, int pg, int psize, int *slot_count,
+                                         int slot_cap) {
   int b = ptab[pg];
   if (b >= 0) return b;
   if (b == -1) {
     int old = atomicCAS((int32_t *)&ptab[pg], -1, -2);
     if (old == -1) {
       int nb = atomicAdd(slot_count, psize);
-      if (nb + psize > kSlots) nb = -3;  // overflow marker
+      if (nb + psize > slot_cap) nb = -3;  // overflow marker
       __threadfence_block();
       ptab[pg] = nb;
       return nb;
@@ -1384,12 +1397,43 @@ __device__ __forceinline__ int page_slot(volatile int32_t *ptab, int pg, int psi
   return b;  // >= 0 or -3 (overflow)
 }
 
-__global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32_t *fail_rows,
-                                                            int *fail_count) {
+// 16-bit page table: the claim marks the entry through a CAS on its 32-bit word
+__device__ __forceinline__ int page_slot(volatile int16_t *ptab, int pg, int psize, int *slot_count,
+                                         int slot_cap) {
+  int b = ptab[pg];
+  if (b >= 0) return b;
+  if (b == -1) {
+    unsigned *word = (unsigned *)((uintptr_t)(ptab + pg) & ~(uintptr_t)3);
+    const int shift = (pg & 1) ? 16 : 0;
+    for (;;) {
+      const unsigned old = *(volatile unsigned *)word;
+      if (((old >> shift) & 0xFFFFu) != 0xFFFFu) break;  // no longer free
+      const unsigned nw = (old & ~(0xFFFFu << shift)) | (0xFFFEu << shift);  // -2: claiming
+      if (atomicCAS(word, old, nw) == old) {
+        int nb = atomicAdd(slot_count, psize);
+        if (nb + psize > slot_cap) nb = -3;  // overflow marker
+        __threadfence_block();
+        ptab[pg] = (int16_t)nb;
+        return nb;
+      }
+    }
+  }
+  while ((b = ptab[pg]) == -2) {
+  }
+  return b;  // >= 0 or -3 (overflow)
+}
+
+template <class CFG>
+__global__ void __launch_bounds__(CFG::kT) k_numeric_paged(NumericArgs a, int32_t *fail_rows,
+                                                           int *fail_count) {
+  constexpr int kThreads = CFG::kT, kWarps = CFG::kW, kSlots = CFG::kSlots, kPages = CFG::kPages;
+  constexpr int kPF = CFG::kPF, NE = CFG::kNE;
+  using PT = typename CFG::PageT;
   extern __shared__ double psm[];
   double *vals = psm;                                              // kSlots
-  int32_t *ptab = reinterpret_cast<int32_t *>(psm + kSlots);       // kPages
-  int32_t *plist = ptab + kPages;                                  // kPages (flush)
+  PT *ptab = reinterpret_cast<PT *>(psm + kSlots);                 // kPages
+  int32_t *plist = reinterpret_cast<int32_t *>(
+      reinterpret_cast<char *>(ptab) + ((kPages * (int)sizeof(PT) + 7) / 8) * 8);  // flush list
   __shared__ long long s_start[kThreads];
   __shared__ int s_len[kThreads];
   __shared__ double s_av[kThreads];
@@ -1430,7 +1474,7 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
       continue;
     }
     const int64_t span = (int64_t)hi - lo + 1;
-    int sh = 4;
+    int sh = CFG::kMinShift;
     while ((span >> sh) >= kPages) sh++;
     if (sh > kMaxPageShift || nk > kSlots) {
       if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
@@ -1441,7 +1485,7 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
     if (a.self_coef != 0.0) {  // 2T term first (Eq. 2.7)
       for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
         const int rel = a.A.col[p] - lo;
-        const int b = page_slot(ptab, rel >> sh, psize, &s_slots);
+        const int b = page_slot(ptab, rel >> sh, psize, &s_slots, kSlots);
         if (b >= 0) vals[b + (rel & (psize - 1))] = __dmul_rn(a.self_coef, a.A.val[p]);
         else s_fail = 1;
       }
@@ -1468,13 +1512,13 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
       }
       __syncthreads();
       const int cn = nk - kc < kThreads ? nk - kc : kThreads;
-      // register ring: the first two entries (tid, tid + 256) of the next kPF k's
-      int32_t pc[kPF][2];
-      double pv[kPF][2];
+      // register ring: entries tid + u * kThreads (u < NE) of the next kPF k's
+      int32_t pc[kPF][NE];
+      double pv[kPF][NE];
 #pragma unroll
       for (int d = 0; d < kPF; d++) {
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+        for (int u = 0; u < NE; u++) {
           pc[d][u] = 0;
           pv[d][u] = 0.0;
           if (d < cn) {
@@ -1494,50 +1538,53 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
             const long long st0 = s_start[kk];
             const int ln = s_len[kk];
             const double av = s_av[kk];
-            const int32_t c0 = pc[d][0], c1 = pc[d][1];
-            const double v0 = pv[d][0], v1 = pv[d][1];
+            int32_t c[NE];
+            double v[NE];
+#pragma unroll
+            for (int u = 0; u < NE; u++) {
+              c[u] = pc[d][u];
+              v[u] = pv[d][u];
+            }
             const int kn = kk + kPF;  // refill this ring slot
             if (kn < cn) {
               const int nl = s_len[kn];
               const long long ns = s_start[kn];
-              if (tid < nl) {
-                pc[d][0] = a.B.col[ns + tid];
-                pv[d][0] = a.B.val[ns + tid];
-              }
-              if (tid + kThreads < nl) {
-                pc[d][1] = a.B.col[ns + tid + kThreads];
-                pv[d][1] = a.B.val[ns + tid + kThreads];
+#pragma unroll
+              for (int u = 0; u < NE; u++) {
+                if (tid + u * kThreads < nl) {
+                  pc[d][u] = a.B.col[ns + tid + u * kThreads];
+                  pv[d][u] = a.B.val[ns + tid + u * kThreads];
+                }
               }
             }
-            if (tid < ln) {
-              int rel = c0 - lo;
-              int b = page_slot(ptab, rel >> sh, psize, &s_slots);
+            // slot lookups, then the cell loads, multiply-adds and stores (the entries of
+            // one B row have distinct columns)
+            int o[NE];
+#pragma unroll
+            for (int u = 0; u < NE; u++) {
+              o[u] = -1;
+              if (tid + u * kThreads < ln) {
+                const int rel = c[u] - lo;
+                const int b = page_slot(ptab, rel >> sh, psize, &s_slots, kSlots);
+                if (b >= 0) o[u] = b + (rel & (psize - 1));
+                else s_fail = 1;
+              }
+            }
+            double x[NE];
+#pragma unroll
+            for (int u = 0; u < NE; u++) x[u] = o[u] >= 0 ? vals[o[u]] : 0.0;
+#pragma unroll
+            for (int u = 0; u < NE; u++)
+              if (o[u] >= 0) vals[o[u]] = __dadd_rn(x[u], __dmul_rn(av, v[u]));
+            for (int e = tid + NE * kThreads; e < ln; e += kThreads) {
+              const int rel = a.B.col[st0 + e] - lo;
+              const double vv = a.B.val[st0 + e];
+              const int b = page_slot(ptab, rel >> sh, psize, &s_slots, kSlots);
               if (b >= 0) {
-                const int o = b + (rel & (psize - 1));
-                vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v0));
+                const int oo = b + (rel & (psize - 1));
+                vals[oo] = __dadd_rn(vals[oo], __dmul_rn(av, vv));
               } else {
                 s_fail = 1;
-              }
-              if (tid + kThreads < ln) {
-                rel = c1 - lo;
-                b = page_slot(ptab, rel >> sh, psize, &s_slots);
-                if (b >= 0) {
-                  const int o = b + (rel & (psize - 1));
-                  vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v1));
-                } else {
-                  s_fail = 1;
-                }
-              }
-              for (int e = tid + 2 * kThreads; e < ln; e += kThreads) {
-                rel = a.B.col[st0 + e] - lo;
-                const double v = a.B.val[st0 + e];
-                b = page_slot(ptab, rel >> sh, psize, &s_slots);
-                if (b >= 0) {
-                  const int o = b + (rel & (psize - 1));
-                  vals[o] = __dadd_rn(vals[o], __dmul_rn(av, v));
-                } else {
-                  s_fail = 1;
-                }
               }
             }
             __syncthreads();  // one writer per slot at any time (k -> k+1)
@@ -1690,13 +1737,22 @@ __global__ void __launch_bounds__(kThreads) k_numeric_paged(NumericArgs a, int32
   }
 }
 
+template <class CFG>
+static void launch_paged_cfg(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                             cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  const int smem = CFG::smem();
+  cudaFuncSetAttribute(k_numeric_paged<CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_paged<CFG><<<a.grid, CFG::kT, smem, st>>>(a, fail_rows, fail_count);
+}
 void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
                           cudaStream_t st) {
-  if (a.A.nrows == 0 || a.nlist == 0) return;
-  int smem = paged_smem_bytes();
-  cudaFuncSetAttribute(k_numeric_paged, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  KL;
-  k_numeric_paged<<<a.grid, kThreads, smem, st>>>(a, fail_rows, fail_count);
+  launch_paged_cfg<PagedV1>(a, fail_rows, fail_count, st);
+}
+void launch_numeric_paged2(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                           cudaStream_t st) {
+  launch_paged_cfg<PagedV2>(a, fail_rows, fail_count, st);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1773,7 +1829,7 @@ __global__ void __launch_bounds__(kThreads) k_taylor_pull(NumericArgs a, CsrView
     for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
       const int32_t k = a.A.col[p];
       const int rel = k - alo;
-      const int b = page_slot(ptab, rel >> sh, psize, &s_slots);
+      const int b = page_slot(ptab, rel >> sh, psize, &s_slots, kTSlots);
       if (b >= 0 && b + psize <= kTSlots) vals[b + (rel & (psize - 1))] = a.A.val[p];
       else s_fail = 1;
       const int64_t kb = (int64_t)k - a.B.row0;

@@ -115,6 +115,10 @@ void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_co
 int paged_smem_bytes();
 void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
                           cudaStream_t st);
+// the same with 128 threads per row, 4 entries per thread per k, smaller footprint
+int paged2_smem_bytes();
+void launch_numeric_paged2(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
+                           cudaStream_t st);
 // Taylor term by pull over H0^T (bit-identical order); BT = CSC of B (= B^T as CSR)
 int taylor_pull_smem_bytes();
 void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_rows,

@@ -260,7 +260,7 @@ def test_alg41_random_vs_oracle(B):
         assert d == pytest.approx(dropped_o, rel=1e-10, abs=1e-300)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
 @pytest.mark.parametrize("name", ["heat2d_pm10_20", "structural_24", "heat3d_9", "banded_nonsym"])
 def test_accumulator_variants(B, kernel, name):
     """Every K3 accumulator (hash, warp-window, block-window) meets parity."""
@@ -269,7 +269,7 @@ def test_accumulator_variants(B, kernel, name):
     assert_parity(Eg, st, Eo, tr)
 
 
-@pytest.mark.parametrize("kernel", [2, 4, 5, 8, 9])
+@pytest.mark.parametrize("kernel", [2, 4, 5, 8, 9, 10])
 @pytest.mark.parametrize("seed", range(4))
 def test_bit_exact_products(B, seed, kernel):
     """The warp-window, k-sync hash, paged and grouped kernels accumulate the self term
@@ -346,7 +346,7 @@ def _coo(n, rows, cols, vals):
     return coo_to_csr(n, rows[first], cols[first], np.asarray(vals, np.float64)[first])
 
 
-@pytest.mark.parametrize("kernel", [8, 9, 0])
+@pytest.mark.parametrize("kernel", [8, 9, 10, 0])
 def test_group_kernel_long_b_rows(B, kernel):
     """B rows longer than the grouped kernel's CTA (> 512 entries): the extra entries loop;
     A x B + 2A is still bit-identical to the oracle."""
