@@ -300,21 +300,31 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic_db = {}
+    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tp):
+        traffic_db = json.load(open(tp))
     if sum(sq_ms) >= sum(ty_ms) and sq_ms:
         dur = sum(sq_ms) / len(sq_ms) / 1e3
         ach = sum(sq_fl) / len(sq_fl) / dur / 1e12
-        roof = {"kernel": "k_numeric (squaring SpGEMM + 2T + filter classify)", "bound": "alu",
+        tr = traffic_db.get("k_numeric_paged")
+        roof = {"kernel": "k_numeric_paged (squaring SpGEMM + 2T + filter classify)", "bound": "alu",
                 "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "frac": ach / FP64_PEAK_TFLOPS,
+                "traffic": tr["dram_bytes"] if tr and args.config == 5 else None,
+                "traffic_launch": tr["launch"] if tr and args.config == 5 else None,
+                "traffic_compulsory_bytes": float(st["sq_numeric_bytes"][1]),
                 "peak_source": "derived fp64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)",
                 "launches_per_step": len(sq_ms), "avg_launch_ms": dur * 1e3,
                 "hbm_gbs_compulsory": sum(float(st["sq_numeric_bytes"][i]) for i in range(1, N + 1)) / len(sq_ms) / dur / 1e9}
     elif ty_ms:
         dur = sum(ty_ms) / len(ty_ms) / 1e3
         ach = sum(ty_by) / len(ty_by) / dur / 1e9
-        roof = {"kernel": "k_numeric (Taylor term S H0 / i + filter classify)", "bound": "hbm",
+        tr = traffic_db.get("k_taylor_dia")
+        roof = {"kernel": "k_taylor_dia (Taylor term S H0 / i + filter classify)", "bound": "hbm",
                 "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "traffic": tr["dram_bytes"] if tr and args.config == 5 else None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "launches_per_step": len(ty_ms), "avg_launch_ms": dur * 1e3}
     else:
         roof = None
