@@ -90,7 +90,9 @@ typedef struct {
   int32_t force_N;        /* -1 = from Eq. (4.20) */
   int32_t output_T;       /* 0 = return E = I + T^_N (default); 1 = return T^_N */
   int32_t window_cols;    /* dense accumulator window of the block-window kernel (0 = 8192) */
-  int32_t kernel;         /* K3 accumulator: 0 auto (k-sync paged for squarings; for Taylor
+  int32_t kernel;         /* K3 accumulator: 0 auto (block-sparse 11 for squarings on one GPU,
+                             k-sync paged 5 for multi-GPU squarings and rows it cannot hold;
+                             for Taylor
                              terms the diagonal push kernel when H0 has <= 16 distinct
                              diagonal offsets, else the pull over H0^T), 1 atomic hash,
                              2 warp-window, 3 block-window, 4 k-synchronous hash, 5 k-synchronous
@@ -98,9 +100,11 @@ typedef struct {
                              push (Taylor terms only; else as 0), 8 grouped rows (4 rows per
                              CTA share each B-row gather, TMA-staged), 9 one warp per row (8
                              rows per CTA share a page table), 10 k-sync paged with 128
-                             threads per row.  All meet parity; 2 and 4-10 reproduce the
-                             oracle's C~ bit for bit.  Rows a kernel cannot hold fall through
-                             8/9/10 -> 5 -> 3, 7 -> 6 -> 1 -> 3 and 1/4/5 -> 3. */
+                             threads per row, 11 block-sparse (BSR-8 view, register-held
+                             8x8 output blocks; squarings on one GPU, else as 5).  All meet
+                             parity; 2 and 4-11 reproduce the oracle's C~ bit for bit.  Rows
+                             a kernel cannot hold fall through 8-11 -> 5 -> 3,
+                             7 -> 5 -> 3, 6 -> 1 -> 3 and 1/4/5 -> 3. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */

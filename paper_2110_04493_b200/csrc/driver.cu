@@ -202,11 +202,13 @@ static void *alloc(size_t bytes, cudaStream_t st, size_t *got) {
     }
   }
   cudaError_t e = cudaMallocAsync(&p, bytes, st);
-  if (e == cudaErrorMemoryAllocation) {
+  if (e == cudaErrorMemoryAllocation) {  // give everything cached back, trim the pool, retry
     cudaGetLastError();
     cudaStreamSynchronize(st);
     release_all();
     cudaDeviceSynchronize();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     e = cudaMallocAsync(&p, bytes, st);
   }
   if (e != cudaSuccess) {
@@ -226,10 +228,19 @@ static void *alloc(size_t bytes, cudaStream_t st, size_t *got) {
             bytes_allocated / 1e9, bytes_cached / 1e9);
   return p;
 }
+// large blocks that are not parked (growth trails of a cold plan) go back to the CUDA pool
+// at once: only the parked final blocks and small blocks are kept
+constexpr size_t kKeepMax = (size_t)64 << 20;
 static void free(void *p, size_t bytes, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
+  if (bytes >= kKeepMax) {
+    if (freeing_idle || st == nullptr) cudaFree(p);
+    else cudaFreeAsync(p, st);
+    bytes_allocated -= (double)bytes;
+    return;
+  }
   free_blocks.emplace(bytes, Block{p, bytes, freeing_idle ? nullptr : st, dev});
   bytes_cached += (double)bytes;
 }
@@ -240,9 +251,9 @@ static void park(int role, void *p, size_t bytes) {  // idle blocks only (plan d
   Block &b = parked[role];
   Block other{p, bytes, nullptr, dev};
   if (!b.p || (b.bytes < bytes && b.dev == dev)) std::swap(b, other);  // keep the larger one
-  if (other.p) {
-    free_blocks.emplace(other.bytes, other);
-    bytes_cached += (double)other.bytes;
+  if (other.p) {  // the smaller block of a role goes back to the pool
+    cudaFree(other.p);
+    bytes_allocated -= (double)other.bytes;
   }
 }
 static void *unpark(int role, size_t bytes, size_t *got) {
@@ -373,6 +384,12 @@ struct Workspace {
   DBuf<int32_t> fail_rows, fail_rows2;
   DBuf<int8_t> ident;
   DBuf<unsigned long long> prof;
+  // BSR-8 view of the squared iterate (kernel 11)
+  DBuf<int64_t> bcnt, brp, scan_tmp2, tp, cnt64, tb, tb_tmp;
+  DBuf<int32_t> bcol, tcnt, tk, tk_tmp;
+  DBuf<double> bval, bscr;
+  DBuf<unsigned char> sort_tmp;
+  DBuf<int32_t> keys_tmp;
   int64_t pool_cap_hint = 0;
 };
 
@@ -646,8 +663,12 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     const bool group_ok = ((uintptr_t)B.col % 16 == 0) && ((uintptr_t)B.val % 16 == 0);
     // squarings: the k-synchronous paged kernel (measured fastest on configs 2, 3 and 5;
     // the grouped kernels 8 / 9 are options)
-    if (kern == 0) kern = self != 0.0 ? 5 : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
+    if (kern == 0) kern = self != 0.0 ? 11 : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
     if (kern == 8 && !group_ok) kern = 5;
+    // the block kernel squares one matrix held whole on this GPU (its BSR view is A's);
+    // Taylor terms keep their own kernels
+    if (kern == 11 && self == 0.0) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 1);
+    if (kern == 11 && (P.world > 1 || B.rp != A.rp)) kern = 5;
     if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 1;
     if (kern == 6 && !taylor_pull_ok) kern = 1;
     if (kern == 7) CK(cudaMemsetAsync(P.dia_prod.p, 0, sizeof(unsigned long long), st));
@@ -679,7 +700,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       int stage = kern;
       bool first = true;
       // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
-      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10);
+      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10 || kern == 11);
       while (nlist > 0) {
         if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
           run_symbolic();
@@ -718,6 +739,57 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         } else if (stage == 5) {
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
+        } else if (stage == 11) {
+          // BSR-8 view of A (= B) and its block transpose, then the block kernel over block
+          // rows in index order
+          const int64_t nbr = (nr + 7) / 8, nbc = (P.n + 7) / 8;
+          w.bcnt.ensure((size_t)nbr + 1, st);
+          w.brp.ensure((size_t)nbr + 1, st);
+          w.scan_tmp2.ensure((size_t)scan_tmp_elems(std::max(nbr, nbc)) + 1, st);
+          CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+          launch_bsr_count(A, nbr, w.bcnt.p, w.flags.p, st);
+          launch_reduce_max_i64(w.bcnt.p, nbr, w.i64tmp.p + 7, st);
+          launch_exclusive_scan(w.bcnt.p, nbr, w.brp.p, w.scan_tmp2.p, st);
+          int64_t nb = 0, bmax = 0;
+          int bflags = 0;
+          CK(cudaMemcpyAsync(&nb, w.brp.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+          CK(cudaMemcpyAsync(&bmax, w.i64tmp.p + 7, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+          CK(cudaMemcpyAsync(&bflags, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          // block rows too wide for the view or for the kernel's shared-memory row of A: the
+          // whole product goes to the paged kernel
+          if ((bflags & 4) || bmax > kBsrMaxRowBlocks) {
+            stage = 5;
+            continue;
+          }
+          w.bcol.ensure((size_t)std::max<int64_t>(nb, 1), st);
+          w.bval.ensure((size_t)std::max<int64_t>(nb, 1) * 64, st);
+          launch_bsr_fill(A, nbr, w.brp.p, w.bcol.p, w.bval.p, w.flags.p, st);
+          w.tcnt.ensure((size_t)nbc + 1, st);
+          w.tp.ensure((size_t)nbc + 1, st);
+          w.cnt64.ensure((size_t)nbc + 1, st);
+          w.tk.ensure((size_t)std::max<int64_t>(nb, 1), st);
+          w.tk_tmp.ensure((size_t)std::max<int64_t>(nb, 1), st);
+          w.tb.ensure((size_t)std::max<int64_t>(nb, 1), st);
+          w.tb_tmp.ensure((size_t)std::max<int64_t>(nb, 1), st);
+          const size_t sbytes = bsr_transpose_temp_bytes(nb);
+          w.sort_tmp.ensure(sbytes + 256, st);
+          w.keys_tmp.ensure((size_t)std::max<int64_t>(nb, 1), st);
+          launch_bsr_transpose(nbr, nbc, nb, w.brp.p, w.bcol.p, w.tcnt.p, w.tp.p, w.tk_tmp.p,
+                               w.tb_tmp.p, w.tk.p, w.tb.p, w.scan_tmp2.p, w.cnt64.p, w.sort_tmp.p,
+                               w.sort_tmp.n, w.keys_tmp.p, st);
+          BsrView Bv;
+          Bv.nbr = nbr;
+          Bv.brp = w.brp.p;
+          Bv.bcol = w.bcol.p;
+          Bv.bval = w.bval.p;
+          Bv.tp = w.tp.p;
+          Bv.tk = w.tk.p;
+          Bv.tb = w.tb.p;
+          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, (int64_t)P.sm_count * 2));
+          w.bscr.ensure((size_t)nh.grid * kBsrScratchPerCta, st);
+          CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
+          launch_numeric_bsr(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
         } else if (stage == 10) {
           nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged2_blocks_per_sm));
           launch_numeric_paged2(nh, fout, w.fail_count.p, st);
@@ -769,8 +841,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         list = fout;
         nlist = nf;
         fb ^= 1;
-        stage = stage == 7 ? (taylor_pull_ok ? 6 : 1)
-                           : (stage == 6 ? 1 : ((stage >= 8 && stage <= 10) ? 5 : 3));
+        // fall-through: K5d rows too wide for its slots -> paged; K5p -> hash; the squaring
+        // kernels -> paged; everything else -> the block-window kernel (no capacity limit)
+        stage = stage == 7 ? 5 : (stage == 6 ? 1 : ((stage >= 8 && stage <= 11) ? 5 : 3));
       }
     }
     rep.window_rows = nfail;
@@ -1515,6 +1588,9 @@ static void do_run(sexpm_plan_s &P) {
       swap_csr(T, Tn);
       swap_csr(Sc, Sn);
       if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();
+      if (getenv("SEXPM_STEP_LOG"))
+        fprintf(stderr, "[sexpm run] taylor %d: nnz %lld passes %d numeric %.1f ms fallback %lld\n", i,
+                (long long)rep.nnz, rep.passes, rep.numeric_ms, (long long)rep.window_rows);
     }
   }
   P.M_eff = M_eff;
@@ -1578,6 +1654,9 @@ static void do_run(sexpm_plan_s &P) {
       for (int q = 0; q < 12; q++) S.sq_group_prof[i][q] = (double)rep.prof[q];
       S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)dst.nnz + 16.0 * (double)nl;
     }
+    if (getenv("SEXPM_STEP_LOG"))
+      fprintf(stderr, "[sexpm run] squaring %d: nnz %lld passes %d numeric %.1f ms (first kernel %.1f) fallback %lld\n",
+              i, (long long)rep.nnz, rep.passes, rep.numeric_ms, rep.first_ms, (long long)rep.window_rows);
     normIT = sqrt(rep.normIT2);
     l1 = rep.l1;
     l2 = rep.l2;
@@ -1736,6 +1815,15 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
     }
     P->ws.pool_col.role = role++;
     P->ws.pool_val.role = role++;
+    P->ws.bval.role = role++;
+    P->ws.bcol.role = role++;
+    P->ws.tk.role = role++;
+    P->ws.tk_tmp.role = role++;
+    P->ws.tb.role = role++;
+    P->ws.tb_tmp.role = role++;
+    P->ws.bscr.role = role++;
+    P->ws.keys_tmp.role = role++;
+    P->ws.sort_tmp.role = role++;
   }
   {
     std::lock_guard<std::mutex> lk(cache::mu);

@@ -7,7 +7,10 @@
 //   (Eq. 2.7, Eq. 4.15, Eq. 4.11), K6 Algorithm 4.1 pass,
 //   K4 compaction ("A~ = A - b_n"), merge T^_0 += S^_i and I + T.
 #include <math.h>
+#include <algorithm>
 #include <stdint.h>
+
+#include <cub/cub.cuh>
 
 #include "kernels.cuh"
 
@@ -350,6 +353,10 @@ void launch_row_lengths(const int64_t *rp, int64_t nrows, int64_t *out, cudaStre
   k_row_lengths<<<grid_for(nrows, kThreads), kThreads, 0, st>>>(rp, nrows, out);
 }
 
+__global__ void k_i32_to_i64(const int32_t *in, int64_t cnt, int64_t *out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) out[i] = in[i];
+}
 __global__ void k_copy_i64_offset(const int64_t *src, int64_t cnt, int64_t off, int64_t *dst) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < cnt) dst[i] = src[i] + off;
@@ -2983,6 +2990,522 @@ void launch_numeric_rowwarp(const NumericArgs &a, int slots, int32_t *fail_rows,
   cudaFuncSetAttribute(k_numeric_rowwarp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
   k_numeric_rowwarp<<<a.grid, kRThreads, smem, st>>>(a, slots, fail_rows, fail_count);
+}
+
+// ------------------------------------------------------------------------------------
+// BSR-8 view of a CSR matrix (squarings, one GPU): block row I = rows 8I..8I+7, block
+// column J = columns 8J..8J+7, dense 8x8 blocks (row-major, zeros where the CSR has no
+// entry), block columns sorted.  Plus the block transpose: for every block column J the
+// block rows K (ascending) holding a block (K, J) and that block's index.
+// ------------------------------------------------------------------------------------
+constexpr int kBsrWarps = 8;
+constexpr int kBsrSpanWords = 512;  // block-column span per block row: 16384 blocks
+
+// count pass (fill = false) and fill pass (fill = true); warp per block row
+template <bool FILL>
+__global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t nbr, int64_t *bcnt,
+                                                              const int64_t *brp, int32_t *bcol,
+                                                              double *bval, int *flags) {
+  __shared__ unsigned bits[kBsrWarps][kBsrSpanWords];
+  __shared__ uint16_t prefs[kBsrWarps][kBsrSpanWords];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t I = (int64_t)blockIdx.x * kBsrWarps + wib;
+  if (I >= nbr) return;
+  unsigned *bm = bits[wib];
+  uint16_t *pref = prefs[wib];
+  const int64_t r0 = 8 * I, r1 = r0 + 8 < A.nrows ? r0 + 8 : A.nrows;
+  int32_t jmin = INT32_MAX, jmax = -1;
+  for (int64_t r = r0; r < r1; r++) {
+    const int64_t p0 = A.rp[r], p1 = A.rp[r + 1];
+    if (p1 > p0) {
+      jmin = min(jmin, A.col[p0] >> 3);
+      jmax = max(jmax, A.col[p1 - 1] >> 3);
+    }
+  }
+  if (jmax < jmin) {
+    if (!FILL && lane == 0) bcnt[I] = 0;
+    return;
+  }
+  const int nw = ((jmax - jmin) >> 5) + 1;
+  if (nw > kBsrSpanWords) {
+    if (lane == 0) {
+      atomicOr(flags, 4);
+      if (!FILL) bcnt[I] = 0;
+    }
+    return;
+  }
+  for (int w = lane; w < nw; w += 32) bm[w] = 0u;
+  __syncwarp();
+  for (int64_t r = r0; r < r1; r++) {
+    for (int64_t p = A.rp[r] + lane; p < A.rp[r + 1]; p += 32) {
+      const int b = (A.col[p] >> 3) - jmin;
+      atomicOr(&bm[b >> 5], 1u << (b & 31));
+    }
+  }
+  __syncwarp();
+  if (!FILL) {
+    int c = 0;
+    for (int w = lane; w < nw; w += 32) c += __popc(bm[w]);
+    c = __reduce_add_sync(FULL_MASK, c);
+    if (lane == 0) bcnt[I] = c;
+    return;
+  }
+  // ranks: exclusive popcount prefix over the words, 1 lane per word chunk
+  const int per = (nw + 31) / 32;
+  const int w0 = min(lane * per, nw), w1 = min(w0 + per, nw);
+  int cnt = 0;
+  for (int w = w0; w < w1; w++) cnt += __popc(bm[w]);
+  int v = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, v, o);
+    if (lane >= o) v += y;
+  }
+  const int64_t base = brp[I];
+  int run = v - cnt;
+  for (int w = w0; w < w1; w++) {
+    pref[w] = (uint16_t)run;
+    unsigned m = bm[w];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      bcol[base + run] = jmin + w * 32 + b;
+      run++;
+    }
+  }
+  const int64_t nb = brp[I + 1] - base;
+  for (int64_t t = lane; t < nb * 64; t += 32) bval[base * 64 + t] = 0.0;
+  __syncwarp();
+  // ranks of each word for the scatter: recompute the prefix in place (word -> rank)
+  // (bm[w] keeps its bits; the rank of block b = popc of the words before + bits below)
+  for (int64_t r = r0; r < r1; r++) {
+    const int ri = (int)(r - r0);
+    for (int64_t p = A.rp[r] + lane; p < A.rp[r + 1]; p += 32) {
+      const int c = A.col[p];
+      const int b = (c >> 3) - jmin;
+      const int rank = pref[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
+      bval[(base + rank) * 64 + ri * 8 + (c & 7)] = A.val[p];
+    }
+  }
+}
+void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st) {
+  if (nbr == 0) return;
+  KL;
+  k_bsr_build<false><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, bcnt, nullptr,
+                                                                           nullptr, nullptr, flags);
+}
+void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
+                     double *bval, int *flags, cudaStream_t st) {
+  if (nbr == 0) return;
+  KL;
+  k_bsr_build<true><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, nullptr, brp,
+                                                                          bcol, bval, flags);
+}
+
+// block transpose: a stable radix sort of the blocks (enumerated block row by block row,
+// i.e. K ascending) by block column J keeps K ascending inside every column; column
+// pointers by a count and a scan.
+__global__ void k_bsr_rows_of_blocks(int64_t nbr, const int64_t *brp, int32_t *brow, int64_t *bidx) {
+  const int64_t K = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (K >= nbr) return;
+  for (int64_t b = brp[K] + lane; b < brp[K + 1]; b += 32) {
+    brow[b] = (int32_t)K;
+    bidx[b] = b;
+  }
+}
+__global__ void k_bsrT_count(int64_t nb, const int32_t *bcol, int32_t *tcnt) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&tcnt[bcol[b]], 1);
+}
+__global__ void k_gather_i32(const int32_t *src, const int64_t *idx, int64_t cnt, int32_t *dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+size_t bsr_transpose_temp_bytes(int64_t nb) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                  (const int64_t *)nullptr, (int64_t *)nullptr, (int)std::max<int64_t>(nb, 1));
+  return bytes;
+}
+void launch_bsr_transpose(int64_t nbr, int64_t nbc, int64_t nb, const int64_t *brp,
+                          const int32_t *bcol, int32_t *tcnt, int64_t *tp, int32_t *tk_tmp,
+                          int64_t *tb_tmp, int32_t *tk, int64_t *tb, int64_t *scan_tmp,
+                          int64_t *cnt64, void *sort_tmp, size_t sort_tmp_bytes, int32_t *keys_out,
+                          cudaStream_t st) {
+  cudaMemsetAsync(tcnt, 0, (size_t)std::max<int64_t>(nbc, 1) * sizeof(int32_t), st);
+  if (nb > 0) {
+    KL;
+    k_bsrT_count<<<grid_for(nb, kThreads, 148 * 16), kThreads, 0, st>>>(nb, bcol, tcnt);
+  }
+  KL;
+  k_i32_to_i64<<<grid_for(nbc, kThreads), kThreads, 0, st>>>(tcnt, nbc, cnt64);
+  launch_exclusive_scan(cnt64, nbc, tp, scan_tmp, st);
+  if (nb == 0) return;
+  KL;
+  k_bsr_rows_of_blocks<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(nbr, brp, tk_tmp, tb_tmp);
+  // sort (J, block index) pairs by J, stable: within a column the block indices (and so K)
+  // stay ascending
+  int bits = 1;
+  while (bits < 31 && (int64_t(1) << bits) <= nbc) bits++;
+  KL;
+  cub::DeviceRadixSort::SortPairs(sort_tmp, sort_tmp_bytes, bcol, keys_out, tb_tmp, tb, (int)nb, 0,
+                                  bits, st);
+  KL;
+  k_gather_i32<<<grid_for(nb, kThreads, 148 * 16), kThreads, 0, st>>>(tk_tmp, tb, nb, tk);
+}
+
+// ------------------------------------------------------------------------------------
+// K3b numeric filtered SpGEMM on the BSR-8 view (squarings, one GPU):
+//
+//   C~_IJ = self * A_IJ + sum_K A_IK B_KJ      (8x8 blocks; Eq. 2.7, Eq. 4.15)
+//
+// One CTA per block row I (8 rows).  A's blocks of row I sit in shared memory (value rows
+// and a bitmap of their block columns K); the candidate output blocks J are the union of the
+// block rows B_K, K in row I (bitmap).  A warp computes whole output blocks: lane l holds
+// C[i][j] for i = l/8 and l/8 + 4, j = l%8, in registers, starting from the self term, then
+// for every K common to row I of A and column J of B (the block transpose lists K
+// ascending) it adds a[i][k] * b[k][j] for k = 0..7 with _rn products and sums.  Every
+// element therefore sees the self term and then ascending k -- a k outside the row's or the
+// column's pattern contributes 0 * b or a * 0, which leaves the value bit-identical -- so C~
+// is bit-identical to the oracle's.  The dense blocks go to this CTA's scratch (L2), the
+// kept counts per (J, row) to shared memory; then each row's entries above the floor are
+// staged contiguously in column order (block columns ascending).  The redundant products on
+// the zeros of partly filled blocks (~3.6x at config 5) are paid in registers, not in
+// shared-memory read-modify-writes.
+// ------------------------------------------------------------------------------------
+constexpr int kBThreads = 256;
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kBACap = kBsrMaxRowBlocks;  // blocks of a row of A held in shared memory
+constexpr int kBKWords = 256;    // K bitmap: block-column span of A's row <= 8192
+constexpr int kBJWords = 512;    // J bitmap: output block-column span <= 16384
+constexpr int kBJCap = kBsrScratchPerCta / 64;  // output blocks per block row
+
+int bsr_numeric_smem_bytes() {
+  return kBACap * 64 * 8 + kBACap * 4 + kBKWords * 4 + kBKWords * 2 + kBJWords * 4 +
+         kBJCap * 4 + kBJCap * 8 * 2 + 64;
+}
+
+// BsrView (kernels.cuh): brp / bcol / bval = block rows, sorted block columns, 64 values
+// per block row-major; tp / tk / tb = block transpose: column J's block rows K (ascending)
+// and block indices.
+
+__global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, BsrView Bv, int64_t nrows,
+                                                              double *scratch, int32_t *fail_rows,
+                                                              int *fail_count) {
+  extern __shared__ double bsm[];
+  double *aval = bsm;                                                  // kBACap * 64
+  int32_t *aK = reinterpret_cast<int32_t *>(aval + kBACap * 64);       // kBACap
+  unsigned *kbits = reinterpret_cast<unsigned *>(aK + kBACap);         // kBKWords
+  uint16_t *kpref = reinterpret_cast<uint16_t *>(kbits + kBKWords);    // kBKWords
+  unsigned *jbits = reinterpret_cast<unsigned *>(kpref + kBKWords);    // kBJWords
+  int32_t *jlist = reinterpret_cast<int32_t *>(jbits + kBJWords);      // kBJCap
+  uint16_t *jcnt = reinterpret_cast<uint16_t *>(jlist + kBJCap);       // kBJCap * 8
+  __shared__ int s_I, s_fail, s_na, s_nj, s_kmin, s_jmin, s_nkw, s_njw;
+  __shared__ double s_fs[kBWarps][8], s_p1[kBWarps][8];
+  __shared__ long long s_nz[kBWarps][8], s_c1[kBWarps][8];
+  __shared__ unsigned long long s_off[8];
+  __shared__ long long s_tot[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *scr = scratch + (size_t)blockIdx.x * kBJCap * 64;
+  for (int i = tid; i < kBKWords; i += kBThreads) kbits[i] = 0u;
+  for (int i = tid; i < kBJWords; i += kBThreads) jbits[i] = 0u;
+  const int li = lane >> 3, lj = lane & 7;  // lane holds C[li][lj] and C[li + 4][lj]
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_I = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int64_t I = s_I;
+    if (I >= Bv.nbr) break;
+    const int64_t r0 = 8 * I;
+    const int nr = (int)(nrows - r0 < 8 ? nrows - r0 : 8);
+    const int64_t ab0 = Bv.brp[I], ab1 = Bv.brp[I + 1];
+    const int na = (int)(ab1 - ab0);
+    if (tid == 0) {
+      int fail = na > kBACap;
+      int jmin = INT32_MAX, jmax = -1;
+      for (int i = 0; i < nr; i++) {
+        const int64_t r = r0 + i;
+        if (a.hi[r] >= a.lo[r]) {
+          jmin = min(jmin, a.lo[r] >> 3);
+          jmax = max(jmax, a.hi[r] >> 3);
+        }
+      }
+      const int kmin = na > 0 ? Bv.bcol[ab0] : 0, kmax = na > 0 ? Bv.bcol[ab1 - 1] : -1;
+      if (na > 0 && ((kmax - kmin) >> 5) + 1 > kBKWords) fail = 1;
+      if (jmax >= jmin && ((jmax - jmin) >> 5) + 1 > kBJWords) fail = 1;
+      s_fail = fail;
+      s_na = na;
+      s_kmin = kmin;
+      s_jmin = jmin;
+      s_nkw = na > 0 ? ((kmax - kmin) >> 5) + 1 : 0;
+      s_njw = jmax >= jmin ? ((jmax - jmin) >> 5) + 1 : 0;
+    }
+    __syncthreads();
+    if (s_fail || na == 0 || s_njw == 0) {
+      if (tid < nr) {
+        const int64_t r = r0 + tid;
+        if (s_fail) {
+          fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+        } else {
+          a.row_off[r] = 0;
+          a.row_cnt[r] = 0;
+          a.row_fsum[r] = 0.0;
+          a.row_nnz[r] = 0;
+          if (a.row_p1) {
+            a.row_p1[r] = 0.0;
+            a.row_c1[r] = 0;
+          }
+        }
+      }
+      continue;
+    }
+    const int kmin = s_kmin, jmin = s_jmin, nkw = s_nkw, njw = s_njw;
+    // (1) row I of A: block columns, values, K bitmap
+    for (int t = tid; t < na; t += kBThreads) {
+      const int K = Bv.bcol[ab0 + t];
+      aK[t] = K;
+      atomicOr(&kbits[(K - kmin) >> 5], 1u << ((K - kmin) & 31));
+    }
+    for (int t = tid; t < na * 64; t += kBThreads) aval[t] = Bv.bval[ab0 * 64 + t];
+    __syncthreads();
+    if (tid < 32) {  // word prefix of the K bitmap
+      const int per = (nkw + 31) / 32;
+      const int w0 = min(lane * per, nkw), w1 = min(w0 + per, nkw);
+      int c = 0;
+      for (int w = w0; w < w1; w++) c += __popc(kbits[w]);
+      int v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, v, o);
+        if (lane >= o) v += y;
+      }
+      int run = v - c;
+      for (int w = w0; w < w1; w++) {
+        kpref[w] = (uint16_t)run;
+        run += __popc(kbits[w]);
+      }
+    }
+    // (2) candidate output blocks: union of the block rows of B at A's block columns
+    for (int t = warp; t < na; t += kBWarps) {
+      const int64_t K = aK[t];
+      if (K < Bv.nbr) {
+        for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
+          const int jb = Bv.bcol[b] - jmin;
+          if (jb >= 0 && jb < njw * 32) atomicOr(&jbits[jb >> 5], 1u << (jb & 31));
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int per = (njw + 31) / 32;
+      const int w0 = min(lane * per, njw), w1 = min(w0 + per, njw);
+      int c = 0;
+      for (int w = w0; w < w1; w++) c += __popc(jbits[w]);
+      int v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, v, o);
+        if (lane >= o) v += y;
+      }
+      const int tot = __shfl_sync(FULL_MASK, v, 31);
+      if (lane == 0) s_nj = tot;
+      if (tot <= kBJCap) {
+        int run = v - c;
+        for (int w = w0; w < w1; w++) {
+          unsigned m = jbits[w];
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            jlist[run++] = jmin + w * 32 + b;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nj = s_nj;
+    const bool over = nj > kBJCap;
+    // (3) output blocks, one warp each
+    double fs0 = 0.0, fs1 = 0.0, q10 = 0.0, q11 = 0.0;
+    long long nz0 = 0, nz1 = 0, c10 = 0, c11 = 0;
+    const int i0 = li, i1 = li + 4;
+    if (!over) {
+      for (int q = warp; q < nj; q += kBWarps) {
+        const int J = jlist[q];
+        double x0 = 0.0, x1 = 0.0;
+        {  // self term: A_IJ, if row I of A has block J
+          const int kb = J - kmin;
+          if (a.self_coef != 0.0 && kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
+            const int ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
+            x0 = __dmul_rn(a.self_coef, aval[ra * 64 + i0 * 8 + lj]);
+            x1 = __dmul_rn(a.self_coef, aval[ra * 64 + i1 * 8 + lj]);
+          }
+        }
+        const int64_t t0 = Bv.tp[J], t1 = Bv.tp[J + 1];
+        for (int64_t tb0 = t0; tb0 < t1; tb0 += 32) {
+          const int64_t t = tb0 + lane;
+          int K = -1;
+          int64_t bidx = 0;
+          int ra = -1;
+          if (t < t1) {
+            K = Bv.tk[t];
+            const int kb = K - kmin;
+            if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
+              ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
+              bidx = Bv.tb[t];
+            }
+          }
+          unsigned m = __ballot_sync(FULL_MASK, ra >= 0);
+          while (m) {  // matches in ascending K (the list is sorted)
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int rk = __shfl_sync(FULL_MASK, ra, src);
+            const int64_t bb = __shfl_sync(FULL_MASK, bidx, src);
+            const double *bp = Bv.bval + bb * 64 + lj;
+            const double *ap0 = aval + rk * 64 + i0 * 8, *ap1 = aval + rk * 64 + i1 * 8;
+            double bk[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) bk[k] = bp[k * 8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              x0 = __dadd_rn(x0, __dmul_rn(ap0[k], bk[k]));
+              x1 = __dadd_rn(x1, __dmul_rn(ap1[k], bk[k]));
+            }
+          }
+        }
+        // classify (Algorithm 4.1 floor), counts per (J, row), block to scratch
+        const bool ok0 = i0 < nr, ok1 = i1 < nr;
+        bool st0 = false, st1 = false;
+        if (ok0 && x0 != 0.0) {
+          nz0++;
+          if (fabs(x0) > a.floor_tau) {
+            st0 = true;
+            if (fabs(x0) <= a.eps_g) q10 += x0 * x0;
+            else c10++;
+          } else {
+            fs0 += x0 * x0;
+          }
+        }
+        if (ok1 && x1 != 0.0) {
+          nz1++;
+          if (fabs(x1) > a.floor_tau) {
+            st1 = true;
+            if (fabs(x1) <= a.eps_g) q11 += x1 * x1;
+            else c11++;
+          } else {
+            fs1 += x1 * x1;
+          }
+        }
+        scr[(size_t)q * 64 + i0 * 8 + lj] = st0 ? x0 : 0.0;
+        scr[(size_t)q * 64 + i1 * 8 + lj] = st1 ? x1 : 0.0;
+        const unsigned b0m = __ballot_sync(FULL_MASK, st0), b1m = __ballot_sync(FULL_MASK, st1);
+        if (lj == 0) {
+          jcnt[q * 8 + i0] = (uint16_t)__popc((b0m >> (li * 8)) & 0xFFu);
+          jcnt[q * 8 + i1] = (uint16_t)__popc((b1m >> (li * 8)) & 0xFFu);
+        }
+      }
+    }
+    // per-row sums: lanes with the same row (8 lanes) then warps, in fixed order
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      fs0 += __shfl_xor_sync(FULL_MASK, fs0, o);
+      fs1 += __shfl_xor_sync(FULL_MASK, fs1, o);
+      q10 += __shfl_xor_sync(FULL_MASK, q10, o);
+      q11 += __shfl_xor_sync(FULL_MASK, q11, o);
+      nz0 += __shfl_xor_sync(FULL_MASK, nz0, o);
+      nz1 += __shfl_xor_sync(FULL_MASK, nz1, o);
+      c10 += __shfl_xor_sync(FULL_MASK, c10, o);
+      c11 += __shfl_xor_sync(FULL_MASK, c11, o);
+    }
+    if (lj == 0) {
+      s_fs[warp][i0] = fs0;
+      s_fs[warp][i1] = fs1;
+      s_p1[warp][i0] = q10;
+      s_p1[warp][i1] = q11;
+      s_nz[warp][i0] = nz0;
+      s_nz[warp][i1] = nz1;
+      s_c1[warp][i0] = c10;
+      s_c1[warp][i1] = c11;
+    }
+    __syncthreads();
+    // (4) stage each row's kept entries contiguously (warp i: row i)
+    if (over) {
+      if (tid < nr) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)(r0 + tid);
+    } else if (warp < nr) {
+      const int i = warp;
+      const int64_t r = r0 + i;
+      long long tot = 0;
+      for (int q0 = 0; q0 < nj; q0 += 32) {
+        const int c = q0 + lane < nj ? jcnt[(q0 + lane) * 8 + i] : 0;
+        tot += __reduce_add_sync(FULL_MASK, c);
+      }
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)tot);
+      off = __shfl_sync(FULL_MASK, off, 0);
+      const bool ok = (long long)off + tot <= a.pool_cap;
+      if (ok) {
+        long long pos = (long long)off;
+        for (int q0 = 0; q0 < nj; q0 += 32) {
+          const int q = q0 + lane;
+          const int c = q < nj ? jcnt[q * 8 + i] : 0;
+          int v = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL_MASK, v, o);
+            if (lane >= o) v += y;
+          }
+          if (c > 0) {
+            long long p = pos + v - c;
+            const double *src = scr + (size_t)q * 64 + i * 8;
+            const int J = jlist[q];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              const double x = src[j];
+              if (x != 0.0) {
+                a.pool_col[p] = 8 * J + j;
+                a.pool_val[p] = x;
+                p++;
+              }
+            }
+          }
+          pos += __shfl_sync(FULL_MASK, v, 31);
+        }
+      }
+      if (lane == 0) {
+        double f = 0.0, p1 = 0.0;
+        long long z = 0, c1 = 0;
+        for (int w = 0; w < kBWarps; w++) {
+          f += s_fs[w][i];
+          p1 += s_p1[w][i];
+          z += s_nz[w][i];
+          c1 += s_c1[w][i];
+        }
+        if (!ok) atomicOr(a.flags, 1);
+        a.row_off[r] = (int64_t)off;
+        a.row_cnt[r] = tot;
+        a.row_fsum[r] = f;
+        a.row_nnz[r] = z;
+        if (a.row_p1) {
+          a.row_p1[r] = p1;
+          a.row_c1[r] = c1;
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < nkw; i += kBThreads) kbits[i] = 0u;
+    for (int i = tid; i < njw; i += kBThreads) jbits[i] = 0u;
+  }
+}
+
+void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+                        int32_t *fail_rows, int *fail_count, cudaStream_t st) {
+  if (Bv.nbr == 0) return;
+  const int smem = bsr_numeric_smem_bytes();
+  cudaFuncSetAttribute(k_numeric_bsr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_bsr<<<a.grid, kBThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
 }
 
 // ------------------------------------------------------------------------------------

@@ -154,6 +154,32 @@ constexpr int kRowWarpRows = 8;
 int rowwarp_smem_bytes(int slots);
 void launch_numeric_rowwarp(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
                             cudaStream_t st);
+// BSR-8 view (squarings on one GPU): conversion, block transpose, numeric kernel
+struct BsrView {
+  int64_t nbr = 0;
+  const int64_t *brp = nullptr;
+  const int32_t *bcol = nullptr;
+  const double *bval = nullptr;
+  const int64_t *tp = nullptr;
+  const int32_t *tk = nullptr;
+  const int64_t *tb = nullptr;
+};
+constexpr int kBsrScratchPerCta = 512 * 64;  // doubles of output-block scratch per CTA
+constexpr int kBsrMaxRowBlocks = 160;        // blocks of a block row the numeric kernel holds
+void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st);
+void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
+                     double *bval, int *flags, cudaStream_t st);
+// tk_tmp / tb_tmp: nb-sized scratch; keys_out: nb int32 scratch; sort_tmp: bytes from
+// bsr_transpose_temp_bytes(nb)
+size_t bsr_transpose_temp_bytes(int64_t nb);
+void launch_bsr_transpose(int64_t nbr, int64_t nbc, int64_t nb, const int64_t *brp,
+                          const int32_t *bcol, int32_t *tcnt, int64_t *tp, int32_t *tk_tmp,
+                          int64_t *tb_tmp, int32_t *tk, int64_t *tb, int64_t *scan_tmp,
+                          int64_t *cnt64, void *sort_tmp, size_t sort_tmp_bytes, int32_t *keys_out,
+                          cudaStream_t st);
+int bsr_numeric_smem_bytes();
+void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+                        int32_t *fail_rows, int *fail_count, cudaStream_t st);
 // hash-accumulator variant; rows whose table over-fills are appended to fail_rows
 int hash_smem_bytes();
 void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
