@@ -292,7 +292,7 @@ def main():
 
     # ---------------- roofline of the dominant kernel ----------------
     import math
-    sq_ms = [float(st["sq_numeric_ms"][i]) for i in range(1, N + 1)]
+    sq_ms = [float(st["sq_kernel_ms"][i]) for i in range(1, N + 1)]
     sq_fl = [2.0 * float(st["sq_fmas"][i]) for i in range(1, N + 1)]
     ty_idx = [i for i in range(2, int(st["M"]) + 1) if st["taylor_numeric_ms"][i] > 0]
     ty_ms = [float(st["taylor_numeric_ms"][i]) for i in ty_idx]
@@ -307,13 +307,18 @@ def main():
     if sum(sq_ms) >= sum(ty_ms) and sq_ms:
         dur = sum(sq_ms) / len(sq_ms) / 1e3
         ach = sum(sq_fl) / len(sq_fl) / dur / 1e12
-        tr = traffic_db.get("k_numeric_paged")
-        roof = {"kernel": "k_numeric_paged (squaring SpGEMM + 2T + filter classify)", "bound": "alu",
+        kname = "k_numeric_bsr" if int(st["sq_bsr_blocks"][1]) > 0 else "k_numeric_paged"
+        tr = traffic_db.get(kname)
+        roof = {"kernel": f"{kname} (squaring SpGEMM + 2T + filter classify)", "bound": "alu",
                 "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP64_PEAK_TFLOPS,
                 "traffic": tr["dram_bytes"] if tr and args.config == 5 else None,
                 "traffic_launch": tr["launch"] if tr and args.config == 5 else None,
                 "traffic_compulsory_bytes": float(st["sq_numeric_bytes"][1]),
+                # the block kernel multiplies whole 8x8 blocks (zeros included): executed fp64
+                # work (2 x 512 per block product) per launch, beside the algorithmic count
+                "executed_fp64_tflops": (sum(1024.0 * float(st["sq_block_products"][i]) for i in range(1, N + 1))
+                                         / len(sq_ms) / dur / 1e12),
                 "peak_source": "derived fp64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)",
                 "launches_per_step": len(sq_ms), "avg_launch_ms": dur * 1e3,
                 "hbm_gbs_compulsory": sum(float(st["sq_numeric_bytes"][i]) for i in range(1, N + 1)) / len(sq_ms) / dur / 1e9}
@@ -348,6 +353,7 @@ def main():
         "steps_detail": [{"ms": times[j], "retries": int(stats[j]["retries"]),
                           "taylor_ms": float(stats[j]["ms_taylor"]),
                           "sq_numeric_ms": [float(x) for x in stats[j]["sq_numeric_ms"][1:N + 1]],
+                          "sq_kernel_ms": [float(x) for x in stats[j]["sq_kernel_ms"][1:N + 1]],
                           "sq_first_ms": [float(x) for x in stats[j]["sq_first_ms"][1:N + 1]],
                           "sq_fallback_rows": [int(x) for x in stats[j]["sq_fallback_rows"][1:N + 1]],
                           "cache_misses": int(stats[j]["cache_misses"])}

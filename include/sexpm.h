@@ -146,7 +146,11 @@ typedef struct {
   int32_t retries;                       /* steps re-run after a staging-pool overflow */
   int64_t taylor_fallback_rows[SEXPM_MAXSTEP]; /* rows the term's first kernel handed on */
   int64_t sq_fallback_rows[SEXPM_MAXSTEP];     /* rows the squaring's first kernel handed on */
-  double sq_first_ms[SEXPM_MAXSTEP];           /* device time of the squaring's first kernel */
+  double sq_first_ms[SEXPM_MAXSTEP];           /* device time of the squaring's first stage */
+  double sq_kernel_ms[SEXPM_MAXSTEP];          /* its product kernel alone (block kernel: without
+                                                  building the BSR view) */
+  int64_t sq_bsr_blocks[SEXPM_MAXSTEP];        /* 8x8 blocks of the BSR view (block kernel) */
+  double sq_block_products[SEXPM_MAXSTEP];     /* 8x8 block products it executed (512 each) */
   /* grouped kernel (kernel 8) per squaring: summed SM clocks of its setup / product / flush
    * phases over all groups, groups processed, union k's, groups handed on (all causes, union
    * too large, slots full), then thread-0 clocks of the product loop: ring wait, rest of

@@ -77,7 +77,8 @@ class Stats(C.Structure):
                 ("ms_finalize", C.c_double), ("ms_total", C.c_double),
                 ("taylor_bytes", C.c_double), ("taylor_fmas", C.c_double),
                 ("nnz_out", C.c_int64), ("gpu_launches", C.c_int32), ("retries", C.c_int32),
-                ("taylor_fallback_rows", _I64), ("sq_fallback_rows", _I64), ("sq_first_ms", _F64),
+                ("taylor_fallback_rows", _I64), ("sq_fallback_rows", _I64), ("sq_first_ms", _F64), ("sq_kernel_ms", _F64), ("sq_bsr_blocks", _I64),
+                ("sq_block_products", _F64),
                 ("sq_group_prof", C.c_double * 12 * MAXSTEP),
                 ("cache_hits", C.c_int64), ("cache_misses", C.c_int64),
                 ("cache_releases", C.c_int64), ("cache_bytes_cached", C.c_double),

@@ -368,6 +368,9 @@ struct StepReport {
   double numeric_bytes = 0.0;
   int64_t window_rows = 0;
   float first_ms = 0.f;  // the first kernel of the fallback chain alone
+  float kernel_ms = 0.f;  // the block kernel alone (kernel 11), else 0
+  int64_t bsr_blocks = 0;  // blocks of the BSR-8 view (kernel 11)
+  double block_products = 0.0;  // 8x8 block products executed (kernel 11)
   unsigned long long prof[12] = {0};  // grouped kernel phase clocks
 };
 
@@ -427,7 +430,8 @@ struct sexpm_plan_s {
   cudaEvent_t ev_pattern = nullptr, ev_order = nullptr;
   bool order_pending = false;
   std::string bg_err;
-  std::vector<int32_t> h_order, h_groups;
+  std::vector<int32_t> h_order, h_groups, h_border;
+  DBuf<int32_t> block_order;  // block rows of the block kernel in locality order
   ~sexpm_plan_s() {
     if (bg.joinable()) bg.join();
     if (bg_st) cudaStreamSynchronize(bg_st);
@@ -786,10 +790,28 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           Bv.tp = w.tp.p;
           Bv.tk = w.tk.p;
           Bv.tb = w.tb.p;
+          if (use_cluster && nr == P.row_end - P.row_begin && !getenv("SEXPM_BSR_NATURAL"))
+            Bv.border = P.block_order.p;
           nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, (int64_t)P.sm_count * 2));
           w.bscr.ensure((size_t)nh.grid * kBsrScratchPerCta, st);
           CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
+          w.prof.ensure(16, st);
+          CK(cudaMemsetAsync(w.prof.p, 0, 16 * sizeof(unsigned long long), st));
+          nh.prof = w.prof.p;
+          cudaEvent_t k0, k1;  // the block kernel alone (the stage also builds the view)
+          CK(cudaEventCreate(&k0));
+          CK(cudaEventCreate(&k1));
+          CK(cudaEventRecord(k0, st));
           launch_numeric_bsr(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
+          CK(cudaEventRecord(k1, st));
+          CK(cudaEventSynchronize(k1));
+          CK(cudaEventElapsedTime(&rep.kernel_ms, k0, k1));
+          cudaEventDestroy(k0);
+          cudaEventDestroy(k1);
+          rep.bsr_blocks = nb;
+          unsigned long long nbp = 0;
+          CK(cudaMemcpy(&nbp, w.prof.p, sizeof(nbp), cudaMemcpyDeviceToHost));
+          rep.block_products = (double)nbp;
         } else if (stage == 10) {
           nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged2_blocks_per_sm));
           launch_numeric_paged2(nh, fout, w.fail_count.p, st);
@@ -1457,6 +1479,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     const int64_t nl = P.row_end - P.row_begin;
     P.proc_order.ensure((size_t)std::max<int64_t>(nl, 1), st);
     P.group_start.ensure((size_t)nl + 2, st);
+    P.block_order.ensure((size_t)std::max<int64_t>((nl + 7) / 8, 1), st);
     CK(cudaEventCreateWithFlags(&P.ev_pattern, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&P.ev_order, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&P.bg_st, cudaStreamNonBlocking));
@@ -1486,6 +1509,21 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
         }
         P.ngroups = (int64_t)gs.size();
         gs.push_back((int32_t)ord.size());
+        // block rows (8 rows) of the block kernel, in the order their first row appears
+        std::vector<int32_t> &bo = P.h_border;
+        bo.clear();
+        {
+          std::vector<uint8_t> seenb((ord.size() + 7) / 8 + 1, 0);
+          for (int32_t r : ord) {
+            const int32_t I = r >> 3;
+            if (!seenb[I]) {
+              seenb[I] = 1;
+              bo.push_back(I);
+            }
+          }
+        }
+        if (!bo.empty())
+          CK(cudaMemcpyAsync(P.block_order.p, bo.data(), bo.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         if (!ord.empty())
           CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         CK(cudaMemcpyAsync(P.group_start.p, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
@@ -1651,6 +1689,9 @@ static void do_run(sexpm_plan_s &P) {
       S.sq_numeric_bytes[i] = rep.numeric_bytes;
       S.sq_fallback_rows[i] = rep.window_rows;
       S.sq_first_ms[i] = rep.first_ms;
+      S.sq_kernel_ms[i] = rep.kernel_ms > 0.f ? rep.kernel_ms : rep.first_ms;
+      S.sq_bsr_blocks[i] = rep.bsr_blocks;
+      S.sq_block_products[i] = rep.block_products;
       for (int q = 0; q < 12; q++) S.sq_group_prof[i][q] = (double)rep.prof[q];
       S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)dst.nnz + 16.0 * (double)nl;
     }

@@ -3179,13 +3179,15 @@ void launch_bsr_transpose(int64_t nbr, int64_t nbc, int64_t nb, const int64_t *b
 constexpr int kBThreads = 256;
 constexpr int kBWarps = kBThreads / 32;
 constexpr int kBACap = kBsrMaxRowBlocks;  // blocks of a row of A held in shared memory
+constexpr int kBML = 64;         // matches (K) of one output block listed at a time per warp
+constexpr int kBPF = 4;          // B blocks in flight per warp
 constexpr int kBKWords = 256;    // K bitmap: block-column span of A's row <= 8192
 constexpr int kBJWords = 512;    // J bitmap: output block-column span <= 16384
 constexpr int kBJCap = kBsrScratchPerCta / 64;  // output blocks per block row
 
 int bsr_numeric_smem_bytes() {
-  return kBACap * 64 * 8 + kBACap * 4 + kBKWords * 4 + kBKWords * 2 + kBJWords * 4 +
-         kBJCap * 4 + kBJCap * 8 * 2 + 64;
+  return kBACap * 64 * 8 + kBWarps * kBPF * 64 * 8 + kBWarps * kBML * 8 + kBWarps * kBML * 4 +
+         kBACap * 4 + kBKWords * 4 + kBKWords * 2 + kBJWords * 4 + kBJCap * 4 + kBJCap * 8 * 2 + 64;
 }
 
 // BsrView (kernels.cuh): brp / bcol / bval = block rows, sorted block columns, 64 values
@@ -3197,7 +3199,10 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
                                                               int *fail_count) {
   extern __shared__ double bsm[];
   double *aval = bsm;                                                  // kBACap * 64
-  int32_t *aK = reinterpret_cast<int32_t *>(aval + kBACap * 64);       // kBACap
+  double *wstage = aval + kBACap * 64;                                 // kBWarps * kBPF * 64
+  int64_t *mlb = reinterpret_cast<int64_t *>(wstage + kBWarps * kBPF * 64);  // kBWarps * kBML
+  int32_t *mlk = reinterpret_cast<int32_t *>(mlb + kBWarps * kBML);    // kBWarps * kBML
+  int32_t *aK = mlk + kBWarps * kBML;                                  // kBACap
   unsigned *kbits = reinterpret_cast<unsigned *>(aK + kBACap);         // kBKWords
   uint16_t *kpref = reinterpret_cast<uint16_t *>(kbits + kBKWords);    // kBKWords
   unsigned *jbits = reinterpret_cast<unsigned *>(kpref + kBKWords);    // kBJWords
@@ -3217,8 +3222,8 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
     __syncthreads();
     if (tid == 0) s_I = atomicAdd(a.row_counter, 1);
     __syncthreads();
-    const int64_t I = s_I;
-    if (I >= Bv.nbr) break;
+    if (s_I >= Bv.nbr) break;
+    const int64_t I = Bv.border ? (int64_t)Bv.border[s_I] : (int64_t)s_I;
     const int64_t r0 = 8 * I;
     const int nr = (int)(nrows - r0 < 8 ? nrows - r0 : 8);
     const int64_t ab0 = Bv.brp[I], ab1 = Bv.brp[I + 1];
@@ -3330,6 +3335,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
     // (3) output blocks, one warp each
     double fs0 = 0.0, fs1 = 0.0, q10 = 0.0, q11 = 0.0;
     long long nz0 = 0, nz1 = 0, c10 = 0, c11 = 0;
+    unsigned long long nbp = 0;  // block products of this warp (uniform over its lanes)
     const int i0 = li, i1 = li + 4;
     if (!over) {
       for (int q = warp; q < nj; q += kBWarps) {
@@ -3343,35 +3349,61 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
             x1 = __dmul_rn(a.self_coef, aval[ra * 64 + i1 * 8 + lj]);
           }
         }
+        // matches K of row I of A and column J of B, listed in ascending K (batches of kBML),
+        // then the B blocks streamed kBPF ahead: one 16-byte load per lane per block
+        // (coalesced 512 bytes), staged in this warp's shared buffer for the column reads
+        int64_t *wb = mlb + warp * kBML;
+        int32_t *wk = mlk + warp * kBML;
+        double *stg = wstage + warp * kBPF * 64;
         const int64_t t0 = Bv.tp[J], t1 = Bv.tp[J + 1];
-        for (int64_t tb0 = t0; tb0 < t1; tb0 += 32) {
-          const int64_t t = tb0 + lane;
-          int K = -1;
-          int64_t bidx = 0;
-          int ra = -1;
-          if (t < t1) {
-            K = Bv.tk[t];
-            const int kb = K - kmin;
-            if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
-              ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
-              bidx = Bv.tb[t];
+        int64_t tb0 = t0;
+        while (tb0 < t1) {
+          int nm = 0;
+          for (; tb0 < t1 && nm <= kBML - 32; tb0 += 32) {
+            const int64_t t = tb0 + lane;
+            int ra = -1;
+            int64_t bidx = 0;
+            if (t < t1) {
+              const int K = Bv.tk[t];
+              const int kb = K - kmin;
+              if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
+                ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
+                bidx = Bv.tb[t];
+              }
             }
+            const unsigned m = __ballot_sync(FULL_MASK, ra >= 0);
+            if (ra >= 0) {
+              const int pos = nm + __popc(m & lanemask_lt());
+              wk[pos] = ra;
+              wb[pos] = bidx;
+            }
+            nm += __popc(m);
           }
-          unsigned m = __ballot_sync(FULL_MASK, ra >= 0);
-          while (m) {  // matches in ascending K (the list is sorted)
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const int rk = __shfl_sync(FULL_MASK, ra, src);
-            const int64_t bb = __shfl_sync(FULL_MASK, bidx, src);
-            const double *bp = Bv.bval + bb * 64 + lj;
-            const double *ap0 = aval + rk * 64 + i0 * 8, *ap1 = aval + rk * 64 + i1 * 8;
-            double bk[8];
+          __syncwarp();
+          nbp += nm;
+          double2 pf[kBPF];
 #pragma unroll
-            for (int k = 0; k < 8; k++) bk[k] = bp[k * 8];
+          for (int d = 0; d < kBPF; d++)
+            if (d < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[d] * 64)[lane];
+          for (int t = 0; t < nm; t += kBPF) {
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-              x0 = __dadd_rn(x0, __dmul_rn(ap0[k], bk[k]));
-              x1 = __dadd_rn(x1, __dmul_rn(ap1[k], bk[k]));
+            for (int d = 0; d < kBPF; d++) {
+              const int u = t + d;
+              if (u < nm) {
+                reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
+                __syncwarp();
+                if (u + kBPF < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[u + kBPF] * 64)[lane];
+                const int rk = wk[u];
+                const double *bq = stg + d * 64 + lj;
+                const double *ap0 = aval + rk * 64 + i0 * 8, *ap1 = aval + rk * 64 + i1 * 8;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                  const double b = bq[k * 8];
+                  x0 = __dadd_rn(x0, __dmul_rn(ap0[k], b));
+                  x1 = __dadd_rn(x1, __dmul_rn(ap1[k], b));
+                }
+                __syncwarp();
+              }
             }
           }
         }
@@ -3407,6 +3439,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
         }
       }
     }
+    if (a.prof && lane == 0 && nbp) atomicAdd(&a.prof[0], nbp);
     // per-row sums: lanes with the same row (8 lanes) then warps, in fixed order
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) {

@@ -163,9 +163,10 @@ struct BsrView {
   const int64_t *tp = nullptr;
   const int32_t *tk = nullptr;
   const int64_t *tb = nullptr;
+  const int32_t *border = nullptr;  // block rows in processing order (locality), or identity
 };
 constexpr int kBsrScratchPerCta = 512 * 64;  // doubles of output-block scratch per CTA
-constexpr int kBsrMaxRowBlocks = 160;        // blocks of a block row the numeric kernel holds
+constexpr int kBsrMaxRowBlocks = 136;        // blocks of a block row the numeric kernel holds
 void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st);
 void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
                      double *bval, int *flags, cudaStream_t st);
