@@ -378,7 +378,7 @@ struct Workspace {
   DBuf<int32_t> lo, hi, order, bin_cnt, bin_off;
   DBuf<int64_t> prod, bound, row_off, row_cnt, row_nnz, cnt, scan_tmp, l1r, l2r, i64tmp;
   DBuf<double> row_fsum, rs, partial, scal, passrow, row_p1;
-  DBuf<int64_t> row_c1;
+  DBuf<int64_t> row_c1, cnt2;
   DBuf<int64_t> cursor;
   DBuf<int32_t> scr_col, pool_col;
   DBuf<double> scr_val, pool_val;
@@ -542,7 +542,8 @@ static void wait_order(sexpm_plan_s &P) {
 
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
                             double div, double eps_g, DCsr &C, StepReport &rep,
-                            const DCsr *BT = nullptr, bool add_identity = false) {
+                            const DCsr *BT = nullptr, bool add_identity = false,
+                            const CsrView *acc = nullptr, DCsr *acc_out = nullptr) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   const int64_t nr = A.nrows;
@@ -959,6 +960,32 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   out.row0 = A.row0;
   out.rp.ensure((size_t)nr + 1, st);
   launch_exclusive_scan(w.cnt.p, nr, out.rp.p, w.scan_tmp.p, st);
+  if (acc != nullptr) {
+    // Taylor term: S^_i and T^_0 + S^_i straight from the staged S~_i (one read of the
+    // staging pool instead of compaction + a second read of S^_i by the merge)
+    DCsr &T2 = *acc_out;  // must not alias acc, A or B
+    w.cnt2.ensure(nr1, st);
+    launch_merge_staged_count(*acc, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
+                              w.cnt2.p, st);
+    T2.nrows = nr;
+    T2.row0 = A.row0;
+    T2.rp.ensure((size_t)nr + 1, st);
+    launch_exclusive_scan(w.cnt2.p, nr, T2.rp.p, w.scan_tmp.p, st);
+    int64_t tot[2];
+    CK(cudaMemcpyAsync(&tot[0], out.rp.p + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&tot[1], T2.rp.p + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    out.nnz = tot[0];
+    T2.nnz = tot[1];
+    out.col.ensure((size_t)out.nnz, st);
+    out.val.ensure((size_t)out.nnz, st);
+    T2.col.ensure((size_t)T2.nnz, st);
+    T2.val.ensure((size_t)T2.nnz, st);
+    launch_merge_staged_write(*acc, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
+                              T2.rp.p, T2.col.p, T2.val.p, out.rp.p, out.col.p, out.val.p, st);
+    rep.nnz = (int64_t)allsum(P, (double)out.nnz);
+    return;
+  }
   out.nnz = d2h(out.rp.p + nr, st);
   out.col.ensure((size_t)out.nnz, st);
   out.val.ensure((size_t)out.nnz, st);
@@ -1603,7 +1630,9 @@ static void do_run(sexpm_plan_s &P) {
     for (int i = 2; i <= P.M; i++) {
       CK(cudaEventRecord(a0, st));
       StepReport rep;
-      filtered_product(P, Sc.view(), P.H0full.view(), 0.0, (double)i, P.eps_g0, Sn, rep, &P.H0T);
+      const CsrView Tv = T.view();
+      filtered_product(P, Sc.view(), P.H0full.view(), 0.0, (double)i, P.eps_g0, Sn, rep, &P.H0T,
+                       false, &Tv, &Tn);  // S^_i and T^_0^(i) = T^_0^(i-1) + S^_i
       if (i < SEXPM_MAXSTEP) {
         S.taylor_nnz_unf[i] = rep.nnz_unf;
         S.taylor_nnz[i] = rep.nnz;
@@ -1621,8 +1650,7 @@ static void do_run(sexpm_plan_s &P) {
         break;
       }
       M_eff = i;
-      merge_add(P, T.view(), Sn.view(), Tn);  // T^_0^(i) = T^_0^(i-1) + S^_i
-      S.taylor_bytes += 12.0 * ((double)T.nnz + (double)Sn.nnz + (double)Tn.nnz);
+      S.taylor_bytes += 12.0 * ((double)T.nnz + (double)Tn.nnz);
       swap_csr(T, Tn);
       swap_csr(Sc, Sn);
       if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();

@@ -4301,6 +4301,94 @@ __global__ void k_merge(CsrView A, CsrView B, const int64_t *rp_out, int64_t *cn
   }
   if (!WRITE && lane == 0) cnt[w] = out;
 }
+// T^_0 + S^_i fused with the compaction of S~_i (Taylor terms, P:416 with P:380): B is
+// the staged S~_i (row r at pool[row_off[r] .. + row_cnt[r]), column order) under the
+// final Algorithm 4.1 threshold tau -- an entry with |x| <= tau is dropped, i.e. merges as
+// a 0, which the merge already treats like an absent entry (a + 0 = a, 0-valued entries
+// are not emitted).  The write pass also writes S^_i itself (the kept entries) at s_rp.
+template <bool WRITE>
+__global__ void k_merge_staged(CsrView A, const int64_t *row_off, const int64_t *row_cnt,
+                               const int32_t *pcol, const double *pval, double tau,
+                               const int64_t *rp_out, int64_t *cnt, int32_t *col_out,
+                               double *val_out, const int64_t *s_rp, int32_t *s_col,
+                               double *s_val) {
+  __shared__ int32_t sA[kWarps][32], sB[kWarps][32];
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  if (w >= A.nrows) return;
+  int64_t a0 = A.rp[w], na = A.rp[w + 1] - a0;
+  int64_t b0 = row_off[w], nb = row_cnt[w];
+  int64_t i = 0, j = 0, out = WRITE ? rp_out[w] : 0, sout = WRITE ? s_rp[w] : 0;
+  while (i < na || j < nb) {
+    bool ina = i + lane < na, inb = j + lane < nb;
+    int32_t ca = ina ? A.col[a0 + i + lane] : INT32_MAX;
+    int32_t cb = inb ? pcol[b0 + j + lane] : INT32_MAX;
+    double va = ina ? A.val[a0 + i + lane] : 0.0;
+    double vb = inb ? pval[b0 + j + lane] : 0.0;
+    if (!(fabs(vb) > tau)) vb = 0.0;  // dropped by Algorithm 4.1
+    int32_t limA = (na - i > 32) ? __shfl_sync(FULL_MASK, ca, 31) : INT32_MAX;
+    int32_t limB = (nb - j > 32) ? __shfl_sync(FULL_MASK, cb, 31) : INT32_MAX;
+    int32_t lim = limA < limB ? limA : limB;
+    bool oka = ina && ca <= lim, okb = inb && cb <= lim;
+    sA[wi][lane] = ca;
+    sB[wi][lane] = cb;
+    __syncwarp();
+    int posB = lower_bound32(sB[wi], ca);
+    int posA = lower_bound32(sA[wi], cb);
+    bool dupA = oka && posB < 32 && sB[wi][posB] == ca;
+    bool dupB = okb && posA < 32 && sA[wi][posA] == cb;
+    double vbm = __shfl_sync(FULL_MASK, vb, posB & 31);
+    double sum = dupA ? va + vbm : va;
+    bool keepA = oka && sum != 0.0;
+    bool uB = okb && !dupB && vb != 0.0;
+    unsigned bKA = __ballot_sync(FULL_MASK, keepA);
+    unsigned bUB = __ballot_sync(FULL_MASK, uB);
+    if (WRITE) {
+      unsigned mB = posB >= 32 ? FULL_MASK : ((1u << posB) - 1u);
+      unsigned mA = posA >= 32 ? FULL_MASK : ((1u << posA) - 1u);
+      if (keepA) {
+        int64_t q = out + __popc(bKA & lanemask_lt()) + __popc(bUB & mB);
+        col_out[q] = ca;
+        val_out[q] = sum;
+      }
+      if (uB) {
+        int64_t q = out + __popc(bKA & mA) + __popc(bUB & lanemask_lt());
+        col_out[q] = cb;
+        val_out[q] = vb;
+      }
+      const bool ks = okb && vb != 0.0;  // kept entry of S^_i
+      const unsigned bS = __ballot_sync(FULL_MASK, ks);
+      if (ks) {
+        const int64_t q = sout + __popc(bS & lanemask_lt());
+        s_col[q] = cb;
+        s_val[q] = vb;
+      }
+      sout += __popc(bS);
+    }
+    out += __popc(bKA) + __popc(bUB);
+    i += __popc(__ballot_sync(FULL_MASK, oka));
+    j += __popc(__ballot_sync(FULL_MASK, okb));
+    __syncwarp();
+  }
+  if (!WRITE && lane == 0) cnt[w] = out;
+}
+void launch_merge_staged_count(const CsrView &A, const int64_t *row_off, const int64_t *row_cnt,
+                               const int32_t *pcol, const double *pval, double tau, int64_t *cnt,
+                               cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_merge_staged<false><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(
+      A, row_off, row_cnt, pcol, pval, tau, nullptr, cnt, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+void launch_merge_staged_write(const CsrView &A, const int64_t *row_off, const int64_t *row_cnt,
+                               const int32_t *pcol, const double *pval, double tau,
+                               const int64_t *rp_out, int32_t *col_out, double *val_out,
+                               const int64_t *s_rp, int32_t *s_col, double *s_val, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_merge_staged<true><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(
+      A, row_off, row_cnt, pcol, pval, tau, rp_out, nullptr, col_out, val_out, s_rp, s_col, s_val);
+}
 void launch_merge_count(const CsrView &A, const CsrView &B, int64_t *cnt, cudaStream_t st) {
   if (A.nrows == 0) return;
   KL;
