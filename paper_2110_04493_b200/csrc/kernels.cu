@@ -3194,6 +3194,18 @@ int bsr_numeric_smem_bytes() {
 // per block row-major; tp / tk / tb = block transpose: column J's block rows K (ascending)
 // and block indices.
 
+// x0 += sum_k a[i0][k] b[k][lj], x1 likewise for row i1: k ascending, _rn products and sums
+__device__ __forceinline__ void bsr_block_fma(const double *bs, const double *as, int i0, int i1,
+                                              int lj, double &x0, double &x1) {
+  const double *bq = bs + lj, *ap0 = as + i0 * 8, *ap1 = as + i1 * 8;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const double b = bq[k * 8];
+    x0 = __dadd_rn(x0, __dmul_rn(ap0[k], b));
+    x1 = __dadd_rn(x1, __dmul_rn(ap1[k], b));
+  }
+}
+
 __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, BsrView Bv, int64_t nrows,
                                                               double *scratch, int32_t *fail_rows,
                                                               int *fail_count) {
@@ -3385,26 +3397,30 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
 #pragma unroll
           for (int d = 0; d < kBPF; d++)
             if (d < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[d] * 64)[lane];
-          for (int t = 0; t < nm; t += kBPF) {
+          int t = 0;
+          // full batches of kBPF blocks: stage all, one warp barrier, then the kBPF block
+          // products back to back (no control flow between them, so the shared loads of the
+          // next product issue while the previous one's sums run)
+          for (; t + kBPF <= nm; t += kBPF) {
 #pragma unroll
-            for (int d = 0; d < kBPF; d++) {
-              const int u = t + d;
-              if (u < nm) {
-                reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
-                __syncwarp();
-                if (u + kBPF < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[u + kBPF] * 64)[lane];
-                const int rk = wk[u];
-                const double *bq = stg + d * 64 + lj;
-                const double *ap0 = aval + rk * 64 + i0 * 8, *ap1 = aval + rk * 64 + i1 * 8;
+            for (int d = 0; d < kBPF; d++) reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
+            __syncwarp();
 #pragma unroll
-                for (int k = 0; k < 8; k++) {
-                  const double b = bq[k * 8];
-                  x0 = __dadd_rn(x0, __dmul_rn(ap0[k], b));
-                  x1 = __dadd_rn(x1, __dmul_rn(ap1[k], b));
-                }
-                __syncwarp();
-              }
-            }
+            for (int d = 0; d < kBPF; d++)
+              if (t + kBPF + d < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[t + kBPF + d] * 64)[lane];
+#pragma unroll
+            for (int d = 0; d < kBPF; d++) bsr_block_fma(stg + d * 64, aval + wk[t + d] * 64, i0, i1, lj, x0, x1);
+            __syncwarp();
+          }
+          if (t < nm) {  // tail batch (< kBPF blocks)
+#pragma unroll
+            for (int d = 0; d < kBPF; d++)
+              if (t + d < nm) reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
+            __syncwarp();
+#pragma unroll
+            for (int d = 0; d < kBPF; d++)
+              if (t + d < nm) bsr_block_fma(stg + d * 64, aval + wk[t + d] * 64, i0, i1, lj, x0, x1);
+            __syncwarp();
           }
         }
         // classify (Algorithm 4.1 floor), counts per (J, row), block to scratch
