@@ -415,7 +415,9 @@ struct sexpm_plan_s {
   DBuf<int32_t> dia_off;
   DBuf<double> dia_val;
   DBuf<unsigned long long> dia_prod;
-  int dia_slots = 1152;
+  int dia_slots = 512;       // K5d accumulator slots per warp: adapted from the previous term's need
+  int dia_slots_max = 1152;  // the most that fit (set at plan time); retry size for rows over dia_slots
+  DBuf<int> dia_need;
   int group_slots = 4096;
   int rowwarp_slots = 3072;
   long long cache0[3] = {0, 0, 0};  // cache counters when the plan was created
@@ -644,7 +646,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.hash_blocks_per_sm));
   const int paged_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged_blocks_per_sm));
+  int nfail_other = 0;  // rows finished by kernels other than the first (and its K5d retry)
+  bool dia_launched = false;
   for (int attempt = 0;; attempt++) {
+    nfail_other = 0;
     w.pool_col.ensure((size_t)cap, st);
     w.pool_val.ensure((size_t)cap, st);
     na.pool_col = w.pool_col.p;
@@ -703,7 +708,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       int32_t *fbuf[2] = {w.fail_rows.p, w.fail_rows2.p};
       int fb = 0;
       int stage = kern;
-      bool first = true;
+      bool first = true, dia_retry = false;
       // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
       fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10 || kern == 11);
       while (nlist > 0) {
@@ -715,7 +720,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         NumericArgs nh = na;
         nh.order = list;
         nh.nlist = nlist;
-        if (first && fused_p1) {
+        if ((first || stage == 7) && fused_p1) {
           nh.row_p1 = w.row_p1.p;
           nh.row_c1 = w.row_c1.p;
           nh.eps_g = eps_g;
@@ -845,10 +850,16 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           D.dmin = P.dia_dmin;
           D.dmax = P.dia_dmax;
           D.prod_count = P.dia_prod.p;
-          const int per_sm = std::max(1, std::min(16, (int)(P.smem_per_sm / (taylor_dia_smem_bytes(P.dia_slots) + 1024))));
+          // slots sized from the previous term's largest row (occupancy: 20 -> 28+ warps/SM
+          // at config 5); rows over it are retried once at twice the slots
+          const int slots = std::min(dia_retry ? 2 * P.dia_slots : P.dia_slots, P.dia_slots_max);
+          if (!dia_retry) CK(cudaMemsetAsync(P.dia_need.p, 0, sizeof(int), st));
+          D.need_max = P.dia_need.p;
+          const int per_sm = std::max(1, std::min(16, (int)(P.smem_per_sm / (taylor_dia_smem_bytes(slots) + 1024))));
           nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kDiaWarpsPerCta - 1) / kDiaWarpsPerCta,
                                                                 (int64_t)P.sm_count * per_sm));
-          launch_taylor_dia(nh, D, P.dia_slots, fout, w.fail_count.p, st);
+          launch_taylor_dia(nh, D, slots, fout, w.fail_count.p, st);
+          dia_launched = true;
         } else {  // 6
           nh.grid = paged_grid;
           launch_taylor_pull(nh, BT->view(), fout, w.fail_count.p, st);
@@ -864,13 +875,19 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         list = fout;
         nlist = nf;
         fb ^= 1;
-        // fall-through: K5d rows too wide for its slots -> paged; K5p -> hash; the squaring
-        // kernels -> paged; everything else -> the block-window kernel (no capacity limit)
-        stage = stage == 7 ? 5 : (stage == 6 ? 1 : ((stage >= 8 && stage <= 11) ? 5 : 3));
+        // fall-through: K5d rows over its slots -> K5d at twice the slots -> paged; K5p ->
+        // hash; the squaring kernels -> paged; everything else -> the block-window kernel (no
+        // capacity limit)
+        if (stage == 7 && !dia_retry && P.dia_slots < P.dia_slots_max) {
+          dia_retry = true;
+        } else {
+          stage = stage == 7 ? 5 : (stage == 6 ? 1 : ((stage >= 8 && stage <= 11) ? 5 : 3));
+          nfail_other += nf;
+        }
       }
     }
     rep.window_rows = nfail;
-    if (nfail > 0) fused_p1 = false;  // rows handled by kernels without the fused pass
+    if (nfail_other > 0) fused_p1 = false;  // rows handled by kernels without the fused pass
     CK(cudaEventRecord(e1, st));
     int flags = 0;
     CK(cudaMemcpyAsync(&flags, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -886,7 +903,12 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   rep.first_ms = rep.numeric_ms;
   if (have_first) CK(cudaEventElapsedTime(&rep.first_ms, e0, e_first));
   cudaEventDestroy(e_first);
-  if (dia_path && !have_symbolic && rep.window_rows == 0) rep.fmas = (double)d2h(P.dia_prod.p, st);
+  if (dia_path && !have_symbolic && nfail_other == 0) rep.fmas = (double)d2h(P.dia_prod.p, st);
+  if (dia_launched) {  // next term's K5d slots: this term's largest row + 12.5 % + 64, 64-aligned
+    const long long nd = d2h(P.dia_need.p, st);
+    P.dia_slots = (int)std::min<long long>(P.dia_slots_max, std::max<long long>(256, ((nd * 9 / 8 + 64 + 63) / 64) * 64));
+    if (getenv("SEXPM_STEP_LOG")) fprintf(stderr, "[sexpm run] K5d need %lld slots, next %d (max %d), retried rows %d\n", nd, P.dia_slots, P.dia_slots_max, (int)(rep.window_rows - nfail_other));
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   w.pool_cap_hint = std::max<int64_t>(w.pool_cap_hint, (int64_t)(1.2 * (double)used));
@@ -1351,6 +1373,14 @@ static void build_diagonals(sexpm_plan_s &P) {
   CK(cudaMemsetAsync(P.dia_val.p, 0, (size_t)P.dia_nd * P.n * sizeof(double), st));
   launch_fill_dia(Hf.view(), offs.data(), P.dia_nd, P.dia_val.p, P.n, st);
   P.dia_prod.alloc(1, st);
+  P.dia_need.alloc(1, st);
+  {  // largest K5d slot count whose 4-warp CTA fits the opt-in shared memory of a block
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.dev));
+    int sl = 8192;
+    while (sl > 256 && taylor_dia_smem_bytes(sl) > optin) sl -= 64;
+    P.dia_slots_max = sl;
+  }
   CK(cudaStreamSynchronize(st));  // offs (host) is captured by value in the launch
 }
 

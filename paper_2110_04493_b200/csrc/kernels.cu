@@ -3652,6 +3652,7 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
   const int32_t dmin = D.dmin, dmax = D.dmax;
   const int64_t n = D.n;
   unsigned long long prods = 0;
+  int need = 0;              // most slots a row of this warp needed
   constexpr int kBatch = 4;  // rows taken per scheduler atomic
   for (;;) {
     int idx0 = 0;
@@ -3718,6 +3719,7 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
           if (lane >= o) v += y;
         }
         npages = __shfl_sync(FULL_MASK, v, 31);
+        need = max(need, npages << sh);
         if ((npages << sh) > slots) {
           fail = true;
         } else {
@@ -3847,6 +3849,7 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
   }
   prods = warp_sum(prods);
   if (lane == 0 && prods) atomicAdd(D.prod_count, prods);
+  if (lane == 0 && D.need_max && need > 0) atomicMax(D.need_max, need);
 }
 
 void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_t *fail_rows,

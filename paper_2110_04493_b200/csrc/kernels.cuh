@@ -131,6 +131,7 @@ struct DiaView {
   int64_t n = 0;
   int32_t dmin = 0, dmax = 0;
   unsigned long long *prod_count = nullptr;  // += products (a_rk h_kj pairs) computed
+  int *need_max = nullptr;  // max over rows of the accumulator slots a row needed (span-fit rows)
 };
 constexpr int kDiaMax = 16;       // most offsets the diagonal kernel handles
 constexpr int kDiaWarpsPerCta = 4;
