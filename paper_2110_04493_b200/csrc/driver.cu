@@ -331,6 +331,10 @@ struct DCsr {
   DBuf<int64_t> rp;
   DBuf<int32_t> col;
   DBuf<double> val;
+  // padded form (the Taylor accumulator T^_0): row r holds len[r] entries from rp[r], rp[r+1]
+  // is a capacity bound; nnz is the capacity
+  bool padded = false;
+  DBuf<int64_t> len;
   CsrView view() const {
     CsrView v;
     v.nrows = nrows;
@@ -545,7 +549,7 @@ static void wait_order(sexpm_plan_s &P) {
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
                             double div, double eps_g, DCsr &C, StepReport &rep,
                             const DCsr *BT = nullptr, bool add_identity = false,
-                            const CsrView *acc = nullptr, DCsr *acc_out = nullptr) {
+                            const DCsr *acc = nullptr, DCsr *acc_out = nullptr) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   const int64_t nr = A.nrows;
@@ -980,15 +984,19 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   DCsr &out = C;  // must not alias A or B
   out.nrows = nr;
   out.row0 = A.row0;
+  out.padded = false;
   out.rp.ensure((size_t)nr + 1, st);
   launch_exclusive_scan(w.cnt.p, nr, out.rp.p, w.scan_tmp.p, st);
   if (acc != nullptr) {
     // Taylor term: S^_i and T^_0 + S^_i straight from the staged S~_i (one read of the
-    // staging pool instead of compaction + a second read of S^_i by the merge)
+    // staging pool instead of compaction + a second read of S^_i by the merge).  T^_0 + S^_i
+    // is written in padded form (row capacity len(T^_0 row) + nnz(S^_i row)), so no count
+    // pass over T^_0 is needed; do_run compacts T^_0 once after the last term.
     DCsr &T2 = *acc_out;  // must not alias acc, A or B
+    const CsrView av = acc->view();
+    const int64_t *alen = acc->padded ? acc->len.p : nullptr;
     w.cnt2.ensure(nr1, st);
-    launch_merge_staged_count(*acc, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
-                              w.cnt2.p, st);
+    launch_add_rowlen(av.rp, alen, w.cnt.p, nr, w.cnt2.p, st);
     T2.nrows = nr;
     T2.row0 = A.row0;
     T2.rp.ensure((size_t)nr + 1, st);
@@ -1003,8 +1011,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     out.val.ensure((size_t)out.nnz, st);
     T2.col.ensure((size_t)T2.nnz, st);
     T2.val.ensure((size_t)T2.nnz, st);
-    launch_merge_staged_write(*acc, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
-                              T2.rp.p, T2.col.p, T2.val.p, out.rp.p, out.col.p, out.val.p, st);
+    T2.len.ensure(nr1, st);
+    T2.padded = true;
+    launch_merge_staged_write(av, alen, w.row_off.p, w.row_cnt.p, w.pool_col.p, w.pool_val.p, tau,
+                              T2.rp.p, T2.col.p, T2.val.p, T2.len.p, out.rp.p, out.col.p, out.val.p, st);
     rep.nnz = (int64_t)allsum(P, (double)out.nnz);
     return;
   }
@@ -1041,6 +1051,7 @@ static void merge_add(sexpm_plan_s &P, const CsrView &A, const CsrView &B, DCsr 
   DCsr &out = C;  // must not alias A or B
   out.nrows = nr;
   out.row0 = A.row0;
+  out.padded = false;
   out.rp.ensure((size_t)nr + 1, st);
   launch_exclusive_scan(w.cnt.p, nr, out.rp.p, w.scan_tmp.p, st);
   out.nnz = d2h(out.rp.p + nr, st);
@@ -1051,6 +1062,7 @@ static void merge_add(sexpm_plan_s &P, const CsrView &A, const CsrView &B, DCsr 
 
 static void copy_csr(sexpm_plan_s &P, const CsrView &A, DCsr &C) {
   cudaStream_t st = P.st;
+  C.padded = false;
   C.nrows = A.nrows;
   C.row0 = A.row0;
   C.nnz = A.nnz;
@@ -1649,6 +1661,7 @@ static void do_run(sexpm_plan_s &P) {
     T.nrows = nl;
     T.row0 = P.row_begin;
     T.nnz = 0;
+    T.padded = false;
     T.rp.ensure((size_t)nl + 1, st);
     CK(cudaMemsetAsync(T.rp.p, 0, (nl + 1) * sizeof(int64_t), st));
     T.col.ensure(1, st);
@@ -1660,9 +1673,8 @@ static void do_run(sexpm_plan_s &P) {
     for (int i = 2; i <= P.M; i++) {
       CK(cudaEventRecord(a0, st));
       StepReport rep;
-      const CsrView Tv = T.view();
       filtered_product(P, Sc.view(), P.H0full.view(), 0.0, (double)i, P.eps_g0, Sn, rep, &P.H0T,
-                       false, &Tv, &Tn);  // S^_i and T^_0^(i) = T^_0^(i-1) + S^_i
+                       false, &T, &Tn);  // S^_i and T^_0^(i) = T^_0^(i-1) + S^_i
       if (i < SEXPM_MAXSTEP) {
         S.taylor_nnz_unf[i] = rep.nnz_unf;
         S.taylor_nnz[i] = rep.nnz;
@@ -1691,6 +1703,27 @@ static void do_run(sexpm_plan_s &P) {
   }
   P.M_eff = M_eff;
   S.M_eff = M_eff;
+  if (T.padded) {  // T^_0 to plain CSR (one pass; the merges wrote it with row capacities)
+    Workspace &w = P.ws;
+    const size_t nl1 = (size_t)std::max<int64_t>(nl, 1);
+    w.cnt.ensure(nl1, st);
+    w.scan_tmp.ensure((size_t)scan_tmp_elems(nl) + 1, st);
+    w.rs.ensure(nl1, st);
+    w.l1r.ensure(nl1, st);
+    w.l2r.ensure(nl1, st);
+    Tn.nrows = nl;
+    Tn.row0 = T.row0;
+    Tn.rp.ensure((size_t)nl + 1, st);
+    launch_exclusive_scan(T.len.p, nl, Tn.rp.p, w.scan_tmp.p, st);
+    Tn.nnz = d2h(Tn.rp.p + nl, st);
+    Tn.col.ensure((size_t)std::max<int64_t>(Tn.nnz, 1), st);
+    Tn.val.ensure((size_t)std::max<int64_t>(Tn.nnz, 1), st);
+    Tn.padded = false;
+    // tau = 0 keeps every entry (the merges never write zeros)
+    launch_compact_write(nl, T.row0, T.rp.p, T.len.p, T.col.p, T.val.p, 0.0, Tn.rp.p, Tn.col.p,
+                         Tn.val.p, w.rs.p, w.l1r.p, w.l2r.p, st);
+    swap_csr(T, Tn);
+  }
   CK(cudaEventRecord(ev_taylor, st));
   // stats of T^_0
   {

@@ -4326,16 +4326,16 @@ __global__ void k_merge(CsrView A, CsrView B, const int64_t *rp_out, int64_t *cn
 // a 0, which the merge already treats like an absent entry (a + 0 = a, 0-valued entries
 // are not emitted).  The write pass also writes S^_i itself (the kept entries) at s_rp.
 template <bool WRITE>
-__global__ void k_merge_staged(CsrView A, const int64_t *row_off, const int64_t *row_cnt,
-                               const int32_t *pcol, const double *pval, double tau,
-                               const int64_t *rp_out, int64_t *cnt, int32_t *col_out,
-                               double *val_out, const int64_t *s_rp, int32_t *s_col,
-                               double *s_val) {
+__global__ void k_merge_staged(CsrView A, const int64_t *alen, const int64_t *row_off,
+                               const int64_t *row_cnt, const int32_t *pcol, const double *pval,
+                               double tau, const int64_t *rp_out, int64_t *cnt, int32_t *col_out,
+                               double *val_out, int64_t *len_out, const int64_t *s_rp,
+                               int32_t *s_col, double *s_val) {
   __shared__ int32_t sA[kWarps][32], sB[kWarps][32];
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   if (w >= A.nrows) return;
-  int64_t a0 = A.rp[w], na = A.rp[w + 1] - a0;
+  int64_t a0 = A.rp[w], na = alen ? alen[w] : A.rp[w + 1] - a0;
   int64_t b0 = row_off[w], nb = row_cnt[w];
   int64_t i = 0, j = 0, out = WRITE ? rp_out[w] : 0, sout = WRITE ? s_rp[w] : 0;
   while (i < na || j < nb) {
@@ -4390,23 +4390,39 @@ __global__ void k_merge_staged(CsrView A, const int64_t *row_off, const int64_t 
     __syncwarp();
   }
   if (!WRITE && lane == 0) cnt[w] = out;
+  if (WRITE && lane == 0 && len_out) len_out[w] = out - rp_out[w];
 }
-void launch_merge_staged_count(const CsrView &A, const int64_t *row_off, const int64_t *row_cnt,
-                               const int32_t *pcol, const double *pval, double tau, int64_t *cnt,
-                               cudaStream_t st) {
+void launch_merge_staged_count(const CsrView &A, const int64_t *alen, const int64_t *row_off,
+                               const int64_t *row_cnt, const int32_t *pcol, const double *pval,
+                               double tau, int64_t *cnt, cudaStream_t st) {
   if (A.nrows == 0) return;
   KL;
   k_merge_staged<false><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(
-      A, row_off, row_cnt, pcol, pval, tau, nullptr, cnt, nullptr, nullptr, nullptr, nullptr, nullptr);
+      A, alen, row_off, row_cnt, pcol, pval, tau, nullptr, cnt, nullptr, nullptr, nullptr, nullptr,
+      nullptr, nullptr);
 }
-void launch_merge_staged_write(const CsrView &A, const int64_t *row_off, const int64_t *row_cnt,
-                               const int32_t *pcol, const double *pval, double tau,
-                               const int64_t *rp_out, int32_t *col_out, double *val_out,
-                               const int64_t *s_rp, int32_t *s_col, double *s_val, cudaStream_t st) {
+void launch_merge_staged_write(const CsrView &A, const int64_t *alen, const int64_t *row_off,
+                               const int64_t *row_cnt, const int32_t *pcol, const double *pval,
+                               double tau, const int64_t *rp_out, int32_t *col_out, double *val_out,
+                               int64_t *len_out, const int64_t *s_rp, int32_t *s_col, double *s_val,
+                               cudaStream_t st) {
   if (A.nrows == 0) return;
   KL;
   k_merge_staged<true><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(
-      A, row_off, row_cnt, pcol, pval, tau, rp_out, nullptr, col_out, val_out, s_rp, s_col, s_val);
+      A, alen, row_off, row_cnt, pcol, pval, tau, rp_out, nullptr, col_out, val_out, len_out, s_rp,
+      s_col, s_val);
+}
+// out[r] = (alen ? alen[r] : rp[r+1] - rp[r]) + b[r]: row capacities of T^_0 + S^_i
+__global__ void k_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
+                             int64_t *out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = (alen ? alen[r] : rp[r + 1] - rp[r]) + b[r];
+}
+void launch_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
+                       int64_t *out, cudaStream_t st) {
+  if (n == 0) return;
+  KL;
+  k_add_rowlen<<<grid_for(n, kThreads, 148 * 16), kThreads, 0, st>>>(rp, alen, b, n, out);
 }
 void launch_merge_count(const CsrView &A, const CsrView &B, int64_t *cnt, cudaStream_t st) {
   if (A.nrows == 0) return;

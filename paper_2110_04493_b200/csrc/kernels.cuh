@@ -224,14 +224,19 @@ void launch_row_stats(const CsrView &C, double *rs, int64_t *l1r, int64_t *l2r,
 void launch_merge_count(const CsrView &A, const CsrView &B, int64_t *cnt, cudaStream_t st);
 void launch_merge_write(const CsrView &A, const CsrView &B, const int64_t *rp_out,
                         int32_t *col_out, double *val_out, cudaStream_t st);
-// C = A + (staged S~ under tau), writing S^ (the kept staged entries) as well (Taylor terms)
-void launch_merge_staged_count(const CsrView &A, const int64_t *row_off, const int64_t *row_cnt,
-                               const int32_t *pcol, const double *pval, double tau, int64_t *cnt,
+// C = A + (staged S~ under tau), writing S^ (the kept staged entries) as well (Taylor terms).
+// A's row r is A.col/val[A.rp[r] .. + alen[r]) (alen null: A.rp[r+1] - A.rp[r]); C's row r is
+// written from rp_out[r] (a capacity offset) and its length stored in len_out[r]
+void launch_merge_staged_count(const CsrView &A, const int64_t *alen, const int64_t *row_off,
+                               const int64_t *row_cnt, const int32_t *pcol, const double *pval,
+                               double tau, int64_t *cnt, cudaStream_t st);
+void launch_merge_staged_write(const CsrView &A, const int64_t *alen, const int64_t *row_off,
+                               const int64_t *row_cnt, const int32_t *pcol, const double *pval,
+                               double tau, const int64_t *rp_out, int32_t *col_out, double *val_out,
+                               int64_t *len_out, const int64_t *s_rp, int32_t *s_col, double *s_val,
                                cudaStream_t st);
-void launch_merge_staged_write(const CsrView &A, const int64_t *row_off, const int64_t *row_cnt,
-                               const int32_t *pcol, const double *pval, double tau,
-                               const int64_t *rp_out, int32_t *col_out, double *val_out,
-                               const int64_t *s_rp, int32_t *s_col, double *s_val, cudaStream_t st);
+void launch_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
+                       int64_t *out, cudaStream_t st);
 // identity rows for rows [row0, row0+nrows)
 void launch_identity(int64_t nrows, int64_t row0, int64_t *rp, int32_t *col, double *val,
                      cudaStream_t st);
