@@ -101,10 +101,12 @@ typedef struct {
                              CTA share each B-row gather, TMA-staged), 9 one warp per row (8
                              rows per CTA share a page table), 10 k-sync paged with 128
                              threads per row, 11 block-sparse (BSR-8 view, register-held
-                             8x8 output blocks; squarings on one GPU, else as 5).  All meet
-                             parity; 2 and 4-11 reproduce the oracle's C~ bit for bit.  Rows
-                             a kernel cannot hold fall through 8-11 -> 5 -> 3,
-                             7 -> 5 -> 3, 6 -> 1 -> 3 and 1/4/5 -> 3. */
+                             8x8 output blocks; squarings on one GPU, else as 5), 12 as 11
+                             over pairs of block rows sharing each B block (squarings on
+                             one GPU, else as 5).  All meet parity; 2 and 4-12 reproduce the
+                             oracle's C~ bit for bit.  Rows a kernel cannot hold fall
+                             through 8-12 -> 5 -> 3, 7 -> 7 at twice the accumulator slots
+                             -> 5 -> 3, 6 -> 1 -> 3 and 1/4/5 -> 3. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */

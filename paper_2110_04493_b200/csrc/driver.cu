@@ -681,8 +681,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     if (kern == 8 && !group_ok) kern = 5;
     // the block kernel squares one matrix held whole on this GPU (its BSR view is A's);
     // Taylor terms keep their own kernels
-    if (kern == 11 && self == 0.0) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 1);
-    if (kern == 11 && (P.world > 1 || B.rp != A.rp)) kern = 5;
+    if ((kern == 11 || kern == 12) && self == 0.0) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 1);
+    if ((kern == 11 || kern == 12) && (P.world > 1 || B.rp != A.rp)) kern = 5;
     if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 1;
     if (kern == 6 && !taylor_pull_ok) kern = 1;
     if (kern == 7) CK(cudaMemsetAsync(P.dia_prod.p, 0, sizeof(unsigned long long), st));
@@ -714,7 +714,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       int stage = kern;
       bool first = true, dia_retry = false;
       // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
-      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10 || kern == 11);
+      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10 || kern == 11 || kern == 12);
       while (nlist > 0) {
         if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
           run_symbolic();
@@ -753,7 +753,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         } else if (stage == 5) {
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
-        } else if (stage == 11) {
+        } else if (stage == 11 || stage == 12) {
           // BSR-8 view of A (= B) and its block transpose, then the block kernel over block
           // rows in index order
           const int64_t nbr = (nr + 7) / 8, nbc = (P.n + 7) / 8;
@@ -802,8 +802,11 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           Bv.tb = w.tb.p;
           if (use_cluster && nr == P.row_end - P.row_begin && !getenv("SEXPM_BSR_NATURAL"))
             Bv.border = P.block_order.p;
-          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, (int64_t)P.sm_count * 2));
-          w.bscr.ensure((size_t)nh.grid * kBsrScratchPerCta, st);
+          if (stage == 12)  // block-row pairs, one 512-thread CTA per SM
+            nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nbr + 1) / 2, (int64_t)P.sm_count));
+          else
+            nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, (int64_t)P.sm_count * 2));
+          w.bscr.ensure((size_t)nh.grid * (stage == 12 ? kBsr2ScratchPerCta : kBsrScratchPerCta), st);
           CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
           w.prof.ensure(16, st);
           CK(cudaMemsetAsync(w.prof.p, 0, 16 * sizeof(unsigned long long), st));
@@ -812,7 +815,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           CK(cudaEventCreate(&k0));
           CK(cudaEventCreate(&k1));
           CK(cudaEventRecord(k0, st));
-          launch_numeric_bsr(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
+          if (stage == 12)
+            launch_numeric_bsr2(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
+          else
+            launch_numeric_bsr(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
           CK(cudaEventRecord(k1, st));
           CK(cudaEventSynchronize(k1));
           CK(cudaEventElapsedTime(&rep.kernel_ms, k0, k1));
@@ -885,7 +891,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         if (stage == 7 && !dia_retry && P.dia_slots < P.dia_slots_max) {
           dia_retry = true;
         } else {
-          stage = stage == 7 ? 5 : (stage == 6 ? 1 : ((stage >= 8 && stage <= 11) ? 5 : 3));
+          stage = stage == 7 ? 5 : (stage == 6 ? 1 : ((stage >= 8 && stage <= 12) ? 5 : 3));
           nfail_other += nf;
         }
       }

@@ -3557,6 +3557,394 @@ void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, 
   k_numeric_bsr<<<a.grid, kBThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
 }
 
+
+// ------------------------------------------------------------------------------------
+// K3b2: K3b over PAIRS of block rows (I0, I1 = consecutive entries of the processing order,
+// spatially adjacent): one CTA of 16 warps per pair, both rows' A blocks in shared memory,
+// candidate output blocks J = union over both rows.  A warp computes C_I0J and C_I1J together:
+// lane holds C_h[i][j], C_h[i+4][j] for h = 0, 1 (i = lane / 8, j = lane % 8).  For every K of
+// column J's block list (ascending) that row I0 or row I1 holds, the staged B_KJ block is read
+// once and multiplied into both rows; a row that lacks K uses an all-zero A block, which adds
+// exact zeros (x + 0 = x), so each element still sees the self term then the products of its
+// own row in ascending k -- bit-identical to K3b and to the oracle.  Sharing each B block
+// between two block rows halves the B-side shared/L1 traffic per block product (the kernel
+// is bound by the L1 wavefront rate).  The output blocks go to scratch
+// raw; the staging pass (one warp per row, 16 rows) derives the Algorithm 4.1 row sums from
+// them while it stages the kept entries.
+// ------------------------------------------------------------------------------------
+constexpr int kB2Threads = 512;
+constexpr int kB2Warps = kB2Threads / 32;
+constexpr int kB2JCap = kBsr2JCap;  // output block pairs per block-row pair (scratch: 128 doubles each)
+
+int bsr2_numeric_smem_bytes() {
+  return (2 * kBACap + 1) * 64 * 8 + kB2Warps * kBPF * 64 * 8 + kB2Warps * kBML * 8 +
+         2 * kB2Warps * kBML * 4 + 2 * kBACap * 4 + 2 * kBKWords * 4 + 2 * kBKWords * 2 +
+         kBJWords * 4 + kB2JCap * 4 + kB2JCap * 16 * 2 + 64;
+}
+
+// x0 += sum_k a0[i0][k] b[k][lj] (and rows i1, and A block a1) -- k ascending, _rn
+__device__ __forceinline__ void bsr2_block_fma(const double *bs, const double *a0, const double *a1,
+                                               int i0, int i1, int lj, double &x00, double &x01,
+                                               double &x10, double &x11) {
+  const double *bq = bs + lj;
+  const double *p00 = a0 + i0 * 8, *p01 = a0 + i1 * 8, *p10 = a1 + i0 * 8, *p11 = a1 + i1 * 8;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const double b = bq[k * 8];
+    x00 = __dadd_rn(x00, __dmul_rn(p00[k], b));
+    x01 = __dadd_rn(x01, __dmul_rn(p01[k], b));
+    x10 = __dadd_rn(x10, __dmul_rn(p10[k], b));
+    x11 = __dadd_rn(x11, __dmul_rn(p11[k], b));
+  }
+}
+
+__global__ void __launch_bounds__(kB2Threads, 1) k_numeric_bsr2(NumericArgs a, BsrView Bv, int64_t nrows,
+                                                                double *scratch, int32_t *fail_rows,
+                                                                int *fail_count) {
+  extern __shared__ double bsm2[];
+  double *aval = bsm2;                                                       // (2 kBACap + 1) * 64
+  double *wstage = aval + (2 * kBACap + 1) * 64;                             // kB2Warps * kBPF * 64
+  int64_t *mlb = reinterpret_cast<int64_t *>(wstage + kB2Warps * kBPF * 64);  // kB2Warps * kBML
+  int32_t *mlk = reinterpret_cast<int32_t *>(mlb + kB2Warps * kBML);         // 2 * kB2Warps * kBML
+  int32_t *aK = mlk + 2 * kB2Warps * kBML;                                   // 2 * kBACap
+  unsigned *kbits = reinterpret_cast<unsigned *>(aK + 2 * kBACap);           // 2 * kBKWords
+  uint16_t *kpref = reinterpret_cast<uint16_t *>(kbits + 2 * kBKWords);      // 2 * kBKWords
+  unsigned *jbits = reinterpret_cast<unsigned *>(kpref + 2 * kBKWords);      // kBJWords
+  int32_t *jlist = reinterpret_cast<int32_t *>(jbits + kBJWords);            // kB2JCap
+  uint16_t *jcnt = reinterpret_cast<uint16_t *>(jlist + kB2JCap);            // kB2JCap * 16
+  __shared__ int s_p, s_fail, s_nj, s_jmin, s_njw;
+  __shared__ int s_na[2], s_kmin[2], s_nkw[2], s_nr[2];
+  __shared__ long long s_I[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *scr = scratch + (size_t)blockIdx.x * kB2JCap * 128;
+  const int zero_blk = 2 * kBACap;  // index of the all-zero A block
+  for (int i = tid; i < 64; i += kB2Threads) aval[zero_blk * 64 + i] = 0.0;
+  for (int i = tid; i < 2 * kBKWords; i += kB2Threads) kbits[i] = 0u;
+  for (int i = tid; i < kBJWords; i += kB2Threads) jbits[i] = 0u;
+  const int li = lane >> 3, lj = lane & 7;
+  const int i0 = li, i1 = li + 4;
+  const int64_t npairs = (Bv.nbr + 1) / 2;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_p = atomicAdd(a.row_counter, 1);
+    __syncthreads();
+    const int p = s_p;
+    if (p >= npairs) break;
+    if (tid < 2) {
+      const int64_t q = 2 * (int64_t)p + tid;
+      const int64_t I = q < Bv.nbr ? (Bv.border ? (int64_t)Bv.border[q] : q) : -1;
+      s_I[tid] = I;
+      const int64_t r0 = 8 * I;
+      const int nr = I < 0 ? 0 : (int)(nrows - r0 < 8 ? nrows - r0 : 8);
+      const int na = I < 0 ? 0 : (int)(Bv.brp[I + 1] - Bv.brp[I]);
+      s_nr[tid] = nr;
+      s_na[tid] = na;
+      const int kmin = na > 0 ? Bv.bcol[Bv.brp[I]] : 0, kmax = na > 0 ? Bv.bcol[Bv.brp[I + 1] - 1] : -1;
+      s_kmin[tid] = kmin;
+      s_nkw[tid] = na > 0 ? ((kmax - kmin) >> 5) + 1 : 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int fail = s_na[0] > kBACap || s_na[1] > kBACap || s_nkw[0] > kBKWords || s_nkw[1] > kBKWords;
+      int jmin = INT32_MAX, jmax = -1;
+      for (int h = 0; h < 2; h++)
+        for (int i = 0; i < s_nr[h]; i++) {
+          const int64_t r = 8 * s_I[h] + i;
+          if (a.hi[r] >= a.lo[r]) {
+            jmin = min(jmin, a.lo[r] >> 3);
+            jmax = max(jmax, a.hi[r] >> 3);
+          }
+        }
+      if (jmax >= jmin && ((jmax - jmin) >> 5) + 1 > kBJWords) fail = 1;
+      s_fail = fail;
+      s_jmin = jmin;
+      s_njw = jmax >= jmin ? ((jmax - jmin) >> 5) + 1 : 0;
+    }
+    __syncthreads();
+    const int nrt = s_nr[0] + s_nr[1];
+    if (s_fail || (s_na[0] == 0 && s_na[1] == 0) || s_njw == 0) {
+      if (tid < 16) {
+        const int h = tid >> 3, i = tid & 7;
+        if (i < s_nr[h]) {
+          const int64_t r = 8 * s_I[h] + i;
+          if (s_fail) {
+            fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+          } else {
+            a.row_off[r] = 0;
+            a.row_cnt[r] = 0;
+            a.row_fsum[r] = 0.0;
+            a.row_nnz[r] = 0;
+            if (a.row_p1) {
+              a.row_p1[r] = 0.0;
+              a.row_c1[r] = 0;
+            }
+          }
+        }
+      }
+      (void)nrt;
+      continue;
+    }
+    const int jmin = s_jmin, njw = s_njw;
+    // (1) both rows of A: block columns, values, K bitmaps
+    for (int h = 0; h < 2; h++) {
+      const int na = s_na[h], kmin = s_kmin[h];
+      const int64_t ab0 = na > 0 ? Bv.brp[s_I[h]] : 0;
+      for (int t = tid; t < na; t += kB2Threads) {
+        const int K = Bv.bcol[ab0 + t];
+        aK[h * kBACap + t] = K;
+        atomicOr(&kbits[h * kBKWords + ((K - kmin) >> 5)], 1u << ((K - kmin) & 31));
+      }
+      for (int t = tid; t < na * 64; t += kB2Threads) aval[h * kBACap * 64 + t] = Bv.bval[ab0 * 64 + t];
+    }
+    __syncthreads();
+    if (warp < 2) {  // word prefix of each K bitmap (warp h: row h)
+      const int h = warp, nkw = s_nkw[h];
+      unsigned *kb = kbits + h * kBKWords;
+      uint16_t *kp = kpref + h * kBKWords;
+      const int per = (nkw + 31) / 32;
+      const int w0 = min(lane * per, nkw), w1 = min(w0 + per, nkw);
+      int c = 0;
+      for (int w = w0; w < w1; w++) c += __popc(kb[w]);
+      int v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, v, o);
+        if (lane >= o) v += y;
+      }
+      int run = v - c;
+      for (int w = w0; w < w1; w++) {
+        kp[w] = (uint16_t)run;
+        run += __popc(kb[w]);
+      }
+    }
+    // (2) candidate output blocks: union of B's block rows at both rows' block columns
+    for (int t = warp; t < s_na[0] + s_na[1]; t += kB2Warps) {
+      const int64_t K = t < s_na[0] ? aK[t] : aK[kBACap + t - s_na[0]];
+      if (K < Bv.nbr) {
+        for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
+          const int jb = Bv.bcol[b] - jmin;
+          if (jb >= 0 && jb < njw * 32) atomicOr(&jbits[jb >> 5], 1u << (jb & 31));
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int per = (njw + 31) / 32;
+      const int w0 = min(lane * per, njw), w1 = min(w0 + per, njw);
+      int c = 0;
+      for (int w = w0; w < w1; w++) c += __popc(jbits[w]);
+      int v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, v, o);
+        if (lane >= o) v += y;
+      }
+      const int tot = __shfl_sync(FULL_MASK, v, 31);
+      if (lane == 0) s_nj = tot;
+      if (tot <= kB2JCap) {
+        int run = v - c;
+        for (int w = w0; w < w1; w++) {
+          unsigned m = jbits[w];
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            jlist[run++] = jmin + w * 32 + b;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nj = s_nj;
+    const bool over = nj > kB2JCap;
+    unsigned long long nbp = 0;
+    const int kmin0 = s_kmin[0], kmin1 = s_kmin[1], nkw0 = s_nkw[0], nkw1 = s_nkw[1];
+    auto lookup = [&](int h, int K) -> int {  // rank of block column K in row h, or -1
+      const int kb = K - (h ? kmin1 : kmin0);
+      const int nkw = h ? nkw1 : nkw0;
+      const unsigned *bits = kbits + h * kBKWords;
+      if (kb < 0 || kb >= nkw * 32 || !((bits[kb >> 5] >> (kb & 31)) & 1u)) return -1;
+      return kpref[h * kBKWords + (kb >> 5)] + __popc(bits[kb >> 5] & ((1u << (kb & 31)) - 1u));
+    };
+    // (3) output blocks (pairs of blocks), one warp each
+    if (!over) {
+      for (int q = warp; q < nj; q += kB2Warps) {
+        const int J = jlist[q];
+        double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;
+        if (a.self_coef != 0.0) {  // self term: A_hJ
+          const int r0 = lookup(0, J), r1 = lookup(1, J);
+          if (r0 >= 0) {
+            x00 = __dmul_rn(a.self_coef, aval[r0 * 64 + i0 * 8 + lj]);
+            x01 = __dmul_rn(a.self_coef, aval[r0 * 64 + i1 * 8 + lj]);
+          }
+          if (r1 >= 0) {
+            x10 = __dmul_rn(a.self_coef, aval[(kBACap + r1) * 64 + i0 * 8 + lj]);
+            x11 = __dmul_rn(a.self_coef, aval[(kBACap + r1) * 64 + i1 * 8 + lj]);
+          }
+        }
+        int64_t *wb = mlb + warp * kBML;
+        int32_t *wk0 = mlk + warp * kBML, *wk1 = mlk + (kB2Warps + warp) * kBML;
+        double *stg = wstage + warp * kBPF * 64;
+        const int64_t t0 = Bv.tp[J], t1 = Bv.tp[J + 1];
+        int64_t tb0 = t0;
+        while (tb0 < t1) {
+          int nm = 0;
+          for (; tb0 < t1 && nm <= kBML - 32; tb0 += 32) {
+            const int64_t t = tb0 + lane;
+            int ra0 = -1, ra1 = -1;
+            int64_t bidx = 0;
+            if (t < t1) {
+              const int K = Bv.tk[t];
+              ra0 = lookup(0, K);
+              ra1 = lookup(1, K);
+              if (ra0 >= 0 || ra1 >= 0) bidx = Bv.tb[t];
+            }
+            const bool hit = ra0 >= 0 || ra1 >= 0;
+            const unsigned m = __ballot_sync(FULL_MASK, hit);
+            if (hit) {
+              const int pos = nm + __popc(m & lanemask_lt());
+              wk0[pos] = ra0 >= 0 ? ra0 : zero_blk;
+              wk1[pos] = ra1 >= 0 ? kBACap + ra1 : zero_blk;
+              wb[pos] = bidx;
+            }
+            nm += __popc(m);
+          }
+          __syncwarp();
+          nbp += nm;
+          double2 pf[kBPF];
+#pragma unroll
+          for (int d = 0; d < kBPF; d++)
+            if (d < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[d] * 64)[lane];
+          int t = 0;
+          for (; t + kBPF <= nm; t += kBPF) {
+#pragma unroll
+            for (int d = 0; d < kBPF; d++) reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
+            __syncwarp();
+#pragma unroll
+            for (int d = 0; d < kBPF; d++)
+              if (t + kBPF + d < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[t + kBPF + d] * 64)[lane];
+#pragma unroll
+            for (int d = 0; d < kBPF; d++)
+              bsr2_block_fma(stg + d * 64, aval + wk0[t + d] * 64, aval + wk1[t + d] * 64, i0, i1, lj,
+                             x00, x01, x10, x11);
+            __syncwarp();
+          }
+          if (t < nm) {
+#pragma unroll
+            for (int d = 0; d < kBPF; d++)
+              if (t + d < nm) reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
+            __syncwarp();
+#pragma unroll
+            for (int d = 0; d < kBPF; d++)
+              if (t + d < nm)
+                bsr2_block_fma(stg + d * 64, aval + wk0[t + d] * 64, aval + wk1[t + d] * 64, i0, i1,
+                               lj, x00, x01, x10, x11);
+            __syncwarp();
+          }
+        }
+        // raw values to scratch (block pair q: row h*8 + i at q*128 + (h*8 + i)*8), kept
+        // counts per (q, row) from ballots
+        double *sq = scr + (size_t)q * 128;
+        sq[i0 * 8 + lj] = x00;
+        sq[i1 * 8 + lj] = x01;
+        sq[64 + i0 * 8 + lj] = x10;
+        sq[64 + i1 * 8 + lj] = x11;
+        auto kept = [&](double x) { return x != 0.0 && fabs(x) > a.floor_tau; };
+        const unsigned m00 = __ballot_sync(FULL_MASK, kept(x00)), m01 = __ballot_sync(FULL_MASK, kept(x01));
+        const unsigned m10 = __ballot_sync(FULL_MASK, kept(x10)), m11 = __ballot_sync(FULL_MASK, kept(x11));
+        if (lj == 0) {
+          jcnt[q * 16 + i0] = (uint16_t)__popc((m00 >> (li * 8)) & 0xFFu);
+          jcnt[q * 16 + i1] = (uint16_t)__popc((m01 >> (li * 8)) & 0xFFu);
+          jcnt[q * 16 + 8 + i0] = (uint16_t)__popc((m10 >> (li * 8)) & 0xFFu);
+          jcnt[q * 16 + 8 + i1] = (uint16_t)__popc((m11 >> (li * 8)) & 0xFFu);
+        }
+      }
+    }
+    if (a.prof && lane == 0 && nbp) atomicAdd(&a.prof[0], 2 * nbp);
+    __syncthreads();
+    // (4) one warp per row (16 rows): Algorithm 4.1 row sums from the raw blocks, kept entries
+    // staged contiguously in column order
+    if (over) {
+      if (tid < 16 && (tid & 7) < s_nr[tid >> 3]) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)(8 * s_I[tid >> 3] + (tid & 7));
+    } else if ((warp & 7) < s_nr[warp >> 3]) {
+      const int h = warp >> 3, i = warp & 7;
+      const int64_t r = 8 * s_I[h] + i;
+      long long tot = 0;
+      for (int q0 = 0; q0 < nj; q0 += 32) {
+        const int c = q0 + lane < nj ? jcnt[(q0 + lane) * 16 + warp] : 0;
+        tot += __reduce_add_sync(FULL_MASK, c);
+      }
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)tot);
+      off = __shfl_sync(FULL_MASK, off, 0);
+      const bool ok = (long long)off + tot <= a.pool_cap;
+      long long pos = (long long)off;
+      double fs = 0.0, p1 = 0.0;
+      long long nz = 0, c1 = 0;
+      for (int q0 = 0; q0 < nj; q0 += 32) {
+        const int q = q0 + lane;
+        const int c = q < nj ? jcnt[q * 16 + warp] : 0;
+        int v = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL_MASK, v, o);
+          if (lane >= o) v += y;
+        }
+        if (q < nj) {
+          long long pp = pos + v - c;
+          const double *src = scr + (size_t)q * 128 + warp * 8;
+          const int J = jlist[q];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const double x = src[j];
+            if (x != 0.0) {
+              nz++;
+              if (fabs(x) > a.floor_tau) {
+                if (fabs(x) <= a.eps_g) p1 += x * x;
+                else c1++;
+                if (ok) {
+                  a.pool_col[pp] = 8 * J + j;
+                  a.pool_val[pp] = x;
+                }
+                pp++;
+              } else {
+                fs += x * x;
+              }
+            }
+          }
+        }
+        pos += __shfl_sync(FULL_MASK, v, 31);
+      }
+      fs = warp_sum(fs);
+      p1 = warp_sum(p1);
+      nz = warp_sum(nz);
+      c1 = warp_sum(c1);
+      if (lane == 0) {
+        if (!ok) atomicOr(a.flags, 1);
+        a.row_off[r] = (int64_t)off;
+        a.row_cnt[r] = tot;
+        a.row_fsum[r] = fs;
+        a.row_nnz[r] = nz;
+        if (a.row_p1) {
+          a.row_p1[r] = p1;
+          a.row_c1[r] = c1;
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < 2 * kBKWords; i += kB2Threads) kbits[i] = 0u;
+    for (int i = tid; i < njw; i += kB2Threads) jbits[i] = 0u;
+  }
+}
+
+void launch_numeric_bsr2(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+                         int32_t *fail_rows, int *fail_count, cudaStream_t st) {
+  if (Bv.nbr == 0) return;
+  const int smem = bsr2_numeric_smem_bytes();
+  cudaFuncSetAttribute(k_numeric_bsr2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_numeric_bsr2<<<a.grid, kB2Threads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
+}
+
 // ------------------------------------------------------------------------------------
 // Diagonal structure of H0 (plan time): offsets d = j - k present anywhere in H0, as a
 // bitmap over [-(n-1), n-1]; then the diagonals h_d[k] = H0(k, k + d).

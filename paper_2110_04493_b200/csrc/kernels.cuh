@@ -168,6 +168,8 @@ struct BsrView {
 };
 constexpr int kBsrScratchPerCta = 512 * 64;  // doubles of output-block scratch per CTA
 constexpr int kBsrMaxRowBlocks = 136;        // blocks of a block row the numeric kernel holds
+constexpr int kBsr2JCap = 768;               // K3b2: output block pairs per block-row pair
+constexpr int kBsr2ScratchPerCta = kBsr2JCap * 128;  // doubles of K3b2 scratch per CTA
 void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st);
 void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
                      double *bval, int *flags, cudaStream_t st);
@@ -182,6 +184,10 @@ void launch_bsr_transpose(int64_t nbr, int64_t nbc, int64_t nb, const int64_t *b
 int bsr_numeric_smem_bytes();
 void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                         int32_t *fail_rows, int *fail_count, cudaStream_t st);
+// K3b2: the same product over pairs of block rows (one 512-thread CTA per pair, scratch of
+// kBsrScratchPerCta * 2 doubles per CTA)
+void launch_numeric_bsr2(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+                         int32_t *fail_rows, int *fail_count, cudaStream_t st);
 // hash-accumulator variant; rows whose table over-fills are appended to fail_rows
 int hash_smem_bytes();
 void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,

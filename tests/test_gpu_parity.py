@@ -260,7 +260,7 @@ def test_alg41_random_vs_oracle(B):
         assert d == pytest.approx(dropped_o, rel=1e-10, abs=1e-300)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 @pytest.mark.parametrize("name", ["heat2d_pm10_20", "structural_24", "heat3d_9", "banded_nonsym"])
 def test_accumulator_variants(B, kernel, name):
     """Every K3 accumulator (hash, warp-window, block-window) meets parity."""
@@ -269,7 +269,7 @@ def test_accumulator_variants(B, kernel, name):
     assert_parity(Eg, st, Eo, tr)
 
 
-@pytest.mark.parametrize("kernel", [2, 4, 5, 8, 9, 10, 11])
+@pytest.mark.parametrize("kernel", [2, 4, 5, 8, 9, 10, 11, 12])
 @pytest.mark.parametrize("seed", range(4))
 def test_bit_exact_products(B, seed, kernel):
     """The warp-window, k-sync hash, paged and grouped kernels accumulate the self term
@@ -365,7 +365,7 @@ def test_group_kernel_long_b_rows(B, kernel):
     assert np.array_equal(G.val, Ct.val)
 
 
-@pytest.mark.parametrize("kernel", [8, 9, 11])
+@pytest.mark.parametrize("kernel", [8, 9, 11, 12])
 def test_group_kernel_fallback_wide_rows(B, kernel):
     """Rows whose k span exceeds the grouped kernel's union bitmap fall through to the paged
     kernel; the result is unchanged (bit-identical to the oracle)."""
@@ -383,13 +383,15 @@ def test_group_kernel_fallback_wide_rows(B, kernel):
     assert np.array_equal(G.val, Ct.val)
 
 
-@pytest.mark.parametrize("n", [1, 7, 8, 9, 250, 1003])
-def test_bsr_kernel_bit_exact_sizes(B, n):
-    """The block kernel (BSR-8 view) on sizes that are not multiples of 8, with empty rows:
-    C~ = 2A + A*A bit-identical to the oracle."""
+@pytest.mark.parametrize("kernel", [11, 12])
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 17, 250, 1003])
+def test_bsr_kernel_bit_exact_sizes(B, n, kernel):
+    """The block kernels (BSR-8 view; 12 = block-row pairs, odd block-row counts at n = 1,
+    9, 17, 1003) on sizes that are not multiples of 8, with empty rows: C~ = 2A + A*A
+    bit-identical to the oracle."""
     A = _rand_csr(n, min(n, 12), 0.5, 400 + n, empty_rows=tuple(r for r in (0, 3, n // 2) if r < n))
     (rp, ci, va), _, _, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(A), 2.0, 1.0, 0.0,
-                                                           kernel=11)
+                                                           kernel=kernel)
     Ct = O.spgemm(A, A, 2.0, 1.0)
     G = from_dev(n, rp, ci, va)
     assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
