@@ -1363,6 +1363,7 @@ static void build_diagonals(sexpm_plan_s &P) {
   P.dia_nd = 0;
   const DCsr &Hf = P.H0full;
   if (Hf.nnz == 0 || P.o.kernel != 0 && P.o.kernel != 7) return;
+  if (P.n > (int64_t(1) << 30)) return;  // K5d computes columns k + d in 32 bits
   const int64_t nbits = 2 * P.n - 1, nwords = (nbits + 31) / 32;
   DBuf<unsigned> bits;
   bits.alloc((size_t)nwords, st);

@@ -4038,7 +4038,7 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
   __syncthreads();
   const int nd = D.ndiag;
   const int32_t dmin = D.dmin, dmax = D.dmax;
-  const int64_t n = D.n;
+  const int n = (int)D.n;  // columns are int32: every column index below fits 32 bits
   unsigned long long prods = 0;
   int need = 0;              // most slots a row of this warp needed
   constexpr int kBatch = 4;  // rows taken per scheduler atomic
@@ -4065,28 +4065,28 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
         }
         continue;
       }
-      int64_t lo = (int64_t)a.A.col[p0] + dmin, hi = (int64_t)a.A.col[p1 - 1] + dmax;
+      int lo = a.A.col[p0] + dmin, hi = a.A.col[p1 - 1] + dmax;
       lo = lo < 0 ? 0 : lo;
       hi = hi > n - 1 ? n - 1 : hi;
       int sh = 3;
-      while (sh < 7 && ((hi >> sh) - (lo >> sh)) >= (int64_t)kDPageWords * 32) sh++;
-      const int64_t pg0 = lo >> sh;
+      while (sh < 7 && ((hi >> sh) - (lo >> sh)) >= kDPageWords * 32) sh++;
+      const int pg0 = lo >> sh;
       const int npg = (int)((hi >> sh) - pg0 + 1);
       bool fail = sh >= 7;
       // (1) mark reachable pages
       // lanes hold ascending k, so equal pages are adjacent lanes: a lane marks its page only
       // if the lane below holds a different one (one atomic per page run)
       if (!fail) {
-        int64_t kn = lane < nx ? (int64_t)a.A.col[p0 + lane] : -1;
+        int kn = lane < nx ? a.A.col[p0 + lane] : -1;
         for (int c0 = 0; c0 < nx; c0 += 32) {
-          const int64_t k = kn;
-          kn = c0 + 32 + lane < nx ? (int64_t)a.A.col[p0 + c0 + 32 + lane] : -1;
+          const int k = kn;
+          kn = c0 + 32 + lane < nx ? a.A.col[p0 + c0 + 32 + lane] : -1;
 #pragma unroll
           for (int di = 0; di < MAXD; di++) {
             if (di < nd) {
-              const int64_t j = k + s_doff[di];
+              const int j = k + s_doff[di];
               const bool v = k >= 0 && j >= 0 && j < n;
-              const int pg = v ? (int)((j >> sh) - pg0) : -1;
+              const int pg = v ? (j >> sh) - pg0 : -1;
               const int pgl = __shfl_up_sync(FULL_MASK, pg, 1);
               if (v && (lane == 0 || pgl != pg)) atomicOr(&pbits[pg >> 5], 1u << (pg & 31));
             }
@@ -4135,27 +4135,28 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
       // (3) products, offsets descending inside each chunk of 32 entries; the next chunk's
       // entries and diagonal values are loaded while this chunk is accumulated
       const int pmask = (1 << sh) - 1;
-      int64_t kc = -1;
+      int kc = -1;
       double sc = 0.0, hc[MAXD];
-      auto load_chunk = [&](int c0, int64_t &k, double &sv, double (&h)[MAXD]) {
+      auto load_chunk = [&](int c0, int &k, double &sv, double (&h)[MAXD]) {
         const int t = c0 + lane;
         const bool in = t < nx;
-        k = in ? (int64_t)a.A.col[p0 + t] : -1;
+        k = in ? a.A.col[p0 + t] : -1;
         sv = in ? a.A.val[p0 + t] : 0.0;
+        const double *hk = D.val + (in ? k : 0);
 #pragma unroll
-        for (int di = 0; di < MAXD; di++) h[di] = (di < nd && in) ? D.val[(int64_t)di * n + k] : 0.0;
+        for (int di = 0; di < MAXD; di++) h[di] = (di < nd && in) ? hk[(size_t)di * (size_t)n] : 0.0;
       };
       load_chunk(0, kc, sc, hc);
       for (int c0 = 0; c0 < nx; c0 += 32) {
-        int64_t kn;
+        int kn;
         double sn, hn[MAXD];
         if (c0 + 32 < nx) load_chunk(c0 + 32, kn, sn, hn);
 #pragma unroll
         for (int di = 0; di < MAXD; di++) {
           if (di < nd) {
             if (hc[di] != 0.0) {
-              const int64_t j = kc + s_doff[di];
-              const int pg = (int)((j >> sh) - pg0);
+              const int j = kc + s_doff[di];
+              const int pg = (j >> sh) - pg0;
               const unsigned wd = pbits[pg >> 5];
               const int rank = pref[pg >> 5] + __popc(wd & ((1u << (pg & 31)) - 1u));
               const int o = (rank << sh) + (int)(j & pmask);
@@ -4215,7 +4216,7 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
         const unsigned m = __ballot_sync(FULL_MASK, st);
         if (st && ok) {
           const long long q = pos + __popc(m & lanemask_lt());
-          a.pool_col[q] = (int32_t)(((pg0 + plist[s0 >> sh]) << sh) + (s0 & pmask));
+          a.pool_col[q] = ((pg0 + plist[s0 >> sh]) << sh) + (s0 & pmask);
           a.pool_val[q] = x;
         }
         pos += __popc(m);
