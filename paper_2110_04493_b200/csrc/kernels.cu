@@ -3446,12 +3446,16 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
             fs1 += x1 * x1;
           }
         }
-        scr[(size_t)q * 64 + i0 * 8 + lj] = st0 ? x0 : 0.0;
-        scr[(size_t)q * 64 + i1 * 8 + lj] = st1 ? x1 : 0.0;
+        // only the staged values go to scratch, packed at the front of their (block, row)
+        // slot; the row's 8-bit keep mask (shared memory) gives their columns
         const unsigned b0m = __ballot_sync(FULL_MASK, st0), b1m = __ballot_sync(FULL_MASK, st1);
+        const unsigned m0 = (b0m >> (li * 8)) & 0xFFu, m1 = (b1m >> (li * 8)) & 0xFFu;
+        const unsigned below = (1u << lj) - 1u;
+        if (st0) scr[(size_t)q * 64 + i0 * 8 + __popc(m0 & below)] = x0;
+        if (st1) scr[(size_t)q * 64 + i1 * 8 + __popc(m1 & below)] = x1;
         if (lj == 0) {
-          jcnt[q * 8 + i0] = (uint16_t)__popc((b0m >> (li * 8)) & 0xFFu);
-          jcnt[q * 8 + i1] = (uint16_t)__popc((b1m >> (li * 8)) & 0xFFu);
+          jcnt[q * 8 + i0] = (uint16_t)m0;
+          jcnt[q * 8 + i1] = (uint16_t)m1;
         }
       }
     }
@@ -3487,7 +3491,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
       const int64_t r = r0 + i;
       long long tot = 0;
       for (int q0 = 0; q0 < nj; q0 += 32) {
-        const int c = q0 + lane < nj ? jcnt[(q0 + lane) * 8 + i] : 0;
+        const int c = q0 + lane < nj ? __popc(jcnt[(q0 + lane) * 8 + i]) : 0;
         tot += __reduce_add_sync(FULL_MASK, c);
       }
       unsigned long long off = 0;
@@ -3498,7 +3502,8 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
         long long pos = (long long)off;
         for (int q0 = 0; q0 < nj; q0 += 32) {
           const int q = q0 + lane;
-          const int c = q < nj ? jcnt[q * 8 + i] : 0;
+          unsigned m = q < nj ? jcnt[q * 8 + i] : 0u;
+          const int c = __popc(m);
           int v = c;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -3509,14 +3514,11 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
             long long p = pos + v - c;
             const double *src = scr + (size_t)q * 64 + i * 8;
             const int J = jlist[q];
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-              const double x = src[j];
-              if (x != 0.0) {
-                a.pool_col[p] = 8 * J + j;
-                a.pool_val[p] = x;
-                p++;
-              }
+            for (int e = 0; m; e++, p++) {
+              const int j = __ffs(m) - 1;
+              m &= m - 1;
+              a.pool_col[p] = 8 * J + j;
+              a.pool_val[p] = src[e];
             }
           }
           pos += __shfl_sync(FULL_MASK, v, 31);
