@@ -196,6 +196,18 @@ int sexpm_run(sexpm_plan_t p, sexpm_csr_out *E);
  * HOST (D2H, pinned or pageable) or DEVICE (D2D) pointers alike; synchronises the stream. */
 int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *vals);
 
+/* N1 apply: Y = R^steps X, R the last result (E = I + T^_N, or T^_N
+ * with output_T), i.e. `steps` steps of the discretised system u_{k+1} = e^H u_k (Eq. 2.2,
+ * P:54; the validation protocol of P:501-503).  X: DEVICE, row-major, n x m (row stride
+ * ldx >= m doubles); Y: DEVICE, row-major, n x m (ldy >= m), caller-owned, must not overlap
+ * X.  m >= 0, steps >= 1.  For m >= 32 every Y entry is the sum over the row's entries in
+ * ascending column order with separately rounded products (bit-identical to the oracle's
+ * or_spmm); for m < 32 the row's entries are split over lane groups and combined by a fixed
+ * tree (deterministic).  steps > 1 uses two plan-owned n x m buffers.  Single GPU only
+ * (world 1, else SEXPM_EINVAL); SEXPM_ESTATE before sexpm_run.  Synchronises the stream. */
+int sexpm_apply(sexpm_plan_t p, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                int32_t steps);
+
 /* Plan scalars, per-step trace and CUDA-event timings of the last run. */
 int sexpm_stats_get(sexpm_plan_t p, sexpm_stats *s);
 
@@ -224,6 +236,12 @@ int sexpm_filtered_product(sexpm_plan_t p, const sexpm_csr_in *A, const sexpm_cs
  * eps_g == 0) and the dropped Frobenius norm. */
 int sexpm_alg41(sexpm_plan_t p, const double *x, int64_t cnt, double eps_g, double e_r,
                 int32_t *passes, double *tau, double *dropped);
+
+/* Y = A X for any device CSR A (rows row_begin..row_end of an n x n matrix, global column
+ * indices) and dense device X (n x m, row-major, ldx >= m) into Y (rows of A x m, ldy >= m):
+ * the kernel of sexpm_apply.  Runs on the plan's stream and synchronises it. */
+int sexpm_spmm(sexpm_plan_t p, const sexpm_csr_in *A, int64_t m, const double *X, int64_t ldx,
+               double *Y, int64_t ldy);
 
 /* Host-side halo planner for the row-partitioned multi-GPU squaring (Lemma 3.1):
  * rank g owns rows [bounds[g], bounds[g+1]); with T^_{i-1} of bandwidths (l1, l2) the

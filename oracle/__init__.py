@@ -11,6 +11,7 @@ from .oracle import (  # noqa: F401
     alg41,
     expm,
     spgemm,
+    spmm,
     add,
     norm_one,
     norm_fro,

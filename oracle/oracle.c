@@ -650,3 +650,49 @@ or_result *or_add(int64_t n, const int64_t *arp, const int32_t *aci, const doubl
   ocsr B = {n, (int64_t *)brp, (int32_t *)bci, (double *)bv};
   return wrap(csr_add(&A, &B));
 }
+
+/* ------------------------------------------------------------------------- */
+/* N1 apply: one step of the discretised system            */
+/*   u_{k+1} = e^H u_k            (Eq. 2.2; validation of P:501-503)   */
+/* for a block of m vectors: Y = A X, A CSR (n x n), X, Y dense row-major    */
+/* (n x m).  Y(r, j) = sum over the entries of row r in ascending column     */
+/* order of a_rk * X(k, j), starting from 0 (products rounded separately,    */
+/* -ffp-contract=off).  steps > 1 applies A `steps` times: Y = A^steps X.    */
+/* Parity pinned by tests/test_oracle_apply.py (dense matmul, E^k = e^{kH},  */
+/* E 1 = 1 for zero-row-sum generators).                                     */
+/* ------------------------------------------------------------------------- */
+static void spmm_once(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                      int64_t m, const double *X, double *Y) {
+  for (int64_t r = 0; r < n; r++) {
+    for (int64_t j = 0; j < m; j++) {
+      double y = 0.0;
+      for (int64_t p = rp[r]; p < rp[r + 1]; p++) y = y + v[p] * X[(int64_t)ci[p] * m + j];
+      Y[r * m + j] = y;
+    }
+  }
+}
+
+int or_spmm(int64_t n, const int64_t *rp, const int32_t *ci, const double *v, int64_t m,
+            const double *X, double *Y, int steps) {
+  if (n < 0 || m < 0 || steps < 1) return 1;
+  if (steps == 1) {
+    spmm_once(n, rp, ci, v, m, X, Y);
+    return 0;
+  }
+  double *a = (double *)malloc(sizeof(double) * (size_t)(n * m > 0 ? n * m : 1));
+  double *b = (double *)malloc(sizeof(double) * (size_t)(n * m > 0 ? n * m : 1));
+  if (!a || !b) {
+    free(a);
+    free(b);
+    return 2;
+  }
+  const double *src = X;
+  for (int s = 1; s <= steps; s++) {
+    double *dst = s == steps ? Y : (s & 1 ? a : b);
+    spmm_once(n, rp, ci, v, m, src, dst);
+    src = dst;
+  }
+  free(a);
+  free(b);
+  return 0;
+}

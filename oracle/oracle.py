@@ -106,6 +106,8 @@ def _L():
         lib.or_spgemm.argtypes = [C.c_int64, P, P, P, P, P, P, C.c_double, C.c_double, C.c_int]
         lib.or_add.restype = P
         lib.or_add.argtypes = [C.c_int64, P, P, P, P, P, P]
+        lib.or_spmm.restype = C.c_int
+        lib.or_spmm.argtypes = [C.c_int64, P, P, P, C.c_int64, P, P, C.c_int]
         lib.or_result_nnz.restype = C.c_int64
         lib.or_result_nnz.argtypes = [P]
         lib.or_result_n.restype = C.c_int64
@@ -214,6 +216,19 @@ def add(A: CSR, B: CSR) -> CSR:
         return _take_result(R)
     finally:
         lib.or_result_free(R)
+
+
+def spmm(A: CSR, X: np.ndarray, steps: int = 1) -> np.ndarray:
+    """N1 apply: Y = A^steps X for a dense X (n x m or n), row order of or_spmm."""
+    lib = _L()
+    X = np.asarray(X, dtype=np.float64)
+    vec = X.ndim == 1
+    X2 = np.ascontiguousarray(X.reshape(A.n, -1))
+    Y = np.zeros_like(X2)
+    rc = lib.or_spmm(A.n, *map(_p, _csr_args(A)), X2.shape[1], _p(X2), _p(Y), int(steps))
+    if rc != 0:
+        raise ValueError(f"or_spmm status {rc}")
+    return Y.reshape(-1) if vec else Y
 
 
 def norm_one(H: CSR) -> float:

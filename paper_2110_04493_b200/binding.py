@@ -25,7 +25,8 @@ EXPORTED = [
     "sexpm_nccl_comm_destroy", "sexpm_plan", "sexpm_plan_host", "sexpm_run",
     "sexpm_result_copy", "sexpm_stats_get", "sexpm_destroy", "sexpm_last_error",
     "sexpm_filtered_product", "sexpm_alg41", "sexpm_halo_ranges", "sexpm_partition_rows",
-    "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache",
+    "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache", "sexpm_apply",
+    "sexpm_spmm",
 ]
 
 
@@ -283,6 +284,12 @@ class Plan:
     def run_only(self) -> CsrOut:
         return sexpm_run(self.h)
 
+    def apply(self, X, steps: int = 1, Y=None):
+        """Y = R^steps X on the device (R = the last result, E by default): X a float64 CUDA
+        tensor of shape (n, m) (or (n,)), row stride >= m.  Returns Y (new tensor unless
+        given)."""
+        return sexpm_apply(self.h, X, steps, Y)
+
     def stats(self) -> dict:
         return sexpm_stats_get(self.h)
 
@@ -383,6 +390,46 @@ def sexpm_filtered_product(n, A, B, self_coef, divisor, eps_g, kernel=0):
     va = torch.empty(max(out.nnz, 1), dtype=torch.float64, device=dev)
     sexpm_result_copy(h, rp.data_ptr(), ci.data_ptr(), va.data_ptr())
     return (rp, ci[:out.nnz], va[:out.nnz]), passes.value, tau.value, nu.value
+
+
+def _dense2(X):
+    if X.dim() == 1:
+        return X.view(-1, 1)
+    return X
+
+
+def sexpm_apply(h, X, steps: int = 1, Y=None):
+    """Y = R^steps X (sexpm_apply); X, Y float64 CUDA tensors (n, m), rows contiguous."""
+    torch = _torch()
+    X2 = _dense2(X)
+    if X2.dtype != torch.float64 or X2.stride(1) != 1:
+        raise ValueError("X must be float64 with contiguous rows")
+    if Y is None:
+        Y = torch.empty_like(X2, memory_format=torch.contiguous_format)
+    Y2 = _dense2(Y)
+    _check(lib().sexpm_apply(h, C.c_int64(X2.shape[1]), C.c_void_p(X2.data_ptr()),
+                             C.c_int64(X2.stride(0)), C.c_void_p(Y2.data_ptr()),
+                             C.c_int64(Y2.stride(0)), C.c_int32(int(steps))))
+    return Y.view(X.shape) if X.dim() == 1 else Y
+
+
+def sexpm_spmm(n, A, X, Y=None, kernel=0):
+    """Y = A X for a device CSR A = (rowptr, col, val) of an n x n matrix and a float64 CUDA
+    tensor X (n, m) (the kernel of sexpm_apply)."""
+    torch = _torch()
+    h = _context(kernel)
+    Ai = _csr_in(n, *A)
+    X2 = _dense2(X)
+    if X2.dtype != torch.float64 or X2.stride(1) != 1:
+        raise ValueError("X must be float64 with contiguous rows")
+    rows = A[0].numel() - 1
+    if Y is None:
+        Y = torch.empty((rows, X2.shape[1]), dtype=torch.float64, device=X2.device)
+    Y2 = _dense2(Y)
+    _check(lib().sexpm_spmm(h, C.byref(Ai), C.c_int64(X2.shape[1]), C.c_void_p(X2.data_ptr()),
+                            C.c_int64(X2.stride(0)), C.c_void_p(Y2.data_ptr()),
+                            C.c_int64(Y2.stride(0))))
+    return Y.view(-1) if X.dim() == 1 else Y
 
 
 def sexpm_alg41(x, eps_g: float, e_r: float = 0.1):

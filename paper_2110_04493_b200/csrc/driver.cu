@@ -446,6 +446,7 @@ struct sexpm_plan_s {
     if (bg_st) cudaStreamDestroy(bg_st);
   }
   bool have_result = false;
+  DBuf<double> apply_buf[2];  // sexpm_apply's intermediate steps
   int M = 0, N = 0, normal = 0, M_eff = 0;
   double norm = 0.0, a = 0.0, eps_g0 = 0.0;
   long double r0 = 0.0L;
@@ -2094,6 +2095,52 @@ int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *
     CK(cudaMemcpyAsync(colidx, p->E.col.p, p->E.nnz * sizeof(int32_t), cudaMemcpyDefault, p->st));
     CK(cudaMemcpyAsync(vals, p->E.val.p, p->E.nnz * sizeof(double), cudaMemcpyDefault, p->st));
   }
+  CK(cudaStreamSynchronize(p->st));
+  ABI_END
+}
+
+int sexpm_apply(sexpm_plan_t p, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                int32_t steps) {
+  ABI_BEGIN
+  REQUIRE(p, SEXPM_EINVAL, "null plan");
+  REQUIRE(p->have_result, SEXPM_ESTATE, "no result: call sexpm_run first");
+  REQUIRE(p->world == 1, SEXPM_EINVAL, "sexpm_apply is single-GPU (multi-GPU needs X halos)");
+  REQUIRE(m >= 0 && steps >= 1 && ldx >= m && ldy >= m, SEXPM_EINVAL, "bad m / ld / steps");
+  REQUIRE(m == 0 || (X && Y), SEXPM_EINVAL, "null X or Y");
+  const int64_t n = p->E.nrows;
+  REQUIRE(m == 0 || X + (n - 1) * ldx + m <= Y || Y + (n - 1) * ldy + m <= X, SEXPM_EINVAL,
+          "X and Y overlap");
+  if (m == 0 || n == 0) return SEXPM_OK;
+  const CsrView Ev = p->E.view();
+  const double *src = X;
+  int64_t lds = ldx;
+  for (int s = 1; s <= steps; s++) {
+    double *dst = Y;
+    int64_t ldd = ldy;
+    if (s < steps) {
+      DBuf<double> &b = p->apply_buf[s & 1];
+      b.ensure((size_t)n * (size_t)m, p->st);
+      dst = b.p;
+      ldd = m;
+    }
+    launch_spmm(Ev, m, src, lds, dst, ldd, p->st);
+    CK(cudaGetLastError());
+    src = dst;
+    lds = ldd;
+  }
+  CK(cudaStreamSynchronize(p->st));
+  ABI_END
+}
+
+int sexpm_spmm(sexpm_plan_t p, const sexpm_csr_in *A, int64_t m, const double *X, int64_t ldx,
+               double *Y, int64_t ldy) {
+  ABI_BEGIN
+  REQUIRE(p && A, SEXPM_EINVAL, "null argument");
+  REQUIRE(m >= 0 && ldx >= m && ldy >= m, SEXPM_EINVAL, "bad m / ld");
+  REQUIRE(m == 0 || (X && Y), SEXPM_EINVAL, "null X or Y");
+  const CsrView Av = view_of(A);
+  launch_spmm(Av, m, X, ldx, Y, ldy, p->st);
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(p->st));
   ABI_END
 }

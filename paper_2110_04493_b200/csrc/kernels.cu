@@ -4855,3 +4855,72 @@ void launch_rebase_rowptr(const int64_t *src, int64_t cnt, int64_t base, int64_t
 }
 
 }  // namespace sx
+
+namespace sx {
+// ------------------------------------------------------------------------------------
+// N1 apply: Y = A X for a CSR A and a dense row-major X (ldx >= m), the
+// product that advances the discretised system by one step, u_{k+1} = e^H u_k (Eq. 2.2
+// P:54).  One warp per row of A.  The warp's lanes form 32/W groups of W lanes;
+// lane c of a group owns columns c, c + W, ... (CT per tile) and group g takes the row's
+// entries g, g + 32/W, ...; the groups' partial sums are combined by a fixed xor tree.  With
+// W = 32 (m >= 32) a lane adds its columns' products over the row's entries in ascending
+// column order, y = y + a_rk x_kj (_rn, no contraction) -- the oracle's order, bit for bit.
+// A row's entries are loaded 32 at a time and broadcast by shuffles; X rows are read as
+// contiguous W * 8-byte segments.
+// ------------------------------------------------------------------------------------
+template <int W, int CT>
+__global__ void __launch_bounds__(256) k_spmm(CsrView A, int64_t m, const double *X, int64_t ldx,
+                                              double *Y, int64_t ldy) {
+  constexpr int G = 32 / W;
+  const int lane = threadIdx.x & 31, g = lane / W, c = lane % W;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < A.nrows; r += nw) {
+    const int64_t p0 = A.rp[r], p1 = A.rp[r + 1];
+    for (int64_t c0 = 0; c0 < m; c0 += (int64_t)W * CT) {
+      double acc[CT];
+#pragma unroll
+      for (int t = 0; t < CT; t++) acc[t] = 0.0;
+      for (int64_t pb = p0; pb < p1; pb += 32) {
+        const int nb = (int)(p1 - pb < 32 ? p1 - pb : 32);
+        const int32_t kc = lane < nb ? A.col[pb + lane] : 0;
+        const double kv = lane < nb ? A.val[pb + lane] : 0.0;
+        for (int e0 = 0; e0 < nb; e0 += G) {
+          const int e = e0 + g;
+          const bool ok = e < nb;
+          const int64_t k = __shfl_sync(FULL_MASK, kc, ok ? e : 0);
+          const double a = __shfl_sync(FULL_MASK, kv, ok ? e : 0);
+          if (ok) {
+            const double *xr = X + k * ldx + c0 + c;
+#pragma unroll
+            for (int t = 0; t < CT; t++)
+              if (c0 + c + (int64_t)W * t < m) acc[t] = __dadd_rn(acc[t], __dmul_rn(a, xr[W * t]));
+          }
+        }
+      }
+#pragma unroll
+      for (int o = W; o < 32; o <<= 1)
+#pragma unroll
+        for (int t = 0; t < CT; t++) acc[t] = __dadd_rn(acc[t], __shfl_xor_sync(FULL_MASK, acc[t], o));
+      if (g == 0) {
+#pragma unroll
+        for (int t = 0; t < CT; t++)
+          if (c0 + c + (int64_t)W * t < m) Y[r * ldy + c0 + c + W * t] = acc[t];
+      }
+    }
+  }
+}
+
+void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                 cudaStream_t st) {
+  if (A.nrows == 0 || m == 0) return;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((A.nrows + 7) / 8, 148 * 16));
+  KL;
+  if (m >= 64) k_spmm<32, 4><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else if (m > 16) k_spmm<32, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else if (m > 8) k_spmm<16, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else if (m > 4) k_spmm<8, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else if (m > 2) k_spmm<4, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else if (m > 1) k_spmm<2, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else k_spmm<1, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+}
+}  // namespace sx

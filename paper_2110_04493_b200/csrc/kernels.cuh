@@ -241,6 +241,10 @@ void launch_merge_staged_write(const CsrView &A, const int64_t *alen, const int6
                                double tau, const int64_t *rp_out, int32_t *col_out, double *val_out,
                                int64_t *len_out, const int64_t *s_rp, int32_t *s_col, double *s_val,
                                cudaStream_t st);
+// N1 apply: Y = A X, A CSR (rows A.nrows, global columns), X dense row-major (rows = A's
+// column range, ldx >= m), Y row-major (A.nrows x m, ldy >= m)
+void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                 cudaStream_t st);
 void launch_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
                        int64_t *out, cudaStream_t st);
 // identity rows for rows [row0, row0+nrows)
