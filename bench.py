@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--plan-norm", default="one", choices=["one", "fro"])
     ap.add_argument("--eps-tol", type=float, default=1e-16)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-apply", action="store_true", help="skip the N1 apply measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-grid", type=int, default=0)
     return ap.parse_args()
@@ -290,6 +291,44 @@ def main():
                    "note": "sexpm_plan_host (H2D of H from pinned memory) + sexpm_run + "
                            "sexpm_result_copy (D2H of E into pinned memory), wall clock"}
 
+    # ---------------- N1 apply: Y = E X on the device ----------------
+    # one e^H, then Y = E X for a seeded dense X of m columns; CUDA events around each call
+    # (E = 14.6 GB >> L2, L2 flushed anyway); compulsory bytes = E + rowptr + X + Y
+    apply_res = None
+    peaks0 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    if world == 1 and not args.no_apply:
+        p = B.Plan(n, rp, ci, va, args.eps_tol, stream=stream, **opts)
+        p.run_only()
+        nnzE = int(p.stats()["nnz_out"])
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(20211010)
+        apply_res = {"kernel": "k_spmm (warp per row, lanes over columns)", "nnz_E": nnzE}
+        for m in (1, 64):
+            X = torch.randn((n, m), dtype=torch.float64, device=dev, generator=gen)
+            Y = torch.empty_like(X)
+            p.apply(X, Y=Y)
+            ts = []
+            for _ in range(5):
+                l2_flush.zero_()
+                torch.cuda.synchronize()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                p.apply(X, Y=Y)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            ms = sorted(ts)[len(ts) // 2]
+            byts = 12.0 * nnzE + 8.0 * (n + 1) + 16.0 * n * m
+            fl = 2.0 * nnzE * m
+            hp = peaks0.get("hbm_gbs", 6650.0)
+            apply_res[f"m{m}"] = {"ms": ms, "hbm_gbs_compulsory": byts / ms / 1e6,
+                                  "hbm_frac": byts / ms / 1e6 / hp,
+                                  "fp64_tflops": fl / ms / 1e9, "fp64_frac": fl / ms / 1e9 / FP64_PEAK_TFLOPS}
+            del X, Y
+        p.close()
+
     # ---------------- roofline of the dominant kernel ----------------
     import math
     sq_ms = [float(st["sq_kernel_ms"][i]) for i in range(1, N + 1)]
@@ -360,6 +399,7 @@ def main():
                          for j in range(len(stats))],
         "gpu_launches": int(launches),
         "e2e": e2e,
+        "apply": apply_res,
     }
     if rank == 0:
         line["clocks"] = clk.summary()

@@ -4880,10 +4880,16 @@ __global__ void __launch_bounds__(256) k_spmm(CsrView A, int64_t m, const double
       double acc[CT];
 #pragma unroll
       for (int t = 0; t < CT; t++) acc[t] = 0.0;
+      int32_t kcn = p0 + lane < p1 ? A.col[p0 + lane] : 0;  // entries prefetched a chunk ahead
+      double kvn = p0 + lane < p1 ? A.val[p0 + lane] : 0.0;
       for (int64_t pb = p0; pb < p1; pb += 32) {
         const int nb = (int)(p1 - pb < 32 ? p1 - pb : 32);
-        const int32_t kc = lane < nb ? A.col[pb + lane] : 0;
-        const double kv = lane < nb ? A.val[pb + lane] : 0.0;
+        const int32_t kc = kcn;
+        const double kv = kvn;
+        if (pb + 32 + lane < p1) {
+          kcn = A.col[pb + 32 + lane];
+          kvn = A.val[pb + 32 + lane];
+        }
         for (int e0 = 0; e0 < nb; e0 += G) {
           const int e = e0 + g;
           const bool ok = e < nb;
@@ -4915,7 +4921,8 @@ void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, doub
   if (A.nrows == 0 || m == 0) return;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((A.nrows + 7) / 8, 148 * 16));
   KL;
-  if (m >= 64) k_spmm<32, 4><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  if (m > 64) k_spmm<32, 4><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else if (m > 32) k_spmm<32, 2><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
   else if (m > 16) k_spmm<32, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
   else if (m > 8) k_spmm<16, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
   else if (m > 4) k_spmm<8, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
