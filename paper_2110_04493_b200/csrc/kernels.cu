@@ -4890,6 +4890,7 @@ __global__ void __launch_bounds__(256) k_spmm(CsrView A, int64_t m, const double
           kcn = A.col[pb + 32 + lane];
           kvn = A.val[pb + 32 + lane];
         }
+#pragma unroll 8
         for (int e0 = 0; e0 < nb; e0 += G) {
           const int e = e0 + g;
           const bool ok = e < nb;
