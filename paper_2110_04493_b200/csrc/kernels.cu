@@ -4021,7 +4021,7 @@ int taylor_dia_smem_bytes(int slots) {
   return kDWarps * (slots * 8 + kDPageWords * 4 + kDPageWords * 2 + (slots >> 3) * 2 + 16);
 }
 
-template <int MAXD>  // compile-time bound on the number of diagonals (>= D.ndiag)
+template <int MAXD, bool EXACT>  // bound on the number of diagonals (EXACT: == D.ndiag)
 __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaView D, int slots,
                                                              int32_t *fail_rows, int *fail_count) {
   extern __shared__ double dsm[];
@@ -4038,7 +4038,7 @@ __global__ void __launch_bounds__(kDWarps * 32) k_taylor_dia(NumericArgs a, DiaV
   for (int i = lane; i < slots; i += 32) acc[i] = 0.0;
   for (int i = lane; i < kDPageWords; i += 32) pbits[i] = 0u;
   __syncthreads();
-  const int nd = D.ndiag;
+  const int nd = EXACT ? MAXD : D.ndiag;
   const int32_t dmin = D.dmin, dmax = D.dmax;
   const int n = (int)D.n;  // columns are int32: every column index below fits 32 bits
   unsigned long long prods = 0;
@@ -4247,7 +4247,13 @@ void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_
                        int *fail_count, cudaStream_t st) {
   if (a.A.nrows == 0 || a.nlist == 0) return;
   const int smem = taylor_dia_smem_bytes(slots);
-  auto kf = D.ndiag <= 4 ? k_taylor_dia<4> : (D.ndiag <= 8 ? k_taylor_dia<8> : k_taylor_dia<16>);
+  // grid stencils (3 / 5 / 7 offsets in 1D / 2D / 3D) get loops of their exact length
+  auto kf = D.ndiag == 3   ? k_taylor_dia<3, true>
+            : D.ndiag == 5 ? k_taylor_dia<5, true>
+            : D.ndiag == 7 ? k_taylor_dia<7, true>
+            : D.ndiag <= 4 ? k_taylor_dia<4, false>
+            : D.ndiag <= 8 ? k_taylor_dia<8, false>
+                           : k_taylor_dia<16, false>;
   cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
   kf<<<a.grid, kDWarps * 32, smem, st>>>(a, D, slots, fail_rows, fail_count);
