@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--eps-tol", type=float, default=1e-16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-apply", action="store_true", help="skip the N1 apply measurement")
+    ap.add_argument("--no-n2", action="store_true", help="skip the N2 filter-off comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-grid", type=int, default=0)
     return ap.parse_args()
@@ -329,6 +330,36 @@ def main():
             del X, Y
         p.close()
 
+    # ---------------- N2: what the filter saves ----------------
+    # BASELINE config 2 (n = 10^4) with the paper's filter and with it off (the unfiltered
+    # PIM: every eps_g = 0): nnz per squaring, device time; config 5 unfiltered would need
+    # ~10^4 entries per row (bandwidth doubling per squaring, Table 3's unfiltered row).
+    n2 = None
+    if world == 1 and not args.no_n2:
+        H2 = make_config(2)
+        r2 = [torch.from_numpy(a).to(dev) for a in (H2.rowptr, H2.col, H2.val)]
+        n2 = {"workload": "BASELINE config 2 (2D heat 100x100, perturbed), eps_tol 1e-16"}
+        for name, flt in (("filtered", 1), ("unfiltered", 0)):
+            ts = []
+            reps = 3 if flt else 1  # the unfiltered run takes seconds: one pass
+            for rep_i in range(reps):
+                p = B.Plan(H2.n, *r2, args.eps_tol, stream=stream, filter=flt, **opts)
+                b0 = torch.cuda.Event(enable_timing=True)
+                b1 = torch.cuda.Event(enable_timing=True)
+                b0.record(stream)
+                p.run_only()
+                b1.record(stream)
+                torch.cuda.synchronize()
+                s2 = p.stats()
+                p.close()
+                if rep_i or reps == 1:
+                    ts.append(b0.elapsed_time(b1))
+            N2 = int(s2["N"])
+            n2[name] = {"ms": min(ts), "nnz_E": int(s2["nnz_out"]),
+                        "sq_nnz": [int(x) for x in s2["sq_nnz"][0:N2 + 1]],
+                        "sq_bandwidth_l1": [int(x) for x in s2["sq_l1"][0:N2 + 1]],
+                        "sq_fmas": float(sum(s2["sq_fmas"][1:N2 + 1]))}
+
     # ---------------- roofline of the dominant kernel ----------------
     import math
     sq_ms = [float(st["sq_kernel_ms"][i]) for i in range(1, N + 1)]
@@ -400,6 +431,7 @@ def main():
         "gpu_launches": int(launches),
         "e2e": e2e,
         "apply": apply_res,
+        "n2_filter_off": n2,
     }
     if rank == 0:
         line["clocks"] = clk.summary()
