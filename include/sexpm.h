@@ -107,6 +107,11 @@ typedef struct {
                              oracle's C~ bit for bit.  Rows a kernel cannot hold fall
                              through 8-12 -> 5 -> 3, 7 -> 7 at twice the accumulator slots
                              -> 5 -> 3, 6 -> 1 -> 3 and 1/4/5 -> 3. */
+  int32_t ssat;           /* 0 = the paper's PIM (default); 1 = the SSAT baseline of Table 1
+                             (SURVEY section 8(f) N2): the same Taylor phase
+                             (filtered per `filter`), then E_0 = I + T^_0 and N plain
+                             squarings E_i = E_{i-1}^2 without the incremental split and
+                             without filtering.  Incompatible with output_T (SEXPM_EINVAL). */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */

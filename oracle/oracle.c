@@ -421,6 +421,7 @@ typedef struct {
   int32_t force_M, force_N; /* -1 = use Eq. (4.20) */
   int32_t output_T;       /* 1 = return T^_N, 0 = E = I + T^_N */
   int32_t nthreads;
+  int32_t ssat;           /* 1 = SSAT baseline (Table 1): E_0 = I + T^_0, E_i = E_{i-1}^2 */
   double e_r;             /* Algorithm 4.1 tolerance (R6: 0.1) */
 } or_options;
 
@@ -490,6 +491,7 @@ or_result *or_expm(int64_t n, const int64_t *rp, const int32_t *ci, const double
   for (int64_t p = 0; p < csr_nnz(&H); p++)
     if (!isfinite(H.val[p])) tr->status = 2;
   if (!(eps_tol >= 1e-16) || !isfinite(eps_tol)) tr->status = 3; /* R13: eps_tol >= u read as 1e-16 */
+  if (o->ssat && o->output_T) tr->status = 2; /* SSAT has no incremental part to return */
   if (tr->status) {
     R->out = csr_alloc(n, 0);
     csr_free(&H);
@@ -566,6 +568,40 @@ or_result *or_expm(int64_t n, const int64_t *rp, const int32_t *ci, const double
   tr->sq_nnz[0] = csr_nnz(&T);
   tr->sq_normIT[0] = norm_fro_I_plus(&T);
   or_bandwidth(n, T.rowptr, T.col, &tr->sq_l1[0], &tr->sq_l2[0]);
+  if (o->ssat) {
+    /* SSAT, the paper's scaling-and-squaring baseline (Table 1 column "SSAT", P:442-451;
+     * SURVEY §8(f) N2): the same Taylor phase, then E_0 = I + T^_0 and N plain squarings
+     * E_i = E_{i-1} E_{i-1} (rows in ascending k, Eq. 2.5's S(H)^2 without the incremental
+     * split of Eq. 2.7), no filter; exact zeros purged (R11). */
+    ocsr I = csr_alloc(n, n);
+    for (int64_t r = 0; r < n; r++) {
+      I.col[r] = (int32_t)r;
+      I.val[r] = 1.0;
+      I.rowptr[r + 1] = r + 1;
+    }
+    ocsr E = csr_add(&T, &I);
+    csr_free(&I);
+    csr_free(&T);
+    for (int i = 1; i <= N; i++) {
+      double fm = count_fmas(&E, &E);
+      ocsr Et = spgemm_rows(&E, &E, 0.0, 1.0, o->nthreads);
+      csr_free(&E);
+      E = Et;
+      int32_t ps;
+      double tau, dr;
+      filter_inplace(&E, 0.0, o->e_r, &ps, &tau, &dr);
+      if (i < OR_MAXSTEP) {
+        tr->sq_nnz_unf[i] = csr_nnz(&E);
+        tr->sq_nnz[i] = csr_nnz(&E);
+        tr->sq_fmas[i] = fm;
+        or_bandwidth(n, E.rowptr, E.col, &tr->sq_l1[i], &tr->sq_l2[i]);
+      }
+    }
+    R->out = E;
+    csr_free(&H);
+    csr_free(&H0);
+    return R;
+  }
   /* Step 4: squarings */
   long double ri = r0;
   for (int i = 1; i <= N; i++) {

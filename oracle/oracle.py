@@ -56,7 +56,7 @@ class _Options(C.Structure):
         ("plan_norm", C.c_int32), ("normal", C.c_int32), ("threshold_mode", C.c_int32),
         ("filter", C.c_int32), ("m_cap", C.c_int32), ("n_window", C.c_int32),
         ("force_M", C.c_int32), ("force_N", C.c_int32), ("output_T", C.c_int32),
-        ("nthreads", C.c_int32), ("e_r", C.c_double),
+        ("nthreads", C.c_int32), ("ssat", C.c_int32), ("e_r", C.c_double),
     ]
 
 
@@ -72,13 +72,14 @@ class Options:
     force_N: int = -1
     output_T: bool = False
     nthreads: int = 1
+    ssat: bool = False            # SSAT baseline (Table 1): E_0 = I + T^_0, E_i = E_{i-1}^2
     e_r: float = 0.1
 
     def to_c(self) -> _Options:
         return _Options(0 if self.plan_norm == "one" else 1, self.normal,
                         0 if self.threshold_mode == "rel_prev" else 1, int(self.filter),
                         self.m_cap, self.n_window, self.force_M, self.force_N,
-                        int(self.output_T), self.nthreads, self.e_r)
+                        int(self.output_T), self.nthreads, int(self.ssat), self.e_r)
 
 
 def _L():

@@ -583,6 +583,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   // product count is bounded by ndiag * nnz(A), a valid K for the floor lemma
   const bool dia_path = self == 0.0 && P.dia_nd > 0 && B.rp == P.H0full.rp.p &&
                         (P.o.kernel == 0 || P.o.kernel == 7);
+  // a squaring (of T^, or of E in the SSAT baseline): A and B are the same matrix (or B its
+  // halo rows), with or without the 2T term
+  const bool sq_like = self != 0.0 || B.rp == A.rp || (P.Bhalo.rp.p && B.rp == P.Bhalo.rp.p);
   int64_t hstat[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   bool have_symbolic = false;
   auto run_symbolic = [&]() {  // K1 symbolic bounds
@@ -611,7 +614,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   // K2 scheduling order: the plan's locality (cluster) order when it covers these rows,
   // else longest-processing-time-first bins
   // the locality order serves the squarings (Taylor terms stream their rows in index order)
-  const bool use_cluster = self != 0.0 && P.proc_order.p && (int64_t)P.proc_order.n >= nr &&
+  const bool use_cluster = sq_like && P.proc_order.p && (int64_t)P.proc_order.n >= nr &&
                            A.row0 == P.row_begin && nr == P.row_end - P.row_begin;
   if (use_cluster) wait_order(P);
   if (!use_cluster && have_symbolic)
@@ -631,7 +634,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   na.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.numeric_blocks_per_sm));
   na.cursor_cap = std::max<int64_t>(hstat[6], 1);
   na.scr_cap = std::max<int64_t>(hstat[1], 1);
-  int64_t cap = std::max<int64_t>(w.pool_cap_hint, (self != 0.0 ? 3 : 2) * A.nnz + 2 * nr + 1024);
+  int64_t cap = std::max<int64_t>(w.pool_cap_hint, (sq_like ? 3 : 2) * A.nnz + 2 * nr + 1024);
   double sum_bound = 0;  // exact upper bound
   sum_bound = (double)hstat[0];
   if ((double)cap > sum_bound) cap = (int64_t)sum_bound + 1;
@@ -678,11 +681,11 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     const bool group_ok = ((uintptr_t)B.col % 16 == 0) && ((uintptr_t)B.val % 16 == 0);
     // squarings: the k-synchronous paged kernel (measured fastest on configs 2, 3 and 5;
     // the grouped kernels 8 / 9 are options)
-    if (kern == 0) kern = self != 0.0 ? 11 : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
+    if (kern == 0) kern = sq_like ? 11 : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
     if (kern == 8 && !group_ok) kern = 5;
     // the block kernel squares one matrix held whole on this GPU (its BSR view is A's);
     // Taylor terms keep their own kernels
-    if ((kern == 11 || kern == 12) && self == 0.0) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 1);
+    if ((kern == 11 || kern == 12) && !sq_like) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 1);
     if ((kern == 11 || kern == 12) && (P.world > 1 || B.rp != A.rp)) kern = 5;
     if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 1;
     if (kern == 6 && !taylor_pull_ok) kern = 1;
@@ -1752,6 +1755,19 @@ static void do_run(sexpm_plan_s &P) {
     S.sq_nnz[0] = (int64_t)allsum(P, (double)T.nnz);
   }
   // ---- squarings ----
+  const bool ssat = P.o.ssat != 0;
+  if (ssat && P.N >= 1) {  // SSAT baseline: E_0 = I + T^_0, then E_i = E_{i-1}^2 (no filter)
+    DCsr &I = P.Ibuf;
+    I.nrows = nl;
+    I.row0 = P.row_begin;
+    I.nnz = nl;
+    I.rp.ensure((size_t)nl + 1, st);
+    I.col.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    I.val.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    launch_identity(nl, P.row_begin, I.rp.p, I.col.p, I.val.p, st);
+    merge_add(P, T.view(), I.view(), Tn);
+    swap_csr(T, Tn);
+  }
   long double ri = P.r0;
   double normIT = S.sq_normIT[0];
   int64_t l1 = S.sq_l1[0], l2 = S.sq_l2[0];
@@ -1760,16 +1776,17 @@ static void do_run(sexpm_plan_s &P) {
     ri = 2.0L * ri;  // r_i = 2 r_{i-1}
     double eps_g = P.o.threshold_mode == 1 ? (double)((long double)P.a * ri)
                                            : (double)((long double)P.a * ri * (long double)normIT);
-    if (!P.o.filter) eps_g = 0.0;
+    if (!P.o.filter || ssat) eps_g = 0.0;
     StepReport rep;
     // last squaring: E = I + T^_N is written by its compaction, no separate merge
-    const bool fuse_I = (i == P.N) && !P.o.output_T;
+    const bool fuse_I = (i == P.N) && !P.o.output_T && !ssat;
     DCsr &dst = fuse_I ? P.E : Tn;
+    const double self = ssat ? 0.0 : 2.0;  // T~ = 2T + T^2 (Eq. 4.15), or E^2 (SSAT)
     if (P.world == 1) {
-      filtered_product(P, T.view(), T.view(), 2.0, 1.0, eps_g, dst, rep, nullptr, fuse_I);
+      filtered_product(P, T.view(), T.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
     } else {
       exchange_halo(P, T, l1, l2, P.Bhalo);
-      filtered_product(P, T.view(), P.Bhalo.view(), 2.0, 1.0, eps_g, dst, rep, nullptr, fuse_I);
+      filtered_product(P, T.view(), P.Bhalo.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
     }
     const double ms = step_ms();
     if (i < SEXPM_MAXSTEP) {
@@ -1804,7 +1821,9 @@ static void do_run(sexpm_plan_s &P) {
   }
   CK(cudaEventRecord(ev_sq, st));
   // ---- e^H = I + T^_N ----
-  if (P.N >= 1 && !P.o.output_T) {
+  if (ssat && P.N >= 1) {
+    copy_csr(P, T.view(), P.E);  // E_N of the SSAT baseline
+  } else if (P.N >= 1 && !P.o.output_T) {
     // already written by the last squaring's compaction
   } else if (P.o.output_T) {
     copy_csr(P, T.view(), P.E);
@@ -1900,6 +1919,7 @@ int sexpm_options_init(sexpm_options *o) {
   o->output_T = 0;
   o->window_cols = 0;
   o->kernel = 0;
+  o->ssat = 0;
   o->e_r = 0.1;
   o->stream = nullptr;
   o->nccl_comm = nullptr;
@@ -1937,6 +1957,7 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
   sexpm_plan_s *P = new sexpm_plan_s();
   if (o) {
     REQUIRE(o->struct_size == sizeof(sexpm_options), SEXPM_EINVAL, "sexpm_options ABI mismatch");
+    REQUIRE(!(o->ssat && o->output_T), SEXPM_EINVAL, "ssat has no incremental part T to return");
     P->o = *o;
   } else {
     sexpm_options_init(&P->o);
