@@ -12,6 +12,7 @@ from .oracle import (  # noqa: F401
     expm,
     spgemm,
     spmm,
+    rcm,
     add,
     norm_one,
     norm_fro,

@@ -732,3 +732,153 @@ int or_spmm(int64_t n, const int64_t *rp, const int32_t *ci, const double *v, in
   free(b);
   return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* N3 reordering: reverse Cuthill-McKee, the standard      */
+/* heuristic for the real bandwidth lambda(A) = min_P l(P A P^T) of Def. 3.2a */
+/* (P:134-136), whose computation is NP-hard.  Graph: the pattern of A + A^T */
+/* without the diagonal.  Deterministic rules (the GPU follows the same):    */
+/*  - components are started in ascending order of their smallest-degree,   */
+/*    smallest-index unvisited node (isolated nodes are components too);     */
+/*  - the start node is pseudo-peripheral (George-Liu): BFS from the        */
+/*    candidate, take the last level's smallest-degree, smallest-index node,  */
+/*    repeat while the number of levels grows;                               */
+/*  - Cuthill-McKee: BFS levels in order; inside level L+1 the nodes are      */
+/*    ordered by (smallest CM position of a neighbour in level L, degree,     */
+/*    index);                                                                */
+/*  - the whole CM sequence is reversed.  perm[new] = old.                   */
+/* Pinned by tests/test_oracle_rcm.py (a permutation; bandwidth of banded   */
+/* matrices under random relabelling restored; vs scipy's RCM bandwidth).   */
+/* ------------------------------------------------------------------------- */
+static int bfs_levels(int64_t n, const int64_t *rp, const int32_t *ci, int64_t s,
+                      int32_t *level, int64_t *queue, int64_t *qlen) {
+  /* level[] must be -1 on the component; returns the number of levels */
+  int64_t head = 0, tail = 0;
+  queue[tail++] = s;
+  level[s] = 0;
+  int maxl = 0;
+  while (head < tail) {
+    int64_t v = queue[head++];
+    for (int64_t p = rp[v]; p < rp[v + 1]; p++) {
+      int64_t u = ci[p];
+      if (level[u] < 0) {
+        level[u] = level[v] + 1;
+        if (level[u] > maxl) maxl = level[u];
+        queue[tail++] = u;
+      }
+    }
+  }
+  *qlen = tail;
+  (void)n;
+  return maxl + 1;
+}
+
+int or_rcm(int64_t n, const int64_t *rp0, const int32_t *ci0, int64_t *perm) {
+  /* symmetric pattern G = pattern(A + A^T) minus the diagonal, rows sorted */
+  int64_t nnz = rp0[n];
+  int64_t *cnt = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  for (int64_t r = 0; r < n; r++)
+    for (int64_t p = rp0[r]; p < rp0[r + 1]; p++)
+      if (ci0[p] != r) {
+        cnt[r + 1]++;
+        cnt[ci0[p] + 1]++;
+      }
+  for (int64_t r = 0; r < n; r++) cnt[r + 1] += cnt[r];
+  int32_t *adj = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cnt[n] > 0 ? cnt[n] : 1));
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t r = 0; r < n; r++) fill[r] = cnt[r];
+  for (int64_t r = 0; r < n; r++)
+    for (int64_t p = rp0[r]; p < rp0[r + 1]; p++)
+      if (ci0[p] != r) {
+        adj[fill[r]++] = ci0[p];
+        adj[fill[ci0[p]]++] = (int32_t)r;
+      }
+  /* sort + dedupe each row */
+  int64_t *rp = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  int64_t w = 0;
+  for (int64_t r = 0; r < n; r++) {
+    int64_t b = cnt[r], e = fill[r];
+    qsort(adj + b, (size_t)(e - b), sizeof(int32_t), cmp_i32);
+    rp[r] = w;
+    for (int64_t p = b; p < e; p++)
+      if (p == b || adj[p] != adj[p - 1]) adj[w++] = adj[p];
+  }
+  rp[n] = w;
+  (void)nnz;
+  int64_t *deg = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t r = 0; r < n; r++) deg[r] = rp[r + 1] - rp[r];
+  int32_t *level = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  int32_t *done = (int32_t *)calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
+  int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t *cm = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t *pos = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t ncm = 0;
+  for (int64_t r = 0; r < n; r++) level[r] = -1;
+  for (;;) {
+    /* next component: smallest (degree, index) among unplaced nodes */
+    int64_t s = -1;
+    for (int64_t r = 0; r < n; r++)
+      if (!done[r] && (s < 0 || deg[r] < deg[s])) s = r;
+    if (s < 0) break;
+    /* pseudo-peripheral start (George-Liu) */
+    int64_t qlen;
+    int nl = bfs_levels(n, rp, adj, s, level, queue, &qlen);
+    for (;;) {
+      int64_t c = -1;
+      for (int64_t q = 0; q < qlen; q++) {
+        int64_t v = queue[q];
+        if (level[v] == nl - 1 && (c < 0 || deg[v] < deg[c] || (deg[v] == deg[c] && v < c))) c = v;
+      }
+      for (int64_t q = 0; q < qlen; q++) level[queue[q]] = -1;
+      int64_t ql2;
+      int nl2 = bfs_levels(n, rp, adj, c, level, queue, &ql2);
+      if (nl2 > nl) {
+        s = c;
+        nl = nl2;
+        qlen = ql2;
+      } else {
+        for (int64_t q = 0; q < ql2; q++) level[queue[q]] = -1;
+        bfs_levels(n, rp, adj, s, level, queue, &qlen);
+        break;
+      }
+    }
+    /* Cuthill-McKee over the levels of s */
+    int64_t lstart = ncm;
+    cm[ncm] = s;
+    pos[s] = ncm;
+    ncm++;
+    for (int L = 1; L < nl; L++) {
+      int64_t b = ncm;
+      for (int64_t q = 0; q < qlen; q++) {
+        int64_t v = queue[q];
+        if (level[v] == L) cm[ncm++] = v;
+      }
+      /* insertion sort by (key, degree, index), key = smallest CM position of a neighbour
+       * in level L-1: plain and obviously correct */
+      for (int64_t a = b + 1; a < ncm; a++) {
+        int64_t v = cm[a];
+        int64_t j = a - 1;
+        while (j >= b) {
+          int64_t u = cm[j];
+          int64_t ku = INT64_MAX, kv = INT64_MAX;
+          for (int64_t p = rp[u]; p < rp[u + 1]; p++)
+            if (level[adj[p]] == L - 1 && pos[adj[p]] < ku) ku = pos[adj[p]];
+          for (int64_t p = rp[v]; p < rp[v + 1]; p++)
+            if (level[adj[p]] == L - 1 && pos[adj[p]] < kv) kv = pos[adj[p]];
+          int gt = ku > kv || (ku == kv && (deg[u] > deg[v] || (deg[u] == deg[v] && u > v)));
+          if (!gt) break;
+          cm[j + 1] = u;
+          j--;
+        }
+        cm[j + 1] = v;
+      }
+      for (int64_t a = b; a < ncm; a++) pos[cm[a]] = a;
+    }
+    for (int64_t a = lstart; a < ncm; a++) done[cm[a]] = 1;
+    for (int64_t a = lstart; a < ncm; a++) level[cm[a]] = -1;
+  }
+  for (int64_t a = 0; a < n; a++) perm[a] = cm[n - 1 - a];
+  free(cnt); free(adj); free(fill); free(rp); free(deg); free(level); free(done); free(queue);
+  free(cm); free(pos);
+  return 0;
+}

@@ -108,6 +108,8 @@ def _L():
         lib.or_add.restype = P
         lib.or_add.argtypes = [C.c_int64, P, P, P, P, P, P]
         lib.or_spmm.restype = C.c_int
+        lib.or_rcm.restype = C.c_int
+        lib.or_rcm.argtypes = [C.c_int64, P, P, P]
         lib.or_spmm.argtypes = [C.c_int64, P, P, P, C.c_int64, P, P, C.c_int]
         lib.or_result_nnz.restype = C.c_int64
         lib.or_result_nnz.argtypes = [P]
@@ -230,6 +232,15 @@ def spmm(A: CSR, X: np.ndarray, steps: int = 1) -> np.ndarray:
     if rc != 0:
         raise ValueError(f"or_spmm status {rc}")
     return Y.reshape(-1) if vec else Y
+
+
+def rcm(H: CSR) -> np.ndarray:
+    """N3: reverse Cuthill-McKee permutation of pattern(H + H^T) (perm[new] = old), the
+    deterministic rules of or_rcm."""
+    rp, ci, _ = _csr_args(H)
+    perm = np.zeros(max(H.n, 1), np.int64)
+    _L().or_rcm(H.n, _p(rp), _p(ci), _p(perm))
+    return perm[:H.n]
 
 
 def norm_one(H: CSR) -> float:
