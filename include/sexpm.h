@@ -112,6 +112,11 @@ typedef struct {
                              (filtered per `filter`), then E_0 = I + T^_0 and N plain
                              squarings E_i = E_{i-1}^2 without the incremental split and
                              without filtering.  Incompatible with output_T (SEXPM_EINVAL). */
+  int32_t reorder;        /* 0 = none (default); 1 = reverse Cuthill-McKee on the device
+                             (Def. 3.2a's real bandwidth):
+                             the plan computes a permutation P of pattern(H + H^T), runs on
+                             P H P^T and returns E = P^T E' P in the caller's order
+                             (e^{PHP^T} = P e^H P^T).  Single GPU; nnz < 2^31. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */
@@ -241,6 +246,11 @@ int sexpm_filtered_product(sexpm_plan_t p, const sexpm_csr_in *A, const sexpm_cs
  * eps_g == 0) and the dropped Frobenius norm. */
 int sexpm_alg41(sexpm_plan_t p, const double *x, int64_t cnt, double eps_g, double e_r,
                 int32_t *passes, double *tau, double *dropped);
+
+/* N3: the reverse Cuthill-McKee permutation (perm[new] = old) of pattern(A + A^T) for a
+ * device CSR A holding all n rows, as option `reorder` computes it (rules in DESIGN.md and
+ * oracle or_rcm).  perm: n int64, host or device.  Runs on the plan's stream; synchronises. */
+int sexpm_rcm(sexpm_plan_t p, const sexpm_csr_in *A, int64_t *perm);
 
 /* Y = A X for any device CSR A (rows row_begin..row_end of an n x n matrix, global column
  * indices) and dense device X (n x m, row-major, ldx >= m) into Y (rows of A x m, ldy >= m):

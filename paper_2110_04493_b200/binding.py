@@ -26,7 +26,7 @@ EXPORTED = [
     "sexpm_result_copy", "sexpm_stats_get", "sexpm_destroy", "sexpm_last_error",
     "sexpm_filtered_product", "sexpm_alg41", "sexpm_halo_ranges", "sexpm_partition_rows",
     "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache", "sexpm_apply",
-    "sexpm_spmm",
+    "sexpm_spmm", "sexpm_rcm",
 ]
 
 
@@ -53,7 +53,7 @@ class Options(C.Structure):
                 ("threshold_mode", C.c_int32), ("filter", C.c_int32), ("m_cap", C.c_int32),
                 ("n_window", C.c_int32), ("force_M", C.c_int32), ("force_N", C.c_int32),
                 ("output_T", C.c_int32), ("window_cols", C.c_int32), ("kernel", C.c_int32),
-                ("ssat", C.c_int32), ("e_r", C.c_double),
+                ("ssat", C.c_int32), ("reorder", C.c_int32), ("e_r", C.c_double),
                 ("stream", C.c_void_p), ("nccl_comm", C.c_void_p)]
 
 
@@ -430,6 +430,16 @@ def sexpm_spmm(n, A, X, Y=None, kernel=0):
                             C.c_int64(X2.stride(0)), C.c_void_p(Y2.data_ptr()),
                             C.c_int64(Y2.stride(0))))
     return Y.view(-1) if X.dim() == 1 else Y
+
+
+def sexpm_rcm(n, A):
+    """Reverse Cuthill-McKee permutation (perm[new] = old) of a device CSR (all n rows)."""
+    torch = _torch()
+    h = _context()
+    Ai = _csr_in(n, *A)
+    perm = torch.empty(max(int(n), 1), dtype=torch.int64, device=A[0].device)
+    _check(lib().sexpm_rcm(h, C.byref(Ai), C.c_void_p(perm.data_ptr())))
+    return perm[:int(n)]
 
 
 def sexpm_alg41(x, eps_g: float, e_r: float = 0.1):

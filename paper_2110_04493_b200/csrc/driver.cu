@@ -447,6 +447,9 @@ struct sexpm_plan_s {
   }
   bool have_result = false;
   DBuf<double> apply_buf[2];  // sexpm_apply's intermediate steps
+  // N3 reordering (option reorder = 1): perm[new] = old, inv[old] = new; H in RCM order
+  DBuf<int64_t> perm, inv;
+  DCsr Hperm, Etmp;
   int M = 0, N = 0, normal = 0, M_eff = 0;
   double norm = 0.0, a = 0.0, eps_g0 = 0.0;
   long double r0 = 0.0L;
@@ -1407,6 +1410,151 @@ static void build_diagonals(sexpm_plan_s &P) {
   CK(cudaStreamSynchronize(st));  // offs (host) is captured by value in the launch
 }
 
+// ------------------------------------------------------------------------------------
+// N3: reverse Cuthill-McKee of pattern(H + H^T) on the device, the
+// oracle's rules (or_rcm): isolated nodes first in index order, then components from their
+// smallest (degree, index) node, pseudo-peripheral start (George-Liu), Cuthill-McKee levels
+// ordered by (smallest position of a neighbour in the previous level, degree, index), the
+// whole sequence reversed.  Host loop over BFS levels, one d2h per level.
+// ------------------------------------------------------------------------------------
+static void permute_csr(sexpm_plan_s &P, const CsrView &A, const int64_t *rowmap, const int64_t *colmap,
+                        DCsr &C) {
+  cudaStream_t st = P.st;
+  Workspace &w = P.ws;
+  const int64_t n = A.nrows;
+  REQUIRE(A.nnz < INT32_MAX, SEXPM_EINVAL, "reorder: nnz must be < 2^31 (segmented sort)");
+  w.cnt.ensure((size_t)std::max<int64_t>(n, 1), st);
+  w.scan_tmp.ensure((size_t)scan_tmp_elems(n) + 1, st);
+  C.nrows = n;
+  C.row0 = 0;
+  C.nnz = A.nnz;
+  C.padded = false;
+  C.rp.ensure((size_t)n + 1, st);
+  C.col.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
+  C.val.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
+  launch_perm_count(A.rp, rowmap, n, w.cnt.p, st);
+  launch_exclusive_scan(w.cnt.p, n, C.rp.p, w.scan_tmp.p, st);
+  DBuf<int32_t> ctmp;
+  DBuf<double> vtmp;
+  ctmp.alloc((size_t)std::max<int64_t>(A.nnz, 1), st);
+  vtmp.alloc((size_t)std::max<int64_t>(A.nnz, 1), st);
+  launch_perm_write(A, rowmap, colmap, n, C.rp.p, ctmp.p, vtmp.p, st);
+  const size_t tb = seg_sort_temp_bytes(A.nnz, n, C.rp.p);
+  DBuf<unsigned char> tmp;
+  tmp.alloc(tb + 256, st);
+  launch_seg_sort(ctmp.p, C.col.p, vtmp.p, C.val.p, A.nnz, n, C.rp.p, tmp.p, tb, st);
+  CK(cudaGetLastError());
+}
+
+static void compute_rcm(sexpm_plan_s &P, const CsrView &H, DBuf<int64_t> &perm, DBuf<int64_t> &inv) {
+  cudaStream_t st = P.st;
+  Workspace &w = P.ws;
+  const int64_t n = H.nrows;
+  const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+  // G = pattern(H + H^T): the merge of H's and H^T's rows with positive stand-in values
+  DCsr HT;
+  build_transpose(P, H, n, HT);
+  DBuf<double> v1, v2;
+  v1.alloc((size_t)std::max<int64_t>(H.nnz, 1), st);
+  v2.alloc((size_t)std::max<int64_t>(H.nnz, 1), st);
+  CK(cudaMemsetAsync(v1.p, 0x3F, std::max<int64_t>(H.nnz, 1) * sizeof(double), st));
+  CK(cudaMemsetAsync(v2.p, 0x3F, std::max<int64_t>(H.nnz, 1) * sizeof(double), st));
+  CsrView Hv = H, Tv = HT.view();
+  Hv.val = v1.p;
+  Tv.val = v2.p;
+  DCsr G;
+  merge_add(P, Hv, Tv, G);
+  const CsrView Gv = G.view();
+  DBuf<int32_t> deg, level, ids, ids2;
+  DBuf<int64_t> queue, pos, cm, flag, rank;
+  DBuf<int8_t> done;
+  DBuf<unsigned long long> key, key2, keyv, tail, mn;
+  deg.alloc(n1, st);
+  level.alloc(n1, st);
+  ids.alloc(n1, st);
+  ids2.alloc(n1, st);
+  queue.alloc(n1, st);
+  pos.alloc(n1, st);
+  cm.alloc(n1, st);
+  flag.alloc(n1, st);
+  rank.alloc(n1, st);
+  done.alloc(n1, st);
+  key.alloc(n1, st);
+  key2.alloc(n1, st);
+  keyv.alloc(n1, st);
+  tail.alloc(1, st);
+  mn.alloc(1, st);
+  const size_t tb = cm_sort_temp_bytes(n);
+  DBuf<unsigned char> tmp;
+  tmp.alloc(tb + 256, st);
+  launch_degree_nodiag(Gv, deg.p, st);
+  CK(cudaMemsetAsync(level.p, 0xFF, n1 * sizeof(int32_t), st));  // -1: unvisited
+  CK(cudaMemsetAsync(done.p, 0, n1, st));
+  w.scan_tmp.ensure((size_t)scan_tmp_elems(n) + 1, st);
+  launch_isolated(deg.p, n, flag.p, rank.p, w.scan_tmp.p, 0, pos.p, cm.p, done.p, st);
+  w.i64tmp.ensure(8, st);
+  launch_reduce_sum_i64(flag.p, n, w.i64tmp.p + 0, st);
+  int64_t placed = d2h(w.i64tmp.p + 0, st);
+  launch_mark_done(cm.p, 0, placed, done.p, level.p, st);
+  std::vector<int64_t> loff;
+  auto bfs = [&](int64_t s) -> int {  // levels from s; loff = level boundaries in queue
+    const int32_t zero = 0;
+    CK(cudaMemcpyAsync(level.p + s, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(queue.p, &s, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    const unsigned long long one = 1;
+    CK(cudaMemcpyAsync(tail.p, &one, sizeof(one), cudaMemcpyHostToDevice, st));
+    loff.assign({0, 1});
+    int64_t a = 0, b = 1;
+    for (int32_t L = 0; b > a; L++) {
+      launch_bfs_expand(Gv, queue.p, a, b, level.p, L, tail.p, st);
+      const int64_t nb = (int64_t)d2h(tail.p, st);
+      a = b;
+      b = nb;
+      if (b > a) loff.push_back(b);
+    }
+    return (int)loff.size() - 1;
+  };
+  auto argmin = [&](const int64_t *q, int64_t a, int64_t b, const int8_t *dn) -> int64_t {
+    const unsigned long long init = ~0ull;
+    CK(cudaMemcpyAsync(mn.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    launch_min_deg(q, a, b, deg.p, dn, mn.p, st);
+    return (int64_t)(d2h(mn.p, st) & 0xFFFFFFFFull);
+  };
+  while (placed < n) {
+    int64_t s = argmin(nullptr, 0, n, done.p);
+    int nl = bfs(s);
+    for (;;) {  // George-Liu pseudo-peripheral node
+      const int64_t c = argmin(queue.p, loff[nl - 1], loff[nl], nullptr);
+      const int64_t qlen = loff[nl];
+      launch_reset_level(queue.p, 0, qlen, level.p, st);
+      const int nl2 = bfs(c);
+      if (nl2 > nl) {
+        s = c;
+        nl = nl2;
+      } else {
+        launch_reset_level(queue.p, 0, loff[nl2], level.p, st);
+        nl = bfs(s);
+        break;
+      }
+    }
+    const int64_t qlen = loff[nl];
+    CK(cudaMemcpyAsync(pos.p + s, &placed, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(cm.p + placed, &s, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    for (int L = 1; L < nl; L++) {
+      const int64_t a = loff[L], b = loff[L + 1];
+      launch_cm_key(Gv, queue.p, a, b, level.p, L - 1, pos.p, deg.p, key.p, ids.p, st);
+      launch_cm_sort_place(key.p, ids.p, b - a, key2.p, ids2.p, keyv.p, tmp.p, tb, placed + a, pos.p,
+                           cm.p, st);
+    }
+    launch_mark_done(cm.p, placed, placed + qlen, done.p, level.p, st);
+    placed += qlen;
+  }
+  perm.ensure(n1, st);
+  inv.ensure(n1, st);
+  launch_reverse_perm(cm.p, n, perm.p, inv.p, st);
+  CK(cudaStreamSynchronize(st));
+}
+
 static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   cudaStream_t st = P.st;
   REQUIRE(H->n >= 1, SEXPM_EINVAL, "n must be >= 1");
@@ -1454,6 +1602,19 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   REQUIRE(!(vf & 8), SEXPM_ENONFINITE, "H holds a non-finite value");
   REQUIRE(!(vf & 7), SEXPM_EINVAL, "malformed CSR (rowptr / column range / column order)");
   mark("validate");
+  sexpm_csr_in Hp_in;
+  if (P.o.reorder) {  // N3: work on P H P^T (RCM order); do_run maps E back
+    REQUIRE(P.world == 1, SEXPM_EINVAL, "reorder is single-GPU (the RCM needs all of H)");
+    compute_rcm(P, L, P.perm, P.inv);
+    permute_csr(P, L, P.perm.p, P.inv.p, P.Hperm);  // row i <- row perm[i], col c -> inv[c]
+    Hp_in = *H;
+    Hp_in.rowptr = P.Hperm.rp.p;
+    Hp_in.colidx = P.Hperm.col.p;
+    Hp_in.vals = P.Hperm.val.p;
+    H = &Hp_in;
+    L = view_of(H);
+    mark("reorder (RCM)");
+  }
   // rank partition
   std::vector<double> rb;
   double mine[2] = {(double)P.row_begin, (double)P.row_end};
@@ -1861,6 +2022,11 @@ static void do_run(sexpm_plan_s &P) {
     S.cache_bytes_cached = cache::bytes_cached;
     S.cache_bytes_allocated = cache::bytes_allocated;
   }
+  if (P.o.reorder) {  // N3: E = P^T E' P (row r <- row inv[r], col c' -> perm[c'])
+    permute_csr(P, P.E.view(), P.inv.p, P.perm.p, P.Etmp);
+    swap_csr(P.E, P.Etmp);
+    CK(cudaStreamSynchronize(st));
+  }
   for (cudaEvent_t e : {ev_start, ev_taylor, ev_sq, ev_end, a0, a1}) cudaEventDestroy(e);
   P.have_result = true;
 }
@@ -1920,6 +2086,7 @@ int sexpm_options_init(sexpm_options *o) {
   o->window_cols = 0;
   o->kernel = 0;
   o->ssat = 0;
+  o->reorder = 0;
   o->e_r = 0.1;
   o->stream = nullptr;
   o->nccl_comm = nullptr;
@@ -2149,6 +2316,18 @@ int sexpm_apply(sexpm_plan_t p, int64_t m, const double *X, int64_t ldx, double 
     src = dst;
     lds = ldd;
   }
+  CK(cudaStreamSynchronize(p->st));
+  ABI_END
+}
+
+int sexpm_rcm(sexpm_plan_t p, const sexpm_csr_in *A, int64_t *perm) {
+  ABI_BEGIN
+  REQUIRE(p && A && perm, SEXPM_EINVAL, "null argument");
+  REQUIRE(A->row_begin == 0 && A->row_end == A->n, SEXPM_EINVAL, "sexpm_rcm needs all rows");
+  const CsrView Av = view_of(A);
+  DBuf<int64_t> pm, iv;
+  compute_rcm(*p, Av, pm, iv);
+  if (A->n) CK(cudaMemcpyAsync(perm, pm.p, A->n * sizeof(int64_t), cudaMemcpyDefault, p->st));
   CK(cudaStreamSynchronize(p->st));
   ABI_END
 }

@@ -4938,3 +4938,248 @@ void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, doub
   else k_spmm<1, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
 }
 }  // namespace sx
+
+namespace sx {
+// ------------------------------------------------------------------------------------
+// N3 reordering: reverse Cuthill-McKee on the device for the real
+// bandwidth of Def. 3.2a.  The host (driver.cu `compute_rcm`) runs the level
+// loop; these kernels do the per-level work: BFS expansion over the symmetric pattern G,
+// the (degree, index) minimum of a node set, the Cuthill-McKee key of a level (smallest
+// position of a neighbour in the previous level), and the permutation of a CSR matrix.
+// The tie rules are the oracle's (or_rcm).
+// ------------------------------------------------------------------------------------
+__global__ void k_degree_nodiag(CsrView G, int32_t *deg) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= G.nrows) return;
+  int c = 0;
+  for (int64_t p = G.rp[w] + lane; p < G.rp[w + 1]; p += 32) c += G.col[p] != (int32_t)w;
+  c = __reduce_add_sync(FULL_MASK, c);
+  if (lane == 0) deg[w] = c;
+}
+void launch_degree_nodiag(const CsrView &G, int32_t *deg, cudaStream_t st) {
+  if (G.nrows == 0) return;
+  KL;
+  k_degree_nodiag<<<grid_for(G.nrows * 32, kThreads), kThreads, 0, st>>>(G, deg);
+}
+
+// frontier queue[a, b) at level L: unvisited neighbours get level L + 1 and are appended
+__global__ void k_bfs_expand(CsrView G, int64_t *queue, int64_t a, int64_t b, int32_t *level,
+                             int32_t L, unsigned long long *tail) {
+  const int64_t w = a + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= b) return;
+  const int64_t v = queue[w];
+  for (int64_t p = G.rp[v] + lane; p < G.rp[v + 1]; p += 32) {
+    const int32_t u = G.col[p];
+    if (u != (int32_t)v && atomicCAS(&level[u], -1, L + 1) == -1)
+      queue[atomicAdd(tail, 1ull)] = u;
+  }
+}
+void launch_bfs_expand(const CsrView &G, int64_t *queue, int64_t a, int64_t b, int32_t *level,
+                       int32_t L, unsigned long long *tail, cudaStream_t st) {
+  if (b <= a) return;
+  KL;
+  k_bfs_expand<<<grid_for((b - a) * 32, kThreads), kThreads, 0, st>>>(G, queue, a, b, level, L, tail);
+}
+
+// out = min over queue[a, b) (or over all nodes with !done[v] when queue == nullptr) of
+// deg << 32 | v  (out must hold ~0 before)
+__global__ void k_min_deg(const int64_t *queue, int64_t a, int64_t b, const int32_t *deg,
+                          const int8_t *done, unsigned long long *out) {
+  unsigned long long m = ~0ull;
+  for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = queue ? queue[i] : i;
+    if (!queue && done[v]) continue;
+    const unsigned long long k = ((unsigned long long)(unsigned)deg[v] << 32) | (unsigned long long)v;
+    m = k < m ? k : m;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(FULL_MASK, m, o);
+    m = y < m ? y : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(out, m);
+}
+void launch_min_deg(const int64_t *queue, int64_t a, int64_t b, const int32_t *deg,
+                    const int8_t *done, unsigned long long *out, cudaStream_t st) {
+  if (b <= a) return;
+  KL;
+  k_min_deg<<<grid_for(b - a, kThreads, 148 * 8), kThreads, 0, st>>>(queue, a, b, deg, done, out);
+}
+
+__global__ void k_reset_level(const int64_t *queue, int64_t a, int64_t b, int32_t *level) {
+  for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b;
+       i += (int64_t)gridDim.x * blockDim.x)
+    level[queue[i]] = -1;
+}
+void launch_reset_level(const int64_t *queue, int64_t a, int64_t b, int32_t *level, cudaStream_t st) {
+  if (b <= a) return;
+  KL;
+  k_reset_level<<<grid_for(b - a, kThreads, 148 * 16), kThreads, 0, st>>>(queue, a, b, level);
+}
+
+// level L + 1 = queue[a, b): key = (smallest position of a neighbour in level L) << 32 | degree
+__global__ void k_cm_key(CsrView G, const int64_t *queue, int64_t a, int64_t b, const int32_t *level,
+                         int32_t L, const int64_t *pos, const int32_t *deg, unsigned long long *key,
+                         int32_t *ids) {
+  const int64_t w = a + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= b) return;
+  const int64_t v = queue[w];
+  long long k = LLONG_MAX;
+  for (int64_t p = G.rp[v] + lane; p < G.rp[v + 1]; p += 32) {
+    const int32_t u = G.col[p];
+    if (u != (int32_t)v && level[u] == L) k = min(k, (long long)pos[u]);
+  }
+  for (int o = 16; o; o >>= 1) k = min(k, __shfl_xor_sync(FULL_MASK, k, o));
+  if (lane == 0) {
+    key[w - a] = ((unsigned long long)k << 32) | (unsigned long long)(unsigned)deg[v];
+    ids[w - a] = (int32_t)v;
+  }
+}
+void launch_cm_key(const CsrView &G, const int64_t *queue, int64_t a, int64_t b, const int32_t *level,
+                   int32_t L, const int64_t *pos, const int32_t *deg, unsigned long long *key,
+                   int32_t *ids, cudaStream_t st) {
+  if (b <= a) return;
+  KL;
+  k_cm_key<<<grid_for((b - a) * 32, kThreads), kThreads, 0, st>>>(G, queue, a, b, level, L, pos, deg, key, ids);
+}
+
+// CUB: ids sorted ascending, then stably by key (cm order of one level)
+size_t cm_sort_temp_bytes(int64_t cnt) {
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b1, (const int32_t *)nullptr, (int32_t *)nullptr, (int)cnt);
+  cub::DeviceRadixSort::SortPairs(nullptr, b2, (const unsigned long long *)nullptr,
+                                  (unsigned long long *)nullptr, (const int32_t *)nullptr,
+                                  (int32_t *)nullptr, (int)cnt);
+  return b1 > b2 ? b1 : b2;
+}
+// key of node: keyv[node] scattered then gathered in id order
+__global__ void k_scatter_key(const unsigned long long *key, const int32_t *ids, int64_t cnt,
+                              unsigned long long *keyv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    keyv[ids[i]] = key[i];
+}
+__global__ void k_gather_keyv(const unsigned long long *keyv, const int32_t *ids, int64_t cnt,
+                              unsigned long long *key) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    key[i] = keyv[ids[i]];
+}
+__global__ void k_place_level(const int32_t *ids, int64_t cnt, int64_t base, int64_t *pos, int64_t *cm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    pos[ids[i]] = base + i;
+    cm[base + i] = ids[i];
+  }
+}
+void launch_cm_sort_place(unsigned long long *key, int32_t *ids, int64_t cnt, unsigned long long *key2,
+                          int32_t *ids2, unsigned long long *keyv, void *tmp, size_t tmp_bytes,
+                          int64_t base, int64_t *pos, int64_t *cm, cudaStream_t st) {
+  if (cnt <= 0) return;
+  const int g = (int)std::min<int64_t>((cnt + kThreads - 1) / kThreads, 148 * 16);
+  if (cnt > 1) {
+    KL;
+    k_scatter_key<<<g, kThreads, 0, st>>>(key, ids, cnt, keyv);
+    size_t b = tmp_bytes;
+    KL;
+    cub::DeviceRadixSort::SortKeys(tmp, b, ids, ids2, (int)cnt, 0, 32, st);  // ids ascending
+    KL;
+    k_gather_keyv<<<g, kThreads, 0, st>>>(keyv, ids2, cnt, key2);
+    b = tmp_bytes;
+    KL;
+    cub::DeviceRadixSort::SortPairs(tmp, b, key2, key, ids2, ids, (int)cnt, 0, 64, st);  // stable by key
+  }
+  KL;
+  k_place_level<<<g, kThreads, 0, st>>>(ids, cnt, base, pos, cm);
+}
+
+// nodes of degree 0 in index order, placed from `base` (and marked done)
+__global__ void k_flag_isolated(const int32_t *deg, int64_t n, int64_t *flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = deg[i] == 0;
+}
+__global__ void k_place_isolated(const int32_t *deg, int64_t n, const int64_t *rank, int64_t base,
+                                 int64_t *pos, int64_t *cm, int8_t *done) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (deg[i] == 0) {
+      pos[i] = base + rank[i];
+      cm[base + rank[i]] = i;
+      done[i] = 1;
+    }
+}
+void launch_isolated(const int32_t *deg, int64_t n, int64_t *flag, int64_t *rank, int64_t *scan_tmp,
+                     int64_t base, int64_t *pos, int64_t *cm, int8_t *done, cudaStream_t st) {
+  if (n == 0) return;
+  const int g = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 16);
+  KL;
+  k_flag_isolated<<<g, kThreads, 0, st>>>(deg, n, flag);
+  launch_exclusive_scan(flag, n, rank, scan_tmp, st);
+  KL;
+  k_place_isolated<<<g, kThreads, 0, st>>>(deg, n, rank, base, pos, cm, done);
+}
+__global__ void k_mark_done(const int64_t *cm, int64_t a, int64_t b, int8_t *done, int32_t *level) {
+  for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += (int64_t)gridDim.x * blockDim.x) {
+    done[cm[i]] = 1;
+    level[cm[i]] = -2;  // placed: never visited again
+  }
+}
+void launch_mark_done(const int64_t *cm, int64_t a, int64_t b, int8_t *done, int32_t *level, cudaStream_t st) {
+  if (b <= a) return;
+  KL;
+  k_mark_done<<<grid_for(b - a, kThreads, 148 * 16), kThreads, 0, st>>>(cm, a, b, done, level);
+}
+__global__ void k_reverse_perm(const int64_t *cm, int64_t n, int64_t *perm, int64_t *inv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = cm[n - 1 - i];
+    perm[i] = v;
+    inv[v] = i;
+  }
+}
+void launch_reverse_perm(const int64_t *cm, int64_t n, int64_t *perm, int64_t *inv, cudaStream_t st) {
+  if (n == 0) return;
+  KL;
+  k_reverse_perm<<<grid_for(n, kThreads, 148 * 16), kThreads, 0, st>>>(cm, n, perm, inv);
+}
+
+// C = A permuted: C row i = A row rowmap[i] with columns colmap[c], then rows sorted (CUB)
+__global__ void k_perm_count(const int64_t *arp, const int64_t *rowmap, int64_t n, int64_t *cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = arp[rowmap[i] + 1] - arp[rowmap[i]];
+}
+__global__ void k_perm_write(CsrView A, const int64_t *rowmap, const int64_t *colmap, int64_t n,
+                             const int64_t *rp_out, int32_t *col_out, double *val_out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const int64_t r = rowmap[w], a0 = A.rp[r], len = A.rp[r + 1] - a0, o = rp_out[w];
+  for (int64_t p = lane; p < len; p += 32) {
+    col_out[o + p] = (int32_t)colmap[A.col[a0 + p]];
+    val_out[o + p] = A.val[a0 + p];
+  }
+}
+void launch_perm_count(const int64_t *arp, const int64_t *rowmap, int64_t n, int64_t *cnt, cudaStream_t st) {
+  if (n == 0) return;
+  KL;
+  k_perm_count<<<grid_for(n, kThreads, 148 * 16), kThreads, 0, st>>>(arp, rowmap, n, cnt);
+}
+void launch_perm_write(const CsrView &A, const int64_t *rowmap, const int64_t *colmap, int64_t n,
+                       const int64_t *rp_out, int32_t *col_out, double *val_out, cudaStream_t st) {
+  if (n == 0) return;
+  KL;
+  k_perm_write<<<grid_for(n * 32, kThreads), kThreads, 0, st>>>(A, rowmap, colmap, n, rp_out, col_out, val_out);
+}
+size_t seg_sort_temp_bytes(int64_t nnz, int64_t n, const int64_t *rp) {
+  size_t b = 0;
+  cub::DeviceSegmentedSort::SortPairs(nullptr, b, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                      (const double *)nullptr, (double *)nullptr, (int)nnz, (int)n, rp,
+                                      rp + 1);
+  return b;
+}
+void launch_seg_sort(const int32_t *kin, int32_t *kout, const double *vin, double *vout, int64_t nnz,
+                     int64_t n, const int64_t *rp, void *tmp, size_t tmp_bytes, cudaStream_t st) {
+  if (nnz == 0 || n == 0) return;
+  size_t b = tmp_bytes;
+  KL;
+  cub::DeviceSegmentedSort::SortPairs(tmp, b, kin, kout, vin, vout, (int)nnz, (int)n, rp, rp + 1, st);
+}
+}  // namespace sx

@@ -245,6 +245,30 @@ void launch_merge_staged_write(const CsrView &A, const int64_t *alen, const int6
 // column range, ldx >= m), Y row-major (A.nrows x m, ldy >= m)
 void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
                  cudaStream_t st);
+// N3 reverse Cuthill-McKee (driver.cu compute_rcm runs the level loop)
+void launch_degree_nodiag(const CsrView &G, int32_t *deg, cudaStream_t st);
+void launch_bfs_expand(const CsrView &G, int64_t *queue, int64_t a, int64_t b, int32_t *level,
+                       int32_t L, unsigned long long *tail, cudaStream_t st);
+void launch_min_deg(const int64_t *queue, int64_t a, int64_t b, const int32_t *deg,
+                    const int8_t *done, unsigned long long *out, cudaStream_t st);
+void launch_reset_level(const int64_t *queue, int64_t a, int64_t b, int32_t *level, cudaStream_t st);
+void launch_cm_key(const CsrView &G, const int64_t *queue, int64_t a, int64_t b, const int32_t *level,
+                   int32_t L, const int64_t *pos, const int32_t *deg, unsigned long long *key,
+                   int32_t *ids, cudaStream_t st);
+size_t cm_sort_temp_bytes(int64_t cnt);
+void launch_cm_sort_place(unsigned long long *key, int32_t *ids, int64_t cnt, unsigned long long *key2,
+                          int32_t *ids2, unsigned long long *keyv, void *tmp, size_t tmp_bytes,
+                          int64_t base, int64_t *pos, int64_t *cm, cudaStream_t st);
+void launch_isolated(const int32_t *deg, int64_t n, int64_t *flag, int64_t *rank, int64_t *scan_tmp,
+                     int64_t base, int64_t *pos, int64_t *cm, int8_t *done, cudaStream_t st);
+void launch_mark_done(const int64_t *cm, int64_t a, int64_t b, int8_t *done, int32_t *level, cudaStream_t st);
+void launch_reverse_perm(const int64_t *cm, int64_t n, int64_t *perm, int64_t *inv, cudaStream_t st);
+void launch_perm_count(const int64_t *arp, const int64_t *rowmap, int64_t n, int64_t *cnt, cudaStream_t st);
+void launch_perm_write(const CsrView &A, const int64_t *rowmap, const int64_t *colmap, int64_t n,
+                       const int64_t *rp_out, int32_t *col_out, double *val_out, cudaStream_t st);
+size_t seg_sort_temp_bytes(int64_t nnz, int64_t n, const int64_t *rp);
+void launch_seg_sort(const int32_t *kin, int32_t *kout, const double *vin, double *vout, int64_t nnz,
+                     int64_t n, const int64_t *rp, void *tmp, size_t tmp_bytes, cudaStream_t st);
 void launch_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
                        int64_t *out, cudaStream_t st);
 // identity rows for rows [row0, row0+nrows)
