@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-apply", action="store_true", help="skip the N1 apply measurement")
     ap.add_argument("--no-n2", action="store_true", help="skip the N2 filter-off comparison")
+    ap.add_argument("--no-n3", action="store_true", help="skip the N3 reordering comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-grid", type=int, default=0)
     return ap.parse_args()
@@ -360,6 +361,41 @@ def main():
                         "sq_bandwidth_l1": [int(x) for x in s2["sq_l1"][0:N2 + 1]],
                         "sq_fmas": float(sum(s2["sq_fmas"][1:N2 + 1]))}
 
+    # ---------------- N3: reordering a scrambled input ----------------
+    # BASELINE config 3 (structural, n = 1.8e5) under a seeded random relabelling: e^H as
+    # given and with option reorder (device RCM, run on P H P^T, E mapped back)
+    n3 = None
+    if world == 1 and not args.no_n3:
+        import scipy.sparse as sps
+        H3 = make_config(3)
+        q = np.random.default_rng(20211010).permutation(H3.n)
+        A3 = sps.csr_matrix((H3.val, H3.col, H3.rowptr), shape=(H3.n, H3.n))[q][:, q].tocsr()
+        A3.sort_indices()
+        r3 = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in
+              (A3.indptr.astype(np.int64), A3.indices.astype(np.int32), A3.data.astype(np.float64))]
+        n3 = {"workload": "BASELINE config 3 (structural 300x300, n = 180000) under a random relabelling"}
+        for name, ro in (("as_given", 0), ("reorder_rcm", 1)):
+            ts, tp = [], []
+            for rep_i in range(2):
+                b0 = torch.cuda.Event(enable_timing=True)
+                b1 = torch.cuda.Event(enable_timing=True)
+                b2 = torch.cuda.Event(enable_timing=True)
+                b0.record(stream)
+                p = B.Plan(H3.n, *r3, args.eps_tol, stream=stream, reorder=ro, **opts)
+                b1.record(stream)
+                p.run_only()
+                b2.record(stream)
+                torch.cuda.synchronize()
+                s3 = p.stats()
+                p.close()
+                if rep_i:
+                    ts.append(b0.elapsed_time(b2))
+                    tp.append(b0.elapsed_time(b1))
+            N3 = int(s3["N"])
+            n3[name] = {"ms_plan_plus_run": min(ts), "ms_plan": min(tp), "nnz_E": int(s3["nnz_out"]),
+                        "bandwidth_l1_T0": int(s3["sq_l1"][0]),
+                        "sq_fallback_rows": [int(x) for x in s3["sq_fallback_rows"][1:N3 + 1]]}
+
     # ---------------- roofline of the dominant kernel ----------------
     import math
     sq_ms = [float(st["sq_kernel_ms"][i]) for i in range(1, N + 1)]
@@ -432,6 +468,7 @@ def main():
         "e2e": e2e,
         "apply": apply_res,
         "n2_filter_off": n2,
+        "n3_reorder": n3,
     }
     if rank == 0:
         line["clocks"] = clk.summary()
