@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-apply", action="store_true", help="skip the N1 apply measurement")
     ap.add_argument("--no-n2", action="store_true", help="skip the N2 filter-off comparison")
     ap.add_argument("--no-n3", action="store_true", help="skip the N3 reordering comparison")
+    ap.add_argument("--no-n4", action="store_true", help="skip the N4 graph workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-grid", type=int, default=0)
     return ap.parse_args()
@@ -396,6 +397,38 @@ def main():
                         "bandwidth_l1_T0": int(s3["sq_l1"][0]),
                         "sq_fallback_rows": [int(x) for x in s3["sq_fallback_rows"][1:N3 + 1]]}
 
+    # ---------------- N4: an unstructured graph workload ----------------
+    # communicability e^{beta A} of a random geometric graph (n = 2e5, mean degree 6,
+    # ||H||_1 = 4, random node order), with the device RCM (option reorder) and as given
+    n4 = None
+    if world == 1 and not args.no_n4:
+        from synth import geometric_graph
+        G4 = geometric_graph(200000, 6.0, 4.0, 20211010)
+        r4 = [torch.from_numpy(a).to(dev) for a in (G4.rowptr, G4.col, G4.val)]
+        n4 = {"workload": "random geometric graph n=200000, mean degree 6, H = beta A, ||H||_1 = 4, random node order",
+              "nnz_H": int(G4.nnz)}
+        for name, ro in (("reorder_rcm", 1), ("as_given", 0)):
+            ts = []
+            for rep_i in range(2 if ro else 1):
+                b0 = torch.cuda.Event(enable_timing=True)
+                b1 = torch.cuda.Event(enable_timing=True)
+                b0.record(stream)
+                p = B.Plan(G4.n, *r4, args.eps_tol, stream=stream, reorder=ro, **opts)
+                p.run_only()
+                b1.record(stream)
+                torch.cuda.synchronize()
+                s4 = p.stats()
+                p.close()
+                if rep_i or not ro:
+                    ts.append(b0.elapsed_time(b1))
+                    ph = {"plan": float(s4["ms_plan"]), "taylor": float(s4["ms_taylor"]),
+                          "squaring": float(s4["ms_squaring"])}
+            N4 = int(s4["N"])
+            n4[name] = {"ms_plan_plus_run": min(ts), "phase_ms": ph, "M": int(s4["M"]), "N": N4,
+                        "nnz_E": int(s4["nnz_out"]),
+                        "bandwidth_l1_T0": int(s4["sq_l1"][0]),
+                        "sq_fallback_rows": [int(x) for x in s4["sq_fallback_rows"][1:N4 + 1]]}
+
     # ---------------- roofline of the dominant kernel ----------------
     import math
     sq_ms = [float(st["sq_kernel_ms"][i]) for i in range(1, N + 1)]
@@ -469,6 +502,7 @@ def main():
         "apply": apply_res,
         "n2_filter_off": n2,
         "n3_reorder": n3,
+        "n4_graph": n4,
     }
     if rank == 0:
         line["clocks"] = clk.summary()

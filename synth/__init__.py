@@ -18,6 +18,7 @@ from .configs import (  # noqa: F401
     random_banded,
     random_skew,
     diagonal,
+    geometric_graph,
     dense_to_csr,
     csr_to_dense,
 )

@@ -248,6 +248,24 @@ CONFIGS = {
 }
 
 
+def geometric_graph(n: int, avg_deg: float, norm1: float, seed: int) -> CSR:
+    """N4 workload (§5.3's network matrices): a random
+    geometric graph -- n points uniform in the unit square, an edge between points closer
+    than r with pi r^2 n = avg_deg -- as H = beta A (communicability e^{beta A}), beta set so
+    that ||H||_1 = norm1.  Nodes keep the random order of the points (unstructured input:
+    the bandwidth is ~n until reordered)."""
+    from scipy.spatial import cKDTree
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, 2))
+    r = np.sqrt(avg_deg / (np.pi * n))
+    pairs = cKDTree(pts).query_pairs(r, output_type="ndarray")
+    rows = np.concatenate([pairs[:, 0], pairs[:, 1]])
+    cols = np.concatenate([pairs[:, 1], pairs[:, 0]])
+    deg = np.bincount(rows, minlength=n)
+    beta = norm1 / max(int(deg.max()), 1)
+    return coo_to_csr(n, rows, cols, np.full(len(rows), beta))
+
+
 def make_config(cid: int, seed: int | None = None, scale_down: int | None = None) -> CSR:
     """Build BASELINE.json config `cid` (1..5).  `scale_down` (tests only) shrinks
     the grid side to the given value while keeping the law of the entries."""

@@ -91,3 +91,17 @@ def test_expm_permutation_invariant():
     E2back = permute(E2, inv)
     ok, res = parity(E2back, E1, max(last_tau(tr1), last_tau(tr2)))
     assert ok, res
+
+
+def test_geometric_graph_input_and_rcm():
+    """The N4 input law: symmetric, no diagonal, ||H||_1 = 4 exactly, random node order
+    (bandwidth ~ n); RCM brings the bandwidth within 1.25x of scipy's."""
+    from synth import geometric_graph
+    H = geometric_graph(3000, 6.0, 4.0, 1)
+    A = _sp(H)
+    assert (A != A.T).nnz == 0 and A.diagonal().max() == 0.0
+    assert O.norm_one(H) == pytest.approx(4.0, rel=1e-15)
+    assert bw(H) > H.n // 2
+    p = O.rcm(H)
+    ps = reverse_cuthill_mckee(A, symmetric_mode=True)
+    assert bw(permute(H, p)) <= 1.25 * bw(permute(H, ps)) + 2
