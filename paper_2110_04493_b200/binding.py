@@ -369,13 +369,14 @@ def _context(kernel=0):
     return h
 
 
-def sexpm_filtered_product(n, A, B, self_coef, divisor, eps_g, kernel=0):
-    """One filtered product (K1-K4) on the GPU. A, B = (rowptr, col, val) device tensors.
-    Returns ((rowptr, col, val) tensors, passes, tau, nnz_unf)."""
+def sexpm_filtered_product(n, A, B, self_coef, divisor, eps_g, kernel=0, a_row0=0, b_row0=0):
+    """One filtered product (K1-K4) on the GPU. A, B = (rowptr, col, val) device tensors of
+    rows [a_row0, ...) and [b_row0, ...) of n x n matrices (B must hold every row A's columns
+    reach).  Returns ((rowptr, col, val) tensors of A's rows, passes, tau, nnz_unf)."""
     torch = _torch()
     h = _context(kernel)
-    Ai = _csr_in(n, *A)
-    Bi = _csr_in(n, *B)
+    Ai = _csr_in(n, *A, row_begin=a_row0)
+    Bi = _csr_in(n, *B, row_begin=b_row0)
     out = CsrOut()
     passes = C.c_int32()
     tau = C.c_double()

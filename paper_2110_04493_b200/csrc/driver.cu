@@ -387,7 +387,7 @@ struct Workspace {
   DBuf<int32_t> scr_col, pool_col;
   DBuf<double> scr_val, pool_val;
   DBuf<unsigned long long> pool_used;
-  DBuf<int> row_counter, flags, fail_count;
+  DBuf<int> row_counter, flags, fail_count, eqflag;
   DBuf<int32_t> fail_rows, fail_rows2;
   DBuf<int8_t> ident;
   DBuf<unsigned long long> prof;
@@ -689,7 +689,20 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     // the block kernel squares one matrix held whole on this GPU (its BSR view is A's);
     // Taylor terms keep their own kernels
     if ((kern == 11 || kern == 12) && !sq_like) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 1);
-    if ((kern == 11 || kern == 12) && (P.world > 1 || B.rp != A.rp)) kern = 5;
+    // the block kernel needs B's rows block-aligned and A's rows a block-aligned slice of them
+    // (one GPU: A = B; several: A = the rank's rows inside its halo B, 8-aligned partition)
+    const bool same = B.rp == A.rp;
+    bool bsr_ok = same;
+    if (!same && (kern == 11 || kern == 12) && B.row0 % 8 == 0 && A.row0 >= B.row0 &&
+        (A.row0 - B.row0) % 8 == 0 && A.row0 + nr <= B.row0 + B.nrows) {
+      // A must be a slice of B (the rank's rows inside its halo): checked, not assumed
+      w.eqflag.ensure(1, st);
+      CK(cudaMemsetAsync(w.eqflag.p, 0, sizeof(int), st));
+      launch_rows_equal(A, B, w.eqflag.p, st);
+      bsr_ok = d2h(w.eqflag.p, st) == 0;
+    }
+    if (kern == 11 && !bsr_ok) kern = 5;
+    if (kern == 12 && !(P.world == 1 && bsr_ok && A.row0 == B.row0 && nr == B.nrows)) kern = bsr_ok ? 11 : 5;
     if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 1;
     if (kern == 6 && !taylor_pull_ok) kern = 1;
     if (kern == 7) CK(cudaMemsetAsync(P.dia_prod.p, 0, sizeof(unsigned long long), st));
@@ -761,14 +774,14 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
         } else if (stage == 11 || stage == 12) {
-          // BSR-8 view of A (= B) and its block transpose, then the block kernel over block
-          // rows in index order
-          const int64_t nbr = (nr + 7) / 8, nbc = (P.n + 7) / 8;
+          // BSR-8 view of B (= A, or A's halo rows) and its block transpose, then the block
+          // kernel over A's block rows
+          const int64_t nbr = (B.nrows + 7) / 8, nbc = (P.n + 7) / 8, nbr_a = (nr + 7) / 8;
           w.bcnt.ensure((size_t)nbr + 1, st);
           w.brp.ensure((size_t)nbr + 1, st);
           w.scan_tmp2.ensure((size_t)scan_tmp_elems(std::max(nbr, nbc)) + 1, st);
           CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
-          launch_bsr_count(A, nbr, w.bcnt.p, w.flags.p, st);
+          launch_bsr_count(B, nbr, w.bcnt.p, w.flags.p, st);
           launch_reduce_max_i64(w.bcnt.p, nbr, w.i64tmp.p + 7, st);
           launch_exclusive_scan(w.bcnt.p, nbr, w.brp.p, w.scan_tmp2.p, st);
           int64_t nb = 0, bmax = 0;
@@ -785,7 +798,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           }
           w.bcol.ensure((size_t)std::max<int64_t>(nb, 1), st);
           w.bval.ensure((size_t)std::max<int64_t>(nb, 1) * 64, st);
-          launch_bsr_fill(A, nbr, w.brp.p, w.bcol.p, w.bval.p, w.flags.p, st);
+          launch_bsr_fill(B, nbr, w.brp.p, w.bcol.p, w.bval.p, w.flags.p, st);
           w.tcnt.ensure((size_t)nbc + 1, st);
           w.tp.ensure((size_t)nbc + 1, st);
           w.cnt64.ensure((size_t)nbc + 1, st);
@@ -807,12 +820,15 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           Bv.tp = w.tp.p;
           Bv.tk = w.tk.p;
           Bv.tb = w.tb.p;
-          if (use_cluster && nr == P.row_end - P.row_begin && !getenv("SEXPM_BSR_NATURAL"))
-            Bv.border = P.block_order.p;
+          Bv.nbr_a = nbr_a;
+          Bv.ib0 = (A.row0 - B.row0) / 8;
+          Bv.kb0 = B.row0 / 8;
+          if (use_cluster && nr == P.row_end - P.row_begin && A.row0 % 8 == 0 && !getenv("SEXPM_BSR_NATURAL"))
+            Bv.border = P.block_order.p;  // block rows of the rank's rows in locality order
           if (stage == 12)  // block-row pairs, one 512-thread CTA per SM
             nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nbr + 1) / 2, (int64_t)P.sm_count));
           else
-            nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, (int64_t)P.sm_count * 2));
+            nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbr_a, (int64_t)P.sm_count * 2));
           w.bscr.ensure((size_t)nh.grid * (stage == 12 ? kBsr2ScratchPerCta : kBsrScratchPerCta), st);
           CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
           w.prof.ensure(16, st);
@@ -1153,10 +1169,18 @@ static void allgather_rows(sexpm_plan_s &P, const CsrView &L, DCsr &F) {
   CK(cudaStreamSynchronize(st));
 }
 
+// rows a rank needs for its squaring (Lemma 3.1): [r0 - l2, r1 + l1), widened to multiples of
+// 8 so that the halo matrix is block-aligned for the block kernel K3b (a superset is valid)
+static void halo_need(const int64_t *bounds, int rank, int64_t n, int64_t l1, int64_t l2,
+                      int64_t &need_lo, int64_t &need_hi) {
+  need_lo = std::max<int64_t>(0, ((bounds[rank] - l2) >> 3) << 3);
+  need_hi = std::min<int64_t>(n, ((bounds[rank + 1] + l1 + 7) >> 3) << 3);
+}
+
 static void halo_ranges_host(int world, int rank, const int64_t *bounds, int64_t n, int64_t l1,
                              int64_t l2, int64_t *lo, int64_t *hi) {
-  const int64_t need_lo = std::max<int64_t>(0, bounds[rank] - l2);
-  const int64_t need_hi = std::min<int64_t>(n, bounds[rank + 1] + l1);
+  int64_t need_lo, need_hi;
+  halo_need(bounds, rank, n, l1, l2, need_lo, need_hi);
   for (int h = 0; h < world; h++) {
     int64_t a = std::max(need_lo, bounds[h]), b = std::min(need_hi, bounds[h + 1]);
     if (h == rank || a >= b) a = b = 0;
@@ -1189,8 +1213,8 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
     if (shi[h] > slo[h])
       cnt_send[h] = (double)(rp[shi[h] - T.row0] - rp[slo[h] - T.row0]);
   gather_doubles(P, cnt_send.data(), W, all);  // all[g*W + h] = nnz g sends to h
-  const int64_t need_lo = std::max<int64_t>(0, P.bounds[R] - l2);
-  const int64_t need_hi = std::min<int64_t>(P.n, P.bounds[R + 1] + l1);
+  int64_t need_lo, need_hi;
+  halo_need(P.bounds.data(), R, P.n, l1, l2, need_lo, need_hi);
   // pieces in row order: peers below, me, peers above
   std::vector<int64_t> piece_rows(W, 0), piece_nnz(W, 0);
   for (int h = 0; h < W; h++) {
@@ -2397,6 +2421,7 @@ int sexpm_filtered_product(sexpm_plan_t p, const sexpm_csr_in *A, const sexpm_cs
   REQUIRE(p->world == 1, SEXPM_EINVAL, "component entry points are single-GPU");
   REQUIRE(divisor != 0.0 && isfinite(eps_g) && eps_g >= 0.0, SEXPM_EINVAL, "bad scalars");
   CsrView Av = view_of(A), Bv = view_of(B);
+  p->n = A->n;  // the column dimension (the context plan's own n is that of its 1x1 matrix)
   StepReport rep;
   DCsr out;
   DCsr BT;
@@ -2485,6 +2510,8 @@ int sexpm_partition_rows(int64_t n, const double *work, int world, int64_t *boun
   }
   while (g < world) bounds[g++] = n;
   bounds[world] = n;
+  // interior bounds on multiples of 8: each rank's rows are whole 8-row blocks (K3b)
+  for (int k = 1; k < world; k++) bounds[k] = std::min<int64_t>(n, ((bounds[k] + 4) >> 3) << 3);
   for (int k = 1; k <= world; k++)
     if (bounds[k] < bounds[k - 1]) bounds[k] = bounds[k - 1];
   ABI_END

@@ -3234,11 +3234,11 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
     __syncthreads();
     if (tid == 0) s_I = atomicAdd(a.row_counter, 1);
     __syncthreads();
-    if (s_I >= Bv.nbr) break;
+    if (s_I >= Bv.nbr_a) break;
     const int64_t I = Bv.border ? (int64_t)Bv.border[s_I] : (int64_t)s_I;
     const int64_t r0 = 8 * I;
     const int nr = (int)(nrows - r0 < 8 ? nrows - r0 : 8);
-    const int64_t ab0 = Bv.brp[I], ab1 = Bv.brp[I + 1];
+    const int64_t ab0 = Bv.brp[I + Bv.ib0], ab1 = Bv.brp[I + Bv.ib0 + 1];
     const int na = (int)(ab1 - ab0);
     if (tid == 0) {
       int fail = na > kBACap;
@@ -3307,8 +3307,8 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
     }
     // (2) candidate output blocks: union of the block rows of B at A's block columns
     for (int t = warp; t < na; t += kBWarps) {
-      const int64_t K = aK[t];
-      if (K < Bv.nbr) {
+      const int64_t K = aK[t] - Bv.kb0;  // the view's block row of block column aK[t]
+      if (K >= 0 && K < Bv.nbr) {
         for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
           const int jb = Bv.bcol[b] - jmin;
           if (jb >= 0 && jb < njw * 32) atomicOr(&jbits[jb >> 5], 1u << (jb & 31));
@@ -3376,7 +3376,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
             int ra = -1;
             int64_t bidx = 0;
             if (t < t1) {
-              const int K = Bv.tk[t];
+              const int K = Bv.tk[t] + (int)Bv.kb0;  // global block row
               const int kb = K - kmin;
               if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
                 ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
@@ -3552,7 +3552,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
 
 void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                         int32_t *fail_rows, int *fail_count, cudaStream_t st) {
-  if (Bv.nbr == 0) return;
+  if (Bv.nbr_a == 0) return;
   const int smem = bsr_numeric_smem_bytes();
   cudaFuncSetAttribute(k_numeric_bsr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
@@ -5181,5 +5181,33 @@ void launch_seg_sort(const int32_t *kin, int32_t *kout, const double *vin, doubl
   size_t b = tmp_bytes;
   KL;
   cub::DeviceSegmentedSort::SortPairs(tmp, b, kin, kout, vin, vout, (int)nnz, (int)n, rp, rp + 1, st);
+}
+}  // namespace sx
+
+namespace sx {
+// flag |= 1 unless A's rows are, bit for bit, B's rows A.row0 - B.row0 + r (the block kernel
+// reads A's blocks from B's BSR view: allowed only when A is a slice of B)
+__global__ void k_rows_equal(CsrView A, CsrView B, int *flag) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= A.nrows) return;
+  const int64_t rb = w + A.row0 - B.row0;
+  const int64_t a0 = A.rp[w], na = A.rp[w + 1] - a0;
+  if (rb < 0 || rb >= B.nrows) {
+    if (lane == 0) atomicOr(flag, 1);
+    return;
+  }
+  const int64_t b0 = B.rp[rb], nb = B.rp[rb + 1] - b0;
+  bool diff = na != nb;
+  if (!diff)
+    for (int64_t p = lane; p < na; p += 32)
+      diff |= A.col[a0 + p] != B.col[b0 + p] ||
+              __double_as_longlong(A.val[a0 + p]) != __double_as_longlong(B.val[b0 + p]);
+  if (__any_sync(FULL_MASK, diff) && lane == 0) atomicOr(flag, 1);
+}
+void launch_rows_equal(const CsrView &A, const CsrView &B, int *flag, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  k_rows_equal<<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, B, flag);
 }
 }  // namespace sx

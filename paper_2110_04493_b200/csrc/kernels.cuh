@@ -165,6 +165,10 @@ struct BsrView {
   const int32_t *tk = nullptr;
   const int64_t *tb = nullptr;
   const int32_t *border = nullptr;  // block rows in processing order (locality), or identity
+  // the rows multiplied (A) may be a slice of the view's rows (B, e.g. a rank's rows inside
+  // its halo): A has nbr_a block rows, its block row I is the view's block row I + ib0, and
+  // the view's first block row is global block row kb0 (block columns are global)
+  int64_t nbr_a = 0, ib0 = 0, kb0 = 0;
 };
 constexpr int kBsrScratchPerCta = 512 * 64;  // doubles of output-block scratch per CTA
 constexpr int kBsrMaxRowBlocks = 136;        // blocks of a block row the numeric kernel holds
@@ -269,6 +273,8 @@ void launch_perm_write(const CsrView &A, const int64_t *rowmap, const int64_t *c
 size_t seg_sort_temp_bytes(int64_t nnz, int64_t n, const int64_t *rp);
 void launch_seg_sort(const int32_t *kin, int32_t *kout, const double *vin, double *vout, int64_t nnz,
                      int64_t n, const int64_t *rp, void *tmp, size_t tmp_bytes, cudaStream_t st);
+// flag |= 1 unless A's rows equal (bit for bit) B's rows at offset A.row0 - B.row0
+void launch_rows_equal(const CsrView &A, const CsrView &B, int *flag, cudaStream_t st);
 void launch_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
                        int64_t *out, cudaStream_t st);
 // identity rows for rows [row0, row0+nrows)

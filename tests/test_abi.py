@@ -54,9 +54,11 @@ def test_halo_ranges_cover_needed_rows(world, l1, l2):
     n = 500
     bounds = B.sexpm_partition_rows(n, None, world)
     assert bounds[0] == 0 and bounds[-1] == n and np.all(np.diff(bounds) >= 0)
+    assert all(b % 8 == 0 or b == n for b in bounds)  # whole 8-row blocks per rank
     for g in range(world):
         lo, hi = B.sexpm_halo_ranges(world, g, bounds, n, l1, l2)
-        need = set(range(max(0, bounds[g] - l2), min(n, bounds[g + 1] + l1)))
+        # Lemma 3.1's rows [r0 - l2, r1 + l1), widened to whole 8-row blocks (block kernel)
+        need = set(range(max(0, ((bounds[g] - l2) // 8) * 8), min(n, -(-(bounds[g + 1] + l1) // 8) * 8)))
         have = set(range(bounds[g], bounds[g + 1]))
         for h in range(world):
             rng = set(range(lo[h], hi[h]))
@@ -71,7 +73,7 @@ def test_partition_balances_work():
     w = rng.uniform(1, 3, 10_000)
     b = B.sexpm_partition_rows(len(w), w, 8)
     loads = [w[b[g]:b[g + 1]].sum() for g in range(8)]
-    assert max(loads) <= 1.01 * (w.sum() / 8) + w.max()
+    assert max(loads) <= 1.01 * (w.sum() / 8) + 8 * w.max()  # bounds on multiples of 8
 
 
 def test_compute_without_gpu_fails_loudly():

@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from synth import (csr_to_dense, dense_to_csr, diagonal, laplacian_2d, make_config,
+from synth import (CSR, csr_to_dense, dense_to_csr, diagonal, laplacian_2d, make_config,
                    neumann_laplacian_2d, random_banded, random_skew, tridiag)
 
 from gpu_helpers import NTHREADS, from_dev, last_tau, parity, to_dev
@@ -396,3 +396,27 @@ def test_bsr_kernel_bit_exact_sizes(B, n, kernel):
     G = from_dev(n, rp, ci, va)
     assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
     assert np.array_equal(G.val, Ct.val)
+
+
+@pytest.mark.parametrize("kernel", [11, 0, 5])
+@pytest.mark.parametrize("r0,r1,h0,h1", [(96, 200, 88, 208), (96, 203, 88, 216), (0, 57, 0, 64),
+                                         (100, 180, 88, 192), (200, 257, 192, 257)])
+def test_block_kernel_rank_slice_in_halo(B, kernel, r0, r1, h0, h1):
+    """The multi-GPU shape of a squaring on one GPU: A = rows [r0, r1) of T, B = its halo rows
+    [h0, h1) (Lemma 3.1 coverage).  Block-aligned slices (r0 - h0 and h0 multiples of 8) run
+    the block kernel K3b on B's BSR view, the others fall through to K3p; C~ = 2A + A B is
+    bit-identical to the oracle's rows either way."""
+    n = 257
+    T = _rand_csr(n, 6, 0.5, 900 + r0, empty_rows=(0, 100, 256))
+    Ct = O.spgemm(T, T, 2.0, 1.0)
+    def rows(M, a, b):
+        rp = M.rowptr[a:b + 1] - M.rowptr[a]
+        sl = slice(M.rowptr[a], M.rowptr[b])
+        return CSR(n, rp.astype(np.int64), M.col[sl].copy(), M.val[sl].copy())
+    A_, B_ = rows(T, r0, r1), rows(T, h0, h1)
+    (rp, ci, va), _, _, nnz_unf = B.sexpm_filtered_product(n, to_dev(A_), to_dev(B_), 2.0, 1.0, 0.0,
+                                                           kernel=kernel, a_row0=r0, b_row0=h0)
+    G = from_dev(n, rp, ci, va)
+    Cr = rows(Ct, r0, r1)
+    assert np.array_equal(G.rowptr, Cr.rowptr) and np.array_equal(G.col, Cr.col)
+    assert np.array_equal(G.val, Cr.val)
