@@ -4923,6 +4923,31 @@ __global__ void __launch_bounds__(256) k_spmm(CsrView A, int64_t m, const double
   }
 }
 
+// m = 1 (SpMV): lanes take the row's entries directly (no broadcast), two chunks of 32 in
+// flight per iteration with separate partial sums, then a fixed xor tree (deterministic)
+__global__ void __launch_bounds__(256) k_spmv(CsrView A, const double *X, int64_t ldx, double *Y,
+                                              int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < A.nrows; r += nw) {
+    const int64_t p0 = A.rp[r], p1 = A.rp[r + 1];
+    double s0 = 0.0, s1 = 0.0;
+    int64_t p = p0 + lane;
+    for (; p + 32 < p1; p += 64) {
+      const int32_t k0 = A.col[p], k1 = A.col[p + 32];
+      const double a0 = A.val[p], a1 = A.val[p + 32];
+      const double x0 = X[(int64_t)k0 * ldx], x1 = X[(int64_t)k1 * ldx];
+      s0 = __dadd_rn(s0, __dmul_rn(a0, x0));
+      s1 = __dadd_rn(s1, __dmul_rn(a1, x1));
+    }
+    if (p < p1) s0 = __dadd_rn(s0, __dmul_rn(A.val[p], X[(int64_t)A.col[p] * ldx]));
+    double s = __dadd_rn(s0, s1);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) s = __dadd_rn(s, __shfl_xor_sync(FULL_MASK, s, o));
+    if (lane == 0) Y[r * ldy] = s;
+  }
+}
+
 void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
                  cudaStream_t st) {
   if (A.nrows == 0 || m == 0) return;
@@ -4935,7 +4960,7 @@ void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, doub
   else if (m > 4) k_spmm<8, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
   else if (m > 2) k_spmm<4, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
   else if (m > 1) k_spmm<2, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
-  else k_spmm<1, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
+  else k_spmv<<<grid, 256, 0, st>>>(A, X, ldx, Y, ldy);
 }
 }  // namespace sx
 
