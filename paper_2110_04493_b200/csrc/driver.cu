@@ -1514,12 +1514,132 @@ static void compute_rcm(sexpm_plan_s &P, const CsrView &H, DBuf<int64_t> &perm, 
   launch_degree_nodiag(Gv, deg.p, st);
   CK(cudaMemsetAsync(level.p, 0xFF, n1 * sizeof(int32_t), st));  // -1: unvisited
   CK(cudaMemsetAsync(done.p, 0, n1, st));
-  w.scan_tmp.ensure((size_t)scan_tmp_elems(n) + 1, st);
-  launch_isolated(deg.p, n, flag.p, rank.p, w.scan_tmp.p, 0, pos.p, cm.p, done.p, st);
-  w.i64tmp.ensure(8, st);
-  launch_reduce_sum_i64(flag.p, n, w.i64tmp.p + 0, st);
-  int64_t placed = d2h(w.i64tmp.p + 0, st);
-  launch_mark_done(cm.p, 0, placed, done.p, level.p, st);
+  // components of G on the host (one copy of G's pattern); their order is that of their
+  // smallest (degree, index) node.  Components of up to kRcmHost nodes (isolated nodes,
+  // the many small clusters of a sparse graph) are ordered on the host by the same rules --
+  // each would cost the device loop a dozen launches and syncs per BFS level -- the large
+  // ones on the device.
+  constexpr int64_t kRcmHost = 4096;
+  std::vector<int64_t> hrp((size_t)n + 1);
+  std::vector<int32_t> hcol((size_t)std::max<int64_t>(G.nnz, 1)), hdeg(n1);
+  CK(cudaMemcpyAsync(hrp.data(), G.rp.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (G.nnz) CK(cudaMemcpyAsync(hcol.data(), G.col.p, G.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hdeg.data(), deg.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int32_t> comp(n1, -1), cnodes;  // component id; nodes grouped by component
+  std::vector<int64_t> cstart, cmin;           // start of each component in cnodes; min key
+  cnodes.reserve((size_t)n);
+  for (int64_t v0 = 0; v0 < n; v0++) {
+    if (comp[v0] >= 0) continue;
+    const int32_t c = (int32_t)cstart.size();
+    cstart.push_back((int64_t)cnodes.size());
+    int64_t mk = INT64_MAX;
+    size_t head = cnodes.size();
+    cnodes.push_back((int32_t)v0);
+    comp[v0] = c;
+    while (head < cnodes.size()) {
+      const int32_t v = cnodes[head++];
+      mk = std::min<int64_t>(mk, ((int64_t)hdeg[v] << 32) | v);
+      for (int64_t p = hrp[v]; p < hrp[v + 1]; p++) {
+        const int32_t u = hcol[p];
+        if (u != v && comp[u] < 0) {
+          comp[u] = c;
+          cnodes.push_back(u);
+        }
+      }
+    }
+    cmin.push_back(mk);
+  }
+  const int64_t ncomp = (int64_t)cstart.size();
+  cstart.push_back((int64_t)cnodes.size());
+  std::vector<int64_t> corder((size_t)ncomp);
+  for (int64_t c = 0; c < ncomp; c++) corder[c] = c;
+  std::sort(corder.begin(), corder.end(), [&](int64_t a, int64_t b) { return cmin[a] < cmin[b]; });
+  std::vector<int64_t> hcm((size_t)n1), hpos(n1);
+  std::vector<int32_t> hlev(n1, -1);
+  std::vector<int32_t> q;
+  auto hbfs = [&](int32_t s, std::vector<int64_t> &lo) -> int {  // host BFS levels of s
+    q.clear();
+    q.push_back(s);
+    hlev[s] = 0;
+    lo.assign({0});
+    size_t head = 0;
+    int cur = 0;
+    while (head < q.size()) {
+      const int32_t v = q[head++];
+      if (hlev[v] != cur) {
+        cur = hlev[v];
+        lo.push_back((int64_t)head - 1);
+      }
+      for (int64_t p = hrp[v]; p < hrp[v + 1]; p++) {
+        const int32_t u = hcol[p];
+        if (u != v && hlev[u] < 0) {
+          hlev[u] = hlev[v] + 1;
+          q.push_back(u);
+        }
+      }
+    }
+    lo.push_back((int64_t)q.size());
+    return (int)lo.size() - 1;
+  };
+  auto hreset = [&]() {
+    for (int32_t v : q) hlev[v] = -1;
+  };
+  std::vector<int64_t> hlo;
+  std::vector<std::pair<int64_t, int64_t>> large;  // (component, base) done on the device
+  int64_t base = 0;
+  for (int64_t ci = 0; ci < ncomp; ci++) {
+    const int64_t c = corder[ci], size = cstart[c + 1] - cstart[c];
+    if (size > kRcmHost) {
+      large.push_back({c, base});
+      base += size;
+      continue;
+    }
+    int32_t s0 = (int32_t)(cmin[c] & 0xFFFFFFFF);
+    int nl = hbfs(s0, hlo);
+    for (;;) {  // George-Liu pseudo-peripheral node
+      int32_t cnd = -1;
+      for (int64_t t = hlo[nl - 1]; t < hlo[nl]; t++) {
+        const int32_t v = q[t];
+        if (cnd < 0 || hdeg[v] < hdeg[cnd] || (hdeg[v] == hdeg[cnd] && v < cnd)) cnd = v;
+      }
+      hreset();
+      const int nl2 = hbfs(cnd, hlo);
+      if (nl2 > nl) {
+        s0 = cnd;
+        nl = nl2;
+      } else {
+        hreset();
+        nl = hbfs(s0, hlo);
+        break;
+      }
+    }
+    // Cuthill-McKee over the levels: (smallest position of a neighbour one level up,
+    // degree, index)
+    std::vector<std::tuple<int64_t, int32_t, int32_t>> lv;
+    hcm[base] = s0;
+    hpos[s0] = base;
+    for (int L = 1; L < nl; L++) {
+      lv.clear();
+      for (int64_t t = hlo[L]; t < hlo[L + 1]; t++) {
+        const int32_t v = q[t];
+        int64_t k = INT64_MAX;
+        for (int64_t p = hrp[v]; p < hrp[v + 1]; p++) {
+          const int32_t u = hcol[p];
+          if (u != v && hlev[u] == L - 1) k = std::min(k, hpos[u]);
+        }
+        lv.emplace_back(k, hdeg[v], v);
+      }
+      std::sort(lv.begin(), lv.end());
+      for (size_t t = 0; t < lv.size(); t++) {
+        const int32_t v = std::get<2>(lv[t]);
+        hcm[base + hlo[L] + (int64_t)t] = v;
+        hpos[v] = base + hlo[L] + (int64_t)t;
+      }
+    }
+    hreset();
+    base += size;
+  }
   std::vector<int64_t> loff;
   auto bfs = [&](int64_t s) -> int {  // levels from s; loff = level boundaries in queue
     const int32_t zero = 0;
@@ -1538,14 +1658,15 @@ static void compute_rcm(sexpm_plan_s &P, const CsrView &H, DBuf<int64_t> &perm, 
     }
     return (int)loff.size() - 1;
   };
-  auto argmin = [&](const int64_t *q, int64_t a, int64_t b, const int8_t *dn) -> int64_t {
+  auto argmin = [&](const int64_t *qq, int64_t a, int64_t b, const int8_t *dn) -> int64_t {
     const unsigned long long init = ~0ull;
     CK(cudaMemcpyAsync(mn.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
-    launch_min_deg(q, a, b, deg.p, dn, mn.p, st);
+    launch_min_deg(qq, a, b, deg.p, dn, mn.p, st);
     return (int64_t)(d2h(mn.p, st) & 0xFFFFFFFFull);
   };
-  while (placed < n) {
-    int64_t s = argmin(nullptr, 0, n, done.p);
+  for (auto &cb : large) {  // the large components on the device
+    const int64_t placed = cb.second;
+    int64_t s = (int64_t)(cmin[cb.first] & 0xFFFFFFFF);
     int nl = bfs(s);
     for (;;) {  // George-Liu pseudo-peripheral node
       const int64_t c = argmin(queue.p, loff[nl - 1], loff[nl], nullptr);
@@ -1571,8 +1692,11 @@ static void compute_rcm(sexpm_plan_s &P, const CsrView &H, DBuf<int64_t> &perm, 
                            cm.p, st);
     }
     launch_mark_done(cm.p, placed, placed + qlen, done.p, level.p, st);
-    placed += qlen;
+    // the device's segment into the host order
+    CK(cudaMemcpyAsync(hcm.data() + placed, cm.p + placed, qlen * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   }
+  CK(cudaMemcpyAsync(cm.p, hcm.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
   perm.ensure(n1, st);
   inv.ensure(n1, st);
   launch_reverse_perm(cm.p, n, perm.p, inv.p, st);

@@ -51,6 +51,9 @@ CASES = {
     "diagonal": lambda: diagonal(np.arange(1.0, 9.0)),
     "components": _two_components,
     "n1": lambda: diagonal(np.array([2.0])),
+    # components above the host threshold (4096 nodes) run the device BFS / CM kernels
+    "grid_device": lambda: shuffled(laplacian_2d(80, 70, 1.0), 8),
+    "graph_mixed": lambda: __import__("synth").geometric_graph(20000, 6.0, 4.0, 3),
 }
 
 
