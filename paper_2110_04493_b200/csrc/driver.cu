@@ -1490,7 +1490,7 @@ static void compute_rcm(sexpm_plan_s &P, const CsrView &H, DBuf<int64_t> &perm, 
   merge_add(P, Hv, Tv, G);
   const CsrView Gv = G.view();
   DBuf<int32_t> deg, level, ids, ids2;
-  DBuf<int64_t> queue, pos, cm, flag, rank;
+  DBuf<int64_t> queue, pos, cm;
   DBuf<int8_t> done;
   DBuf<unsigned long long> key, key2, keyv, tail, mn;
   deg.alloc(n1, st);
@@ -1500,8 +1500,6 @@ static void compute_rcm(sexpm_plan_s &P, const CsrView &H, DBuf<int64_t> &perm, 
   queue.alloc(n1, st);
   pos.alloc(n1, st);
   cm.alloc(n1, st);
-  flag.alloc(n1, st);
-  rank.alloc(n1, st);
   done.alloc(n1, st);
   key.alloc(n1, st);
   key2.alloc(n1, st);

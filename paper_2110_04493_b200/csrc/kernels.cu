@@ -5118,30 +5118,6 @@ void launch_cm_sort_place(unsigned long long *key, int32_t *ids, int64_t cnt, un
   k_place_level<<<g, kThreads, 0, st>>>(ids, cnt, base, pos, cm);
 }
 
-// nodes of degree 0 in index order, placed from `base` (and marked done)
-__global__ void k_flag_isolated(const int32_t *deg, int64_t n, int64_t *flag) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    flag[i] = deg[i] == 0;
-}
-__global__ void k_place_isolated(const int32_t *deg, int64_t n, const int64_t *rank, int64_t base,
-                                 int64_t *pos, int64_t *cm, int8_t *done) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (deg[i] == 0) {
-      pos[i] = base + rank[i];
-      cm[base + rank[i]] = i;
-      done[i] = 1;
-    }
-}
-void launch_isolated(const int32_t *deg, int64_t n, int64_t *flag, int64_t *rank, int64_t *scan_tmp,
-                     int64_t base, int64_t *pos, int64_t *cm, int8_t *done, cudaStream_t st) {
-  if (n == 0) return;
-  const int g = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 16);
-  KL;
-  k_flag_isolated<<<g, kThreads, 0, st>>>(deg, n, flag);
-  launch_exclusive_scan(flag, n, rank, scan_tmp, st);
-  KL;
-  k_place_isolated<<<g, kThreads, 0, st>>>(deg, n, rank, base, pos, cm, done);
-}
 __global__ void k_mark_done(const int64_t *cm, int64_t a, int64_t b, int8_t *done, int32_t *level) {
   for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += (int64_t)gridDim.x * blockDim.x) {
     done[cm[i]] = 1;

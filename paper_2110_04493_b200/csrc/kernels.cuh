@@ -263,8 +263,6 @@ size_t cm_sort_temp_bytes(int64_t cnt);
 void launch_cm_sort_place(unsigned long long *key, int32_t *ids, int64_t cnt, unsigned long long *key2,
                           int32_t *ids2, unsigned long long *keyv, void *tmp, size_t tmp_bytes,
                           int64_t base, int64_t *pos, int64_t *cm, cudaStream_t st);
-void launch_isolated(const int32_t *deg, int64_t n, int64_t *flag, int64_t *rank, int64_t *scan_tmp,
-                     int64_t base, int64_t *pos, int64_t *cm, int8_t *done, cudaStream_t st);
 void launch_mark_done(const int64_t *cm, int64_t a, int64_t b, int8_t *done, int32_t *level, cudaStream_t st);
 void launch_reverse_perm(const int64_t *cm, int64_t n, int64_t *perm, int64_t *inv, cudaStream_t st);
 void launch_perm_count(const int64_t *arp, const int64_t *rowmap, int64_t n, int64_t *cnt, cudaStream_t st);
