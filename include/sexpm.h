@@ -37,6 +37,12 @@
  * Errors: every entry point returns an sexpm_status; no exception crosses the ABI;
  * sexpm_last_error() returns a thread-local message for the last non-OK status.
  * Sticky CUDA errors map to SEXPM_ECUDA.
+ *
+ * Diagnostics (environment, read at call time; they change no result): SEXPM_PLAN_LOG
+ * (host phase times of sexpm_plan, synchronising), SEXPM_STEP_LOG (per Taylor term /
+ * squaring: nnz, passes, kernel times, accumulator sizing), SEXPM_CACHE_LOG (device-block
+ * cache traffic), SEXPM_BSR_NATURAL (block kernel in index order instead of the locality
+ * order; for measurements).
  */
 #ifndef SEXPM_H
 #define SEXPM_H
