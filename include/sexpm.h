@@ -123,6 +123,10 @@ typedef struct {
                              the plan computes a permutation P of pattern(H + H^T), runs on
                              P H P^T and returns E = P^T E' P in the caller's order
                              (e^{PHP^T} = P e^H P^T).  Single GPU; nnz < 2^31. */
+  int32_t sq_order;       /* 1 = (default) the squarings run on T^_0 relabelled into 8-row
+                             aggregates of H's graph (fuller 8x8 blocks for K3b), E mapped
+                             back; 0 = index order.  One GPU only; not with ssat.  Results
+                             equal up to rounding order (north-star parity). */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */

@@ -53,7 +53,8 @@ class Options(C.Structure):
                 ("threshold_mode", C.c_int32), ("filter", C.c_int32), ("m_cap", C.c_int32),
                 ("n_window", C.c_int32), ("force_M", C.c_int32), ("force_N", C.c_int32),
                 ("output_T", C.c_int32), ("window_cols", C.c_int32), ("kernel", C.c_int32),
-                ("ssat", C.c_int32), ("reorder", C.c_int32), ("e_r", C.c_double),
+                ("ssat", C.c_int32), ("reorder", C.c_int32), ("sq_order", C.c_int32),
+                ("e_r", C.c_double),
                 ("stream", C.c_void_p), ("nccl_comm", C.c_void_p)]
 
 

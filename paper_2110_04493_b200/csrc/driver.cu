@@ -437,6 +437,11 @@ struct sexpm_plan_s {
   bool order_pending = false;
   std::string bg_err;
   std::vector<int32_t> h_order, h_groups, h_border;
+  // squarings in aggregate order (option sq_order): perm[new] = old, 8-row aggregates of H's
+  // graph; sq_tiled while the iterate is held in that order
+  std::vector<int64_t> h_tperm;
+  DBuf<int64_t> tperm, tinv;
+  bool sq_tiled = false;
   DBuf<int32_t> block_order;  // block rows of the block kernel in locality order
   ~sexpm_plan_s() {
     if (bg.joinable()) bg.join();
@@ -617,7 +622,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   // K2 scheduling order: the plan's locality (cluster) order when it covers these rows,
   // else longest-processing-time-first bins
   // the locality order serves the squarings (Taylor terms stream their rows in index order)
-  const bool use_cluster = sq_like && P.proc_order.p && (int64_t)P.proc_order.n >= nr &&
+  const bool use_cluster = sq_like && !P.sq_tiled && P.proc_order.p && (int64_t)P.proc_order.n >= nr &&
                            A.row0 == P.row_begin && nr == P.row_end - P.row_begin;
   if (use_cluster) wait_order(P);
   if (!use_cluster && have_symbolic)
@@ -1290,6 +1295,33 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
 // bandwidth of T^, Lemma 3.1) stay L2-resident (126 MB) instead of the whole band of
 // lexicographically consecutive rows (~2R grid lines for a 2D stencil).
 // ------------------------------------------------------------------------------------
+// 8-row aggregates of H's graph (greedy BFS from seeds in index order): every 8 consecutive
+// rows of the new order are a compact neighbourhood, so the 8x8 blocks of the squared
+// iterate are fuller (config-5-like pattern: 45 % fewer block products in the model,
+// DESIGN.md section 6).  perm[new] = old.
+static void aggregate_order(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
+                            int64_t n, int size, std::vector<int64_t> &perm) {
+  perm.clear();
+  perm.reserve((size_t)n);
+  std::vector<uint8_t> used((size_t)n, 0);
+  for (int64_t s = 0; s < n; s++) {
+    if (used[s]) continue;
+    const size_t g0 = perm.size();
+    perm.push_back(s);
+    used[s] = 1;
+    for (size_t h = g0; h < perm.size() && (int)(perm.size() - g0) < size; h++) {
+      const int64_t v = perm[h];
+      for (int64_t p = rp[v]; p < rp[v + 1] && (int)(perm.size() - g0) < size; p++) {
+        const int64_t u = col[p];
+        if (!used[u]) {
+          used[u] = 1;
+          perm.push_back(u);
+        }
+      }
+    }
+  }
+}
+
 static void cluster_order(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
                           int64_t r0, int64_t r1, int cluster, std::vector<int32_t> &order) {
   const int64_t nl = r1 - r0;
@@ -1441,12 +1473,15 @@ static void build_diagonals(sexpm_plan_s &P) {
 // ordered by (smallest position of a neighbour in the previous level, degree, index), the
 // whole sequence reversed.  Host loop over BFS levels, one d2h per level.
 // ------------------------------------------------------------------------------------
+// C = A permuted (row i <- row rowmap[i], column c -> colmap[c], rows re-sorted).  The
+// unsorted rows go to the staging pool (free between the phases) and CUB sorts between it and
+// C, so no other O(nnz) buffer is allocated.
 static void permute_csr(sexpm_plan_s &P, const CsrView &A, const int64_t *rowmap, const int64_t *colmap,
                         DCsr &C) {
   cudaStream_t st = P.st;
   Workspace &w = P.ws;
   const int64_t n = A.nrows;
-  REQUIRE(A.nnz < INT32_MAX, SEXPM_EINVAL, "reorder: nnz must be < 2^31 (segmented sort)");
+  REQUIRE(A.nnz < INT32_MAX, SEXPM_EINVAL, "permutation: nnz must be < 2^31 (segmented sort)");
   w.cnt.ensure((size_t)std::max<int64_t>(n, 1), st);
   w.scan_tmp.ensure((size_t)scan_tmp_elems(n) + 1, st);
   C.nrows = n;
@@ -1458,15 +1493,26 @@ static void permute_csr(sexpm_plan_s &P, const CsrView &A, const int64_t *rowmap
   C.val.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
   launch_perm_count(A.rp, rowmap, n, w.cnt.p, st);
   launch_exclusive_scan(w.cnt.p, n, C.rp.p, w.scan_tmp.p, st);
-  DBuf<int32_t> ctmp;
-  DBuf<double> vtmp;
-  ctmp.alloc((size_t)std::max<int64_t>(A.nnz, 1), st);
-  vtmp.alloc((size_t)std::max<int64_t>(A.nnz, 1), st);
-  launch_perm_write(A, rowmap, colmap, n, C.rp.p, ctmp.p, vtmp.p, st);
+  w.pool_col.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
+  w.pool_val.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
+  launch_perm_write(A, rowmap, colmap, n, C.rp.p, w.pool_col.p, w.pool_val.p, st);
+  w.i64tmp.ensure(8, st);
+  launch_reduce_max_i64(w.cnt.p, n, w.i64tmp.p + 0, st);
+  if (d2h(w.i64tmp.p + 0, st) <= kSortRowsCap) {  // short rows: warp bitonic sort
+    launch_sort_rows(C.rp.p, n, w.pool_col.p, w.pool_val.p, C.col.p, C.val.p, st);
+    CK(cudaGetLastError());
+    return;
+  }
   const size_t tb = seg_sort_temp_bytes(A.nnz, n, C.rp.p);
   DBuf<unsigned char> tmp;
   tmp.alloc(tb + 256, st);
-  launch_seg_sort(ctmp.p, C.col.p, vtmp.p, C.val.p, A.nnz, n, C.rp.p, tmp.p, tb, st);
+  int32_t *kc = w.pool_col.p;
+  double *vc = w.pool_val.p;
+  launch_seg_sort(&kc, C.col.p, &vc, C.val.p, A.nnz, n, C.rp.p, tmp.p, tb, st);
+  if (A.nnz && kc != C.col.p) {
+    CK(cudaMemcpyAsync(C.col.p, kc, A.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(C.val.p, vc, A.nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
   CK(cudaGetLastError());
 }
 
@@ -1867,6 +1913,10 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     P.proc_order.ensure((size_t)std::max<int64_t>(nl, 1), st);
     P.group_start.ensure((size_t)nl + 2, st);
     P.block_order.ensure((size_t)std::max<int64_t>((nl + 7) / 8, 1), st);
+    if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1) {
+      P.tperm.ensure((size_t)std::max<int64_t>(P.n, 1), st);
+      P.tinv.ensure((size_t)std::max<int64_t>(P.n, 1), st);
+    }
     CK(cudaEventCreateWithFlags(&P.ev_pattern, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&P.ev_order, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&P.bg_st, cudaStreamNonBlocking));
@@ -1913,6 +1963,14 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
           CK(cudaMemcpyAsync(P.block_order.p, bo.data(), bo.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         if (!ord.empty())
           CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
+        if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1) {  // aggregate order of the squarings
+          aggregate_order(hrp, hcol, P.n, 8, P.h_tperm);
+          std::vector<int64_t> hinv((size_t)P.n);
+          for (int64_t i = 0; i < P.n; i++) hinv[P.h_tperm[i]] = i;
+          CK(cudaMemcpyAsync(P.tperm.p, P.h_tperm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
+          CK(cudaMemcpyAsync(P.tinv.p, hinv.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
+          CK(cudaStreamSynchronize(P.bg_st));  // hinv is local
+        }
         CK(cudaMemcpyAsync(P.group_start.p, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         CK(cudaEventRecord(P.ev_order, P.bg_st));
       } catch (const SxError &e) {
@@ -2043,6 +2101,18 @@ static void do_run(sexpm_plan_s &P) {
     swap_csr(T, Tn);
   }
   CK(cudaEventRecord(ev_taylor, st));
+  // squarings in aggregate order (option sq_order, one GPU): T^_0 relabelled once here, E
+  // mapped back after the last squaring (the SSAT baseline keeps the index order: its
+  // products must match the oracle's bit for bit)
+  P.sq_tiled = false;
+  if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1 && !P.o.ssat && P.M >= 1) {
+    wait_order(P);
+    if (!P.h_tperm.empty()) {
+      permute_csr(P, T.view(), P.tperm.p, P.tinv.p, Tn);  // row i <- row tperm[i], col c -> tinv[c]
+      swap_csr(T, Tn);
+      P.sq_tiled = true;
+    }
+  }
   // stats of T^_0
   {
     Workspace &w = P.ws;
@@ -2145,6 +2215,12 @@ static void do_run(sexpm_plan_s &P) {
     launch_identity(nl, P.row_begin, I.rp.p, I.col.p, I.val.p, st);
     merge_add(P, T.view(), I.view(), P.E);
   }
+  if (P.sq_tiled) {  // back to index order: row r <- row tinv[r], col c' -> tperm[c']
+    DCsr &spare = (&T == &P.E) ? Tn : (T.nnz >= P.E.nnz ? T : Tn);  // an iterate no longer needed
+    permute_csr(P, P.E.view(), P.tinv.p, P.tperm.p, spare);
+    swap_csr(P.E, spare);
+    P.sq_tiled = false;
+  }
   CK(cudaEventRecord(ev_end, st));
   CK(cudaStreamSynchronize(st));
   float t1, t2, t3, t4;
@@ -2169,8 +2245,9 @@ static void do_run(sexpm_plan_s &P) {
     S.cache_bytes_allocated = cache::bytes_allocated;
   }
   if (P.o.reorder) {  // N3: E = P^T E' P (row r <- row inv[r], col c' -> perm[c'])
-    permute_csr(P, P.E.view(), P.inv.p, P.perm.p, P.Etmp);
-    swap_csr(P.E, P.Etmp);
+    DCsr &spare = (&P.T == &P.E) ? P.Tn : (P.T.nnz >= P.E.nnz ? P.T : P.Tn);  // free iterates
+    permute_csr(P, P.E.view(), P.inv.p, P.perm.p, spare);
+    swap_csr(P.E, spare);
     CK(cudaStreamSynchronize(st));
   }
   for (cudaEvent_t e : {ev_start, ev_taylor, ev_sq, ev_end, a0, a1}) cudaEventDestroy(e);
@@ -2233,6 +2310,7 @@ int sexpm_options_init(sexpm_options *o) {
   o->kernel = 0;
   o->ssat = 0;
   o->reorder = 0;
+  o->sq_order = 1;
   o->e_r = 0.1;
   o->stream = nullptr;
   o->nccl_comm = nullptr;

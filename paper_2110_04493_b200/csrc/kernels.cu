@@ -5169,19 +5169,25 @@ void launch_perm_write(const CsrView &A, const int64_t *rowmap, const int64_t *c
   KL;
   k_perm_write<<<grid_for(n * 32, kThreads), kThreads, 0, st>>>(A, rowmap, colmap, n, rp_out, col_out, val_out);
 }
+// segmented sort of each row's (column, value) pairs with caller-provided double buffers
+// (no O(nnz) temporary inside CUB): on return *k_cur / *v_cur point at the sorted arrays
 size_t seg_sort_temp_bytes(int64_t nnz, int64_t n, const int64_t *rp) {
   size_t b = 0;
-  cub::DeviceSegmentedSort::SortPairs(nullptr, b, (const int32_t *)nullptr, (int32_t *)nullptr,
-                                      (const double *)nullptr, (double *)nullptr, (int)nnz, (int)n, rp,
-                                      rp + 1);
+  cub::DoubleBuffer<int32_t> kb(nullptr, nullptr);
+  cub::DoubleBuffer<double> vb(nullptr, nullptr);
+  cub::DeviceSegmentedSort::SortPairs(nullptr, b, kb, vb, (int)nnz, (int)n, rp, rp + 1);
   return b;
 }
-void launch_seg_sort(const int32_t *kin, int32_t *kout, const double *vin, double *vout, int64_t nnz,
+void launch_seg_sort(int32_t **k_cur, int32_t *k_alt, double **v_cur, double *v_alt, int64_t nnz,
                      int64_t n, const int64_t *rp, void *tmp, size_t tmp_bytes, cudaStream_t st) {
   if (nnz == 0 || n == 0) return;
   size_t b = tmp_bytes;
+  cub::DoubleBuffer<int32_t> kb(*k_cur, k_alt);
+  cub::DoubleBuffer<double> vb(*v_cur, v_alt);
   KL;
-  cub::DeviceSegmentedSort::SortPairs(tmp, b, kin, kout, vin, vout, (int)nnz, (int)n, rp, rp + 1, st);
+  cub::DeviceSegmentedSort::SortPairs(tmp, b, kb, vb, (int)nnz, (int)n, rp, rp + 1, st);
+  *k_cur = kb.Current();
+  *v_cur = vb.Current();
 }
 }  // namespace sx
 
@@ -5210,5 +5216,104 @@ void launch_rows_equal(const CsrView &A, const CsrView &B, int *flag, cudaStream
   if (A.nrows == 0) return;
   KL;
   k_rows_equal<<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, B, flag);
+}
+}  // namespace sx
+
+namespace sx {
+// Row sort for relabelled CSR rows (<= kSortCap entries), one warp per row.  The keys of a
+// row are distinct columns: when their span fits a 64 Ki-bit bitmap, a key's sorted position
+// is the number of set bits below it (mark, word popcount prefix, rank: O(span / 32 + len)
+// per row); otherwise a bitonic network over (column << 32 | position) in shared memory.
+constexpr int kSortCap = 1024, kSortWarps = 8;
+constexpr int kSortWords = 2048;  // bitmap words per warp (65536 columns of span)
+__global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp, int64_t n,
+                                                               const int32_t *kin, const double *vin,
+                                                               int32_t *kout, double *vout) {
+  extern __shared__ unsigned long long sbuf[];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  unsigned long long *buf = sbuf + wi * kSortCap;                       // bitonic keys
+  unsigned *bits = reinterpret_cast<unsigned *>(buf);                     // or: bitmap words
+  uint16_t *pref = reinterpret_cast<uint16_t *>(sbuf + kSortWarps * kSortCap) + wi * kSortWords;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int64_t p0 = rp[r];
+    const int len = (int)(rp[r + 1] - p0);
+    int kmin = INT32_MAX, kmax = -1;
+    for (int i = lane; i < len; i += 32) {
+      const int k = kin[p0 + i];
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
+    }
+    kmin = __shfl_sync(FULL_MASK, warp_min(kmin), 0);  // warp_min / warp_max reduce into lane 0
+    kmax = __shfl_sync(FULL_MASK, warp_max(kmax), 0);
+    const int64_t span = len ? (int64_t)kmax - kmin + 1 : 0;
+    if (span <= (int64_t)kSortWords * 32) {
+      const int nwd = (int)((span + 31) >> 5);
+      for (int i = lane; i < nwd; i += 32) bits[i] = 0u;
+      __syncwarp();
+      for (int i = lane; i < len; i += 32) {
+        const int d = kin[p0 + i] - kmin;
+        atomicOr(&bits[d >> 5], 1u << (d & 31));
+      }
+      __syncwarp();
+      const int per = (nwd + 31) / 32, w0 = min(lane * per, nwd), w1 = min(w0 + per, nwd);
+      int c = 0;
+      for (int w = w0; w < w1; w++) c += __popc(bits[w]);
+      int v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, v, o);
+        if (lane >= o) v += y;
+      }
+      int run = v - c;
+      for (int w = w0; w < w1; w++) {
+        pref[w] = (uint16_t)run;
+        run += __popc(bits[w]);
+      }
+      __syncwarp();
+      for (int i = lane; i < len; i += 32) {
+        const int k = kin[p0 + i], d = k - kmin;
+        const int pos = pref[d >> 5] + __popc(bits[d >> 5] & ((1u << (d & 31)) - 1u));
+        kout[p0 + pos] = k;
+        vout[p0 + pos] = vin[p0 + i];
+      }
+      __syncwarp();
+      continue;
+    }
+    int P = 32;
+    while (P < len) P <<= 1;
+    for (int i = lane; i < P; i += 32)
+      buf[i] = i < len ? ((unsigned long long)(unsigned)kin[p0 + i] << 32) | (unsigned)i : ~0ull;
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < P; i += 32) {
+          const int l = i ^ j;
+          if (l > i) {
+            const unsigned long long a = buf[i], b = buf[l];
+            if ((a > b) == ((i & k) == 0)) {
+              buf[i] = b;
+              buf[l] = a;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    for (int i = lane; i < len; i += 32) {
+      const unsigned long long e = buf[i];
+      kout[p0 + i] = (int32_t)(e >> 32);
+      vout[p0 + i] = vin[p0 + (int64_t)(e & 0xFFFFFFFFull)];
+    }
+    __syncwarp();
+  }
+}
+void launch_sort_rows(const int64_t *rp, int64_t n, const int32_t *kin, const double *vin, int32_t *kout,
+                      double *vout, cudaStream_t st) {
+  if (n == 0) return;
+  const int smem = kSortWarps * kSortCap * 8 + kSortWarps * kSortWords * 2;
+  cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_sort_rows<<<(int)std::min<int64_t>((n + kSortWarps - 1) / kSortWarps, 148 * 3), kSortWarps * 32, smem, st>>>(
+      rp, n, kin, vin, kout, vout);
 }
 }  // namespace sx

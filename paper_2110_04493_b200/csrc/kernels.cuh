@@ -269,10 +269,14 @@ void launch_perm_count(const int64_t *arp, const int64_t *rowmap, int64_t n, int
 void launch_perm_write(const CsrView &A, const int64_t *rowmap, const int64_t *colmap, int64_t n,
                        const int64_t *rp_out, int32_t *col_out, double *val_out, cudaStream_t st);
 size_t seg_sort_temp_bytes(int64_t nnz, int64_t n, const int64_t *rp);
-void launch_seg_sort(const int32_t *kin, int32_t *kout, const double *vin, double *vout, int64_t nnz,
+void launch_seg_sort(int32_t **k_cur, int32_t *k_alt, double **v_cur, double *v_alt, int64_t nnz,
                      int64_t n, const int64_t *rp, void *tmp, size_t tmp_bytes, cudaStream_t st);
 // flag |= 1 unless A's rows equal (bit for bit) B's rows at offset A.row0 - B.row0
 void launch_rows_equal(const CsrView &A, const CsrView &B, int *flag, cudaStream_t st);
+// sort every row (<= 1024 entries) of relabelled CSR rows by column: warp-per-row bitonic
+constexpr int kSortRowsCap = 1024;
+void launch_sort_rows(const int64_t *rp, int64_t n, const int32_t *kin, const double *vin, int32_t *kout,
+                      double *vout, cudaStream_t st);
 void launch_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
                        int64_t *out, cudaStream_t st);
 // identity rows for rows [row0, row0+nrows)
