@@ -441,6 +441,7 @@ struct sexpm_plan_s {
   // graph; sq_tiled while the iterate is held in that order
   std::vector<int64_t> h_tperm;
   DBuf<int64_t> tperm, tinv;
+  DBuf<int32_t> block_order_t;  // the aggregates (block rows in that order) in locality order
   bool sq_tiled = false;
   DBuf<int32_t> block_order;  // block rows of the block kernel in locality order
   ~sexpm_plan_s() {
@@ -830,6 +831,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           Bv.kb0 = B.row0 / 8;
           if (use_cluster && nr == P.row_end - P.row_begin && A.row0 % 8 == 0 && !getenv("SEXPM_BSR_NATURAL"))
             Bv.border = P.block_order.p;  // block rows of the rank's rows in locality order
+          if (P.sq_tiled && same && nr == P.n && !getenv("SEXPM_BSR_NATURAL"))
+            Bv.border = P.block_order_t.p;  // the aggregates in locality order
           if (stage == 12)  // block-row pairs, one 512-thread CTA per SM
             nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nbr + 1) / 2, (int64_t)P.sm_count));
           else
@@ -1916,6 +1919,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1) {
       P.tperm.ensure((size_t)std::max<int64_t>(P.n, 1), st);
       P.tinv.ensure((size_t)std::max<int64_t>(P.n, 1), st);
+      P.block_order_t.ensure((size_t)std::max<int64_t>((P.n + 7) / 8, 1), st);
     }
     CK(cudaEventCreateWithFlags(&P.ev_pattern, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&P.ev_order, cudaEventDisableTiming));
@@ -1967,6 +1971,24 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
           aggregate_order(hrp, hcol, P.n, 8, P.h_tperm);
           std::vector<int64_t> hinv((size_t)P.n);
           for (int64_t i = 0; i < P.n; i++) hinv[P.h_tperm[i]] = i;
+          // block rows of the relabelled matrix in the locality order of H's clusters: each
+          // aggregate ranked by the earliest position of its rows in `ord`
+          {
+            std::vector<int32_t> at((size_t)P.n);
+            for (size_t j = 0; j < ord.size(); j++) at[ord[j]] = (int32_t)j;
+            const int64_t nbt = (P.n + 7) / 8;
+            std::vector<std::pair<int32_t, int32_t>> key((size_t)nbt);
+            for (int64_t g = 0; g < nbt; g++) {
+              int32_t k = INT32_MAX;
+              for (int64_t i = 8 * g; i < std::min<int64_t>(P.n, 8 * g + 8); i++) k = std::min(k, at[P.h_tperm[i]]);
+              key[g] = {k, (int32_t)g};
+            }
+            std::sort(key.begin(), key.end());
+            std::vector<int32_t> bot((size_t)nbt);
+            for (int64_t g = 0; g < nbt; g++) bot[g] = key[g].second;
+            CK(cudaMemcpyAsync(P.block_order_t.p, bot.data(), nbt * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
+            CK(cudaStreamSynchronize(P.bg_st));  // bot is local
+          }
           CK(cudaMemcpyAsync(P.tperm.p, P.h_tperm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
           CK(cudaMemcpyAsync(P.tinv.p, hinv.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
           CK(cudaStreamSynchronize(P.bg_st));  // hinv is local
