@@ -1971,9 +1971,55 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
           aggregate_order(hrp, hcol, P.n, 8, P.h_tperm);
           std::vector<int64_t> hinv((size_t)P.n);
           for (int64_t i = 0; i < P.n; i++) hinv[P.h_tperm[i]] = i;
+          // keep it only where it fills the 8x8 blocks better: for a sample of block rows,
+          // count the distinct column blocks covered by the radius-3 neighbourhood of their
+          // 8 rows (the iterates' patterns are such neighbourhoods) in both orders
+          {
+            const int64_t nbt = (P.n + 7) / 8, step = std::max<int64_t>(1, nbt / 512);
+            std::vector<int32_t> mark((size_t)P.n, -1), fr, nx;
+            std::vector<int64_t> blk;
+            auto proxy = [&](bool agg) {
+              int64_t total = 0;
+              int32_t stamp = 0;
+              std::fill(mark.begin(), mark.end(), -1);
+              for (int64_t g = 0; g < nbt; g += step, stamp++) {
+                fr.clear();
+                for (int64_t i = 8 * g; i < std::min<int64_t>(P.n, 8 * g + 8); i++) {
+                  const int32_t v = (int32_t)(agg ? P.h_tperm[i] : i);
+                  if (mark[v] != stamp) {
+                    mark[v] = stamp;
+                    fr.push_back(v);
+                  }
+                }
+                blk.clear();
+                for (int32_t v : fr) blk.push_back((agg ? hinv[v] : v) >> 3);
+                for (int rad = 0; rad < 3; rad++) {
+                  nx.clear();
+                  for (int32_t v : fr)
+                    for (int64_t p = hrp[v]; p < hrp[v + 1]; p++) {
+                      const int32_t u = hcol[p];
+                      if (mark[u] != stamp) {
+                        mark[u] = stamp;
+                        nx.push_back(u);
+                        blk.push_back((agg ? hinv[u] : u) >> 3);
+                      }
+                    }
+                  fr.swap(nx);
+                }
+                std::sort(blk.begin(), blk.end());
+                total += std::unique(blk.begin(), blk.end()) - blk.begin();
+              }
+              return total;
+            };
+            const int64_t b_idx = proxy(false), b_agg = proxy(true);
+            if (getenv("SEXPM_PLAN_LOG"))
+              fprintf(stderr, "[sexpm plan] aggregate order: sampled blocks %lld (index order %lld)%s\n",
+                      (long long)b_agg, (long long)b_idx, 10 * b_agg <= 9 * b_idx ? "" : " -> index order");
+            if (10 * b_agg > 9 * b_idx) P.h_tperm.clear();
+          }
           // block rows of the relabelled matrix in the locality order of H's clusters: each
           // aggregate ranked by the earliest position of its rows in `ord`
-          {
+          if (!P.h_tperm.empty()) {
             std::vector<int32_t> at((size_t)P.n);
             for (size_t j = 0; j < ord.size(); j++) at[ord[j]] = (int32_t)j;
             const int64_t nbt = (P.n + 7) / 8;
@@ -1989,9 +2035,11 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
             CK(cudaMemcpyAsync(P.block_order_t.p, bot.data(), nbt * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
             CK(cudaStreamSynchronize(P.bg_st));  // bot is local
           }
-          CK(cudaMemcpyAsync(P.tperm.p, P.h_tperm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
-          CK(cudaMemcpyAsync(P.tinv.p, hinv.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
-          CK(cudaStreamSynchronize(P.bg_st));  // hinv is local
+          if (!P.h_tperm.empty()) {
+            CK(cudaMemcpyAsync(P.tperm.p, P.h_tperm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
+            CK(cudaMemcpyAsync(P.tinv.p, hinv.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
+            CK(cudaStreamSynchronize(P.bg_st));  // hinv is local
+          }
         }
         CK(cudaMemcpyAsync(P.group_start.p, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         CK(cudaEventRecord(P.ev_order, P.bg_st));

@@ -420,3 +420,32 @@ def test_block_kernel_rank_slice_in_halo(B, kernel, r0, r1, h0, h1):
     Cr = rows(Ct, r0, r1)
     assert np.array_equal(G.rowptr, Cr.rowptr) and np.array_equal(G.col, Cr.col)
     assert np.array_equal(G.val, Cr.val)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_aggregate_order_matches_index_order(B, cid):
+    """Squarings in 8-row aggregate order (default) and in index order (sq_order = 0) give
+    the same e^H up to rounding order (north-star parity between the two), the same plan,
+    and the aggregate order does not execute more block products."""
+    H = make_config(cid)
+    Ea, sa = run_gpu(B, H)
+    Ei, si = run_gpu(B, H, sq_order=0)
+    assert (sa["M"], sa["N"]) == (si["M"], si["N"])
+    ok, res = parity(Ea, Ei, max(si["sq_tau"][si["N"]], sa["sq_tau"][sa["N"]], 1e-300))
+    assert ok, res
+    N = sa["N"]
+    assert sa["sq_block_products"][1:N + 1].sum() <= si["sq_block_products"][1:N + 1].sum()
+
+
+def test_aggregate_order_with_reorder(B):
+    """Both relabellings at once (RCM of a scrambled input, then the aggregates of the
+    squarings): parity against the oracle."""
+    import scipy.sparse as sp
+    H0 = laplacian_2d(40, 30, 1.0)
+    q = np.random.default_rng(3).permutation(H0.n)
+    A = sp.csr_matrix((H0.val, H0.col, H0.rowptr), shape=(H0.n, H0.n))[q][:, q].tocsr()
+    A.sort_indices()
+    H = CSR(H0.n, A.indptr.astype(np.int64), A.indices.astype(np.int32), A.data.astype(np.float64))
+    Eg, st = run_gpu(B, H, reorder=1)
+    Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS)
+    assert_parity(Eg, st, Eo, tr)
