@@ -4476,7 +4476,7 @@ void launch_numeric_warp(const NumericArgs &a, cudaStream_t st) {
 // ident != nullptr (E = I + T^_N fused into the last compaction): per row,
 // ident[w] = 0 no kept diagonal (insert 1.0), 1 kept diagonal t (write 1 + t), 2 kept
 // diagonal with 1 + t == 0 (purged, reading R11); cnt counts the entries of E's row.
-__global__ void k_compact_count(int64_t nrows, int64_t row0, const int64_t *row_off,
+__global__ void __launch_bounds__(kThreads, 8) k_compact_count(int64_t nrows, int64_t row0, const int64_t *row_off,
                                 const int64_t *row_cnt, const int32_t *pool_col,
                                 const double *pool_val, double tau, int64_t *cnt,
                                 int8_t *ident) {
@@ -4547,7 +4547,7 @@ __device__ __forceinline__ void row_stat_finish(int lane, int64_t w, double s, i
   }
 }
 
-__global__ void k_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
+__global__ void __launch_bounds__(kThreads, 6) k_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
                                 const int64_t *row_cnt, const int32_t *pool_col,
                                 const double *pool_val, double tau, const int64_t *rp_out,
                                 int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
@@ -4723,7 +4723,7 @@ __global__ void k_merge(CsrView A, CsrView B, const int64_t *rp_out, int64_t *cn
 // a 0, which the merge already treats like an absent entry (a + 0 = a, 0-valued entries
 // are not emitted).  The write pass also writes S^_i itself (the kept entries) at s_rp.
 template <bool WRITE>
-__global__ void k_merge_staged(CsrView A, const int64_t *alen, const int64_t *row_off,
+__global__ void __launch_bounds__(kThreads, 8) k_merge_staged(CsrView A, const int64_t *alen, const int64_t *row_off,
                                const int64_t *row_cnt, const int32_t *pcol, const double *pval,
                                double tau, const int64_t *rp_out, int64_t *cnt, int32_t *col_out,
                                double *val_out, int64_t *len_out, const int64_t *s_rp,
