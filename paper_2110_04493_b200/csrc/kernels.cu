@@ -5239,10 +5239,15 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
     const int64_t p0 = rp[r];
     const int len = (int)(rp[r + 1] - p0);
     int kmin = INT32_MAX, kmax = -1;
-    for (int i = lane; i < len; i += 32) {
-      const int k = kin[p0 + i];
-      kmin = min(kmin, k);
-      kmax = max(kmax, k);
+    int kr[kSortCap / 32];  // the row's keys, loaded once (len <= kSortCap)
+#pragma unroll
+    for (int t = 0; t < kSortCap / 32; t++) {
+      const int i = lane + 32 * t;
+      kr[t] = i < len ? kin[p0 + i] : 0;
+      if (i < len) {
+        kmin = min(kmin, kr[t]);
+        kmax = max(kmax, kr[t]);
+      }
     }
     kmin = __shfl_sync(FULL_MASK, warp_min(kmin), 0);  // warp_min / warp_max reduce into lane 0
     kmax = __shfl_sync(FULL_MASK, warp_max(kmax), 0);
@@ -5251,10 +5256,12 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
       const int nwd = (int)((span + 31) >> 5);
       for (int i = lane; i < nwd; i += 32) bits[i] = 0u;
       __syncwarp();
-      for (int i = lane; i < len; i += 32) {
-        const int d = kin[p0 + i] - kmin;
-        atomicOr(&bits[d >> 5], 1u << (d & 31));
-      }
+#pragma unroll
+      for (int t = 0; t < kSortCap / 32; t++)
+        if (lane + 32 * t < len) {
+          const int d = kr[t] - kmin;
+          atomicOr(&bits[d >> 5], 1u << (d & 31));
+        }
       __syncwarp();
       const int per = (nwd + 31) / 32, w0 = min(lane * per, nwd), w1 = min(w0 + per, nwd);
       int c = 0;
@@ -5271,12 +5278,14 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
         run += __popc(bits[w]);
       }
       __syncwarp();
-      for (int i = lane; i < len; i += 32) {
-        const int k = kin[p0 + i], d = k - kmin;
-        const int pos = pref[d >> 5] + __popc(bits[d >> 5] & ((1u << (d & 31)) - 1u));
-        kout[p0 + pos] = k;
-        vout[p0 + pos] = vin[p0 + i];
-      }
+#pragma unroll
+      for (int t = 0; t < kSortCap / 32; t++)
+        if (lane + 32 * t < len) {
+          const int k = kr[t], d = k - kmin;
+          const int pos = pref[d >> 5] + __popc(bits[d >> 5] & ((1u << (d & 31)) - 1u));
+          kout[p0 + pos] = k;
+          vout[p0 + pos] = vin[p0 + lane + 32 * t];
+        }
       __syncwarp();
       continue;
     }
