@@ -420,6 +420,7 @@ struct sexpm_plan_s {
   DBuf<double> dia_val;
   DBuf<unsigned long long> dia_prod;
   int dia_slots = 512;       // K5d accumulator slots per warp: adapted from the previous term's need
+  bool dia_short_ok = true;  // the previous Taylor term's rows all fitted the short-row kernel K5s
   int dia_slots_max = 1152;  // the most that fit (set at plan time); retry size for rows over dia_slots
   DBuf<int> dia_need;
   int group_slots = 4096;
@@ -739,6 +740,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       int fb = 0;
       int stage = kern;
       bool first = true, dia_retry = false;
+      // short rows first (thread-per-row K5s) while the previous term's rows were short
+      bool dia_short = P.dia_short_ok;
       // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
       fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10 || kern == 11 || kern == 12);
       while (nlist > 0) {
@@ -893,6 +896,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           D.prod_count = P.dia_prod.p;
           // slots sized from the previous term's largest row (occupancy: 20 -> 28+ warps/SM
           // at config 5); rows over it are retried once at twice the slots
+          if (dia_short) {
+            launch_taylor_dia_short(nh, D, fout, w.fail_count.p, st);
+          } else {
           const int slots = std::min(dia_retry ? 2 * P.dia_slots : P.dia_slots, P.dia_slots_max);
           if (!dia_retry) CK(cudaMemsetAsync(P.dia_need.p, 0, sizeof(int), st));
           D.need_max = P.dia_need.p;
@@ -901,6 +907,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
                                                                 (int64_t)P.sm_count * per_sm));
           launch_taylor_dia(nh, D, slots, fout, w.fail_count.p, st);
           dia_launched = true;
+          }
         } else {  // 6
           nh.grid = paged_grid;
           launch_taylor_pull(nh, BT->view(), fout, w.fail_count.p, st);
@@ -919,7 +926,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         // fall-through: K5d rows over its slots -> K5d at twice the slots -> paged; K5p ->
         // hash; the squaring kernels -> paged; everything else -> the block-window kernel (no
         // capacity limit)
-        if (stage == 7 && !dia_retry && P.dia_slots < P.dia_slots_max) {
+        if (stage == 7 && dia_short) {
+          dia_short = false;  // rows wider than K5s's window: the warp kernel K5d
+        } else if (stage == 7 && !dia_retry && P.dia_slots < P.dia_slots_max) {
           dia_retry = true;
         } else {
           stage = stage == 7 ? 5 : (stage == 6 ? 1 : ((stage >= 8 && stage <= 12) ? 5 : 3));
@@ -945,6 +954,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   if (have_first) CK(cudaEventElapsedTime(&rep.first_ms, e0, e_first));
   cudaEventDestroy(e_first);
   if (dia_path && !have_symbolic && nfail_other == 0) rep.fmas = (double)d2h(P.dia_prod.p, st);
+  if (dia_path) P.dia_short_ok = !dia_launched;  // next term: K5s first only if every row fitted it
   if (dia_launched) {  // next term's K5d slots: this term's largest row + 12.5 % + 64, 64-aligned
     const long long nd = d2h(P.dia_need.p, st);
     P.dia_slots = (int)std::min<long long>(P.dia_slots_max, std::max<long long>(256, ((nd * 9 / 8 + 64 + 63) / 64) * 64));
@@ -2098,6 +2108,7 @@ static void do_run(sexpm_plan_s &P) {
     return (double)ms;
   };
   CK(cudaEventRecord(ev_start, st));
+  P.dia_short_ok = true;  // the first Taylor term tries the short-row kernel K5s
   const int64_t nl = P.row_end - P.row_begin;
   DCsr &H0loc = P.H0loc;
   DCsr &T = P.T, &Tn = P.Tn, &Sc = P.S, &Sn = P.Sn;

@@ -5326,3 +5326,135 @@ void launch_sort_rows(const int64_t *rp, int64_t n, const int32_t *kin, const do
       rp, n, kin, vin, kout, vout);
 }
 }  // namespace sx
+
+namespace sx {
+// ------------------------------------------------------------------------------------
+// K5s: the Taylor product S~ = S^ H0 / i for SHORT rows (1D-like bands): one THREAD per row
+// with a dense window of kShortWin slots over the row's output span [lo, hi] in shared
+// memory (slot t of thread x at t * blockDim + x: consecutive threads, consecutive words).
+// The thread adds, for its entries k in ascending order and the diagonals in descending
+// offset order, s_rk * h_d[k] into column k + d: every column sees its products in
+// ascending k -- the order of K5d and of the oracle, bit for bit.  Then / i, the Algorithm
+// 4.1 floor classification (and the fused first pass), staging in column order with one
+// pool reservation per warp.  Rows whose span exceeds the window go to the fail list (K5d).
+// ------------------------------------------------------------------------------------
+constexpr int kShortWin = 64, kShortThreads = 128;
+__global__ void __launch_bounds__(kShortThreads) k_taylor_dia_short(NumericArgs a, DiaView D,
+                                                                   int32_t *fail_rows, int *fail_count) {
+  extern __shared__ double ssm[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ int32_t s_doff[kDiaMax];
+  if (tid < kDiaMax) s_doff[tid] = tid < D.ndiag ? D.off[tid] : 0;
+  __syncthreads();
+  const int nd = D.ndiag;
+  const int n = (int)D.n;
+  unsigned long long prods = 0;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count so that the warp-wide reservation below is safe
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (tid & ~31); base < a.nlist; base += nthr) {
+    const int64_t idx = base + lane;
+    const bool have = idx < a.nlist;
+    const int64_t r = have ? (a.order ? (int64_t)a.order[idx] : idx) : 0;
+    int64_t p0 = 0, p1 = 0;
+    if (have) {
+      p0 = a.A.rp[r];
+      p1 = a.A.rp[r + 1];
+    }
+    int lo = 0, span = 0;
+    bool fit = true;
+    if (have && p1 > p0) {
+      lo = a.A.col[p0] + D.dmin;
+      int hi = a.A.col[p1 - 1] + D.dmax;
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > n - 1 ? n - 1 : hi;
+      span = hi - lo + 1;
+      fit = span <= kShortWin;
+    }
+    const bool work = have && fit && p1 > p0;
+    if (have && !fit) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+    if (work) {
+      for (int t = 0; t < span; t++) ssm[t * kShortThreads + tid] = 0.0;
+      for (int64_t p = p0; p < p1; p++) {
+        const int k = a.A.col[p];
+        const double s = a.A.val[p];
+        for (int di = 0; di < nd; di++) {
+          const double h = D.val[(size_t)di * (size_t)n + k];
+          if (h != 0.0) {
+            const int t = k + s_doff[di] - lo;
+            ssm[t * kShortThreads + tid] = __dadd_rn(ssm[t * kShortThreads + tid], __dmul_rn(s, h));
+            prods++;
+          }
+        }
+      }
+    }
+    // flush pass 1: / i, classify, count
+    int nst = 0;
+    double fs = 0.0, q1 = 0.0;
+    long long nnzu = 0, c1 = 0;
+    if (work) {
+      for (int t = 0; t < span; t++) {
+        double x = ssm[t * kShortThreads + tid];
+        if (x != 0.0) {
+          x = x / a.divisor;
+          ssm[t * kShortThreads + tid] = x;
+          if (x != 0.0) {
+            nnzu++;
+            if (fabs(x) > a.floor_tau) {
+              nst++;
+              if (fabs(x) <= a.eps_g) q1 += x * x;
+              else c1++;
+            } else {
+              fs += x * x;
+            }
+          }
+        }
+      }
+    }
+    // one pool reservation per warp
+    int v = nst;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL_MASK, v, o);
+      if (lane >= o) v += y;
+    }
+    const int tot = __shfl_sync(FULL_MASK, v, 31);
+    unsigned long long off = 0;
+    if (lane == 0 && tot) off = atomicAdd(a.pool_used, (unsigned long long)tot);
+    off = __shfl_sync(FULL_MASK, off, 0) + (unsigned long long)(v - nst);
+    const bool ok = (long long)off + nst <= a.pool_cap;
+    if (work && ok) {
+      long long q = (long long)off;
+      for (int t = 0; t < span; t++) {
+        const double x = ssm[t * kShortThreads + tid];
+        if (x != 0.0 && fabs(x) > a.floor_tau) {
+          a.pool_col[q] = lo + t;
+          a.pool_val[q] = x;
+          q++;
+        }
+      }
+    }
+    if (have && fit) {
+      if (!ok) atomicOr(a.flags, 1);
+      a.row_off[r] = (int64_t)off;
+      a.row_cnt[r] = nst;
+      a.row_fsum[r] = fs;
+      a.row_nnz[r] = nnzu;
+      if (a.row_p1) {
+        a.row_p1[r] = q1;
+        a.row_c1[r] = c1;
+      }
+    }
+  }
+  prods = warp_sum(prods);
+  if (lane == 0 && prods) atomicAdd(D.prod_count, prods);
+}
+void launch_taylor_dia_short(const NumericArgs &a, const DiaView &D, int32_t *fail_rows, int *fail_count,
+                             cudaStream_t st) {
+  if (a.A.nrows == 0 || a.nlist == 0) return;
+  const int smem = kShortWin * kShortThreads * 8;
+  cudaFuncSetAttribute(k_taylor_dia_short, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((a.nlist + kShortThreads - 1) / kShortThreads, 148 * 3));
+  KL;
+  k_taylor_dia_short<<<grid, kShortThreads, smem, st>>>(a, D, fail_rows, fail_count);
+}
+}  // namespace sx

@@ -302,7 +302,7 @@ def test_taylor_pull_bit_exact(B, seed):
     assert np.array_equal(G.val, Ct.val)
 
 
-@pytest.mark.parametrize("name", ["heat2d", "structural", "heat3d"])
+@pytest.mark.parametrize("name", ["heat2d", "structural", "heat3d", "heat1d", "banded1d"])
 def test_taylor_dia_bit_exact(B, name):
     """Unfiltered Taylor phase (filter off, N = 0) through the diagonal push kernel K5d:
     every term S~ = S^ H0 / i accumulates k ascending with _rn products and sums, the
@@ -312,8 +312,12 @@ def test_taylor_dia_bit_exact(B, name):
         H = laplacian_2d(40, 40, 0.6, "pm10", seed=3)
     elif name == "structural":
         H = structural_state_space(12, 10, 0.5, seed=4)
-    else:
+    elif name == "heat3d":
         H = laplacian_3d(8, 7, 6, 0.25, "u0812", seed=5)
+    elif name == "heat1d":  # short rows: the thread-per-row kernel K5s
+        H = tridiag(3001, 0.45, -0.9, 0.45)
+    else:  # 5 diagonals, short rows, ragged ends (K5s)
+        H = random_banded(2000, 2, 1.0, 0.3, seed=6)
     opts = dict(filter=0, force_N=0, force_M=9)
     Eg, st = run_gpu(B, H, kernel=7, **opts)
     Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS, **opts)
