@@ -2108,7 +2108,9 @@ static void do_run(sexpm_plan_s &P) {
     return (double)ms;
   };
   CK(cudaEventRecord(ev_start, st));
-  P.dia_short_ok = true;  // the first Taylor term tries the short-row kernel K5s
+  // the first Taylor term tries the short-row kernel K5s only if S^_2 = H0 H0 / 2 can fit
+  // its window: a row of H0 H0 spans at most 2 (dmax - dmin) + 1 columns
+  P.dia_short_ok = 2 * ((int64_t)P.dia_dmax - P.dia_dmin) + 1 <= 64;
   const int64_t nl = P.row_end - P.row_begin;
   DCsr &H0loc = P.H0loc;
   DCsr &T = P.T, &Tn = P.Tn, &Sc = P.S, &Sn = P.Sn;
