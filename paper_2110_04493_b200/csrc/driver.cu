@@ -525,11 +525,7 @@ static void build_transpose(sexpm_plan_s &P, const CsrView &Bv, int64_t ncols, D
   launch_col_count(Bv, ccnt.p, st);
   DBuf<int64_t> cnt64, cursor;
   cnt64.alloc((size_t)std::max<int64_t>(ncols, 1), st);
-  std::vector<int32_t> hc32((size_t)ncols);
-  CK(cudaMemcpyAsync(hc32.data(), ccnt.p, ncols * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  std::vector<int64_t> hc64(hc32.begin(), hc32.end());
-  CK(cudaMemcpyAsync(cnt64.p, hc64.data(), ncols * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  launch_i32_to_i64(ccnt.p, ncols, cnt64.p, st);
   BT.nrows = ncols;
   BT.row0 = 0;
   BT.nnz = Bv.nnz;
@@ -1845,12 +1841,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     w.scan_tmp.ensure((size_t)scan_tmp_elems(P.n) + 1, st);
     // row_off = rp[0..n), row_cnt = rp diff
     launch_copy_i64_offset(Hraw.rp.p, P.n, 0, w.row_off.p, st);
-    std::vector<int64_t> hrp((size_t)P.n + 1);
-    CK(cudaMemcpyAsync(hrp.data(), Hraw.rp.p, hrp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::vector<int64_t> hc((size_t)P.n);
-    for (int64_t r = 0; r < P.n; r++) hc[r] = hrp[r + 1] - hrp[r];
-    CK(cudaMemcpyAsync(w.row_cnt.p, hc.data(), hc.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    launch_row_lengths(Hraw.rp.p, P.n, w.row_cnt.p, st);
     launch_compact_count(P.n, w.row_off.p, w.row_cnt.p, Hraw.val.p, 0.0, w.cnt.p, st);
     DCsr Hc;
     Hc.nrows = P.n;

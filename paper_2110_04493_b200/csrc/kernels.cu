@@ -5458,3 +5458,12 @@ void launch_taylor_dia_short(const NumericArgs &a, const DiaView &D, int32_t *fa
   k_taylor_dia_short<<<grid, kShortThreads, smem, st>>>(a, D, fail_rows, fail_count);
 }
 }  // namespace sx
+
+namespace sx {
+// out64[i] = in32[i] (plan-time helper, no host round trip)
+void launch_i32_to_i64(const int32_t *in, int64_t n, int64_t *out, cudaStream_t st) {
+  if (n == 0) return;
+  KL;
+  k_i32_to_i64<<<grid_for(n, kThreads), kThreads, 0, st>>>(in, n, out);
+}
+}  // namespace sx

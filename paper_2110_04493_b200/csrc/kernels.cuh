@@ -280,6 +280,7 @@ void launch_sort_rows(const int64_t *rp, int64_t n, const int32_t *kin, const do
 // K5s: Taylor product for short rows (thread per row, output span <= 64 columns)
 void launch_taylor_dia_short(const NumericArgs &a, const DiaView &D, int32_t *fail_rows, int *fail_count,
                              cudaStream_t st);
+void launch_i32_to_i64(const int32_t *in, int64_t n, int64_t *out, cudaStream_t st);
 void launch_add_rowlen(const int64_t *rp, const int64_t *alen, const int64_t *b, int64_t n,
                        int64_t *out, cudaStream_t st);
 // identity rows for rows [row0, row0+nrows)
