@@ -201,8 +201,12 @@ int or_plan(double norm, double eps_tol, int m_cap, int n_window, int *M_out, in
  * Output: keep[p] = 1 for the entries of A~ = A - b_n.  Returns the number of
  * passes; *tau_final = last eps_f (entries kept are exactly |x| > tau_final);
  * *dropped = ||A - A~||_F.
- * Readings: R1 scalar b_0 = 1, m_0 = 1 as printed; if the loop never
- * runs, A~ = A - b_0 = 0.  R2 strict '>'.  R3 eps_g = 0 -> no filter. */
+ * Readings: R1 m_0 = 1 as printed and the first pass is unconditional:
+ * Theorem 4.1's proof starts from "n = 0, m_0 = 1, eps_f^(1) = eps_g, b_1"
+ * (P:384), and only then does ||A - A~|| <= eps_g (1 + e_r) hold for
+ * every eps_g (the printed scalar b_0 = 1 would skip the loop and drop all of A
+ * whenever eps_g (1 + e_r) >= 1).  Identical to the printed b_0 = 1 whenever
+ * eps_g (1 + e_r) < 1.  R2 strict '>'.  R3 eps_g = 0 -> no filter. */
 #define OR_MAX_PASSES 256
 int or_alg41(int64_t cnt, const double *x, double eps_g, double e_r, uint8_t *keep,
              double *tau_final, double *dropped, double *tau_hist, int hist_cap) {
@@ -212,15 +216,15 @@ int or_alg41(int64_t cnt, const double *x, double eps_g, double e_r, uint8_t *ke
     *dropped = 0.0;
     return 0;
   }
-  /* step 1: m_0 = 1, b_0 = 1, n = 0, residual matrix b_0 = A */
+  /* step 1: m_0 = 1, n = 0, residual matrix b_0 = A (R1: first pass always runs) */
   uint8_t *in_res = (uint8_t *)malloc((size_t)(cnt > 0 ? cnt : 1));
   for (int64_t p = 0; p < cnt; p++) in_res[p] = 1;
   long double m = 1.0L, b = 1.0L;
   long double eg = eps_g;
   long double epsf = INFINITY;
   int n = 0;
-  /* step 2 */
-  while (b > eg * (1.0L + (long double)e_r)) {
+  /* step 2 (R1: tested after each pass, the first pass unconditional) */
+  do {
     epsf = eg / m;                             /* eps_f^{(n+1)} = eps_g / m_n */
     long double s = 0.0L;
     for (int64_t p = 0; p < cnt; p++) {
@@ -236,19 +240,14 @@ int or_alg41(int64_t cnt, const double *x, double eps_g, double e_r, uint8_t *ke
     if (n < hist_cap && tau_hist) tau_hist[n] = (double)epsf;
     n++;
     if (n >= OR_MAX_PASSES) break;             /* Theorem 4.1 guard; never hit in tests */
-  }
+  } while (b > eg * (1.0L + (long double)e_r));
   /* step 3: A~ = A - b_n */
   long double d = 0.0L;
   for (int64_t p = 0; p < cnt; p++) {
-    if (n == 0) {
-      keep[p] = 0; /* R1: loop never ran, b_0 = A, A~ = 0 */
-      d += (long double)x[p] * (long double)x[p];
-    } else {
-      keep[p] = (uint8_t)(!in_res[p]);
-      if (in_res[p]) d += (long double)x[p] * (long double)x[p];
-    }
+    keep[p] = (uint8_t)(!in_res[p]);
+    if (in_res[p]) d += (long double)x[p] * (long double)x[p];
   }
-  *tau_final = (n == 0) ? INFINITY : (double)epsf;
+  *tau_final = (double)epsf;
   *dropped = (double)sqrtl(d);
   free(in_res);
   return n;

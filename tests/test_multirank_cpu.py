@@ -100,15 +100,17 @@ def _worker(rank, port, T_full_parts, eps_g, result_q):
     Bm = _rows_as_full(T, need_lo, need_hi)
     A = _rows_as_full(T, r0, r1)
     Ct = O.spgemm(A, Bm, 2.0, 1.0)
-    # Algorithm 4.1 with rank-order scalar sums (R1: b0 = 1, m0 = 1)
+    # Algorithm 4.1 with rank-order scalar sums (R1: m0 = 1, first pass unconditional)
     vals = Ct.val
-    m, b, tau, passes = 1.0, 1.0, float("inf"), 0
-    while b > eps_g * 1.1:
+    m, tau, passes = 1.0, float("inf"), 0
+    while True:
         tau = eps_g / m
         s = _allsum(float(np.sum(vals[np.abs(vals) <= tau] ** 2)))
         b = np.sqrt(s)
         m = b / tau
         passes += 1
+        if b <= eps_g * 1.1:
+            break
     keep = np.abs(vals) > tau
     rows = np.repeat(np.arange(n), np.diff(Ct.rowptr))[keep]
     result_q.put((rank, rows, Ct.col[keep], vals[keep], tau, passes))

@@ -76,8 +76,30 @@ def test_eps_zero_keeps_nonzeros():
     assert keep.tolist() == [False, True, True, False] and passes == 0 and tau == 0.0
 
 
-def test_loop_never_runs_returns_zero_matrix():
-    # reading R1: scalar b_0 = 1; if 1 <= eps_g (1 + e_r) the loop never runs and A~ = A - A = 0
+def test_first_pass_unconditional_large_eps():
+    # reading R1: the first pass always runs (Theorem 4.1's proof starts from eps_f^(1) = eps_g,
+    # P:384), so the certificate ||A - A~||_F <= eps_g (1 + e_r) holds even when
+    # eps_g (1 + e_r) >= 1 (the printed scalar b_0 = 1 would drop all of A here: ||A - 0|| = 5.02)
     x = np.array([5.0, 0.5])
     keep, tau, passes, dropped, _ = O.alg41(x, 1.0, 0.1)
-    assert passes == 0 and not keep.any()
+    assert passes == 1 and tau == 1.0 and keep.tolist() == [True, False]
+    assert dropped == 0.5 <= 1.1
+
+
+@pytest.mark.parametrize("eps_g", [1.0, 3.0, 40.0, 1e3])
+def test_certificate_holds_for_large_eps(eps_g):
+    # ||A||_F >> 1 and eps_g (1 + e_r) >= 1: still ||A - A~||_F <= eps_g (1 + e_r)
+    rng = np.random.default_rng(int(eps_g))
+    x = rng.standard_normal(5000) * rng.choice([1e-3, 1.0, 30.0], 5000)
+    keep, tau, passes, dropped, _ = O.alg41(x, eps_g, 0.1)
+    assert passes >= 1
+    assert np.sqrt(np.sum(x[~keep] ** 2)) == pytest.approx(dropped, rel=1e-12)
+    assert dropped <= eps_g * 1.1 * (1 + 1e-12)
+    assert np.array_equal(keep, np.abs(x) > tau)
+
+
+def test_whole_matrix_below_budget_keeps_entries_above_eps():
+    # ||A||_F <= eps_g (1 + e_r): one pass at tau = eps_g keeps exactly |x| > eps_g
+    x = np.array([0.8, 0.3, -0.2])
+    keep, tau, passes, dropped, _ = O.alg41(x, 0.7, 0.5)
+    assert passes == 1 and keep.tolist() == [True, False, False]
