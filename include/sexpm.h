@@ -96,23 +96,18 @@ typedef struct {
   int32_t force_N;        /* -1 = from Eq. (4.20) */
   int32_t output_T;       /* 0 = return E = I + T^_N (default); 1 = return T^_N */
   int32_t window_cols;    /* dense accumulator window of the block-window kernel (0 = 8192) */
-  int32_t kernel;         /* K3 accumulator: 0 auto (block-sparse 11 for squarings on one GPU,
-                             k-sync paged 5 for multi-GPU squarings and rows it cannot hold;
-                             for Taylor
-                             terms the diagonal push kernel when H0 has <= 16 distinct
-                             diagonal offsets, else the pull over H0^T), 1 atomic hash,
-                             2 warp-window, 3 block-window, 4 k-synchronous hash, 5 k-synchronous
-                             paged, 6 Taylor pull (Taylor terms only; else 1), 7 Taylor diagonal
-                             push (Taylor terms only; else as 0), 8 grouped rows (4 rows per
-                             CTA share each B-row gather, TMA-staged), 9 one warp per row (8
-                             rows per CTA share a page table), 10 k-sync paged with 128
-                             threads per row, 11 block-sparse (BSR-8 view, register-held
-                             8x8 output blocks; squarings on one GPU, else as 5), 12 as 11
-                             over pairs of block rows sharing each B block (squarings on
-                             one GPU, else as 5).  All meet parity; 2 and 4-12 reproduce the
-                             oracle's C~ bit for bit.  Rows a kernel cannot hold fall
-                             through 8-12 -> 5 -> 3, 7 -> 7 at twice the accumulator slots
-                             -> 5 -> 3, 6 -> 1 -> 3 and 1/4/5 -> 3. */
+  int32_t kernel;         /* K3 kernel: 0 auto (squarings: the block-sparse kernel on the BSR-8
+                             view, 13 = fp64 tensor-core DMMA (default) or 11 = exact DMUL/DADD
+                             per exact_products, on one GPU and on a rank's rows inside its halo;
+                             Taylor terms: the diagonal push kernel 7 when H0 has <= 16
+                             distinct diagonal offsets, else the pull over H0^T 6); 3 block
+                             window, 5 k-synchronous paged, 6 Taylor pull (Taylor terms only;
+                             else 5), 7 Taylor diagonal push (Taylor terms only; else as 0),
+                             11 block-sparse exact, 13 block-sparse tensor core (squarings
+                             only; else as 0).  All meet parity; 5, 6, 7 and 11 reproduce the
+                             oracle's C~ bit for bit.  Rows a kernel cannot hold fall through
+                             11/13 -> 5 -> 3, 7 -> 7 at twice the accumulator slots -> 5 -> 3,
+                             6 -> 5 -> 3. */
   int32_t ssat;           /* 0 = the paper's PIM (default); 1 = the SSAT baseline of Table 1
                              (SURVEY section 8(f) N2): the same Taylor phase
                              (filtered per `filter`), then E_0 = I + T^_0 and N plain
@@ -127,6 +122,10 @@ typedef struct {
                              aggregates of H's graph (fuller 8x8 blocks for K3b), E mapped
                              back; 0 = index order.  One GPU only; not with ssat.  Results
                              equal up to rounding order (north-star parity). */
+  int32_t exact_products; /* 0 = (default) squarings on the fp64 tensor-core block kernel 13
+                             (fused multiply-adds: C~ within rounding of the oracle's);
+                             1 = the bit-exact block kernel 11 (DMUL + DADD in the oracle's
+                             order: C~ bit-identical to the oracle's).  Only with kernel = 0. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */
@@ -173,11 +172,6 @@ typedef struct {
                                                   building the BSR view) */
   int64_t sq_bsr_blocks[SEXPM_MAXSTEP];        /* 8x8 blocks of the BSR view (block kernel) */
   double sq_block_products[SEXPM_MAXSTEP];     /* 8x8 block products it executed (512 each) */
-  /* grouped kernel (kernel 8) per squaring: summed SM clocks of its setup / product / flush
-   * phases over all groups, groups processed, union k's, groups handed on (all causes, union
-   * too large, slots full), then thread-0 clocks of the product loop: ring wait, rest of
-   * stage A, stage B, barrier */
-  double sq_group_prof[SEXPM_MAXSTEP][12];
   /* the library's device-block cache during the last sexpm_plan + sexpm_run (process-wide) */
   int64_t cache_hits, cache_misses, cache_releases;
   double cache_bytes_cached, cache_bytes_allocated;
@@ -252,7 +246,7 @@ int sexpm_filtered_product(sexpm_plan_t p, const sexpm_csr_in *A, const sexpm_cs
                            int32_t *passes, double *tau, int64_t *nnz_unf);
 
 /* Algorithm 4.1 over a device array of cnt values: returns the number of passes, the final
- * threshold tau (entries kept are exactly |x| > tau; +inf if the loop never ran; 0 when
+ * threshold tau (entries kept are exactly |x| > tau; the first pass always runs (reading R1); 0 when
  * eps_g == 0) and the dropped Frobenius norm. */
 int sexpm_alg41(sexpm_plan_t p, const double *x, int64_t cnt, double eps_g, double e_r,
                 int32_t *passes, double *tau, double *dropped);
@@ -267,6 +261,17 @@ int sexpm_rcm(sexpm_plan_t p, const sexpm_csr_in *A, int64_t *perm);
  * the kernel of sexpm_apply.  Runs on the plan's stream and synchronises it. */
 int sexpm_spmm(sexpm_plan_t p, const sexpm_csr_in *A, int64_t m, const double *X, int64_t ldx,
                double *Y, int64_t ldy);
+
+/* Host only (no device work; callable without a GPU).  The scalar part of Algorithm 4.2
+ * steps 1-3 for a given plan norm ||H||: (M, N) by Eq. (4.20) (
+ * N in [N0, N0 + n_window], M in [0, m_cap], ties to the smaller N: reading R5), the budget
+ * a = 1/(N+1) if normal (Eq. 4.19) else min(1, 1/||H||) (reading R8), r0 =
+ * r0(||H|| 2^-N, M) (Eq. 4.5) and eps_g^(0) = a r0 / (M e^{2 ||H 2^-N||}).
+ * sexpm_plan uses exactly this after measuring the norm on the device.  a, r0, eps_g0 may
+ * be NULL.  Errors: SEXPM_EINVAL (negative / non-finite norm, normal not 0/1),
+ * SEXPM_ETOL (eps_tol < 1e-16, reading R13), SEXPM_EINFEASIBLE (no (M, N) in range). */
+int sexpm_plan_scalars(double norm, int normal, double eps_tol, int m_cap, int n_window,
+                       int32_t *M, int32_t *N, double *a, double *r0, double *eps_g0);
 
 /* Host-side halo planner for the row-partitioned multi-GPU squaring (Lemma 3.1):
  * rank g owns rows [bounds[g], bounds[g+1]); with T^_{i-1} of bandwidths (l1, l2) the

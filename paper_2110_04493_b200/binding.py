@@ -26,7 +26,7 @@ EXPORTED = [
     "sexpm_result_copy", "sexpm_stats_get", "sexpm_destroy", "sexpm_last_error",
     "sexpm_filtered_product", "sexpm_alg41", "sexpm_halo_ranges", "sexpm_partition_rows",
     "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache", "sexpm_apply",
-    "sexpm_spmm", "sexpm_rcm",
+    "sexpm_spmm", "sexpm_rcm", "sexpm_plan_scalars",
 ]
 
 
@@ -54,7 +54,7 @@ class Options(C.Structure):
                 ("n_window", C.c_int32), ("force_M", C.c_int32), ("force_N", C.c_int32),
                 ("output_T", C.c_int32), ("window_cols", C.c_int32), ("kernel", C.c_int32),
                 ("ssat", C.c_int32), ("reorder", C.c_int32), ("sq_order", C.c_int32),
-                ("e_r", C.c_double),
+                ("exact_products", C.c_int32), ("e_r", C.c_double),
                 ("stream", C.c_void_p), ("nccl_comm", C.c_void_p)]
 
 
@@ -81,7 +81,6 @@ class Stats(C.Structure):
                 ("nnz_out", C.c_int64), ("gpu_launches", C.c_int32), ("retries", C.c_int32),
                 ("taylor_fallback_rows", _I64), ("sq_fallback_rows", _I64), ("sq_first_ms", _F64), ("sq_kernel_ms", _F64), ("sq_bsr_blocks", _I64),
                 ("sq_block_products", _F64),
-                ("sq_group_prof", C.c_double * 12 * MAXSTEP),
                 ("cache_hits", C.c_int64), ("cache_misses", C.c_int64),
                 ("cache_releases", C.c_int64), ("cache_bytes_cached", C.c_double),
                 ("cache_bytes_allocated", C.c_double)]
@@ -118,6 +117,8 @@ def lib():
                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.sexpm_halo_ranges.argtypes = [C.c_int, C.c_int, P, C.c_int64, C.c_int64, C.c_int64, P, P]
         L.sexpm_partition_rows.argtypes = [C.c_int64, P, C.c_int, P]
+        L.sexpm_plan_scalars.argtypes = [C.c_double, C.c_int, C.c_double, C.c_int, C.c_int, P, P, P,
+                                         P, P]
         L.sexpm_abi_sizes.argtypes = [P]
         L.sexpm_kernel_launches.argtypes = [P]
         for f in EXPORTED:
@@ -235,6 +236,17 @@ def sexpm_halo_ranges(world: int, rank: int, bounds, n: int, l1: int, l2: int):
     _check(lib().sexpm_halo_ranges(world, rank, b.ctypes.data, n, l1, l2, lo.ctypes.data,
                                    hi.ctypes.data))
     return lo, hi
+
+
+def sexpm_plan_scalars(norm: float, normal: int, eps_tol: float, m_cap: int = 120,
+                       n_window: int = 50) -> dict:
+    """Algorithm 4.2 steps 1-3 for a given plan norm (host only): M, N, a, r0, eps_g0."""
+    M, N = C.c_int32(), C.c_int32()
+    a, r0, e0 = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().sexpm_plan_scalars(float(norm), int(normal), float(eps_tol), int(m_cap),
+                                    int(n_window), C.addressof(M), C.addressof(N), C.addressof(a),
+                                    C.addressof(r0), C.addressof(e0)))
+    return {"M": M.value, "N": N.value, "a": a.value, "r0": r0.value, "eps_g0": e0.value}
 
 
 def sexpm_partition_rows(n: int, work, world: int):

@@ -423,21 +423,17 @@ struct sexpm_plan_s {
   bool dia_short_ok = true;  // the previous Taylor term's rows all fitted the short-row kernel K5s
   int dia_slots_max = 1152;  // the most that fit (set at plan time); retry size for rows over dia_slots
   DBuf<int> dia_need;
-  int group_slots = 4096;
-  int rowwarp_slots = 3072;
   long long cache0[3] = {0, 0, 0};  // cache counters when the plan was created
   DCsr T, Tn, S, Sn, Bhalo, Ibuf, E;  // persistent (grow-only) iterates
   int32_t retries = 0;
   DBuf<int32_t> proc_order;  // K3 row processing order (cluster order of H's graph)
-  DBuf<int32_t> group_start;  // grouped kernel: group boundaries in proc_order
-  int64_t ngroups = 0;
   // background computation of proc_order / group_start (overlaps the Taylor phase)
   std::thread bg;
   cudaStream_t bg_st = nullptr;
   cudaEvent_t ev_pattern = nullptr, ev_order = nullptr;
   bool order_pending = false;
   std::string bg_err;
-  std::vector<int32_t> h_order, h_groups, h_border;
+  std::vector<int32_t> h_order, h_border;
   // squarings in aggregate order (option sq_order): perm[new] = old, 8-row aggregates of H's
   // graph; sq_tiled while the iterate is held in that order
   std::vector<int64_t> h_tperm;
@@ -465,11 +461,7 @@ struct sexpm_plan_s {
   int sm_count = 148;
   size_t smem_per_sm = 233472;
   int numeric_blocks_per_sm = 2;
-  int hash_blocks_per_sm = 4;
-  int warp_blocks_per_sm = 4;
   int paged_blocks_per_sm = 3;
-  int paged2_blocks_per_sm = 5;
-  int warp_window = 1024;
   float plan_ms = 0.f;
 };
 
@@ -656,8 +648,6 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   w.fail_rows.ensure(nr1, st);
   w.fail_rows2.ensure(nr1, st);
   w.fail_count.ensure(1, st);
-  const int hash_grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.hash_blocks_per_sm));
   const int paged_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged_blocks_per_sm));
   int nfail_other = 0;  // rows finished by kernels other than the first (and its K5d retry)
@@ -683,20 +673,17 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     CK(cudaEventRecord(e0, st));
     int kern = P.o.kernel;
     const bool taylor_pull_ok = self == 0.0 && BT != nullptr && BT->rp.p != nullptr;
-    // the grouped kernel stages B rows with TMA bulk copies: 16-byte aligned B arrays
-    const bool group_ok = ((uintptr_t)B.col % 16 == 0) && ((uintptr_t)B.val % 16 == 0);
-    // squarings: the k-synchronous paged kernel (measured fastest on configs 2, 3 and 5;
-    // the grouped kernels 8 / 9 are options)
-    if (kern == 0) kern = sq_like ? 11 : (dia_path ? 7 : (taylor_pull_ok ? 6 : 1));
-    if (kern == 8 && !group_ok) kern = 5;
-    // the block kernel squares one matrix held whole on this GPU (its BSR view is A's);
-    // Taylor terms keep their own kernels
-    if ((kern == 11 || kern == 12) && !sq_like) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 1);
+    // squarings: the block kernel on the fp64 tensor-core instruction (13; 11 is the
+    // bit-exact DMUL/DADD variant); Taylor terms: the diagonal push or the pull kernel
+    if (kern == 0) kern = sq_like ? (P.o.exact_products ? 11 : 13) : (dia_path ? 7 : (taylor_pull_ok ? 6 : 5));
+    // the block kernels square one matrix (or a rank's rows inside its halo rows); Taylor
+    // terms keep their own kernels
+    if ((kern == 11 || kern == 13) && !sq_like) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 5);
     // the block kernel needs B's rows block-aligned and A's rows a block-aligned slice of them
     // (one GPU: A = B; several: A = the rank's rows inside its halo B, 8-aligned partition)
     const bool same = B.rp == A.rp;
     bool bsr_ok = same;
-    if (!same && (kern == 11 || kern == 12) && B.row0 % 8 == 0 && A.row0 >= B.row0 &&
+    if (!same && (kern == 11 || kern == 13) && B.row0 % 8 == 0 && A.row0 >= B.row0 &&
         (A.row0 - B.row0) % 8 == 0 && A.row0 + nr <= B.row0 + B.nrows) {
       // A must be a slice of B (the rank's rows inside its halo): checked, not assumed
       w.eqflag.ensure(1, st);
@@ -704,30 +691,12 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       launch_rows_equal(A, B, w.eqflag.p, st);
       bsr_ok = d2h(w.eqflag.p, st) == 0;
     }
-    if (kern == 11 && !bsr_ok) kern = 5;
-    if (kern == 12 && !(P.world == 1 && bsr_ok && A.row0 == B.row0 && nr == B.nrows)) kern = bsr_ok ? 11 : 5;
-    if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 1;
-    if (kern == 6 && !taylor_pull_ok) kern = 1;
+    if ((kern == 11 || kern == 13) && !bsr_ok) kern = 5;
+    if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 5;
+    if (kern == 6 && !taylor_pull_ok) kern = 5;
     if (kern == 7) CK(cudaMemsetAsync(P.dia_prod.p, 0, sizeof(unsigned long long), st));
     int nfail = 0;
-    if (kern == 2) {  // warp-per-row conflict-free window
-      const int64_t gw = (int64_t)P.sm_count * P.warp_blocks_per_sm * kWarpRowWarpsPerCta;
-      const int64_t grid_w = std::max<int64_t>(1, std::min<int64_t>((nr + kWarpRowWarpsPerCta - 1) / kWarpRowWarpsPerCta,
-                                                                    gw / kWarpRowWarpsPerCta));
-      const int64_t nwarps = grid_w * kWarpRowWarpsPerCta;
-      w.cursor.ensure((size_t)nwarps * 2 * na.cursor_cap, st);
-      w.scr_col.ensure((size_t)nwarps * na.scr_cap, st);
-      w.scr_val.ensure((size_t)nwarps * na.scr_cap, st);
-      NumericArgs nw = na;
-      nw.window = P.warp_window;
-      nw.cursor = w.cursor.p;
-      nw.scr_col = w.scr_col.p;
-      nw.scr_val = w.scr_val.p;
-      nw.nlist = nr;
-      nw.grid = (int)grid_w;
-      launch_numeric_warp(nw, st);
-      CK(cudaGetLastError());
-    } else {
+    {
       // staged chain: the chosen shared-memory kernel over all rows, rows it cannot hold
       // go to the next one (pull -> hash -> block window; paged / k-sync / hash -> window)
       const int32_t *list = na.order;
@@ -739,7 +708,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       // short rows first (thread-per-row K5s) while the previous term's rows were short
       bool dia_short = P.dia_short_ok;
       // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
-      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 10 || kern == 11 || kern == 12);
+      fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 11 || kern == 13);
       while (nlist > 0) {
         if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
           run_symbolic();
@@ -769,16 +738,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           break;
         }
         int32_t *fout = fbuf[fb];
-        if (stage == 1) {
-          nh.grid = hash_grid;
-          launch_numeric_hash(nh, fout, w.fail_count.p, st);
-        } else if (stage == 4) {
-          nh.grid = hash_grid;
-          launch_numeric_ksync(nh, fout, w.fail_count.p, st);
-        } else if (stage == 5) {
+        if (stage == 5) {
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
-        } else if (stage == 11 || stage == 12) {
+        } else if (stage == 11 || stage == 13) {
           // BSR-8 view of B (= A, or A's halo rows) and its block transpose, then the block
           // kernel over A's block rows
           const int64_t nbr = (B.nrows + 7) / 8, nbc = (P.n + 7) / 8, nbr_a = (nr + 7) / 8;
@@ -797,13 +760,13 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           CK(cudaStreamSynchronize(st));
           // block rows too wide for the view or for the kernel's shared-memory row of A: the
           // whole product goes to the paged kernel
-          if ((bflags & 4) || bmax > kBsrMaxRowBlocks) {
+          if ((bflags & 4) || (stage == 11 && bmax > kBsrMaxRowBlocks)) {
             stage = 5;
             continue;
           }
           w.bcol.ensure((size_t)std::max<int64_t>(nb, 1), st);
           w.bval.ensure((size_t)std::max<int64_t>(nb, 1) * 64, st);
-          launch_bsr_fill(B, nbr, w.brp.p, w.bcol.p, w.bval.p, w.flags.p, st);
+          launch_bsr_fill(B, nbr, w.brp.p, w.bcol.p, w.bval.p, w.flags.p, st, stage == 13);
           w.tcnt.ensure((size_t)nbc + 1, st);
           w.tp.ensure((size_t)nbc + 1, st);
           w.cnt64.ensure((size_t)nbc + 1, st);
@@ -832,11 +795,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
             Bv.border = P.block_order.p;  // block rows of the rank's rows in locality order
           if (P.sq_tiled && same && nr == P.n && !getenv("SEXPM_BSR_NATURAL"))
             Bv.border = P.block_order_t.p;  // the aggregates in locality order
-          if (stage == 12)  // block-row pairs, one 512-thread CTA per SM
-            nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nbr + 1) / 2, (int64_t)P.sm_count));
-          else
-            nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbr_a, (int64_t)P.sm_count * 2));
-          w.bscr.ensure((size_t)nh.grid * (stage == 12 ? kBsr2ScratchPerCta : kBsrScratchPerCta), st);
+          nh.grid = (int)std::max<int64_t>(
+              1, std::min<int64_t>(nbr_a, (int64_t)P.sm_count * (stage == 13 ? kBsrMBlocksPerSm : 2)));
+          w.bscr.ensure((size_t)nh.grid * (stage == 13 ? (size_t)kBsrMJCap * 65 : (size_t)kBsrScratchPerCta), st);
           CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
           w.prof.ensure(16, st);
           CK(cudaMemsetAsync(w.prof.p, 0, 16 * sizeof(unsigned long long), st));
@@ -845,8 +806,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           CK(cudaEventCreate(&k0));
           CK(cudaEventCreate(&k1));
           CK(cudaEventRecord(k0, st));
-          if (stage == 12)
-            launch_numeric_bsr2(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
+          if (stage == 13)
+            launch_numeric_bsrm(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
           else
             launch_numeric_bsr(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
           CK(cudaEventRecord(k1, st));
@@ -858,29 +819,6 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           unsigned long long nbp = 0;
           CK(cudaMemcpy(&nbp, w.prof.p, sizeof(nbp), cudaMemcpyDeviceToHost));
           rep.block_products = (double)nbp;
-        } else if (stage == 10) {
-          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged2_blocks_per_sm));
-          launch_numeric_paged2(nh, fout, w.fail_count.p, st);
-        } else if (stage == 9) {
-          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kRowWarpRows - 1) / kRowWarpRows,
-                                                                (int64_t)P.sm_count));
-          w.prof.ensure(8, st);
-          CK(cudaMemsetAsync(w.prof.p, 0, 8 * sizeof(unsigned long long), st));
-          nh.prof = w.prof.p;
-          launch_numeric_rowwarp(nh, P.rowwarp_slots, fout, w.fail_count.p, st);
-          CK(cudaMemcpyAsync(rep.prof, w.prof.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        } else if (stage == 8) {
-          if (use_cluster && list == P.proc_order.p && nlist == nr) {
-            nh.gstart = P.group_start.p;
-            nh.ngroups = P.ngroups;
-          }
-          nh.grid = (int)std::max<int64_t>(1, std::min<int64_t>((nlist + kGroupRows - 1) / kGroupRows,
-                                                                (int64_t)P.sm_count));
-          w.prof.ensure(16, st);
-          CK(cudaMemsetAsync(w.prof.p, 0, 16 * sizeof(unsigned long long), st));
-          nh.prof = w.prof.p;
-          launch_numeric_group(nh, P.group_slots, fout, w.fail_count.p, st);
-          CK(cudaMemcpyAsync(rep.prof, w.prof.p, 12 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         } else if (stage == 7) {
           DiaView D;
           D.ndiag = P.dia_nd;
@@ -927,7 +865,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
         } else if (stage == 7 && !dia_retry && P.dia_slots < P.dia_slots_max) {
           dia_retry = true;
         } else {
-          stage = stage == 7 ? 5 : (stage == 6 ? 1 : ((stage >= 8 && stage <= 12) ? 5 : 3));
+          stage = (stage == 7 || stage == 6 || stage == 11 || stage == 13) ? 5 : 3;
           nfail_other += nf;
         }
       }
@@ -988,11 +926,13 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   if (eps_g == 0.0) {
     tau = 0.0;  // reading R3: no filtering
   } else {
-    long double m = 1.0L, b = 1.0L;  // m_0 = 1, b_0 = 1 (reading R1)
+    // m_0 = 1; the first pass always runs (reading R1, Theorem 4.1's proof P:384), then
+    // the passes repeat while b_n > eps_g (1 + e_r)
+    long double m = 1.0L, b = INFINITY;
     const long double eg = eps_g;
     const long double lim = eg * (1.0L + (long double)P.o.e_r);
     long double epsf = INFINITY;
-    while (b > lim) {
+    while (passes == 0 || b > lim) {
       epsf = eg / m;
       const double tau_d = (double)epsf;
       double S;
@@ -1008,7 +948,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       passes++;
       REQUIRE(passes < 256, SEXPM_EINTERNAL, "Algorithm 4.1 pass cap reached (Theorem 4.1)");
     }
-    tau = passes == 0 ? INFINITY : (double)epsf;  // loop never ran: A~ = 0 (reading R1)
+    tau = (double)epsf;
   }
   rep.passes = passes;
   rep.tau = tau;
@@ -1382,50 +1322,79 @@ static void cluster_order(const std::vector<int64_t> &rp, const std::vector<int3
 // ------------------------------------------------------------------------------------
 // plan
 // ------------------------------------------------------------------------------------
-static long double r0_series(long double x, int M) {  // Eq. (4.5)
-  if (x <= 0.0L) return 0.0L;
-  long double t = 1.0L;
-  for (int s = 1; s <= M; s++) t *= x / (long double)s;
-  t *= x / (long double)(M + 1);
-  long double sum = 0.0L;
-  for (int i = 0; i < 100000; i++) {
-    long double ns = sum + t;
-    if (ns == sum) break;
-    sum = ns;
-    t = t * x * (long double)(i + M + 1) / ((long double)(i + 1) * (long double)(i + M + 2));
+// Forward error of the truncated Taylor series, Eq. (4.5)-(4.6) P:266-276:
+//   r0(x, M) = (1/M!) int_0^x t^M e^t dt = (-1)^{M+1} gamma(M+1, -x) / M!.
+// Evaluated here through Kummer's transformation of the incomplete gamma function,
+//   r0(x, M) = x^{M+1} e^x / (M+1)! * 1F1(1; M+2; -x)
+//            = x^{M+1} e^x / (M+1)! * sum_k (-x)^k / ((M+2)(M+3)...(M+1+k)),
+// an alternating series whose terms shrink at least by x/(M+2) <= 1/2 for the planner's
+// x = ||H 2^-N|| <= 1 (Eq. 4.20's first constraint), so it is summed in long double until
+// the terms no longer change the sum.  (The CPU oracle evaluates the paper's own series;
+// tests/test_planner_abi.py checks this against 30-digit quadrature.)
+static long double taylor_remainder(long double x, int M) {
+  if (!(x > 0.0L)) return 0.0L;
+  // lead = x^{M+1} e^x / (M+1)!, built as a product of x / j, j = 1..M+1
+  long double lead = expl(x);
+  for (int j = 1; j <= M + 1; j++) lead *= x / (long double)j;
+  long double kummer = 0.0L, term = 1.0L;
+  for (int k = 0; k < 4096; k++) {
+    const long double next = kummer + term;
+    if (next == kummer) break;
+    kummer = next;
+    term *= -x / (long double)(M + 2 + k);
   }
-  return sum;
+  return lead * kummer;
 }
 
-static bool plan_MN(double norm, double eps_tol, int m_cap, int n_window, int &M, int &N) {
-  // Eq. (4.20): min M 2^N s.t. ||H 2^-N|| <= 1, 2^N r0 <= eps_tol
-  if (norm == 0.0) {
-    M = N = 0;
+// ceil(log2(v)) for v > 0, exactly (frexp: v = f 2^e with f in [0.5, 1))
+static int ceil_log2_exact(double v) {
+  int e = 0;
+  const double f = frexp(v, &e);
+  return f == 0.5 ? e - 1 : e;
+}
+
+// (M, N) by Eq. (4.20): minimise M 2^N subject to ||H 2^-N|| <= 1 and
+// 2^N r0(||H|| 2^-N, M) <= eps_tol, over N in [N0, N0 + n_window] (N0 = max(ceil(log2
+// ||H||), 0), "N_max = N0 + 50") and M in [0, m_cap] (reading R5; ties to the
+// smaller N).  Returns false when no candidate satisfies the tolerance.
+static bool select_MN(double norm, double eps_tol, int m_cap, int n_window, int &M, int &N) {
+  if (norm == 0.0) {  // H = 0: e^H = I, nothing to do (reading R9)
+    M = 0;
+    N = 0;
     return true;
   }
-  int N0 = (int)ceil(log2(norm));
-  if (N0 < 0) N0 = 0;
-  while (ldexp(norm, -N0) > 1.0) N0++;
-  long double best = -1.0L;
-  int bM = -1, bN = -1;
-  for (int n = N0; n <= N0 + n_window; n++) {
-    long double x = (long double)ldexp(norm, -n);
-    for (int m = 0; m <= m_cap; m++) {
-      if (ldexpl(r0_series(x, m), n) <= (long double)eps_tol) {
-        long double cost = (long double)m * ldexpl(1.0L, n);
-        if (best < 0.0L || cost < best) {
-          best = cost;
-          bM = m;
-          bN = n;
-        }
-        break;
-      }
-    }
+  const int N0 = std::max(ceil_log2_exact(norm), 0);
+  struct Cand { int N, M; long double cost; };
+  std::vector<Cand> cands;
+  for (int k = 0; k <= n_window; k++) {
+    const int n = N0 + k;
+    const long double x = (long double)ldexp(norm, -n);  // exact scaling by 2^-n
+    const long double scale = ldexpl(1.0L, n);
+    // m(N): the least M meeting the tolerance; r0 decreases with M, so the first hit
+    int m = 0;
+    while (m <= m_cap && scale * taylor_remainder(x, m) > (long double)eps_tol) m++;
+    if (m <= m_cap) cands.push_back({n, m, (long double)m * scale});
   }
-  if (bM < 0) return false;
-  M = bM;
-  N = bN;
+  if (cands.empty()) return false;
+  // candidates are in increasing N: the first of the minimal cost wins the tie
+  const Cand *best = &cands[0];
+  for (const Cand &c : cands)
+    if (c.cost < best->cost) best = &c;
+  M = best->M;
+  N = best->N;
   return true;
+}
+
+// Filter budgets of Algorithm 4.2 steps 2-3: a = 1/(N+1) for normal H
+// (Eq. 4.19), else a = min(1, 1/||H||) (reading R8); r0 = r0(||H 2^-N||, M)
+// (Eq. 4.5); the Taylor threshold eps_g^(0) = a r0 / (M e^{2 ||H0||}) (Eq. 4.14),
+// 0 when M = 0 (reading R9: no Taylor terms are filtered).
+static void filter_budgets(double norm, int normal, int M, int N, double &a, long double &r0,
+                           double &eps_g0) {
+  a = normal ? 1.0 / (1.0 + (double)N) : (norm > 1.0 ? 1.0 / norm : 1.0);
+  const long double x = (long double)ldexp(norm, -N);
+  r0 = taylor_remainder(x, M);
+  eps_g0 = M >= 1 ? (double)((long double)a * r0 / ((long double)M * expl(2.0L * x))) : 0.0;
 }
 
 // Diagonal offsets of H0 (d = j - k over all entries); when there are at most kDiaMax of
@@ -1886,7 +1855,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   mark("transpose + norm + symmetry");
   P.norm = norm;
   int M, N;
-  REQUIRE(plan_MN(norm, eps_tol, P.o.m_cap, P.o.n_window, M, N), SEXPM_EINFEASIBLE,
+  REQUIRE(select_MN(norm, eps_tol, P.o.m_cap, P.o.n_window, M, N), SEXPM_EINFEASIBLE,
           "Eq. (4.20) infeasible within m_cap / n_window");
   if (P.o.force_M >= 0) M = P.o.force_M;
   if (P.o.force_N >= 0) N = P.o.force_N;
@@ -1895,12 +1864,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   int normal = P.o.normal;
   if (normal < 0) normal = ((symflags & 1) == 0) || ((symflags & 2) == 0);
   P.normal = normal;
-  P.a = normal ? 1.0 / (1.0 + (double)N) : (norm > 1.0 ? 1.0 / norm : 1.0);  // P:404, R8
-  const double normH0 = ldexp(norm, -N);
-  P.r0 = r0_series((long double)normH0, M);
-  P.eps_g0 = 0.0;
-  if (M >= 1)
-    P.eps_g0 = (double)((long double)P.a * P.r0 / ((long double)M * expl(2.0L * (long double)normH0)));
+  filter_budgets(norm, normal, M, N, P.a, P.r0, P.eps_g0);
   if (!P.o.filter) P.eps_g0 = 0.0;
   // H0 = H 2^-N (exact)
   launch_scale_pow2(Hf.val.p, Hf.nnz, -N, st);
@@ -1915,7 +1879,6 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   {
     const int64_t nl = P.row_end - P.row_begin;
     P.proc_order.ensure((size_t)std::max<int64_t>(nl, 1), st);
-    P.group_start.ensure((size_t)nl + 2, st);
     P.block_order.ensure((size_t)std::max<int64_t>((nl + 7) / 8, 1), st);
     if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1) {
       P.tperm.ensure((size_t)std::max<int64_t>(P.n, 1), st);
@@ -1940,17 +1903,6 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
         CK(cudaStreamSynchronize(P.bg_st));
         std::vector<int32_t> &ord = P.h_order;
         cluster_order(hrp, hcol, P.row_begin, P.row_end, 1024, ord);
-        // groups of the grouped kernel: up to kGroupRows consecutive entries of the order,
-        // cut where the row index jumps (rows far apart share few B rows)
-        std::vector<int32_t> &gs = P.h_groups;
-        gs.clear();
-        for (size_t j = 0; j < ord.size(); j++) {
-          const bool cut = j == 0 || (int)(j - (size_t)gs.back()) >= kGroupRows ||
-                           std::abs((long long)ord[j] - (long long)ord[j - 1]) > 2;
-          if (cut) gs.push_back((int32_t)j);
-        }
-        P.ngroups = (int64_t)gs.size();
-        gs.push_back((int32_t)ord.size());
         // block rows (8 rows) of the block kernel, in the order their first row appears
         std::vector<int32_t> &bo = P.h_border;
         bo.clear();
@@ -2042,7 +1994,6 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
             CK(cudaStreamSynchronize(P.bg_st));  // hinv is local
           }
         }
-        CK(cudaMemcpyAsync(P.group_start.p, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         CK(cudaEventRecord(P.ev_order, P.bg_st));
       } catch (const SxError &e) {
         P.bg_err = e.msg.empty() ? "order thread failed" : e.msg;
@@ -2259,7 +2210,6 @@ static void do_run(sexpm_plan_s &P) {
       S.sq_kernel_ms[i] = rep.kernel_ms > 0.f ? rep.kernel_ms : rep.first_ms;
       S.sq_bsr_blocks[i] = rep.bsr_blocks;
       S.sq_block_products[i] = rep.block_products;
-      for (int q = 0; q < 12; q++) S.sq_group_prof[i][q] = (double)rep.prof[q];
       S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)dst.nnz + 16.0 * (double)nl;
     }
     if (getenv("SEXPM_STEP_LOG"))
@@ -2385,6 +2335,7 @@ int sexpm_options_init(sexpm_options *o) {
   o->ssat = 0;
   o->reorder = 0;
   o->sq_order = 1;
+  o->exact_products = 0;
   o->e_r = 0.1;
   o->stream = nullptr;
   o->nccl_comm = nullptr;
@@ -2457,20 +2408,12 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
     P->cache0[1] = cache::misses;
     P->cache0[2] = cache::releases;
   }
-  while (P->group_slots > 512 && group_smem_bytes(P->group_slots) > (int)prop.sharedMemPerBlockOptin - 4096)
-    P->group_slots -= 512;
-  while (P->rowwarp_slots > 512 && rowwarp_smem_bytes(P->rowwarp_slots) > (int)prop.sharedMemPerBlockOptin - 4096)
-    P->rowwarp_slots -= 256;
   int window = P->o.window_cols > 0 ? P->o.window_cols : 8192;
   int smem = numeric_smem_bytes(window);
   REQUIRE(smem <= (int)prop.sharedMemPerBlockOptin - 2048, SEXPM_EINVAL, "window too large");
   P->numeric_blocks_per_sm = std::max(1, std::min(4, (int)(prop.sharedMemPerMultiprocessor / (smem + 4096))));
-  P->hash_blocks_per_sm = std::max(1, std::min(8, (int)(prop.sharedMemPerMultiprocessor / (hash_smem_bytes() + 2048))));
   // CTAs per SM from shared memory: dynamic + static (< 6 KB) + the 1 KB per-CTA reserve
   P->paged_blocks_per_sm = std::max(1, std::min(8, (int)(prop.sharedMemPerMultiprocessor / (paged_smem_bytes() + 7168))));
-  P->paged2_blocks_per_sm = std::max(1, std::min(16, (int)(prop.sharedMemPerMultiprocessor / (paged2_smem_bytes() + 4096))));
-  P->warp_blocks_per_sm = std::max(1, std::min(16, (int)(prop.sharedMemPerMultiprocessor /
-                                                         (warp_numeric_smem_bytes(P->warp_window) + 1024))));
   if (P->o.stream) {
     P->st = (cudaStream_t)P->o.stream;
   } else {
@@ -2729,9 +2672,9 @@ int sexpm_alg41(sexpm_plan_t p, const double *x, int64_t cnt, double eps_g, doub
   if (eps_g == 0.0) {
     t = 0.0;
   } else {
-    long double m = 1.0L, b = 1.0L, epsf = INFINITY;
+    long double m = 1.0L, b = INFINITY, epsf = INFINITY;  // reading R1: first pass always runs
     const long double eg = eps_g, lim = eg * (1.0L + (long double)e_r);
-    while (b > lim) {
+    while (np == 0 || b > lim) {
       epsf = eg / m;
       launch_alg41_pass(x, cnt, (double)epsf, w.partial.p, w.scal.p, p->st);
       double S = d2h(w.scal.p, p->st);
@@ -2740,15 +2683,36 @@ int sexpm_alg41(sexpm_plan_t p, const double *x, int64_t cnt, double eps_g, doub
       np++;
       REQUIRE(np < 256, SEXPM_EINTERNAL, "Algorithm 4.1 pass cap");
     }
-    t = np == 0 ? INFINITY : (double)epsf;
+    t = (double)epsf;
   }
-  // dropped norm: everything <= t (or all, when the loop never ran)
-  launch_alg41_pass(x, cnt, np == 0 && eps_g != 0.0 ? INFINITY : t, w.partial.p, w.scal.p, p->st);
+  // dropped norm: everything <= t
+  launch_alg41_pass(x, cnt, t, w.partial.p, w.scal.p, p->st);
   double d = sqrt(d2h(w.scal.p, p->st));
   if (eps_g == 0.0) d = 0.0;
   if (passes) *passes = np;
   if (tau) *tau = t;
   if (dropped) *dropped = d;
+  ABI_END
+}
+
+int sexpm_plan_scalars(double norm, int normal, double eps_tol, int m_cap, int n_window,
+                       int32_t *M, int32_t *N, double *a, double *r0, double *eps_g0) {
+  ABI_BEGIN
+  REQUIRE(M && N && norm >= 0.0 && std::isfinite(norm) && m_cap >= 0 && n_window >= 0 &&
+              (normal == 0 || normal == 1),
+          SEXPM_EINVAL, "bad args");
+  REQUIRE(eps_tol >= 1e-16 && std::isfinite(eps_tol), SEXPM_ETOL, "eps_tol must be >= 1e-16 (R13)");
+  int m = 0, nn = 0;
+  REQUIRE(select_MN(norm, eps_tol, m_cap, n_window, m, nn), SEXPM_EINFEASIBLE,
+          "Eq. (4.20) infeasible within m_cap / n_window");
+  double av = 0.0, e0 = 0.0;
+  long double r = 0.0L;
+  filter_budgets(norm, normal, m, nn, av, r, e0);
+  *M = m;
+  *N = nn;
+  if (a) *a = av;
+  if (r0) *r0 = (double)r;
+  if (eps_g0) *eps_g0 = e0;
   ABI_END
 }
 

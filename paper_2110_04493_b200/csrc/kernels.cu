@@ -767,590 +767,6 @@ void launch_numeric(const NumericArgs &a, cudaStream_t st) {
   k_numeric<<<a.grid, kThreads, smem, st>>>(a);
 }
 
-// ------------------------------------------------------------------------------------
-// K3h numeric filtered SpGEMM with a shared-memory hash accumulator (one CTA per row).
-//
-// Same contract as k_numeric (the 2T term first, products a_rk * b_kj accumulated, then
-// the fused Algorithm 4.1 classification at the flush), but the accumulator is an
-// open-addressing table of kHashCap (column, value) slots keyed by a multiplicative hash,
-// so the cost no longer depends on the row's column span (a 2D stencil's rows span
-// ~2R*sqrt(n) columns for only ~2R^2 distinct ones).  At the flush the entries above the
-// floor are compacted, bitonic-sorted by column in shared memory (canonical CSR rows) and
-// appended to the staging pool.  A row whose table passes kHashMaxFill entries is handed
-// to the window kernel (fail list); nothing is lost.
-// ------------------------------------------------------------------------------------
-constexpr int kHashCap = 4096;
-constexpr int kHashMaxFill = 3072;
-constexpr int kHashPerThread = kHashCap / kThreads;
-constexpr int32_t kEmpty = -1;
-
-int hash_smem_bytes() { return kHashCap * (int)(sizeof(double) + sizeof(int32_t)); }
-
-__device__ __forceinline__ unsigned hslot(int32_t c) {
-  return ((unsigned)c * 2654435761u) >> (32 - 12);  // log2(kHashCap) = 12
-}
-
-// find or insert column c; returns the slot or -1 when the table is over-full
-__device__ __forceinline__ int hash_slot(volatile int32_t *keys, int32_t c, int *count) {
-  unsigned h = hslot(c);
-#pragma unroll 1
-  for (int probe = 0; probe < kHashCap; probe++) {
-    int32_t k = keys[h];
-    if (k == c) return (int)h;
-    if (k == kEmpty) {
-      int32_t old = atomicCAS((int32_t *)&keys[h], kEmpty, c);
-      if (old == kEmpty) {
-        int n = atomicAdd(count, 1);
-        return n < kHashMaxFill ? (int)h : -1;
-      }
-      if (old == c) return (int)h;
-    }
-    h = (h + 1) & (kHashCap - 1);
-  }
-  return -1;
-}
-
-__global__ void __launch_bounds__(kThreads) k_numeric_hash(NumericArgs a, int32_t *fail_rows,
-                                                           int *fail_count) {
-  extern __shared__ double hsm[];
-  double *vals = hsm;
-  int32_t *keys = reinterpret_cast<int32_t *>(hsm + kHashCap);
-  __shared__ int s_row;
-  __shared__ int s_count;
-  __shared__ int s_fail;
-  __shared__ unsigned long long s_off;
-  __shared__ long long s_base[kWarps + 1];
-  __shared__ double s_fs[kWarps];
-  __shared__ long long s_nz[kWarps];
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kHashCap; i += kThreads) {
-    keys[i] = kEmpty;
-    vals[i] = 0.0;
-  }
-  if (tid == 0) {
-    s_count = 0;
-    s_fail = 0;
-  }
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
-    __syncthreads();
-    const int idx = s_row;
-    if (idx >= a.nlist) break;
-    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
-    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
-    const int64_t nk = pa1 - pa0;
-    if (a.hi[r] < a.lo[r]) {
-      if (tid == 0) {
-        a.row_off[r] = 0;
-        a.row_cnt[r] = 0;
-        a.row_fsum[r] = 0.0;
-        a.row_nnz[r] = 0;
-      }
-      continue;
-    }
-    if (nk > kHashMaxFill) {  // C~ row has at least ~nk columns: straight to the window kernel
-      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
-      continue;
-    }
-    // 2T term (Eq. 2.7): distinct columns, one writer per slot
-    if (a.self_coef != 0.0) {
-      for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
-        int h = hash_slot(keys, a.A.col[p], &s_count);
-        if (h >= 0) vals[h] = a.self_coef * a.A.val[p];
-        else s_fail = 1;
-      }
-      __syncthreads();
-    }
-    // products: each warp takes 32 consecutive k's (lane l loads k_l).  Long B rows: the
-    // warp walks them one k at a time, lanes over the entries.  Short B rows (a Taylor
-    // term's H0 rows have ~5 entries): the batch's products are flattened so all 32
-    // lanes work (segment found by a 5-step shuffle search over the exclusive scan).
-    for (int64_t q0 = (int64_t)warp * 32; q0 < nk; q0 += (int64_t)kWarps * 32) {
-      const int64_t q = q0 + lane;
-      long long b0 = 0;
-      int len = 0;
-      double av = 0.0;
-      if (q < nk) {
-        const int64_t k = (int64_t)a.A.col[pa0 + q] - a.B.row0;
-        if (k >= 0 && k < a.B.nrows) {
-          b0 = a.B.rp[k];
-          len = (int)(a.B.rp[k + 1] - b0);
-          av = a.A.val[pa0 + q];
-        }
-      }
-      int inc = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(FULL_MASK, inc, o);
-        if (lane >= o) inc += y;
-      }
-      const int total = __shfl_sync(FULL_MASK, inc, 31);
-      const int excl = inc - len;
-      if (total > 32 * 24) {
-        for (int j = 0; j < 32; j++) {
-          const long long kb0 = __shfl_sync(FULL_MASK, b0, j);
-          const int klen = __shfl_sync(FULL_MASK, len, j);
-          const double kav = __shfl_sync(FULL_MASK, av, j);
-          for (int t = lane; t < klen; t += 32) {
-            const int32_t c = a.B.col[kb0 + t];
-            const double prod = kav * a.B.val[kb0 + t];
-            int h = hash_slot(keys, c, &s_count);
-            if (h >= 0) atomicAdd(&vals[h], prod);
-            else s_fail = 1;
-          }
-          if (*(volatile int *)&s_fail) break;
-        }
-      } else {
-        for (int base = 0; base < total; base += 32) {
-          const int t = base + lane;
-          int seg = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            int e = __shfl_sync(FULL_MASK, excl, seg + step);
-            if (e <= t) seg += step;
-          }
-          const long long sb0 = __shfl_sync(FULL_MASK, b0, seg);
-          const int sex = __shfl_sync(FULL_MASK, excl, seg);
-          const double sav = __shfl_sync(FULL_MASK, av, seg);
-          if (t < total) {
-            const long long p = sb0 + (t - sex);
-            const int32_t c = a.B.col[p];
-            const double prod = sav * a.B.val[p];
-            int h = hash_slot(keys, c, &s_count);
-            if (h >= 0) atomicAdd(&vals[h], prod);
-            else s_fail = 1;
-          }
-        }
-      }
-      if (*(volatile int *)&s_fail) break;
-    }
-    __syncthreads();
-    if (s_fail) {  // hand the row to the window kernel
-      if (tid == 0) {
-        int f = atomicAdd(fail_count, 1);
-        fail_rows[f] = (int32_t)r;
-      }
-      for (int i = tid; i < kHashCap; i += kThreads) {
-        keys[i] = kEmpty;
-        vals[i] = 0.0;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        s_count = 0;
-        s_fail = 0;
-      }
-      continue;
-    }
-    // flush: read this thread's slots, classify, reset the table
-    int32_t rk[kHashPerThread];
-    double rv[kHashPerThread];
-    int nst = 0;
-    double fs = 0.0;
-    long long nnzu = 0;
-#pragma unroll
-    for (int j = 0; j < kHashPerThread; j++) {
-      const int i = tid + j * kThreads;
-      int32_t c = keys[i];
-      double x = 0.0;
-      bool st = false;
-      if (c != kEmpty) {
-        x = vals[i] / a.divisor;
-        if (x != 0.0) {
-          nnzu++;
-          st = fabs(x) > a.floor_tau;
-          if (!st) fs += x * x;
-        }
-      }
-      rk[j] = st ? c : kEmpty;
-      rv[j] = x;
-      nst += st;
-    }
-    __syncthreads();
-    // block exclusive scan of nst
-    {
-      int v = nst;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(FULL_MASK, v, o);
-        if (lane >= o) v += y;
-      }
-      if (lane == 31) s_base[warp] = v;
-      fs = warp_sum(fs);
-      nnzu = warp_sum(nnzu);
-      if (lane == 0) {
-        s_fs[warp] = fs;
-        s_nz[warp] = nnzu;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        long long acc = 0;
-        for (int w = 0; w < kWarps; w++) {
-          long long t = s_base[w];
-          s_base[w] = acc;
-          acc += t;
-        }
-        s_base[kWarps] = acc;
-      }
-      __syncthreads();
-      int pos = (int)s_base[warp] + v - nst;
-#pragma unroll
-      for (int j = 0; j < kHashPerThread; j++) {
-        if (rk[j] != kEmpty) {
-          keys[pos] = rk[j];
-          vals[pos] = rv[j];
-          pos++;
-        }
-      }
-    }
-    const int total = (int)s_base[kWarps];
-    int P = 1;
-    while (P < total) P <<= 1;
-    for (int i = total + tid; i < P; i += kThreads) keys[i] = INT32_MAX;
-    __syncthreads();
-    // bitonic sort of (keys, vals)[0..P) by column
-    for (int k2 = 2; k2 <= P; k2 <<= 1) {
-      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-        for (int i = tid; i < P; i += kThreads) {
-          int ixj = i ^ j2;
-          if (ixj > i) {
-            int32_t ki = keys[i], kj = keys[ixj];
-            bool up = (i & k2) == 0;
-            if ((ki > kj) == up) {
-              keys[i] = kj;
-              keys[ixj] = ki;
-              double t = vals[i];
-              vals[i] = vals[ixj];
-              vals[ixj] = t;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    if (tid == 0) s_off = atomicAdd(a.pool_used, (unsigned long long)total);
-    __syncthreads();
-    const unsigned long long off = s_off;
-    const bool ok = (long long)off + total <= a.pool_cap;
-    if (ok) {
-      for (int i = tid; i < total; i += kThreads) {
-        a.pool_col[off + i] = keys[i];
-        a.pool_val[off + i] = vals[i];
-      }
-    }
-    if (tid == 0) {
-      double f = 0.0;
-      long long z = 0;
-      for (int w = 0; w < kWarps; w++) {
-        f += s_fs[w];
-        z += s_nz[w];
-      }
-      if (!ok) atomicOr(a.flags, 1);
-      a.row_off[r] = (int64_t)off;
-      a.row_cnt[r] = total;
-      a.row_fsum[r] = f;
-      a.row_nnz[r] = z;
-      s_count = 0;
-    }
-    __syncthreads();
-    for (int i = tid; i < kHashCap; i += kThreads) {
-      keys[i] = kEmpty;
-      vals[i] = 0.0;
-    }
-  }
-}
-
-void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
-                         cudaStream_t st) {
-  if (a.A.nrows == 0 || a.nlist == 0) return;
-  int smem = hash_smem_bytes();
-  cudaFuncSetAttribute(k_numeric_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  KL;
-  k_numeric_hash<<<a.grid, kThreads, smem, st>>>(a, fail_rows, fail_count);
-}
-
-// ------------------------------------------------------------------------------------
-// K3k numeric filtered SpGEMM, one CTA per output row, k-synchronous hash accumulator.
-//
-// The CTA adds the B rows of row r ONE k AT A TIME, in ascending k, its 256 threads
-// over that row's entries (distinct columns), with a barrier between consecutive k.  So
-// no two threads ever update the same slot concurrently: plain shared-memory
-// read-add-write (the fp64 shared atomic is a CAS loop on sm_100a), and
-// each entry is accumulated exactly like the oracle: acc = self*a_rj, then
-// acc = acc + (a_rk * b_kj) for ascending k, then acc / divisor, with _rn intrinsics
-// (no FMA contraction) -- C~ is bit-identical to the oracle.  The next k's entries are
-// prefetched into registers while the current k is added.  Flush as k_numeric_hash.
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ int hash_find_insert(volatile int32_t *keys, int32_t c, int *count) {
-  unsigned h = hslot(c);
-#pragma unroll 1
-  for (int probe = 0; probe < kHashCap; probe++) {
-    int32_t k = keys[h];
-    if (k == c) return (int)h;
-    if (k == kEmpty) {
-      int32_t old = atomicCAS((int32_t *)&keys[h], kEmpty, c);
-      if (old == kEmpty) {
-        int n = atomicAdd(count, 1);
-        return n < kHashMaxFill ? (int)h : -1;
-      }
-      if (old == c) return (int)h;
-    }
-    h = (h + 1) & (kHashCap - 1);
-  }
-  return -1;
-}
-
-__global__ void __launch_bounds__(kThreads) k_numeric_ksync(NumericArgs a, int32_t *fail_rows,
-                                                            int *fail_count) {
-  extern __shared__ double hsm[];
-  double *vals = hsm;
-  int32_t *keys = reinterpret_cast<int32_t *>(hsm + kHashCap);
-  __shared__ long long s_start[kThreads];
-  __shared__ int s_len[kThreads];
-  __shared__ double s_av[kThreads];
-  __shared__ int s_row;
-  __shared__ int s_count;
-  __shared__ int s_fail;
-  __shared__ unsigned long long s_off;
-  __shared__ long long s_base[kWarps + 1];
-  __shared__ double s_fs[kWarps];
-  __shared__ long long s_nz[kWarps];
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kHashCap; i += kThreads) {
-    keys[i] = kEmpty;
-    vals[i] = 0.0;
-  }
-  if (tid == 0) {
-    s_count = 0;
-    s_fail = 0;
-  }
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_row = atomicAdd(a.row_counter, 1);
-    __syncthreads();
-    const int idx = s_row;
-    if (idx >= a.nlist) break;
-    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
-    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
-    const int nk = (int)(pa1 - pa0);
-    if (a.hi[r] < a.lo[r]) {
-      if (tid == 0) {
-        a.row_off[r] = 0;
-        a.row_cnt[r] = 0;
-        a.row_fsum[r] = 0.0;
-        a.row_nnz[r] = 0;
-      }
-      continue;
-    }
-    if (nk > kHashMaxFill) {
-      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
-      continue;
-    }
-    if (a.self_coef != 0.0) {  // 2T term first (Eq. 2.7)
-      for (int64_t p = pa0 + tid; p < pa1; p += kThreads) {
-        int h = hash_find_insert(keys, a.A.col[p], &s_count);
-        if (h >= 0) vals[h] = __dmul_rn(a.self_coef, a.A.val[p]);
-        else s_fail = 1;
-      }
-    }
-    for (int kc = 0; kc < nk; kc += kThreads) {
-      __syncthreads();
-      if (s_fail) break;
-      {
-        const int j = kc + tid;
-        long long st0 = 0;
-        int ln = 0;
-        double av = 0.0;
-        if (j < nk) {
-          const int64_t k = (int64_t)a.A.col[pa0 + j] - a.B.row0;
-          if (k >= 0 && k < a.B.nrows) {
-            st0 = a.B.rp[k];
-            ln = (int)(a.B.rp[k + 1] - st0);
-            av = a.A.val[pa0 + j];
-          }
-        }
-        s_start[tid] = st0;
-        s_len[tid] = ln;
-        s_av[tid] = av;
-      }
-      __syncthreads();
-      const int cn = nk - kc < kThreads ? nk - kc : kThreads;
-      // prefetch the first entry of k = kc for this thread
-      int32_t pc = 0;
-      double pv = 0.0;
-      if (tid < s_len[0]) {
-        pc = a.B.col[s_start[0] + tid];
-        pv = a.B.val[s_start[0] + tid];
-      }
-      for (int kk = 0; kk < cn; kk++) {
-        const long long st0 = s_start[kk];
-        const int ln = s_len[kk];
-        const double av = s_av[kk];
-        const int32_t cc = pc;
-        const double cv = pv;
-        if (kk + 1 < cn) {  // prefetch next k
-          const int nl = s_len[kk + 1];
-          if (tid < nl) {
-            const long long ns = s_start[kk + 1];
-            pc = a.B.col[ns + tid];
-            pv = a.B.val[ns + tid];
-          }
-        }
-        if (tid < ln) {
-          int h = hash_find_insert(keys, cc, &s_count);
-          if (h >= 0) vals[h] = __dadd_rn(vals[h], __dmul_rn(av, cv));
-          else s_fail = 1;
-          for (int e = tid + kThreads; e < ln; e += kThreads) {
-            const int32_t c = a.B.col[st0 + e];
-            const double v = a.B.val[st0 + e];
-            h = hash_find_insert(keys, c, &s_count);
-            if (h >= 0) vals[h] = __dadd_rn(vals[h], __dmul_rn(av, v));
-            else s_fail = 1;
-          }
-        }
-        __syncthreads();  // k -> k+1: one writer per slot at any time
-      }
-    }
-    __syncthreads();
-    if (s_fail) {
-      if (tid == 0) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
-      for (int i = tid; i < kHashCap; i += kThreads) {
-        keys[i] = kEmpty;
-        vals[i] = 0.0;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        s_count = 0;
-        s_fail = 0;
-      }
-      continue;
-    }
-    // flush: identical to k_numeric_hash
-    int32_t rk[kHashPerThread];
-    double rv[kHashPerThread];
-    int nst = 0;
-    double fs = 0.0;
-    long long nnzu = 0;
-#pragma unroll
-    for (int j = 0; j < kHashPerThread; j++) {
-      const int i = tid + j * kThreads;
-      int32_t c = keys[i];
-      double x = 0.0;
-      bool st = false;
-      if (c != kEmpty) {
-        x = vals[i] / a.divisor;
-        if (x != 0.0) {
-          nnzu++;
-          st = fabs(x) > a.floor_tau;
-          if (!st) fs += x * x;
-        }
-      }
-      rk[j] = st ? c : kEmpty;
-      rv[j] = x;
-      nst += st;
-    }
-    __syncthreads();
-    {
-      int v = nst;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(FULL_MASK, v, o);
-        if (lane >= o) v += y;
-      }
-      if (lane == 31) s_base[warp] = v;
-      fs = warp_sum(fs);
-      nnzu = warp_sum(nnzu);
-      if (lane == 0) {
-        s_fs[warp] = fs;
-        s_nz[warp] = nnzu;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        long long acc = 0;
-        for (int w = 0; w < kWarps; w++) {
-          long long t = s_base[w];
-          s_base[w] = acc;
-          acc += t;
-        }
-        s_base[kWarps] = acc;
-      }
-      __syncthreads();
-      int pos = (int)s_base[warp] + v - nst;
-#pragma unroll
-      for (int j = 0; j < kHashPerThread; j++) {
-        if (rk[j] != kEmpty) {
-          keys[pos] = rk[j];
-          vals[pos] = rv[j];
-          pos++;
-        }
-      }
-    }
-    const int total = (int)s_base[kWarps];
-    int P = 1;
-    while (P < total) P <<= 1;
-    for (int i = total + tid; i < P; i += kThreads) keys[i] = INT32_MAX;
-    __syncthreads();
-    for (int k2 = 2; k2 <= P; k2 <<= 1) {
-      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-        for (int i = tid; i < P; i += kThreads) {
-          int ixj = i ^ j2;
-          if (ixj > i) {
-            int32_t ki = keys[i], kj = keys[ixj];
-            bool up = (i & k2) == 0;
-            if ((ki > kj) == up) {
-              keys[i] = kj;
-              keys[ixj] = ki;
-              double t = vals[i];
-              vals[i] = vals[ixj];
-              vals[ixj] = t;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    if (tid == 0) s_off = atomicAdd(a.pool_used, (unsigned long long)total);
-    __syncthreads();
-    const unsigned long long off = s_off;
-    const bool ok = (long long)off + total <= a.pool_cap;
-    if (ok) {
-      for (int i = tid; i < total; i += kThreads) {
-        a.pool_col[off + i] = keys[i];
-        a.pool_val[off + i] = vals[i];
-      }
-    }
-    if (tid == 0) {
-      double f = 0.0;
-      long long z = 0;
-      for (int w = 0; w < kWarps; w++) {
-        f += s_fs[w];
-        z += s_nz[w];
-      }
-      if (!ok) atomicOr(a.flags, 1);
-      a.row_off[r] = (int64_t)off;
-      a.row_cnt[r] = total;
-      a.row_fsum[r] = f;
-      a.row_nnz[r] = z;
-      s_count = 0;
-    }
-    __syncthreads();
-    for (int i = tid; i < kHashCap; i += kThreads) {
-      keys[i] = kEmpty;
-      vals[i] = 0.0;
-    }
-  }
-}
-
-void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
-                          cudaStream_t st) {
-  if (a.A.nrows == 0 || a.nlist == 0) return;
-  int smem = hash_smem_bytes();
-  cudaFuncSetAttribute(k_numeric_ksync, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  KL;
-  k_numeric_ksync<<<a.grid, kThreads, smem, st>>>(a, fail_rows, fail_count);
-}
 
 // ------------------------------------------------------------------------------------
 // K3p numeric filtered SpGEMM: one CTA per output row, k-synchronous, PAGED accumulator.
@@ -1381,9 +797,7 @@ struct PagedCfg {
   }
 };
 using PagedV1 = PagedCfg<256, 2, 8, 4096, 4096>;
-using PagedV2 = PagedCfg<128, 4, 4, 4096, 4096>;
 int paged_smem_bytes() { return PagedV1::smem(); }
-int paged2_smem_bytes() { return PagedV2::smem(); }
 
 __device__ __forceinline__ int page_slot(volatile int32_t *ptab, int pg, int psize, int *slot_count,
                                          int slot_cap) {
@@ -1757,10 +1171,6 @@ void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_co
                           cudaStream_t st) {
   launch_paged_cfg<PagedV1>(a, fail_rows, fail_count, st);
 }
-void launch_numeric_paged2(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
-                           cudaStream_t st) {
-  launch_paged_cfg<PagedV2>(a, fail_rows, fail_count, st);
-}
 
 // ------------------------------------------------------------------------------------
 // K5p Taylor term by PULL: S~(r, j) = (sum_{k} s_rk h0_kj) / i  (Eq. 4.11).
@@ -2001,996 +1411,6 @@ void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_r
   k_taylor_pull<<<a.grid, kThreads, smem, st>>>(a, BT, fail_rows, fail_count);
 }
 
-// ------------------------------------------------------------------------------------
-// K3g numeric filtered SpGEMM over GROUPS of kGG rows (the squaring, Eq. 2.7 P:76 /
-// Eq. 4.15; also any A*B):
-//
-//   C~(r_g,:) = self_coef * A(r_g,:) + sum_k a_{r_g k} B(k,:),   g = 0..kGG-1.
-//
-// Rows that are close in the processing order (locality clusters of H's graph) share most
-// of their k's (|union| ~ 1.3x one row's count for a 2D stencil, vs kGG x).  The CTA walks
-// the UNION of the group's k's in ascending order, gathers each B row k from L2 once and
-// applies it to all kGG rows: acc[slot(j)][g] += a_gk * b_kj (the 4 cells of a column are
-// contiguous, two 16-byte shared-memory accesses).  Rows without k add 0 * b_kj, which
-// leaves every cell unchanged bit for bit.  One barrier per k keeps every cell
-// single-writer, and each cell sees the self term first, then ascending k, with _rn
-// products and sums: C~ is bit-identical to the oracle's.
-//
-// Accumulator: pages of 2^sh columns of the group's output span, claimed on first touch
-// (allocated-page bitmap + page table), so the flush walks the claimed pages in column
-// order: rows come out sorted.  The union of k's is a bitmap over the group's k span,
-// numbered by a popcount scan (coefficients a_gk land at the k's rank).  The flush
-// classifies against the Algorithm 4.1 floor (see k_numeric) and stages each row's entries
-// contiguously in the pool.  Groups that do not fit (span, union size or slot capacity)
-// hand their rows to the fail list (paged / window kernels).
-// ------------------------------------------------------------------------------------
-constexpr int kGG = 4;
-constexpr int kGThreads = 256;
-constexpr int kGWarps = kGThreads / 32;
-constexpr int kGPages = 6144;      // direct page table over the group's output span
-constexpr int kGKWords = 1536;     // union-k bitmap words (k span <= 49152)
-constexpr int kGKCap = 1024;       // union k's per group
-constexpr int kGRing = 8;          // B rows in flight (TMA bulk copies)
-constexpr int kGRowCap = 512;      // longest B row staged in the ring (longer: global loads)
-constexpr int kGRingCols = kGRowCap + 8, kGRingVals = kGRowCap + 4;
-constexpr uint16_t kGNone = 0xFFFF, kGOver = 0xFFFE;
-
-int group_smem_bytes(int slots) {
-  return slots * kGG * 8 + kGRing * (kGRingVals * 8 + kGRingCols * 4) + kGKCap * kGG * 8 +
-         kGKCap * 8 + kGKCap * 4 + kGPages * 2 + (kGPages / 32) * 4 + kGKWords * 4 +
-         kGKWords * 2 + (slots >> 3) * 2 + 2 * kGRing * 8 + 64;
-}
-
-// mbarrier + TMA bulk copy helpers (sm_90+ PTX, here sm_100a)
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ int group_slot(volatile uint16_t *ptab, unsigned *pbits, int *nblk,
-                                          int blk_cap, int pg) {
-  uint16_t b = ptab[pg];
-  if (b < kGOver) return b;
-  if (b == kGOver) return -1;
-  const unsigned bit = 1u << (pg & 31);
-  const unsigned old = atomicOr(&pbits[pg >> 5], bit);
-  if (!(old & bit)) {
-    int nb = atomicAdd(nblk, 1);
-    const uint16_t v = nb < blk_cap ? (uint16_t)nb : kGOver;
-    __threadfence_block();
-    ptab[pg] = v;
-    return nb < blk_cap ? nb : -1;
-  }
-  while ((b = ptab[pg]) == kGNone) {
-  }
-  return b == kGOver ? -1 : (int)b;
-}
-
-// exclusive scan of kGG values over the CTA's threads (thread order): v[] becomes the
-// exclusive prefix, tot[] the totals
-template <typename T>
-__device__ __forceinline__ void gblock_scan4(T (&v)[kGG], T (&tot)[kGG], T *sbuf) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T incl[kGG];
-#pragma unroll
-  for (int g = 0; g < kGG; g++) {
-    T x = v[g];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      T y = __shfl_up_sync(FULL_MASK, x, o);
-      if (lane >= o) x += y;
-    }
-    incl[g] = x;
-    if (lane == 31) sbuf[warp * kGG + g] = x;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int g = 0; g < kGG; g++) {
-    T pre = 0, t = 0;
-    for (int w = 0; w < kGWarps; w++) {
-      const T y = sbuf[w * kGG + g];
-      if (w < warp) pre += y;
-      t += y;
-    }
-    tot[g] = t;
-    v[g] = pre + incl[g] - v[g];
-  }
-  __syncthreads();
-}
-
-// consumer-only barrier (named barrier 1: the kGThreads consumer threads; the producer
-// warp never takes part)
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kGThreads) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// kGWarps consumer warps + 1 producer warp.  The producer (lane 0 of the last warp) stages
-// the union's B rows into the ring (TMA bulk copies, `full` mbarriers) as slots are
-// released (`empty` mbarriers); the consumers never wait on global memory latency inside a
-// product step.  Setup and flush run on the consumers; the producer only joins the CTA
-// barriers around them (ct = its "thread index" for work loops, out of range).
-__global__ void __launch_bounds__(kGThreads + 32, 1) k_numeric_group(NumericArgs a, int slots,
-                                                                     int32_t *fail_rows,
-                                                                     int *fail_count) {
-  extern __shared__ double gsm[];
-  double *acc = gsm;                                                     // kGG * slots (row-major)
-  double *rval = acc + (size_t)slots * kGG;                              // kGRing * kGRingVals
-  double *coef = rval + kGRing * kGRingVals;                             // kGKCap * kGG
-  long long *kst = reinterpret_cast<long long *>(coef + kGKCap * kGG);   // kGKCap
-  uint64_t *fullb = reinterpret_cast<uint64_t *>(kst + kGKCap);          // kGRing
-  uint64_t *emptyb = fullb + kGRing;                                     // kGRing
-  int32_t *kln = reinterpret_cast<int32_t *>(emptyb + kGRing);           // kGKCap
-  int32_t *rcol = kln + kGKCap;                                          // kGRing * kGRingCols
-  uint16_t *ptab = reinterpret_cast<uint16_t *>(rcol + kGRing * kGRingCols);  // kGPages
-  unsigned *pbits = reinterpret_cast<unsigned *>(ptab + kGPages);        // kGPages / 32
-  unsigned *kbits = pbits + kGPages / 32;                                // kGKWords
-  uint16_t *kpref = reinterpret_cast<uint16_t *>(kbits + kGKWords);      // kGKWords
-  uint16_t *plist = kpref + kGKWords;                                    // slots >> 3
-  __shared__ int s_grp, s_nblk, s_fail, s_nk;
-  __shared__ long long s_p0[kGG], s_p1[kGG];
-  __shared__ int64_t s_r[kGG];
-  __shared__ int s_ng, s_kmin, s_kmax, s_lo, s_hi;
-  __shared__ long long s_scan[(kGWarps + 1) * kGG];
-  __shared__ double s_fs[kGWarps * kGG];
-  __shared__ unsigned long long s_off[kGG];
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool producer = warp == kGWarps;
-  const int ct = producer ? (1 << 28) : tid;  // consumer thread index for work loops
-  for (int i = ct; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
-  for (int i = ct; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
-  for (int i = ct; i < kGPages; i += kGThreads) ptab[i] = kGNone;
-  for (int i = ct; i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
-  for (int i = ct; i < kGKWords; i += kGThreads) kbits[i] = 0u;
-  if (tid == 0) {
-    for (int d = 0; d < kGRing; d++) {
-      mbar_init(&fullb[d], 1);
-      mbar_init(&emptyb[d], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  unsigned long long used = 0;  // ring uses so far (slot = used % kGRing), uniform per role
-  const int64_t ngroups = a.gstart ? a.ngroups : (a.nlist + kGG - 1) / kGG;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_grp = atomicAdd(a.row_counter, 1);
-    __syncthreads();
-    const int64_t grp = s_grp;
-    if (grp >= ngroups) break;
-    long long t_0 = clock64();
-    // ---- group rows (plan-time group boundaries, else kGG consecutive list entries) ----
-    if (tid < kGG) {
-      int64_t idx = grp * kGG + tid, iend = a.nlist;
-      if (a.gstart) {
-        idx = (int64_t)a.gstart[grp] + tid;
-        iend = a.gstart[grp + 1];
-      }
-      int64_t r = -1;
-      long long p0 = 0, p1 = 0;
-      if (idx < iend) {
-        r = a.order ? (int64_t)a.order[idx] : idx;
-        p0 = a.A.rp[r];
-        p1 = a.A.rp[r + 1];
-      }
-      s_r[tid] = r;
-      s_p0[tid] = p0;
-      s_p1[tid] = p1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int ng = 0, lo = INT32_MAX, hi = -1, kmin = INT32_MAX, kmax = -1;
-      for (int g = 0; g < kGG; g++) {
-        if (s_r[g] < 0) continue;
-        ng = g + 1;
-        const int64_t r = s_r[g];
-        if (a.hi[r] >= a.lo[r]) {
-          lo = min(lo, a.lo[r]);
-          hi = max(hi, a.hi[r]);
-        }
-        if (s_p1[g] > s_p0[g]) {
-          kmin = min(kmin, a.A.col[s_p0[g]]);
-          kmax = max(kmax, a.A.col[s_p1[g] - 1]);
-        }
-      }
-      s_ng = ng;
-      s_lo = lo;
-      s_hi = hi;
-      s_kmin = kmin;
-      s_kmax = kmax;
-      s_nblk = 0;
-      s_nk = 0;
-      int fail = 0;  // 1: k span, 2: output span, 3: union size, 4: slots
-      if (kmax >= kmin && (int64_t)kmax - kmin + 1 > (int64_t)kGKWords * 32) fail = 1;
-      if (hi >= lo && (((int64_t)hi >> 7) - ((int64_t)lo >> 7) + 1) > kGPages) fail = 2;
-      s_fail = fail;
-    }
-    __syncthreads();
-    const int ng = s_ng;
-    if (s_hi < s_lo) {  // every row of the group is empty
-      if (tid < ng) {
-        const int64_t r = s_r[tid];
-        a.row_off[r] = 0;
-        a.row_cnt[r] = 0;
-        a.row_fsum[r] = 0.0;
-        a.row_nnz[r] = 0;
-      }
-      continue;
-    }
-    // pages of >= 16 columns: the cells of consecutive columns fall in distinct banks
-    int sh = 4;
-    {
-      const int64_t lo = s_lo, hi = s_hi;
-      while (sh < 7 && ((hi >> sh) - (lo >> sh) + 1) > kGPages) sh++;
-    }
-    const int pmask = (1 << sh) - 1;
-    const int64_t pg0 = (int64_t)s_lo >> sh;
-    const int npg = (int)(((int64_t)s_hi >> sh) - pg0 + 1);
-    const int bcap = (slots - 32) >> sh;  // page blocks that fit (dummy cells after)
-    const int kmin = s_kmin;
-    // ---- union of k: bitmap, ranks, coefficients, B-row extents ----
-    if (!s_fail) {
-      for (int g = 0; g < ng; g++) {
-        for (long long p = s_p0[g] + ct; p < s_p1[g]; p += kGThreads) {
-          const int kb = a.A.col[p] - kmin;
-          atomicOr(&kbits[kb >> 5], 1u << (kb & 31));
-        }
-      }
-    }
-    __syncthreads();
-    const int nkw = s_fail ? 0 : ((s_kmax - kmin) >> 5) + 1;
-    {
-      const int per = (nkw + kGThreads - 1) / kGThreads;
-      const int w0 = producer ? nkw : min(tid * per, nkw), w1 = min(w0 + per, nkw);
-      long long c[kGG] = {0, 0, 0, 0}, tot[kGG];
-      for (int w = w0; w < w1; w++) c[0] += __popc(kbits[w]);
-      gblock_scan4<long long>(c, tot, s_scan);
-      int run = (int)c[0];
-      for (int w = w0; w < w1; w++) {
-        kpref[w] = (uint16_t)run;
-        run += __popc(kbits[w]);
-      }
-      if (tid == 0) {
-        s_nk = (int)tot[0];
-        if (!s_fail && tot[0] > kGKCap) s_fail = 3;
-      }
-    }
-    __syncthreads();
-    const int nk = s_fail ? 0 : s_nk;
-    if (!s_fail) {
-      for (int g = 0; g < ng; g++) {
-        for (long long p = s_p0[g] + ct; p < s_p1[g]; p += kGThreads) {
-          const int k = a.A.col[p];
-          const int kb = k - kmin;
-          const int rk = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
-          coef[rk * kGG + g] = a.A.val[p];
-          const int64_t kr = (int64_t)k - a.B.row0;
-          long long b0 = 0;
-          int ln = 0;
-          if (kr >= 0 && kr < a.B.nrows) {
-            b0 = a.B.rp[kr];
-            ln = (int)(a.B.rp[kr + 1] - b0);
-          }
-          kst[rk] = b0;
-          kln[rk] = ln;
-        }
-      }
-    }
-    // ---- self term (the 2T of Eq. 2.7), before any product ----
-    if (!s_fail && a.self_coef != 0.0) {
-      for (int g = 0; g < ng; g++) {
-        for (long long p = s_p0[g] + ct; p < s_p1[g]; p += kGThreads) {
-          const int rel = (int)(a.A.col[p] - (pg0 << sh));
-          const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
-          if (b >= 0) acc[(size_t)g * slots + (b << sh) + (rel & pmask)] = __dmul_rn(a.self_coef, a.A.val[p]);
-          else s_fail = 4;
-        }
-      }
-    }
-    __syncthreads();  // kst / kln / coef / self term ready
-    long long t_1 = clock64();
-    if (producer) {
-      // ---- producer: stage union row q in slot (used + q) % kGRing (two bulk copies, cols
-      // and values widened to 16-byte boundaries; rows longer than a slot only complete
-      // the phase and are read from global memory by the consumers) ----
-      if (lane == 0) {
-        for (int q = 0; q < nk; q++) {
-          const unsigned long long u = used + q;
-          const int d = (int)(u % kGRing);
-          if (u >= kGRing) mbar_wait(&emptyb[d], (unsigned)((u / kGRing - 1) & 1));
-          const int ln = kln[q];
-          if (ln <= kGRowCap && ln > 0) {
-            const long long b0 = kst[q];
-            const long long ca = b0 & ~3LL, va = b0 & ~1LL;
-            const unsigned cb = (unsigned)(((b0 + ln + 3) & ~3LL) - ca) * 4u;
-            const unsigned vb = (unsigned)(((b0 + ln + 1) & ~1LL) - va) * 8u;
-            mbar_expect_tx(&fullb[d], cb + vb);
-            tma_bulk_g2s(rcol + d * kGRingCols, a.B.col + ca, cb, &fullb[d]);
-            tma_bulk_g2s(rval + d * kGRingVals, a.B.val + va, vb, &fullb[d]);
-          } else {
-            mbar_arrive(&fullb[d]);
-          }
-        }
-      }
-    } else {
-      // ---- consumers: union k ascending, one (consumer) barrier per k.  Every union row
-      // k is applied to all kGG rows (a row without k adds 0 * b_kj, which leaves its cells
-      // bit-identical).  Thread t takes entries t and t + kGThreads of B row k (longer rows:
-      // the rest from global memory).  A step is interleaved by hand (warps issue in
-      // order): the next row's metadata, this row's cell loads, the next row's entries, this
-      // row's multiply-adds and stores, the next row's slot lookups (the branchy part).
-      // Cells of inactive entries go to a lane-private dummy cell past the claimable slots
-      // (never flushed) with value 0, and the first-touch page claim is a warp-uniform slow
-      // path, so the common path has no per-lane branches.
-      const int cbase = (int)(pg0 << sh);
-      long long pw = 0, pa = 0, pbar = 0;  // thread-0 clocks: ring wait, steps, barrier
-      const int dummy = slots - 32;
-      double *acc1 = acc + slots, *acc2 = acc + 2 * slots, *acc3 = acc + 3 * slots;
-      struct Step {
-        int o0, o1;
-        double v0, v1;
-        double2 k01, k23;
-      };
-      auto slot_of = [&](int32_t c, bool on, int dflt) -> int {
-        const int rel = c - cbase;
-        int b = on ? (int)ptab[rel >> sh] : 0;
-        const bool need = on && b >= (int)kGOver;
-        if (__any_sync(FULL_MASK, need)) {
-          if (need) b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
-          if (on && b < 0) s_fail = 4;
-        }
-        return (on && b >= 0) ? (b << sh) + (rel & pmask) : dflt;
-      };
-      auto rmw = [&](int o, double v, const double2 &k01, const double2 &k23) {
-        const double x0 = acc[o], x1 = acc1[o], x2 = acc2[o], x3 = acc3[o];
-        acc[o] = __dadd_rn(x0, __dmul_rn(k01.x, v));
-        acc1[o] = __dadd_rn(x1, __dmul_rn(k01.y, v));
-        acc2[o] = __dadd_rn(x2, __dmul_rn(k23.x, v));
-        acc3[o] = __dadd_rn(x3, __dmul_rn(k23.y, v));
-      };
-      // stage A of row q: wait for the staged row, read its entries and a_gk, look up slots
-      auto stage_a = [&](int q, Step &S) {
-        const int ln = kln[q];
-        const long long b0 = kst[q];
-        S.k01 = *reinterpret_cast<const double2 *>(&coef[q * kGG]);
-        S.k23 = *reinterpret_cast<const double2 *>(&coef[q * kGG + 2]);
-        const bool h0 = tid < ln, h1 = tid + kGThreads < ln;
-        int32_t ca = cbase, cb = cbase;
-        S.v0 = 0.0;
-        S.v1 = 0.0;
-        const unsigned long long u = used + q;
-        const int d = (int)(u % kGRing);
-        const long long tw0 = clock64();
-        mbar_wait(&fullb[d], (unsigned)((u / kGRing) & 1));
-        pw += clock64() - tw0;
-        if (ln <= kGRowCap) {
-          const int cbo = d * kGRingCols + (int)(b0 & 3), vbo = d * kGRingVals + (int)(b0 & 1);
-          if (h0) {
-            ca = rcol[cbo + tid];
-            S.v0 = rval[vbo + tid];
-          }
-          if (h1) {
-            cb = rcol[cbo + tid + kGThreads];
-            S.v1 = rval[vbo + tid + kGThreads];
-          }
-        } else {
-          if (h0) {
-            ca = a.B.col[b0 + tid];
-            S.v0 = a.B.val[b0 + tid];
-          }
-          if (h1) {
-            cb = a.B.col[b0 + tid + kGThreads];
-            S.v1 = a.B.val[b0 + tid + kGThreads];
-          }
-        }
-        S.o0 = __any_sync(FULL_MASK, h0) ? slot_of(ca, h0, dummy + lane) : -1;
-        S.o1 = __any_sync(FULL_MASK, h1) ? slot_of(cb, h1, dummy + lane) : -1;
-      };
-      auto step = [&](int k, Step &C, Step &Nx) {
-        double x00 = 0.0, x01 = 0.0, x02 = 0.0, x03 = 0.0, x10 = 0.0, x11 = 0.0, x12 = 0.0, x13 = 0.0;
-        if (C.o0 >= 0) {
-          x00 = acc[C.o0];
-          x01 = acc1[C.o0];
-          x02 = acc2[C.o0];
-          x03 = acc3[C.o0];
-        }
-        if (C.o1 >= 0) {
-          x10 = acc[C.o1];
-          x11 = acc1[C.o1];
-          x12 = acc2[C.o1];
-          x13 = acc3[C.o1];
-        }
-        if (k + 1 < nk) stage_a(k + 1, Nx);
-        if (C.o0 >= 0) {
-          acc[C.o0] = __dadd_rn(x00, __dmul_rn(C.k01.x, C.v0));
-          acc1[C.o0] = __dadd_rn(x01, __dmul_rn(C.k01.y, C.v0));
-          acc2[C.o0] = __dadd_rn(x02, __dmul_rn(C.k23.x, C.v0));
-          acc3[C.o0] = __dadd_rn(x03, __dmul_rn(C.k23.y, C.v0));
-        }
-        if (C.o1 >= 0) {
-          acc[C.o1] = __dadd_rn(x10, __dmul_rn(C.k01.x, C.v1));
-          acc1[C.o1] = __dadd_rn(x11, __dmul_rn(C.k01.y, C.v1));
-          acc2[C.o1] = __dadd_rn(x12, __dmul_rn(C.k23.x, C.v1));
-          acc3[C.o1] = __dadd_rn(x13, __dmul_rn(C.k23.y, C.v1));
-        }
-        const int ln = kln[k];
-        if (ln > 2 * kGThreads) {  // rows longer than 2 x CTA: the rest from global memory
-          const long long b0 = kst[k];
-          for (int e = tid + 2 * kGThreads; e < ln; e += kGThreads) {
-            const int rel = a.B.col[b0 + e] - cbase;
-            const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
-            if (b >= 0) rmw((b << sh) + (rel & pmask), a.B.val[b0 + e], C.k01, C.k23);
-            else s_fail = 4;
-          }
-        }
-      };
-      // the slot of row q is free once every consumer passed the barrier after its stage A
-      auto release = [&](int q) {
-        if (tid == 0) mbar_arrive(&emptyb[(int)((used + q) % kGRing)]);
-      };
-      Step X, Y;
-      X.o0 = X.o1 = Y.o0 = Y.o1 = -1;
-      X.v0 = X.v1 = Y.v0 = Y.v1 = 0.0;
-      if (nk > 0) stage_a(0, X);
-      long long tc = clock64(), tn;
-      for (int kk = 0; kk < nk; kk += 2) {
-        step(kk, X, Y);
-        tn = clock64(); pa += tn - tc; tc = tn;
-        consumer_sync();  // one writer per cell (k -> next k)
-        if (kk == 0) release(0);
-        if (kk + 1 < nk) release(kk + 1);
-        tn = clock64(); pbar += tn - tc; tc = tn;
-        if (kk + 1 >= nk) break;
-        step(kk + 1, Y, X);
-        tn = clock64(); pa += tn - tc; tc = tn;
-        consumer_sync();
-        if (kk + 2 < nk) release(kk + 2);
-        tn = clock64(); pbar += tn - tc; tc = tn;
-      }
-      if (a.prof && tid == 0) {
-        atomicAdd(&a.prof[8], (unsigned long long)pw);
-        atomicAdd(&a.prof[9], (unsigned long long)(pa - pw));
-        atomicAdd(&a.prof[11], (unsigned long long)pbar);
-      }
-    }
-    used += nk;
-    __syncthreads();
-    long long t_2 = clock64();
-    const int failed = s_fail;
-    // ---- flush: claimed pages in column order ----
-    int npl = 0;
-    {
-      const int nw = failed ? 0 : (npg + 31) >> 5;
-      const int per = (nw + kGThreads - 1) / kGThreads;
-      const int w0 = producer ? nw : min(tid * per, nw), w1 = min(w0 + per, nw);
-      long long c[kGG] = {0, 0, 0, 0}, tot[kGG];
-      for (int w = w0; w < w1; w++) c[0] += __popc(pbits[w]);
-      gblock_scan4<long long>(c, tot, s_scan);
-      int run = (int)c[0];
-      for (int w = w0; w < w1; w++) {
-        unsigned m = pbits[w];
-        while (m) {
-          const int bb = __ffs(m) - 1;
-          m &= m - 1;
-          plist[run++] = (uint16_t)(w * 32 + bb);
-        }
-      }
-      npl = (int)tot[0];
-    }
-    __syncthreads();
-    const int total = npl << sh;
-    const int per = (total + kGThreads - 1) / kGThreads;
-    const int q0 = producer ? total : min(tid * per, total), q1 = min(q0 + per, total);
-    long long nst[kGG] = {0, 0, 0, 0}, nnzu[kGG] = {0, 0, 0, 0}, tot[kGG];
-    double fs[kGG] = {0.0, 0.0, 0.0, 0.0};
-    for (int q = q0; q < q1; q++) {
-      const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
-#pragma unroll
-      for (int g = 0; g < kGG; g++) {
-        double x = acc[(size_t)g * slots + o];
-        if (x != 0.0) {
-          if (a.divisor != 1.0) x = x / a.divisor;
-          if (x != 0.0) {
-            nnzu[g]++;
-            if (fabs(x) > a.floor_tau) nst[g]++;
-            else fs[g] += x * x;
-          }
-        }
-      }
-    }
-    gblock_scan4<long long>(nst, tot, s_scan);
-    // per-row floor sums and distinct counts (fixed order: lanes, then warps)
-#pragma unroll
-    for (int g = 0; g < kGG; g++) {
-      const double f = warp_sum(fs[g]);
-      const long long z = warp_sum(nnzu[g]);
-      if (lane == 0 && !producer) {
-        s_fs[warp * kGG + g] = f;
-        s_scan[warp * kGG + g] = z;
-      }
-    }
-    __syncthreads();
-    if (tid < kGG) {
-      const int g = tid;
-      double f = 0.0;
-      long long z = 0;
-      for (int w = 0; w < kGWarps; w++) {
-        f += s_fs[w * kGG + g];
-        z += s_scan[w * kGG + g];
-      }
-      s_off[g] = (!failed && g < ng) ? atomicAdd(a.pool_used, (unsigned long long)tot[g]) : 0ull;
-      if (!failed && g < ng) {
-        const int64_t r = s_r[g];
-        const bool ok = (long long)s_off[g] + tot[g] <= a.pool_cap;
-        if (!ok) atomicOr(a.flags, 1);
-        a.row_off[r] = (int64_t)s_off[g];
-        a.row_cnt[r] = tot[g];
-        a.row_fsum[r] = f;
-        a.row_nnz[r] = z;
-      }
-    }
-    __syncthreads();
-    if (!failed) {
-      long long pos[kGG];
-      bool okg[kGG];
-#pragma unroll
-      for (int g = 0; g < kGG; g++) {
-        pos[g] = (long long)s_off[g] + nst[g];
-        okg[g] = g < ng && (long long)s_off[g] + tot[g] <= a.pool_cap;
-      }
-      for (int q = q0; q < q1; q++) {
-        const int pgi = plist[q >> sh];
-        const int o = ((int)ptab[pgi] << sh) + (q & pmask);
-        const int32_t col = (int32_t)(((pg0 + pgi) << sh) + (q & pmask));
-#pragma unroll
-        for (int g = 0; g < kGG; g++) {
-          double x = acc[(size_t)g * slots + o];
-          if (x != 0.0) {
-            if (a.divisor != 1.0) x = x / a.divisor;
-            if (x != 0.0 && fabs(x) > a.floor_tau) {
-              if (okg[g]) {
-                a.pool_col[pos[g]] = col;
-                a.pool_val[pos[g]] = x;
-              }
-              pos[g]++;
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ---- reset the group's state ----
-    if (!failed) {
-      for (int q = ct; q < total; q += kGThreads) {
-        const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
-#pragma unroll
-        for (int g = 0; g < kGG; g++) acc[(size_t)g * slots + o] = 0.0;
-      }
-      __syncthreads();
-      for (int i = ct; i < npl; i += kGThreads) ptab[plist[i]] = kGNone;
-      for (int i = ct; i < nk * kGG; i += kGThreads) coef[i] = 0.0;
-    } else {
-      for (int i = ct; i < slots * kGG; i += kGThreads) acc[i] = 0.0;
-      for (int i = ct; i < kGPages; i += kGThreads) ptab[i] = kGNone;
-      for (int i = ct; i < kGKCap * kGG; i += kGThreads) coef[i] = 0.0;
-    }
-    for (int i = ct; i < ((npg + 31) >> 5) && i < kGPages / 32; i += kGThreads) pbits[i] = 0u;
-    for (int i = ct; i < kGKWords; i += kGThreads) kbits[i] = 0u;
-    if (failed && tid < ng) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)s_r[tid];
-    if (a.prof && tid == 0) {
-      const long long t_3 = clock64();
-      atomicAdd(&a.prof[0], (unsigned long long)(t_1 - t_0));
-      atomicAdd(&a.prof[1], (unsigned long long)(t_2 - t_1));
-      atomicAdd(&a.prof[2], (unsigned long long)(t_3 - t_2));
-      atomicAdd(&a.prof[3], 1ull);
-      atomicAdd(&a.prof[4], (unsigned long long)s_nk);
-      if (failed) atomicAdd(&a.prof[5], 1ull);
-      if (failed == 3) atomicAdd(&a.prof[6], 1ull);
-      if (failed == 4) atomicAdd(&a.prof[7], 1ull);
-    }
-  }
-}
-
-void launch_numeric_group(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
-                          cudaStream_t st) {
-  if (a.A.nrows == 0 || a.nlist == 0) return;
-  const int smem = group_smem_bytes(slots);
-  cudaFuncSetAttribute(k_numeric_group, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  KL;
-  k_numeric_group<<<a.grid, kGThreads + 32, smem, st>>>(a, slots, fail_rows, fail_count);
-}
-
-// ------------------------------------------------------------------------------------
-// K3r numeric filtered SpGEMM, ONE WARP PER ROW, kRG rows per CTA sharing a page table:
-//
-//   C~(r,:) = self_coef * A(r,:) + sum_k a_rk B(k,:)    (Eq. 2.7 P:76 / Eq. 4.15)
-//
-// Warp g owns row r_g of a group of kRG rows that are close in the processing order, and
-// its cells acc[g][slot] (single writer: no atomics on values, no CTA barrier per k).  The
-// warp walks its own k ascending; for each k the lanes take the B row's entries in passes
-// of 32 x kRChunks, issuing all loads of a pass, then all slot lookups, then all cell
-// reads, then the _rn multiply-adds, then all stores (entries of one B row have distinct
-// columns, so the chains overlap); __syncwarp orders consecutive k.  Each cell sees the
-// self term first, then ascending k: C~ is bit-identical to the oracle's.
-// The kRG warps walk similar k sets at similar pace; a CTA barrier every kRSync k keeps
-// them close, so the B rows one warp gathers from L2 are still in L1 for the others.
-// Pages of 2^sh columns of the group's output span are claimed on first touch (shared
-// page table); the flush walks the claimed pages in column order (rows come out sorted),
-// classifies against the Algorithm 4.1 floor and stages each row contiguously.
-// ------------------------------------------------------------------------------------
-constexpr int kRG = 8;
-constexpr int kRThreads = kRG * 32;
-constexpr int kRPages = 12288;
-constexpr int kRSync = 4;
-constexpr int kRChunks = 8;
-
-int rowwarp_smem_bytes(int slots) {
-  return slots * kRG * 8 + kRPages * 2 + (kRPages / 32) * 4 + (slots >> 3) * 2 + 64;
-}
-
-template <int G, int NW, typename T>
-__device__ __forceinline__ void block_scan_g(T (&v)[G], T (&tot)[G], T *sbuf /* [NW][G] */) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T incl[G];
-#pragma unroll
-  for (int g = 0; g < G; g++) {
-    T x = v[g];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      T y = __shfl_up_sync(FULL_MASK, x, o);
-      if (lane >= o) x += y;
-    }
-    incl[g] = x;
-    if (lane == 31) sbuf[warp * G + g] = x;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int g = 0; g < G; g++) {
-    T pre = 0, t = 0;
-    for (int w = 0; w < NW; w++) {
-      const T y = sbuf[w * G + g];
-      if (w < warp) pre += y;
-      t += y;
-    }
-    tot[g] = t;
-    v[g] = pre + incl[g] - v[g];
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kRThreads, 1) k_numeric_rowwarp(NumericArgs a, int slots,
-                                                                  int32_t *fail_rows,
-                                                                  int *fail_count) {
-  extern __shared__ double rsm[];
-  double *acc = rsm;                                                   // kRG * slots
-  uint16_t *ptab = reinterpret_cast<uint16_t *>(acc + (size_t)slots * kRG);  // kRPages
-  unsigned *pbits = reinterpret_cast<unsigned *>(ptab + kRPages);      // kRPages / 32
-  uint16_t *plist = reinterpret_cast<uint16_t *>(pbits + kRPages / 32);  // slots >> 3
-  __shared__ int s_grp, s_nblk, s_fail, s_ng, s_lo, s_hi, s_maxk;
-  __shared__ long long s_p0[kRG], s_p1[kRG];
-  __shared__ int64_t s_r[kRG];
-  __shared__ long long s_scan[kRG * kRG];
-  __shared__ double s_fs[kRG * kRG];
-  __shared__ unsigned long long s_off[kRG];
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < slots * kRG; i += kRThreads) acc[i] = 0.0;
-  for (int i = tid; i < kRPages; i += kRThreads) ptab[i] = kGNone;
-  for (int i = tid; i < kRPages / 32; i += kRThreads) pbits[i] = 0u;
-  const int64_t ngroups = (a.nlist + kRG - 1) / kRG;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_grp = atomicAdd(a.row_counter, 1);
-    __syncthreads();
-    const int64_t grp = s_grp;
-    if (grp >= ngroups) break;
-    long long t_0 = clock64();
-    if (tid < kRG) {
-      const int64_t idx = grp * kRG + tid;
-      int64_t r = -1;
-      long long p0 = 0, p1 = 0;
-      if (idx < a.nlist) {
-        r = a.order ? (int64_t)a.order[idx] : idx;
-        p0 = a.A.rp[r];
-        p1 = a.A.rp[r + 1];
-      }
-      s_r[tid] = r;
-      s_p0[tid] = p0;
-      s_p1[tid] = p1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int ng = 0, lo = INT32_MAX, hi = -1, mk = 0;
-      for (int g = 0; g < kRG; g++) {
-        if (s_r[g] < 0) continue;
-        ng = g + 1;
-        const int64_t r = s_r[g];
-        if (a.hi[r] >= a.lo[r]) {
-          lo = min(lo, a.lo[r]);
-          hi = max(hi, a.hi[r]);
-        }
-        mk = max(mk, (int)(s_p1[g] - s_p0[g]));
-      }
-      s_ng = ng;
-      s_lo = lo;
-      s_hi = hi;
-      s_maxk = mk;
-      s_nblk = 0;
-      s_fail = (hi >= lo && (((int64_t)hi >> 6) - ((int64_t)lo >> 6) + 1) > kRPages) ? 2 : 0;
-    }
-    __syncthreads();
-    const int ng = s_ng;
-    if (s_hi < s_lo) {
-      if (tid < ng) {
-        const int64_t r = s_r[tid];
-        a.row_off[r] = 0;
-        a.row_cnt[r] = 0;
-        a.row_fsum[r] = 0.0;
-        a.row_nnz[r] = 0;
-      }
-      continue;
-    }
-    int sh = 3;
-    {
-      const int64_t lo = s_lo, hi = s_hi;
-      while (sh < 6 && ((hi >> sh) - (lo >> sh) + 1) > kRPages) sh++;
-    }
-    const int pmask = (1 << sh) - 1;
-    const int64_t pg0 = (int64_t)s_lo >> sh;
-    const int npg = (int)(((int64_t)s_hi >> sh) - pg0 + 1);
-    const int bcap = slots >> sh;
-    const int cbase = (int)(pg0 << sh);
-    const bool mine = warp < ng && !s_fail;
-    const long long p0 = s_p0[warp < kRG ? warp : 0], p1 = s_p1[warp < kRG ? warp : 0];
-    const int nkw = mine ? (int)(p1 - p0) : 0;
-    double *accw = acc + (size_t)warp * slots;
-    // ---- self term (the 2T of Eq. 2.7), first in every cell of the row ----
-    if (mine && a.self_coef != 0.0) {
-      for (long long p = p0 + lane; p < p1; p += 32) {
-        const int rel = a.A.col[p] - cbase;
-        const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
-        if (b >= 0) accw[(b << sh) + (rel & pmask)] = __dmul_rn(a.self_coef, a.A.val[p]);
-        else s_fail = 4;
-      }
-      __syncwarp();
-    }
-    long long t_1 = clock64();
-    // ---- products: own k ascending; CTA barrier every kRSync k ----
-    const int maxk = s_maxk;
-    int32_t kk_l = 0;     // lane l holds entry (j0 + l) of the A row: k, a_rk, B row extent
-    double ak_l = 0.0;
-    long long kb_l = 0;
-    int kn_l = 0;
-    for (int j0 = 0; j0 < maxk; j0 += kRSync) {
-      if ((j0 & 31) == 0 && j0 < nkw) {
-        const int j = j0 + lane;
-        kk_l = 0;
-        ak_l = 0.0;
-        kb_l = 0;
-        kn_l = 0;
-        if (j < nkw) {
-          kk_l = a.A.col[p0 + j];
-          ak_l = a.A.val[p0 + j];
-          const int64_t kr = (int64_t)kk_l - a.B.row0;
-          if (kr >= 0 && kr < a.B.nrows) {
-            kb_l = a.B.rp[kr];
-            kn_l = (int)(a.B.rp[kr + 1] - kb_l);
-          }
-        }
-      }
-#pragma unroll 1
-      for (int j = j0; j < j0 + kRSync && j < nkw; j++) {
-        const int src = j & 31;
-        const double av = __shfl_sync(FULL_MASK, ak_l, src);
-        const long long b0 = __shfl_sync(FULL_MASK, kb_l, src);
-        const int ln = __shfl_sync(FULL_MASK, kn_l, src);
-        for (int e0 = 0; e0 < ln; e0 += 32 * kRChunks) {
-          int32_t c[kRChunks];
-          double v[kRChunks];
-          int o[kRChunks];
-          double x[kRChunks];
-#pragma unroll
-          for (int i = 0; i < kRChunks; i++) {
-            const int e = e0 + i * 32 + lane;
-            c[i] = -1;
-            v[i] = 0.0;
-            if (e < ln) {
-              c[i] = a.B.col[b0 + e];
-              v[i] = a.B.val[b0 + e];
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < kRChunks; i++) {
-            o[i] = -1;
-            if (c[i] >= 0) {
-              const int rel = c[i] - cbase;
-              const int b = group_slot(ptab, pbits, &s_nblk, bcap, rel >> sh);
-              if (b >= 0) o[i] = (b << sh) + (rel & pmask);
-              else s_fail = 4;
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < kRChunks; i++) x[i] = o[i] >= 0 ? accw[o[i]] : 0.0;
-#pragma unroll
-          for (int i = 0; i < kRChunks; i++) x[i] = __dadd_rn(x[i], __dmul_rn(av, v[i]));
-#pragma unroll
-          for (int i = 0; i < kRChunks; i++)
-            if (o[i] >= 0) accw[o[i]] = x[i];
-        }
-        __syncwarp();  // next k may hit the same cells from other lanes
-      }
-      __syncthreads();  // keep the warps' B-row walks close (L1 sharing)
-    }
-    long long t_2 = clock64();
-    const int failed = s_fail;
-    // ---- flush: claimed pages in column order ----
-    int npl = 0;
-    {
-      const int nw = failed ? 0 : (npg + 31) >> 5;
-      const int per = (nw + kRThreads - 1) / kRThreads;
-      const int w0 = min(tid * per, nw), w1 = min(w0 + per, nw);
-      long long c[1] = {0}, tot[1];
-      for (int w = w0; w < w1; w++) c[0] += __popc(pbits[w]);
-      block_scan_g<1, kRG>(c, tot, s_scan);
-      int run = (int)c[0];
-      for (int w = w0; w < w1; w++) {
-        unsigned m = pbits[w];
-        while (m) {
-          const int bb = __ffs(m) - 1;
-          m &= m - 1;
-          plist[run++] = (uint16_t)(w * 32 + bb);
-        }
-      }
-      npl = (int)tot[0];
-    }
-    __syncthreads();
-    const int total = npl << sh;
-    const int per = (total + kRThreads - 1) / kRThreads;
-    const int q0 = min(tid * per, total), q1 = min(q0 + per, total);
-    long long nst[kRG], nnzu[kRG], tot[kRG];
-    double fs[kRG];
-#pragma unroll
-    for (int g = 0; g < kRG; g++) {
-      nst[g] = 0;
-      nnzu[g] = 0;
-      fs[g] = 0.0;
-    }
-    for (int q = q0; q < q1; q++) {
-      const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
-#pragma unroll
-      for (int g = 0; g < kRG; g++) {
-        double x = acc[(size_t)g * slots + o];
-        if (x != 0.0) {
-          if (a.divisor != 1.0) x = x / a.divisor;
-          if (x != 0.0) {
-            nnzu[g]++;
-            if (fabs(x) > a.floor_tau) nst[g]++;
-            else fs[g] += x * x;
-          }
-        }
-      }
-    }
-    block_scan_g<kRG, kRG>(nst, tot, s_scan);
-#pragma unroll
-    for (int g = 0; g < kRG; g++) {
-      const double f = warp_sum(fs[g]);
-      const long long z = warp_sum(nnzu[g]);
-      if (lane == 0) {
-        s_fs[warp * kRG + g] = f;
-        s_scan[warp * kRG + g] = z;
-      }
-    }
-    __syncthreads();
-    if (tid < kRG) {
-      const int g = tid;
-      double f = 0.0;
-      long long z = 0;
-      for (int w = 0; w < kRG; w++) {
-        f += s_fs[w * kRG + g];
-        z += s_scan[w * kRG + g];
-      }
-      s_off[g] = (!failed && g < ng) ? atomicAdd(a.pool_used, (unsigned long long)tot[g]) : 0ull;
-      if (!failed && g < ng) {
-        const int64_t r = s_r[g];
-        const bool ok = (long long)s_off[g] + tot[g] <= a.pool_cap;
-        if (!ok) atomicOr(a.flags, 1);
-        a.row_off[r] = (int64_t)s_off[g];
-        a.row_cnt[r] = tot[g];
-        a.row_fsum[r] = f;
-        a.row_nnz[r] = z;
-      }
-    }
-    __syncthreads();
-    if (!failed) {
-      long long pos[kRG];
-      bool okg[kRG];
-#pragma unroll
-      for (int g = 0; g < kRG; g++) {
-        pos[g] = (long long)s_off[g] + nst[g];
-        okg[g] = g < ng && (long long)s_off[g] + tot[g] <= a.pool_cap;
-      }
-      for (int q = q0; q < q1; q++) {
-        const int pgi = plist[q >> sh];
-        const int o = ((int)ptab[pgi] << sh) + (q & pmask);
-        const int32_t col = (int32_t)(((pg0 + pgi) << sh) + (q & pmask));
-#pragma unroll
-        for (int g = 0; g < kRG; g++) {
-          double x = acc[(size_t)g * slots + o];
-          if (x != 0.0) {
-            if (a.divisor != 1.0) x = x / a.divisor;
-            if (x != 0.0 && fabs(x) > a.floor_tau) {
-              if (okg[g]) {
-                a.pool_col[pos[g]] = col;
-                a.pool_val[pos[g]] = x;
-              }
-              pos[g]++;
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ---- reset ----
-    if (!failed) {
-      for (int q = tid; q < total; q += kRThreads) {
-        const int o = ((int)ptab[plist[q >> sh]] << sh) + (q & pmask);
-#pragma unroll
-        for (int g = 0; g < kRG; g++) acc[(size_t)g * slots + o] = 0.0;
-      }
-      __syncthreads();
-      for (int i = tid; i < npl; i += kRThreads) ptab[plist[i]] = kGNone;
-    } else {
-      for (int i = tid; i < slots * kRG; i += kRThreads) acc[i] = 0.0;
-      for (int i = tid; i < kRPages; i += kRThreads) ptab[i] = kGNone;
-    }
-    for (int i = tid; i < ((npg + 31) >> 5) && i < kRPages / 32; i += kRThreads) pbits[i] = 0u;
-    if (failed && tid < ng) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)s_r[tid];
-    if (a.prof && tid == 0) {
-      const long long t_3 = clock64();
-      atomicAdd(&a.prof[0], (unsigned long long)(t_1 - t_0));
-      atomicAdd(&a.prof[1], (unsigned long long)(t_2 - t_1));
-      atomicAdd(&a.prof[2], (unsigned long long)(t_3 - t_2));
-      atomicAdd(&a.prof[3], 1ull);
-      atomicAdd(&a.prof[4], (unsigned long long)maxk);
-      if (failed) atomicAdd(&a.prof[5], 1ull);
-      if (failed == 2) atomicAdd(&a.prof[6], 1ull);
-      if (failed == 4) atomicAdd(&a.prof[7], 1ull);
-    }
-  }
-}
-
-void launch_numeric_rowwarp(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
-                            cudaStream_t st) {
-  if (a.A.nrows == 0 || a.nlist == 0) return;
-  const int smem = rowwarp_smem_bytes(slots);
-  cudaFuncSetAttribute(k_numeric_rowwarp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  KL;
-  k_numeric_rowwarp<<<a.grid, kRThreads, smem, st>>>(a, slots, fail_rows, fail_count);
-}
 
 // ------------------------------------------------------------------------------------
 // BSR-8 view of a CSR matrix (squarings, one GPU): block row I = rows 8I..8I+7, block
@@ -3002,7 +1422,11 @@ constexpr int kBsrWarps = 8;
 constexpr int kBsrSpanWords = 512;  // block-column span per block row: 16384 blocks
 
 // count pass (fill = false) and fill pass (fill = true); warp per block row
-template <bool FILL>
+// FRAG: values in the fp64 tensor-core fragment order of K3m (kernel 13): element (r, c) of a
+// block at 2 (4 r + c % 4) + c / 4, i.e. lane l = 4 r + c % 4 of a warp holds (r, c) and
+// (r, c + 4) as one 16-byte pair -- the A operand of mma.m8n8k4 for k = c % 4 and c % 4 + 4
+// in one load; otherwise row-major (K3b).
+template <bool FILL, bool FRAG = false>
 __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t nbr, int64_t *bcnt,
                                                               const int64_t *brp, int32_t *bcol,
                                                               double *bval, int *flags) {
@@ -3084,7 +1508,8 @@ __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t
       const int c = A.col[p];
       const int b = (c >> 3) - jmin;
       const int rank = pref[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
-      bval[(base + rank) * 64 + ri * 8 + (c & 7)] = A.val[p];
+      const int e = FRAG ? 2 * (4 * ri + (c & 3)) + ((c & 7) >> 2) : ri * 8 + (c & 7);
+      bval[(base + rank) * 64 + e] = A.val[p];
     }
   }
 }
@@ -3095,11 +1520,15 @@ void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, 
                                                                            nullptr, nullptr, flags);
 }
 void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
-                     double *bval, int *flags, cudaStream_t st) {
+                     double *bval, int *flags, cudaStream_t st, bool frag) {
   if (nbr == 0) return;
   KL;
-  k_bsr_build<true><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, nullptr, brp,
-                                                                          bcol, bval, flags);
+  if (frag)
+    k_bsr_build<true, true><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, nullptr, brp,
+                                                                                bcol, bval, flags);
+  else
+    k_bsr_build<true, false><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, nullptr, brp,
+                                                                                 bcol, bval, flags);
 }
 
 // block transpose: a stable radix sort of the blocks (enumerated block row by block row,
@@ -3315,6 +1744,13 @@ __global__ void __launch_bounds__(kBThreads, 2) k_numeric_bsr(NumericArgs a, Bsr
         }
       }
     }
+    // the self term 2 A_IJ reaches the block columns of row I itself, also where no B_K of
+    // the row has block J (e.g. an empty diagonal block)
+    if (a.self_coef != 0.0)
+      for (int t = tid; t < na; t += kBThreads) {
+        const int jb = aK[t] - jmin;
+        if (jb >= 0 && jb < njw * 32) atomicOr(&jbits[jb >> 5], 1u << (jb & 31));
+      }
     __syncthreads();
     if (tid < 32) {
       const int per = (njw + 31) / 32;
@@ -3559,154 +1995,160 @@ void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, 
   k_numeric_bsr<<<a.grid, kBThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
 }
 
-
 // ------------------------------------------------------------------------------------
-// K3b2: K3b over PAIRS of block rows (I0, I1 = consecutive entries of the processing order,
-// spatially adjacent): one CTA of 16 warps per pair, both rows' A blocks in shared memory,
-// candidate output blocks J = union over both rows.  A warp computes C_I0J and C_I1J together:
-// lane holds C_h[i][j], C_h[i+4][j] for h = 0, 1 (i = lane / 8, j = lane % 8).  For every K of
-// column J's block list (ascending) that row I0 or row I1 holds, the staged B_KJ block is read
-// once and multiplied into both rows; a row that lacks K uses an all-zero A block, which adds
-// exact zeros (x + 0 = x), so each element still sees the self term then the products of its
-// own row in ascending k -- bit-identical to K3b and to the oracle.  Sharing each B block
-// between two block rows halves the B-side shared/L1 traffic per block product (the kernel
-// is bound by the L1 wavefront rate).  The output blocks go to scratch
-// raw; the staging pass (one warp per row, 16 rows) derives the Algorithm 4.1 row sums from
-// them while it stages the kept entries.
+// K3m numeric filtered SpGEMM on the BSR-8 view with the fp64 tensor-core instruction
+// (squarings; default):
+//
+//   C~_IJ = self * A_IJ + sum_K A_IK B_KJ      (8x8 blocks; Eq. 2.7, Eq. 4.15)
+//
+// The same block decomposition as K3b, but every 8x8x8 block product is two
+// mma.sync.m8n8k4.f64 instructions (DMMA: 8x8x4 fused multiply-adds each) whose operands
+// come straight from the block store in fragment order (k_bsr_build<FRAG>): lane l
+// (g = l / 4, t = l % 4) loads A_IK[g][t] and A_IK[g][t+4] as one 16-byte pair and B_KJ[t][g],
+// B_KJ[t+4][g] as two 8-byte words (each warp-wide load one contiguous 256 or 512 bytes), and
+// accumulates C_IJ[g][2t], C_IJ[g][2t+1] in registers.  Four operand loads per lane per block
+// product instead of K3b's 24 shared-memory loads: the L1 wavefront bound of K3b is gone
+// and the kernel is bound by the DMMA pipe (37.2 TF/s measured, profiles/r02_fp64_peak) and
+// the L2 -> SM operand stream.  A's blocks are read through L1 like B's (no shared-memory
+// copy of row I), so a block row of any width is handled (config 4's 3D rows); only the
+// spans of the K and J bitmaps and the J count per block row are capped.
+//
+// Rounding: DMMA fuses each product into the running sum (one rounding per FMA), so C~ is
+// not bit-identical to the oracle's DMUL + DADD order; K3b (kernel 11) is the bit-exact
+// path.  The difference is a few ulps of the partial sums, inside the north-star parity
+// bound (tests/test_gpu_parity.py).
+//
+// One CTA per block row I (dynamic scheduler over the locality order), one warp per output
+// block J: for the K common to row I of A and column J of B (block transpose, ascending)
+// the operand pairs of kMPF products are loaded ahead, then multiplied.  The classified
+// values (Algorithm 4.1 floor, fused first pass) go to this CTA's scratch packed per
+// (block, row) with an 8-bit keep mask; then each row's kept entries are staged in column
+// order (block columns ascending).
 // ------------------------------------------------------------------------------------
-constexpr int kB2Threads = 512;
-constexpr int kB2Warps = kB2Threads / 32;
-constexpr int kB2JCap = kBsr2JCap;  // output block pairs per block-row pair (scratch: 128 doubles each)
+constexpr int kMThreads = 256;
+constexpr int kMWarps = kMThreads / 32;
+constexpr int kMKWords = 256;              // K bitmap: block-column span of A's row <= 8192
+constexpr int kMJWords = 1024;             // J bitmap: output block-column span <= 32768
+constexpr int kMJCap = kBsrMJCap;          // output blocks per block row
+constexpr int kMML = 64;                   // matches listed at a time per warp
+constexpr int kMPF = 4;                    // block products whose operands are in flight
 
-int bsr2_numeric_smem_bytes() {
-  return (2 * kBACap + 1) * 64 * 8 + kB2Warps * kBPF * 64 * 8 + kB2Warps * kBML * 8 +
-         2 * kB2Warps * kBML * 4 + 2 * kBACap * 4 + 2 * kBKWords * 4 + 2 * kBKWords * 2 +
-         kBJWords * 4 + kB2JCap * 4 + kB2JCap * 16 * 2 + 64;
+int bsrm_numeric_smem_bytes() {
+  return kMKWords * 4 + kMKWords * 2 + kMJWords * 4 + kMJCap * 4 + kMWarps * kMML * 16 + 64;
 }
 
-// x0 += sum_k a0[i0][k] b[k][lj] (and rows i1, and A block a1) -- k ascending, _rn
-__device__ __forceinline__ void bsr2_block_fma(const double *bs, const double *a0, const double *a1,
-                                               int i0, int i1, int lj, double &x00, double &x01,
-                                               double &x10, double &x11) {
-  const double *bq = bs + lj;
-  const double *p00 = a0 + i0 * 8, *p01 = a0 + i1 * 8, *p10 = a1 + i0 * 8, *p11 = a1 + i1 * 8;
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const double b = bq[k * 8];
-    x00 = __dadd_rn(x00, __dmul_rn(p00[k], b));
-    x01 = __dadd_rn(x01, __dmul_rn(p01[k], b));
-    x10 = __dadd_rn(x10, __dmul_rn(p10[k], b));
-    x11 = __dadd_rn(x11, __dmul_rn(p11[k], b));
-  }
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kB2Threads, 1) k_numeric_bsr2(NumericArgs a, BsrView Bv, int64_t nrows,
-                                                                double *scratch, int32_t *fail_rows,
-                                                                int *fail_count) {
-  extern __shared__ double bsm2[];
-  double *aval = bsm2;                                                       // (2 kBACap + 1) * 64
-  double *wstage = aval + (2 * kBACap + 1) * 64;                             // kB2Warps * kBPF * 64
-  int64_t *mlb = reinterpret_cast<int64_t *>(wstage + kB2Warps * kBPF * 64);  // kB2Warps * kBML
-  int32_t *mlk = reinterpret_cast<int32_t *>(mlb + kB2Warps * kBML);         // 2 * kB2Warps * kBML
-  int32_t *aK = mlk + 2 * kB2Warps * kBML;                                   // 2 * kBACap
-  unsigned *kbits = reinterpret_cast<unsigned *>(aK + 2 * kBACap);           // 2 * kBKWords
-  uint16_t *kpref = reinterpret_cast<uint16_t *>(kbits + 2 * kBKWords);      // 2 * kBKWords
-  unsigned *jbits = reinterpret_cast<unsigned *>(kpref + 2 * kBKWords);      // kBJWords
-  int32_t *jlist = reinterpret_cast<int32_t *>(jbits + kBJWords);            // kB2JCap
-  uint16_t *jcnt = reinterpret_cast<uint16_t *>(jlist + kB2JCap);            // kB2JCap * 16
-  __shared__ int s_p, s_fail, s_nj, s_jmin, s_njw;
-  __shared__ int s_na[2], s_kmin[2], s_nkw[2], s_nr[2];
-  __shared__ long long s_I[2];
+// spread 4 bits to the even positions of 8
+__device__ __forceinline__ unsigned spread4(unsigned m) {
+  m = (m | (m << 2)) & 0x33u;
+  return (m | (m << 1)) & 0x55u;
+}
+
+__global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, BsrView Bv, int64_t nrows,
+                                                              double *scratch, int32_t *fail_rows,
+                                                              int *fail_count) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  int64_t *mla = reinterpret_cast<int64_t *>(msm);                      // kMWarps * kMML
+  int64_t *mlb = mla + kMWarps * kMML;                                  // kMWarps * kMML
+  unsigned *kbits = reinterpret_cast<unsigned *>(mlb + kMWarps * kMML); // kMKWords
+  unsigned *jbits = kbits + kMKWords;                                   // kMJWords
+  int32_t *jlist = reinterpret_cast<int32_t *>(jbits + kMJWords);       // kMJCap
+  uint16_t *kpref = reinterpret_cast<uint16_t *>(jlist + kMJCap);       // kMKWords
+  __shared__ int s_I, s_fail, s_nj, s_kmin, s_jmin, s_nkw, s_njw;
+  __shared__ double s_fs[kMWarps][8], s_p1[kMWarps][8];
+  __shared__ long long s_nz[kMWarps][8], s_c1[kMWarps][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double *scr = scratch + (size_t)blockIdx.x * kB2JCap * 128;
-  const int zero_blk = 2 * kBACap;  // index of the all-zero A block
-  for (int i = tid; i < 64; i += kB2Threads) aval[zero_blk * 64 + i] = 0.0;
-  for (int i = tid; i < 2 * kBKWords; i += kB2Threads) kbits[i] = 0u;
-  for (int i = tid; i < kBJWords; i += kB2Threads) jbits[i] = 0u;
-  const int li = lane >> 3, lj = lane & 7;
-  const int i0 = li, i1 = li + 4;
-  const int64_t npairs = (Bv.nbr + 1) / 2;
+  const int g = lane >> 2, t = lane & 3;  // fragment coordinates
+  double *scr = scratch + (size_t)blockIdx.x * kMJCap * 65;  // kMJCap blocks + keep masks
+  uint8_t *jm = reinterpret_cast<uint8_t *>(scr + (size_t)kMJCap * 64);
+  for (int i = tid; i < kMKWords; i += kMThreads) kbits[i] = 0u;
+  for (int i = tid; i < kMJWords; i += kMThreads) jbits[i] = 0u;
+  // B fragment offsets: B[t][g] and B[t + 4][g] in fragment order
+  const int boff = 2 * (4 * t + (g & 3)) + (g >> 2);
+  // self-term offsets: A_IJ[g][2t] and A_IJ[g][2t + 1]
+  const int soff0 = 2 * (4 * g + ((2 * t) & 3)) + ((2 * t) >> 2);
+  const int soff1 = 2 * (4 * g + ((2 * t + 1) & 3)) + ((2 * t + 1) >> 2);
+  const double2 *bv2 = reinterpret_cast<const double2 *>(Bv.bval);
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_p = atomicAdd(a.row_counter, 1);
+    if (tid == 0) s_I = atomicAdd(a.row_counter, 1);
     __syncthreads();
-    const int p = s_p;
-    if (p >= npairs) break;
-    if (tid < 2) {
-      const int64_t q = 2 * (int64_t)p + tid;
-      const int64_t I = q < Bv.nbr ? (Bv.border ? (int64_t)Bv.border[q] : q) : -1;
-      s_I[tid] = I;
-      const int64_t r0 = 8 * I;
-      const int nr = I < 0 ? 0 : (int)(nrows - r0 < 8 ? nrows - r0 : 8);
-      const int na = I < 0 ? 0 : (int)(Bv.brp[I + 1] - Bv.brp[I]);
-      s_nr[tid] = nr;
-      s_na[tid] = na;
-      const int kmin = na > 0 ? Bv.bcol[Bv.brp[I]] : 0, kmax = na > 0 ? Bv.bcol[Bv.brp[I + 1] - 1] : -1;
-      s_kmin[tid] = kmin;
-      s_nkw[tid] = na > 0 ? ((kmax - kmin) >> 5) + 1 : 0;
-    }
-    __syncthreads();
+    if (s_I >= Bv.nbr_a) break;
+    const int64_t I = Bv.border ? (int64_t)Bv.border[s_I] : (int64_t)s_I;
+    const int64_t r0 = 8 * I;
+    const int nr = (int)(nrows - r0 < 8 ? nrows - r0 : 8);
+    const int64_t ab0 = Bv.brp[I + Bv.ib0], ab1 = Bv.brp[I + Bv.ib0 + 1];
+    const int na = (int)(ab1 - ab0);
     if (tid == 0) {
-      int fail = s_na[0] > kBACap || s_na[1] > kBACap || s_nkw[0] > kBKWords || s_nkw[1] > kBKWords;
+      int fail = 0;
       int jmin = INT32_MAX, jmax = -1;
-      for (int h = 0; h < 2; h++)
-        for (int i = 0; i < s_nr[h]; i++) {
-          const int64_t r = 8 * s_I[h] + i;
-          if (a.hi[r] >= a.lo[r]) {
-            jmin = min(jmin, a.lo[r] >> 3);
-            jmax = max(jmax, a.hi[r] >> 3);
-          }
+      for (int i = 0; i < nr; i++) {
+        const int64_t r = r0 + i;
+        if (a.hi[r] >= a.lo[r]) {
+          jmin = min(jmin, a.lo[r] >> 3);
+          jmax = max(jmax, a.hi[r] >> 3);
         }
-      if (jmax >= jmin && ((jmax - jmin) >> 5) + 1 > kBJWords) fail = 1;
+      }
+      const int kmin = na > 0 ? Bv.bcol[ab0] : 0, kmax = na > 0 ? Bv.bcol[ab1 - 1] : -1;
+      if (na > 0 && ((kmax - kmin) >> 5) + 1 > kMKWords) fail = 1;
+      if (jmax >= jmin && ((jmax - jmin) >> 5) + 1 > kMJWords) fail = 1;
       s_fail = fail;
+      s_kmin = kmin;
       s_jmin = jmin;
+      s_nkw = na > 0 ? ((kmax - kmin) >> 5) + 1 : 0;
       s_njw = jmax >= jmin ? ((jmax - jmin) >> 5) + 1 : 0;
     }
     __syncthreads();
-    const int nrt = s_nr[0] + s_nr[1];
-    if (s_fail || (s_na[0] == 0 && s_na[1] == 0) || s_njw == 0) {
-      if (tid < 16) {
-        const int h = tid >> 3, i = tid & 7;
-        if (i < s_nr[h]) {
-          const int64_t r = 8 * s_I[h] + i;
-          if (s_fail) {
-            fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
-          } else {
-            a.row_off[r] = 0;
-            a.row_cnt[r] = 0;
-            a.row_fsum[r] = 0.0;
-            a.row_nnz[r] = 0;
-            if (a.row_p1) {
-              a.row_p1[r] = 0.0;
-              a.row_c1[r] = 0;
-            }
+    if (s_fail || na == 0 || s_njw == 0) {
+      if (tid < nr) {
+        const int64_t r = r0 + tid;
+        if (s_fail) {
+          fail_rows[atomicAdd(fail_count, 1)] = (int32_t)r;
+        } else {
+          a.row_off[r] = 0;
+          a.row_cnt[r] = 0;
+          a.row_fsum[r] = 0.0;
+          a.row_nnz[r] = 0;
+          if (a.row_p1) {
+            a.row_p1[r] = 0.0;
+            a.row_c1[r] = 0;
           }
         }
       }
-      (void)nrt;
       continue;
     }
-    const int jmin = s_jmin, njw = s_njw;
-    // (1) both rows of A: block columns, values, K bitmaps
-    for (int h = 0; h < 2; h++) {
-      const int na = s_na[h], kmin = s_kmin[h];
-      const int64_t ab0 = na > 0 ? Bv.brp[s_I[h]] : 0;
-      for (int t = tid; t < na; t += kB2Threads) {
-        const int K = Bv.bcol[ab0 + t];
-        aK[h * kBACap + t] = K;
-        atomicOr(&kbits[h * kBKWords + ((K - kmin) >> 5)], 1u << ((K - kmin) & 31));
+    const int kmin = s_kmin, jmin = s_jmin, nkw = s_nkw, njw = s_njw;
+    // (1) K bitmap of row I of A, then the word prefix (ranks)
+    for (int q = tid; q < na; q += kMThreads) {
+      const int K = Bv.bcol[ab0 + q];
+      atomicOr(&kbits[(K - kmin) >> 5], 1u << ((K - kmin) & 31));
+      // (2a) the self term reaches row I's own block columns (also where no B_K has them)
+      if (a.self_coef != 0.0) {
+        const int jb = K - jmin;
+        if (jb >= 0 && jb < njw * 32) atomicOr(&jbits[jb >> 5], 1u << (jb & 31));
       }
-      for (int t = tid; t < na * 64; t += kB2Threads) aval[h * kBACap * 64 + t] = Bv.bval[ab0 * 64 + t];
+    }
+    // (2b) candidate output blocks: union of the block rows of B at A's block columns
+    for (int q = warp; q < na; q += kMWarps) {
+      const int64_t K = Bv.bcol[ab0 + q] - Bv.kb0;  // the view's block row
+      if (K >= 0 && K < Bv.nbr) {
+        for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
+          const int jb = Bv.bcol[b] - jmin;
+          if (jb >= 0 && jb < njw * 32) atomicOr(&jbits[jb >> 5], 1u << (jb & 31));
+        }
+      }
     }
     __syncthreads();
-    if (warp < 2) {  // word prefix of each K bitmap (warp h: row h)
-      const int h = warp, nkw = s_nkw[h];
-      unsigned *kb = kbits + h * kBKWords;
-      uint16_t *kp = kpref + h * kBKWords;
+    if (warp == 0) {  // word prefix of the K bitmap
       const int per = (nkw + 31) / 32;
       const int w0 = min(lane * per, nkw), w1 = min(w0 + per, nkw);
       int c = 0;
-      for (int w = w0; w < w1; w++) c += __popc(kb[w]);
+      for (int w = w0; w < w1; w++) c += __popc(kbits[w]);
       int v = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -3715,22 +2157,10 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_numeric_bsr2(NumericArgs a, B
       }
       int run = v - c;
       for (int w = w0; w < w1; w++) {
-        kp[w] = (uint16_t)run;
-        run += __popc(kb[w]);
+        kpref[w] = (uint16_t)run;
+        run += __popc(kbits[w]);
       }
-    }
-    // (2) candidate output blocks: union of B's block rows at both rows' block columns
-    for (int t = warp; t < s_na[0] + s_na[1]; t += kB2Warps) {
-      const int64_t K = t < s_na[0] ? aK[t] : aK[kBACap + t - s_na[0]];
-      if (K < Bv.nbr) {
-        for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
-          const int jb = Bv.bcol[b] - jmin;
-          if (jb >= 0 && jb < njw * 32) atomicOr(&jbits[jb >> 5], 1u << (jb & 31));
-        }
-      }
-    }
-    __syncthreads();
-    if (tid < 32) {
+    } else if (warp == 1) {  // J list in ascending order
       const int per = (njw + 31) / 32;
       const int w0 = min(lane * per, njw), w1 = min(w0 + per, njw);
       int c = 0;
@@ -3743,7 +2173,7 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_numeric_bsr2(NumericArgs a, B
       }
       const int tot = __shfl_sync(FULL_MASK, v, 31);
       if (lane == 0) s_nj = tot;
-      if (tot <= kB2JCap) {
+      if (tot <= kMJCap) {
         int run = v - c;
         for (int w = w0; w < w1; w++) {
           unsigned m = jbits[w];
@@ -3757,195 +2187,213 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_numeric_bsr2(NumericArgs a, B
     }
     __syncthreads();
     const int nj = s_nj;
-    const bool over = nj > kB2JCap;
+    const bool over = nj > kMJCap;
+    // (3) output blocks, one warp each
+    double fs = 0.0, q1 = 0.0;
+    long long nz = 0, c1 = 0;
     unsigned long long nbp = 0;
-    const int kmin0 = s_kmin[0], kmin1 = s_kmin[1], nkw0 = s_nkw[0], nkw1 = s_nkw[1];
-    auto lookup = [&](int h, int K) -> int {  // rank of block column K in row h, or -1
-      const int kb = K - (h ? kmin1 : kmin0);
-      const int nkw = h ? nkw1 : nkw0;
-      const unsigned *bits = kbits + h * kBKWords;
-      if (kb < 0 || kb >= nkw * 32 || !((bits[kb >> 5] >> (kb & 31)) & 1u)) return -1;
-      return kpref[h * kBKWords + (kb >> 5)] + __popc(bits[kb >> 5] & ((1u << (kb & 31)) - 1u));
-    };
-    // (3) output blocks (pairs of blocks), one warp each
     if (!over) {
-      for (int q = warp; q < nj; q += kB2Warps) {
+      int64_t *wa = mla + warp * kMML;
+      int64_t *wb = mlb + warp * kMML;
+      for (int q = warp; q < nj; q += kMWarps) {
         const int J = jlist[q];
-        double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;
-        if (a.self_coef != 0.0) {  // self term: A_hJ
-          const int r0 = lookup(0, J), r1 = lookup(1, J);
-          if (r0 >= 0) {
-            x00 = __dmul_rn(a.self_coef, aval[r0 * 64 + i0 * 8 + lj]);
-            x01 = __dmul_rn(a.self_coef, aval[r0 * 64 + i1 * 8 + lj]);
-          }
-          if (r1 >= 0) {
-            x10 = __dmul_rn(a.self_coef, aval[(kBACap + r1) * 64 + i0 * 8 + lj]);
-            x11 = __dmul_rn(a.self_coef, aval[(kBACap + r1) * 64 + i1 * 8 + lj]);
+        double x0 = 0.0, x1 = 0.0;
+        if (a.self_coef != 0.0) {  // self term: A_IJ, if row I of A has block J
+          const int kb = J - kmin;
+          if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
+            const int ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
+            const double *ap = Bv.bval + (ab0 + ra) * 64;
+            x0 = a.self_coef * __ldg(ap + soff0);
+            x1 = a.self_coef * __ldg(ap + soff1);
           }
         }
-        int64_t *wb = mlb + warp * kBML;
-        int32_t *wk0 = mlk + warp * kBML, *wk1 = mlk + (kB2Warps + warp) * kBML;
-        double *stg = wstage + warp * kBPF * 64;
         const int64_t t0 = Bv.tp[J], t1 = Bv.tp[J + 1];
         int64_t tb0 = t0;
         while (tb0 < t1) {
+          // matches K of row I and column J (ascending K), listed in batches
           int nm = 0;
-          for (; tb0 < t1 && nm <= kBML - 32; tb0 += 32) {
-            const int64_t t = tb0 + lane;
-            int ra0 = -1, ra1 = -1;
+          for (; tb0 < t1 && nm <= kMML - 32; tb0 += 32) {
+            const int64_t tt = tb0 + lane;
+            int ra = -1;
             int64_t bidx = 0;
-            if (t < t1) {
-              const int K = Bv.tk[t];
-              ra0 = lookup(0, K);
-              ra1 = lookup(1, K);
-              if (ra0 >= 0 || ra1 >= 0) bidx = Bv.tb[t];
+            if (tt < t1) {
+              const int kb = Bv.tk[tt] + (int)Bv.kb0 - kmin;
+              if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
+                ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
+                bidx = Bv.tb[tt];
+              }
             }
-            const bool hit = ra0 >= 0 || ra1 >= 0;
-            const unsigned m = __ballot_sync(FULL_MASK, hit);
-            if (hit) {
+            const unsigned m = __ballot_sync(FULL_MASK, ra >= 0);
+            if (ra >= 0) {
               const int pos = nm + __popc(m & lanemask_lt());
-              wk0[pos] = ra0 >= 0 ? ra0 : zero_blk;
-              wk1[pos] = ra1 >= 0 ? kBACap + ra1 : zero_blk;
+              wa[pos] = ab0 + ra;
               wb[pos] = bidx;
             }
             nm += __popc(m);
           }
           __syncwarp();
           nbp += nm;
-          double2 pf[kBPF];
+          double2 av[kMPF];
+          double bl[kMPF], bh[kMPF];
 #pragma unroll
-          for (int d = 0; d < kBPF; d++)
-            if (d < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[d] * 64)[lane];
-          int t = 0;
-          for (; t + kBPF <= nm; t += kBPF) {
+          for (int d = 0; d < kMPF; d++)
+            if (d < nm) {
+              av[d] = __ldg(bv2 + wa[d] * 32 + lane);
+              const double *bp = Bv.bval + wb[d] * 64 + boff;
+              bl[d] = __ldg(bp);
+              bh[d] = __ldg(bp + 32);
+            }
+          for (int u = 0; u < nm; u += kMPF) {
+            double2 ca[kMPF];
+            double cl[kMPF], ch[kMPF];
 #pragma unroll
-            for (int d = 0; d < kBPF; d++) reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
-            __syncwarp();
+            for (int d = 0; d < kMPF; d++) {
+              ca[d] = av[d];
+              cl[d] = bl[d];
+              ch[d] = bh[d];
+            }
 #pragma unroll
-            for (int d = 0; d < kBPF; d++)
-              if (t + kBPF + d < nm) pf[d] = reinterpret_cast<const double2 *>(Bv.bval + wb[t + kBPF + d] * 64)[lane];
+            for (int d = 0; d < kMPF; d++)
+              if (u + kMPF + d < nm) {
+                av[d] = __ldg(bv2 + wa[u + kMPF + d] * 32 + lane);
+                const double *bp = Bv.bval + wb[u + kMPF + d] * 64 + boff;
+                bl[d] = __ldg(bp);
+                bh[d] = __ldg(bp + 32);
+              }
 #pragma unroll
-            for (int d = 0; d < kBPF; d++)
-              bsr2_block_fma(stg + d * 64, aval + wk0[t + d] * 64, aval + wk1[t + d] * 64, i0, i1, lj,
-                             x00, x01, x10, x11);
-            __syncwarp();
+            for (int d = 0; d < kMPF; d++)
+              if (u + d < nm) {
+                dmma884(x0, x1, ca[d].x, cl[d]);
+                dmma884(x0, x1, ca[d].y, ch[d]);
+              }
           }
-          if (t < nm) {
-#pragma unroll
-            for (int d = 0; d < kBPF; d++)
-              if (t + d < nm) reinterpret_cast<double2 *>(stg + d * 64)[lane] = pf[d];
-            __syncwarp();
-#pragma unroll
-            for (int d = 0; d < kBPF; d++)
-              if (t + d < nm)
-                bsr2_block_fma(stg + d * 64, aval + wk0[t + d] * 64, aval + wk1[t + d] * 64, i0, i1,
-                               lj, x00, x01, x10, x11);
-            __syncwarp();
+          __syncwarp();
+        }
+        // classify (Algorithm 4.1 floor, fused first pass) and pack into scratch
+        const bool ok = g < nr;
+        bool st0 = false, st1 = false;
+        if (ok && x0 != 0.0) {
+          nz++;
+          if (fabs(x0) > a.floor_tau) {
+            st0 = true;
+            if (fabs(x0) <= a.eps_g) q1 += x0 * x0;
+            else c1++;
+          } else {
+            fs += x0 * x0;
           }
         }
-        // raw values to scratch (block pair q: row h*8 + i at q*128 + (h*8 + i)*8), kept
-        // counts per (q, row) from ballots
-        double *sq = scr + (size_t)q * 128;
-        sq[i0 * 8 + lj] = x00;
-        sq[i1 * 8 + lj] = x01;
-        sq[64 + i0 * 8 + lj] = x10;
-        sq[64 + i1 * 8 + lj] = x11;
-        auto kept = [&](double x) { return x != 0.0 && fabs(x) > a.floor_tau; };
-        const unsigned m00 = __ballot_sync(FULL_MASK, kept(x00)), m01 = __ballot_sync(FULL_MASK, kept(x01));
-        const unsigned m10 = __ballot_sync(FULL_MASK, kept(x10)), m11 = __ballot_sync(FULL_MASK, kept(x11));
-        if (lj == 0) {
-          jcnt[q * 16 + i0] = (uint16_t)__popc((m00 >> (li * 8)) & 0xFFu);
-          jcnt[q * 16 + i1] = (uint16_t)__popc((m01 >> (li * 8)) & 0xFFu);
-          jcnt[q * 16 + 8 + i0] = (uint16_t)__popc((m10 >> (li * 8)) & 0xFFu);
-          jcnt[q * 16 + 8 + i1] = (uint16_t)__popc((m11 >> (li * 8)) & 0xFFu);
+        if (ok && x1 != 0.0) {
+          nz++;
+          if (fabs(x1) > a.floor_tau) {
+            st1 = true;
+            if (fabs(x1) <= a.eps_g) q1 += x1 * x1;
+            else c1++;
+          } else {
+            fs += x1 * x1;
+          }
         }
+        const unsigned b0m = __ballot_sync(FULL_MASK, st0), b1m = __ballot_sync(FULL_MASK, st1);
+        const unsigned mask = spread4((b0m >> (4 * g)) & 0xFu) | (spread4((b1m >> (4 * g)) & 0xFu) << 1);
+        const int p0 = __popc(mask & ((1u << (2 * t)) - 1u));
+        double *dst = scr + ((size_t)q * 8 + g) * 8;
+        if (st0) dst[p0] = x0;
+        if (st1) dst[p0 + (st0 ? 1 : 0)] = x1;
+        if (t == 0) jm[q * 8 + g] = (uint8_t)mask;
       }
     }
-    if (a.prof && lane == 0 && nbp) atomicAdd(&a.prof[0], 2 * nbp);
+    if (a.prof && lane == 0 && nbp) atomicAdd(&a.prof[0], nbp);
+    // per-row sums: the 4 lanes of a row, then warps in fixed order
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      fs += __shfl_xor_sync(FULL_MASK, fs, o);
+      q1 += __shfl_xor_sync(FULL_MASK, q1, o);
+      nz += __shfl_xor_sync(FULL_MASK, nz, o);
+      c1 += __shfl_xor_sync(FULL_MASK, c1, o);
+    }
+    if (t == 0) {
+      s_fs[warp][g] = fs;
+      s_p1[warp][g] = q1;
+      s_nz[warp][g] = nz;
+      s_c1[warp][g] = c1;
+    }
     __syncthreads();
-    // (4) one warp per row (16 rows): Algorithm 4.1 row sums from the raw blocks, kept entries
-    // staged contiguously in column order
+    // (4) stage each row's kept entries contiguously (warp i: row i)
     if (over) {
-      if (tid < 16 && (tid & 7) < s_nr[tid >> 3]) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)(8 * s_I[tid >> 3] + (tid & 7));
-    } else if ((warp & 7) < s_nr[warp >> 3]) {
-      const int h = warp >> 3, i = warp & 7;
-      const int64_t r = 8 * s_I[h] + i;
+      if (tid < nr) fail_rows[atomicAdd(fail_count, 1)] = (int32_t)(r0 + tid);
+    } else if (warp < nr) {
+      const int i = warp;
+      const int64_t r = r0 + i;
       long long tot = 0;
       for (int q0 = 0; q0 < nj; q0 += 32) {
-        const int c = q0 + lane < nj ? jcnt[(q0 + lane) * 16 + warp] : 0;
+        const int c = q0 + lane < nj ? __popc((unsigned)jm[(q0 + lane) * 8 + i]) : 0;
         tot += __reduce_add_sync(FULL_MASK, c);
       }
       unsigned long long off = 0;
       if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)tot);
       off = __shfl_sync(FULL_MASK, off, 0);
-      const bool ok = (long long)off + tot <= a.pool_cap;
-      long long pos = (long long)off;
-      double fs = 0.0, p1 = 0.0;
-      long long nz = 0, c1 = 0;
-      for (int q0 = 0; q0 < nj; q0 += 32) {
-        const int q = q0 + lane;
-        const int c = q < nj ? jcnt[q * 16 + warp] : 0;
-        int v = c;
+      const bool okp = (long long)off + tot <= a.pool_cap;
+      if (okp) {
+        long long pos = (long long)off;
+        for (int q0 = 0; q0 < nj; q0 += 32) {
+          const int q = q0 + lane;
+          unsigned m = q < nj ? (unsigned)jm[q * 8 + i] : 0u;
+          const int c = __popc(m);
+          int v = c;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(FULL_MASK, v, o);
-          if (lane >= o) v += y;
-        }
-        if (q < nj) {
-          long long pp = pos + v - c;
-          const double *src = scr + (size_t)q * 128 + warp * 8;
-          const int J = jlist[q];
-#pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const double x = src[j];
-            if (x != 0.0) {
-              nz++;
-              if (fabs(x) > a.floor_tau) {
-                if (fabs(x) <= a.eps_g) p1 += x * x;
-                else c1++;
-                if (ok) {
-                  a.pool_col[pp] = 8 * J + j;
-                  a.pool_val[pp] = x;
-                }
-                pp++;
-              } else {
-                fs += x * x;
-              }
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL_MASK, v, o);
+            if (lane >= o) v += y;
+          }
+          if (c > 0) {
+            long long p = pos + v - c;
+            const double *src = scr + ((size_t)q * 8 + i) * 8;
+            const int J = jlist[q];
+            for (int e = 0; m; e++, p++) {
+              const int j = __ffs(m) - 1;
+              m &= m - 1;
+              a.pool_col[p] = 8 * J + j;
+              a.pool_val[p] = src[e];
             }
           }
+          pos += __shfl_sync(FULL_MASK, v, 31);
         }
-        pos += __shfl_sync(FULL_MASK, v, 31);
       }
-      fs = warp_sum(fs);
-      p1 = warp_sum(p1);
-      nz = warp_sum(nz);
-      c1 = warp_sum(c1);
       if (lane == 0) {
-        if (!ok) atomicOr(a.flags, 1);
+        double f = 0.0, p1 = 0.0;
+        long long z = 0, cc = 0;
+        for (int w = 0; w < kMWarps; w++) {
+          f += s_fs[w][i];
+          p1 += s_p1[w][i];
+          z += s_nz[w][i];
+          cc += s_c1[w][i];
+        }
+        if (!okp) atomicOr(a.flags, 1);
         a.row_off[r] = (int64_t)off;
         a.row_cnt[r] = tot;
-        a.row_fsum[r] = fs;
-        a.row_nnz[r] = nz;
+        a.row_fsum[r] = f;
+        a.row_nnz[r] = z;
         if (a.row_p1) {
           a.row_p1[r] = p1;
-          a.row_c1[r] = c1;
+          a.row_c1[r] = cc;
         }
       }
     }
     __syncthreads();
-    for (int i = tid; i < 2 * kBKWords; i += kB2Threads) kbits[i] = 0u;
-    for (int i = tid; i < njw; i += kB2Threads) jbits[i] = 0u;
+    for (int i = tid; i < nkw; i += kMThreads) kbits[i] = 0u;
+    for (int i = tid; i < njw; i += kMThreads) jbits[i] = 0u;
   }
 }
 
-void launch_numeric_bsr2(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+void launch_numeric_bsrm(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                          int32_t *fail_rows, int *fail_count, cudaStream_t st) {
-  if (Bv.nbr == 0) return;
-  const int smem = bsr2_numeric_smem_bytes();
-  cudaFuncSetAttribute(k_numeric_bsr2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (Bv.nbr_a == 0) return;
+  const int smem = bsrm_numeric_smem_bytes();
+  cudaFuncSetAttribute(k_numeric_bsrm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
-  k_numeric_bsr2<<<a.grid, kB2Threads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
+  k_numeric_bsrm<<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
 }
+
+
 
 // ------------------------------------------------------------------------------------
 // Diagonal structure of H0 (plan time): offsets d = j - k present anywhere in H0, as a
@@ -4259,216 +2707,6 @@ void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_
   kf<<<a.grid, kDWarps * 32, smem, st>>>(a, D, slots, fail_rows, fail_count);
 }
 
-// ------------------------------------------------------------------------------------
-// K3w numeric filtered SpGEMM, one WARP per output row, conflict-free dense window.
-//
-// Row r of C~ = self_coef * A(r,:) + sum_k a_rk B(k,:) is built in column passes: a pass
-// starts at the smallest column any remaining entry of row r's sources reaches (B rows
-// are sorted, every k keeps a cursor that only moves forward) and covers `window`
-// columns of a private shared-memory window.  Inside a pass the warp adds the self term
-// first, then the B rows one k at a time in ascending k, lanes over a row's entries
-// (distinct columns), so no two lanes ever touch the same slot: no atomics, no barriers,
-// and every entry is accumulated exactly as the oracle does it --
-// acc = self*a_rj; acc = acc + (a_rk * b_kj) for ascending k, then acc / divisor -- with
-// explicit _rn intrinsics (no FMA contraction), i.e. bit-identical values of C~.
-// The flush scans only the touched span of the window, classifies (Algorithm 4.1 floor,
-// see k_numeric) and stages entries in column order: rows come out sorted.
-// ------------------------------------------------------------------------------------
-constexpr int kWarpRowWarps = 4;        // warps per CTA
-constexpr int kWarpRowCursors = 512;    // cursors kept in shared memory per warp
-
-int warp_numeric_smem_bytes(int window) {
-  return kWarpRowWarps * (window * (int)sizeof(double) + kWarpRowCursors * 12);
-}
-
-__global__ void __launch_bounds__(kWarpRowWarps * 32) k_numeric_warp(NumericArgs a) {
-  extern __shared__ double wsm[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int W = a.window;
-  double *win = wsm + (size_t)wib * (W + (kWarpRowCursors * 12) / 8);
-  int64_t *scur = reinterpret_cast<int64_t *>(win + W);
-  int32_t *slen = reinterpret_cast<int32_t *>(scur + kWarpRowCursors);
-  const int64_t gw = (int64_t)blockIdx.x * kWarpRowWarps + wib;
-  int64_t *gcur = a.cursor + gw * 2 * a.cursor_cap;
-  int32_t *sc = a.scr_col + gw * a.scr_cap;
-  double *sv = a.scr_val + gw * a.scr_cap;
-  for (int i = lane; i < W; i += 32) win[i] = 0.0;
-  __syncwarp();
-  for (;;) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(a.row_counter, 1);
-    idx = __shfl_sync(FULL_MASK, idx, 0);
-    if (idx >= a.nlist) break;
-    const int64_t r = a.order ? (int64_t)a.order[idx] : (int64_t)idx;
-    const int64_t pa0 = a.A.rp[r], pa1 = a.A.rp[r + 1];
-    const int nk = (int)(pa1 - pa0);
-    // per-k cursor (absolute position in B) and entries left; shared memory when they
-    // fit, else this warp's global scratch
-    int64_t *cur = nk <= kWarpRowCursors ? scur : gcur;
-    int32_t *rem_end = nk <= kWarpRowCursors ? slen : reinterpret_cast<int32_t *>(gcur + a.cursor_cap);
-    for (int j = lane; j < nk; j += 32) {
-      const int64_t k = (int64_t)a.A.col[pa0 + j] - a.B.row0;
-      int64_t b0 = 0, b1 = 0;
-      if (k >= 0 && k < a.B.nrows) {
-        b0 = a.B.rp[k];
-        b1 = a.B.rp[k + 1];
-      }
-      cur[j] = b0;
-      rem_end[j] = (int32_t)(b1 - b0);
-    }
-    __syncwarp();
-    long long self_pos = pa0;
-    long long nst = 0;
-    double fs = 0.0;
-    long long nnzu = 0;
-    for (;;) {
-      // next column reached by any remaining source
-      int32_t nxt = INT32_MAX;
-      for (int j = lane; j < nk; j += 32) {
-        if (rem_end[j] > 0) {
-          int32_t c = a.B.col[cur[j]];
-          nxt = c < nxt ? c : nxt;
-        }
-      }
-      if (a.self_coef != 0.0 && lane == 0 && self_pos < pa1) {
-        int32_t c = a.A.col[self_pos];
-        nxt = c < nxt ? c : nxt;
-      }
-      nxt = warp_min(nxt);
-      nxt = __shfl_sync(FULL_MASK, nxt, 0);
-      if (nxt == INT32_MAX) break;
-      const int64_t c0 = nxt;
-      const int64_t c1 = c0 + W;
-      int tmin = INT32_MAX, tmax = -1;
-      // self term (the 2T of Eq. 2.7), stored first
-      if (a.self_coef != 0.0) {
-        for (;;) {
-          const long long p = self_pos + lane;
-          bool v = false;
-          if (p < pa1) {
-            const int32_t c = a.A.col[p];
-            v = (int64_t)c < c1;
-            if (v) {
-              const int o = (int)(c - c0);
-              win[o] = __dmul_rn(a.self_coef, a.A.val[p]);
-              tmin = o < tmin ? o : tmin;
-              tmax = o > tmax ? o : tmax;
-            }
-          }
-          const int cnt = __popc(__ballot_sync(FULL_MASK, v));
-          self_pos += cnt;
-          if (cnt < 32) break;
-        }
-      }
-      // products, ascending k
-      for (int j0 = 0; j0 < nk; j0 += 32) {
-        const int j = j0 + lane;
-        long long mypos = 0;
-        int myrem = 0;
-        bool act = false;
-        if (j < nk) {
-          myrem = rem_end[j];
-          if (myrem > 0) {
-            mypos = cur[j];
-            act = (int64_t)a.B.col[mypos] < c1;
-          }
-        }
-        unsigned mask = __ballot_sync(FULL_MASK, act);
-        while (mask) {
-          const int jj = __ffs(mask) - 1;
-          mask &= mask - 1;
-          long long pos = __shfl_sync(FULL_MASK, mypos, jj);
-          const int rem = __shfl_sync(FULL_MASK, myrem, jj);
-          const long long end = pos + rem;
-          const double av = a.A.val[pa0 + j0 + jj];
-          for (;;) {
-            const long long p = pos + lane;
-            bool v = false;
-            if (p < end) {
-              const int32_t c = a.B.col[p];
-              v = (int64_t)c < c1;
-              if (v) {
-                const int o = (int)(c - c0);
-                win[o] = __dadd_rn(win[o], __dmul_rn(av, a.B.val[p]));
-                tmin = o < tmin ? o : tmin;
-                tmax = o > tmax ? o : tmax;
-              }
-            }
-            const int cnt = __popc(__ballot_sync(FULL_MASK, v));
-            pos += cnt;
-            if (cnt < 32 || pos >= end) break;
-          }
-          if (lane == jj) {
-            myrem -= (int)(pos - mypos);
-            mypos = pos;
-          }
-        }
-        if (j < nk && act) {
-          cur[j] = mypos;
-          rem_end[j] = myrem;
-        }
-      }
-      __syncwarp();
-      // flush the touched span [tmin, tmax] in column order
-      tmin = warp_min(tmin);
-      tmax = warp_max(tmax);
-      tmin = __shfl_sync(FULL_MASK, tmin, 0);
-      tmax = __shfl_sync(FULL_MASK, tmax, 0);
-      for (int base = tmin; base <= tmax; base += 32) {
-        const int o = base + lane;
-        bool st = false;
-        double x = 0.0;
-        if (o <= tmax) {
-          x = win[o] / a.divisor;
-          win[o] = 0.0;
-          if (x != 0.0) {
-            nnzu++;
-            st = fabs(x) > a.floor_tau;
-            if (!st) fs += x * x;
-          }
-        }
-        const unsigned m = __ballot_sync(FULL_MASK, st);
-        if (st) {
-          const long long pp = nst + __popc(m & lanemask_lt());
-          if (pp < a.scr_cap) {
-            sc[pp] = (int32_t)(c0 + o);
-            sv[pp] = x;
-          }
-        }
-        nst += __popc(m);
-      }
-      __syncwarp();
-    }
-    fs = warp_sum(fs);
-    nnzu = warp_sum(nnzu);
-    unsigned long long off = 0;
-    if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)nst);
-    off = __shfl_sync(FULL_MASK, off, 0);
-    const bool ok = (long long)off + nst <= a.pool_cap && nst <= a.scr_cap;
-    if (ok) {
-      for (long long t = lane; t < nst; t += 32) {
-        a.pool_col[off + t] = sc[t];
-        a.pool_val[off + t] = sv[t];
-      }
-    }
-    if (lane == 0) {
-      if (!ok) atomicOr(a.flags, nst > a.scr_cap ? 2 : 1);
-      a.row_off[r] = (int64_t)off;
-      a.row_cnt[r] = nst;
-      a.row_fsum[r] = fs;
-      a.row_nnz[r] = nnzu;
-    }
-    __syncwarp();
-  }
-}
-
-void launch_numeric_warp(const NumericArgs &a, cudaStream_t st) {
-  if (a.A.nrows == 0 || a.nlist == 0) return;
-  int smem = warp_numeric_smem_bytes(a.window);
-  cudaFuncSetAttribute(k_numeric_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  KL;
-  k_numeric_warp<<<a.grid, kWarpRowWarps * 32, smem, st>>>(a);
-}
 
 // ------------------------------------------------------------------------------------
 // K4 compaction: keep staged entries with |x| > tau (Alg. 4.1 step 3).

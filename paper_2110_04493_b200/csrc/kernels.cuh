@@ -104,21 +104,10 @@ struct NumericArgs {
 };
 int numeric_smem_bytes(int window);
 void launch_numeric(const NumericArgs &a, cudaStream_t st);
-// warp-per-row conflict-free window variant (bit-identical accumulation order)
-constexpr int kWarpRowWarpsPerCta = 4;
-int warp_numeric_smem_bytes(int window);
-void launch_numeric_warp(const NumericArgs &a, cudaStream_t st);
-// k-synchronous hash variant (no atomics on values, bit-identical accumulation order)
-void launch_numeric_ksync(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
-                          cudaStream_t st);
 // k-synchronous paged variant (no probing, sorted flush, bit-identical order)
 int paged_smem_bytes();
 void launch_numeric_paged(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
                           cudaStream_t st);
-// the same with 128 threads per row, 4 entries per thread per k, smaller footprint
-int paged2_smem_bytes();
-void launch_numeric_paged2(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
-                           cudaStream_t st);
 // Taylor term by pull over H0^T (bit-identical order); BT = CSC of B (= B^T as CSR)
 int taylor_pull_smem_bytes();
 void launch_taylor_pull(const NumericArgs &a, const CsrView &BT, int32_t *fail_rows,
@@ -143,18 +132,6 @@ int taylor_dia_smem_bytes(int slots);
 // Taylor term by diagonal push (bit-identical order); rows that do not fit -> fail_rows
 void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_t *fail_rows,
                        int *fail_count, cudaStream_t st);
-// grouped-row variant (kGroupRows rows per CTA share the B-row gathers; bit-identical
-// order); rows of groups that do not fit -> fail_rows
-constexpr int kGroupRows = 4;
-int group_smem_bytes(int slots);
-void launch_numeric_group(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
-                          cudaStream_t st);
-// one-warp-per-row variant (kRowWarpRows rows per CTA share a page table; no barrier per
-// k; bit-identical order); rows of groups that do not fit -> fail_rows
-constexpr int kRowWarpRows = 8;
-int rowwarp_smem_bytes(int slots);
-void launch_numeric_rowwarp(const NumericArgs &a, int slots, int32_t *fail_rows, int *fail_count,
-                            cudaStream_t st);
 // BSR-8 view (squarings on one GPU): conversion, block transpose, numeric kernel
 struct BsrView {
   int64_t nbr = 0;
@@ -172,11 +149,10 @@ struct BsrView {
 };
 constexpr int kBsrScratchPerCta = 512 * 64;  // doubles of output-block scratch per CTA
 constexpr int kBsrMaxRowBlocks = 136;        // blocks of a block row the numeric kernel holds
-constexpr int kBsr2JCap = 768;               // K3b2: output block pairs per block-row pair
-constexpr int kBsr2ScratchPerCta = kBsr2JCap * 128;  // doubles of K3b2 scratch per CTA
 void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st);
+// frag = true: values in K3m's tensor-core fragment order (see kernels.cu), else row-major
 void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
-                     double *bval, int *flags, cudaStream_t st);
+                     double *bval, int *flags, cudaStream_t st, bool frag = false);
 // tk_tmp / tb_tmp: nb-sized scratch; keys_out: nb int32 scratch; sort_tmp: bytes from
 // bsr_transpose_temp_bytes(nb)
 size_t bsr_transpose_temp_bytes(int64_t nb);
@@ -188,14 +164,14 @@ void launch_bsr_transpose(int64_t nbr, int64_t nbc, int64_t nb, const int64_t *b
 int bsr_numeric_smem_bytes();
 void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                         int32_t *fail_rows, int *fail_count, cudaStream_t st);
-// K3b2: the same product over pairs of block rows (one 512-thread CTA per pair, scratch of
-// kBsrScratchPerCta * 2 doubles per CTA)
-void launch_numeric_bsr2(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+// K3m: the block product on the fp64 tensor-core instruction (DMMA m8n8k4; BSR values in
+// fragment order, launch_bsr_fill(frag = true)); no limit on the blocks of a row of A; scratch
+// of kBsrMJCap * 65 doubles per CTA; rows it cannot hold -> fail_rows
+constexpr int kBsrMJCap = 8192;              // output blocks per block row (K3m)
+constexpr int kBsrMBlocksPerSm = 2;          // K3m CTAs per SM
+int bsrm_numeric_smem_bytes();
+void launch_numeric_bsrm(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                          int32_t *fail_rows, int *fail_count, cudaStream_t st);
-// hash-accumulator variant; rows whose table over-fills are appended to fail_rows
-int hash_smem_bytes();
-void launch_numeric_hash(const NumericArgs &a, int32_t *fail_rows, int *fail_count,
-                         cudaStream_t st);
 
 // --- K6 Algorithm 4.1 pass -------------------------------------------------------
 // out[0] = sum over x[0..cnt) of x^2 for |x| <= tau (deterministic order for fixed layout)

@@ -31,7 +31,7 @@ def run_gpu(B, H, eps_tol=1e-16, **opts):
 
 def run_both(B, H, eps_tol=1e-16, **opts):
     Eg, st = run_gpu(B, H, eps_tol, **opts)
-    oo = {k: v for k, v in opts.items() if k not in ("window_cols", "kernel")}
+    oo = {k: v for k, v in opts.items() if k not in ("window_cols", "kernel", "exact_products")}
     Eo, tr = O.expm(H, eps_tol, nthreads=NTHREADS, **oo)
     return Eg, st, Eo, tr
 
@@ -232,7 +232,7 @@ HAND = [
     ([1.0] * 4, 1e-12, 0.1, 1, 1e-12),
     ([1.0] + [1e-4] * 16, 1e-3, 0.1, 1, 1e-3),
     ([1.0] * 2 + [4e-4] * 25 + [1e-4] * 100, 1e-3, 0.1, 3, 2e-4),
-    ([5.0, 0.5], 1.0, 0.1, 0, float("inf")),
+    ([5.0, 0.5], 1.0, 0.1, 1, 1.0),  # reading R1: the first pass always runs
 ]
 
 
@@ -260,21 +260,49 @@ def test_alg41_random_vs_oracle(B):
         assert d == pytest.approx(dropped_o, rel=1e-10, abs=1e-300)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
+@pytest.mark.parametrize("kernel", [0, 3, 5, 6, 7, 11, 13])
 @pytest.mark.parametrize("name", ["heat2d_pm10_20", "structural_24", "heat3d_9", "banded_nonsym"])
 def test_accumulator_variants(B, kernel, name):
-    """Every K3 accumulator (hash, warp-window, block-window) meets parity."""
+    """Every K3 kernel (block-window 3, paged 5, Taylor pull 6 / diagonal 7, block-sparse
+    exact 11 and tensor-core 13) meets parity."""
     H = SMALL[name]()
     Eg, st, Eo, tr = run_both(B, H, kernel=kernel)
     assert_parity(Eg, st, Eo, tr)
 
 
-@pytest.mark.parametrize("kernel", [2, 4, 5, 8, 9, 10, 11, 12])
+def assert_products_close(G, Ct, A, Bm, self_coef, row_slice=None):
+    """C~ from the tensor-core kernel 13 (fused multiply-adds, K ascending in 8x8x4 steps)
+    against the oracle's C~: same pattern, and every value within the running-sum rounding
+    bound (m + 2) u sum_k |a_rk||b_kj| (+ |self a_rj|), m = the products of the row (Higham's
+    gamma_m bound, u = 2^-53)."""
+    Aa = CSR(A.n, A.rowptr, A.col, np.abs(A.val))
+    Ba = CSR(Bm.n, Bm.rowptr, Bm.col, np.abs(Bm.val))
+    Abs = O.spgemm(Aa, Ba, abs(self_coef), 1.0)
+    rows_prod = np.array([np.diff(Bm.rowptr)[A.col[A.rowptr[r]:A.rowptr[r + 1]]].sum() + 1
+                          for r in range(A.rowptr.size - 1)], dtype=np.float64)
+    gs, cs = scipy_like(G), scipy_like(Ct)
+    bound = scipy_like(Abs).multiply(2.0 ** -53 * (rows_prod[:, None] + 2)).toarray()
+    if row_slice is not None:
+        bound = bound[row_slice[0]:row_slice[1]]
+    diff = np.abs((gs - cs).toarray())
+    assert (diff <= bound + 1e-300).all(), float((diff - bound).max())
+    # pattern: equal except where the exact value cancels to (near) zero
+    pg, pc = (gs != 0).toarray(), (cs != 0).toarray()
+    assert ((pg == pc) | (np.maximum(np.abs(gs.toarray()), np.abs(cs.toarray())) <= bound)).all()
+
+
+def scipy_like(M):
+    import scipy.sparse as sp
+    return sp.csr_matrix((M.val, M.col, M.rowptr), shape=(M.rowptr.size - 1, M.n))
+
+
+@pytest.mark.parametrize("kernel", [5, 11, 13])
 @pytest.mark.parametrize("seed", range(4))
 def test_bit_exact_products(B, seed, kernel):
-    """The warp-window, k-sync hash, paged and grouped kernels accumulate the self term
-    first, then ascending k with round-to-nearest products and sums (no FMA): C~ is
-    bit-identical to the oracle."""
+    """The paged (5) and exact block (11) kernels accumulate the self term first, then
+    ascending k with round-to-nearest products and sums (no FMA): C~ is bit-identical to the
+    oracle.  The tensor-core block kernel (13) fuses the products: within the rounding
+    bound."""
     import torch
     n = 300
     A = _rand_csr(n, 9, 0.6, 300 + seed, empty_rows=(3, 200))
@@ -282,6 +310,9 @@ def test_bit_exact_products(B, seed, kernel):
                                                                   0.0, kernel=kernel)
     Ct = O.spgemm(A, A, 2.0, 1.0)
     G = from_dev(n, rp, ci, va)
+    if kernel == 13:
+        assert_products_close(G, Ct, A, A, 2.0)
+        return
     assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
     assert np.array_equal(G.val, Ct.val)  # bit-exact
 
@@ -350,10 +381,10 @@ def _coo(n, rows, cols, vals):
     return coo_to_csr(n, rows[first], cols[first], np.asarray(vals, np.float64)[first])
 
 
-@pytest.mark.parametrize("kernel", [8, 9, 10, 0])
-def test_group_kernel_long_b_rows(B, kernel):
-    """B rows longer than the grouped kernel's CTA (> 512 entries): the extra entries loop;
-    A x B + 2A is still bit-identical to the oracle."""
+@pytest.mark.parametrize("kernel", [5, 3])
+def test_long_b_rows(B, kernel):
+    """B rows longer than a CTA (> 512 entries) in the paged and window kernels (A != B:
+    not a squaring): A x B + 2A is bit-identical to the oracle."""
     n = 3000
     rng = np.random.default_rng(11)
     Bm = random_banded(n, 450, 0.85, 1.0, 12)
@@ -369,10 +400,10 @@ def test_group_kernel_long_b_rows(B, kernel):
     assert np.array_equal(G.val, Ct.val)
 
 
-@pytest.mark.parametrize("kernel", [8, 9, 11, 12])
-def test_group_kernel_fallback_wide_rows(B, kernel):
-    """Rows whose k span exceeds the grouped kernel's union bitmap fall through to the paged
-    kernel; the result is unchanged (bit-identical to the oracle)."""
+@pytest.mark.parametrize("kernel", [11, 13])
+def test_block_kernel_fallback_wide_rows(B, kernel):
+    """Block rows whose column span exceeds the block kernels' bitmaps fall through to the
+    paged kernel; the result is unchanged (bit-identical to the oracle)."""
     n = 150_000
     rng = np.random.default_rng(13)
     rows = np.repeat(np.arange(n), 3)
@@ -387,22 +418,55 @@ def test_group_kernel_fallback_wide_rows(B, kernel):
     assert np.array_equal(G.val, Ct.val)
 
 
-@pytest.mark.parametrize("kernel", [11, 12])
+@pytest.mark.parametrize("kernel", [11, 13])
 @pytest.mark.parametrize("n", [1, 7, 8, 9, 17, 250, 1003])
 def test_bsr_kernel_bit_exact_sizes(B, n, kernel):
-    """The block kernels (BSR-8 view; 12 = block-row pairs, odd block-row counts at n = 1,
-    9, 17, 1003) on sizes that are not multiples of 8, with empty rows: C~ = 2A + A*A
-    bit-identical to the oracle."""
+    """The block kernels (BSR-8 view) on sizes that are not multiples of 8, with empty
+    rows: C~ = 2A + A*A bit-identical to the oracle (11), within the rounding bound (13)."""
     A = _rand_csr(n, min(n, 12), 0.5, 400 + n, empty_rows=tuple(r for r in (0, 3, n // 2) if r < n))
     (rp, ci, va), _, _, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(A), 2.0, 1.0, 0.0,
                                                            kernel=kernel)
     Ct = O.spgemm(A, A, 2.0, 1.0)
     G = from_dev(n, rp, ci, va)
+    if kernel == 13:
+        assert_products_close(G, Ct, A, A, 2.0)
+        return
     assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
     assert np.array_equal(G.val, Ct.val)
 
 
-@pytest.mark.parametrize("kernel", [11, 0, 5])
+EMPTY_DIAG = {
+    # a single entry in block (0, 1): block row 1 is empty, so no B_K of row 0 has block 1;
+    # the self term 2 A alone must produce C~(0, 8) (ADVICE r1)
+    "single_offdiag": lambda: _coo(16, [0], [8], [1.5]),
+    # strictly upper triangular (nilpotent, DAG-like): empty diagonal blocks everywhere
+    "strict_upper": lambda: dense_to_csr(np.triu(csr_to_dense(random_banded(200, 20, 0.2, 1.0, 41)), 1)),
+    # bipartite [[0, X], [0, 0]]
+    "bipartite": lambda: dense_to_csr(np.block([[np.zeros((64, 64)), csr_to_dense(random_banded(64, 30, 0.3, 1.0, 42))],
+                                               [np.zeros((64, 64)), np.zeros((64, 64))]])),
+}
+
+
+@pytest.mark.parametrize("kernel", [11, 13, 5])
+@pytest.mark.parametrize("name", sorted(EMPTY_DIAG))
+def test_block_kernels_empty_diagonal_blocks(B, kernel, name):
+    """Squarings C~ = 2A + A*A where A has empty diagonal blocks: every self-term block is a
+    candidate output block even when no product reaches it."""
+    A = EMPTY_DIAG[name]()
+    n = A.n
+    (rp, ci, va), _, _, nnz_unf = B.sexpm_filtered_product(n, to_dev(A), to_dev(A), 2.0, 1.0, 0.0,
+                                                           kernel=kernel)
+    Ct = O.spgemm(A, A, 2.0, 1.0)
+    G = from_dev(n, rp, ci, va)
+    assert nnz_unf == Ct.nnz
+    if kernel == 13:
+        assert_products_close(G, Ct, A, A, 2.0)
+        return
+    assert np.array_equal(G.rowptr, Ct.rowptr) and np.array_equal(G.col, Ct.col)
+    assert np.array_equal(G.val, Ct.val)
+
+
+@pytest.mark.parametrize("kernel", [11, 13, 5])
 @pytest.mark.parametrize("r0,r1,h0,h1", [(96, 200, 88, 208), (96, 203, 88, 216), (0, 57, 0, 64),
                                          (100, 180, 88, 192), (200, 257, 192, 257)])
 def test_block_kernel_rank_slice_in_halo(B, kernel, r0, r1, h0, h1):
@@ -422,6 +486,9 @@ def test_block_kernel_rank_slice_in_halo(B, kernel, r0, r1, h0, h1):
                                                            kernel=kernel, a_row0=r0, b_row0=h0)
     G = from_dev(n, rp, ci, va)
     Cr = rows(Ct, r0, r1)
+    if kernel == 13:
+        assert_products_close(G, Cr, T, T, 2.0, row_slice=(r0, r1))
+        return
     assert np.array_equal(G.rowptr, Cr.rowptr) and np.array_equal(G.col, Cr.col)
     assert np.array_equal(G.val, Cr.val)
 
@@ -453,3 +520,19 @@ def test_aggregate_order_with_reorder(B):
     Eg, st = run_gpu(B, H, reorder=1)
     Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS)
     assert_parity(Eg, st, Eo, tr)
+
+
+@pytest.mark.parametrize("g", [16])
+def test_wide_3d_rows_on_tensor_core_kernel(B, g):
+    """Config 4's law (3D 7-point heat, c ~ U(0.8, 1.2)) at 16^3: the squarings' block rows
+    hold more blocks of A than the exact kernel's shared-memory row (K3b hands them to the
+    paged kernel), while the tensor-core kernel takes every row (no fallback rows) and the
+    result meets parity against the oracle (BASELINE config 4)."""
+    H = make_config(4, scale_down=g)
+    Eg, st, Eo, tr = run_both(B, H)
+    assert_plan_equal(st, tr)
+    assert_parity(Eg, st, Eo, tr)
+    N = st["N"]
+    assert N >= 1 and all(st["sq_fallback_rows"][1:N + 1] == 0)
+    _, s11 = run_gpu(B, H, kernel=11)
+    assert s11["sq_fallback_rows"][1:N + 1].sum() > 0  # K3b cannot hold these rows

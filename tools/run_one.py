@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--eps-tol", type=float, default=1e-16)
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--kernel", type=int, default=0)
+    ap.add_argument("--exact", type=int, default=0)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -26,7 +27,8 @@ def main():
     dev = torch.device("cuda", 0)
     rp, ci, va = (torch.from_numpy(x).to(dev) for x in (H.rowptr, H.col, H.val))
     for rep in range(args.repeat):
-        p = B.Plan(H.n, rp, ci, va, args.eps_tol, plan_norm=args.plan_norm, kernel=args.kernel)
+        p = B.Plan(H.n, rp, ci, va, args.eps_tol, plan_norm=args.plan_norm, kernel=args.kernel,
+                   exact_products=args.exact)
         p.run_only()
         st = p.stats()
         p.close()
@@ -39,13 +41,9 @@ def main():
             f"{[int(x) for x in st['sq_fallback_rows'][1:N + 1]]} cache hits/misses/releases "
             f"{st['cache_hits']}/{st['cache_misses']}/{st['cache_releases']} cached "
             f"{st['cache_bytes_cached'] / 1e9:.1f} GB allocated {st['cache_bytes_allocated'] / 1e9:.1f} GB\n")
-        for i in range(1, N + 1):
-            g = st["sq_group_prof"][i]
-            if g[3] > 0:
-                sys.stderr.write(f"  sq{i} group: setup {g[0] / g[3]:.0f} products {g[1] / g[3]:.0f} "
-                                 f"flush {g[2] / g[3]:.0f} clk/group, groups {g[3]:.0f}, "
-                                 f"union k/group {g[4] / g[3]:.1f}, failed {g[5]:.0f} (union {g[6]:.0f}, slots {g[7]:.0f}); "
-                                 f"per k: wait {g[8] / g[4]:.0f} A {g[9] / g[4]:.0f} B {g[10] / g[4]:.0f} bar {g[11] / g[4]:.0f}\n")
+        sys.stderr.write(f"  sq_kernel_ms {[round(float(x), 1) for x in st['sq_kernel_ms'][1:N + 1]]} "
+                         f"block products {[float(x) for x in st['sq_block_products'][1:N + 1]]} "
+                         f"fmas {[float(x) for x in st['sq_fmas'][1:N + 1]]}\n")
     M, N = int(st["M"]), int(st["N"])
     out = {k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in st.items()}
     for k, v in list(out.items()):
