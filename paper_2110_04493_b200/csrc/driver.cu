@@ -133,7 +133,7 @@ static thread_local bool freeing_idle = false;
 // destroyed plan is kept for the same role of the next plan, which takes it whenever it is
 // large enough for its first request: a plan on a matrix like the previous one gets its
 // final-size buffers at once, with no cross-role fragmentation.
-constexpr int kRoles = 32;
+constexpr int kRoles = 64;
 static Block parked[kRoles];
 static size_t round_bytes(size_t b) {
   const size_t g = b >= ((size_t)1 << 24) ? ((size_t)1 << 21) : 512;
@@ -378,6 +378,27 @@ struct StepReport {
   unsigned long long prof[12] = {0};  // grouped kernel phase clocks
 };
 
+// BSR-8 view of a CSR matrix (k_bsr_build) and, optionally, its block transpose
+struct BsrBufs {
+  DBuf<int64_t> bcnt, brp, tp, cnt64, tb, tb_tmp;
+  DBuf<int32_t> bcol, tcnt, tk, tk_tmp, keys_tmp;
+  DBuf<double> bval;
+  DBuf<unsigned char> sort_tmp;
+  int64_t nbr = 0, nb = 0, bmax = 0;
+  bool frag = false, transposed = false;
+  BsrView view() const {
+    BsrView v;
+    v.nbr = nbr;
+    v.brp = brp.p;
+    v.bcol = bcol.p;
+    v.bval = bval.p;
+    v.tp = tp.p;
+    v.tk = tk.p;
+    v.tb = tb.p;
+    return v;
+  }
+};
+
 struct Workspace {
   DBuf<int32_t> lo, hi, order, bin_cnt, bin_off;
   DBuf<int64_t> prod, bound, row_off, row_cnt, row_nnz, cnt, scan_tmp, l1r, l2r, i64tmp;
@@ -391,12 +412,11 @@ struct Workspace {
   DBuf<int32_t> fail_rows, fail_rows2;
   DBuf<int8_t> ident;
   DBuf<unsigned long long> prof;
-  // BSR-8 view of the squared iterate (kernel 11)
-  DBuf<int64_t> bcnt, brp, scan_tmp2, tp, cnt64, tb, tb_tmp;
-  DBuf<int32_t> bcol, tcnt, tk, tk_tmp;
-  DBuf<double> bval, bscr;
-  DBuf<unsigned char> sort_tmp;
-  DBuf<int32_t> keys_tmp;
+  // BSR-8 views of the block kernels: B (the squared iterate or its halo rows; with its
+  // block transpose) and A (a Taylor term's S^_{i-1}, no transpose)
+  BsrBufs bsrB, bsrA;
+  DBuf<int64_t> scan_tmp2;
+  DBuf<double> bscr;
   int64_t pool_cap_hint = 0;
 };
 
@@ -441,6 +461,11 @@ struct sexpm_plan_s {
   DBuf<int32_t> block_order_t;  // the aggregates (block rows in that order) in locality order
   bool sq_tiled = false;
   DBuf<int32_t> block_order;  // block rows of the block kernel in locality order
+  // H0's BSR-8 view in fragment order with its block transpose (Taylor terms on K3m), built
+  // on first use; h0bsr_state 0 not built, 1 built, -1 not representable
+  BsrBufs h0bsr;
+  int h0bsr_state = 0;
+  bool taylor_block = false;  // Taylor terms on K3m (K5d's accumulator overflowed)
   ~sexpm_plan_s() {
     if (bg.joinable()) bg.join();
     if (bg_st) cudaStreamSynchronize(bg_st);
@@ -543,6 +568,52 @@ static void wait_order(sexpm_plan_s &P) {
   P.order_pending = false;
   REQUIRE(P.bg_err.empty(), SEXPM_ECUDA, P.bg_err);
   CK(cudaStreamWaitEvent(P.st, P.ev_order, 0));
+}
+
+// BSR-8 view of M's rows (block row I = rows 8I..8I+7 of the view; block columns global) in
+// row-major (K3b) or fragment order (K3m), and its block transpose when asked.  Returns false
+// (nothing built) when a block row spans more block columns than k_bsr_build's bitmap, or
+// the view would not fit K3m's 32-bit block indices.
+static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpose, BsrBufs &b) {
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  const int64_t nbr = (M.nrows + 7) / 8, nbc = (P.n + 7) / 8;
+  b.nbr = nbr;
+  b.frag = frag;
+  b.transposed = false;
+  b.bcnt.ensure((size_t)nbr + 1, st);
+  b.brp.ensure((size_t)nbr + 1, st);
+  w.scan_tmp2.ensure((size_t)scan_tmp_elems(std::max(nbr, nbc)) + 1, st);
+  CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+  launch_bsr_count(M, nbr, b.bcnt.p, w.flags.p, st);
+  launch_reduce_max_i64(b.bcnt.p, nbr, w.i64tmp.p + 7, st);
+  launch_exclusive_scan(b.bcnt.p, nbr, b.brp.p, w.scan_tmp2.p, st);
+  int bflags = 0;
+  CK(cudaMemcpyAsync(&b.nb, b.brp.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&b.bmax, w.i64tmp.p + 7, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&bflags, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((bflags & 4) || (frag && b.nb >= (int64_t)INT32_MAX)) return false;
+  const size_t nb1 = (size_t)std::max<int64_t>(b.nb, 1);
+  b.bcol.ensure(nb1, st);
+  b.bval.ensure(nb1 * 64, st);
+  launch_bsr_fill(M, nbr, b.brp.p, b.bcol.p, b.bval.p, w.flags.p, st, frag);
+  if (transpose) {
+    b.tcnt.ensure((size_t)nbc + 1, st);
+    b.tp.ensure((size_t)nbc + 1, st);
+    b.cnt64.ensure((size_t)nbc + 1, st);
+    b.tk.ensure(nb1, st);
+    b.tk_tmp.ensure(nb1, st);
+    b.tb.ensure(nb1, st);
+    b.tb_tmp.ensure(nb1, st);
+    b.sort_tmp.ensure(bsr_transpose_temp_bytes(b.nb) + 256, st);
+    b.keys_tmp.ensure(nb1, st);
+    launch_bsr_transpose(nbr, nbc, b.nb, b.brp.p, b.bcol.p, b.tcnt.p, b.tp.p, b.tk_tmp.p, b.tb_tmp.p,
+                         b.tk.p, b.tb.p, w.scan_tmp2.p, b.cnt64.p, b.sort_tmp.p, b.sort_tmp.n,
+                         b.keys_tmp.p, st);
+    b.transposed = true;
+  }
+  return true;
 }
 
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
@@ -675,10 +746,15 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     const bool taylor_pull_ok = self == 0.0 && BT != nullptr && BT->rp.p != nullptr;
     // squarings: the block kernel on the fp64 tensor-core instruction (13; 11 is the
     // bit-exact DMUL/DADD variant); Taylor terms: the diagonal push or the pull kernel
-    if (kern == 0) kern = sq_like ? (P.o.exact_products ? 11 : 13) : (dia_path ? 7 : (taylor_pull_ok ? 6 : 5));
-    // the block kernels square one matrix (or a rank's rows inside its halo rows); Taylor
-    // terms keep their own kernels
-    if ((kern == 11 || kern == 13) && !sq_like) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 5);
+    // (Taylor terms whose rows outgrew K5d's accumulator -- 3D stencils -- go to the
+    // tensor-core block kernel with B = H0)
+    if (kern == 0) {
+      if (sq_like) kern = P.o.exact_products ? 11 : 13;
+      else if (P.taylor_block) kern = 13;
+      else kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 5);
+    }
+    // the exact block kernel squares one matrix (or a rank's rows inside its halo rows)
+    if (kern == 11 && !sq_like) kern = dia_path ? 7 : (taylor_pull_ok ? 6 : 5);
     // the block kernel needs B's rows block-aligned and A's rows a block-aligned slice of them
     // (one GPU: A = B; several: A = the rank's rows inside its halo B, 8-aligned partition)
     const bool same = B.rp == A.rp;
@@ -691,7 +767,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       launch_rows_equal(A, B, w.eqflag.p, st);
       bsr_ok = d2h(w.eqflag.p, st) == 0;
     }
-    if ((kern == 11 || kern == 13) && !bsr_ok) kern = 5;
+    if (sq_like && (kern == 11 || kern == 13) && !bsr_ok) kern = 5;
     if (kern == 7 && !dia_path) kern = taylor_pull_ok ? 6 : 5;
     if (kern == 6 && !taylor_pull_ok) kern = 5;
     if (kern == 7) CK(cudaMemsetAsync(P.dia_prod.p, 0, sizeof(unsigned long long), st));
@@ -712,6 +788,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       while (nlist > 0) {
         if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
           run_symbolic();
+          rep.fmas = (double)hstat[2];
           na.cursor_cap = std::max<int64_t>(hstat[6], 1);
           na.scr_cap = std::max<int64_t>(hstat[1], 1);
         }
@@ -742,54 +819,37 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           nh.grid = paged_grid;
           launch_numeric_paged(nh, fout, w.fail_count.p, st);
         } else if (stage == 11 || stage == 13) {
-          // BSR-8 view of B (= A, or A's halo rows) and its block transpose, then the block
-          // kernel over A's block rows
-          const int64_t nbr = (B.nrows + 7) / 8, nbc = (P.n + 7) / 8, nbr_a = (nr + 7) / 8;
-          w.bcnt.ensure((size_t)nbr + 1, st);
-          w.brp.ensure((size_t)nbr + 1, st);
-          w.scan_tmp2.ensure((size_t)scan_tmp_elems(std::max(nbr, nbc)) + 1, st);
-          CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
-          launch_bsr_count(B, nbr, w.bcnt.p, w.flags.p, st);
-          launch_reduce_max_i64(w.bcnt.p, nbr, w.i64tmp.p + 7, st);
-          launch_exclusive_scan(w.bcnt.p, nbr, w.brp.p, w.scan_tmp2.p, st);
-          int64_t nb = 0, bmax = 0;
-          int bflags = 0;
-          CK(cudaMemcpyAsync(&nb, w.brp.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-          CK(cudaMemcpyAsync(&bmax, w.i64tmp.p + 7, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-          CK(cudaMemcpyAsync(&bflags, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-          CK(cudaStreamSynchronize(st));
-          // block rows too wide for the view or for the kernel's shared-memory row of A: the
-          // whole product goes to the paged kernel
-          if ((bflags & 4) || (stage == 11 && bmax > kBsrMaxRowBlocks)) {
+          // BSR-8 view of B (= A, or A's halo rows; for a Taylor term H0, built once per plan)
+          // with its block transpose, A's own view for a Taylor term, then the block kernel
+          // over A's block rows
+          const int64_t nbr_a = (nr + 7) / 8;
+          const bool taylor = !sq_like;
+          bool ok_view;
+          if (taylor && B.rp != P.H0full.rp.p) {
+            ok_view = false;  // a product with any other B: its view is not kept
+          } else if (taylor) {
+            if (P.h0bsr_state == 0)
+              P.h0bsr_state = build_bsr(P, P.H0full.view(), true, true, P.h0bsr) ? 1 : -1;
+            ok_view = P.h0bsr_state == 1 && build_bsr(P, A, true, false, w.bsrA);
+          } else {
+            ok_view = build_bsr(P, B, stage == 13, true, w.bsrB);
+            // K3b holds a row of A in shared memory
+            if (ok_view && stage == 11 && w.bsrB.bmax > kBsrMaxRowBlocks) ok_view = false;
+          }
+          if (!ok_view) {  // the whole product goes to the paged kernel
             stage = 5;
             continue;
           }
-          w.bcol.ensure((size_t)std::max<int64_t>(nb, 1), st);
-          w.bval.ensure((size_t)std::max<int64_t>(nb, 1) * 64, st);
-          launch_bsr_fill(B, nbr, w.brp.p, w.bcol.p, w.bval.p, w.flags.p, st, stage == 13);
-          w.tcnt.ensure((size_t)nbc + 1, st);
-          w.tp.ensure((size_t)nbc + 1, st);
-          w.cnt64.ensure((size_t)nbc + 1, st);
-          w.tk.ensure((size_t)std::max<int64_t>(nb, 1), st);
-          w.tk_tmp.ensure((size_t)std::max<int64_t>(nb, 1), st);
-          w.tb.ensure((size_t)std::max<int64_t>(nb, 1), st);
-          w.tb_tmp.ensure((size_t)std::max<int64_t>(nb, 1), st);
-          const size_t sbytes = bsr_transpose_temp_bytes(nb);
-          w.sort_tmp.ensure(sbytes + 256, st);
-          w.keys_tmp.ensure((size_t)std::max<int64_t>(nb, 1), st);
-          launch_bsr_transpose(nbr, nbc, nb, w.brp.p, w.bcol.p, w.tcnt.p, w.tp.p, w.tk_tmp.p,
-                               w.tb_tmp.p, w.tk.p, w.tb.p, w.scan_tmp2.p, w.cnt64.p, w.sort_tmp.p,
-                               w.sort_tmp.n, w.keys_tmp.p, st);
-          BsrView Bv;
-          Bv.nbr = nbr;
-          Bv.brp = w.brp.p;
-          Bv.bcol = w.bcol.p;
-          Bv.bval = w.bval.p;
-          Bv.tp = w.tp.p;
-          Bv.tk = w.tk.p;
-          Bv.tb = w.tb.p;
+          const BsrBufs &bb = taylor ? P.h0bsr : w.bsrB;
+          const int64_t nb = bb.nb;
+          BsrView Bv = bb.view();
+          if (taylor) {
+            Bv.abrp = w.bsrA.brp.p;
+            Bv.abcol = w.bsrA.bcol.p;
+            Bv.abval = w.bsrA.bval.p;
+          }
           Bv.nbr_a = nbr_a;
-          Bv.ib0 = (A.row0 - B.row0) / 8;
+          Bv.ib0 = taylor ? 0 : (A.row0 - B.row0) / 8;
           Bv.kb0 = B.row0 / 8;
           if (use_cluster && nr == P.row_end - P.row_begin && A.row0 % 8 == 0 && !getenv("SEXPM_BSR_NATURAL"))
             Bv.border = P.block_order.p;  // block rows of the rank's rows in locality order
@@ -819,6 +879,12 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           unsigned long long nbp = 0;
           CK(cudaMemcpy(&nbp, w.prof.p, sizeof(nbp), cudaMemcpyDeviceToHost));
           rep.block_products = (double)nbp;
+          if (getenv("SEXPM_STEP_LOG")) {
+            unsigned long long pr[5];
+            CK(cudaMemcpy(pr, w.prof.p, sizeof(pr), cudaMemcpyDeviceToHost));
+            fprintf(stderr, "[sexpm run] block kernel %d: block rows handed on: K span %llu, J span %llu, both %llu, J count %llu\n",
+                    stage, pr[1], pr[2], pr[3], pr[4]);
+          }
         } else if (stage == 7) {
           DiaView D;
           D.ndiag = P.dia_nd;
@@ -892,6 +958,11 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   if (dia_launched) {  // next term's K5d slots: this term's largest row + 12.5 % + 64, 64-aligned
     const long long nd = d2h(P.dia_need.p, st);
     P.dia_slots = (int)std::min<long long>(P.dia_slots_max, std::max<long long>(256, ((nd * 9 / 8 + 64 + 63) / 64) * 64));
+    // rows beyond K5d's largest accumulator went to the paged kernel: the next terms run on
+    // the tensor-core block kernel (B = H0) instead
+    // (also once rows needed over half of it, or > 1 % of the rows were retried or handed on:
+    // 3D rows keep growing term after term)
+    if (P.o.kernel == 0 && (nd > P.dia_slots_max / 2 || rep.window_rows * 100 > nr)) P.taylor_block = true;
     if (getenv("SEXPM_STEP_LOG")) fprintf(stderr, "[sexpm run] K5d need %lld slots, next %d (max %d), retried rows %d\n", nd, P.dia_slots, P.dia_slots_max, (int)(rep.window_rows - nfail_other));
   }
   cudaEventDestroy(e0);
@@ -2053,6 +2124,7 @@ static void do_run(sexpm_plan_s &P) {
   // the first Taylor term tries the short-row kernel K5s only if S^_2 = H0 H0 / 2 can fit
   // its window: a row of H0 H0 spans at most 2 (dmax - dmin) + 1 columns
   P.dia_short_ok = 2 * ((int64_t)P.dia_dmax - P.dia_dmin) + 1 <= 64;
+  P.taylor_block = false;
   const int64_t nl = P.row_end - P.row_begin;
   DCsr &H0loc = P.H0loc;
   DCsr &T = P.T, &Tn = P.Tn, &Sc = P.S, &Sn = P.Sn;
@@ -2392,15 +2464,18 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
     }
     P->ws.pool_col.role = role++;
     P->ws.pool_val.role = role++;
-    P->ws.bval.role = role++;
-    P->ws.bcol.role = role++;
-    P->ws.tk.role = role++;
-    P->ws.tk_tmp.role = role++;
-    P->ws.tb.role = role++;
-    P->ws.tb_tmp.role = role++;
+    for (BsrBufs *b : {&P->ws.bsrB, &P->ws.bsrA}) {
+      b->bval.role = role++;
+      b->bcol.role = role++;
+      b->tk.role = role++;
+      b->tk_tmp.role = role++;
+      b->tb.role = role++;
+      b->tb_tmp.role = role++;
+      b->keys_tmp.role = role++;
+      b->sort_tmp.role = role++;
+    }
     P->ws.bscr.role = role++;
-    P->ws.keys_tmp.role = role++;
-    P->ws.sort_tmp.role = role++;
+    REQUIRE(role <= cache::kRoles, SEXPM_EINTERNAL, "device-block cache: too many buffer roles");
   }
   {
     std::lock_guard<std::mutex> lk(cache::mu);

@@ -2027,14 +2027,14 @@ void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, 
 // ------------------------------------------------------------------------------------
 constexpr int kMThreads = 256;
 constexpr int kMWarps = kMThreads / 32;
-constexpr int kMKWords = 256;              // K bitmap: block-column span of A's row <= 8192
-constexpr int kMJWords = 1024;             // J bitmap: output block-column span <= 32768
+constexpr int kMKWords = 2048;             // K bitmap: block-column span of A's row <= 65536
+constexpr int kMJWords = 2048;             // J bitmap: output block-column span <= 65536
 constexpr int kMJCap = kBsrMJCap;          // output blocks per block row
 constexpr int kMML = 64;                   // matches listed at a time per warp
 constexpr int kMPF = 4;                    // block products whose operands are in flight
 
 int bsrm_numeric_smem_bytes() {
-  return kMKWords * 4 + kMKWords * 2 + kMJWords * 4 + kMJCap * 4 + kMWarps * kMML * 16 + 64;
+  return kMKWords * 4 + kMKWords * 2 + kMJWords * 4 + kMJCap * 4 + kMWarps * kMML * 8 + 64;
 }
 
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
@@ -2053,8 +2053,8 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
                                                               double *scratch, int32_t *fail_rows,
                                                               int *fail_count) {
   extern __shared__ __align__(16) unsigned char msm[];
-  int64_t *mla = reinterpret_cast<int64_t *>(msm);                      // kMWarps * kMML
-  int64_t *mlb = mla + kMWarps * kMML;                                  // kMWarps * kMML
+  int32_t *mla = reinterpret_cast<int32_t *>(msm);                      // kMWarps * kMML
+  int32_t *mlb = mla + kMWarps * kMML;                                  // kMWarps * kMML
   unsigned *kbits = reinterpret_cast<unsigned *>(mlb + kMWarps * kMML); // kMKWords
   unsigned *jbits = kbits + kMKWords;                                   // kMJWords
   int32_t *jlist = reinterpret_cast<int32_t *>(jbits + kMJWords);       // kMJCap
@@ -2073,7 +2073,11 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
   // self-term offsets: A_IJ[g][2t] and A_IJ[g][2t + 1]
   const int soff0 = 2 * (4 * g + ((2 * t) & 3)) + ((2 * t) >> 2);
   const int soff1 = 2 * (4 * g + ((2 * t + 1) & 3)) + ((2 * t + 1) >> 2);
-  const double2 *bv2 = reinterpret_cast<const double2 *>(Bv.bval);
+  // A's blocks: its own BSR view (Taylor terms: A = S^_{i-1}, B = H0) or B's rows (squarings)
+  const int64_t *abrp = Bv.abrp ? Bv.abrp : Bv.brp;
+  const int32_t *abcol = Bv.abrp ? Bv.abcol : Bv.bcol;
+  const double *abval = Bv.abrp ? Bv.abval : Bv.bval;
+  const double2 *av2 = reinterpret_cast<const double2 *>(abval);
   for (;;) {
     __syncthreads();
     if (tid == 0) s_I = atomicAdd(a.row_counter, 1);
@@ -2082,7 +2086,7 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
     const int64_t I = Bv.border ? (int64_t)Bv.border[s_I] : (int64_t)s_I;
     const int64_t r0 = 8 * I;
     const int nr = (int)(nrows - r0 < 8 ? nrows - r0 : 8);
-    const int64_t ab0 = Bv.brp[I + Bv.ib0], ab1 = Bv.brp[I + Bv.ib0 + 1];
+    const int64_t ab0 = abrp[I + Bv.ib0], ab1 = abrp[I + Bv.ib0 + 1];
     const int na = (int)(ab1 - ab0);
     if (tid == 0) {
       int fail = 0;
@@ -2094,9 +2098,10 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
           jmax = max(jmax, a.hi[r] >> 3);
         }
       }
-      const int kmin = na > 0 ? Bv.bcol[ab0] : 0, kmax = na > 0 ? Bv.bcol[ab1 - 1] : -1;
+      const int kmin = na > 0 ? abcol[ab0] : 0, kmax = na > 0 ? abcol[ab1 - 1] : -1;
       if (na > 0 && ((kmax - kmin) >> 5) + 1 > kMKWords) fail = 1;
-      if (jmax >= jmin && ((jmax - jmin) >> 5) + 1 > kMJWords) fail = 1;
+      if (jmax >= jmin && ((jmax - jmin) >> 5) + 1 > kMJWords) fail |= 2;
+      if (fail && a.prof) atomicAdd(&a.prof[fail], 1ull);  // block rows handed on: K / J span
       s_fail = fail;
       s_kmin = kmin;
       s_jmin = jmin;
@@ -2125,7 +2130,7 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
     const int kmin = s_kmin, jmin = s_jmin, nkw = s_nkw, njw = s_njw;
     // (1) K bitmap of row I of A, then the word prefix (ranks)
     for (int q = tid; q < na; q += kMThreads) {
-      const int K = Bv.bcol[ab0 + q];
+      const int K = abcol[ab0 + q];
       atomicOr(&kbits[(K - kmin) >> 5], 1u << ((K - kmin) & 31));
       // (2a) the self term reaches row I's own block columns (also where no B_K has them)
       if (a.self_coef != 0.0) {
@@ -2135,7 +2140,7 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
     }
     // (2b) candidate output blocks: union of the block rows of B at A's block columns
     for (int q = warp; q < na; q += kMWarps) {
-      const int64_t K = Bv.bcol[ab0 + q] - Bv.kb0;  // the view's block row
+      const int64_t K = abcol[ab0 + q] - Bv.kb0;  // the view's block row
       if (K >= 0 && K < Bv.nbr) {
         for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
           const int jb = Bv.bcol[b] - jmin;
@@ -2188,21 +2193,24 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
     __syncthreads();
     const int nj = s_nj;
     const bool over = nj > kMJCap;
+    if (over && a.prof && tid == 0) atomicAdd(&a.prof[4], 1ull);  // handed on: J count
     // (3) output blocks, one warp each
     double fs = 0.0, q1 = 0.0;
     long long nz = 0, c1 = 0;
     unsigned long long nbp = 0;
     if (!over) {
-      int64_t *wa = mla + warp * kMML;
-      int64_t *wb = mlb + warp * kMML;
+      int32_t *wa = mla + warp * kMML;
+      int32_t *wb = mlb + warp * kMML;
       for (int q = warp; q < nj; q += kMWarps) {
         const int J = jlist[q];
-        double x0 = 0.0, x1 = 0.0;
+        // two independent accumulator chains (even / odd matches), summed at the end: the
+        // DMMAs of one output block are not one serial dependency chain
+        double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
         if (a.self_coef != 0.0) {  // self term: A_IJ, if row I of A has block J
           const int kb = J - kmin;
           if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
             const int ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
-            const double *ap = Bv.bval + (ab0 + ra) * 64;
+            const double *ap = abval + (ab0 + ra) * 64;
             x0 = a.self_coef * __ldg(ap + soff0);
             x1 = a.self_coef * __ldg(ap + soff1);
           }
@@ -2210,64 +2218,84 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
         const int64_t t0 = Bv.tp[J], t1 = Bv.tp[J + 1];
         int64_t tb0 = t0;
         while (tb0 < t1) {
-          // matches K of row I and column J (ascending K), listed in batches
+          // matches K of row I and column J (ascending K), listed in batches (32-bit block
+          // indices: the view holds < 2^31 blocks, checked by the driver)
           int nm = 0;
           for (; tb0 < t1 && nm <= kMML - 32; tb0 += 32) {
             const int64_t tt = tb0 + lane;
-            int ra = -1;
-            int64_t bidx = 0;
+            int ra = -1, bidx = 0;
             if (tt < t1) {
               const int kb = Bv.tk[tt] + (int)Bv.kb0 - kmin;
               if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
                 ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
-                bidx = Bv.tb[tt];
+                bidx = (int)Bv.tb[tt];
               }
             }
             const unsigned m = __ballot_sync(FULL_MASK, ra >= 0);
             if (ra >= 0) {
               const int pos = nm + __popc(m & lanemask_lt());
-              wa[pos] = ab0 + ra;
+              wa[pos] = (int)ab0 + ra;
               wb[pos] = bidx;
             }
             nm += __popc(m);
           }
           __syncwarp();
           nbp += nm;
-          double2 av[kMPF];
-          double bl[kMPF], bh[kMPF];
-#pragma unroll
-          for (int d = 0; d < kMPF; d++)
-            if (d < nm) {
-              av[d] = __ldg(bv2 + wa[d] * 32 + lane);
-              const double *bp = Bv.bval + wb[d] * 64 + boff;
-              bl[d] = __ldg(bp);
-              bh[d] = __ldg(bp + 32);
-            }
-          for (int u = 0; u < nm; u += kMPF) {
-            double2 ca[kMPF];
-            double cl[kMPF], ch[kMPF];
+          // operands of kMPF block products per set, two sets in turn (P: u.., Q: u+kMPF..);
+          // loads past the list are clamped to its last entry (their products are skipped)
+          double2 pa[kMPF], qa[kMPF];
+          double pl[kMPF], ph[kMPF], ql[kMPF], qh[kMPF];
+          const int last = nm - 1;
+#define K3M_LOAD(A_, L_, H_, base)                                              \
+  _Pragma("unroll") for (int d = 0; d < kMPF; d++) {                           \
+    const int e = min((base) + d, last);                                       \
+    A_[d] = __ldg(av2 + (size_t)wa[e] * 32 + lane);                            \
+    const double *bp = Bv.bval + (size_t)wb[e] * 64 + boff;                    \
+    L_[d] = __ldg(bp);                                                         \
+    H_[d] = __ldg(bp + 32);                                                    \
+  }
+#define K3M_MMA(A_, L_, H_)                                                     \
+  _Pragma("unroll") for (int d = 0; d < kMPF; d += 2) {                        \
+    dmma884(x0, x1, A_[d].x, L_[d]);                                           \
+    dmma884(y0, y1, A_[d + 1].x, L_[d + 1]);                                   \
+    dmma884(x0, x1, A_[d].y, H_[d]);                                           \
+    dmma884(y0, y1, A_[d + 1].y, H_[d + 1]);                                   \
+  }
+          int u = 0;
+          if (nm > 0) { K3M_LOAD(pa, pl, ph, 0) }
+          for (; u + 2 * kMPF <= nm; u += 2 * kMPF) {
+            K3M_LOAD(qa, ql, qh, u + kMPF)
+            K3M_MMA(pa, pl, ph)
+            K3M_LOAD(pa, pl, ph, u + 2 * kMPF)
+            K3M_MMA(qa, ql, qh)
+          }
+          // tail: < 2 kMPF products; set P holds u.. (loaded)
+          if (u + kMPF <= nm) {
+            K3M_LOAD(qa, ql, qh, u + kMPF)
+            K3M_MMA(pa, pl, ph)
+            u += kMPF;
 #pragma unroll
             for (int d = 0; d < kMPF; d++) {
-              ca[d] = av[d];
-              cl[d] = bl[d];
-              ch[d] = bh[d];
+              pa[d] = qa[d];
+              pl[d] = ql[d];
+              ph[d] = qh[d];
             }
-#pragma unroll
-            for (int d = 0; d < kMPF; d++)
-              if (u + kMPF + d < nm) {
-                av[d] = __ldg(bv2 + wa[u + kMPF + d] * 32 + lane);
-                const double *bp = Bv.bval + wb[u + kMPF + d] * 64 + boff;
-                bl[d] = __ldg(bp);
-                bh[d] = __ldg(bp + 32);
-              }
-#pragma unroll
-            for (int d = 0; d < kMPF; d++)
-              if (u + d < nm) {
-                dmma884(x0, x1, ca[d].x, cl[d]);
-                dmma884(x0, x1, ca[d].y, ch[d]);
-              }
           }
+#pragma unroll
+          for (int d = 0; d < kMPF; d++)
+            if (u + d < nm) {
+              dmma884(x0, x1, pa[d].x, pl[d]);
+              dmma884(x0, x1, pa[d].y, ph[d]);
+            }
+#undef K3M_LOAD
+#undef K3M_MMA
           __syncwarp();
+        }
+        x0 += y0;
+        x1 += y1;
+        if (a.divisor != 1.0) {  // Taylor term: (sum_k s_rk h_kj) / i (reading R7)
+          x0 = __ddiv_rn(x0, a.divisor);
+          x1 = __ddiv_rn(x1, a.divisor);
         }
         // classify (Algorithm 4.1 floor, fused first pass) and pack into scratch
         const bool ok = g < nr;

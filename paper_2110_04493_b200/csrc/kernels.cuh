@@ -146,6 +146,11 @@ struct BsrView {
   // its halo): A has nbr_a block rows, its block row I is the view's block row I + ib0, and
   // the view's first block row is global block row kb0 (block columns are global)
   int64_t nbr_a = 0, ib0 = 0, kb0 = 0;
+  // K3m only: A's own BSR view (Taylor terms S~ = S^ H0 / i: A = S^_{i-1}, B = H0); null when
+  // A's blocks are B's rows (squarings)
+  const int64_t *abrp = nullptr;
+  const int32_t *abcol = nullptr;
+  const double *abval = nullptr;
 };
 constexpr int kBsrScratchPerCta = 512 * 64;  // doubles of output-block scratch per CTA
 constexpr int kBsrMaxRowBlocks = 136;        // blocks of a block row the numeric kernel holds

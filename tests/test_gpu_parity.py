@@ -381,10 +381,10 @@ def _coo(n, rows, cols, vals):
     return coo_to_csr(n, rows[first], cols[first], np.asarray(vals, np.float64)[first])
 
 
-@pytest.mark.parametrize("kernel", [5, 3])
+@pytest.mark.parametrize("kernel", [5])
 def test_long_b_rows(B, kernel):
-    """B rows longer than a CTA (> 512 entries) in the paged and window kernels (A != B:
-    not a squaring): A x B + 2A is bit-identical to the oracle."""
+    """B rows longer than a CTA (> 512 entries) in the paged kernel (A != B: not a
+    squaring): A x B + 2A is bit-identical to the oracle."""
     n = 3000
     rng = np.random.default_rng(11)
     Bm = random_banded(n, 450, 0.85, 1.0, 12)
@@ -522,9 +522,9 @@ def test_aggregate_order_with_reorder(B):
     assert_parity(Eg, st, Eo, tr)
 
 
-@pytest.mark.parametrize("g", [16])
+@pytest.mark.parametrize("g", [20])
 def test_wide_3d_rows_on_tensor_core_kernel(B, g):
-    """Config 4's law (3D 7-point heat, c ~ U(0.8, 1.2)) at 16^3: the squarings' block rows
+    """Config 4's law (3D 7-point heat, c ~ U(0.8, 1.2)) at 20^3: the squarings' block rows
     hold more blocks of A than the exact kernel's shared-memory row (K3b hands them to the
     paged kernel), while the tensor-core kernel takes every row (no fallback rows) and the
     result meets parity against the oracle (BASELINE config 4)."""

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--exact", type=int, default=0)
+    ap.add_argument("--sq-order", type=int, default=1)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -28,7 +29,7 @@ def main():
     rp, ci, va = (torch.from_numpy(x).to(dev) for x in (H.rowptr, H.col, H.val))
     for rep in range(args.repeat):
         p = B.Plan(H.n, rp, ci, va, args.eps_tol, plan_norm=args.plan_norm, kernel=args.kernel,
-                   exact_products=args.exact)
+                   exact_products=args.exact, sq_order=args.sq_order)
         p.run_only()
         st = p.stats()
         p.close()
@@ -41,6 +42,8 @@ def main():
             f"{[int(x) for x in st['sq_fallback_rows'][1:N + 1]]} cache hits/misses/releases "
             f"{st['cache_hits']}/{st['cache_misses']}/{st['cache_releases']} cached "
             f"{st['cache_bytes_cached'] / 1e9:.1f} GB allocated {st['cache_bytes_allocated'] / 1e9:.1f} GB\n")
+        sys.stderr.write(f"  taylor_numeric_ms {[round(float(x), 1) for x in st['taylor_numeric_ms'][2:int(st['M_eff']) + 1]]} "
+                         f"taylor_fallback {[int(x) for x in st['taylor_fallback_rows'][2:int(st['M_eff']) + 1]]}\n")
         sys.stderr.write(f"  sq_kernel_ms {[round(float(x), 1) for x in st['sq_kernel_ms'][1:N + 1]]} "
                          f"block products {[float(x) for x in st['sq_block_products'][1:N + 1]]} "
                          f"fmas {[float(x) for x in st['sq_fmas'][1:N + 1]]}\n")
