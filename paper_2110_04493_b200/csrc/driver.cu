@@ -1342,6 +1342,53 @@ static void aggregate_order(const std::vector<int64_t> &rp, const std::vector<in
   }
 }
 
+// Compact aggregates: from each unused seed (index order) add, one at a time, the unused
+// neighbour of the aggregate with the most edges into it; ties go to the candidate adjacent
+// to the earliest-added member, then to the smaller index.  On a 3D grid this builds
+// 2 x 2 x 2 cubes (on a 2D grid 4 x 2 rectangles): the iterates' rows are balls of the
+// grid graph, and blocks of compact aggregates fill them with fewer partial blocks than
+// the star-shaped BFS aggregates or index-order line segments.
+static void aggregate_order_compact(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
+                                    int64_t n, int size, std::vector<int64_t> &perm) {
+  perm.clear();
+  perm.reserve((size_t)n);
+  std::vector<uint8_t> used((size_t)n, 0);
+  std::vector<int32_t> cnt((size_t)n, 0), firstm((size_t)n, 0);  // per candidate: edges, first member
+  std::vector<int64_t> agg, cand;
+  for (int64_t s = 0; s < n; s++) {
+    if (used[s]) continue;
+    agg.clear();
+    cand.clear();
+    int64_t v = s;
+    for (;;) {
+      used[v] = 1;
+      const int m = (int)agg.size();
+      agg.push_back(v);
+      if ((int)agg.size() >= size) break;
+      for (int64_t p = rp[v]; p < rp[v + 1]; p++) {  // v's edges raise its neighbours' counts
+        const int64_t u = col[p];
+        if (used[u]) continue;
+        if (cnt[u] == 0) {
+          firstm[u] = m;
+          cand.push_back(u);
+        }
+        cnt[u]++;
+      }
+      int64_t best = -1;
+      for (int64_t u : cand) {
+        if (used[u]) continue;
+        if (best < 0 || cnt[u] > cnt[best] ||
+            (cnt[u] == cnt[best] && (firstm[u] < firstm[best] || (firstm[u] == firstm[best] && u < best))))
+          best = u;
+      }
+      if (best < 0) break;
+      v = best;
+    }
+    for (int64_t u : cand) cnt[u] = 0;
+    perm.insert(perm.end(), agg.begin(), agg.end());
+  }
+}
+
 static void cluster_order(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
                           int64_t r0, int64_t r1, int cluster, std::vector<int32_t> &order) {
   const int64_t nl = r1 - r0;
@@ -1992,55 +2039,62 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
         if (!ord.empty())
           CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1) {  // aggregate order of the squarings
-          aggregate_order(hrp, hcol, P.n, 8, P.h_tperm);
-          std::vector<int64_t> hinv((size_t)P.n);
-          for (int64_t i = 0; i < P.n; i++) hinv[P.h_tperm[i]] = i;
-          // keep it only where it fills the 8x8 blocks better: for a sample of block rows,
-          // count the distinct column blocks covered by the radius-3 neighbourhood of their
-          // 8 rows (the iterates' patterns are such neighbourhoods) in both orders
-          {
-            const int64_t nbt = (P.n + 7) / 8, step = std::max<int64_t>(1, nbt / 512);
-            std::vector<int32_t> mark((size_t)P.n, -1), fr, nx;
-            std::vector<int64_t> blk;
-            auto proxy = [&](bool agg) {
-              int64_t total = 0;
-              int32_t stamp = 0;
-              std::fill(mark.begin(), mark.end(), -1);
-              for (int64_t g = 0; g < nbt; g += step, stamp++) {
-                fr.clear();
-                for (int64_t i = 8 * g; i < std::min<int64_t>(P.n, 8 * g + 8); i++) {
-                  const int32_t v = (int32_t)(agg ? P.h_tperm[i] : i);
-                  if (mark[v] != stamp) {
-                    mark[v] = stamp;
-                    fr.push_back(v);
-                  }
+          // candidates: BFS aggregates and compact aggregates; kept only where it fills the
+          // 8x8 blocks better than index order: for a sample of block rows, count the distinct
+          // column blocks covered by the radius-r neighbourhood of their 8 rows (the iterates'
+          // rows are such neighbourhoods; r ~ 0.8 M, the reach of the filtered Taylor phase)
+          std::vector<int64_t> cand[2];
+          aggregate_order(hrp, hcol, P.n, 8, cand[0]);
+          aggregate_order_compact(hrp, hcol, P.n, 8, cand[1]);
+          const int rad = std::max(3, std::min(16, (int)lround(0.8 * P.M)));
+          const int64_t nbt = (P.n + 7) / 8, step = std::max<int64_t>(1, nbt / 512);
+          std::vector<int32_t> mark((size_t)P.n, -1), fr, nx;
+          std::vector<int64_t> blk, hinv((size_t)P.n);
+          auto proxy = [&](const std::vector<int64_t> *perm) {
+            if (perm)
+              for (int64_t i = 0; i < P.n; i++) hinv[(*perm)[i]] = i;
+            int64_t total = 0;
+            int32_t stamp = 0;
+            std::fill(mark.begin(), mark.end(), -1);
+            for (int64_t g = 0; g < nbt; g += step, stamp++) {
+              fr.clear();
+              for (int64_t i = 8 * g; i < std::min<int64_t>(P.n, 8 * g + 8); i++) {
+                const int32_t v = (int32_t)(perm ? (*perm)[i] : i);
+                if (mark[v] != stamp) {
+                  mark[v] = stamp;
+                  fr.push_back(v);
                 }
-                blk.clear();
-                for (int32_t v : fr) blk.push_back((agg ? hinv[v] : v) >> 3);
-                for (int rad = 0; rad < 3; rad++) {
-                  nx.clear();
-                  for (int32_t v : fr)
-                    for (int64_t p = hrp[v]; p < hrp[v + 1]; p++) {
-                      const int32_t u = hcol[p];
-                      if (mark[u] != stamp) {
-                        mark[u] = stamp;
-                        nx.push_back(u);
-                        blk.push_back((agg ? hinv[u] : u) >> 3);
-                      }
-                    }
-                  fr.swap(nx);
-                }
-                std::sort(blk.begin(), blk.end());
-                total += std::unique(blk.begin(), blk.end()) - blk.begin();
               }
-              return total;
-            };
-            const int64_t b_idx = proxy(false), b_agg = proxy(true);
-            if (getenv("SEXPM_PLAN_LOG"))
-              fprintf(stderr, "[sexpm plan] aggregate order: sampled blocks %lld (index order %lld)%s\n",
-                      (long long)b_agg, (long long)b_idx, 10 * b_agg <= 9 * b_idx ? "" : " -> index order");
-            if (10 * b_agg > 9 * b_idx) P.h_tperm.clear();
-          }
+              blk.clear();
+              for (int32_t v : fr) blk.push_back((perm ? hinv[v] : v) >> 3);
+              for (int r = 0; r < rad; r++) {
+                nx.clear();
+                for (int32_t v : fr)
+                  for (int64_t p = hrp[v]; p < hrp[v + 1]; p++) {
+                    const int32_t u = hcol[p];
+                    if (mark[u] != stamp) {
+                      mark[u] = stamp;
+                      nx.push_back(u);
+                      blk.push_back((perm ? hinv[u] : u) >> 3);
+                    }
+                  }
+                fr.swap(nx);
+              }
+              std::sort(blk.begin(), blk.end());
+              total += std::unique(blk.begin(), blk.end()) - blk.begin();
+            }
+            return total;
+          };
+          const int64_t b_idx = proxy(nullptr), b_bfs = proxy(&cand[0]), b_cmp = proxy(&cand[1]);
+          const int pick = b_cmp < b_bfs ? 1 : 0;
+          const int64_t b_agg = pick ? b_cmp : b_bfs;
+          if (getenv("SEXPM_PLAN_LOG"))
+            fprintf(stderr, "[sexpm plan] aggregate order (radius %d): sampled blocks index %lld, BFS %lld, compact %lld -> %s\n",
+                    rad, (long long)b_idx, (long long)b_bfs, (long long)b_cmp,
+                    10 * b_agg <= 9 * b_idx ? (pick ? "compact" : "BFS") : "index order");
+          P.h_tperm.clear();
+          if (10 * b_agg <= 9 * b_idx) P.h_tperm.swap(cand[pick]);
+          for (int64_t i = 0; i < (int64_t)P.h_tperm.size(); i++) hinv[P.h_tperm[i]] = i;
           // block rows of the relabelled matrix in the locality order of H's clusters: each
           // aggregate ranked by the earliest position of its rows in `ord`
           if (!P.h_tperm.empty()) {
