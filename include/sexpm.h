@@ -123,7 +123,8 @@ typedef struct {
                              back; 0 = index order.  One GPU only; not with ssat.  Results
                              equal up to rounding order (north-star parity). */
   int32_t exact_products; /* 0 = (default) squarings on the fp64 tensor-core block kernel 13
-                             (fused multiply-adds: C~ within rounding of the oracle's);
+                             (fused multiply-adds: C~ within rounding of the oracle's), Taylor
+                             terms too once their rows outgrow the diagonal kernel;
                              1 = the bit-exact block kernel 11 (DMUL + DADD in the oracle's
                              order: C~ bit-identical to the oracle's).  Only with kernel = 0. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */

@@ -855,9 +855,12 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
             Bv.border = P.block_order.p;  // block rows of the rank's rows in locality order
           if (P.sq_tiled && same && nr == P.n && !getenv("SEXPM_BSR_NATURAL"))
             Bv.border = P.block_order_t.p;  // the aggregates in locality order
+          // long match lists (3D): fewer, deeper-pipelined warps
+          const BsrBufs &av = taylor ? w.bsrA : w.bsrB;
+          const bool long_lists = av.nbr > 0 && av.nb > (int64_t)kBsrMLongRow * av.nbr;
           nh.grid = (int)std::max<int64_t>(
-              1, std::min<int64_t>(nbr_a, (int64_t)P.sm_count * (stage == 13 ? kBsrMBlocksPerSm : 2)));
-          w.bscr.ensure((size_t)nh.grid * (stage == 13 ? (size_t)kBsrMJCap * 65 : (size_t)kBsrScratchPerCta), st);
+              1, std::min<int64_t>(nbr_a, (int64_t)P.sm_count * (stage == 13 ? (long_lists ? kBsrMBlocksPerSmLong : kBsrMBlocksPerSm) : 2)));
+          w.bscr.ensure((size_t)nh.grid * (stage == 13 ? (size_t)kBsrMJCap * 66 : (size_t)kBsrScratchPerCta), st);
           CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
           w.prof.ensure(16, st);
           CK(cudaMemsetAsync(w.prof.p, 0, 16 * sizeof(unsigned long long), st));
@@ -867,7 +870,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           CK(cudaEventCreate(&k1));
           CK(cudaEventRecord(k0, st));
           if (stage == 13)
-            launch_numeric_bsrm(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
+            launch_numeric_bsrm(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st, long_lists);
           else
             launch_numeric_bsr(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
           CK(cudaEventRecord(k1, st));
@@ -962,7 +965,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     // the tensor-core block kernel (B = H0) instead
     // (also once rows needed over half of it, or > 1 % of the rows were retried or handed on:
     // 3D rows keep growing term after term)
-    if (P.o.kernel == 0 && (nd > P.dia_slots_max / 2 || rep.window_rows * 100 > nr)) P.taylor_block = true;
+    if (P.o.kernel == 0 && !P.o.exact_products && (nd > P.dia_slots_max / 2 || rep.window_rows * 100 > nr))
+      P.taylor_block = true;
     if (getenv("SEXPM_STEP_LOG")) fprintf(stderr, "[sexpm run] K5d need %lld slots, next %d (max %d), retried rows %d\n", nd, P.dia_slots, P.dia_slots_max, (int)(rep.window_rows - nfail_other));
   }
   cudaEventDestroy(e0);

@@ -2031,10 +2031,9 @@ constexpr int kMKWords = 2048;             // K bitmap: block-column span of A's
 constexpr int kMJWords = 2048;             // J bitmap: output block-column span <= 65536
 constexpr int kMJCap = kBsrMJCap;          // output blocks per block row
 constexpr int kMML = 64;                   // matches listed at a time per warp
-constexpr int kMPF = 4;                    // block products whose operands are in flight
 
 int bsrm_numeric_smem_bytes() {
-  return kMKWords * 4 + kMKWords * 2 + kMJWords * 4 + kMJCap * 4 + kMWarps * kMML * 8 + 64;
+  return kMKWords * 4 + kMKWords * 2 + kMJWords * 4 + kMWarps * kMML * 8 + 64;
 }
 
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
@@ -2049,7 +2048,10 @@ __device__ __forceinline__ unsigned spread4(unsigned m) {
   return (m | (m << 1)) & 0x55u;
 }
 
-__global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, BsrView Bv, int64_t nrows,
+// kMPF block products' operands per set (two sets in flight), kMinB CTAs per SM: <2, 4> for
+// short match lists (2D: more warps), <4, 2> for long ones (3D: more loads per warp)
+template <int kMPF, int kMinB>
+__global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a, BsrView Bv, int64_t nrows,
                                                               double *scratch, int32_t *fail_rows,
                                                               int *fail_count) {
   extern __shared__ __align__(16) unsigned char msm[];
@@ -2057,15 +2059,16 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
   int32_t *mlb = mla + kMWarps * kMML;                                  // kMWarps * kMML
   unsigned *kbits = reinterpret_cast<unsigned *>(mlb + kMWarps * kMML); // kMKWords
   unsigned *jbits = kbits + kMKWords;                                   // kMJWords
-  int32_t *jlist = reinterpret_cast<int32_t *>(jbits + kMJWords);       // kMJCap
-  uint16_t *kpref = reinterpret_cast<uint16_t *>(jlist + kMJCap);       // kMKWords
+  uint16_t *kpref = reinterpret_cast<uint16_t *>(jbits + kMJWords);     // kMKWords
   __shared__ int s_I, s_fail, s_nj, s_kmin, s_jmin, s_nkw, s_njw;
   __shared__ double s_fs[kMWarps][8], s_p1[kMWarps][8];
   __shared__ long long s_nz[kMWarps][8], s_c1[kMWarps][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;  // fragment coordinates
-  double *scr = scratch + (size_t)blockIdx.x * kMJCap * 65;  // kMJCap blocks + keep masks
+  // per-CTA scratch (L2): kMJCap output blocks, their keep masks and the J list
+  double *scr = scratch + (size_t)blockIdx.x * kMJCap * 66;
   uint8_t *jm = reinterpret_cast<uint8_t *>(scr + (size_t)kMJCap * 64);
+  int32_t *jlist = reinterpret_cast<int32_t *>(scr + (size_t)kMJCap * 65);
   for (int i = tid; i < kMKWords; i += kMThreads) kbits[i] = 0u;
   for (int i = tid; i < kMJWords; i += kMThreads) jbits[i] = 0u;
   // B fragment offsets: B[t][g] and B[t + 4][g] in fragment order
@@ -2413,12 +2416,17 @@ __global__ void __launch_bounds__(kMThreads, 2) k_numeric_bsrm(NumericArgs a, Bs
 }
 
 void launch_numeric_bsrm(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
-                         int32_t *fail_rows, int *fail_count, cudaStream_t st) {
+                         int32_t *fail_rows, int *fail_count, cudaStream_t st, bool long_lists) {
   if (Bv.nbr_a == 0) return;
   const int smem = bsrm_numeric_smem_bytes();
-  cudaFuncSetAttribute(k_numeric_bsrm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
-  k_numeric_bsrm<<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
+  if (long_lists) {
+    cudaFuncSetAttribute(k_numeric_bsrm<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_numeric_bsrm<4, 2><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
+  } else {
+    cudaFuncSetAttribute(k_numeric_bsrm<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_numeric_bsrm<2, 4><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
+  }
 }
 
 

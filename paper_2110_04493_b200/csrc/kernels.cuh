@@ -171,12 +171,14 @@ void launch_numeric_bsr(const NumericArgs &a, const BsrView &Bv, int64_t nrows, 
                         int32_t *fail_rows, int *fail_count, cudaStream_t st);
 // K3m: the block product on the fp64 tensor-core instruction (DMMA m8n8k4; BSR values in
 // fragment order, launch_bsr_fill(frag = true)); no limit on the blocks of a row of A; scratch
-// of kBsrMJCap * 65 doubles per CTA; rows it cannot hold -> fail_rows
+// of kBsrMJCap * 66 doubles per CTA; rows it cannot hold -> fail_rows
 constexpr int kBsrMJCap = 8192;              // output blocks per block row (K3m)
-constexpr int kBsrMBlocksPerSm = 2;          // K3m CTAs per SM
+// K3m CTAs per SM: 4 (short match lists, 2 products in flight per operand set) or 2 (long
+// lists: a block row of A with more than kBsrMLongRow blocks on average, 4 per set)
+constexpr int kBsrMBlocksPerSm = 4, kBsrMBlocksPerSmLong = 2, kBsrMLongRow = 200;
 int bsrm_numeric_smem_bytes();
 void launch_numeric_bsrm(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
-                         int32_t *fail_rows, int *fail_count, cudaStream_t st);
+                         int32_t *fail_rows, int *fail_count, cudaStream_t st, bool long_lists);
 
 // --- K6 Algorithm 4.1 pass -------------------------------------------------------
 // out[0] = sum over x[0..cnt) of x^2 for |x| <= tau (deterministic order for fixed layout)
