@@ -28,7 +28,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "e^H wall time & squarings/s; achieved HBM GB/s vs peak, 1/2/4/8 B200"
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # derived: SMs x fp64 FMA lanes x 2 x max clock
 
 
 def parse():
@@ -46,6 +45,7 @@ def parse():
     ap.add_argument("--no-n3", action="store_true", help="skip the N3 reordering comparison")
     ap.add_argument("--no-n4", action="store_true", help="skip the N4 graph workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip configs 2-4 and the F-norm plan")
     ap.add_argument("--cpu-sample-grid", type=int, default=0)
     return ap.parse_args()
 
@@ -108,27 +108,32 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------------------
-def cpu_oracle_sample(args, target_seconds=12.0, grid=0):
-    """The oracle as it stands (OpenMP over rows, all host cores) on a bounded sample of
-    the workload: the same law (config 5: uniform 2D Dirichlet heat, r = 0.5, same plan
-    options) on a g x g grid; scaled to config 5's size by rows (interior rows carry the
-    same work).  Returns (e^H/s scaled, cores, sample description, seconds)."""
-    import oracle as O
+CPU_SAMPLE_GRID = {5: 256, 2: 100, 1: 1000, 3: 100, 4: 20}
+
+
+def sample_config(args):
+    """The bounded sample of the workload both the CPU baseline and the reference arm time:
+    the same law as the benched config on a smaller grid (config 5: the uniform 2D Dirichlet
+    heat matrix r = 0.5 on a 256 x 256 grid, n = 65536), same eps_tol and plan norm."""
     from synth import make_config
+    g = args.cpu_sample_grid or CPU_SAMPLE_GRID.get(args.config, 64)
+    return make_config(args.config, scale_down=g), g
+
+
+def cpu_oracle_sample(args, H=None, g=None):
+    """One e^H of the sample by the oracle as it stands (OpenMP over rows, all host cores):
+    (e^H/s of the sample as measured, cores, description, seconds).  Not scaled."""
+    import oracle as O
+    if H is None:
+        H, g = sample_config(args)
     cores = os.cpu_count() or 1
-    n_full = make_config_n(args.config)
-    g = grid or 48
-    while True:
-        H = make_config(args.config, scale_down=g)
-        t0 = time.perf_counter()
-        O.expm(H, args.eps_tol, plan_norm=args.plan_norm, nthreads=cores)
-        dt = time.perf_counter() - t0
-        if dt >= target_seconds / 4 or grid or g >= 400:
-            break
-        g = int(g * 1.6)
-    rows_per_s = H.n / dt
-    value = rows_per_s / n_full  # e^H per second at full size
-    return value, cores, f"config {args.config} law on a {g}x{g} grid (n={H.n}), scaled by rows to n={n_full}", dt
+    t0 = time.perf_counter()
+    O.expm(H, args.eps_tol, plan_norm=args.plan_norm, nthreads=cores)
+    dt = time.perf_counter() - t0
+    desc = (f"one e^H of the config-{args.config} law on a {g}x{g} grid (n={H.n}, eps_tol "
+            f"{args.eps_tol:g}, {args.plan_norm}-norm plan), oracle with {cores} OpenMP threads; "
+            "measured, not scaled")
+    return 1.0 / dt, cores, desc, dt
 
 
 def make_config_n(cid):
@@ -137,21 +142,28 @@ def make_config_n(cid):
 
 
 def run_reference(args):
+    """The reference arm for this tier: the CPU oracle (oracle/, as it stands) on the box's
+    host cores; each step = one e^H of the bounded sample of the workload (sample_config),
+    timed whole; value = e^H/s of that sample (our line reports the GPU on the same sample
+    under "same_sample")."""
     rank, world, _ = dist_env()
     if rank != 0:
         return  # other ranks exit without work
-    vals = []
+    H, g = sample_config(args)
+    times = []
     for i in range(args.warmup + args.steps):
-        v, cores, sample, dt = cpu_oracle_sample(args, grid=args.cpu_sample_grid or 64)
+        v, cores, sample, dt = cpu_oracle_sample(args, H, g)
         if i >= args.warmup:
-            vals.append(v)
-    value = sum(vals) / len(vals)
+            times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = 1000.0 / ms
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "e^H/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE config {args.config}", "eps_tol": args.eps_tol,
-                       "plan_norm": args.plan_norm},
+            "config": {"workload": f"BASELINE config {args.config} law on a {g}x{g} grid (n={H.n}): "
+                                   "the bounded CPU sample of the benched workload",
+                       "eps_tol": args.eps_tol, "plan_norm": args.plan_norm},
             "cpu_baseline": {"value": value, "unit": "e^H/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "e^H/s", "h2d_bytes_per_step": 0,
@@ -179,6 +191,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         dist.barrier()
     B.lib()
+    # fp64 roofline denominators measured on this GPU (DFMA chains and DMMA accumulators)
+    fp64_peak = B.sexpm_fp64_peak()
+    FP64_PEAK_TFLOPS = fp64_peak["dfma_tflops"]
     from synth import make_config
     H = make_config(args.config)
     n = H.n
@@ -429,6 +444,66 @@ def main():
                         "bandwidth_l1_T0": int(s4["sq_l1"][0]),
                         "sq_fallback_rows": [int(x) for x in s4["sq_fallback_rows"][1:N4 + 1]]}
 
+    # ---------------- the other configurations (one GPU; outside the timed steps) --------
+    # e^H (plan + run) device time of BASELINE configs 2-4 and of config 5 with the paper's
+    # Frobenius-norm plan ((M, N) = (19, 12)), best of 2 after a warm-up run
+    others = None
+    if world == 1 and not args.no_others:
+        others = {}
+        cases = [("config5_fro_plan", 5, "fro"), ("config2", 2, "one"), ("config3", 3, "one"),
+                 ("config4", 4, "one")]
+        for name, cid, pn in cases:
+            if cid == args.config and pn == args.plan_norm:
+                continue
+            Hc = H if cid == args.config else make_config(cid)
+            rc = [torch.from_numpy(a).to(dev) for a in (Hc.rowptr, Hc.col, Hc.val)]
+            ts = []
+            for rep_i in range(3):
+                b0 = torch.cuda.Event(enable_timing=True)
+                b1 = torch.cuda.Event(enable_timing=True)
+                b0.record(stream)
+                p = B.Plan(Hc.n, *rc, args.eps_tol, stream=stream, plan_norm=pn)
+                p.run_only()
+                b1.record(stream)
+                torch.cuda.synchronize()
+                sc = p.stats()
+                p.close()
+                if rep_i:
+                    ts.append(b0.elapsed_time(b1))
+            Nc = int(sc["N"])
+            sqk = [float(x) for x in sc["sq_kernel_ms"][1:Nc + 1]]
+            sqf = [2.0 * float(x) for x in sc["sq_fmas"][1:Nc + 1]]
+            others[name] = {"n": Hc.n, "plan_norm": pn, "M": int(sc["M"]), "N": Nc,
+                            "ms_expm": min(ts), "e_per_s": 1000.0 / min(ts),
+                            "phase_ms": {"plan": float(sc["ms_plan"]), "taylor": float(sc["ms_taylor"]),
+                                         "squaring": float(sc["ms_squaring"]), "finalize": float(sc["ms_finalize"])},
+                            "squarings_per_s": Nc / (float(sum(sc["sq_ms"][1:Nc + 1])) / 1e3) if Nc else None,
+                            "sq_kernel_ms": sqk,
+                            "sq_fp64_tflops_algorithmic": [f / (m * 1e9) for f, m in zip(sqf, sqk) if m > 0],
+                            "sq_fallback_rows": [int(x) for x in sc["sq_fallback_rows"][1:Nc + 1]],
+                            "nnz_E": int(sc["nnz_out"])}
+            del rc
+
+    # ---------------- the CPU sample on the GPU (same work as cpu_baseline / reference) ------
+    same_sample = None
+    if world == 1:
+        Hs, gs = sample_config(args)
+        rs_ = [torch.from_numpy(a).to(dev) for a in (Hs.rowptr, Hs.col, Hs.val)]
+        ts = []
+        for rep_i in range(4):
+            b0 = torch.cuda.Event(enable_timing=True)
+            b1 = torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            p = B.Plan(Hs.n, *rs_, args.eps_tol, stream=stream, **opts)
+            p.run_only()
+            b1.record(stream)
+            torch.cuda.synchronize()
+            p.close()
+            if rep_i:
+                ts.append(b0.elapsed_time(b1))
+        same_sample = {"workload": f"config-{args.config} law on a {gs}x{gs} grid (n={Hs.n})",
+                       "gpu_ms": min(ts), "gpu_e_per_s": 1000.0 / min(ts)}
+
     # ---------------- roofline of the dominant kernel ----------------
     import math
     sq_ms = [float(st["sq_kernel_ms"][i]) for i in range(1, N + 1)]
@@ -440,13 +515,13 @@ def main():
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     traffic_db = {}
-    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tp):
         traffic_db = json.load(open(tp))
     if sum(sq_ms) >= sum(ty_ms) and sq_ms:
         dur = sum(sq_ms) / len(sq_ms) / 1e3
         ach = sum(sq_fl) / len(sq_fl) / dur / 1e12
-        kname = "k_numeric_bsr" if int(st["sq_bsr_blocks"][1]) > 0 else "k_numeric_paged"
+        kname = "k_numeric_bsrm" if int(st["sq_bsr_blocks"][1]) > 0 else "k_numeric_paged"
         tr = traffic_db.get(kname)
         roof = {"kernel": f"{kname} (squaring SpGEMM + 2T + filter classify)", "bound": "alu",
                 "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -458,7 +533,10 @@ def main():
                 # work (2 x 512 per block product) per launch, beside the algorithmic count
                 "executed_fp64_tflops": (sum(1024.0 * float(st["sq_block_products"][i]) for i in range(1, N + 1))
                                          / len(sq_ms) / dur / 1e12),
-                "peak_source": "derived fp64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)",
+                "peak_source": "measured on this GPU before the timed steps: sexpm_fp64_peak DFMA chains "
+                               f"({FP64_PEAK_TFLOPS:.2f} TF/s; DMMA m8n8k4 {fp64_peak['dmma_tflops']:.2f} TF/s, "
+                               "the instruction the kernel issues)",
+                "dmma_peak": fp64_peak["dmma_tflops"],
                 "launches_per_step": len(sq_ms), "avg_launch_ms": dur * 1e3,
                 "hbm_gbs_compulsory": sum(float(st["sq_numeric_bytes"][i]) for i in range(1, N + 1)) / len(sq_ms) / dur / 1e9}
     elif ty_ms:
@@ -503,13 +581,19 @@ def main():
         "n2_filter_off": n2,
         "n3_reorder": n3,
         "n4_graph": n4,
+        "other_configs": others,
+        "same_sample": same_sample,
+        "fp64_peak_measured": fp64_peak,
     }
     if rank == 0:
         line["clocks"] = clk.summary()
         if world == 1 and not args.no_cpu_baseline:
-            v, cores, sample, dt = cpu_oracle_sample(args, grid=args.cpu_sample_grid)
+            v, cores, sample, dt = cpu_oracle_sample(args)
             line["cpu_baseline"] = {"value": v, "unit": "e^H/s", "cores": cores, "kind": "oracle",
                                     "sample": sample, "sample_seconds": dt}
+            if same_sample:
+                same_sample["cpu_s"] = dt
+                same_sample["gpu_over_cpu"] = dt * 1000.0 / same_sample["gpu_ms"]
         print(json.dumps(line, default=lambda o: float(o) if hasattr(o, "__float__") else str(o)),
               flush=True)
     if comm is not None:

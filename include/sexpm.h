@@ -185,6 +185,13 @@ int sexpm_abi_sizes(uint32_t *sizes);
 /* Kernels enqueued by this library since it was loaded (all plans, all threads). */
 int sexpm_kernel_launches(int64_t *count);
 
+/* fp64 throughput of the current device, measured (the squaring kernels' roofline
+ * denominator): best of 5 timed launches of 8 independent DFMA chains per thread (TF/s, 2
+ * flops per DFMA) and of 8 independent mma.sync.m8n8k4.f64 accumulators per warp (TF/s, 512
+ * flops per DMMA), 8 CTAs x 256 threads per SM.  Either pointer may be NULL (not both).
+ * Synchronous; allocates and frees its own scratch.  Errors: SEXPM_EINVAL, SEXPM_ECUDA. */
+int sexpm_fp64_peak(double *dfma_tflops, double *dmma_tflops);
+
 /* Fill defaults (see field comments). */
 int sexpm_options_init(sexpm_options *o);
 

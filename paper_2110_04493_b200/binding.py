@@ -26,7 +26,7 @@ EXPORTED = [
     "sexpm_result_copy", "sexpm_stats_get", "sexpm_destroy", "sexpm_last_error",
     "sexpm_filtered_product", "sexpm_alg41", "sexpm_halo_ranges", "sexpm_partition_rows",
     "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache", "sexpm_apply",
-    "sexpm_spmm", "sexpm_rcm", "sexpm_plan_scalars",
+    "sexpm_spmm", "sexpm_rcm", "sexpm_plan_scalars", "sexpm_fp64_peak",
 ]
 
 
@@ -121,6 +121,7 @@ def lib():
                                          P, P]
         L.sexpm_abi_sizes.argtypes = [P]
         L.sexpm_kernel_launches.argtypes = [P]
+        L.sexpm_fp64_peak.argtypes = [P, P]
         for f in EXPORTED:
             if f != "sexpm_last_error":
                 getattr(L, f).restype = C.c_int
@@ -195,6 +196,13 @@ def sexpm_stats_get(h) -> dict:
         v = getattr(s, k)
         d[k] = np.ctypeslib.as_array(v).copy() if hasattr(v, "_length_") else v
     return d
+
+
+def sexpm_fp64_peak() -> dict:
+    """Measured fp64 throughput of the current device: DFMA and DMMA TF/s."""
+    a, b = C.c_double(), C.c_double()
+    _check(lib().sexpm_fp64_peak(C.byref(a), C.byref(b)))
+    return {"dfma_tflops": a.value, "dmma_tflops": b.value}
 
 
 def sexpm_kernel_launches() -> int:

@@ -2438,6 +2438,42 @@ int sexpm_kernel_launches(int64_t *count) {
   return SEXPM_OK;
 }
 
+int sexpm_fp64_peak(double *dfma_tflops, double *dmma_tflops) {
+  ABI_BEGIN
+  REQUIRE(dfma_tflops || dmma_tflops, SEXPM_EINVAL, "bad args");
+  int dev = 0, sms = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double *out = nullptr;
+  CK(cudaMalloc(&out, (size_t)sms * 8 * 256 * sizeof(double)));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (int which = 0; which < 2; which++) {
+    double *dst = which == 0 ? dfma_tflops : dmma_tflops;
+    if (!dst) continue;
+    launch_fp64_peak(which, sms, out, st);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; rep++) {  // best of 5, CUDA events on the launching stream
+      CK(cudaEventRecord(e0, st));
+      launch_fp64_peak(which, sms, out, st);
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, ms);
+    }
+    *dst = fp64_peak_flops_per_launch(which, sms) / (best * 1e-3) / 1e12;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(cudaFree(out));
+  CK(cudaStreamDestroy(st));
+  ABI_END
+}
+
 int sexpm_abi_sizes(uint32_t *sizes) {
   if (!sizes) return SEXPM_EINVAL;
   sizes[0] = sizeof(sexpm_options);

@@ -3740,4 +3740,49 @@ void launch_i32_to_i64(const int32_t *in, int64_t n, int64_t *out, cudaStream_t 
   KL;
   k_i32_to_i64<<<grid_for(n, kThreads), kThreads, 0, st>>>(in, n, out);
 }
+// ------------------------------------------------------------------------------------
+// fp64 throughput of this GPU (the roofline denominator of the squaring kernels, measured
+// where the bench runs): 8 independent DFMA chains per thread, or 8 independent DMMA
+// (mma.m8n8k4.f64) accumulators per warp, over a grid of 8 CTAs x 256 threads per SM.
+// ------------------------------------------------------------------------------------
+constexpr int kPeakIters = 4096, kPeakChains = 8;
+__global__ void __launch_bounds__(256) k_peak_dfma(double *out, double a, double b) {
+  double x[kPeakChains];
+#pragma unroll
+  for (int c = 0; c < kPeakChains; c++) x[c] = threadIdx.x * 1e-3 + c;
+  for (int it = 0; it < kPeakIters; it++) {
+#pragma unroll
+    for (int c = 0; c < kPeakChains; c++) x[c] = fma(x[c], a, b);
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int c = 0; c < kPeakChains; c++) t += x[c];
+  out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = t;
+}
+__global__ void __launch_bounds__(256) k_peak_dmma(double *out, double a, double b) {
+  double d0[kPeakChains], d1[kPeakChains];
+#pragma unroll
+  for (int c = 0; c < kPeakChains; c++) d0[c] = d1[c] = threadIdx.x * 1e-3 + c;
+  for (int it = 0; it < kPeakIters; it++) {
+#pragma unroll
+    for (int c = 0; c < kPeakChains; c++) dmma884(d0[c], d1[c], a, b);
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int c = 0; c < kPeakChains; c++) t += d0[c] + d1[c];
+  out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = t;
+}
+double fp64_peak_flops_per_launch(int which, int sms) {
+  const double threads = (double)sms * 8 * 256;
+  return which == 0 ? threads * kPeakIters * kPeakChains * 2.0                  // 2 per DFMA
+                    : threads / 32 * kPeakIters * kPeakChains * 512.0;        // 8x8x4 x 2 per DMMA
+}
+void launch_fp64_peak(int which, int sms, double *out, cudaStream_t st) {
+  KL;
+  if (which == 0)
+    k_peak_dfma<<<sms * 8, 256, 0, st>>>(out, 0.999, 1e-3);
+  else
+    k_peak_dmma<<<sms * 8, 256, 0, st>>>(out, 0.999, 1e-3);
+}
+
 }  // namespace sx

@@ -273,4 +273,8 @@ void launch_identity(int64_t nrows, int64_t row0, int64_t *rp, int32_t *col, dou
 void launch_rebase_rowptr(const int64_t *src, int64_t cnt, int64_t base, int64_t *dst,
                           cudaStream_t st);
 
+// fp64 peak microbenchmark: which = 0 DFMA chains, 1 DMMA accumulators; out: sms*8*256 doubles
+double fp64_peak_flops_per_launch(int which, int sms);
+void launch_fp64_peak(int which, int sms, double *out, cudaStream_t st);
+
 }  // namespace sx
