@@ -129,7 +129,8 @@ typedef struct {
                              order: C~ bit-identical to the oracle's).  Only with kernel = 0. */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
-  void *nccl_comm;        /* ncclComm_t from sexpm_nccl_comm_init, or NULL for one GPU */
+  void *nccl_comm;        /* communicator handle from sexpm_nccl_comm_init (NCCL) or
+                             sexpm_virtual_comm_create (virtual ranks), or NULL for one GPU */
 } sexpm_options;
 
 #define SEXPM_MAXSTEP 160
@@ -201,6 +202,16 @@ int sexpm_options_init(sexpm_options *o);
 int sexpm_nccl_unique_id(void *id128);
 int sexpm_nccl_comm_init(int rank, int world, const void *id128, void **comm);
 int sexpm_nccl_comm_destroy(void *comm);
+
+/* Virtual ranks (testing the multi-rank path on one GPU): creates `world` communicator
+ * handles comms[0..world) that connect `world` plans in ONE process on ONE device, each
+ * driven by its own host thread (its own stream).  Every collective of the row-partitioned
+ * path (scalar all-gathers, the all-gather of H, the halo exchange of every squaring) is a
+ * host barrier, device-to-device copies from the peers' buffers on the caller's stream, and
+ * a second barrier; no kernel waits on another rank.  A rank that does not arrive within
+ * 300 s makes the others fail with SEXPM_ENCCL.  Pass comms[r] as options.nccl_comm of rank
+ * r; destroy each with sexpm_nccl_comm_destroy.  world in [1, 64], else SEXPM_EINVAL. */
+int sexpm_virtual_comm_create(int world, void **comms);
 
 /* Step 1-3 set-up: validate H (device CSR), compute ||H|| on the device, solve Eq. (4.20),
  * choose a, r0, eps_g^(0), scale H0 = H 2^-N.  eps_tol: target relative error bound r_N. */

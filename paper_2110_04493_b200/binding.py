@@ -26,7 +26,7 @@ EXPORTED = [
     "sexpm_result_copy", "sexpm_stats_get", "sexpm_destroy", "sexpm_last_error",
     "sexpm_filtered_product", "sexpm_alg41", "sexpm_halo_ranges", "sexpm_partition_rows",
     "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache", "sexpm_apply",
-    "sexpm_spmm", "sexpm_rcm", "sexpm_plan_scalars", "sexpm_fp64_peak",
+    "sexpm_spmm", "sexpm_rcm", "sexpm_plan_scalars", "sexpm_fp64_peak", "sexpm_virtual_comm_create",
 ]
 
 
@@ -122,6 +122,7 @@ def lib():
         L.sexpm_abi_sizes.argtypes = [P]
         L.sexpm_kernel_launches.argtypes = [P]
         L.sexpm_fp64_peak.argtypes = [P, P]
+        L.sexpm_virtual_comm_create.argtypes = [C.c_int, P]
         for f in EXPORTED:
             if f != "sexpm_last_error":
                 getattr(L, f).restype = C.c_int
@@ -196,6 +197,14 @@ def sexpm_stats_get(h) -> dict:
         v = getattr(s, k)
         d[k] = np.ctypeslib.as_array(v).copy() if hasattr(v, "_length_") else v
     return d
+
+
+def sexpm_virtual_comm_create(world: int) -> list:
+    """`world` communicator handles of virtual ranks (one process, one GPU, one host thread
+    per rank): pass handle r as nccl_comm of rank r's Plan."""
+    arr = (C.c_void_p * world)()
+    _check(lib().sexpm_virtual_comm_create(int(world), arr))
+    return [arr[i] for i in range(world)]
 
 
 def sexpm_fp64_peak() -> dict:

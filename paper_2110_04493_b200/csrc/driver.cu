@@ -13,6 +13,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <memory>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -106,6 +109,117 @@ static NcclApi &nccl() {
       throw SxError{SEXPM_ENCCL, std::string(#x) + ": " +                                \
                                      (g_nccl.ErrStr ? g_nccl.ErrStr(r_) : "nccl error")}; \
   } while (0)
+
+// ------------------------------------------------------------------------------------
+// Transport between the ranks of a row-partitioned plan: an all-gather
+// of equal-size pieces and a group of point-to-point transfers.  NcclTransport runs them over
+// NCCL (one process per GPU, NVLink / NVSwitch); VirtualTransport runs W ranks as host threads
+// of one process on one device (the multi-rank code path executed and tested on a single
+// GPU): every call is a host barrier, then device-to-device copies out of the peers' posted
+// buffers on the caller's stream, then a second barrier.  No kernel ever waits on another
+// rank: the waiting is on the host.
+// ------------------------------------------------------------------------------------
+struct Transport {
+  int world = 1, rank = 0;
+  struct Xfer {
+    int peer;
+    const void *src;
+    void *dst;
+    size_t bytes;
+  };
+  virtual ~Transport() = default;
+  // recv[g * bytes .. (g+1) * bytes) = rank g's send (device pointers, all ranks the same size)
+  virtual void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) = 0;
+  // sends[k] goes to sends[k].peer, recvs[k] comes from recvs[k].peer; the transfers between a
+  // pair of ranks are matched in the order listed (src / dst of sends / recvs respectively)
+  virtual void exchange(const std::vector<Xfer> &sends, const std::vector<Xfer> &recvs,
+                        cudaStream_t st) = 0;
+};
+
+struct NcclTransport : Transport {
+  ncclComm_t comm = nullptr;
+  void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+    NK(nccl().AllGather(send, recv, bytes, ncclChar, comm, st));
+  }
+  void exchange(const std::vector<Xfer> &sends, const std::vector<Xfer> &recvs,
+                cudaStream_t st) override {
+    NK(nccl().GroupStart());
+    for (const Xfer &x : sends)
+      if (x.bytes) NK(nccl().Send(x.src, x.bytes, ncclChar, x.peer, comm, st));
+    for (const Xfer &x : recvs)
+      if (x.bytes) NK(nccl().Recv(x.dst, x.bytes, ncclChar, x.peer, comm, st));
+    NK(nccl().GroupEnd());
+  }
+};
+
+struct VirtualHub {
+  int W = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const void *> ag;                   // posted all-gather sources
+  std::vector<std::vector<Transport::Xfer>> sent;  // posted sends per rank
+  std::atomic<int> refs{0};
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == W) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+      return;
+    }
+    const bool ok = cv.wait_for(lk, std::chrono::seconds(300), [&] { return gen != g; });
+    REQUIRE(ok, SEXPM_ENCCL, "virtual transport: a rank did not arrive within 300 s");
+  }
+};
+
+struct VirtualTransport : Transport {
+  VirtualHub *hub = nullptr;
+  void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+    CK(cudaStreamSynchronize(st));  // the piece is complete before peers read it
+    hub->ag[rank] = send;
+    hub->barrier();
+    for (int g = 0; g < world; g++)
+      if (bytes) CK(cudaMemcpyAsync((char *)recv + (size_t)g * bytes, hub->ag[g], bytes, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    hub->barrier();  // nobody reuses its send buffer before every peer has read it
+  }
+  void exchange(const std::vector<Xfer> &sends, const std::vector<Xfer> &recvs,
+                cudaStream_t st) override {
+    CK(cudaStreamSynchronize(st));
+    hub->sent[rank] = sends;
+    hub->barrier();
+    std::vector<size_t> next((size_t)world, 0);  // next unmatched send of each peer to me
+    for (const Xfer &r : recvs) {
+      const std::vector<Xfer> &ps = hub->sent[r.peer];
+      size_t &k = next[r.peer];
+      while (k < ps.size() && ps[k].peer != rank) k++;
+      REQUIRE(k < ps.size() && ps[k].bytes == r.bytes, SEXPM_EINTERNAL,
+              "virtual transport: receive without a matching send");
+      if (r.bytes) CK(cudaMemcpyAsync(r.dst, ps[k].src, r.bytes, cudaMemcpyDeviceToDevice, st));
+      k++;
+    }
+    CK(cudaStreamSynchronize(st));
+    hub->barrier();
+  }
+};
+
+// the communicator handle of the C ABI (sexpm_nccl_comm_init / sexpm_virtual_comm_create)
+struct SxComm {
+  uint64_t magic = 0x53584d434f4d4d31ull;  // "SXMCOMM1"
+  int kind = 0;                           // 0 NCCL, 1 virtual
+  int world = 1, rank = 0;
+  ncclComm_t nccl = nullptr;
+  VirtualHub *hub = nullptr;
+};
+static SxComm *as_comm(void *h) {
+  SxComm *c = reinterpret_cast<SxComm *>(h);
+  REQUIRE(c && c->magic == 0x53584d434f4d4d31ull, SEXPM_EINVAL,
+          "options.nccl_comm is not a handle from sexpm_nccl_comm_init / sexpm_virtual_comm_create");
+  return c;
+}
 
 // ------------------------------------------------------------------------------------
 // device buffers (stream-ordered allocator)
@@ -426,7 +540,7 @@ struct sexpm_plan_s {
   bool own_stream = false;
   sexpm_options o{};
   int world = 1, rank = 0;
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<Transport> tr;  // world > 1
   int64_t n = 0, row_begin = 0, row_end = 0;
   std::vector<int64_t> bounds;  // world + 1 row bounds
   double eps_tol = 0.0;
@@ -502,7 +616,7 @@ static void gather_doubles(sexpm_plan_s &P, const double *local, int cnt, std::v
   DBuf<double> d;
   d.alloc((size_t)cnt * (P.world + 1), P.st);
   CK(cudaMemcpyAsync(d.p, local, cnt * sizeof(double), cudaMemcpyHostToDevice, P.st));
-  NK(nccl().AllGather(d.p, d.p + cnt, cnt, ncclDouble, P.comm, P.st));
+  P.tr->allgather(d.p, d.p + cnt, cnt * sizeof(double), P.st);
   CK(cudaMemcpyAsync(all.data(), d.p + cnt, (size_t)cnt * P.world * sizeof(double),
                      cudaMemcpyDeviceToHost, P.st));
   CK(cudaStreamSynchronize(P.st));
@@ -1180,19 +1294,29 @@ static void allgather_rows(sexpm_plan_s &P, const CsrView &L, DCsr &F) {
   F.col.alloc((size_t)F.nnz, st);
   F.val.alloc((size_t)F.nnz, st);
   F.rp.alloc((size_t)P.n + 1, st);
-  NK(nccl().GroupStart());
+  // my block to every peer, every peer's block from it (pieces listed in the same order on
+  // both sides: rowptr, columns, values); my own block copied in place
+  std::vector<Transport::Xfer> sends, recvs;
+  const int me = P.rank;
   for (int g = 0; g < P.world; g++) {
-    const bool me = g == P.rank;
-    NK(nccl().Bcast(me ? (const void *)L.rp : nullptr, rp_parts.p + roff[g] + g, rows[g] + 1,
-                    ncclInt64, g, P.comm, st));
+    if (g == me) continue;
+    sends.push_back({g, L.rp, nullptr, (size_t)(rows[me] + 1) * sizeof(int64_t)});
+    if (nnzs[me]) {
+      sends.push_back({g, L.col, nullptr, (size_t)nnzs[me] * sizeof(int32_t)});
+      sends.push_back({g, L.val, nullptr, (size_t)nnzs[me] * sizeof(double)});
+    }
+    recvs.push_back({g, nullptr, rp_parts.p + roff[g] + g, (size_t)(rows[g] + 1) * sizeof(int64_t)});
     if (nnzs[g]) {
-      NK(nccl().Bcast(me ? (const void *)L.col : nullptr, F.col.p + noff[g], nnzs[g], ncclInt32,
-                      g, P.comm, st));
-      NK(nccl().Bcast(me ? (const void *)L.val : nullptr, F.val.p + noff[g], nnzs[g], ncclDouble,
-                      g, P.comm, st));
+      recvs.push_back({g, nullptr, F.col.p + noff[g], (size_t)nnzs[g] * sizeof(int32_t)});
+      recvs.push_back({g, nullptr, F.val.p + noff[g], (size_t)nnzs[g] * sizeof(double)});
     }
   }
-  NK(nccl().GroupEnd());
+  CK(cudaMemcpyAsync(rp_parts.p + roff[me] + me, L.rp, (rows[me] + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  if (nnzs[me]) {
+    CK(cudaMemcpyAsync(F.col.p + noff[me], L.col, nnzs[me] * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(F.val.p + noff[me], L.val, nnzs[me] * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  P.tr->exchange(sends, recvs, st);
   for (int g = 0; g < P.world; g++)
     launch_rebase_rowptr(rp_parts.p + roff[g] + g, rows[g], noff[g], F.rp.p + roff[g], st);
   CK(cudaStreamSynchronize(st));
@@ -1275,27 +1399,27 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
     to += piece_rows[h] ? piece_rows[h] + 1 : 0;
   }
   REQUIRE(ro == B.nrows, SEXPM_EINTERNAL, "halo rows do not tile the needed range");
-  NK(nccl().GroupStart());
+  std::vector<Transport::Xfer> sends, recvs;
   for (int h = 0; h < W; h++) {
     if (h == R) continue;
     if (shi[h] > slo[h]) {
       int64_t a = slo[h] - T.row0, b = shi[h] - T.row0;
-      NK(nccl().Send(T.rp.p + a, b - a + 1, ncclInt64, h, P.comm, st));
+      sends.push_back({h, T.rp.p + a, nullptr, (size_t)(b - a + 1) * sizeof(int64_t)});
       int64_t na = rp[a], nb = rp[b];
       if (nb > na) {
-        NK(nccl().Send(T.col.p + na, nb - na, ncclInt32, h, P.comm, st));
-        NK(nccl().Send(T.val.p + na, nb - na, ncclDouble, h, P.comm, st));
+        sends.push_back({h, T.col.p + na, nullptr, (size_t)(nb - na) * sizeof(int32_t)});
+        sends.push_back({h, T.val.p + na, nullptr, (size_t)(nb - na) * sizeof(double)});
       }
     }
     if (piece_rows[h]) {
-      NK(nccl().Recv(rp_tmp.p + tmp_at[h], piece_rows[h] + 1, ncclInt64, h, P.comm, st));
+      recvs.push_back({h, nullptr, rp_tmp.p + tmp_at[h], (size_t)(piece_rows[h] + 1) * sizeof(int64_t)});
       if (piece_nnz[h]) {
-        NK(nccl().Recv(B.col.p + nnz_at[h], piece_nnz[h], ncclInt32, h, P.comm, st));
-        NK(nccl().Recv(B.val.p + nnz_at[h], piece_nnz[h], ncclDouble, h, P.comm, st));
+        recvs.push_back({h, nullptr, B.col.p + nnz_at[h], (size_t)piece_nnz[h] * sizeof(int32_t)});
+        recvs.push_back({h, nullptr, B.val.p + nnz_at[h], (size_t)piece_nnz[h] * sizeof(double)});
       }
     }
   }
-  NK(nccl().GroupEnd());
+  P.tr->exchange(sends, recvs, st);
   // my own rows
   CK(cudaMemcpyAsync(rp_tmp.p + tmp_at[R], T.rp.p, (T.nrows + 1) * sizeof(int64_t),
                      cudaMemcpyDeviceToDevice, st));
@@ -2523,15 +2647,45 @@ int sexpm_nccl_comm_init(int rank, int world, const void *id128, void **comm) {
   REQUIRE(id128 && comm && world >= 1 && rank >= 0 && rank < world, SEXPM_EINVAL, "bad args");
   ncclUniqueId id;
   memcpy(&id, id128, sizeof(id));
-  ncclComm_t c;
-  NK(nccl().CommInitRank(&c, world, id, rank));
+  ncclComm_t nc;
+  NK(nccl().CommInitRank(&nc, world, id, rank));
+  SxComm *c = new SxComm();
+  c->kind = 0;
+  c->world = world;
+  c->rank = rank;
+  c->nccl = nc;
   *comm = c;
+  ABI_END
+}
+
+int sexpm_virtual_comm_create(int world, void **comms) {
+  ABI_BEGIN
+  REQUIRE(comms && world >= 1 && world <= 64, SEXPM_EINVAL, "bad args");
+  VirtualHub *hub = new VirtualHub();
+  hub->W = world;
+  hub->ag.assign((size_t)world, nullptr);
+  hub->sent.assign((size_t)world, {});
+  hub->refs = world;
+  for (int r = 0; r < world; r++) {
+    SxComm *c = new SxComm();
+    c->kind = 1;
+    c->world = world;
+    c->rank = r;
+    c->hub = hub;
+    comms[r] = c;
+  }
   ABI_END
 }
 
 int sexpm_nccl_comm_destroy(void *comm) {
   ABI_BEGIN
-  if (comm) NK(nccl().CommDestroy((ncclComm_t)comm));
+  if (comm) {
+    SxComm *c = as_comm(comm);
+    if (c->kind == 0) NK(nccl().CommDestroy(c->nccl));
+    else if (--c->hub->refs == 0) delete c->hub;
+    c->magic = 0;
+    delete c;
+  }
   ABI_END
 }
 
@@ -2595,19 +2749,18 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (P->o.nccl_comm) {
-    P->comm = (ncclComm_t)P->o.nccl_comm;
-    int r = 0, w = 1;
-    auto &api = nccl();
-    (void)api;
-    ncclResult_t (*CountF)(const ncclComm_t, int *) =
-        reinterpret_cast<ncclResult_t (*)(const ncclComm_t, int *)>(dlsym(RTLD_DEFAULT, "ncclCommCount"));
-    ncclResult_t (*RankF)(const ncclComm_t, int *) =
-        reinterpret_cast<ncclResult_t (*)(const ncclComm_t, int *)>(dlsym(RTLD_DEFAULT, "ncclCommUserRank"));
-    REQUIRE(CountF && RankF, SEXPM_ENCCL, "ncclCommCount / ncclCommUserRank missing");
-    NK(CountF(P->comm, &w));
-    NK(RankF(P->comm, &r));
-    P->world = w;
-    P->rank = r;
+    SxComm *c = as_comm(P->o.nccl_comm);
+    if (c->kind == 0) {
+      auto t = std::make_unique<NcclTransport>();
+      t->comm = c->nccl;
+      P->tr = std::move(t);
+    } else {
+      auto t = std::make_unique<VirtualTransport>();
+      t->hub = c->hub;
+      P->tr = std::move(t);
+    }
+    P->tr->world = P->world = c->world;
+    P->tr->rank = P->rank = c->rank;
   }
   return P;
 }

@@ -16,7 +16,7 @@
 
 namespace sx {
 
-long long g_kernel_launches = 0;  // kernels enqueued (reported as gpu_launches)
+std::atomic<long long> g_kernel_launches{0};  // kernels enqueued (reported as gpu_launches)
 #define KL (++g_kernel_launches)
 
 #define FULL_MASK 0xffffffffu

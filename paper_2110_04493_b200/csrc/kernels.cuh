@@ -5,9 +5,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace sx {
 
-extern long long g_kernel_launches;  // incremented by every launcher
+extern std::atomic<long long> g_kernel_launches;  // incremented by every launcher
 
 constexpr int kThreads = 256;                 // row kernels: 8 warps per CTA
 constexpr int kWarps = kThreads / 32;
