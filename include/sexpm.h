@@ -177,6 +177,10 @@ typedef struct {
   /* the library's device-block cache during the last sexpm_plan + sexpm_run (process-wide) */
   int64_t cache_hits, cache_misses, cache_releases;
   double cache_bytes_cached, cache_bytes_allocated;
+  int32_t sq_order_used;                       /* squarings ran in: 0 index order, 1 BFS
+                                                  aggregates, 2 compact aggregates (sq_order) */
+  double sq_exchange_ms[SEXPM_MAXSTEP];        /* world > 1: halo exchange of the squaring
+                                                  (host wall clock, incl. the peers' wait) */
 } sexpm_stats;
 
 /* sizes[0..3] = sizeof(sexpm_options), sizeof(sexpm_stats), sizeof(sexpm_csr_in),

@@ -83,7 +83,8 @@ class Stats(C.Structure):
                 ("sq_block_products", _F64),
                 ("cache_hits", C.c_int64), ("cache_misses", C.c_int64),
                 ("cache_releases", C.c_int64), ("cache_bytes_cached", C.c_double),
-                ("cache_bytes_allocated", C.c_double)]
+                ("cache_bytes_allocated", C.c_double), ("sq_order_used", C.c_int32),
+                ("sq_exchange_ms", _F64)]
 
 
 _lib = None

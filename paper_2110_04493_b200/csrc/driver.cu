@@ -571,9 +571,11 @@ struct sexpm_plan_s {
   // squarings in aggregate order (option sq_order): perm[new] = old, 8-row aggregates of H's
   // graph; sq_tiled while the iterate is held in that order
   std::vector<int64_t> h_tperm;
-  DBuf<int64_t> tperm, tinv;
+  DBuf<int64_t> tperm, tinv;          // global maps (columns)
+  DBuf<int64_t> tperm_loc, tinv_loc;  // this rank's rows (local indices)
   DBuf<int32_t> block_order_t;  // the aggregates (block rows in that order) in locality order
   bool sq_tiled = false;
+  int agg_kind = 0;  // 0 none, 1 BFS aggregates, 2 compact aggregates
   DBuf<int32_t> block_order;  // block rows of the block kernel in locality order
   // H0's BSR-8 view in fragment order with its block transpose (Taylor terms on K3m), built
   // on first use; h0bsr_state 0 not built, 1 built, -1 not representable
@@ -1447,13 +1449,22 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
 // rows of the new order are a compact neighbourhood, so the 8x8 blocks of the squared
 // iterate are fuller (config-5-like pattern: 45 % fewer block products in the model,
 // DESIGN.md section 6).  perm[new] = old.
+// Aggregates never cross the rank partition `bounds` (rows [bounds[g], bounds[g+1]) stay
+// together): the permutation is block-diagonal, so every rank relabels only its own rows.
+static inline int range_of(const std::vector<int64_t> &bounds, int64_t v) {
+  return (int)(std::upper_bound(bounds.begin(), bounds.end(), v) - bounds.begin()) - 1;
+}
 static void aggregate_order(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
-                            int64_t n, int size, std::vector<int64_t> &perm) {
+                            int64_t n, int size, const std::vector<int64_t> &bounds,
+                            std::vector<int64_t> &perm) {
   perm.clear();
   perm.reserve((size_t)n);
   std::vector<uint8_t> used((size_t)n, 0);
+  int g = 0;
   for (int64_t s = 0; s < n; s++) {
     if (used[s]) continue;
+    while (s >= bounds[g + 1]) g++;
+    const int64_t lo = bounds[g], hi = bounds[g + 1];
     const size_t g0 = perm.size();
     perm.push_back(s);
     used[s] = 1;
@@ -1461,7 +1472,7 @@ static void aggregate_order(const std::vector<int64_t> &rp, const std::vector<in
       const int64_t v = perm[h];
       for (int64_t p = rp[v]; p < rp[v + 1] && (int)(perm.size() - g0) < size; p++) {
         const int64_t u = col[p];
-        if (!used[u]) {
+        if (!used[u] && u >= lo && u < hi) {
           used[u] = 1;
           perm.push_back(u);
         }
@@ -1477,14 +1488,18 @@ static void aggregate_order(const std::vector<int64_t> &rp, const std::vector<in
 // grid graph, and blocks of compact aggregates fill them with fewer partial blocks than
 // the star-shaped BFS aggregates or index-order line segments.
 static void aggregate_order_compact(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
-                                    int64_t n, int size, std::vector<int64_t> &perm) {
+                                    int64_t n, int size, const std::vector<int64_t> &bounds,
+                                    std::vector<int64_t> &perm) {
   perm.clear();
   perm.reserve((size_t)n);
   std::vector<uint8_t> used((size_t)n, 0);
   std::vector<int32_t> cnt((size_t)n, 0), firstm((size_t)n, 0);  // per candidate: edges, first member
   std::vector<int64_t> agg, cand;
+  int g = 0;
   for (int64_t s = 0; s < n; s++) {
     if (used[s]) continue;
+    while (s >= bounds[g + 1]) g++;
+    const int64_t lo = bounds[g], hi = bounds[g + 1];
     agg.clear();
     cand.clear();
     int64_t v = s;
@@ -1495,7 +1510,7 @@ static void aggregate_order_compact(const std::vector<int64_t> &rp, const std::v
       if ((int)agg.size() >= size) break;
       for (int64_t p = rp[v]; p < rp[v + 1]; p++) {  // v's edges raise its neighbours' counts
         const int64_t u = col[p];
-        if (used[u]) continue;
+        if (used[u] || u < lo || u >= hi) continue;
         if (cnt[u] == 0) {
           firstm[u] = m;
           cand.push_back(u);
@@ -1709,7 +1724,7 @@ static void permute_csr(sexpm_plan_s &P, const CsrView &A, const int64_t *rowmap
   w.cnt.ensure((size_t)std::max<int64_t>(n, 1), st);
   w.scan_tmp.ensure((size_t)scan_tmp_elems(n) + 1, st);
   C.nrows = n;
-  C.row0 = 0;
+  C.row0 = A.row0;  // rows are relabelled within the view (a rank's own rows)
   C.nnz = A.nnz;
   C.padded = false;
   C.rp.ensure((size_t)n + 1, st);
@@ -2126,9 +2141,11 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     const int64_t nl = P.row_end - P.row_begin;
     P.proc_order.ensure((size_t)std::max<int64_t>(nl, 1), st);
     P.block_order.ensure((size_t)std::max<int64_t>((nl + 7) / 8, 1), st);
-    if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1) {
+    if (P.o.sq_order == 1 && P.N >= 1) {
       P.tperm.ensure((size_t)std::max<int64_t>(P.n, 1), st);
       P.tinv.ensure((size_t)std::max<int64_t>(P.n, 1), st);
+      P.tperm_loc.ensure((size_t)std::max<int64_t>(nl, 1), st);
+      P.tinv_loc.ensure((size_t)std::max<int64_t>(nl, 1), st);
       P.block_order_t.ensure((size_t)std::max<int64_t>((P.n + 7) / 8, 1), st);
     }
     CK(cudaEventCreateWithFlags(&P.ev_pattern, cudaEventDisableTiming));
@@ -2166,14 +2183,14 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
           CK(cudaMemcpyAsync(P.block_order.p, bo.data(), bo.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         if (!ord.empty())
           CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
-        if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1) {  // aggregate order of the squarings
+        if (P.o.sq_order == 1 && P.N >= 1) {  // aggregate order of the squarings (per rank range)
           // candidates: BFS aggregates and compact aggregates; kept only where it fills the
           // 8x8 blocks better than index order: for a sample of block rows, count the distinct
           // column blocks covered by the radius-r neighbourhood of their 8 rows (the iterates'
           // rows are such neighbourhoods; r ~ 0.8 M, the reach of the filtered Taylor phase)
           std::vector<int64_t> cand[2];
-          aggregate_order(hrp, hcol, P.n, 8, cand[0]);
-          aggregate_order_compact(hrp, hcol, P.n, 8, cand[1]);
+          aggregate_order(hrp, hcol, P.n, 8, P.bounds, cand[0]);
+          aggregate_order_compact(hrp, hcol, P.n, 8, P.bounds, cand[1]);
           const int rad = std::max(3, std::min(16, (int)lround(0.8 * P.M)));
           const int64_t nbt = (P.n + 7) / 8, step = std::max<int64_t>(1, nbt / 512);
           std::vector<int32_t> mark((size_t)P.n, -1), fr, nx;
@@ -2221,11 +2238,15 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
                     rad, (long long)b_idx, (long long)b_bfs, (long long)b_cmp,
                     10 * b_agg <= 9 * b_idx ? (pick ? "compact" : "BFS") : "index order");
           P.h_tperm.clear();
-          if (10 * b_agg <= 9 * b_idx) P.h_tperm.swap(cand[pick]);
+          P.agg_kind = 0;
+          if (10 * b_agg <= 9 * b_idx) {
+            P.h_tperm.swap(cand[pick]);
+            P.agg_kind = 1 + pick;
+          }
           for (int64_t i = 0; i < (int64_t)P.h_tperm.size(); i++) hinv[P.h_tperm[i]] = i;
           // block rows of the relabelled matrix in the locality order of H's clusters: each
           // aggregate ranked by the earliest position of its rows in `ord`
-          if (!P.h_tperm.empty()) {
+          if (!P.h_tperm.empty() && P.world == 1) {
             std::vector<int32_t> at((size_t)P.n);
             for (size_t j = 0; j < ord.size(); j++) at[ord[j]] = (int32_t)j;
             const int64_t nbt = (P.n + 7) / 8;
@@ -2242,9 +2263,18 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
             CK(cudaStreamSynchronize(P.bg_st));  // bot is local
           }
           if (!P.h_tperm.empty()) {
+            // this rank's rows: local old row of local new row i, and the inverse
+            const int64_t rb = P.row_begin, nloc = P.row_end - P.row_begin;
+            std::vector<int64_t> ploc((size_t)std::max<int64_t>(nloc, 1)), iloc((size_t)std::max<int64_t>(nloc, 1));
+            for (int64_t i = 0; i < nloc; i++) {
+              ploc[i] = P.h_tperm[rb + i] - rb;
+              iloc[i] = hinv[rb + i] - rb;
+            }
             CK(cudaMemcpyAsync(P.tperm.p, P.h_tperm.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
             CK(cudaMemcpyAsync(P.tinv.p, hinv.data(), P.n * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
-            CK(cudaStreamSynchronize(P.bg_st));  // hinv is local
+            CK(cudaMemcpyAsync(P.tperm_loc.p, ploc.data(), nloc * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
+            CK(cudaMemcpyAsync(P.tinv_loc.p, iloc.data(), nloc * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
+            CK(cudaStreamSynchronize(P.bg_st));  // host vectors are local
           }
         }
         CK(cudaEventRecord(P.ev_order, P.bg_st));
@@ -2384,12 +2414,13 @@ static void do_run(sexpm_plan_s &P) {
   // mapped back after the last squaring (the SSAT baseline keeps the index order: its
   // products must match the oracle's bit for bit)
   P.sq_tiled = false;
-  if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1 && !P.o.ssat && P.M >= 1) {
+  if (P.o.sq_order == 1 && P.N >= 1 && !P.o.ssat && P.M >= 1) {
     wait_order(P);
     if (!P.h_tperm.empty()) {
-      permute_csr(P, T.view(), P.tperm.p, P.tinv.p, Tn);  // row i <- row tperm[i], col c -> tinv[c]
+      permute_csr(P, T.view(), P.tperm_loc.p, P.tinv.p, Tn);  // row i <- row tperm[i], col c -> tinv[c]
       swap_csr(T, Tn);
       P.sq_tiled = true;
+      S.sq_order_used = P.agg_kind;
     }
   }
   // stats of T^_0
@@ -2441,7 +2472,10 @@ static void do_run(sexpm_plan_s &P) {
     if (P.world == 1) {
       filtered_product(P, T.view(), T.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
     } else {
+      const auto x0 = std::chrono::steady_clock::now();
       exchange_halo(P, T, l1, l2, P.Bhalo);
+      if (i < SEXPM_MAXSTEP)
+        S.sq_exchange_ms[i] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - x0).count();
       filtered_product(P, T.view(), P.Bhalo.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
     }
     const double ms = step_ms();
@@ -2495,7 +2529,7 @@ static void do_run(sexpm_plan_s &P) {
   }
   if (P.sq_tiled) {  // back to index order: row r <- row tinv[r], col c' -> tperm[c']
     DCsr &spare = (&T == &P.E) ? Tn : (T.nnz >= P.E.nnz ? T : Tn);  // an iterate no longer needed
-    permute_csr(P, P.E.view(), P.tinv.p, P.tperm.p, spare);
+    permute_csr(P, P.E.view(), P.tinv_loc.p, P.tperm.p, spare);
     swap_csr(P.E, spare);
     P.sq_tiled = false;
   }

@@ -106,6 +106,8 @@ def test_virtual_ranks_match_oracle(B, W, name):
     ok, res = parity(Eg, Eo, last_tau(tr, st))
     assert ok, res
     if name != "banded_nonsym":  # stencil rows: every rank squares on the block kernel
+        if name.startswith(("heat2d", "config5")):  # 2D: aggregates of each rank's own rows
+            assert st["sq_order_used"] in (1, 2)
         for s in sts:
             assert s["sq_fallback_rows"][1:int(s["N"]) + 1].sum() == 0
             assert all(s["sq_bsr_blocks"][1:int(s["N"]) + 1] > 0)
