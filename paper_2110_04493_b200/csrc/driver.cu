@@ -802,8 +802,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   const bool use_cluster = sq_like && !P.sq_tiled && P.proc_order.p && (int64_t)P.proc_order.n >= nr &&
                            A.row0 == P.row_begin && nr == P.row_end - P.row_begin;
   if (use_cluster) wait_order(P);
-  if (!use_cluster && have_symbolic)
-    launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
+  // the block kernels schedule block rows themselves: row bins only for the row kernels
+  const bool block_sq = sq_like && (P.o.kernel == 0 || P.o.kernel == 11 || P.o.kernel == 13);
+  const bool binned = !use_cluster && have_symbolic && !block_sq;
+  if (binned) launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
 
   // K3 numeric
   NumericArgs na;
@@ -814,7 +816,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   na.floor_tau = floor_tau;
   na.lo = w.lo.p;
   na.hi = w.hi.p;
-  na.order = use_cluster ? P.proc_order.p : (have_symbolic ? w.order.p : nullptr);
+  na.order = use_cluster ? P.proc_order.p : (binned ? w.order.p : nullptr);
   na.window = P.o.window_cols > 0 ? P.o.window_cols : 8192;
   na.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.numeric_blocks_per_sm));
   na.cursor_cap = std::max<int64_t>(hstat[6], 1);

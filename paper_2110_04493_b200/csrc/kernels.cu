@@ -1553,6 +1553,56 @@ __global__ void k_gather_i32(const int32_t *src, const int64_t *idx, int64_t cnt
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[idx[i]];
 }
+// block transpose without a library sort: blocks scattered to their column's segment with
+// an atomic cursor (any order), then every column's block indices sorted ascending (block
+// indices enumerate block rows in order, so ascending index = ascending K): one CTA per column,
+// bitonic network in shared memory over <= kTSortCap entries
+constexpr int kTSortCap = 2048;
+__global__ void k_bsrT_scatter(int64_t nbr, const int64_t *brp, const int32_t *bcol, const int64_t *tp,
+                               int32_t *cur, int64_t *tb) {
+  const int64_t K = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (K >= nbr) return;
+  for (int64_t b = brp[K] + lane; b < brp[K + 1]; b += 32) {
+    const int J = bcol[b];
+    tb[tp[J] + atomicAdd(&cur[J], 1)] = b;
+  }
+}
+__global__ void __launch_bounds__(256) k_sort_segments_i64(const int64_t *sp, int64_t nseg, int64_t *x,
+                                                             int *too_long) {
+  __shared__ int64_t key[kTSortCap];
+  for (int64_t sgm = blockIdx.x; sgm < nseg; sgm += gridDim.x) {
+    const int64_t a = sp[sgm];
+    const int len = (int)(sp[sgm + 1] - a);
+    if (len <= 1) continue;
+    if (len > kTSortCap) {
+      if (threadIdx.x == 0) atomicOr(too_long, 1);
+      continue;
+    }
+    int m = 2;
+    while (m < len) m <<= 1;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) key[i] = i < len ? x[a + i] : INT64_MAX;
+    __syncthreads();
+    for (int k = 2; k <= m; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+          const int p = i ^ j;
+          if (p > i) {
+            const bool up = (i & k) == 0;
+            const int64_t u = key[i], v = key[p];
+            if ((u > v) == up) {
+              key[i] = v;
+              key[p] = u;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) x[a + i] = key[i];
+    __syncthreads();
+  }
+}
+
 size_t bsr_transpose_temp_bytes(int64_t nb) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t *)nullptr, (int32_t *)nullptr,
@@ -1575,13 +1625,24 @@ void launch_bsr_transpose(int64_t nbr, int64_t nbc, int64_t nb, const int64_t *b
   if (nb == 0) return;
   KL;
   k_bsr_rows_of_blocks<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(nbr, brp, tk_tmp, tb_tmp);
-  // sort (J, block index) pairs by J, stable: within a column the block indices (and so K)
-  // stay ascending
-  int bits = 1;
-  while (bits < 31 && (int64_t(1) << bits) <= nbc) bits++;
+  // in-house: scatter by column, sort each column's block indices (tcnt reused as cursors,
+  // keys_out's first word as the overflow flag)
+  cudaMemsetAsync(tcnt, 0, (size_t)std::max<int64_t>(nbc, 1) * sizeof(int32_t), st);
+  cudaMemsetAsync(keys_out, 0, sizeof(int32_t), st);
   KL;
-  cub::DeviceRadixSort::SortPairs(sort_tmp, sort_tmp_bytes, bcol, keys_out, tb_tmp, tb, (int)nb, 0,
-                                  bits, st);
+  k_bsrT_scatter<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(nbr, brp, bcol, tp, tcnt, tb);
+  KL;
+  k_sort_segments_i64<<<(int)std::max<int64_t>(1, std::min<int64_t>(nbc, 148 * 8)), 256, 0, st>>>(tp, nbc, tb, keys_out);
+  int too_long = 0;
+  cudaMemcpyAsync(&too_long, keys_out, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  if (too_long) {  // a column with more than kTSortCap blocks: stable radix sort by column
+    int bits = 1;
+    while (bits < 31 && (int64_t(1) << bits) <= nbc) bits++;
+    KL;
+    cub::DeviceRadixSort::SortPairs(sort_tmp, sort_tmp_bytes, bcol, keys_out, tb_tmp, tb, (int)nb, 0,
+                                    bits, st);
+  }
   KL;
   k_gather_i32<<<grid_for(nb, kThreads, 148 * 16), kThreads, 0, st>>>(tk_tmp, tb, nb, tk);
 }
