@@ -565,7 +565,9 @@ def main():
         "expm_wall_s": ms_per_step / 1e3,
         "squarings_per_s": (N / (sq_total_ms / 1e3)) if N and sq_total_ms > 0 else None,
         "phase_ms": {"plan": float(st["ms_plan"]), "taylor": float(st["ms_taylor"]),
-                     "squaring": float(st["ms_squaring"]), "finalize": float(st["ms_finalize"])},
+                     "squaring": float(st["ms_squaring"]), "finalize": float(st["ms_finalize"]),
+                     "order_host_thread": float(st["ms_order_host"]),
+                     "order_wait": float(st["ms_order_wait"])},
         "roofline": roof,
         "steps_detail": [{"ms": times[j], "retries": int(stats[j]["retries"]),
                           "taylor_ms": float(stats[j]["ms_taylor"]),

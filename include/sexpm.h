@@ -181,6 +181,9 @@ typedef struct {
                                                   aggregates, 2 compact aggregates (sq_order) */
   double sq_exchange_ms[SEXPM_MAXSTEP];        /* world > 1: halo exchange of the squaring
                                                   (host wall clock, incl. the peers' wait) */
+  double ms_order_host;  /* the squarings' locality / aggregate order, computed on a host
+                            thread from H's pattern while the Taylor phase runs (wall ms) */
+  double ms_order_wait;  /* how long the first squaring waited for it (0 when hidden) */
 } sexpm_stats;
 
 /* sizes[0..3] = sizeof(sexpm_options), sizeof(sexpm_stats), sizeof(sexpm_csr_in),

@@ -576,6 +576,7 @@ struct sexpm_plan_s {
   DBuf<int32_t> block_order_t;  // the aggregates (block rows in that order) in locality order
   bool sq_tiled = false;
   int agg_kind = 0;  // 0 none, 1 BFS aggregates, 2 compact aggregates
+  double order_host_ms = 0.0, order_wait_ms = 0.0;  // background ordering thread: duration, wait
   DBuf<int32_t> block_order;  // block rows of the block kernel in locality order
   // H0's BSR-8 view in fragment order with its block transpose (Taylor terms on K3m), built
   // on first use; h0bsr_state 0 not built, 1 built, -1 not representable
@@ -680,7 +681,9 @@ static void build_transpose(sexpm_plan_s &P, const CsrView &Bv, int64_t ncols, D
 // join the background order thread (once) and order the plan's stream after its upload
 static void wait_order(sexpm_plan_s &P) {
   if (!P.order_pending) return;
+  const auto w0 = std::chrono::steady_clock::now();
   if (P.bg.joinable()) P.bg.join();
+  P.order_wait_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
   P.order_pending = false;
   REQUIRE(P.bg_err.empty(), SEXPM_ECUDA, P.bg_err);
   CK(cudaStreamWaitEvent(P.st, P.ev_order, 0));
@@ -1451,31 +1454,30 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
 // rows of the new order are a compact neighbourhood, so the 8x8 blocks of the squared
 // iterate are fuller (config-5-like pattern: 45 % fewer block products in the model,
 // DESIGN.md section 6).  perm[new] = old.
-// Aggregates never cross the rank partition `bounds` (rows [bounds[g], bounds[g+1]) stay
-// together): the permutation is block-diagonal, so every rank relabels only its own rows.
-static inline int range_of(const std::vector<int64_t> &bounds, int64_t v) {
-  return (int)(std::upper_bound(bounds.begin(), bounds.end(), v) - bounds.begin()) - 1;
-}
+// 8-row aggregates of the rows [lo, hi) of H's graph (one rank's range: aggregates never
+// cross the rank partition, so the relabelling is block-diagonal over it and every rank
+// relabels only its own rows).  perm receives the range's nodes in the new order (global ids).
+//   aggregate_order: greedy BFS from seeds in index order (every aggregate a compact
+//     neighbourhood: a star of the seed's ring on a grid);
+//   aggregate_order_compact: from each seed add, one at a time, the unused neighbour with the
+//     most edges into the aggregate; ties to the candidate adjacent to the earliest-added
+//     member, then to the smaller index (2 x 2 x 2 cubes on a 3D grid, 4 x 2 rectangles in 2D).
 static void aggregate_order(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
-                            int64_t n, int size, const std::vector<int64_t> &bounds,
-                            std::vector<int64_t> &perm) {
+                            int64_t lo, int64_t hi, int size, std::vector<int64_t> &perm) {
   perm.clear();
-  perm.reserve((size_t)n);
-  std::vector<uint8_t> used((size_t)n, 0);
-  int g = 0;
-  for (int64_t s = 0; s < n; s++) {
-    if (used[s]) continue;
-    while (s >= bounds[g + 1]) g++;
-    const int64_t lo = bounds[g], hi = bounds[g + 1];
+  perm.reserve((size_t)(hi - lo));
+  std::vector<uint8_t> used((size_t)(hi - lo), 0);
+  for (int64_t s = lo; s < hi; s++) {
+    if (used[s - lo]) continue;
     const size_t g0 = perm.size();
     perm.push_back(s);
-    used[s] = 1;
+    used[s - lo] = 1;
     for (size_t h = g0; h < perm.size() && (int)(perm.size() - g0) < size; h++) {
       const int64_t v = perm[h];
       for (int64_t p = rp[v]; p < rp[v + 1] && (int)(perm.size() - g0) < size; p++) {
         const int64_t u = col[p];
-        if (!used[u] && u >= lo && u < hi) {
-          used[u] = 1;
+        if (u >= lo && u < hi && !used[u - lo]) {
+          used[u - lo] = 1;
           perm.push_back(u);
         }
       }
@@ -1483,55 +1485,95 @@ static void aggregate_order(const std::vector<int64_t> &rp, const std::vector<in
   }
 }
 
-// Compact aggregates: from each unused seed (index order) add, one at a time, the unused
-// neighbour of the aggregate with the most edges into it; ties go to the candidate adjacent
-// to the earliest-added member, then to the smaller index.  On a 3D grid this builds
-// 2 x 2 x 2 cubes (on a 2D grid 4 x 2 rectangles): the iterates' rows are balls of the
-// grid graph, and blocks of compact aggregates fill them with fewer partial blocks than
-// the star-shaped BFS aggregates or index-order line segments.
 static void aggregate_order_compact(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
-                                    int64_t n, int size, const std::vector<int64_t> &bounds,
-                                    std::vector<int64_t> &perm) {
+                                    int64_t lo, int64_t hi, int size, std::vector<int64_t> &perm) {
+  const int64_t m = hi - lo;
   perm.clear();
-  perm.reserve((size_t)n);
-  std::vector<uint8_t> used((size_t)n, 0);
-  std::vector<int32_t> cnt((size_t)n, 0), firstm((size_t)n, 0);  // per candidate: edges, first member
+  perm.reserve((size_t)m);
+  std::vector<uint8_t> used((size_t)m, 0);
+  std::vector<int32_t> cnt((size_t)m, 0), firstm((size_t)m, 0);  // per candidate: edges, first member
   std::vector<int64_t> agg, cand;
-  int g = 0;
-  for (int64_t s = 0; s < n; s++) {
-    if (used[s]) continue;
-    while (s >= bounds[g + 1]) g++;
-    const int64_t lo = bounds[g], hi = bounds[g + 1];
+  for (int64_t s = lo; s < hi; s++) {
+    if (used[s - lo]) continue;
     agg.clear();
     cand.clear();
     int64_t v = s;
     for (;;) {
-      used[v] = 1;
-      const int m = (int)agg.size();
+      used[v - lo] = 1;
+      const int mi = (int)agg.size();
       agg.push_back(v);
       if ((int)agg.size() >= size) break;
       for (int64_t p = rp[v]; p < rp[v + 1]; p++) {  // v's edges raise its neighbours' counts
         const int64_t u = col[p];
-        if (used[u] || u < lo || u >= hi) continue;
-        if (cnt[u] == 0) {
-          firstm[u] = m;
+        if (u < lo || u >= hi || used[u - lo]) continue;
+        if (cnt[u - lo] == 0) {
+          firstm[u - lo] = mi;
           cand.push_back(u);
         }
-        cnt[u]++;
+        cnt[u - lo]++;
       }
       int64_t best = -1;
       for (int64_t u : cand) {
-        if (used[u]) continue;
-        if (best < 0 || cnt[u] > cnt[best] ||
-            (cnt[u] == cnt[best] && (firstm[u] < firstm[best] || (firstm[u] == firstm[best] && u < best))))
+        if (used[u - lo]) continue;
+        const int64_t ul = u - lo, bl = best - lo;
+        if (best < 0 || cnt[ul] > cnt[bl] ||
+            (cnt[ul] == cnt[bl] && (firstm[ul] < firstm[bl] || (firstm[ul] == firstm[bl] && u < best))))
           best = u;
       }
       if (best < 0) break;
       v = best;
     }
-    for (int64_t u : cand) cnt[u] = 0;
+    for (int64_t u : cand) cnt[u - lo] = 0;
     perm.insert(perm.end(), agg.begin(), agg.end());
   }
+}
+
+// Block-fill proxy of an order of the rows [lo, hi): for sampled block rows (8 consecutive
+// positions of the order), the distinct column blocks covered by the radius-rad neighbourhood
+// of their 8 rows in H's graph -- the iterates' rows are such neighbourhoods, rad ~ 0.8 M the
+// reach of the filtered Taylor phase -- counting only rows of the range (so the result
+// depends on the range alone).  Sampling stops after ~2e6 visited rows.  perm = null: index
+// order.
+static int64_t sampled_blocks(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
+                              int64_t lo, int64_t hi, const std::vector<int64_t> *perm, int rad) {
+  const int64_t m = hi - lo, nbt = (m + 7) / 8, step = std::max<int64_t>(1, nbt / 512);
+  std::vector<int64_t> pos;  // position in the order of each row of the range
+  if (perm) {
+    pos.resize((size_t)m);
+    for (int64_t i = 0; i < m; i++) pos[(*perm)[i] - lo] = i;
+  }
+  std::vector<int32_t> mark((size_t)m, -1);
+  std::vector<int64_t> fr, nx, blk;
+  int64_t total = 0, visited = 0;
+  int32_t stamp = 0;
+  for (int64_t b = 0; b < nbt && visited < 2000000; b += step, stamp++) {
+    fr.clear();
+    blk.clear();
+    for (int64_t i = 8 * b; i < std::min<int64_t>(m, 8 * b + 8); i++) {
+      const int64_t v = perm ? (*perm)[i] : lo + i;
+      if (mark[v - lo] != stamp) {
+        mark[v - lo] = stamp;
+        fr.push_back(v);
+        blk.push_back(i >> 3);
+      }
+    }
+    for (int r = 0; r < rad; r++) {
+      nx.clear();
+      for (int64_t v : fr)
+        for (int64_t p = rp[v]; p < rp[v + 1]; p++) {
+          const int64_t u = col[p];
+          if (u < lo || u >= hi || mark[u - lo] == stamp) continue;
+          mark[u - lo] = stamp;
+          nx.push_back(u);
+          blk.push_back((perm ? pos[u - lo] : u - lo) >> 3);
+        }
+      visited += (int64_t)nx.size();
+      fr.swap(nx);
+    }
+    std::sort(blk.begin(), blk.end());
+    total += std::unique(blk.begin(), blk.end()) - blk.begin();
+  }
+  return total;
 }
 
 static void cluster_order(const std::vector<int64_t> &rp, const std::vector<int32_t> &col,
@@ -2156,6 +2198,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
     CK(cudaEventRecord(P.ev_pattern, st));
     P.order_pending = true;
     P.bg = std::thread([&P]() {
+      const auto b0 = std::chrono::steady_clock::now();
       try {
         CK(cudaSetDevice(P.dev));
         CK(cudaStreamWaitEvent(P.bg_st, P.ev_pattern, 0));
@@ -2166,8 +2209,79 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
         if (F.nnz)
           CK(cudaMemcpyAsync(hcol.data(), F.col.p, F.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, P.bg_st));
         CK(cudaStreamSynchronize(P.bg_st));
+        auto lap = [&](const char *what) {
+          if (getenv("SEXPM_PLAN_LOG"))
+            fprintf(stderr, "[sexpm order] %-28s %8.1f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - b0).count());
+        };
+        lap("pattern D2H");
         std::vector<int32_t> &ord = P.h_order;
-        cluster_order(hrp, hcol, P.row_begin, P.row_end, 1024, ord);
+        // the cluster order of this rank's rows runs on its own host thread, beside the
+        // aggregate candidates below
+        std::thread t_clu([&] { cluster_order(hrp, hcol, P.row_begin, P.row_end, 1024, ord); });
+        // the aggregate order: for every rank range whose rows can be columns of this rank's
+        // T^_0 rows (within M x H's bandwidth, Lemma 3.1), both candidates built and judged
+        // on that range alone (so every rank takes the same decision for a range)
+        const bool want_agg = P.o.sq_order == 1 && P.N >= 1;
+        std::vector<std::vector<int64_t>> range_perm;
+        std::vector<int> range_kind;
+        std::vector<int> needed;
+        std::vector<int64_t> range_blocks;  // per needed range: sampled blocks idx, BFS, compact
+        if (want_agg) {
+          int64_t lH = 0;
+          for (int64_t r = 0; r < P.n; r++)
+            if (hrp[r + 1] > hrp[r])
+              lH = std::max<int64_t>(lH, std::max<int64_t>(std::llabs((int64_t)hcol[hrp[r]] - r),
+                                                           std::llabs((int64_t)hcol[hrp[r + 1] - 1] - r)));
+          // columns of this rank's iterates, and of the halo rows it receives, stay within
+          // 2^(N+1) M l(H) of its rows (Lemma 3.1: l(T^_0) <= M l(H), each squaring at most
+          // doubles it, a halo row is within l(T^_{i-1}) of the range)
+          const int64_t reach = (int64_t)std::min<double>((double)P.n, std::ldexp((double)std::max(P.M, 1) * (double)lH, P.N + 1));
+          const int64_t wlo = std::max<int64_t>(0, P.row_begin - reach), whi = std::min<int64_t>(P.n, P.row_end + reach);
+          for (int g = 0; g < P.world; g++)
+            if (P.bounds[g] < whi && P.bounds[g + 1] > wlo && P.bounds[g + 1] > P.bounds[g]) needed.push_back(g);
+          range_perm.assign(needed.size(), {});
+          range_kind.assign(needed.size(), 0);
+          range_blocks.assign(needed.size() * 3, 0);
+          const int rad = std::max(3, std::min(16, (int)lround(0.8 * P.M)));
+          std::vector<std::thread> ts;
+          for (size_t q = 0; q < needed.size(); q++)
+            ts.emplace_back([&, q] {
+              const int g = needed[q];
+              const int64_t lo = P.bounds[g], hi = P.bounds[g + 1];
+              // judged on a window of <= 2^16 rows in the middle of the range (8-aligned),
+              // then only the chosen candidate is built for the whole range
+              const int64_t wn = std::min<int64_t>(hi - lo, 65536);
+              const int64_t wlo = std::min<int64_t>(hi - wn, lo + (((hi - lo - wn) / 2) & ~(int64_t)7));
+              const int64_t whi = wlo + wn;
+              std::vector<int64_t> cb, cc;
+              std::thread tb([&] { aggregate_order(hrp, hcol, wlo, whi, 8, cb); });
+              aggregate_order_compact(hrp, hcol, wlo, whi, 8, cc);
+              tb.join();
+              int64_t bl[3];
+              std::thread p0([&] { bl[0] = sampled_blocks(hrp, hcol, wlo, whi, nullptr, rad); });
+              std::thread p1([&] { bl[1] = sampled_blocks(hrp, hcol, wlo, whi, &cb, rad); });
+              bl[2] = sampled_blocks(hrp, hcol, wlo, whi, &cc, rad);
+              p0.join();
+              p1.join();
+              const int pick = bl[2] < bl[1] ? 1 : 0;
+              const int64_t b_agg = pick ? bl[2] : bl[1];
+              for (int k = 0; k < 3; k++) range_blocks[3 * q + k] = bl[k];
+              if (10 * b_agg <= 9 * bl[0]) {
+                if (wlo == lo && whi == hi) {
+                  range_perm[q].swap(pick ? cc : cb);
+                } else if (pick) {
+                  aggregate_order_compact(hrp, hcol, lo, hi, 8, range_perm[q]);
+                } else {
+                  aggregate_order(hrp, hcol, lo, hi, 8, range_perm[q]);
+                }
+                range_kind[q] = 1 + pick;
+              }
+            });
+          for (auto &t : ts) t.join();
+        }
+        t_clu.join();
+        lap("cluster order + aggregates");
         // block rows (8 rows) of the block kernel, in the order their first row appears
         std::vector<int32_t> &bo = P.h_border;
         bo.clear();
@@ -2185,67 +2299,31 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
           CK(cudaMemcpyAsync(P.block_order.p, bo.data(), bo.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
         if (!ord.empty())
           CK(cudaMemcpyAsync(P.proc_order.p, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice, P.bg_st));
-        if (P.o.sq_order == 1 && P.N >= 1) {  // aggregate order of the squarings (per rank range)
-          // candidates: BFS aggregates and compact aggregates; kept only where it fills the
-          // 8x8 blocks better than index order: for a sample of block rows, count the distinct
-          // column blocks covered by the radius-r neighbourhood of their 8 rows (the iterates'
-          // rows are such neighbourhoods; r ~ 0.8 M, the reach of the filtered Taylor phase)
-          std::vector<int64_t> cand[2];
-          aggregate_order(hrp, hcol, P.n, 8, P.bounds, cand[0]);
-          aggregate_order_compact(hrp, hcol, P.n, 8, P.bounds, cand[1]);
-          const int rad = std::max(3, std::min(16, (int)lround(0.8 * P.M)));
-          const int64_t nbt = (P.n + 7) / 8, step = std::max<int64_t>(1, nbt / 512);
-          std::vector<int32_t> mark((size_t)P.n, -1), fr, nx;
-          std::vector<int64_t> blk, hinv((size_t)P.n);
-          auto proxy = [&](const std::vector<int64_t> *perm) {
-            if (perm)
-              for (int64_t i = 0; i < P.n; i++) hinv[(*perm)[i]] = i;
-            int64_t total = 0;
-            int32_t stamp = 0;
-            std::fill(mark.begin(), mark.end(), -1);
-            for (int64_t g = 0; g < nbt; g += step, stamp++) {
-              fr.clear();
-              for (int64_t i = 8 * g; i < std::min<int64_t>(P.n, 8 * g + 8); i++) {
-                const int32_t v = (int32_t)(perm ? (*perm)[i] : i);
-                if (mark[v] != stamp) {
-                  mark[v] = stamp;
-                  fr.push_back(v);
-                }
-              }
-              blk.clear();
-              for (int32_t v : fr) blk.push_back((perm ? hinv[v] : v) >> 3);
-              for (int r = 0; r < rad; r++) {
-                nx.clear();
-                for (int32_t v : fr)
-                  for (int64_t p = hrp[v]; p < hrp[v + 1]; p++) {
-                    const int32_t u = hcol[p];
-                    if (mark[u] != stamp) {
-                      mark[u] = stamp;
-                      nx.push_back(u);
-                      blk.push_back((perm ? hinv[u] : u) >> 3);
-                    }
-                  }
-                fr.swap(nx);
-              }
-              std::sort(blk.begin(), blk.end());
-              total += std::unique(blk.begin(), blk.end()) - blk.begin();
-            }
-            return total;
-          };
-          const int64_t b_idx = proxy(nullptr), b_bfs = proxy(&cand[0]), b_cmp = proxy(&cand[1]);
-          const int pick = b_cmp < b_bfs ? 1 : 0;
-          const int64_t b_agg = pick ? b_cmp : b_bfs;
-          if (getenv("SEXPM_PLAN_LOG"))
-            fprintf(stderr, "[sexpm plan] aggregate order (radius %d): sampled blocks index %lld, BFS %lld, compact %lld -> %s\n",
-                    rad, (long long)b_idx, (long long)b_bfs, (long long)b_cmp,
-                    10 * b_agg <= 9 * b_idx ? (pick ? "compact" : "BFS") : "index order");
+        if (want_agg) {
+          // assemble the global permutation: each needed range relabelled within itself,
+          // identity elsewhere (those labels never occur in this rank's data)
           P.h_tperm.clear();
           P.agg_kind = 0;
-          if (10 * b_agg <= 9 * b_idx) {
-            P.h_tperm.swap(cand[pick]);
-            P.agg_kind = 1 + pick;
+          bool any = false;
+          for (size_t q = 0; q < needed.size(); q++) {
+            if (getenv("SEXPM_PLAN_LOG"))
+              fprintf(stderr, "[sexpm plan] aggregate order, rows [%lld, %lld): sampled blocks index %lld, BFS %lld, compact %lld -> %s\n",
+                      (long long)P.bounds[needed[q]], (long long)P.bounds[needed[q] + 1], (long long)range_blocks[3 * q],
+                      (long long)range_blocks[3 * q + 1], (long long)range_blocks[3 * q + 2],
+                      range_kind[q] == 0 ? "index order" : (range_kind[q] == 1 ? "BFS" : "compact"));
+            if (range_kind[q]) any = true;
+            if (needed[q] == P.rank) P.agg_kind = range_kind[q];
           }
-          for (int64_t i = 0; i < (int64_t)P.h_tperm.size(); i++) hinv[P.h_tperm[i]] = i;
+          std::vector<int64_t> hinv;
+          if (any) {
+            P.h_tperm.resize((size_t)P.n);
+            for (int64_t i = 0; i < P.n; i++) P.h_tperm[i] = i;
+            for (size_t q = 0; q < needed.size(); q++)
+              if (range_kind[q])
+                std::copy(range_perm[q].begin(), range_perm[q].end(), P.h_tperm.begin() + P.bounds[needed[q]]);
+            hinv.resize((size_t)P.n);
+            for (int64_t i = 0; i < P.n; i++) hinv[P.h_tperm[i]] = i;
+          }
           // block rows of the relabelled matrix in the locality order of H's clusters: each
           // aggregate ranked by the earliest position of its rows in `ord`
           if (!P.h_tperm.empty() && P.world == 1) {
@@ -2279,7 +2357,9 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
             CK(cudaStreamSynchronize(P.bg_st));  // host vectors are local
           }
         }
+        lap("done");
         CK(cudaEventRecord(P.ev_order, P.bg_st));
+        P.order_host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - b0).count();
       } catch (const SxError &e) {
         P.bg_err = e.msg.empty() ? "order thread failed" : e.msg;
       } catch (...) {
@@ -2557,6 +2637,8 @@ static void do_run(sexpm_plan_s &P) {
     S.cache_releases = cache::releases - P.cache0[2];
     S.cache_bytes_cached = cache::bytes_cached;
     S.cache_bytes_allocated = cache::bytes_allocated;
+    S.ms_order_host = P.order_host_ms;
+    S.ms_order_wait = P.order_wait_ms;
   }
   if (P.o.reorder) {  // N3: E = P^T E' P (row r <- row inv[r], col c' -> perm[c'])
     DCsr &spare = (&P.T == &P.E) ? P.Tn : (P.T.nnz >= P.E.nnz ? P.T : P.Tn);  // free iterates

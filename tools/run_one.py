@@ -40,7 +40,8 @@ def main():
             f"{[round(float(x), 1) for x in st['sq_numeric_ms'][1:N + 1]]} sq_first "
             f"{[round(float(x), 1) for x in st['sq_first_ms'][1:N + 1]]} sq_fallback "
             f"{[int(x) for x in st['sq_fallback_rows'][1:N + 1]]} cache hits/misses/releases "
-            f"{st['cache_hits']}/{st['cache_misses']}/{st['cache_releases']} cached "
+            f"{st['cache_hits']}/{st['cache_misses']}/{st['cache_releases']} order host/wait "
+            f"{st['ms_order_host']:.1f}/{st['ms_order_wait']:.1f} ms cached "
             f"{st['cache_bytes_cached'] / 1e9:.1f} GB allocated {st['cache_bytes_allocated'] / 1e9:.1f} GB\n")
         sys.stderr.write(f"  taylor_numeric_ms {[round(float(x), 1) for x in st['taylor_numeric_ms'][2:int(st['M_eff']) + 1]]} "
                          f"taylor_fallback {[int(x) for x in st['taylor_fallback_rows'][2:int(st['M_eff']) + 1]]}\n")

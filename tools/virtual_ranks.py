@@ -57,7 +57,8 @@ def main():
                       "sq_exchange_ms": [round(float(x), 2) for x in st["sq_exchange_ms"][1:N + 1]],
                       "sq_kernel_ms": [round(float(x), 2) for x in st["sq_kernel_ms"][1:N + 1]],
                       "sq_fallback_rows": [int(x) for x in st["sq_fallback_rows"][1:N + 1]],
-                      "sq_order_used": int(st["sq_order_used"]), "nnz_E_rank": int(st["nnz_out"])}
+                      "sq_order_used": int(st["sq_order_used"]), "nnz_E_rank": int(st["nnz_out"]),
+                      "order_host_ms": float(st["ms_order_host"]), "order_wait_ms": float(st["ms_order_wait"])}
 
         ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(W)]
         for t in ts:
