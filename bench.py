@@ -484,6 +484,47 @@ def main():
                             "nnz_E": int(sc["nnz_out"])}
             del rc
 
+    # ---------------- config S (HBM-roofline case, 1D rows) ----------------
+    # 0.5 tridiag(1,-2,1) at n = 2^25 (2^26 exceeds the device memory with the staging pool
+    # and the padded Taylor accumulator), built on the device; one warm-up, one timed run
+    config_s = None
+    if world == 1 and not args.no_others:
+        ns = 1 << 25
+        r_ = torch.arange(ns, device=dev, dtype=torch.int64)
+        cnt_ = torch.full((ns,), 3, dtype=torch.int64, device=dev)
+        cnt_[0] = 2
+        cnt_[-1] = 2
+        rp_s = torch.zeros(ns + 1, dtype=torch.int64, device=dev)
+        rp_s[1:] = torch.cumsum(cnt_, 0)
+        cols_ = torch.stack([r_ - 1, r_, r_ + 1], 1).reshape(-1)
+        vals_ = torch.tensor([0.5, -1.0, 0.5], dtype=torch.float64, device=dev).repeat(ns)
+        keep_ = (cols_ >= 0) & (cols_ < ns)
+        ci_s = cols_[keep_].to(torch.int32).contiguous()
+        va_s = vals_[keep_].contiguous()
+        del r_, cnt_, cols_, vals_, keep_
+        for rep_i in range(2):
+            b0 = torch.cuda.Event(enable_timing=True)
+            b1 = torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            p = B.Plan(ns, rp_s, ci_s, va_s, args.eps_tol, stream=stream)
+            p.run_only()
+            b1.record(stream)
+            torch.cuda.synchronize()
+            ss = p.stats()
+            p.close()
+        Ns, Ms = int(ss["N"]), int(ss["M"])
+        ty = [i for i in range(2, Ms + 1) if ss["taylor_numeric_ms"][i] > 0]
+        tyb = sum(float(ss["taylor_numeric_bytes"][i]) for i in ty)
+        tym = sum(float(ss["taylor_numeric_ms"][i]) for i in ty)
+        config_s = {"workload": f"config S: 0.5 tridiag(1,-2,1), n = 2^25 (2^26 does not fit in 178 GB)",
+                    "M": Ms, "N": Ns, "nnz_E": int(ss["nnz_out"]), "ms_expm": b0.elapsed_time(b1),
+                    "phase_ms": {"plan": float(ss["ms_plan"]), "taylor": float(ss["ms_taylor"]),
+                                 "squaring": float(ss["ms_squaring"]), "finalize": float(ss["ms_finalize"])},
+                    "taylor_kernels_ms": tym, "taylor_kernels_compulsory_gbs": tyb / tym / 1e6 if tym else None,
+                    "sq_kernel_ms": [float(x) for x in ss["sq_kernel_ms"][1:Ns + 1]]}
+        del rp_s, ci_s, va_s
+        B.sexpm_release_cache()
+
     # ---------------- the CPU sample on the GPU (same work as cpu_baseline / reference) ------
     same_sample = None
     if world == 1:
@@ -584,6 +625,7 @@ def main():
         "n3_reorder": n3,
         "n4_graph": n4,
         "other_configs": others,
+        "config_s": config_s,
         "same_sample": same_sample,
         "fp64_peak_measured": fp64_peak,
     }
