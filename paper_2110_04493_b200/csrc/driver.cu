@@ -1776,16 +1776,16 @@ static void permute_csr(sexpm_plan_s &P, const CsrView &A, const int64_t *rowmap
   C.val.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
   launch_perm_count(A.rp, rowmap, n, w.cnt.p, st);
   launch_exclusive_scan(w.cnt.p, n, C.rp.p, w.scan_tmp.p, st);
-  w.pool_col.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
-  w.pool_val.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
-  launch_perm_write(A, rowmap, colmap, n, C.rp.p, w.pool_col.p, w.pool_val.p, st);
   w.i64tmp.ensure(8, st);
   launch_reduce_max_i64(w.cnt.p, n, w.i64tmp.p + 0, st);
-  if (d2h(w.i64tmp.p + 0, st) <= kSortRowsCap) {  // short rows: warp bitonic sort
-    launch_sort_rows(C.rp.p, n, w.pool_col.p, w.pool_val.p, C.col.p, C.val.p, st);
+  if (d2h(w.i64tmp.p + 0, st) <= kSortRowsCap) {  // short rows: relabel and sort in one pass
+    launch_perm_sort_rows(A, rowmap, colmap, n, C.rp.p, C.col.p, C.val.p, st);
     CK(cudaGetLastError());
     return;
   }
+  w.pool_col.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
+  w.pool_val.ensure((size_t)std::max<int64_t>(A.nnz, 1), st);
+  launch_perm_write(A, rowmap, colmap, n, C.rp.p, w.pool_col.p, w.pool_val.p, st);
   const size_t tb = seg_sort_temp_bytes(A.nnz, n, C.rp.p);
   DBuf<unsigned char> tmp;
   tmp.alloc(tb + 256, st);

@@ -3561,9 +3561,15 @@ namespace sx {
 // per row); otherwise a bitonic network over (column << 32 | position) in shared memory.
 constexpr int kSortCap = 1024, kSortWarps = 8;
 constexpr int kSortWords = 2048;  // bitmap words per warp (65536 columns of span)
+// PERM: output row r is input row rowmap[r] (input row pointers irp), every key mapped
+// through colmap, output rows at rp -- the relabelling and the sort in one pass
+template <bool PERM>
 __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp, int64_t n,
                                                                const int32_t *kin, const double *vin,
-                                                               int32_t *kout, double *vout) {
+                                                               int32_t *kout, double *vout,
+                                                               const int64_t *irp = nullptr,
+                                                               const int64_t *rowmap = nullptr,
+                                                               const int64_t *colmap = nullptr) {
   extern __shared__ unsigned long long sbuf[];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   unsigned long long *buf = sbuf + wi * kSortCap;                       // bitonic keys
@@ -3572,13 +3578,14 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
     const int64_t p0 = rp[r];
+    const int64_t q0 = PERM ? irp[rowmap[r]] : p0;  // the input row
     const int len = (int)(rp[r + 1] - p0);
     int kmin = INT32_MAX, kmax = -1;
     int kr[kSortCap / 32];  // the row's keys, loaded once (len <= kSortCap)
 #pragma unroll
     for (int t = 0; t < kSortCap / 32; t++) {
       const int i = lane + 32 * t;
-      kr[t] = i < len ? kin[p0 + i] : 0;
+      kr[t] = i < len ? (PERM ? (int)colmap[kin[q0 + i]] : kin[p0 + i]) : 0;
       if (i < len) {
         kmin = min(kmin, kr[t]);
         kmax = max(kmax, kr[t]);
@@ -3619,7 +3626,7 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
           const int k = kr[t], d = k - kmin;
           const int pos = pref[d >> 5] + __popc(bits[d >> 5] & ((1u << (d & 31)) - 1u));
           kout[p0 + pos] = k;
-          vout[p0 + pos] = vin[p0 + lane + 32 * t];
+          vout[p0 + pos] = vin[q0 + lane + 32 * t];
         }
       __syncwarp();
       continue;
@@ -3627,7 +3634,7 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
     int P = 32;
     while (P < len) P <<= 1;
     for (int i = lane; i < P; i += 32)
-      buf[i] = i < len ? ((unsigned long long)(unsigned)kin[p0 + i] << 32) | (unsigned)i : ~0ull;
+      buf[i] = i < len ? ((unsigned long long)(unsigned)(PERM ? (int)colmap[kin[q0 + i]] : kin[p0 + i]) << 32) | (unsigned)i : ~0ull;
     __syncwarp();
     for (int k = 2; k <= P; k <<= 1)
       for (int j = k >> 1; j > 0; j >>= 1) {
@@ -3646,7 +3653,7 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
     for (int i = lane; i < len; i += 32) {
       const unsigned long long e = buf[i];
       kout[p0 + i] = (int32_t)(e >> 32);
-      vout[p0 + i] = vin[p0 + (int64_t)(e & 0xFFFFFFFFull)];
+      vout[p0 + i] = vin[q0 + (int64_t)(e & 0xFFFFFFFFull)];
     }
     __syncwarp();
   }
@@ -3655,10 +3662,19 @@ void launch_sort_rows(const int64_t *rp, int64_t n, const int32_t *kin, const do
                       double *vout, cudaStream_t st) {
   if (n == 0) return;
   const int smem = kSortWarps * kSortCap * 8 + kSortWarps * kSortWords * 2;
-  cudaFuncSetAttribute(k_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_sort_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
-  k_sort_rows<<<(int)std::min<int64_t>((n + kSortWarps - 1) / kSortWarps, 148 * 3), kSortWarps * 32, smem, st>>>(
+  k_sort_rows<false><<<(int)std::min<int64_t>((n + kSortWarps - 1) / kSortWarps, 148 * 3), kSortWarps * 32, smem, st>>>(
       rp, n, kin, vin, kout, vout);
+}
+void launch_perm_sort_rows(const CsrView &A, const int64_t *rowmap, const int64_t *colmap, int64_t n,
+                           const int64_t *rp_out, int32_t *col_out, double *val_out, cudaStream_t st) {
+  if (n == 0) return;
+  const int smem = kSortWarps * kSortCap * 8 + kSortWarps * kSortWords * 2;
+  cudaFuncSetAttribute(k_sort_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_sort_rows<true><<<(int)std::min<int64_t>((n + kSortWarps - 1) / kSortWarps, 148 * 3), kSortWarps * 32, smem, st>>>(
+      rp_out, n, A.col, A.val, col_out, val_out, A.rp, rowmap, colmap);
 }
 }  // namespace sx
 

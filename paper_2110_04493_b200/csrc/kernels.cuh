@@ -262,6 +262,10 @@ void launch_rows_equal(const CsrView &A, const CsrView &B, int *flag, cudaStream
 constexpr int kSortRowsCap = 1024;
 void launch_sort_rows(const int64_t *rp, int64_t n, const int32_t *kin, const double *vin, int32_t *kout,
                       double *vout, cudaStream_t st);
+// relabel + sort in one pass: output row r = input row rowmap[r] with keys colmap[k], sorted
+// (rows <= kSortRowsCap entries)
+void launch_perm_sort_rows(const CsrView &A, const int64_t *rowmap, const int64_t *colmap, int64_t n,
+                           const int64_t *rp_out, int32_t *col_out, double *val_out, cudaStream_t st);
 // K5s: Taylor product for short rows (thread per row, output span <= 64 columns)
 void launch_taylor_dia_short(const NumericArgs &a, const DiaView &D, int32_t *fail_rows, int *fail_count,
                              cudaStream_t st);
