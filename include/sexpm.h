@@ -243,8 +243,11 @@ int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *
  * X.  m >= 0, steps >= 1.  For m >= 32 every Y entry is the sum over the row's entries in
  * ascending column order with separately rounded products (bit-identical to the oracle's
  * or_spmm); for m < 32 the row's entries are split over lane groups and combined by a fixed
- * tree (deterministic).  steps > 1 uses two plan-owned n x m buffers.  Single GPU only
- * (world 1, else SEXPM_EINVAL); SEXPM_ESTATE before sexpm_run.  Synchronises the stream. */
+ * tree (deterministic).  steps > 1 uses two plan-owned n x m buffers.  With several ranks
+ * (collective: every rank calls it with the same m and steps): X and Y hold this rank's rows
+ * [row_begin, row_end); each step exchanges the rows of the current block within E's
+ * bandwidth (Lemma 3.1) with the peers through the plan's communicator, then
+ * multiplies the rank's rows of E.  SEXPM_ESTATE before sexpm_run.  Synchronises the stream. */
 int sexpm_apply(sexpm_plan_t p, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
                 int32_t steps);
 

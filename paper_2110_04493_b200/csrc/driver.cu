@@ -2973,31 +2973,102 @@ int sexpm_apply(sexpm_plan_t p, int64_t m, const double *X, int64_t ldx, double 
   ABI_BEGIN
   REQUIRE(p, SEXPM_EINVAL, "null plan");
   REQUIRE(p->have_result, SEXPM_ESTATE, "no result: call sexpm_run first");
-  REQUIRE(p->world == 1, SEXPM_EINVAL, "sexpm_apply is single-GPU (multi-GPU needs X halos)");
   REQUIRE(m >= 0 && steps >= 1 && ldx >= m && ldy >= m, SEXPM_EINVAL, "bad m / ld / steps");
   REQUIRE(m == 0 || (X && Y), SEXPM_EINVAL, "null X or Y");
-  const int64_t n = p->E.nrows;
+  sexpm_plan_s &P = *p;
+  const int64_t n = P.E.nrows;  // this rank's rows
   REQUIRE(m == 0 || X + (n - 1) * ldx + m <= Y || Y + (n - 1) * ldy + m <= X, SEXPM_EINVAL,
           "X and Y overlap");
-  if (m == 0 || n == 0) return SEXPM_OK;
-  const CsrView Ev = p->E.view();
+  if (P.world == 1 && (m == 0 || n == 0)) return SEXPM_OK;
+  const CsrView Ev = P.E.view();
+  cudaStream_t st = P.st;
+  if (P.world == 1) {
+    const double *src = X;
+    int64_t lds = ldx;
+    for (int s = 1; s <= steps; s++) {
+      double *dst = Y;
+      int64_t ldd = ldy;
+      if (s < steps) {
+        DBuf<double> &b = P.apply_buf[s & 1];
+        b.ensure((size_t)n * (size_t)m, st);
+        dst = b.p;
+        ldd = m;
+      }
+      launch_spmm(Ev, m, src, lds, dst, ldd, st);
+      CK(cudaGetLastError());
+      src = dst;
+      lds = ldd;
+    }
+    CK(cudaStreamSynchronize(st));
+    return SEXPM_OK;
+  }
+  // several ranks (collective): E's rows of this rank reach the columns [r0 - l2, r1 + l1) of
+  // X (Lemma 3.1 with E's bandwidth, measured here); every step assembles those rows of the
+  // current block -- own rows copied, the others received from the peers that own them -- and
+  // multiplies (global column indices address the assembled block shifted by its first row)
+  const int W = P.world, R = P.rank;
+  const int64_t r0 = P.row_begin, r1 = P.row_end;
+  Workspace &w = P.ws;
+  w.rs.ensure((size_t)std::max<int64_t>(n, 1), st);
+  w.l1r.ensure((size_t)std::max<int64_t>(n, 1), st);
+  w.l2r.ensure((size_t)std::max<int64_t>(n, 1), st);
+  w.i64tmp.ensure(8, st);
+  int64_t bw[2] = {0, 0};
+  if (n) {
+    launch_row_stats(Ev, w.rs.p, w.l1r.p, w.l2r.p, st);
+    launch_reduce_max_i64(w.l1r.p, n, w.i64tmp.p + 0, st);
+    launch_reduce_max_i64(w.l2r.p, n, w.i64tmp.p + 1, st);
+    CK(cudaMemcpyAsync(bw, w.i64tmp.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  const int64_t l1 = (int64_t)allmax(P, (double)bw[0]), l2 = (int64_t)allmax(P, (double)bw[1]);
+  int64_t need_lo, need_hi;
+  halo_need(P.bounds.data(), R, P.n, l1, l2, need_lo, need_hi);
+  std::vector<int64_t> rlo(W), rhi(W), slo(W), shi(W);
+  halo_ranges_host(W, R, P.bounds.data(), P.n, l1, l2, rlo.data(), rhi.data());
+  for (int h = 0; h < W; h++) {
+    std::vector<int64_t> lo(W), hi(W);
+    halo_ranges_host(W, h, P.bounds.data(), P.n, l1, l2, lo.data(), hi.data());
+    slo[h] = lo[R];
+    shi[h] = hi[R];
+  }
+  const size_t rowb = (size_t)m * sizeof(double);
+  DBuf<double> xh, xc;  // the assembled rows [need_lo, need_hi) and my rows, both ld = m
+  xh.alloc((size_t)std::max<int64_t>(need_hi - need_lo, 1) * (size_t)std::max<int64_t>(m, 1), st);
+  xc.alloc((size_t)std::max<int64_t>(n, 1) * (size_t)std::max<int64_t>(m, 1), st);
   const double *src = X;
   int64_t lds = ldx;
   for (int s = 1; s <= steps; s++) {
+    if (m && n) {
+      CK(cudaMemcpy2DAsync(xc.p, rowb, src, (size_t)lds * sizeof(double), rowb, (size_t)n,
+                           cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(xh.p + (size_t)(r0 - need_lo) * m, xc.p, (size_t)n * rowb,
+                         cudaMemcpyDeviceToDevice, st));
+    }
+    std::vector<Transport::Xfer> sends, recvs;
+    for (int h = 0; h < W; h++) {
+      if (h == R) continue;
+      if (shi[h] > slo[h])
+        sends.push_back({h, xc.p + (size_t)(slo[h] - r0) * m, nullptr, (size_t)(shi[h] - slo[h]) * rowb});
+      if (rhi[h] > rlo[h])
+        recvs.push_back({h, nullptr, xh.p + (size_t)(rlo[h] - need_lo) * m, (size_t)(rhi[h] - rlo[h]) * rowb});
+    }
+    P.tr->exchange(sends, recvs, st);
     double *dst = Y;
     int64_t ldd = ldy;
     if (s < steps) {
-      DBuf<double> &b = p->apply_buf[s & 1];
-      b.ensure((size_t)n * (size_t)m, p->st);
+      DBuf<double> &b = P.apply_buf[s & 1];
+      b.ensure((size_t)std::max<int64_t>(n, 1) * (size_t)std::max<int64_t>(m, 1), st);
       dst = b.p;
       ldd = m;
     }
-    launch_spmm(Ev, m, src, lds, dst, ldd, p->st);
+    // X addressed by global column c at xh + (c - need_lo) m
+    if (m && n) launch_spmm(Ev, m, xh.p - (ptrdiff_t)need_lo * m, m, dst, ldd, st);
     CK(cudaGetLastError());
     src = dst;
     lds = ldd;
   }
-  CK(cudaStreamSynchronize(p->st));
+  CK(cudaStreamSynchronize(st));
   ABI_END
 }
 

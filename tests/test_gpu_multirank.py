@@ -135,3 +135,59 @@ def test_virtual_ranks_equal_single_rank(B):
     assert (st["M"], st["N"]) == (st1[0]["M"], st1[0]["N"])
     ok, res = parity(Eg, E1, max(st["sq_tau"][st["N"]], st1[0]["sq_tau"][st["N"]], 1e-300))
     assert ok, res
+
+
+@pytest.mark.parametrize("W,steps,m", [(2, 1, 1), (2, 3, 5), (3, 2, 33), (4, 1, 64)])
+def test_virtual_ranks_apply(B, W, steps, m):
+    """N1 apply on the row partition (Y = E^steps X, each rank its rows of X and Y; every step
+    exchanges the X rows within E's bandwidth): equals the oracle's SpMM of the assembled E
+    (P:501-503)."""
+    import torch
+    H = laplacian_2d(36, 30, 1.0, "pm10", seed=11)
+    n = H.n
+    bounds = B.sexpm_partition_rows(n, np.diff(H.rowptr).astype(np.float64) ** 2, W)
+    X = np.random.default_rng(5).standard_normal((n, m))
+    comms = B.sexpm_virtual_comm_create(W)
+    outE, outY, errs = [None] * W, [None] * W, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            r0, r1 = int(bounds[r]), int(bounds[r + 1])
+            Hl = H.rows(r0, r1)
+            with torch.cuda.stream(s):
+                rp, ci, va = to_dev(Hl)
+                Xl = torch.from_numpy(np.ascontiguousarray(X[r0:r1])).cuda()
+                s.synchronize()
+                p = B.Plan(n, rp, ci, va, 1e-16, row_begin=r0, row_end=r1, nccl_comm=comms[r], stream=s)
+                E = p.run()
+                Y = p.apply(Xl, steps=steps)
+                s.synchronize()
+                p.close()
+            outE[r] = [x.cpu().numpy() for x in E]
+            outY[r] = Y.cpu().numpy()
+        except Exception as e:
+            errs.append((r, repr(e)))
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(W)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    for c in comms:
+        B.sexpm_nccl_comm_destroy(c)
+    assert not errs, errs
+    rps, cols, vals, off = [], [], [], 0
+    for r in range(W):
+        rp, ci, va = outE[r]
+        rps.append(rp[:-1] + off if r < W - 1 else rp + off)
+        off += int(rp[-1])
+        cols.append(ci)
+        vals.append(va)
+    E = CSR(n, np.concatenate(rps).astype(np.int64), np.concatenate(cols).astype(np.int32),
+            np.concatenate(vals).astype(np.float64))
+    Yg = np.concatenate(outY, axis=0).reshape(n, m)
+    Yo = O.spmm(E, X, steps=steps)
+    scale = np.abs(Yo).max()
+    assert np.abs(Yg - Yo).max() <= 1e-13 * steps * scale
