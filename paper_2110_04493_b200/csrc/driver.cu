@@ -1363,15 +1363,18 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
     slo[h] = lo[R];
     shi[h] = hi[R];
   }
-  // host copy of my rowptr (needed to size sends)
-  std::vector<int64_t> rp((size_t)T.nrows + 1);
-  CK(cudaMemcpyAsync(rp.data(), T.rp.p, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // my rowptr at the boundaries of the pieces I send (2 values per peer, not the whole rowptr)
+  std::vector<int64_t> rpa(W, 0), rpb(W, 0);
+  for (int h = 0; h < W; h++)
+    if (h != R && shi[h] > slo[h]) {
+      CK(cudaMemcpyAsync(&rpa[h], T.rp.p + (slo[h] - T.row0), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&rpb[h], T.rp.p + (shi[h] - T.row0), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    }
   CK(cudaStreamSynchronize(st));
   // exchange nnz counts of the pieces
   std::vector<double> cnt_send(W, 0.0), all;
   for (int h = 0; h < W; h++)
-    if (shi[h] > slo[h])
-      cnt_send[h] = (double)(rp[shi[h] - T.row0] - rp[slo[h] - T.row0]);
+    if (h != R && shi[h] > slo[h]) cnt_send[h] = (double)(rpb[h] - rpa[h]);
   gather_doubles(P, cnt_send.data(), W, all);  // all[g*W + h] = nnz g sends to h
   int64_t need_lo, need_hi;
   halo_need(P.bounds.data(), R, P.n, l1, l2, need_lo, need_hi);
@@ -1412,7 +1415,7 @@ static void exchange_halo(sexpm_plan_s &P, const DCsr &T, int64_t l1, int64_t l2
     if (shi[h] > slo[h]) {
       int64_t a = slo[h] - T.row0, b = shi[h] - T.row0;
       sends.push_back({h, T.rp.p + a, nullptr, (size_t)(b - a + 1) * sizeof(int64_t)});
-      int64_t na = rp[a], nb = rp[b];
+      int64_t na = rpa[h], nb = rpb[h];
       if (nb > na) {
         sends.push_back({h, T.col.p + na, nullptr, (size_t)(nb - na) * sizeof(int32_t)});
         sends.push_back({h, T.val.p + na, nullptr, (size_t)(nb - na) * sizeof(double)});
