@@ -42,7 +42,8 @@ def main():
            "nnz_E": int(st["nnz_out"]), "phase_ms": {k: float(st["ms_" + k]) for k in ("plan", "taylor", "squaring", "finalize")},
            "wall_s": wall, "taylor_kernel_ms": ms, "taylor_kernel_compulsory_gbs": by / ms / 1e6,
            "sq_kernel_ms": [float(x) for x in st["sq_kernel_ms"][1:N + 1]],
-           "sq_numeric_gbs_compulsory": [float(st["sq_numeric_bytes"][i]) / float(st["sq_numeric_ms"][i]) / 1e6 for i in range(1, N + 1)]}
+           "sq_numeric_gbs_compulsory": [float(st["sq_numeric_bytes"][i]) / float(st["sq_numeric_ms"][i]) / 1e6 for i in range(1, N + 1)],
+           "device_gb_allocated": float(st["cache_bytes_allocated"]) / 1e9, "retries": int(st["retries"])}
     print(json.dumps(out))
 
 
