@@ -99,12 +99,16 @@ typedef struct {
   int32_t kernel;         /* K3 kernel: 0 auto (squarings: the block-sparse kernel on the BSR-8
                              view, 13 = fp64 tensor-core DMMA (default) or 11 = exact DMUL/DADD
                              per exact_products, on one GPU and on a rank's rows inside its halo;
-                             Taylor terms: the diagonal push kernel 7 when H0 has <= 16
-                             distinct diagonal offsets, else the pull over H0^T 6); 3 block
+                             Taylor terms: the offset-window kernel 8 when H0 has <= 16
+                             distinct diagonal offsets whose Minkowski sums up to order M
+                             fit its shared-memory rows (<= 4096 offsets: 1D / 2D
+                             stencils), else the diagonal push kernel 7 when H0 has <= 16
+                             offsets, else the pull over H0^T 6); 3 block
                              window, 5 k-synchronous paged, 6 Taylor pull (Taylor terms only;
                              else 5), 7 Taylor diagonal push (Taylor terms only; else as 0),
+                             8 Taylor offset window (Taylor phase only; else as 0),
                              11 block-sparse exact, 13 block-sparse tensor core (squarings
-                             only; else as 0).  All meet parity; 5, 6, 7 and 11 reproduce the
+                             only; else as 0).  All meet parity; 5, 6, 7, 8 and 11 reproduce the
                              oracle's C~ bit for bit.  Rows a kernel cannot hold fall through
                              11/13 -> 5 -> 3, 7 -> 7 at twice the accumulator slots -> 5 -> 3,
                              6 -> 5 -> 3. */
@@ -184,6 +188,9 @@ typedef struct {
   double ms_order_host;  /* the squarings' locality / aggregate order, computed on a host
                             thread from H's pattern while the Taylor phase runs (wall ms) */
   double ms_order_wait;  /* how long the first squaring waited for it (0 when hidden) */
+  int32_t taylor_window; /* 1: the Taylor phase ran on the offset-window kernel K5w (dense
+                            rows over the Minkowski sums of H0's diagonal offsets); 0: term
+                            by term on the product kernels */
 } sexpm_stats;
 
 /* sizes[0..3] = sizeof(sexpm_options), sizeof(sexpm_stats), sizeof(sexpm_csr_in),

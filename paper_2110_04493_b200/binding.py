@@ -84,7 +84,8 @@ class Stats(C.Structure):
                 ("cache_hits", C.c_int64), ("cache_misses", C.c_int64),
                 ("cache_releases", C.c_int64), ("cache_bytes_cached", C.c_double),
                 ("cache_bytes_allocated", C.c_double), ("sq_order_used", C.c_int32),
-                ("sq_exchange_ms", _F64), ("ms_order_host", C.c_double), ("ms_order_wait", C.c_double)]
+                ("sq_exchange_ms", _F64), ("ms_order_host", C.c_double), ("ms_order_wait", C.c_double),
+                ("taylor_window", C.c_int32)]
 
 
 _lib = None

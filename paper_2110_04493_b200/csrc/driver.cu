@@ -557,6 +557,23 @@ struct sexpm_plan_s {
   bool dia_short_ok = true;  // the previous Taylor term's rows all fitted the short-row kernel K5s
   int dia_slots_max = 1152;  // the most that fit (set at plan time); retry size for rows over dia_slots
   DBuf<int> dia_need;
+  std::vector<int32_t> h_dia_off;  // host copy of dia_off (descending)
+  // K5w offset-window tables (build_window): U = the union of the Minkowski sums W_j of H0's
+  // offsets, j = 1..M; lcnt[j] = |W_j|, ccnt[j] = |W_1 u ... u W_j| (ccnt[0] = 0)
+  struct Win {
+    bool ok = false;
+    int nU = 0, dzero = -1, rw = 0;
+    int64_t pad = 0, npad = 0;
+    std::vector<int> lcnt, ccnt;      // |W_j|, |cum_j| (index j; ccnt[0] = 0)
+    std::vector<int64_t> woff, coff;  // per term: start of its W-indexed / cum-indexed tables
+    DBuf<int32_t> rec;                // TERM records (k_taylor_win), rw int32 per position
+    DBuf<int16_t> mapC, mapW;         // per cum position (T^_0 pass, FINAL)
+    DBuf<int32_t> coffs;
+    DBuf<double> dpad;                // H0's diagonals zero-padded, plus a zero plane
+    DBuf<double> ck_t[2];  // T^_0 checkpoints (position-major), Taylor phase only; the S~
+                           // checkpoints live in Tn.val and E.val (idle until the squarings)
+    DBuf<unsigned long long> cnt, need;
+  } win;
   long long cache0[3] = {0, 0, 0};  // cache counters when the plan was created
   DCsr T, Tn, S, Sn, Bhalo, Ibuf, E;  // persistent (grow-only) iterates
   int32_t retries = 0;
@@ -735,6 +752,41 @@ static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpo
   return true;
 }
 
+// Algorithm 4.1: the scalar threshold recurrence on the host over the staged
+// values of the rows (row_off / row_cnt / pool_val): F = sum of x^2 below the floor (dropped
+// for sure), p1 = the first pass's sum when the product kernel fused it (tau_1 = eps_g).
+// Returns the final threshold tau (keep |x| > tau) and the number of passes.
+static double alg41_threshold(sexpm_plan_s &P, double eps_g, double F, bool fused_p1, double p1_local,
+                              int64_t nr, int &passes) {
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  passes = 0;
+  if (eps_g == 0.0) return 0.0;  // reading R3: no filtering
+  // m_0 = 1; the first pass always runs (reading R1, Theorem 4.1's proof P:384), then
+  // the passes repeat while b_n > eps_g (1 + e_r)
+  long double m = 1.0L, b = INFINITY;
+  const long double eg = eps_g;
+  const long double lim = eg * (1.0L + (long double)P.o.e_r);
+  long double epsf = INFINITY;
+  while (passes == 0 || b > lim) {
+    epsf = eg / m;
+    const double tau_d = (double)epsf;
+    double S;
+    if (passes == 0 && fused_p1 && tau_d == eps_g) {
+      S = allsum(P, p1_local);  // tau_1 = eps_g: summed in the product kernel's flush
+    } else {
+      launch_alg41_pass_rows(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p,
+                             w.partial.p, w.scal.p + 1, st);
+      S = allsum(P, d2h(w.scal.p + 1, st));
+    }
+    b = sqrtl((long double)F + (long double)S);
+    m = b / epsf;
+    passes++;
+    REQUIRE(passes < 256, SEXPM_EINTERNAL, "Algorithm 4.1 pass cap reached (Theorem 4.1)");
+  }
+  return (double)epsf;
+}
+
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
                             double div, double eps_g, DCsr &C, StepReport &rep,
                             const DCsr *BT = nullptr, bool add_identity = false,
@@ -742,6 +794,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   const int64_t nr = A.nrows;
+  const int okern = P.o.kernel == 8 ? 0 : P.o.kernel;  // 8: the window kernel (Taylor phase)
   const size_t nr1 = (size_t)std::max<int64_t>(nr, 1);
   w.lo.ensure(nr1, st);
   w.hi.ensure(nr1, st);
@@ -770,7 +823,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   // Taylor term with a diagonal H0: the push kernel K5d needs no symbolic pass; every
   // product count is bounded by ndiag * nnz(A), a valid K for the floor lemma
   const bool dia_path = self == 0.0 && P.dia_nd > 0 && B.rp == P.H0full.rp.p &&
-                        (P.o.kernel == 0 || P.o.kernel == 7);
+                        (okern == 0 || okern == 7);
   // a squaring (of T^, or of E in the SSAT baseline): A and B are the same matrix (or B its
   // halo rows), with or without the 2T term
   const bool sq_like = self != 0.0 || B.rp == A.rp || (P.Bhalo.rp.p && B.rp == P.Bhalo.rp.p);
@@ -806,7 +859,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
                            A.row0 == P.row_begin && nr == P.row_end - P.row_begin;
   if (use_cluster) wait_order(P);
   // the block kernels schedule block rows themselves: row bins only for the row kernels
-  const bool block_sq = sq_like && (P.o.kernel == 0 || P.o.kernel == 11 || P.o.kernel == 13);
+  const bool block_sq = sq_like && (okern == 0 || okern == 11 || okern == 13);
   const bool binned = !use_cluster && have_symbolic && !block_sq;
   if (binned) launch_bin_rows(nr, w.prod.p, w.bin_cnt.p, w.bin_off.p, w.order.p, st);
 
@@ -863,7 +916,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
     CK(cudaMemsetAsync(w.fail_count.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
-    int kern = P.o.kernel;
+    int kern = okern;
     const bool taylor_pull_ok = self == 0.0 && BT != nullptr && BT->rp.p != nullptr;
     // squarings: the block kernel on the fp64 tensor-core instruction (13; 11 is the
     // bit-exact DMUL/DADD variant); Taylor terms: the diagonal push or the pull kernel
@@ -1086,7 +1139,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     // the tensor-core block kernel (B = H0) instead
     // (also once rows needed over half of it, or > 1 % of the rows were retried or handed on:
     // 3D rows keep growing term after term)
-    if (P.o.kernel == 0 && !P.o.exact_products && (nd > P.dia_slots_max / 2 || rep.window_rows * 100 > nr))
+    if (okern == 0 && !P.o.exact_products && (nd > P.dia_slots_max / 2 || rep.window_rows * 100 > nr))
       P.taylor_block = true;
     if (getenv("SEXPM_STEP_LOG")) fprintf(stderr, "[sexpm run] K5d need %lld slots, next %d (max %d), retried rows %d\n", nd, P.dia_slots, P.dia_slots_max, (int)(rep.window_rows - nfail_other));
   }
@@ -1117,35 +1170,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   rep.nnz_unf = (int64_t)allsum(P, (double)hnz);
   const double F = allsum(P, Floc);
   rep.fsum = F;
-  double tau;
   int passes = 0;
-  if (eps_g == 0.0) {
-    tau = 0.0;  // reading R3: no filtering
-  } else {
-    // m_0 = 1; the first pass always runs (reading R1, Theorem 4.1's proof P:384), then
-    // the passes repeat while b_n > eps_g (1 + e_r)
-    long double m = 1.0L, b = INFINITY;
-    const long double eg = eps_g;
-    const long double lim = eg * (1.0L + (long double)P.o.e_r);
-    long double epsf = INFINITY;
-    while (passes == 0 || b > lim) {
-      epsf = eg / m;
-      const double tau_d = (double)epsf;
-      double S;
-      if (passes == 0 && fused_p1 && tau_d == eps_g) {
-        S = allsum(P, hs[3]);  // tau_1 = eps_g: summed in the product kernel's flush
-      } else {
-        launch_alg41_pass_rows(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p,
-                               w.partial.p, w.scal.p + 1, st);
-        S = allsum(P, d2h(w.scal.p + 1, st));
-      }
-      b = sqrtl((long double)F + (long double)S);
-      m = b / epsf;
-      passes++;
-      REQUIRE(passes < 256, SEXPM_EINTERNAL, "Algorithm 4.1 pass cap reached (Theorem 4.1)");
-    }
-    tau = (double)epsf;
-  }
+  const double tau = alg41_threshold(P, eps_g, F, fused_p1, fused_p1 ? hs[3] : 0.0, nr, passes);
   rep.passes = passes;
   rep.tau = tau;
 
@@ -1711,7 +1737,7 @@ static void build_diagonals(sexpm_plan_s &P) {
   cudaStream_t st = P.st;
   P.dia_nd = 0;
   const DCsr &Hf = P.H0full;
-  if (Hf.nnz == 0 || P.o.kernel != 0 && P.o.kernel != 7) return;
+  if (Hf.nnz == 0 || P.o.kernel != 0 && P.o.kernel != 7 && P.o.kernel != 8) return;
   if (P.n > (int64_t(1) << 30)) return;  // K5d computes columns k + d in 32 bits
   const int64_t nbits = 2 * P.n - 1, nwords = (nbits + 31) / 32;
   DBuf<unsigned> bits;
@@ -1733,6 +1759,7 @@ static void build_diagonals(sexpm_plan_s &P) {
   if (offs.empty() || (int)offs.size() > kDiaMax) return;
   std::sort(offs.begin(), offs.end(), std::greater<int32_t>());  // descending: k ascending per column
   P.dia_nd = (int)offs.size();
+  P.h_dia_off = offs;
   P.dia_dmax = offs.front();
   P.dia_dmin = offs.back();
   P.dia_off.alloc(offs.size(), st);
@@ -1750,6 +1777,146 @@ static void build_diagonals(sexpm_plan_s &P) {
     P.dia_slots_max = sl;
   }
   CK(cudaStreamSynchronize(st));  // offs (host) is captured by value in the launch
+}
+
+// K5w tables (kernels.cu k_taylor_win): the offsets a row of S~_j can reach are the Minkowski
+// sums W_j = W_{j-1} + D (W_1 = D, H0's diagonal offsets), offsets with |o| >= n pruned (no
+// row has such a column).  U = W_1 u ... u W_M ascending; per U-index and diagonal the U-index
+// of o - d (the input offset of the product s(r, r+o-d) h_d(r+o-d)); per term the U-indices of
+// W_j and of the cumulative union (the support of T^_0 after term j), ascending.  The window is
+// used when U is small enough for shared memory (grid stencils in 1D / 2D; 3D octahedra of
+// radius M are not) with at least 8 resident warps per SM.
+static void build_window(sexpm_plan_s &P) {
+  auto &W = P.win;
+  cudaStream_t st = P.st;
+  W.ok = false;
+  if (P.dia_nd == 0 || P.M < 1 || P.o.kernel != 0 && P.o.kernel != 8) return;
+  if (getenv("SEXPM_NO_WIN")) return;
+  constexpr int kCap = 4096;
+  const int nd = P.dia_nd;
+  std::vector<int64_t> D(P.h_dia_off.begin(), P.h_dia_off.end());
+  std::vector<std::vector<int64_t>> Wj((size_t)P.M + 1);
+  std::vector<int64_t> cur;
+  for (int64_t d : D)
+    if (d > -P.n && d < P.n) cur.push_back(d);
+  std::sort(cur.begin(), cur.end());
+  cur.erase(std::unique(cur.begin(), cur.end()), cur.end());
+  Wj[1] = cur;
+  std::vector<int64_t> U = cur;
+  for (int j = 2; j <= P.M; j++) {
+    std::vector<int64_t> nx;
+    nx.reserve(cur.size() * D.size());
+    for (int64_t o : cur)
+      for (int64_t d : D) {
+        const int64_t v = o + d;
+        if (v > -P.n && v < P.n) nx.push_back(v);
+      }
+    std::sort(nx.begin(), nx.end());
+    nx.erase(std::unique(nx.begin(), nx.end()), nx.end());
+    std::vector<int64_t> un;
+    std::set_union(U.begin(), U.end(), nx.begin(), nx.end(), std::back_inserter(un));
+    U.swap(un);
+    if ((int)U.size() > kCap) return;
+    Wj[j] = nx;
+    cur.swap(nx);
+  }
+  const int nU = (int)U.size();
+  // positions: binary search in a sorted offset list
+  auto pos = [](const std::vector<int64_t> &v, int64_t o) -> int {
+    auto it = std::lower_bound(v.begin(), v.end(), o);
+    return (it != v.end() && *it == o) ? (int)(it - v.begin()) : -1;
+  };
+  int dzero = -1;
+  for (int di = 0; di < nd; di++)
+    if (D[di] == 0) dzero = di;
+  const int64_t nl = P.row_end - P.row_begin;
+  int64_t maxo = 0, maxd = 0;
+  for (int64_t o : U) maxo = std::max<int64_t>(maxo, o < 0 ? -o : o);
+  for (int64_t d : D) maxd = std::max<int64_t>(maxd, d < 0 ? -d : d);
+  const int64_t pad = maxo + maxd + 1, npad = P.n + 2 * pad;
+  const int knd = taylor_win_kernel_nd(nd), rw = taylor_win_rec_words(nd);
+  // the records hold int32 element offsets
+  int64_t maxl = 0, maxc = 0;
+  {
+    std::vector<int64_t> cu;
+    for (int j = 1; j <= P.M; j++) {
+      std::vector<int64_t> un;
+      std::set_union(cu.begin(), cu.end(), Wj[j].begin(), Wj[j].end(), std::back_inserter(un));
+      cu.swap(un);
+      maxl = std::max<int64_t>(maxl, (int64_t)Wj[j].size());
+      maxc = std::max<int64_t>(maxc, (int64_t)cu.size());
+    }
+  }
+  if ((maxl + 1) * nl >= INT32_MAX || (maxc + 1) * nl >= INT32_MAX || (int64_t)(nd + 1) * npad >= INT32_MAX) return;
+  W.lcnt.assign((size_t)P.M + 1, 0);
+  W.ccnt.assign((size_t)P.M + 1, 0);
+  W.woff.assign((size_t)P.M + 2, 0);
+  W.coff.assign((size_t)P.M + 2, 0);
+  std::vector<int32_t> hrec, hco;
+  std::vector<int16_t> hmc, hmw;
+  std::vector<int64_t> cum, cum_prev, cum_prev2;
+  for (int j = 1; j <= P.M; j++) {
+    std::vector<int64_t> un;
+    std::set_union(cum.begin(), cum.end(), Wj[j].begin(), Wj[j].end(), std::back_inserter(un));
+    cum_prev2 = cum_prev;
+    cum_prev = cum;  // cum_{j-1}
+    cum.swap(un);    // cum_j
+    W.lcnt[j] = (int)Wj[j].size();
+    W.ccnt[j] = (int)cum.size();
+    W.woff[j] = (int64_t)hrec.size();
+    W.coff[j] = (int64_t)hco.size();
+    if (j >= 2) {  // TERM launch i = j: records over W_j
+      const int64_t zs = j == 2 ? (int64_t)nd * npad : (int64_t)W.lcnt[j - 1] * nl;  // zero planes
+      const int64_t zt = (int64_t)W.ccnt[j - 2] * nl;
+      for (int64_t o : Wj[j]) {
+        for (int di = 0; di < knd; di++) {
+          const int p = di < nd ? pos(Wj[j - 1], o - D[di]) : -1;
+          hrec.push_back((int32_t)(p < 0 ? zs : (j == 2 ? (int64_t)(nd - 1 - p) * npad : (int64_t)p * nl)));
+        }
+        const int q = dzero >= 0 ? pos(cum_prev, o) : -1;  // T^_0 fused only when 0 is in D
+        const int pc = pos(cum_prev2, o);
+        hrec.push_back((int32_t)(q < 0 ? -1 : (int64_t)q * nl));
+        hrec.push_back((int32_t)(pc < 0 ? zt : (int64_t)pc * nl));
+        hrec.push_back((int32_t)o);
+        for (int w = knd + 3; w < rw; w++) hrec.push_back(0);
+      }
+      // the fused T^_0 update needs cum_{j-1} inside W_j (true when 0 is in D)
+      if (dzero >= 0)
+        for (int64_t o : cum_prev) REQUIRE(pos(Wj[j], o) >= 0, SEXPM_EINTERNAL, "window tables: cum not in W");
+    }
+    for (int64_t o : cum) {
+      hco.push_back((int32_t)o);
+      hmc.push_back((int16_t)pos(cum_prev, o));
+      hmw.push_back((int16_t)pos(Wj[j], o));
+    }
+  }
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.dev));
+  for (int j = 2; j <= P.M; j++)
+    if (taylor_win_smem_bytes(nd, W.lcnt[j], W.ccnt[j - 1]) > optin - 1024) return;
+  W.nU = nU;
+  W.dzero = dzero;
+  W.rw = rw;
+  W.pad = pad;
+  W.npad = npad;
+  W.rec.alloc(std::max<size_t>(hrec.size(), 4), st);
+  if (!hrec.empty()) CK(cudaMemcpyAsync(W.rec.p, hrec.data(), hrec.size() * 4, cudaMemcpyHostToDevice, st));
+  W.coffs.alloc(std::max<size_t>(hco.size(), 1), st);
+  CK(cudaMemcpyAsync(W.coffs.p, hco.data(), hco.size() * 4, cudaMemcpyHostToDevice, st));
+  W.mapC.alloc(std::max<size_t>(hmc.size(), 1), st);
+  CK(cudaMemcpyAsync(W.mapC.p, hmc.data(), hmc.size() * 2, cudaMemcpyHostToDevice, st));
+  W.mapW.alloc(std::max<size_t>(hmw.size(), 1), st);
+  CK(cudaMemcpyAsync(W.mapW.p, hmw.data(), hmw.size() * 2, cudaMemcpyHostToDevice, st));
+  // zero-padded diagonals (+ a zero plane): h_d(k) for any k the window can form
+  W.dpad.alloc((size_t)(nd + 1) * (size_t)npad, st);
+  CK(cudaMemsetAsync(W.dpad.p, 0, (size_t)(nd + 1) * (size_t)npad * sizeof(double), st));
+  for (int di = 0; di < nd; di++)
+    CK(cudaMemcpyAsync(W.dpad.p + (size_t)di * npad + pad, P.dia_val.p + (size_t)di * P.n, (size_t)P.n * sizeof(double),
+                       cudaMemcpyDeviceToDevice, st));
+  W.cnt.alloc(1, st);
+  W.need.alloc(1, st);
+  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+  W.ok = true;
 }
 
 // ------------------------------------------------------------------------------------
@@ -2179,6 +2346,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   launch_scale_pow2(P.H0T.val.p, P.H0T.nnz, -N, st);
   mark("plan (M,N) + scale");
   build_diagonals(P);
+  build_window(P);
   mark("diagonals");
   slice_rows(P, Hf, P.row_begin, P.row_end, P.H0loc);
   // The squarings' processing order (locality clusters of H's graph, host BFS) is computed
@@ -2387,6 +2555,238 @@ static void swap_csr(DCsr &a, DCsr &b) {
   b = std::move(t);
 }
 
+// Taylor phase on the offset window K5w (Alg. 4.2 step 3): one launch per term
+// i = 2..M (S~_i from the checkpoint of S~_{i-1}, T^_0^(i-1) accumulated on the way), the
+// Algorithm 4.1 passes over the staged band values, then T^_0 = T^_0^(m-1) + S^_m
+// (m = M_eff) written as CSR (count, scan, write).  Returns M_eff.
+static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()> &step_ms,
+                         cudaEvent_t a0) {
+  auto &W = P.win;
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  sexpm_stats &S = P.stats;
+  const auto h_start = std::chrono::steady_clock::now();
+  const int64_t nl = P.row_end - P.row_begin;
+  const size_t nl1 = (size_t)std::max<int64_t>(nl, 1);
+  int maxl = 1, maxc = 1;
+  for (int j = 1; j <= P.M; j++) {
+    maxl = std::max(maxl, W.lcnt[j]);
+    maxc = std::max(maxc, W.ccnt[j]);
+  }
+  DBuf<double> *ck_s[2] = {&P.Tn.val, &P.E.val};
+  if (P.M >= 2) {  // one extra (zero) plane each: the records' "absent" operand
+    for (int k = 0; k < 2; k++) {
+      ck_s[k]->ensure(nl1 * (size_t)(maxl + 1), st);
+      W.ck_t[k].ensure(nl1 * (size_t)(maxc + 1), st);
+    }
+  }
+  // band values staged in the staging pool (position-major, band_cap per row)
+  // (a row of S~_i has at most |W_i| <= maxl values: sized for that, no term ever re-runs; the
+  // pool is the squarings' staging pool, which is larger anyway)
+  int64_t band_cap = maxl;
+  if (getenv("SEXPM_WIN_BAND")) band_cap = std::max<int64_t>(1, atoll(getenv("SEXPM_WIN_BAND")));  // debug: initial band slots
+  w.row_cnt.ensure(nl1, st);
+  w.row_nnz.ensure(nl1, st);
+  w.row_fsum.ensure(nl1, st);
+  w.row_p1.ensure(nl1, st);
+  w.row_c1.ensure(nl1, st);
+  w.passrow.ensure(nl1, st);
+  w.cnt.ensure(nl1, st);
+  w.cnt2.ensure(nl1, st);
+  w.scan_tmp.ensure((size_t)scan_tmp_elems(nl) + 1, st);
+  w.partial.ensure(1024, st);
+  w.scal.ensure(8, st);
+  w.i64tmp.ensure(8, st);
+  WinArgs base;
+  base.nrows = nl;
+  base.row0 = P.row_begin;
+  base.n = P.n;
+  base.nd = P.dia_nd;
+  base.dia = P.dia_val.p;
+  base.doff = P.dia_off.p;
+  base.dzero = W.dzero;
+  base.dpad = W.dpad.p + W.pad;
+  base.hpad = (int32_t)W.pad;
+  for (int di = 0; di < kDiaMax; di++)
+    base.hoff[di] = di < P.dia_nd ? (int32_t)((int64_t)di * W.npad - P.h_dia_off[di]) : 0;
+  base.row_cnt = w.row_cnt.p;
+  base.row_nnz = w.row_nnz.p;
+  base.row_c1 = w.row_c1.p;
+  base.row_fsum = w.row_fsum.p;
+  base.row_p1 = w.row_p1.p;
+  // CTAs (4 warps) per SM of the term kernel (default: one CTA per tile of 128 rows)
+  const int win_ctas = getenv("SEXPM_WIN_CTAS") ? std::max(1, atoi(getenv("SEXPM_WIN_CTAS"))) : 1 << 20;
+  cudaEvent_t k0, k1;
+  CK(cudaEventCreate(&k0));
+  CK(cudaEventCreate(&k1));
+  int sa = 0, ta = 0;  // ck_s[sa] = S~_{i-1}, ck_t[ta] = T^_0^(i-2)
+  double tau_prev = 0.0;
+  int64_t prev_nnz_local = 0;
+  int M_eff = 1;
+  if (getenv("SEXPM_STEP_LOG")) CK(cudaStreamSynchronize(st));
+  const auto h_loop = std::chrono::steady_clock::now();
+  const double eps_g = P.eps_g0;
+  for (int i = 2; i <= P.M; i++) {
+    CK(cudaEventRecord(a0, st));
+    WinArgs a = base;
+    a.prev_is_h0 = i == 2;
+    a.pS = ck_s[sa]->p;
+    a.tau_prev = tau_prev;
+    a.T0old = W.ck_t[ta].p;
+    a.T0new = W.ck_t[ta ^ 1].p;
+    a.c1cnt = W.ccnt[i - 1];
+    a.mapC = W.mapC.p + W.coff[i - 1];
+    a.mapW = W.mapW.p + W.coff[i - 1];
+    a.ncnt = W.lcnt[i];
+    a.rec = W.rec.p + W.woff[i];
+    a.nS = ck_s[sa ^ 1]->p;
+    // zero planes of the inputs (absent operands)
+    if (i > 2) CK(cudaMemsetAsync(ck_s[sa]->p + (size_t)W.lcnt[i - 1] * nl, 0, nl1 * sizeof(double), st));
+    CK(cudaMemsetAsync(W.ck_t[ta].p + (size_t)W.ccnt[i - 2] * nl, 0, nl1 * sizeof(double), st));
+    if (W.dzero < 0) launch_taylor_win_t0(a, st);  // T^_0 update not fused
+    a.divisor = (double)i;
+    // floor lemma: K = n |W_i| bounds the entries of S~_i
+    const double K = (double)P.n * (double)W.lcnt[i];
+    a.floor_tau = (eps_g > 0.0 && K > 0.0) ? eps_g / sqrt(K) : 0.0;
+    a.eps_g = eps_g;
+    // band staging sized from the previous terms; re-run once at the size a row needed (the
+    // launch is idempotent: its outputs never alias its inputs)
+    for (int attempt = 0;; attempt++) {
+      w.pool_val.ensure(nl1 * (size_t)band_cap, st);
+      w.pool_col.ensure(nl1 * (size_t)band_cap, st);
+      a.band_val = w.pool_val.p;
+      a.band_col = w.pool_col.p;
+      a.band_cap = band_cap;
+      a.band_need = W.need.p;
+      CK(cudaMemsetAsync(W.need.p, 0, sizeof(unsigned long long), st));
+      CK(cudaEventRecord(k0, st));
+      launch_taylor_win(a, win_ctas, P.sm_count, st);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(k1, st));
+      const unsigned long long need = d2h(W.need.p, st);
+      if (need == 0) break;
+      REQUIRE(attempt < 2, SEXPM_EINTERNAL, "window Taylor kernel: band staging keeps overflowing");
+      band_cap = std::min<int64_t>(maxl, (int64_t)need + need / 4 + 16);
+      P.retries++;
+    }
+    // Algorithm 4.1 over the band values
+    launch_reduce_sum(w.row_fsum.p, nl, w.partial.p, w.scal.p + 0, st);
+    launch_reduce_sum(w.row_p1.p, nl, w.partial.p, w.scal.p + 3, st);
+    launch_reduce_sum_i64(w.row_nnz.p, nl, w.i64tmp.p + 3, st);
+    launch_reduce_sum_i64(w.row_c1.p, nl, w.i64tmp.p + 4, st);
+    launch_reduce_sum_i64(w.row_cnt.p, nl, w.i64tmp.p + 5, st);
+    double hs[4];
+    int64_t hi[3];
+    // products with a nonzero left operand: nd per entry of S^_{i-1} (h may be 0 at a boundary)
+    const double prods = (double)P.dia_nd * (double)(i == 2 ? P.H0loc.nnz : prev_nnz_local);
+    CK(cudaMemcpyAsync(hs, w.scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hi, w.i64tmp.p + 3, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double F = allsum(P, hs[0]);
+    int passes = 0;
+    double tau = 0.0;
+    if (eps_g > 0.0) {
+      // m_0 = 1; the first pass always runs (reading R1; tau_1 = eps_g: fused), then the
+      // passes repeat while b_n > eps_g (1 + e_r)
+      long double m = 1.0L, b = INFINITY;
+      const long double eg = eps_g, lim = eg * (1.0L + (long double)P.o.e_r);
+      long double epsf = INFINITY;
+      while (passes == 0 || b > lim) {
+        epsf = eg / m;
+        const double tau_d = (double)epsf;
+        double Sp;
+        if (passes == 0 && tau_d == eps_g) {
+          Sp = allsum(P, hs[3]);
+        } else {
+          launch_win_band_pass(nl, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p, nullptr, st);
+          launch_reduce_sum(w.passrow.p, nl, w.partial.p, w.scal.p + 1, st);
+          Sp = allsum(P, d2h(w.scal.p + 1, st));
+        }
+        b = sqrtl((long double)F + (long double)Sp);
+        m = b / epsf;
+        passes++;
+        REQUIRE(passes < 256, SEXPM_EINTERNAL, "Algorithm 4.1 pass cap reached (Theorem 4.1)");
+      }
+      tau = (double)epsf;
+    }
+    // nnz(S^_i) = sure keeps + band values above tau
+    int64_t kept = hi[1];
+    if (eps_g > 0.0 && !(passes == 1 && tau == eps_g) && hi[2] > 0) {
+      launch_win_band_pass(nl, w.row_cnt.p, w.pool_val.p, tau, nullptr, w.cnt2.p, st);
+      launch_reduce_sum_i64(w.cnt2.p, nl, w.i64tmp.p + 6, st);
+      kept += d2h(w.i64tmp.p + 6, st);
+    }
+    const int64_t nnz = (int64_t)allsum(P, (double)kept);
+    const int64_t kept_local = kept;
+    float kms = 0.f;
+    CK(cudaEventElapsedTime(&kms, k0, k1));
+    const double bytes = 8.0 * (double)nl * (W.lcnt[i - 1] + W.ccnt[i - 2] + W.ccnt[i - 1] + W.lcnt[i]) +
+                         12.0 * (double)hi[2] + 40.0 * (double)nl;
+    if (i < SEXPM_MAXSTEP) {
+      S.taylor_nnz_unf[i] = (int64_t)allsum(P, (double)hi[0]);
+      S.taylor_nnz[i] = nnz;
+      S.taylor_passes[i] = passes;
+      S.taylor_tau[i] = tau;
+      S.taylor_numeric_ms[i] = kms;
+      S.taylor_numeric_bytes[i] = bytes;
+      S.taylor_fmas_i[i] = allsum(P, prods);
+      S.taylor_fallback_rows[i] = 0;
+    }
+    S.taylor_fmas += allsum(P, prods);
+    S.taylor_bytes += bytes;
+    if (getenv("SEXPM_STEP_LOG"))
+      fprintf(stderr, "[sexpm run] taylor %d (window): nnz %lld passes %d kernel %.2f ms (%.0f GB/s) band %lld\n", i,
+              (long long)nnz, passes, kms, bytes / (kms * 1e6), (long long)hi[2]);
+    if (nnz == 0) {  // S^_i = 0: all later terms vanish
+      if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();
+      break;
+    }
+    M_eff = i;
+    tau_prev = tau;
+    prev_nnz_local = kept_local;
+    sa ^= 1;
+    ta ^= 1;
+    if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();
+  }
+  // T^_0 = T^_0^(m-1) + S^_m as CSR: count, scan, write
+  const auto h_fin = std::chrono::steady_clock::now();
+  {
+    const int m = M_eff;
+    WinArgs a = base;
+    a.prev_is_h0 = m == 1;
+    a.pS = ck_s[sa]->p;
+    a.tau_prev = tau_prev;
+    a.T0old = W.ck_t[ta].p;
+    a.c1cnt = W.ccnt[m];
+    a.mapC = W.mapC.p + W.coff[m];
+    a.mapW = W.mapW.p + W.coff[m];
+    a.coffs = W.coffs.p + W.coff[m];
+    launch_taylor_win_final(a, w.cnt.p, nullptr, nullptr, nullptr, st);
+    T.nrows = nl;
+    T.row0 = P.row_begin;
+    T.padded = false;
+    T.rp.ensure((size_t)nl + 1, st);
+    launch_exclusive_scan(w.cnt.p, nl, T.rp.p, w.scan_tmp.p, st);
+    T.nnz = d2h(T.rp.p + nl, st);
+    T.col.ensure((size_t)std::max<int64_t>(T.nnz, 1), st);
+    T.val.ensure((size_t)std::max<int64_t>(T.nnz, 1), st);
+    launch_taylor_win_final(a, nullptr, T.rp.p, T.col.p, T.val.p, st);
+    CK(cudaGetLastError());
+    S.taylor_bytes += 16.0 * (double)nl * a.c1cnt * 2 + 12.0 * (double)T.nnz;
+    if (getenv("SEXPM_STEP_LOG")) {
+      CK(cudaStreamSynchronize(st));
+      fprintf(stderr, "[sexpm run] taylor (window): setup %.1f ms, T^_0 to CSR %.1f ms (host wall)\n",
+              std::chrono::duration<double, std::milli>(h_loop - h_start).count(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h_fin).count());
+    }
+  }
+  cudaEventDestroy(k0);
+  cudaEventDestroy(k1);
+  // the checkpoints live for the Taylor phase only
+  for (int k = 0; k < 2; k++) W.ck_t[k].release();
+  return M_eff;
+}
+
 static void do_run(sexpm_plan_s &P) {
   cudaStream_t st = P.st;
   sexpm_stats &S = P.stats;
@@ -2427,7 +2827,10 @@ static void do_run(sexpm_plan_s &P) {
   DCsr &T = P.T, &Tn = P.Tn, &Sc = P.S, &Sn = P.Sn;
   // ---- Taylor phase ----
   int M_eff = 0;
-  if (P.M == 0) {  // reading R9: T^_0 = 0
+  if (P.M >= 1 && P.win.ok) {
+    M_eff = taylor_window(P, T, step_ms, a0);
+    S.taylor_window = 1;
+  } else if (P.M == 0) {  // reading R9: T^_0 = 0
     T.nrows = nl;
     T.row0 = P.row_begin;
     T.nnz = 0;

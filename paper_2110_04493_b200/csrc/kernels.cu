@@ -3811,6 +3811,339 @@ void launch_taylor_dia_short(const NumericArgs &a, const DiaView &D, int32_t *fa
 }  // namespace sx
 
 namespace sx {
+// ------------------------------------------------------------------------------------
+// K5w: Taylor terms on the dense OFFSET WINDOW (Eq. 4.10-4.11, Alg. 4.2 step 3
+// P:410-418).  For an H0 with few diagonal offsets D (grid stencils), row r of S~_j is
+// nonzero only at columns r + o, o in the Minkowski sum W_j = D + ... + D (j times); T^_0
+// after term j only at cum_j = W_1 u ... u W_j.  The driver enumerates them once per plan
+// (ascending); a term is stored POSITION-MAJOR and dense: S~_j(r, r + W_j[q]) at
+// S[q * nl + l] (l = local row), T^_0 likewise over cum_j.  One thread per row: every load
+// and store of a warp covers 32 consecutive rows of one position (coalesced, no column
+// indices, no shared-memory rows), and the tables (uniform across the warp) sit in shared
+// memory.
+//
+// TERM launch i (thread = row r):
+//   S~_i(r, r+o) = (sum over di, offsets d DESCENDING, of S^_{i-1}(r, r+o-d) h_d(r+o-d)) / i,
+//   S^_{i-1} = keep(S~_{i-1}, |x| > tau_{i-1}) applied on load (S^_1 = H0's row, unfiltered,
+//   reading R9).  For a fixed output column the k = r+o-d run ascending: the oracle's
+//   Gustavson order with _rn products and sums, then an IEEE division (R7) -- bit-identical.
+//   When 0 is in D, T^_0^(i-1) = T^_0^(i-2) + S^_{i-1} is fused into the same loop (the d = 0
+//   operand is S^_{i-1} at the output's own offset; cum_{i-1} = W_{i-1} is inside W_i).
+//   Classification against the Algorithm 4.1 floor (see k_numeric): |x| <= floor dropped
+//   (x^2 summed), floor < |x| <= eps_g staged per row, position-major (band[k * nl + l]), the
+//   only values Algorithm 4.1's passes can still decide, |x| > eps_g kept for sure (counted).
+// S~ at a column outside [0, n) is exactly zero (h_d(k) = 0 where column k + d does not
+// exist); the h_d loads are guarded by 0 <= k < n because they are issued before the operand
+// is known (all loads of an output in flight together).
+// ------------------------------------------------------------------------------------
+constexpr int kWinThreads = 128;
+// per output position t of W_i one record of int32 element offsets (built at plan time for
+// this rank's row count nl, read with two broadcast shared-memory loads):
+//   [0, ND)  the source of each diagonal: p * nl for position p of S~_{i-1} (i = 2: the plane
+//            of H0's diagonal in the padded diagonal array), or the zero plane when absent
+//   ND       T^_0^(i-1) store: q * nl for o_t's position q in cum_{i-1}, or -1
+//   ND + 1   T^_0^(i-2) load: its position * nl, or the zero plane
+//   ND + 2   o_t
+int taylor_win_rec_words(int nd) { return ((taylor_win_kernel_nd(nd) + 3) + 3) / 4 * 4; }
+int taylor_win_smem_bytes(int nd, int ncnt, int ccnt) {
+  (void)ccnt;
+  return ncnt * taylor_win_rec_words(nd) * 4 + 16;
+}
+template <int ND, bool H0PREV>  // H0PREV: S~_{i-1} = H0 (i = 2)
+__global__ void __launch_bounds__(kWinThreads) k_taylor_win(WinArgs a) {
+  extern __shared__ int4 wsm4[];
+  constexpr int RW = ((ND + 3) + 3) / 4 * 4;
+  const int tid = threadIdx.x;
+  const int ncnt = a.ncnt;
+  const int32_t *s_rec = reinterpret_cast<const int32_t *>(wsm4);
+  {
+    const int4 *src = reinterpret_cast<const int4 *>(a.rec);
+    for (int i = tid; i < ncnt * (RW / 4); i += kWinThreads) wsm4[i] = src[i];
+  }
+  __syncthreads();
+  const int nl = (int)a.nrows;
+  const double tau_prev = a.tau_prev;
+  const double div = a.divisor, floor_tau = a.floor_tau, eps_g = a.eps_g;
+  const int dz = a.dzero;
+  uint32_t hoff[ND];
+#pragma unroll
+  for (int di = 0; di < ND; di++) hoff[di] = (uint32_t)(a.hoff[di] + a.hpad);  // >= 0
+  // one output's operands: ND sources, ND diagonal values, the T^_0 value; all loads of the
+  // next output are issued before the current one is summed (software pipeline)
+  struct Ops {
+    double x[ND], h[ND], t0;
+    int t0n, o;
+  };
+  // persistent CTAs over tiles of 128 rows
+  for (int64_t tile = blockIdx.x; tile * kWinThreads < a.nrows; tile += gridDim.x) {
+    const int l = (int)(tile * kWinThreads) + tid;
+    if (l >= nl) break;
+    const int64_t r = a.row0 + l;
+    const double *hb = a.dpad - a.hpad + r;         // h_d(r + o - d) = hb[hoff[di] + o]
+    const double *xb = H0PREV ? a.dpad + r : a.pS + l;  // S~_{i-1}(r, r + o') = xb[rec]
+    const double *t0ob = a.T0old + l;
+    double *t0nb = a.T0new + l;
+    double *nsb = a.nS + l;
+    auto load = [&](int t, Ops &op) {
+      int rc[RW];
+#pragma unroll
+      for (int w = 0; w < RW; w += 4) {
+        const int4 v4 = *reinterpret_cast<const int4 *>(s_rec + t * RW + w);
+        rc[w] = v4.x;
+        rc[w + 1] = v4.y;
+        rc[w + 2] = v4.z;
+        rc[w + 3] = v4.w;
+      }
+      op.o = rc[ND + 2];
+      op.t0n = rc[ND];
+#pragma unroll
+      for (int di = 0; di < ND; di++) {
+        op.x[di] = __ldg(xb + (uint32_t)rc[di]);
+        op.h[di] = __ldg(hb + (hoff[di] + (uint32_t)op.o));
+      }
+      op.t0 = __ldg(t0ob + (uint32_t)rc[ND + 1]);
+    };
+    double fs = 0.0, q1 = 0.0;
+    int nnzu = 0, c1 = 0, nb = 0;
+    uint32_t nso = 0;
+    Ops cur, nxt;
+    if (ncnt > 0) load(0, cur);
+    for (int t = 0; t < ncnt; t++) {
+      if (t + 1 < ncnt) load(t + 1, nxt);
+      // products k ascending (offsets descending); a zero operand adds +-0, which leaves the
+      // running sum unchanged (it is never -0), exactly as the oracle's skipped product
+      double acc = 0.0, v0 = 0.0;
+#pragma unroll
+      for (int di = 0; di < ND; di++) {
+        const double v = H0PREV ? cur.x[di] : (fabs(cur.x[di]) > tau_prev ? cur.x[di] : 0.0);
+        if (di == dz) v0 = v;
+        acc = __dadd_rn(acc, __dmul_rn(v, cur.h[di]));
+      }
+      if (cur.t0n >= 0) t0nb[(uint32_t)cur.t0n] = cur.t0 + v0;  // fused T^_0 update (d = 0 operand)
+      const double x = acc / div;  // acc = +0 gives +0
+      nsb[nso] = x;
+      nso += (uint32_t)nl;
+      if (x != 0.0) {
+        nnzu++;
+        const double ax = fabs(x);
+        if (ax <= floor_tau) {
+          fs += x * x;
+        } else if (ax <= eps_g) {
+          q1 += x * x;
+          if (nb < a.band_cap) {
+            a.band_val[(int64_t)nb * nl + l] = x;
+            a.band_col[(int64_t)nb * nl + l] = (int32_t)(r + cur.o);
+          }
+          nb++;
+        } else {
+          c1++;
+        }
+      }
+      cur = nxt;
+    }
+    a.row_cnt[l] = nb;
+    a.row_fsum[l] = fs;
+    a.row_p1[l] = q1;
+    a.row_nnz[l] = nnzu;
+    a.row_c1[l] = c1;
+    if (nb > a.band_cap) atomicMax(a.band_need, (unsigned long long)nb);
+  }
+}
+// T^_0^(i-1) = T^_0^(i-2) + S^_{i-1} as a separate streaming pass (H0 without a main
+// diagonal: cum_{i-1} is then not inside W_i, so the update cannot ride on the term's loop)
+__global__ void __launch_bounds__(kWinThreads) k_taylor_win_t0(WinArgs a) {
+  extern __shared__ double wsm[];
+  const int ccnt = a.c1cnt;
+  int16_t *s_mc = reinterpret_cast<int16_t *>(wsm);
+  int16_t *s_mw = s_mc + ccnt;
+  for (int i = threadIdx.x; i < ccnt; i += blockDim.x) {
+    s_mc[i] = a.mapC[i];
+    s_mw[i] = a.mapW[i];
+  }
+  __syncthreads();
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= a.nrows) return;
+  const int64_t r = a.row0 + l;
+  for (int q = 0; q < ccnt; q++) {
+    const int pc = s_mc[q], pw = s_mw[q];
+    const double t0 = pc >= 0 ? __ldg(a.T0old + (size_t)pc * a.nrows + l) : 0.0;
+    double sv = 0.0;
+    if (pw >= 0) {
+      sv = a.prev_is_h0 ? __ldg(a.dia + (size_t)(a.nd - 1 - pw) * (size_t)a.n + (size_t)r)
+                        : __ldg(a.pS + (size_t)pw * a.nrows + l);
+      if (!a.prev_is_h0 && !(fabs(sv) > a.tau_prev)) sv = 0.0;
+    }
+    a.T0new[(size_t)q * a.nrows + l] = t0 + sv;
+  }
+}
+void launch_taylor_win_t0(const WinArgs &a, cudaStream_t st) {
+  if (a.nrows == 0 || a.c1cnt == 0) return;
+  const int smem = a.c1cnt * 4 + 16;
+  cudaFuncSetAttribute(k_taylor_win_t0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_taylor_win_t0<<<(unsigned)((a.nrows + kWinThreads - 1) / kWinThreads), kWinThreads, smem, st>>>(a);
+}
+template <int ND>
+static void launch_win_nd(const WinArgs &a, int smem, int ctas_per_sm, int sms, cudaStream_t st) {
+  auto kf = a.prev_is_h0 ? k_taylor_win<ND, true> : k_taylor_win<ND, false>;
+  cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int64_t tiles = (a.nrows + kWinThreads - 1) / kWinThreads;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * ctas_per_sm));
+  KL;
+  kf<<<grid, kWinThreads, smem, st>>>(a);
+}
+void launch_taylor_win(const WinArgs &a, int ctas_per_sm, int sms, cudaStream_t st) {
+  if (a.nrows == 0) return;
+  const int smem = taylor_win_smem_bytes(a.nd, a.ncnt, a.c1cnt);
+  // the kernel is specialised on the number of diagonals (records and sums unrolled)
+  switch (taylor_win_kernel_nd(a.nd)) {
+    case 3: launch_win_nd<3>(a, smem, ctas_per_sm, sms, st); break;
+    case 5: launch_win_nd<5>(a, smem, ctas_per_sm, sms, st); break;
+    case 7: launch_win_nd<7>(a, smem, ctas_per_sm, sms, st); break;
+    case 1: launch_win_nd<1>(a, smem, ctas_per_sm, sms, st); break;
+    case 2: launch_win_nd<2>(a, smem, ctas_per_sm, sms, st); break;
+    case 4: launch_win_nd<4>(a, smem, ctas_per_sm, sms, st); break;
+    case 6: launch_win_nd<6>(a, smem, ctas_per_sm, sms, st); break;
+    case 8: launch_win_nd<8>(a, smem, ctas_per_sm, sms, st); break;
+    case 9: launch_win_nd<9>(a, smem, ctas_per_sm, sms, st); break;
+    default: launch_win_nd<kDiaMax>(a, smem, ctas_per_sm, sms, st); break;
+  }
+}
+// Algorithm 4.1 pass over the staged band values (position-major, row_cnt per row):
+// rowsum[l] = sum over k < cnt of x^2 with |x| <= tau (k order), count[l] = |x| > tau
+__global__ void k_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val, double tau,
+                                double *rowsum, int64_t *rowcnt) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  const int64_t c = cnt[l];
+  double s = 0.0;
+  int64_t k = 0;
+  for (int64_t j = 0; j < c; j++) {
+    const double x = band_val[(size_t)j * nl + l];
+    if (fabs(x) <= tau) s += x * x;
+    else k++;
+  }
+  if (rowsum) rowsum[l] = s;
+  if (rowcnt) rowcnt[l] = k;
+}
+void launch_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val, double tau, double *rowsum,
+                          int64_t *rowcnt, cudaStream_t st) {
+  if (nl == 0) return;
+  KL;
+  k_win_band_pass<<<grid_for(nl, kThreads), kThreads, 0, st>>>(nl, cnt, band_val, tau, rowsum, rowcnt);
+}
+// FINAL: T^_0 = T^_0^(m-1) + S^_m over cum_m.  Count pass (thread per row), then the write
+// pass: a CTA takes 32 rows, computes 32 positions x 32 rows per round into a shared tile
+// (loads coalesced over rows) and each warp writes 4 rows' nonzeros of the round
+// contiguously (columns ascending) at rp_out[l] + the row's running count.
+__device__ __forceinline__ double win_prev(const WinArgs &a, int p, int64_t l, int64_t r, int nd) {
+  if (a.prev_is_h0) return __ldg(a.dia + (size_t)(nd - 1 - p) * (size_t)a.n + (size_t)r);
+  const double x = __ldg(a.pS + (size_t)p * (size_t)a.nrows + (size_t)l);
+  return fabs(x) > a.tau_prev ? x : 0.0;
+}
+__device__ __forceinline__ double win_t0(const WinArgs &a, const int16_t *mc, const int16_t *mw, int q,
+                                         int64_t l, int64_t r, int nd) {
+  const int pc = mc[q], pw = mw[q];
+  const double t0 = pc >= 0 ? __ldg(a.T0old + (size_t)pc * a.nrows + l) : 0.0;
+  const double sv = pw >= 0 ? win_prev(a, pw, l, r, nd) : 0.0;
+  return t0 + sv;
+}
+__global__ void __launch_bounds__(kWinThreads) k_taylor_win_count(WinArgs a, int64_t *cnt) {
+  extern __shared__ double wsm[];
+  const int ccnt = a.c1cnt;
+  int16_t *s_mc = reinterpret_cast<int16_t *>(wsm);
+  int16_t *s_mw = s_mc + ccnt;
+  for (int i = threadIdx.x; i < ccnt; i += blockDim.x) {
+    s_mc[i] = a.mapC[i];
+    s_mw[i] = a.mapW[i];
+  }
+  __syncthreads();
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= a.nrows) return;
+  const int64_t r = a.row0 + l;
+  int64_t c = 0;
+#pragma unroll 4
+  for (int q = 0; q < ccnt; q++) c += win_t0(a, s_mc, s_mw, q, l, r, a.nd) != 0.0;
+  cnt[l] = c;
+}
+constexpr int kWinWT = 256;  // write pass: 8 warps, 32 rows per CTA
+__global__ void __launch_bounds__(kWinWT) k_taylor_win_write(WinArgs a, const int64_t *rp_out, int32_t *col_out,
+                                                             double *val_out) {
+  extern __shared__ double wsm[];
+  const int ccnt = a.c1cnt;
+  double *tile = wsm;  // [32][33]
+  int16_t *s_mc = reinterpret_cast<int16_t *>(tile + 32 * 33);
+  int16_t *s_mw = s_mc + ccnt;
+  int32_t *s_off = reinterpret_cast<int32_t *>(s_mw + ccnt);  // 4 ccnt bytes after s_mc
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i < ccnt; i += blockDim.x) {
+    s_mc[i] = a.mapC[i];
+    s_mw[i] = a.mapW[i];
+    s_off[i] = a.coffs[i];
+  }
+  __syncthreads();
+  const int64_t lb = (int64_t)blockIdx.x * 32;
+  const int64_t lr = lb + lane;  // the row this lane loads
+  const bool lok = lr < a.nrows;
+  int64_t cur[4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const int64_t lw = lb + w * 4 + j;
+    cur[j] = lw < a.nrows ? rp_out[lw] : 0;
+  }
+  for (int q0 = 0; q0 < ccnt; q0 += 32) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int q = q0 + w * 4 + j;
+      tile[(w * 4 + j) * 33 + lane] = (lok && q < ccnt) ? win_t0(a, s_mc, s_mw, q, lr, a.row0 + lr, a.nd) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int rl = w * 4 + j;
+      const int64_t lw = lb + rl;
+      const double v = tile[lane * 33 + rl];
+      const unsigned m = __ballot_sync(FULL_MASK, v != 0.0);
+      if (v != 0.0 && lw < a.nrows) {
+        const int64_t p = cur[j] + __popc(m & lanemask_lt());
+        col_out[p] = (int32_t)(a.row0 + lw + s_off[q0 + lane]);
+        val_out[p] = v;
+      }
+      cur[j] += __popc(m);
+    }
+    __syncthreads();
+  }
+}
+void launch_taylor_win_final(const WinArgs &a, int64_t *cnt, const int64_t *rp_out, int32_t *col_out,
+                             double *val_out, cudaStream_t st) {
+  if (a.nrows == 0) return;
+  if (!rp_out) {
+    const int smem = a.c1cnt * 4 + 16;
+    cudaFuncSetAttribute(k_taylor_win_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    KL;
+    k_taylor_win_count<<<(unsigned)((a.nrows + kWinThreads - 1) / kWinThreads), kWinThreads, smem, st>>>(a, cnt);
+  } else {
+    const int smem = 32 * 33 * 8 + a.c1cnt * 8 + 32;
+    cudaFuncSetAttribute(k_taylor_win_write, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    KL;
+    k_taylor_win_write<<<(unsigned)((a.nrows + 31) / 32), kWinWT, smem, st>>>(a, rp_out, col_out, val_out);
+  }
+}
+// count of x[0..cnt) with |x| > tau (nnz of a term's kept band values)
+__global__ void k_count_above(const double *x, int64_t cnt, double tau, unsigned long long *out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    c += fabs(x[i]) > tau;
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+void launch_count_above(const double *x, int64_t cnt, double tau, unsigned long long *out, cudaStream_t st) {
+  cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  if (cnt == 0) return;
+  KL;
+  k_count_above<<<grid_for(cnt, kThreads, 148 * 8), kThreads, 0, st>>>(x, cnt, tau, out);
+}
+
 // out64[i] = in32[i] (plan-time helper, no host round trip)
 void launch_i32_to_i64(const int32_t *in, int64_t n, int64_t *out, cudaStream_t st) {
   if (n == 0) return;

@@ -134,6 +134,54 @@ int taylor_dia_smem_bytes(int slots);
 // Taylor term by diagonal push (bit-identical order); rows that do not fit -> fail_rows
 void launch_taylor_dia(const NumericArgs &a, const DiaView &D, int slots, int32_t *fail_rows,
                        int *fail_count, cudaStream_t st);
+// K5w: Taylor terms on the dense offset window (kernels.cu), position-major dense rows
+struct WinArgs {
+  int64_t nrows = 0, row0 = 0, n = 0;  // local rows, first global row, matrix order
+  int nd = 0;
+  const double *dia = nullptr;     // DiaView layout
+  const int32_t *doff = nullptr;   // descending
+  int dzero = -1;                  // index of the offset 0 in doff (-1: none)
+  int prev_is_h0 = 0;              // S~_{i-1} = H0 (i = 2; FINAL with m = 1): read from dia
+  const double *pS = nullptr;      // S~_{i-1}: [|W_{i-1}|][nrows]
+  double tau_prev = 0.0;           // S^_{i-1} keeps |x| > tau_prev
+  const double *T0old = nullptr;   // T^_0^(i-2): [|cum_{i-2}|][nrows]
+  double *T0new = nullptr;         // T^_0^(i-1): [|cum_{i-1}|][nrows] (TERM)
+  int c1cnt = 0;                   // |cum_{i-1}| (TERM) / |cum_m| (FINAL)
+  const int16_t *mapC = nullptr;   // per cum position: position in the previous cum, or -1
+  const int16_t *mapW = nullptr;   // per cum position: position in W_{i-1} (W_m), or -1
+  const int32_t *coffs = nullptr;  // per cum position: its offset (FINAL)
+  int ncnt = 0;                    // |W_i| (TERM)
+  const int32_t *rec = nullptr;    // TERM: per position t of W_i a record of element offsets
+                                   // (kernels.cu k_taylor_win; taylor_win_rec_words(nd) int32)
+  const double *dpad = nullptr;    // H0's diagonals zero-padded: h_d(k) = dpad[di * npad + k]
+                                   // (the pointer is at the padding's end: k may be negative)
+  int32_t hoff[kDiaMax] = {0};     // di * npad - d_di
+  int32_t hpad = 0;                // the padding (dpad - hpad is the array's start)
+  double *nS = nullptr;            // S~_i: [|W_i|][nrows]
+  double divisor = 1.0, floor_tau = 0.0, eps_g = 0.0;
+  double *band_val = nullptr;      // [band_cap][nrows] staged floor < |x| <= eps_g
+  int32_t *band_col = nullptr;
+  int64_t band_cap = 0;
+  unsigned long long *band_need = nullptr;  // atomicMax of a row's band count over band_cap
+  int64_t *row_cnt = nullptr, *row_nnz = nullptr, *row_c1 = nullptr;
+  double *row_fsum = nullptr, *row_p1 = nullptr;
+  unsigned long long *prod_count = nullptr;
+};
+// the TERM kernel is compiled for 1..9 and 16 diagonals; records are built for that count
+// (extra diagonals read the zero plane)
+inline int taylor_win_kernel_nd(int nd) { return nd <= 9 ? nd : kDiaMax; }
+int taylor_win_smem_bytes(int nd, int ncnt, int ccnt);
+int taylor_win_rec_words(int nd);
+void launch_taylor_win_t0(const WinArgs &a, cudaStream_t st);  // T^_0 update when 0 is not in D
+// persistent grid of ctas_per_sm CTAs per SM over tiles of 128 rows
+void launch_taylor_win(const WinArgs &a, int ctas_per_sm, int sms, cudaStream_t st);
+void launch_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val, double tau, double *rowsum,
+                          int64_t *rowcnt, cudaStream_t st);
+// FINAL: rp_out null -> per-row counts of T^_0 into cnt; else write T^_0's rows (CSR)
+void launch_taylor_win_final(const WinArgs &a, int64_t *cnt, const int64_t *rp_out, int32_t *col_out,
+                             double *val_out, cudaStream_t st);
+void launch_count_above(const double *x, int64_t cnt, double tau, unsigned long long *out, cudaStream_t st);
+
 // BSR-8 view (squarings on one GPU): conversion, block transpose, numeric kernel
 struct BsrView {
   int64_t nbr = 0;

@@ -357,12 +357,74 @@ def test_taylor_dia_bit_exact(B, name):
     assert st["taylor_fmas"] > 0
 
 
+@pytest.mark.parametrize("name", ["heat2d", "structural", "heat3d", "heat1d", "banded1d", "tiny"])
+def test_taylor_window_bit_exact(B, name):
+    """Unfiltered Taylor phase (filter off, N = 0) on the offset-window kernel K5w: every
+    term is a dense row over the Minkowski sums of H0's offsets, products summed with the
+    offsets descending (k ascending, the oracle's order) and divided by i, T^_0 accumulated
+    term by term -- E = I + T^_0 equals the oracle's bit for bit."""
+    from synth import structural_state_space, laplacian_3d
+    if name == "heat2d":
+        H = laplacian_2d(40, 40, 0.6, "pm10", seed=3)
+    elif name == "structural":
+        H = structural_state_space(12, 10, 0.5, seed=4)
+    elif name == "heat3d":
+        H = laplacian_3d(8, 7, 6, 0.25, "u0812", seed=5)
+    elif name == "heat1d":
+        H = tridiag(3001, 0.45, -0.9, 0.45)
+    elif name == "banded1d":  # 5 diagonals, ragged ends
+        H = random_banded(2000, 2, 1.0, 0.3, seed=6)
+    else:  # fewer rows than the window's offsets
+        H = tridiag(7, 0.45, -0.9, 0.45)
+    opts = dict(filter=0, force_N=0, force_M=9)
+    Eg, st = run_gpu(B, H, kernel=8, **opts)
+    Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS, **opts)
+    assert st["taylor_window"] == 1
+    assert np.array_equal(Eg.rowptr, Eo.rowptr) and np.array_equal(Eg.col, Eo.col)
+    assert np.array_equal(Eg.val, Eo.val)
+    assert st["taylor_fmas"] > 0
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_taylor_window_filtered_vs_oracle(B, cid):
+    """Filtered Taylor phase on K5w (default for these stencils): per term the same Algorithm
+    4.1 decisions as the oracle (nnz of S^_i, passes; tau within rounding of the pass sums),
+    and T^_0 (output_T with N = 0) within the north-star criteria."""
+    H = make_config(cid)
+    Eg, st, Eo, tr = run_both(B, H, force_N=0, output_T=True)
+    assert st["taylor_window"] == 1
+    assert st["M_eff"] == tr["M_eff"]
+    for i in range(2, tr["M_eff"] + 1):
+        assert st["taylor_nnz_unf"][i] == tr["taylor_nnz_unf"][i]
+        assert abs(int(st["taylor_nnz"][i]) - int(tr["taylor_nnz"][i])) <= max(2, tr["taylor_nnz"][i] // 10**6)
+        assert st["taylor_passes"][i] == tr["taylor_passes"][i]
+        assert st["taylor_tau"][i] == pytest.approx(tr["taylor_tau"][i], rel=1e-12)
+    assert_parity(Eg, st, Eo, tr)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_taylor_window_matches_dia(B, cid):
+    """The window kernel (8) and the diagonal push kernel (7) take the same Taylor-phase
+    decisions on the BASELINE configs (both reproduce the oracle's S~ bit for bit)."""
+    H = make_config(cid)
+    _, s8 = run_gpu(B, H, kernel=8)
+    _, s7 = run_gpu(B, H, kernel=7)
+    assert s8["taylor_window"] == 1 and s7["taylor_window"] == 0
+    M = s8["M_eff"]
+    assert M == s7["M_eff"]
+    for i in range(2, M + 1):
+        assert s8["taylor_nnz_unf"][i] == s7["taylor_nnz_unf"][i]
+        assert s8["taylor_nnz"][i] == s7["taylor_nnz"][i]
+        assert s8["taylor_tau"][i] == pytest.approx(s7["taylor_tau"][i], rel=1e-12)
+    assert s8["sq_nnz"][0] == s7["sq_nnz"][0]
+
+
 @pytest.mark.parametrize("cid", [1, 2, 3])
 def test_taylor_dia_default_matches_pull(B, cid):
     """Filtered runs through K5d (default) and the pull kernel (kernel=6) give the same
     Taylor-phase patterns (both reproduce the oracle's S~ bit for bit)."""
     H = make_config(cid)
-    _, s7 = run_gpu(B, H)
+    _, s7 = run_gpu(B, H, kernel=7)
     _, s6 = run_gpu(B, H, kernel=6)
     M = s7["M_eff"]
     assert M == s6["M_eff"]
