@@ -182,7 +182,10 @@ typedef struct {
   int64_t cache_hits, cache_misses, cache_releases;
   double cache_bytes_cached, cache_bytes_allocated;
   int32_t sq_order_used;                       /* squarings ran in: 0 index order, 1 BFS
-                                                  aggregates, 2 compact aggregates (sq_order) */
+                                                  aggregates, 2 compact aggregates (host
+                                                  thread), 3 diamond tiles of a 2D grid, 4
+                                                  2x2x2 cubes of a 3D grid (device, one GPU)
+                                                  (sq_order) */
   double sq_exchange_ms[SEXPM_MAXSTEP];        /* world > 1: halo exchange of the squaring
                                                   (host wall clock, incl. the peers' wait) */
   double ms_order_host;  /* the squarings' locality / aggregate order, computed on a host

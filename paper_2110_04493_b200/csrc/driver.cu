@@ -567,11 +567,14 @@ struct sexpm_plan_s {
     std::vector<int> lcnt, ccnt;      // |W_j|, |cum_j| (index j; ccnt[0] = 0)
     std::vector<int64_t> woff, coff;  // per term: start of its W-indexed / cum-indexed tables
     DBuf<int32_t> rec;                // TERM records (k_taylor_win), rw int32 per position
-    DBuf<int16_t> mapC, mapW;         // per cum position (T^_0 pass, FINAL)
+    DBuf<int16_t> neg1;               // -1 per cum position (FINAL when T^_0 is already complete)
+    DBuf<int16_t> mapC, mapW, cumU;   // per cum position (T^_0 pass, FINAL): U-index if in the
+                                      // previous cum (else -1), position in W_j (else -1), U-index
     DBuf<int32_t> coffs;
     DBuf<double> dpad;                // H0's diagonals zero-padded, plus a zero plane
-    DBuf<double> ck_t[2];  // T^_0 checkpoints (position-major), Taylor phase only; the S~
-                           // checkpoints live in Tn.val and E.val (idle until the squarings)
+    // T^_0 lives in place over U (position-major, plane u = offset U[u], plus a zero plane) in
+    // the BSR view's value buffer, the S~ checkpoints in Tn.val and E.val: all three idle
+    // until the squarings, so the Taylor phase maps no memory of its own
     DBuf<unsigned long long> cnt, need;
   } win;
   long long cache0[3] = {0, 0, 0};  // cache counters when the plan was created
@@ -592,7 +595,8 @@ struct sexpm_plan_s {
   DBuf<int64_t> tperm_loc, tinv_loc;  // this rank's rows (local indices)
   DBuf<int32_t> block_order_t;  // the aggregates (block rows in that order) in locality order
   bool sq_tiled = false;
-  int agg_kind = 0;  // 0 none, 1 BFS aggregates, 2 compact aggregates
+  int agg_kind = 0;  // 0 none, 1 BFS aggregates, 2 compact aggregates, 3 lattice diamonds, 4 lattice cubes
+  bool tperm_ready = false;  // tperm / tinv (/ _loc) hold the squarings' aggregate relabelling
   double order_host_ms = 0.0, order_wait_ms = 0.0;  // background ordering thread: duration, wait
   DBuf<int32_t> block_order;  // block rows of the block kernel in locality order
   // H0's BSR-8 view in fragment order with its block transpose (Taylor terms on K3m), built
@@ -1779,6 +1783,52 @@ static void build_diagonals(sexpm_plan_s &P) {
   CK(cudaStreamSynchronize(st));  // offs (host) is captured by value in the launch
 }
 
+// Grid structure of H0 from its diagonal offsets (row r = x + G y [+ G Gy z]): 2D when the
+// positive offsets are {1, G} with G | n, 3D when they are {1, G, G Gy} with G Gy | n.  Only a
+// heuristic for the squarings' row order: any H is handled correctly, a banded matrix that
+// merely looks like a grid just gets a less useful order.
+static bool detect_lattice(const sexpm_plan_s &P, LatticeDesc &L) {
+  if (P.dia_nd == 0 || getenv("SEXPM_NO_LATTICE")) return false;
+  std::vector<int64_t> pos;
+  for (int32_t d : P.h_dia_off)
+    if (d > 0) pos.push_back(d);
+  std::sort(pos.begin(), pos.end());
+  for (int32_t d : P.h_dia_off)  // symmetric offset set
+    if (std::find(P.h_dia_off.begin(), P.h_dia_off.end(), -d) == P.h_dia_off.end()) return false;
+  L = LatticeDesc{};
+  L.n = P.n;
+  if (pos.size() == 2 && pos[0] == 1 && pos[1] > 1 && P.n % pos[1] == 0 && P.n / pos[1] > 1) {
+    L.dims = 2;
+    L.G = pos[1];
+    L.Gy = P.n / pos[1];
+    L.GH = P.n;
+    L.Dp = 4 * ((L.Gy + 3) / 4);
+    const int64_t nu = (L.G + L.Gy - 2) / 4 + 1;
+    L.nv = (L.G - 1 + L.Dp) / 4 + 1;
+    L.nv16 = (L.nv + 15) / 16;
+    L.ntiles = nu * L.nv;
+    L.nsuper = ((nu + 15) / 16) * L.nv16;
+    return true;
+  }
+  if (pos.size() == 3 && pos[0] == 1 && pos[1] > 1 && pos[2] % pos[1] == 0 && pos[2] / pos[1] > 1 &&
+      P.n % pos[2] == 0 && P.n / pos[2] > 1) {
+    L.dims = 3;
+    L.G = pos[1];
+    L.Gy = pos[2] / pos[1];
+    L.GH = pos[2];
+    const int64_t Gz = P.n / pos[2];
+    L.ntx = (L.G + 1) / 2;
+    L.nty = (L.Gy + 1) / 2;
+    const int64_t ntz = (Gz + 1) / 2;
+    L.nx8 = (L.ntx + 7) / 8;
+    L.ny8 = (L.nty + 7) / 8;
+    L.ntiles = L.ntx * L.nty * ntz;
+    L.nsuper = L.nx8 * L.ny8 * ((ntz + 7) / 8);
+    return true;
+  }
+  return false;
+}
+
 // K5w tables (kernels.cu k_taylor_win): the offsets a row of S~_j can reach are the Minkowski
 // sums W_j = W_{j-1} + D (W_1 = D, H0's diagonal offsets), offsets with |o| >= n pruned (no
 // row has such a column).  U = W_1 u ... u W_M ascending; per U-index and diagonal the U-index
@@ -1847,13 +1897,14 @@ static void build_window(sexpm_plan_s &P) {
       maxc = std::max<int64_t>(maxc, (int64_t)cu.size());
     }
   }
-  if ((maxl + 1) * nl >= INT32_MAX || (maxc + 1) * nl >= INT32_MAX || (int64_t)(nd + 1) * npad >= INT32_MAX) return;
+  if ((maxl + 1) * nl >= INT32_MAX || (int64_t)(U.size() + 1) * nl >= INT32_MAX || (int64_t)(nd + 1) * npad >= INT32_MAX)
+    return;
   W.lcnt.assign((size_t)P.M + 1, 0);
   W.ccnt.assign((size_t)P.M + 1, 0);
   W.woff.assign((size_t)P.M + 2, 0);
   W.coff.assign((size_t)P.M + 2, 0);
   std::vector<int32_t> hrec, hco;
-  std::vector<int16_t> hmc, hmw;
+  std::vector<int16_t> hmc, hmw, hcu;
   std::vector<int64_t> cum, cum_prev, cum_prev2;
   for (int j = 1; j <= P.M; j++) {
     std::vector<int64_t> un;
@@ -1867,16 +1918,19 @@ static void build_window(sexpm_plan_s &P) {
     W.coff[j] = (int64_t)hco.size();
     if (j >= 2) {  // TERM launch i = j: records over W_j
       const int64_t zs = j == 2 ? (int64_t)nd * npad : (int64_t)W.lcnt[j - 1] * nl;  // zero planes
-      const int64_t zt = (int64_t)W.ccnt[j - 2] * nl;
+      const int64_t zt = (int64_t)nU * nl;  // T^_0's zero plane
       for (int64_t o : Wj[j]) {
         for (int di = 0; di < knd; di++) {
           const int p = di < nd ? pos(Wj[j - 1], o - D[di]) : -1;
           hrec.push_back((int32_t)(p < 0 ? zs : (j == 2 ? (int64_t)(nd - 1 - p) * npad : (int64_t)p * nl)));
         }
-        const int q = dzero >= 0 ? pos(cum_prev, o) : -1;  // T^_0 fused only when 0 is in D
+        // T^_0 (in place over U): written when o is in cum_{j-1} (fused only when 0 is in D),
+        // read back when o was already in cum_{j-2} (else the zero plane)
+        const int q = dzero >= 0 ? pos(cum_prev, o) : -1;
         const int pc = pos(cum_prev2, o);
-        hrec.push_back((int32_t)(q < 0 ? -1 : (int64_t)q * nl));
-        hrec.push_back((int32_t)(pc < 0 ? zt : (int64_t)pc * nl));
+        const int64_t uo = pos(U, o);
+        hrec.push_back((int32_t)(q < 0 ? -1 : uo * nl));
+        hrec.push_back((int32_t)(pc < 0 ? zt : uo * nl));
         hrec.push_back((int32_t)o);
         for (int w = knd + 3; w < rw; w++) hrec.push_back(0);
       }
@@ -1886,8 +1940,9 @@ static void build_window(sexpm_plan_s &P) {
     }
     for (int64_t o : cum) {
       hco.push_back((int32_t)o);
-      hmc.push_back((int16_t)pos(cum_prev, o));
+      hmc.push_back((int16_t)(pos(cum_prev, o) >= 0 ? pos(U, o) : -1));
       hmw.push_back((int16_t)pos(Wj[j], o));
+      hcu.push_back((int16_t)pos(U, o));
     }
   }
   int optin = 0;
@@ -1907,6 +1962,10 @@ static void build_window(sexpm_plan_s &P) {
   CK(cudaMemcpyAsync(W.mapC.p, hmc.data(), hmc.size() * 2, cudaMemcpyHostToDevice, st));
   W.mapW.alloc(std::max<size_t>(hmw.size(), 1), st);
   CK(cudaMemcpyAsync(W.mapW.p, hmw.data(), hmw.size() * 2, cudaMemcpyHostToDevice, st));
+  W.cumU.alloc(std::max<size_t>(hcu.size(), 1), st);
+  CK(cudaMemcpyAsync(W.cumU.p, hcu.data(), hcu.size() * 2, cudaMemcpyHostToDevice, st));
+  W.neg1.alloc((size_t)std::max<int64_t>(maxc, 1), st);
+  CK(cudaMemsetAsync(W.neg1.p, 0xff, (size_t)std::max<int64_t>(maxc, 1) * 2, st));  // int16 -1
   // zero-padded diagonals (+ a zero plane): h_d(k) for any k the window can form
   W.dpad.alloc((size_t)(nd + 1) * (size_t)npad, st);
   CK(cudaMemsetAsync(W.dpad.p, 0, (size_t)(nd + 1) * (size_t)npad * sizeof(double), st));
@@ -2363,6 +2422,37 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
       P.tinv_loc.ensure((size_t)std::max<int64_t>(nl, 1), st);
       P.block_order_t.ensure((size_t)std::max<int64_t>((P.n + 7) / 8, 1), st);
     }
+    LatticeDesc Ld;
+    if (P.world == 1 && P.o.sq_order == 1 && P.N >= 1 && !P.o.ssat && P.M >= 1 && detect_lattice(P, Ld)) {
+      // grid stencil on one GPU: the aggregate order is arithmetic, computed on the device
+      // (no host thread, no pattern download); row / block orders of the untiled kernels =
+      // index order
+      DBuf<unsigned> mask;
+      DBuf<int64_t> cnt, off;
+      DBuf<int32_t> key, scnt, cur;
+      DBuf<int> flag;
+      const int64_t nbt = (P.n + 7) / 8, big = std::max(std::max(2 * (Ld.ntiles + 1), Ld.nsuper + 1), nbt);
+      mask.alloc((size_t)Ld.ntiles, st);
+      cnt.alloc((size_t)big, st);
+      off.alloc((size_t)big, st);
+      key.alloc((size_t)nbt, st);
+      scnt.alloc((size_t)Ld.nsuper, st);
+      cur.alloc((size_t)Ld.nsuper, st);
+      flag.alloc(1, st);
+      w.scan_tmp.ensure((size_t)scan_tmp_elems(big) + 1, st);
+      launch_lattice_order(Ld, mask.p, cnt.p, off.p, w.scan_tmp.p, key.p, scnt.p, cur.p, flag.p, P.tperm.p,
+                           P.tinv.p, P.block_order_t.p, st);
+      REQUIRE(d2h(flag.p, st) == 0, SEXPM_EINTERNAL, "lattice order: a supertile holds more block rows than the segment sort");
+      CK(cudaMemcpyAsync(P.tperm_loc.p, P.tperm.p, P.n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(P.tinv_loc.p, P.tinv.p, P.n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      launch_iota_i32(nl, P.proc_order.p, st);
+      launch_iota_i32((nl + 7) / 8, P.block_order.p, st);
+      CK(cudaStreamSynchronize(st));  // the scratch buffers are local
+      P.tperm_ready = true;
+      P.agg_kind = Ld.dims == 2 ? 3 : 4;
+      P.order_pending = false;
+      mark("lattice order (device)");
+    } else {
     CK(cudaEventCreateWithFlags(&P.ev_pattern, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&P.ev_order, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&P.bg_st, cudaStreamNonBlocking));
@@ -2526,6 +2616,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
             CK(cudaMemcpyAsync(P.tperm_loc.p, ploc.data(), nloc * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
             CK(cudaMemcpyAsync(P.tinv_loc.p, iloc.data(), nloc * sizeof(int64_t), cudaMemcpyHostToDevice, P.bg_st));
             CK(cudaStreamSynchronize(P.bg_st));  // host vectors are local
+            P.tperm_ready = true;
           }
         }
         lap("done");
@@ -2537,6 +2628,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
         P.bg_err = "order thread failed";
       }
     });
+    }
   }
   mark("groups + upload");
   CK(cudaEventRecord(e1, st));
@@ -2574,12 +2666,12 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
     maxc = std::max(maxc, W.ccnt[j]);
   }
   DBuf<double> *ck_s[2] = {&P.Tn.val, &P.E.val};
-  if (P.M >= 2) {  // one extra (zero) plane each: the records' "absent" operand
-    for (int k = 0; k < 2; k++) {
-      ck_s[k]->ensure(nl1 * (size_t)(maxl + 1), st);
-      W.ck_t[k].ensure(nl1 * (size_t)(maxc + 1), st);
-    }
-  }
+  DBuf<double> &t0buf = w.bsrB.bval;
+  // one extra (zero) plane each: the records' "absent" operand
+  if (P.M >= 2)
+    for (int k = 0; k < 2; k++) ck_s[k]->ensure(nl1 * (size_t)(maxl + 1), st);
+  t0buf.ensure(nl1 * (size_t)(W.nU + 1), st);
+  CK(cudaMemsetAsync(t0buf.p + (size_t)W.nU * nl, 0, nl1 * sizeof(double), st));
   // band values staged in the staging pool (position-major, band_cap per row)
   // (a row of S~_i has at most |W_i| <= maxl values: sized for that, no term ever re-runs; the
   // pool is the squarings' staging pool, which is larger anyway)
@@ -2619,9 +2711,10 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
   cudaEvent_t k0, k1;
   CK(cudaEventCreate(&k0));
   CK(cudaEventCreate(&k1));
-  int sa = 0, ta = 0;  // ck_s[sa] = S~_{i-1}, ck_t[ta] = T^_0^(i-2)
+  int sa = 0;  // ck_s[sa] = S~_{i-1}
   double tau_prev = 0.0;
   int64_t prev_nnz_local = 0;
+  bool t0_complete = false;
   int M_eff = 1;
   if (getenv("SEXPM_STEP_LOG")) CK(cudaStreamSynchronize(st));
   const auto h_loop = std::chrono::steady_clock::now();
@@ -2632,17 +2725,17 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
     a.prev_is_h0 = i == 2;
     a.pS = ck_s[sa]->p;
     a.tau_prev = tau_prev;
-    a.T0old = W.ck_t[ta].p;
-    a.T0new = W.ck_t[ta ^ 1].p;
+    a.T0old = t0buf.p;  // in place
+    a.T0new = t0buf.p;
     a.c1cnt = W.ccnt[i - 1];
     a.mapC = W.mapC.p + W.coff[i - 1];
     a.mapW = W.mapW.p + W.coff[i - 1];
+    a.cumU = W.cumU.p + W.coff[i - 1];
     a.ncnt = W.lcnt[i];
     a.rec = W.rec.p + W.woff[i];
     a.nS = ck_s[sa ^ 1]->p;
     // zero planes of the inputs (absent operands)
     if (i > 2) CK(cudaMemsetAsync(ck_s[sa]->p + (size_t)W.lcnt[i - 1] * nl, 0, nl1 * sizeof(double), st));
-    CK(cudaMemsetAsync(W.ck_t[ta].p + (size_t)W.ccnt[i - 2] * nl, 0, nl1 * sizeof(double), st));
     if (W.dzero < 0) launch_taylor_win_t0(a, st);  // T^_0 update not fused
     a.divisor = (double)i;
     // floor lemma: K = n |W_i| bounds the entries of S~_i
@@ -2739,13 +2832,13 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
               (long long)nnz, passes, kms, bytes / (kms * 1e6), (long long)hi[2]);
     if (nnz == 0) {  // S^_i = 0: all later terms vanish
       if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();
+      t0_complete = true;  // this launch already added S^_{i-1}: T^_0 is final
       break;
     }
     M_eff = i;
     tau_prev = tau;
     prev_nnz_local = kept_local;
     sa ^= 1;
-    ta ^= 1;
     if (i < SEXPM_MAXSTEP) S.taylor_ms[i] = step_ms();
   }
   // T^_0 = T^_0^(m-1) + S^_m as CSR: count, scan, write
@@ -2756,10 +2849,14 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
     a.prev_is_h0 = m == 1;
     a.pS = ck_s[sa]->p;
     a.tau_prev = tau_prev;
-    a.T0old = W.ck_t[ta].p;
+    a.T0old = t0buf.p;
     a.c1cnt = W.ccnt[m];
     a.mapC = W.mapC.p + W.coff[m];
     a.mapW = W.mapW.p + W.coff[m];
+    if (t0_complete) {  // T^_0 = the buffer over cum_m as it stands
+      a.mapC = W.cumU.p + W.coff[m];
+      a.mapW = W.neg1.p;
+    }
     a.coffs = W.coffs.p + W.coff[m];
     launch_taylor_win_final(a, w.cnt.p, nullptr, nullptr, nullptr, st);
     T.nrows = nl;
@@ -2783,7 +2880,6 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
   cudaEventDestroy(k0);
   cudaEventDestroy(k1);
   // the checkpoints live for the Taylor phase only
-  for (int k = 0; k < 2; k++) W.ck_t[k].release();
   return M_eff;
 }
 
@@ -2904,7 +3000,7 @@ static void do_run(sexpm_plan_s &P) {
   P.sq_tiled = false;
   if (P.o.sq_order == 1 && P.N >= 1 && !P.o.ssat && P.M >= 1) {
     wait_order(P);
-    if (!P.h_tperm.empty()) {
+    if (P.tperm_ready) {
       permute_csr(P, T.view(), P.tperm_loc.p, P.tinv.p, Tn);  // row i <- row tperm[i], col c -> tinv[c]
       swap_csr(T, Tn);
       P.sq_tiled = true;

@@ -3901,7 +3901,7 @@ __global__ void __launch_bounds__(kWinThreads) k_taylor_win(WinArgs a) {
         op.x[di] = __ldg(xb + (uint32_t)rc[di]);
         op.h[di] = __ldg(hb + (hoff[di] + (uint32_t)op.o));
       }
-      op.t0 = __ldg(t0ob + (uint32_t)rc[ND + 1]);
+      op.t0 = t0ob[(uint32_t)rc[ND + 1]];  // plain load: T^_0 is updated in place
     };
     double fs = 0.0, q1 = 0.0;
     int nnzu = 0, c1 = 0, nb = 0;
@@ -3966,14 +3966,14 @@ __global__ void __launch_bounds__(kWinThreads) k_taylor_win_t0(WinArgs a) {
   const int64_t r = a.row0 + l;
   for (int q = 0; q < ccnt; q++) {
     const int pc = s_mc[q], pw = s_mw[q];
-    const double t0 = pc >= 0 ? __ldg(a.T0old + (size_t)pc * a.nrows + l) : 0.0;
+    const double t0 = pc >= 0 ? a.T0old[(size_t)pc * a.nrows + l] : 0.0;  // in place: plain load
     double sv = 0.0;
     if (pw >= 0) {
       sv = a.prev_is_h0 ? __ldg(a.dia + (size_t)(a.nd - 1 - pw) * (size_t)a.n + (size_t)r)
                         : __ldg(a.pS + (size_t)pw * a.nrows + l);
       if (!a.prev_is_h0 && !(fabs(sv) > a.tau_prev)) sv = 0.0;
     }
-    a.T0new[(size_t)q * a.nrows + l] = t0 + sv;
+    a.T0new[(size_t)a.cumU[q] * a.nrows + l] = t0 + sv;
   }
 }
 void launch_taylor_win_t0(const WinArgs &a, cudaStream_t st) {
@@ -4128,6 +4128,149 @@ void launch_taylor_win_final(const WinArgs &a, int64_t *cnt, const int64_t *rp_o
     KL;
     k_taylor_win_write<<<(unsigned)((a.nrows + 31) / 32), kWinWT, smem, st>>>(a, rp_out, col_out, val_out);
   }
+}
+// ------------------------------------------------------------------------------------
+// Squaring order for lattice-structured H (grid stencils; plan time, on the device): the
+// rows are relabelled into 8-row aggregates that tile the grid -- 2D: the diamond tiles
+// {0 <= x+y-4u < 4, 0 <= x-y+D-4v < 4} (8 lattice points each, the shape of the L1 balls the
+// iterates' rows cover: as few column blocks per block row as the host BFS aggregates),
+// 3D: 2 x 2 x 2 cubes.  Tiles are numbered line by line (u-major / z-major), so the relabelled
+// matrix keeps the bandwidth of the index order (the BSR build's per-block-row column span);
+// the block kernel's PROCESSING order takes the block rows supertile by supertile (16 x 16
+// diamonds / 8 x 8 x 8 cubes) for L2 locality of the block rows in flight.  Tiles cut by
+// the grid's boundary hold fewer rows: new index = (rows of earlier tiles) + (rank of the
+// row's cell among its tile's occupied cells) -- a mask pass, a count + scan, a placement.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void lattice_tile(const LatticeDesc &L, int64_t r, int64_t &tile, int &c,
+                                             int64_t &super) {
+  if (L.dims == 2) {
+    const int64_t x = r % L.G, y = r / L.G;
+    const int64_t sx = x + y, dx = x - y + L.Dp;
+    const int64_t u = sx >> 2, v = dx >> 2;
+    c = (int)((sx & 3) * 2 + ((dx & 3) >> 1));
+    tile = u * L.nv + v;
+    super = (u >> 4) * L.nv16 + (v >> 4);
+  } else {
+    const int64_t x = r % L.G, y = (r / L.G) % L.Gy, z = r / L.GH;
+    const int64_t tx = x >> 1, ty = y >> 1, tz = z >> 1;
+    c = (int)(((z & 1) << 2) | ((y & 1) << 1) | (x & 1));
+    tile = (tz * L.nty + ty) * L.ntx + tx;
+    super = ((tz >> 3) * L.ny8 + (ty >> 3)) * L.nx8 + (tx >> 3);
+  }
+}
+__global__ void k_lattice_mask(LatticeDesc L, unsigned *mask) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= L.n) return;
+  int64_t t, sp;
+  int c;
+  lattice_tile(L, r, t, c, sp);
+  atomicOr(&mask[t], 1u << c);
+}
+// per tile: 1 if full (8 rows) / the row count if partial, for the two scans below
+__global__ void k_lattice_counts(int64_t ntiles, const unsigned *mask, int64_t *full, int64_t *part) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int c = __popc(mask[t]);
+  full[t] = c == 8;
+  part[t] = c == 8 ? 0 : c;
+}
+// New index of row r.  Every 8-row group of the new numbering is one full tile, or 8 rows of
+// partial (boundary-cut) tiles taken in tile order and placed where the 8th of them appears:
+// groups before tile t = F_t (full tiles before t) + floor(P_t / 8) (completed partial groups,
+// P_t = partial rows before t).  So the block rows of the BSR view stay tile-aligned across
+// the boundary.
+__global__ void k_lattice_place(LatticeDesc L, const unsigned *mask, const int64_t *F, const int64_t *P,
+                                int64_t ntiles, int64_t *perm, int64_t *inv) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= L.n) return;
+  int64_t t, sp;
+  int c;
+  lattice_tile(L, r, t, c, sp);
+  const unsigned m = mask[t];
+  const int k = __popc(m & ((1u << c) - 1u));
+  int64_t ni;
+  if (__popc(m) == 8) {
+    ni = 8 * (F[t] + (P[t] >> 3)) + k;
+  } else {
+    const int64_t q = P[t] + k, g = q >> 3, last = 8 * g + 7;
+    // the tile holding the group's 8th row: the first j with P[j] > last, minus one
+    // (P has ntiles + 1 entries; none: the final, incomplete group goes after every tile)
+    int64_t lo = 0, hi = ntiles + 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (P[mid] > last) hi = mid;
+      else lo = mid + 1;
+    }
+    const int64_t istar = lo - 1;  // in [t, ntiles]
+    ni = 8 * (F[istar] + g) + (q & 7);
+  }
+  inv[r] = ni;
+  perm[ni] = r;
+}
+// processing order of the block rows: counting sort by the supertile of each block row's
+// first row, then each supertile's block rows sorted ascending (deterministic)
+__global__ void k_lattice_block_keys(LatticeDesc L, const int64_t *perm, int64_t nbt, int32_t *key,
+                                     int32_t *scnt) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbt) return;
+  int64_t t, sp;
+  int c;
+  lattice_tile(L, perm[8 * b], t, c, sp);
+  key[b] = (int32_t)sp;
+  atomicAdd(&scnt[sp], 1);
+}
+__global__ void k_lattice_block_scatter(int64_t nbt, const int32_t *key, const int64_t *start, int32_t *cur,
+                                        int64_t *x) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbt) return;
+  const int32_t k = key[b];
+  x[start[k] + atomicAdd(&cur[k], 1)] = b;
+}
+__global__ void k_i64_to_i32(const int64_t *in, int64_t n, int32_t *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int32_t)in[i];
+}
+__global__ void k_iota_i32(int64_t n, int32_t *x) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = (int32_t)i;
+}
+// scratch: mask ntiles u32; cnt and off 2 (ntiles + 1) i64 each (reused for the nsuper
+// supertiles and the block rows: sized >= max(2 (ntiles + 1), nsuper + 1, nbt)), key nbt i32,
+// scnt / cur nsuper i32, flag 1 int
+void launch_lattice_order(const LatticeDesc &L, unsigned *mask, int64_t *cnt, int64_t *off, int64_t *scan_tmp,
+                          int32_t *key, int32_t *scnt, int32_t *cur, int *flag, int64_t *perm, int64_t *inv,
+                          int32_t *border, cudaStream_t st) {
+  // cnt / off hold two arrays of ntiles + 1 each: [full | part] and their scans [F | P]
+  const int64_t nt1 = L.ntiles + 1;
+  cudaMemsetAsync(mask, 0, (size_t)L.ntiles * sizeof(unsigned), st);
+  KL;
+  k_lattice_mask<<<grid_for(L.n, kThreads), kThreads, 0, st>>>(L, mask);
+  KL;
+  k_lattice_counts<<<grid_for(L.ntiles, kThreads), kThreads, 0, st>>>(L.ntiles, mask, cnt, cnt + nt1);
+  launch_exclusive_scan(cnt, L.ntiles, off, scan_tmp, st);
+  launch_exclusive_scan(cnt + nt1, L.ntiles, off + nt1, scan_tmp, st);
+  KL;
+  k_lattice_place<<<grid_for(L.n, kThreads), kThreads, 0, st>>>(L, mask, off, off + nt1, L.ntiles, perm, inv);
+  const int64_t nbt = (L.n + 7) / 8;
+  cudaMemsetAsync(scnt, 0, (size_t)L.nsuper * sizeof(int32_t), st);
+  cudaMemsetAsync(cur, 0, (size_t)L.nsuper * sizeof(int32_t), st);
+  cudaMemsetAsync(flag, 0, sizeof(int), st);
+  KL;
+  k_lattice_block_keys<<<grid_for(nbt, kThreads), kThreads, 0, st>>>(L, perm, nbt, key, scnt);
+  KL;
+  k_i32_to_i64<<<grid_for(L.nsuper, kThreads), kThreads, 0, st>>>(scnt, L.nsuper, cnt);
+  launch_exclusive_scan(cnt, L.nsuper, off, scan_tmp, st);
+  KL;
+  k_lattice_block_scatter<<<grid_for(nbt, kThreads), kThreads, 0, st>>>(nbt, key, off, cur, cnt);
+  KL;
+  k_sort_segments_i64<<<(int)std::max<int64_t>(1, std::min<int64_t>(L.nsuper, 148 * 8)), 256, 0, st>>>(off, L.nsuper, cnt, flag);
+  KL;
+  k_i64_to_i32<<<grid_for(nbt, kThreads), kThreads, 0, st>>>(cnt, nbt, border);
+}
+void launch_iota_i32(int64_t n, int32_t *x, cudaStream_t st) {
+  if (n == 0) return;
+  KL;
+  k_iota_i32<<<grid_for(n, kThreads), kThreads, 0, st>>>(n, x);
 }
 // count of x[0..cnt) with |x| > tau (nnz of a term's kept band values)
 __global__ void k_count_above(const double *x, int64_t cnt, double tau, unsigned long long *out) {

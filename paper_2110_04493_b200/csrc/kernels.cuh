@@ -144,11 +144,12 @@ struct WinArgs {
   int prev_is_h0 = 0;              // S~_{i-1} = H0 (i = 2; FINAL with m = 1): read from dia
   const double *pS = nullptr;      // S~_{i-1}: [|W_{i-1}|][nrows]
   double tau_prev = 0.0;           // S^_{i-1} keeps |x| > tau_prev
-  const double *T0old = nullptr;   // T^_0^(i-2): [|cum_{i-2}|][nrows]
-  double *T0new = nullptr;         // T^_0^(i-1): [|cum_{i-1}|][nrows] (TERM)
+  const double *T0old = nullptr;   // T^_0 over U: [|U| + 1][nrows] (the last plane zero),
+  double *T0new = nullptr;         // updated in place (TERM: T0new == T0old)
   int c1cnt = 0;                   // |cum_{i-1}| (TERM) / |cum_m| (FINAL)
-  const int16_t *mapC = nullptr;   // per cum position: position in the previous cum, or -1
+  const int16_t *mapC = nullptr;   // per cum position: its U-index if in the previous cum, or -1
   const int16_t *mapW = nullptr;   // per cum position: position in W_{i-1} (W_m), or -1
+  const int16_t *cumU = nullptr;   // per cum position: its U-index (T^_0 is stored over U)
   const int32_t *coffs = nullptr;  // per cum position: its offset (FINAL)
   int ncnt = 0;                    // |W_i| (TERM)
   const int32_t *rec = nullptr;    // TERM: per position t of W_i a record of element offsets
@@ -181,6 +182,25 @@ void launch_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val
 void launch_taylor_win_final(const WinArgs &a, int64_t *cnt, const int64_t *rp_out, int32_t *col_out,
                              double *val_out, cudaStream_t st);
 void launch_count_above(const double *x, int64_t cnt, double tau, unsigned long long *out, cudaStream_t st);
+
+// squaring order of a lattice-structured H (kernels.cu): 2D diamond tiles / 3D cubes of 8 rows
+struct LatticeDesc {
+  int dims = 0;              // 2 or 3
+  int64_t n = 0;
+  int64_t G = 0, Gy = 0;     // extents of the first two dimensions (row r = x + G y [+ G Gy z])
+  int64_t GH = 0;            // G * Gy
+  int64_t Dp = 0;            // 2D: even shift making x - y + Dp >= 0
+  int64_t nv = 0, nv16 = 0;  // 2D: tiles / supertiles along v
+  int64_t ntx = 0, nty = 0;  // 3D: tiles along x, y
+  int64_t nx8 = 0, ny8 = 0;  // 3D: supertiles along x, y
+  int64_t ntiles = 0, nsuper = 0;
+};
+// perm[new] = old, inv[old] = new, border = the block rows in supertile order (see kernels.cu
+// for the scratch sizes)
+void launch_lattice_order(const LatticeDesc &L, unsigned *mask, int64_t *cnt, int64_t *off, int64_t *scan_tmp,
+                          int32_t *key, int32_t *scnt, int32_t *cur, int *flag, int64_t *perm, int64_t *inv,
+                          int32_t *border, cudaStream_t st);
+void launch_iota_i32(int64_t n, int32_t *x, cudaStream_t st);
 
 // BSR-8 view (squarings on one GPU): conversion, block transpose, numeric kernel
 struct BsrView {

@@ -570,6 +570,34 @@ def test_aggregate_order_matches_index_order(B, cid):
     assert sa["sq_block_products"][1:N + 1].sum() <= si["sq_block_products"][1:N + 1].sum()
 
 
+@pytest.mark.parametrize("name", ["heat2d", "heat2d_ragged", "heat3d"])
+def test_lattice_order_on_device(B, name, monkeypatch):
+    """Grid stencils on one GPU: the squarings' aggregate relabelling is computed on the
+    device (2D diamond tiles / 3D 2x2x2 cubes, sq_order_used 3 / 4) -- parity against the
+    oracle, and against the host-thread aggregates (SEXPM_NO_LATTICE); no more block products
+    than index order."""
+    from synth import laplacian_3d
+    if name == "heat2d":
+        H = laplacian_2d(64, 48, 1.0, "pm10", seed=11)
+    elif name == "heat2d_ragged":  # extents not multiples of the tiles (partial tiles)
+        H = laplacian_2d(37, 29, 0.8, "pm10", seed=12)
+    else:
+        H = laplacian_3d(18, 16, 14, 0.25, "u0812", seed=13)
+    Eg, st = run_gpu(B, H)
+    assert st["sq_order_used"] == (4 if name == "heat3d" else 3)
+    Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS)
+    assert_parity(Eg, st, Eo, tr)
+    monkeypatch.setenv("SEXPM_NO_LATTICE", "1")
+    Eh, sh = run_gpu(B, H)
+    assert sh["sq_order_used"] in (0, 1, 2)
+    ok, res = parity(Eg, Eh, max(st["sq_tau"][st["N"]], sh["sq_tau"][sh["N"]], 1e-300))
+    assert ok, res
+    monkeypatch.delenv("SEXPM_NO_LATTICE")
+    Ei, si = run_gpu(B, H, sq_order=0)
+    N = st["N"]
+    assert st["sq_block_products"][1:N + 1].sum() <= si["sq_block_products"][1:N + 1].sum()
+
+
 def test_aggregate_order_with_reorder(B):
     """Both relabellings at once (RCM of a scrambled input, then the aggregates of the
     squarings): parity against the oracle."""
