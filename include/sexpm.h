@@ -131,6 +131,14 @@ typedef struct {
                              terms too once their rows outgrow the diagonal kernel;
                              1 = the bit-exact block kernel 11 (DMUL + DADD in the oracle's
                              order: C~ bit-identical to the oracle's).  Only with kernel = 0. */
+  int32_t sym_squaring;   /* -1 = (default) auto: when H is bit-exactly symmetric, one GPU,
+                             kernel 0 / 13, not exact_products / ssat, the squarings compute
+                             only the output blocks J >= I of T~ = 2T + T^2 (symmetric for a
+                             symmetric T) and read the others as transposes (K3c count, K3s
+                             product, K3a row assembly; kernels.cuh SymOut), after making T^_0
+                             exactly symmetric from its upper triangle (reading R21: changes
+                             T^_0 by rounding only).  Falls back to the full product when a
+                             block row does not fit.  0 = off (the full product). */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
   void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
   void *nccl_comm;        /* communicator handle from sexpm_nccl_comm_init (NCCL) or
@@ -194,6 +202,9 @@ typedef struct {
   int32_t taylor_window; /* 1: the Taylor phase ran on the offset-window kernel K5w (dense
                             rows over the Minkowski sums of H0's diagonal offsets); 0: term
                             by term on the product kernels */
+  int32_t sq_sym_used;   /* squarings that ran on the symmetric path (sym_squaring) */
+  double sq_assemble_ms[SEXPM_MAXSTEP]; /* symmetric path: K3c count + K3a row assembly
+                                           (sq_kernel_ms is the product kernel K3s alone) */
 } sexpm_stats;
 
 /* sizes[0..3] = sizeof(sexpm_options), sizeof(sexpm_stats), sizeof(sexpm_csr_in),

@@ -54,7 +54,7 @@ class Options(C.Structure):
                 ("n_window", C.c_int32), ("force_M", C.c_int32), ("force_N", C.c_int32),
                 ("output_T", C.c_int32), ("window_cols", C.c_int32), ("kernel", C.c_int32),
                 ("ssat", C.c_int32), ("reorder", C.c_int32), ("sq_order", C.c_int32),
-                ("exact_products", C.c_int32), ("e_r", C.c_double),
+                ("exact_products", C.c_int32), ("sym_squaring", C.c_int32), ("e_r", C.c_double),
                 ("stream", C.c_void_p), ("nccl_comm", C.c_void_p)]
 
 
@@ -85,7 +85,8 @@ class Stats(C.Structure):
                 ("cache_releases", C.c_int64), ("cache_bytes_cached", C.c_double),
                 ("cache_bytes_allocated", C.c_double), ("sq_order_used", C.c_int32),
                 ("sq_exchange_ms", _F64), ("ms_order_host", C.c_double), ("ms_order_wait", C.c_double),
-                ("taylor_window", C.c_int32)]
+                ("taylor_window", C.c_int32), ("sq_sym_used", C.c_int32),
+                ("sq_assemble_ms", _F64)]
 
 
 _lib = None

@@ -490,6 +490,8 @@ struct StepReport {
   int64_t bsr_blocks = 0;  // blocks of the BSR-8 view (kernel 11)
   double block_products = 0.0;  // 8x8 block products executed (kernel 11)
   unsigned long long prof[12] = {0};  // grouped kernel phase clocks
+  float asm_ms = 0.f;  // symmetric path: K3c + K3a
+  bool sym = false;    // the product ran on the symmetric path
 };
 
 // BSR-8 view of a CSR matrix (k_bsr_build) and, optionally, its block transpose
@@ -532,6 +534,15 @@ struct Workspace {
   DBuf<int64_t> scan_tmp2;
   DBuf<double> bscr;
   int64_t pool_cap_hint = 0;
+  // symmetric squaring (K3c / K3s / K3a): per block row |cand(I)|, |cand(I) >= I| and their
+  // scans, the candidate lists and the upper output blocks
+  DBuf<int64_t> sym_nj, sym_nup, sym_cjoff, sym_oboff;
+  DBuf<int32_t> sym_cj, sym_wlo, sym_whi;
+  DBuf<unsigned long long> sym_bmask;
+  DBuf<double> sym_fsI;
+  DBuf<int64_t> sym_nzI;
+  DBuf<double> sym_bstore;
+  DBuf<int> sym_flag;
 };
 
 struct sexpm_plan_s {
@@ -595,6 +606,8 @@ struct sexpm_plan_s {
   DBuf<int64_t> tperm_loc, tinv_loc;  // this rank's rows (local indices)
   DBuf<int32_t> block_order_t;  // the aggregates (block rows in that order) in locality order
   bool sq_tiled = false;
+  bool h_sym = false;   // H bit-exactly symmetric (plan time)
+  bool sym_sq = false;  // this run squares on the symmetric path (option sym_squaring)
   int agg_kind = 0;  // 0 none, 1 BFS aggregates, 2 compact aggregates, 3 lattice diamonds, 4 lattice cubes
   bool tperm_ready = false;  // tperm / tinv (/ _loc) hold the squarings' aggregate relabelling
   double order_host_ms = 0.0, order_wait_ms = 0.0;  // background ordering thread: duration, wait
@@ -791,6 +804,105 @@ static double alg41_threshold(sexpm_plan_s &P, double eps_g, double F, bool fuse
   return (double)epsf;
 }
 
+// The symmetric squaring stage (option sym_squaring; kernels.cuh SymOut): K3c counts, scans
+// for the store layout, K3s products of the blocks J >= I, K3a rows.  Records k0 / k1 around
+// K3s (rep.kernel_ms) and the K3c + K3a time in rep.asm_ms.  Returns false (nothing staged;
+// the caller runs the full K3m) when a block row does not fit or the lists disagree.
+static bool sym_squaring_stage(sexpm_plan_s &P, const NumericArgs &nh, const BsrView &Bv, int64_t nr,
+                               bool long_lists, cudaEvent_t k0, cudaEvent_t k1, StepReport &rep) {
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  const int64_t nbr = Bv.nbr;
+  const size_t nb1 = (size_t)std::max<int64_t>(nbr, 1);
+  w.sym_nj.ensure(nb1, st);
+  w.sym_nup.ensure(nb1, st);
+  w.sym_wlo.ensure(nb1, st);
+  w.sym_whi.ensure(nb1, st);
+  w.sym_cjoff.ensure(nb1 + 1, st);
+  w.sym_oboff.ensure(nb1 + 1, st);
+  w.sym_flag.ensure(1, st);
+  w.scan_tmp2.ensure((size_t)scan_tmp_elems(nbr) + 1, st);
+  cudaEvent_t c0, c1, a0, a1;
+  CK(cudaEventCreate(&c0));
+  CK(cudaEventCreate(&c1));
+  CK(cudaEventCreate(&a0));
+  CK(cudaEventCreate(&a1));
+  CK(cudaEventRecord(c0, st));
+  CK(cudaMemsetAsync(w.sym_flag.p, 0, sizeof(int), st));
+  launch_sym_count(Bv, w.sym_nj.p, w.sym_nup.p, w.sym_wlo.p, w.sym_whi.p, w.sym_flag.p, st);
+  launch_exclusive_scan(w.sym_nj.p, nbr, w.sym_cjoff.p, w.scan_tmp2.p, st);
+  launch_exclusive_scan(w.sym_nup.p, nbr, w.sym_oboff.p, w.scan_tmp2.p, st);
+  int64_t tot[2];
+  int flag = 0;
+  CK(cudaMemcpyAsync(&tot[0], w.sym_cjoff.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[1], w.sym_oboff.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(c1, st));
+  CK(cudaStreamSynchronize(st));
+  bool ok = flag == 0 && tot[1] < ((int64_t)1 << 31);  // K3a's block indices are int32
+  if (ok) {  // the stores must fit beside the live buffers (else: the full product)
+    const double need = 4.0 * (double)tot[0] + 520.0 * (double)tot[1];
+    const double have_now = (double)(w.sym_cj.n * 4 + w.sym_bstore.n * 8 + w.sym_bmask.n * 8);
+    std::lock_guard<std::mutex> lk(cache::mu);
+    if (cache::budget == 0) {
+      size_t fr = 0, tt = 0;
+      cudaMemGetInfo(&fr, &tt);
+      cache::budget = (size_t)(0.90 * (double)tt);
+    }
+    const double headroom = (double)cache::budget - (cache::bytes_allocated - cache::bytes_cached);
+    if (need > have_now && 1.25 * need - have_now > 0.9 * headroom) ok = false;
+  }
+  if (ok) {
+    w.sym_cj.ensure((size_t)std::max<int64_t>(tot[0], 1), st);
+    w.sym_bstore.ensure((size_t)std::max<int64_t>(tot[1], 1) * 64, st);
+    SymOut so;
+    so.bstore = w.sym_bstore.p;
+    so.cj = w.sym_cj.p;
+    so.ob_off = w.sym_oboff.p;
+    so.cj_off = w.sym_cjoff.p;
+    so.nj = w.sym_nj.p;
+    so.nup = w.sym_nup.p;
+    so.wlo = w.sym_wlo.p;
+    w.sym_bmask.ensure((size_t)std::max<int64_t>(tot[1], 1), st);
+    w.sym_fsI.ensure(nb1, st);
+    w.sym_nzI.ensure(nb1, st);
+    so.bmask = w.sym_bmask.p;
+    so.fsI = w.sym_fsI.p;
+    so.nzI = w.sym_nzI.p;
+    so.whi = w.sym_whi.p;
+    so.flag = w.sym_flag.p;
+    CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
+    CK(cudaEventRecord(k0, st));
+    launch_numeric_bsrm_sym(nh, Bv, nr, w.bscr.p, so, st, long_lists);
+    CK(cudaEventRecord(k1, st));
+    CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ok = flag == 0;
+    if (ok) {  // K3a only over K3s's complete lists
+      CK(cudaEventRecord(a0, st));
+      launch_sym_assemble(nh, so, nbr, nr, P.sm_count * 4, st);
+      CK(cudaEventRecord(a1, st));
+      CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      ok = flag == 0;
+      float ms_c = 0.f, ms_a = 0.f;
+      CK(cudaEventElapsedTime(&ms_c, c0, c1));
+      CK(cudaEventElapsedTime(&ms_a, a0, a1));
+      rep.asm_ms = ms_c + ms_a;
+    }
+  }
+  if (!ok) {
+    if (getenv("SEXPM_STEP_LOG"))
+      fprintf(stderr, "[sexpm run] symmetric squaring handed to the full product (flag %d)\n", flag);
+    CK(cudaMemsetAsync(w.pool_used.p, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));  // K3s consumed the scheduler
+    CK(cudaEventRecord(k0, st));
+  }
+  for (cudaEvent_t e : {c0, c1, a0, a1}) cudaEventDestroy(e);
+  return ok;
+}
+
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
                             double div, double eps_g, DCsr &C, StepReport &rep,
                             const DCsr *BT = nullptr, bool add_identity = false,
@@ -901,6 +1013,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       1, std::min<int64_t>(nr, (int64_t)P.sm_count * P.paged_blocks_per_sm));
   int nfail_other = 0;  // rows finished by kernels other than the first (and its K5d retry)
   bool dia_launched = false;
+  bool sym_failed = false;  // the symmetric path could not hold this product: full K3m
   for (int attempt = 0;; attempt++) {
     nfail_other = 0;
     w.pool_col.ensure((size_t)cap, st);
@@ -1047,11 +1160,21 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           CK(cudaEventCreate(&k0));
           CK(cudaEventCreate(&k1));
           CK(cudaEventRecord(k0, st));
-          if (stage == 13)
+          // symmetric squaring: one GPU, T exactly symmetric (do_run), A = B
+          bool sym_done = false;
+          if (stage == 13 && P.sym_sq && sq_like && same && !taylor && nr == P.n && self == 2.0 &&
+              !sym_failed) {
+            sym_done = sym_squaring_stage(P, nh, Bv, nr, long_lists, k0, k1, rep);
+            if (!sym_done) sym_failed = true;
+            rep.sym = sym_done;
+          }
+          if (sym_done) {
+            // K3s + K3a staged every row
+          } else if (stage == 13)
             launch_numeric_bsrm(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st, long_lists);
           else
             launch_numeric_bsr(nh, Bv, nr, w.bscr.p, fout, w.fail_count.p, st);
-          CK(cudaEventRecord(k1, st));
+          if (!sym_done) CK(cudaEventRecord(k1, st));
           CK(cudaEventSynchronize(k1));
           CK(cudaEventElapsedTime(&rep.kernel_ms, k0, k1));
           cudaEventDestroy(k0);
@@ -2397,6 +2520,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   P.N = N;
   int normal = P.o.normal;
   if (normal < 0) normal = ((symflags & 1) == 0) || ((symflags & 2) == 0);
+  P.h_sym = (symflags & 1) == 0;
   P.normal = normal;
   filter_budgets(norm, normal, M, N, P.a, P.r0, P.eps_g0);
   if (!P.o.filter) P.eps_g0 = 0.0;
@@ -2858,6 +2982,7 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
       a.mapW = W.neg1.p;
     }
     a.coffs = W.coffs.p + W.coff[m];
+    a.sym = P.sym_sq ? 1 : 0;  // T^_0 exactly symmetric for the symmetric squarings (R21)
     launch_taylor_win_final(a, w.cnt.p, nullptr, nullptr, nullptr, st);
     T.nrows = nl;
     T.row0 = P.row_begin;
@@ -2919,6 +3044,10 @@ static void do_run(sexpm_plan_s &P) {
   P.dia_short_ok = 2 * ((int64_t)P.dia_dmax - P.dia_dmin) + 1 <= 64;
   P.taylor_block = false;
   const int64_t nl = P.row_end - P.row_begin;
+  // symmetric squarings (option sym_squaring, reading R21): H bit-exactly symmetric, one GPU,
+  // the tensor-core block kernel
+  P.sym_sq = P.o.sym_squaring != 0 && P.h_sym && P.world == 1 && !P.o.exact_products && !P.o.ssat &&
+             (P.o.kernel == 0 || P.o.kernel == 8 || P.o.kernel == 13) && P.N >= 1;
   DCsr &H0loc = P.H0loc;
   DCsr &T = P.T, &Tn = P.Tn, &Sc = P.S, &Sn = P.Sn;
   // ---- Taylor phase ----
@@ -2991,6 +3120,24 @@ static void do_run(sexpm_plan_s &P) {
     // tau = 0 keeps every entry (the merges never write zeros)
     launch_compact_write(nl, T.row0, T.rp.p, T.len.p, T.col.p, T.val.p, 0.0, Tn.rp.p, Tn.col.p,
                          Tn.val.p, w.rs.p, w.l1r.p, w.l2r.p, st);
+    swap_csr(T, Tn);
+  }
+  // symmetric squarings need T^_0 exactly symmetric: the window path wrote it so; otherwise
+  // keep (r, c) iff (c, r) is present, both with the upper triangle's value (R21)
+  if (P.sym_sq && M_eff >= 2 && !S.taylor_window) {
+    Workspace &w = P.ws;
+    w.cnt.ensure((size_t)std::max<int64_t>(nl, 1), st);
+    w.scan_tmp.ensure((size_t)scan_tmp_elems(nl) + 1, st);
+    launch_sym_intersect(T.view(), w.cnt.p, nullptr, nullptr, nullptr, st);
+    Tn.nrows = nl;
+    Tn.row0 = T.row0;
+    Tn.padded = false;
+    Tn.rp.ensure((size_t)nl + 1, st);
+    launch_exclusive_scan(w.cnt.p, nl, Tn.rp.p, w.scan_tmp.p, st);
+    Tn.nnz = d2h(Tn.rp.p + nl, st);
+    Tn.col.ensure((size_t)std::max<int64_t>(Tn.nnz, 1), st);
+    Tn.val.ensure((size_t)std::max<int64_t>(Tn.nnz, 1), st);
+    launch_sym_intersect(T.view(), nullptr, Tn.rp.p, Tn.col.p, Tn.val.p, st);
     swap_csr(T, Tn);
   }
   CK(cudaEventRecord(ev_taylor, st));
@@ -3082,6 +3229,8 @@ static void do_run(sexpm_plan_s &P) {
       S.sq_kernel_ms[i] = rep.kernel_ms > 0.f ? rep.kernel_ms : rep.first_ms;
       S.sq_bsr_blocks[i] = rep.bsr_blocks;
       S.sq_block_products[i] = rep.block_products;
+      S.sq_assemble_ms[i] = rep.asm_ms;
+      S.sq_sym_used += rep.sym ? 1 : 0;
       S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)dst.nnz + 16.0 * (double)nl;
     }
     if (getenv("SEXPM_STEP_LOG"))
@@ -3246,6 +3395,7 @@ int sexpm_options_init(sexpm_options *o) {
   o->reorder = 0;
   o->sq_order = 1;
   o->exact_products = 0;
+  o->sym_squaring = -1;
   o->e_r = 0.1;
   o->stream = nullptr;
   o->nccl_comm = nullptr;
@@ -3343,6 +3493,8 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
       b->sort_tmp.role = role++;
     }
     P->ws.bscr.role = role++;
+    P->ws.sym_bstore.role = role++;
+    P->ws.sym_cj.role = role++;
     REQUIRE(role <= cache::kRoles, SEXPM_EINTERNAL, "device-block cache: too many buffer roles");
   }
   {

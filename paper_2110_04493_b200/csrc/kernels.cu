@@ -2103,6 +2103,15 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
       : "d"(a), "d"(b));
 }
 
+// bit l of x to bit 2l
+__device__ __forceinline__ unsigned long long spread32(unsigned x) {
+  unsigned long long v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  return (v | (v << 1)) & 0x5555555555555555ull;
+}
 // spread 4 bits to the even positions of 8
 __device__ __forceinline__ unsigned spread4(unsigned m) {
   m = (m | (m << 2)) & 0x33u;
@@ -2111,17 +2120,20 @@ __device__ __forceinline__ unsigned spread4(unsigned m) {
 
 // kMPF block products' operands per set (two sets in flight), kMinB CTAs per SM: <2, 4> for
 // short match lists (2D: more warps), <4, 2> for long ones (3D: more loads per warp)
-template <int kMPF, int kMinB>
+// SYM (K3s, see kernels.cuh SymOut): only the output blocks J >= I, written raw to the block
+// store; cand(I) to the J store; classification and staging are left to K3a
+template <int kMPF, int kMinB, bool SYM = false>
 __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a, BsrView Bv, int64_t nrows,
                                                               double *scratch, int32_t *fail_rows,
-                                                              int *fail_count) {
+                                                              int *fail_count, SymOut so) {
   extern __shared__ __align__(16) unsigned char msm[];
   int32_t *mla = reinterpret_cast<int32_t *>(msm);                      // kMWarps * kMML
   int32_t *mlb = mla + kMWarps * kMML;                                  // kMWarps * kMML
   unsigned *kbits = reinterpret_cast<unsigned *>(mlb + kMWarps * kMML); // kMKWords
   unsigned *jbits = kbits + kMKWords;                                   // kMJWords
   uint16_t *kpref = reinterpret_cast<uint16_t *>(jbits + kMJWords);     // kMKWords
-  __shared__ int s_I, s_fail, s_nj, s_kmin, s_jmin, s_nkw, s_njw;
+  __shared__ int s_I, s_fail, s_nj, s_kmin, s_jmin, s_nkw, s_njw, s_nlow, s_sok;
+  __shared__ long long s_cjo, s_obo;
   __shared__ double s_fs[kMWarps][8], s_p1[kMWarps][8];
   __shared__ long long s_nz[kMWarps][8], s_c1[kMWarps][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2155,11 +2167,16 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
     if (tid == 0) {
       int fail = 0;
       int jmin = INT32_MAX, jmax = -1;
-      for (int i = 0; i < nr; i++) {
-        const int64_t r = r0 + i;
-        if (a.hi[r] >= a.lo[r]) {
-          jmin = min(jmin, a.lo[r] >> 3);
-          jmax = max(jmax, a.hi[r] >> 3);
+      if constexpr (SYM) {  // the block union's extent (K3c): cand(I) exactly symmetric
+        jmin = so.wlo[I];
+        jmax = so.whi[I];
+      } else {
+        for (int i = 0; i < nr; i++) {
+          const int64_t r = r0 + i;
+          if (a.hi[r] >= a.lo[r]) {
+            jmin = min(jmin, a.lo[r] >> 3);
+            jmax = max(jmax, a.hi[r] >> 3);
+          }
         }
       }
       const int kmin = na > 0 ? abcol[ab0] : 0, kmax = na > 0 ? abcol[ab1 - 1] : -1;
@@ -2174,6 +2191,14 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
     }
     __syncthreads();
     if (s_fail || na == 0 || s_njw == 0) {
+      if constexpr (SYM) {
+        if (tid == 0) {
+          if (s_fail || so.nj[I] != 0) atomicOr(so.flag, s_fail ? 1 : 2);
+          so.fsI[I] = 0.0;
+          so.nzI[I] = 0;
+        }
+        continue;
+      }
       if (tid < nr) {
         const int64_t r = r0 + tid;
         if (s_fail) {
@@ -2258,6 +2283,43 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
     const int nj = s_nj;
     const bool over = nj > kMJCap;
     if (over && a.prof && tid == 0) atomicAdd(&a.prof[4], 1ull);  // handed on: J count
+    int qbeg = 0;  // first output block computed (SYM: the first J >= I)
+    long long obo = 0;
+    if constexpr (SYM) {
+      if (tid == 0) {
+        int nlow = 0, sok = 0;
+        long long cjo = 0, ob = 0;
+        if (over) {
+          atomicOr(so.flag, 1);
+        } else {
+          int lo = 0, hi = nj;  // first J >= I in the ascending list
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (jlist[mid] < (int)I) lo = mid + 1;
+            else hi = mid;
+          }
+          nlow = lo;
+          // the layout from K3c's counts (scanned): both must agree with this list
+          cjo = so.cj_off[I];
+          ob = so.ob_off[I];
+          if (so.nj[I] != nj || so.nj[I] - so.nup[I] != nlow) atomicOr(so.flag, 2);
+          else sok = 1;
+        }
+        s_nlow = nlow;
+        s_sok = sok;
+        s_cjo = cjo;
+        s_obo = ob;
+      }
+      __syncthreads();
+      if (!s_sok) {
+        for (int i = tid; i < nkw; i += kMThreads) kbits[i] = 0u;
+        for (int i = tid; i < njw; i += kMThreads) jbits[i] = 0u;
+        continue;
+      }
+      for (int q = tid; q < nj; q += kMThreads) so.cj[s_cjo + q] = jlist[q];
+      qbeg = s_nlow;
+      obo = s_obo;
+    }
     // (3) output blocks, one warp each
     double fs = 0.0, q1 = 0.0;
     long long nz = 0, c1 = 0;
@@ -2265,7 +2327,7 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
     if (!over) {
       int32_t *wa = mla + warp * kMML;
       int32_t *wb = mlb + warp * kMML;
-      for (int q = warp; q < nj; q += kMWarps) {
+      for (int q = qbeg + warp; q < nj; q += kMWarps) {
         const int J = jlist[q];
         // two independent accumulator chains (even / odd matches), summed at the end: the
         // DMMAs of one output block are not one serial dependency chain
@@ -2357,6 +2419,34 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
         }
         x0 += y0;
         x1 += y1;
+        if constexpr (SYM) {
+          // lane l = 4g + t holds elements e = 2l, 2l + 1 = (g, 2t), (g, 2t + 1) of C_IJ.  The
+          // diagonal block owns its upper triangle (K3a mirrors it).  Kept entries (|x| above
+          // the floor) packed in element order at the block's slot, their 64-bit mask beside;
+          // dropped nonzeros only as sum x^2 and count, each entry counted for itself and its
+          // mirror (x 2 off the diagonal)
+          const bool dg = J == (int)I;
+          const double v0 = (!dg || 2 * t >= g) ? x0 : 0.0, v1 = (!dg || 2 * t + 1 >= g) ? x1 : 0.0;
+          const bool k0 = v0 != 0.0 && fabs(v0) > a.floor_tau, k1 = v1 != 0.0 && fabs(v1) > a.floor_tau;
+          const double m0 = (dg && 2 * t == g) ? 1.0 : 2.0, m1 = (dg && 2 * t + 1 == g) ? 1.0 : 2.0;
+          if (v0 != 0.0) {
+            nz += (long long)m0;
+            if (!k0) fs += m0 * (v0 * v0);
+          }
+          if (v1 != 0.0) {
+            nz += (long long)m1;
+            if (!k1) fs += m1 * (v1 * v1);
+          }
+          const unsigned long long msk = spread32(__ballot_sync(FULL_MASK, k0)) |
+                                         (spread32(__ballot_sync(FULL_MASK, k1)) << 1);
+          const int p0 = __popcll(msk & ((1ull << (2 * lane)) - 1ull));
+          const size_t blk = (size_t)(obo + q - qbeg);
+          double *slot = so.bstore + blk * 64;
+          if (k0) slot[p0] = v0;
+          if (k1) slot[p0 + (k0 ? 1 : 0)] = v1;
+          if (lane == 0) so.bmask[blk] = msk;
+          continue;
+        }
         if (a.divisor != 1.0) {  // Taylor term: (sum_k s_rk h_kj) / i (reading R7)
           x0 = __ddiv_rn(x0, a.divisor);
           x1 = __ddiv_rn(x1, a.divisor);
@@ -2394,6 +2484,28 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
       }
     }
     if (a.prof && lane == 0 && nbp) atomicAdd(&a.prof[0], nbp);
+    if constexpr (SYM) {  // the block row's dropped sum x^2 and nonzero count (warps in order)
+      fs = warp_sum(fs);
+      nz = warp_sum(nz);
+      if (lane == 0) {
+        s_fs[warp][0] = fs;
+        s_nz[warp][0] = nz;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double f = 0.0;
+        long long z = 0;
+        for (int w = 0; w < kMWarps; w++) {
+          f += s_fs[w][0];
+          z += s_nz[w][0];
+        }
+        so.fsI[I] = f;
+        so.nzI[I] = z;
+      }
+      for (int i = tid; i < nkw; i += kMThreads) kbits[i] = 0u;
+      for (int i = tid; i < njw; i += kMThreads) jbits[i] = 0u;
+      continue;
+    }
     // per-row sums: the 4 lanes of a row, then warps in fixed order
 #pragma unroll
     for (int o = 1; o < 4; o <<= 1) {
@@ -2483,11 +2595,305 @@ void launch_numeric_bsrm(const NumericArgs &a, const BsrView &Bv, int64_t nrows,
   KL;
   if (long_lists) {
     cudaFuncSetAttribute(k_numeric_bsrm<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_numeric_bsrm<4, 2><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
+    k_numeric_bsrm<4, 2><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count, SymOut{});
   } else {
     cudaFuncSetAttribute(k_numeric_bsrm<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_numeric_bsrm<2, 4><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count);
+    k_numeric_bsrm<2, 4><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, fail_rows, fail_count, SymOut{});
   }
+}
+void launch_numeric_bsrm_sym(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+                             const SymOut &so, cudaStream_t st, bool long_lists) {
+  if (Bv.nbr_a == 0) return;
+  const int smem = bsrm_numeric_smem_bytes();
+  KL;
+  if (long_lists) {
+    cudaFuncSetAttribute(k_numeric_bsrm<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_numeric_bsrm<4, 2, true><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, nullptr, nullptr, so);
+  } else {
+    cudaFuncSetAttribute(k_numeric_bsrm<2, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_numeric_bsrm<2, 4, true><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, nullptr, nullptr, so);
+  }
+}
+
+// K3c: per block row I of the symmetric squaring, |cand(I)| (the union of the block rows K of
+// the view at row I's block columns, and row I's own blocks -- K3m's candidate list) and how
+// many of them are >= I: exact sizes of K3s's stores, so its layout is a scan (no atomics).
+// Warp per block row, a 65536-block-column bitmap per warp; wider unions -> flag 1.
+constexpr int kSymCntWarps = 8, kSymCntWords = 2048;
+__global__ void __launch_bounds__(kSymCntWarps * 32) k_sym_count(BsrView Bv, int64_t *nj, int64_t *nup,
+                                                                 int32_t *wlo, int32_t *whi, int *flag) {
+  extern __shared__ unsigned scw[];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  unsigned *bm = scw + wi * kSymCntWords;
+  const int64_t I = (int64_t)blockIdx.x * kSymCntWarps + wi;
+  if (I >= Bv.nbr) return;
+  const int64_t a0 = Bv.brp[I], a1 = Bv.brp[I + 1];
+  // the union's extent (K3s's bitmap window): row I's own blocks and B's block rows K
+  int jlo = INT32_MAX, jhi = -1;
+  for (int64_t q = a0 + lane; q < a1; q += 32) {
+    const int K = Bv.bcol[q];
+    jlo = min(jlo, K);
+    jhi = max(jhi, K);
+    if (K < Bv.nbr && Bv.brp[K + 1] > Bv.brp[K]) {
+      jlo = min(jlo, Bv.bcol[Bv.brp[K]]);
+      jhi = max(jhi, Bv.bcol[Bv.brp[K + 1] - 1]);
+    }
+  }
+  jlo = __shfl_sync(FULL_MASK, warp_min(jlo), 0);
+  jhi = __shfl_sync(FULL_MASK, warp_max(jhi), 0);
+  if (lane == 0) {
+    wlo[I] = jlo;
+    whi[I] = jhi;
+  }
+  if (jhi < jlo) {
+    if (lane == 0) {
+      nj[I] = 0;
+      nup[I] = 0;
+    }
+    return;
+  }
+  const int nw = ((jhi - jlo) >> 5) + 1;
+  if (nw > kSymCntWords) {
+    if (lane == 0) {
+      atomicOr(flag, 1);
+      nj[I] = 0;
+      nup[I] = 0;
+    }
+    return;
+  }
+  for (int w = lane; w < nw; w += 32) bm[w] = 0u;
+  __syncwarp();
+  const int lim = nw * 32;
+  for (int64_t q = a0; q < a1; q++) {
+    const int K = Bv.bcol[q];
+    if (lane == 0 && K - jlo >= 0 && K - jlo < lim)
+      atomicOr(&bm[(K - jlo) >> 5], 1u << ((K - jlo) & 31));  // the 2T term
+    if (K < Bv.nbr)
+      for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
+        const int d = Bv.bcol[b] - jlo;
+        if (d >= 0 && d < lim) atomicOr(&bm[d >> 5], 1u << (d & 31));
+      }
+  }
+  __syncwarp();
+  const int iw = (int)I - jlo;  // bits >= iw are J >= I
+  int c = 0, u = 0;
+  for (int w = lane; w < nw; w += 32) {
+    const unsigned m = bm[w];
+    c += __popc(m);
+    const int b0 = w * 32;
+    if (b0 >= iw) u += __popc(m);
+    else if (b0 + 32 > iw) u += __popc(m >> (iw - b0));
+  }
+  c = __reduce_add_sync(FULL_MASK, c);
+  u = __reduce_add_sync(FULL_MASK, u);
+  if (lane == 0) {
+    nj[I] = c;
+    nup[I] = u;
+  }
+}
+void launch_sym_count(const BsrView &Bv, int64_t *nj, int64_t *nup, int32_t *wlo, int32_t *whi, int *flag,
+                      cudaStream_t st) {
+  if (Bv.nbr == 0) return;
+  const int smem = kSymCntWarps * kSymCntWords * 4;
+  cudaFuncSetAttribute(k_sym_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  KL;
+  k_sym_count<<<(unsigned)((Bv.nbr + kSymCntWarps - 1) / kSymCntWarps), kSymCntWarps * 32, smem, st>>>(Bv, nj, nup, wlo,
+                                                                                                   whi, flag);
+}
+
+// ------------------------------------------------------------------------------------
+// K3a: rows of the symmetric squaring from K3s's upper blocks (kernels.cuh SymOut).  One CTA
+// per block row I (persistent over I), warp i = row r = 8I + i.  The lower blocks C_JI (J < I)
+// are located once per block row (binary search of I in J's ascending list).  A row's values
+// in column order: column i of C_JI for J < I, the diagonal block C_II with (i, j < i) read as
+// its mirror (j, i) (T~ exactly symmetric), row i of C_IJ for J > I.  Each value x != 0 is
+// classified as in the product kernels' flush (Algorithm 4.1 floor and fused first pass);
+// the row is counted, reserved in the pool, then staged in a second pass over its values.
+// ------------------------------------------------------------------------------------
+constexpr int kAsmThreads = 256, kAsmLowCap = 4096;
+__global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, SymOut so, int64_t nbr,
+                                                                 int64_t nrows) {
+  __shared__ int32_t s_lidx[kAsmLowCap];
+  const int tid = threadIdx.x, lane = tid & 31, i = tid >> 5;
+  const unsigned long long colm = 0x0101010101010101ull << i;  // column i of a block
+  for (int64_t I = blockIdx.x; I < nbr; I += gridDim.x) {
+    const int nj = (int)so.nj[I], nlow = (int)(so.nj[I] - so.nup[I]);
+    const int32_t *cj = so.cj + so.cj_off[I];
+    const int64_t obo = so.ob_off[I];
+    if (nlow > kAsmLowCap) {
+      if (tid == 0) atomicOr(so.flag, 8);
+      continue;  // uniform per CTA; the host falls back to the full product
+    }
+    __syncthreads();  // the previous block row's s_lidx consumed
+    for (int p = tid; p < nlow; p += kAsmThreads) {
+      const int J = cj[p];
+      const int32_t *lj = so.cj + so.cj_off[J];
+      const int njJ = (int)so.nj[J], nlJ = (int)(so.nj[J] - so.nup[J]);
+      int lo = nlJ, hi = njJ;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (lj[mid] < (int)I) lo = mid + 1;
+        else hi = mid;
+      }
+      int idx = -1;
+      if (lo < njJ && lj[lo] == (int)I) idx = (int)(so.ob_off[J] + (lo - nlJ));
+      else atomicOr(so.flag, 4);
+      s_lidx[p] = idx;
+    }
+    __syncthreads();
+    const int64_t r = 8 * I + i;
+    if (r >= nrows) continue;
+    const bool hasdiag = nlow < nj && cj[nlow] == (int)I;
+    // block q of row i: its global index, mask, and the bits of row i's entries j = 0..7 (the
+    // element of the block: (j, i) for a lower block or j < i of the diagonal one, else (i, j))
+    auto blk_of = [&](int q, unsigned long long &m, int &kind) -> int64_t {
+      int64_t b;
+      if (q < nlow) {
+        b = s_lidx[q];
+        kind = 0;
+      } else {
+        b = obo + (q - nlow);
+        kind = (q == nlow && hasdiag) ? 1 : 2;
+      }
+      m = b >= 0 ? __ldg(so.bmask + b) : 0ull;
+      return b;
+    };
+    auto bit_of = [&](int kind, int j) { return (kind == 0 || (kind == 1 && j < i)) ? 8 * j + i : 8 * i + j; };
+    long long tot = 0;
+    for (int q0 = 0; q0 < nj; q0 += 32) {  // pass 1: kept counts from the masks
+      const int q = q0 + lane;
+      if (q < nj) {
+        unsigned long long m;
+        int kind;
+        blk_of(q, m, kind);
+        if (kind == 0) tot += __popcll(m & colm);
+        else if (kind == 2) tot += __popc((unsigned)(m >> (8 * i)) & 0xFFu);
+        else tot += __popcll(m & colm & ((1ull << (8 * i)) - 1ull)) + __popc((unsigned)(m >> (9 * i)) & (0xFFu >> i));
+      }
+    }
+    tot = __shfl_sync(FULL_MASK, warp_sum(tot), 0);  // warp_sum reduces into lane 0
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)tot);
+    off = __shfl_sync(FULL_MASK, off, 0);
+    const bool okp = (long long)off + tot <= a.pool_cap;
+    double q1 = 0.0;
+    long long c1 = 0;
+    if (okp) {  // pass 2: the kept values, in column order
+      long long pos = (long long)off;
+      for (int q0 = 0; q0 < nj; q0 += 32) {
+        const int q = q0 + lane;
+        unsigned long long m = 0;
+        int kind = 2;
+        int64_t b = 0;
+        unsigned rb = 0;  // row i's kept entries j (bits)
+        if (q < nj) {
+          b = blk_of(q, m, kind);
+#pragma unroll
+          for (int j = 0; j < 8; j++) rb |= (unsigned)((m >> bit_of(kind, j)) & 1ull) << j;
+        }
+        const int c = __popc(rb);
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL_MASK, x, o);
+          if (lane >= o) x += y;
+        }
+        if (c > 0) {
+          long long p = pos + x - c;
+          const int J = cj[q];
+          const double *slot = so.bstore + (size_t)b * 64;
+          while (rb) {
+            const int j = __ffs(rb) - 1;
+            rb &= rb - 1;
+            const int e = bit_of(kind, j);
+            const double v = __ldg(slot + __popcll(m & ((1ull << e) - 1ull)));
+            const double av = fabs(v);
+            if (av <= a.eps_g) q1 += v * v;
+            else c1++;
+            a.pool_col[p] = 8 * J + j;
+            a.pool_val[p] = v;
+            p++;
+          }
+        }
+        pos += __shfl_sync(FULL_MASK, x, 31);
+      }
+    }
+    q1 = warp_sum(q1);
+    c1 = warp_sum(c1);
+    if (lane == 0) {
+      if (!okp) atomicOr(a.flags, 1);
+      a.row_off[r] = (int64_t)off;
+      a.row_cnt[r] = tot;
+      // Algorithm 4.1's floor sum and the distinct count per block row (K3s), on its first row
+      a.row_fsum[r] = i == 0 ? so.fsI[I] : 0.0;
+      a.row_nnz[r] = i == 0 ? so.nzI[I] : 0;
+      if (a.row_p1) {
+        a.row_p1[r] = q1;
+        a.row_c1[r] = c1;
+      }
+    }
+  }
+}
+void launch_sym_assemble(const NumericArgs &a, const SymOut &so, int64_t nbr, int64_t nrows, int grid,
+                         cudaStream_t st) {
+  if (nbr == 0) return;
+  KL;
+  k_sym_assemble<<<grid, kAsmThreads, 0, st>>>(a, so, nbr, nrows);
+}
+
+// symmetric part from the upper triangle (kernels.cuh launch_sym_intersect); warp per row
+__device__ __forceinline__ int64_t csr_find(const CsrView &A, int64_t row, int32_t c) {
+  int64_t lo = A.rp[row], hi = A.rp[row + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (A.col[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < A.rp[row + 1] && A.col[lo] == c) ? lo : -1;
+}
+template <bool WRITE>
+__global__ void k_sym_intersect(CsrView A, int64_t *cnt, const int64_t *rp_out, int32_t *col_out,
+                                double *val_out) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= A.nrows) return;
+  const int64_t p0 = A.rp[r], p1 = A.rp[r + 1];
+  int64_t out = WRITE ? rp_out[r] : 0;
+  for (int64_t b = p0; b < p1; b += 32) {
+    const int64_t p = b + lane;
+    bool keep = false;
+    double v = 0.0;
+    if (p < p1) {
+      const int32_t c = A.col[p];
+      if (c >= r) {
+        keep = true;
+        v = A.val[p];
+      } else {
+        const int64_t q = csr_find(A, c, (int32_t)r);
+        if (q >= 0) {
+          keep = true;
+          v = A.val[q];
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(FULL_MASK, keep);
+    if (WRITE && keep) {
+      const int64_t o = out + __popc(m & lanemask_lt());
+      col_out[o] = A.col[p];
+      val_out[o] = v;
+    }
+    out += __popc(m);
+  }
+  if (!WRITE && lane == 0) cnt[r] = out;
+}
+void launch_sym_intersect(const CsrView &A, int64_t *cnt, const int64_t *rp_out, int32_t *col_out,
+                          double *val_out, cudaStream_t st) {
+  if (A.nrows == 0) return;
+  KL;
+  if (rp_out)
+    k_sym_intersect<true><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, cnt, rp_out, col_out, val_out);
+  else
+    k_sym_intersect<false><<<grid_for(A.nrows * 32, kThreads), kThreads, 0, st>>>(A, cnt, rp_out, col_out, val_out);
 }
 
 
@@ -4048,14 +4454,26 @@ __device__ __forceinline__ double win_t0(const WinArgs &a, const int16_t *mc, co
   const double sv = pw >= 0 ? win_prev(a, pw, l, r, nd) : 0.0;
   return t0 + sv;
 }
+// sym (one GPU, symmetric H, symmetric offset list): an entry below the diagonal (o < 0) is
+// read as its mirror (r + o, -o), position ccnt - 1 - q: T^_0 exactly symmetric (K3s input)
+__device__ __forceinline__ double win_t0s(const WinArgs &a, const int16_t *mc, const int16_t *mw,
+                                          const int32_t *offs, int q, int64_t l, int64_t r, int nd) {
+  if (a.sym) {
+    const int32_t o = offs[q];
+    if (o < 0) return l + o < 0 ? 0.0 : win_t0(a, mc, mw, a.c1cnt - 1 - q, l + o, r + o, nd);
+  }
+  return win_t0(a, mc, mw, q, l, r, nd);
+}
 __global__ void __launch_bounds__(kWinThreads) k_taylor_win_count(WinArgs a, int64_t *cnt) {
   extern __shared__ double wsm[];
   const int ccnt = a.c1cnt;
-  int16_t *s_mc = reinterpret_cast<int16_t *>(wsm);
+  int32_t *s_off = reinterpret_cast<int32_t *>(wsm);
+  int16_t *s_mc = reinterpret_cast<int16_t *>(s_off + ccnt);
   int16_t *s_mw = s_mc + ccnt;
   for (int i = threadIdx.x; i < ccnt; i += blockDim.x) {
     s_mc[i] = a.mapC[i];
     s_mw[i] = a.mapW[i];
+    s_off[i] = a.coffs[i];
   }
   __syncthreads();
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -4063,7 +4481,7 @@ __global__ void __launch_bounds__(kWinThreads) k_taylor_win_count(WinArgs a, int
   const int64_t r = a.row0 + l;
   int64_t c = 0;
 #pragma unroll 4
-  for (int q = 0; q < ccnt; q++) c += win_t0(a, s_mc, s_mw, q, l, r, a.nd) != 0.0;
+  for (int q = 0; q < ccnt; q++) c += win_t0s(a, s_mc, s_mw, s_off, q, l, r, a.nd) != 0.0;
   cnt[l] = c;
 }
 constexpr int kWinWT = 256;  // write pass: 8 warps, 32 rows per CTA
@@ -4095,7 +4513,7 @@ __global__ void __launch_bounds__(kWinWT) k_taylor_win_write(WinArgs a, const in
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       const int q = q0 + w * 4 + j;
-      tile[(w * 4 + j) * 33 + lane] = (lok && q < ccnt) ? win_t0(a, s_mc, s_mw, q, lr, a.row0 + lr, a.nd) : 0.0;
+      tile[(w * 4 + j) * 33 + lane] = (lok && q < ccnt) ? win_t0s(a, s_mc, s_mw, s_off, q, lr, a.row0 + lr, a.nd) : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -4118,7 +4536,7 @@ void launch_taylor_win_final(const WinArgs &a, int64_t *cnt, const int64_t *rp_o
                              double *val_out, cudaStream_t st) {
   if (a.nrows == 0) return;
   if (!rp_out) {
-    const int smem = a.c1cnt * 4 + 16;
+    const int smem = a.c1cnt * 8 + 16;
     cudaFuncSetAttribute(k_taylor_win_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     KL;
     k_taylor_win_count<<<(unsigned)((a.nrows + kWinThreads - 1) / kWinThreads), kWinThreads, smem, st>>>(a, cnt);

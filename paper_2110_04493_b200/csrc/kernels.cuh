@@ -151,6 +151,7 @@ struct WinArgs {
   const int16_t *mapW = nullptr;   // per cum position: position in W_{i-1} (W_m), or -1
   const int16_t *cumU = nullptr;   // per cum position: its U-index (T^_0 is stored over U)
   const int32_t *coffs = nullptr;  // per cum position: its offset (FINAL)
+  int sym = 0;                     // FINAL: lower entries read as their mirrors (K3s input)
   int ncnt = 0;                    // |W_i| (TERM)
   const int32_t *rec = nullptr;    // TERM: per position t of W_i a record of element offsets
                                    // (kernels.cu k_taylor_win; taylor_win_rec_words(nd) int32)
@@ -249,6 +250,41 @@ constexpr int kBsrMBlocksPerSm = 4, kBsrMBlocksPerSmLong = 2, kBsrMLongRow = 200
 int bsrm_numeric_smem_bytes();
 void launch_numeric_bsrm(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                          int32_t *fail_rows, int *fail_count, cudaStream_t st, bool long_lists);
+
+// K3s: the squaring of an exactly symmetric iterate T (T~ = 2T + T^2 is symmetric): K3m over
+// the output blocks J >= I of every block row only.  Per block row I the candidate list
+// cand(I) (all J, ascending) goes to cj[cj_off[I] ..), nlow[I] of them below I; the upper
+// blocks C_IJ (raw, row-major 8 x 8) to bstore[(ob_off[I] + q - nlow[I]) * 64 ..].
+// K3a then assembles every row r = 8I + i in column order -- column i of C_JI for J < I
+// (found in J's list), the diagonal block mirrored from its upper triangle, row i of C_IJ
+// for J > I -- classifies (Algorithm 4.1 floor, fused first pass) and stages exactly like the
+// full kernels, so Algorithm 4.1 and the compaction run unchanged.
+struct SymOut {
+  double *bstore = nullptr;               // per upper block: its kept values, packed
+  unsigned long long *bmask = nullptr;    // per upper block: kept elements (bit 8 row + col)
+  double *fsI = nullptr;                  // per block row: dropped sum x^2 (mirrors counted)
+  int64_t *nzI = nullptr;                 // per block row: distinct nonzeros (mirrors counted)
+  int32_t *cj = nullptr;
+  const int64_t *ob_off = nullptr, *cj_off = nullptr;  // scans of K3c's counts
+  const int64_t *nj = nullptr, *nup = nullptr;         // K3c: |cand(I)|, |cand(I) >= I|
+  const int32_t *wlo = nullptr, *whi = nullptr;        // K3c: the union's block-column extent
+  int *flag = nullptr;  // 1: a block row K3s or K3c could not hold, 2: K3s's list differs from
+                        // K3c's count, 4: pattern not symmetric (a lower block missing from its
+                        // mirror's list), 8: K3a's lower-list cap
+};
+// K3c: nj[I] = |cand(I)|, nup[I] = |cand(I) >= I| over the view's block rows (A = B)
+// and the union's block-column extent [wlo, whi] (K3s's window: cand(I) is then the exact block
+// union, symmetric for a symmetric block pattern)
+void launch_sym_count(const BsrView &Bv, int64_t *nj, int64_t *nup, int32_t *wlo, int32_t *whi, int *flag,
+                      cudaStream_t st);
+void launch_numeric_bsrm_sym(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
+                             const SymOut &so, cudaStream_t st, bool long_lists);
+void launch_sym_assemble(const NumericArgs &a, const SymOut &so, int64_t nbr, int64_t nrows, int grid,
+                         cudaStream_t st);
+// T := the symmetric part read from the upper triangle: entry (r, c) kept iff (c, r) is
+// present, value T(min(r,c), max(r,c)) (binary search in row c); count pass (cnt) or write
+void launch_sym_intersect(const CsrView &A, int64_t *cnt, const int64_t *rp_out, int32_t *col_out,
+                          double *val_out, cudaStream_t st);
 
 // --- K6 Algorithm 4.1 pass -------------------------------------------------------
 // out[0] = sum over x[0..cnt) of x^2 for |x| <= tau (deterministic order for fixed layout)

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--exact", type=int, default=0)
     ap.add_argument("--sq-order", type=int, default=1)
+    ap.add_argument("--sym", type=int, default=-1)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -29,7 +30,8 @@ def main():
     rp, ci, va = (torch.from_numpy(x).to(dev) for x in (H.rowptr, H.col, H.val))
     for rep in range(args.repeat):
         p = B.Plan(H.n, rp, ci, va, args.eps_tol, plan_norm=args.plan_norm, kernel=args.kernel,
-                   exact_products=args.exact, sq_order=args.sq_order)
+                   exact_products=args.exact, sq_order=args.sq_order,
+                   sym_squaring=args.sym)
         p.run_only()
         st = p.stats()
         p.close()
@@ -47,7 +49,8 @@ def main():
                          f"taylor_fallback {[int(x) for x in st['taylor_fallback_rows'][2:int(st['M_eff']) + 1]]}\n")
         sys.stderr.write(f"  sq_kernel_ms {[round(float(x), 1) for x in st['sq_kernel_ms'][1:N + 1]]} "
                          f"block products {[float(x) for x in st['sq_block_products'][1:N + 1]]} "
-                         f"fmas {[float(x) for x in st['sq_fmas'][1:N + 1]]}\n")
+                         f"fmas {[float(x) for x in st['sq_fmas'][1:N + 1]]} sym {st['sq_sym_used']} "
+                         f"assemble_ms {[round(float(x), 1) for x in st['sq_assemble_ms'][1:N + 1]]}\n")
     M, N = int(st["M"]), int(st["N"])
     out = {k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in st.items()}
     for k, v in list(out.items()):
