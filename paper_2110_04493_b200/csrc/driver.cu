@@ -540,7 +540,7 @@ struct Workspace {
   DBuf<int32_t> sym_cj, sym_wlo, sym_whi;
   DBuf<unsigned long long> sym_bmask;
   DBuf<double> sym_fsI;
-  DBuf<int64_t> sym_nzI;
+  DBuf<int64_t> sym_nzI, sym_rowcnt, sym_rowoff;
   DBuf<double> sym_bstore;
   DBuf<int> sym_flag;
 };
@@ -727,6 +727,7 @@ static void wait_order(sexpm_plan_s &P) {
 // row-major (K3b) or fragment order (K3m), and its block transpose when asked.  Returns false
 // (nothing built) when a block row spans more block columns than k_bsr_build's bitmap, or
 // the view would not fit K3m's 32-bit block indices.
+static void bsr_transpose(sexpm_plan_s &P, BsrBufs &b);
 static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpose, BsrBufs &b) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
@@ -751,7 +752,17 @@ static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpo
   b.bcol.ensure(nb1, st);
   b.bval.ensure(nb1 * 64, st);
   launch_bsr_fill(M, nbr, b.brp.p, b.bcol.p, b.bval.p, w.flags.p, st, frag);
-  if (transpose) {
+  if (transpose) bsr_transpose(P, b);
+  return true;
+}
+
+// the block transpose of a built view (column J's block rows K ascending, their block index)
+static void bsr_transpose(sexpm_plan_s &P, BsrBufs &b) {
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  const int64_t nbr = b.nbr, nbc = (P.n + 7) / 8;
+  const size_t nb1 = (size_t)std::max<int64_t>(b.nb, 1);
+  {
     b.tcnt.ensure((size_t)nbc + 1, st);
     b.tp.ensure((size_t)nbc + 1, st);
     b.cnt64.ensure((size_t)nbc + 1, st);
@@ -766,7 +777,6 @@ static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpo
                          b.keys_tmp.p, st);
     b.transposed = true;
   }
-  return true;
 }
 
 // Algorithm 4.1: the scalar threshold recurrence on the host over the staged
@@ -808,7 +818,7 @@ static double alg41_threshold(sexpm_plan_s &P, double eps_g, double F, bool fuse
 // for the store layout, K3s products of the blocks J >= I, K3a rows.  Records k0 / k1 around
 // K3s (rep.kernel_ms) and the K3c + K3a time in rep.asm_ms.  Returns false (nothing staged;
 // the caller runs the full K3m) when a block row does not fit or the lists disagree.
-static bool sym_squaring_stage(sexpm_plan_s &P, const NumericArgs &nh, const BsrView &Bv, int64_t nr,
+static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &Bv, int64_t nr,
                                bool long_lists, cudaEvent_t k0, cudaEvent_t k1, StepReport &rep) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
@@ -869,17 +879,35 @@ static bool sym_squaring_stage(sexpm_plan_s &P, const NumericArgs &nh, const Bsr
     so.bmask = w.sym_bmask.p;
     so.fsI = w.sym_fsI.p;
     so.nzI = w.sym_nzI.p;
+    w.sym_rowcnt.ensure((size_t)std::max<int64_t>(nr, 1), st);
+    w.sym_rowoff.ensure((size_t)nr + 1, st);
+    w.scan_tmp.ensure((size_t)scan_tmp_elems(nr) + 1, st);
+    so.rowcnt = w.sym_rowcnt.p;
+    so.rowoff = w.sym_rowoff.p;
+    CK(cudaMemsetAsync(w.sym_rowcnt.p, 0, (size_t)nr * sizeof(int64_t), st));
     so.whi = w.sym_whi.p;
     so.flag = w.sym_flag.p;
     CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
     CK(cudaEventRecord(k0, st));
     launch_numeric_bsrm_sym(nh, Bv, nr, w.bscr.p, so, st, long_lists);
     CK(cudaEventRecord(k1, st));
+    // the rows' pool offsets: a scan of K3s's kept counts (deterministic layout)
+    CK(cudaEventRecord(a0, st));
+    launch_exclusive_scan(w.sym_rowcnt.p, nr, w.sym_rowoff.p, w.scan_tmp.p, st);
+    int64_t total = 0;
     CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&total, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     ok = flag == 0;
+    if (ok && total > nh.pool_cap) {  // exact size known: grow the pool, no re-run
+      w.pool_col.ensure((size_t)total, st);
+      w.pool_val.ensure((size_t)total, st);
+      nh.pool_col = w.pool_col.p;
+      nh.pool_val = w.pool_val.p;
+      nh.pool_cap = (int64_t)std::min(w.pool_col.n, w.pool_val.n);
+    }
     if (ok) {  // K3a only over K3s's complete lists
-      CK(cudaEventRecord(a0, st));
+      CK(cudaMemcpyAsync(w.pool_used.p, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
       launch_sym_assemble(nh, so, nbr, nr, P.sm_count * 4, st);
       CK(cudaEventRecord(a1, st));
       CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1116,6 +1144,7 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           const int64_t nbr_a = (nr + 7) / 8;
           const bool taylor = !sq_like;
           bool ok_view;
+          bool sym_try = false;
           if (taylor && B.rp != P.H0full.rp.p) {
             ok_view = false;  // a product with any other B: its view is not kept
           } else if (taylor) {
@@ -1123,7 +1152,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
               P.h0bsr_state = build_bsr(P, P.H0full.view(), true, true, P.h0bsr) ? 1 : -1;
             ok_view = P.h0bsr_state == 1 && build_bsr(P, A, true, false, w.bsrA);
           } else {
-            ok_view = build_bsr(P, B, stage == 13, true, w.bsrB);
+            // the symmetric kernel reads B_KJ as B_JK^T: no block transpose (built on fallback)
+            sym_try = stage == 13 && P.sym_sq && same && nr == P.n && self == 2.0 && !sym_failed;
+            ok_view = build_bsr(P, B, stage == 13, !sym_try, w.bsrB);
             // K3b holds a row of A in shared memory
             if (ok_view && stage == 11 && w.bsrB.bmax > kBsrMaxRowBlocks) ok_view = false;
           }
@@ -1162,11 +1193,17 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           CK(cudaEventRecord(k0, st));
           // symmetric squaring: one GPU, T exactly symmetric (do_run), A = B
           bool sym_done = false;
-          if (stage == 13 && P.sym_sq && sq_like && same && !taylor && nr == P.n && self == 2.0 &&
-              !sym_failed) {
+          if (sym_try) {
             sym_done = sym_squaring_stage(P, nh, Bv, nr, long_lists, k0, k1, rep);
-            if (!sym_done) sym_failed = true;
             rep.sym = sym_done;
+            if (!sym_done) {  // the full K3m: it needs the block transpose
+              sym_failed = true;
+              bsr_transpose(P, w.bsrB);
+              Bv.tp = w.bsrB.tp.p;
+              Bv.tk = w.bsrB.tk.p;
+              Bv.tb = w.bsrB.tb.p;
+              CK(cudaEventRecord(k0, st));
+            }
           }
           if (sym_done) {
             // K3s + K3a staged every row

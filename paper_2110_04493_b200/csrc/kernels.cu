@@ -2323,6 +2323,7 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
     // (3) output blocks, one warp each
     double fs = 0.0, q1 = 0.0;
     long long nz = 0, c1 = 0;
+    int rkept = 0;  // SYM: kept entries of row g over this lane's output blocks
     unsigned long long nbp = 0;
     if (!over) {
       int32_t *wa = mla + warp * kMML;
@@ -2341,7 +2342,9 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
             x1 = a.self_coef * __ldg(ap + soff1);
           }
         }
-        const int64_t t0 = Bv.tp[J], t1 = Bv.tp[J + 1];
+        // column J's block rows K: the block transpose, or (SYM: exactly symmetric T, one
+        // view) row J's own block columns, B_KJ read as the transpose of B_JK
+        const int64_t t0 = SYM ? Bv.brp[J] : Bv.tp[J], t1 = SYM ? Bv.brp[J + 1] : Bv.tp[J + 1];
         int64_t tb0 = t0;
         while (tb0 < t1) {
           // matches K of row I and column J (ascending K), listed in batches (32-bit block
@@ -2351,10 +2354,10 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
             const int64_t tt = tb0 + lane;
             int ra = -1, bidx = 0;
             if (tt < t1) {
-              const int kb = Bv.tk[tt] + (int)Bv.kb0 - kmin;
+              const int kb = (SYM ? Bv.bcol[tt] : Bv.tk[tt] + (int)Bv.kb0) - kmin;
               if (kb >= 0 && kb < nkw * 32 && ((kbits[kb >> 5] >> (kb & 31)) & 1u)) {
                 ra = kpref[kb >> 5] + __popc(kbits[kb >> 5] & ((1u << (kb & 31)) - 1u));
-                bidx = (int)Bv.tb[tt];
+                bidx = SYM ? (int)tt : (int)Bv.tb[tt];
               }
             }
             const unsigned m = __ballot_sync(FULL_MASK, ra >= 0);
@@ -2376,9 +2379,15 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
   _Pragma("unroll") for (int d = 0; d < kMPF; d++) {                           \
     const int e = min((base) + d, last);                                       \
     A_[d] = __ldg(av2 + (size_t)wa[e] * 32 + lane);                            \
-    const double *bp = Bv.bval + (size_t)wb[e] * 64 + boff;                    \
-    L_[d] = __ldg(bp);                                                         \
-    H_[d] = __ldg(bp + 32);                                                    \
+    if (SYM) { /* B_KJ[t][g], B_KJ[t+4][g] = B_JK[g][t], B_JK[g][t+4]: A's pair */ \
+      const double2 bb = __ldg(av2 + (size_t)wb[e] * 32 + lane);               \
+      L_[d] = bb.x;                                                            \
+      H_[d] = bb.y;                                                            \
+    } else {                                                                   \
+      const double *bp = Bv.bval + (size_t)wb[e] * 64 + boff;                  \
+      L_[d] = __ldg(bp);                                                       \
+      H_[d] = __ldg(bp + 32);                                                  \
+    }                                                                          \
   }
 #define K3M_MMA(A_, L_, H_)                                                     \
   _Pragma("unroll") for (int d = 0; d < kMPF; d += 2) {                        \
@@ -2445,6 +2454,19 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
           if (k0) slot[p0] = v0;
           if (k1) slot[p0 + (k0 ? 1 : 0)] = v1;
           if (lane == 0) so.bmask[blk] = msk;
+          // kept counts of the rows: row g of I here (summed per CTA below), column c's
+          // mirrors (strictly above the diagonal of a diagonal block) to row 8J + c now
+          rkept += (k0 ? 1 : 0) + (k1 ? 1 : 0);
+          int mc0 = (k0 && (!dg || 2 * t > g)) ? 1 : 0, mc1 = (k1 && (!dg || 2 * t + 1 > g)) ? 1 : 0;
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            mc0 += __shfl_xor_sync(FULL_MASK, mc0, o);
+            mc1 += __shfl_xor_sync(FULL_MASK, mc1, o);
+          }
+          if (g == 0) {
+            if (mc0) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * (int64_t)J + 2 * t), (unsigned long long)mc0);
+            if (mc1) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * (int64_t)J + 2 * t + 1), (unsigned long long)mc1);
+          }
           continue;
         }
         if (a.divisor != 1.0) {  // Taylor term: (sum_k s_rk h_kj) / i (reading R7)
@@ -2487,11 +2509,19 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
     if constexpr (SYM) {  // the block row's dropped sum x^2 and nonzero count (warps in order)
       fs = warp_sum(fs);
       nz = warp_sum(nz);
+      rkept += __shfl_xor_sync(FULL_MASK, rkept, 1);  // row g: its 4 lanes
+      rkept += __shfl_xor_sync(FULL_MASK, rkept, 2);
       if (lane == 0) {
         s_fs[warp][0] = fs;
         s_nz[warp][0] = nz;
       }
+      if (t == 0) s_c1[warp][g] = rkept;
       __syncthreads();
+      if (tid < 8 && 8 * I + tid < nrows) {
+        long long c = 0;
+        for (int w = 0; w < kMWarps; w++) c += s_c1[w][tid];
+        if (c) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * I + tid), (unsigned long long)c);
+      }
       if (tid == 0) {
         double f = 0.0;
         long long z = 0;
@@ -2759,26 +2789,13 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
       return b;
     };
     auto bit_of = [&](int kind, int j) { return (kind == 0 || (kind == 1 && j < i)) ? 8 * j + i : 8 * i + j; };
-    long long tot = 0;
-    for (int q0 = 0; q0 < nj; q0 += 32) {  // pass 1: kept counts from the masks
-      const int q = q0 + lane;
-      if (q < nj) {
-        unsigned long long m;
-        int kind;
-        blk_of(q, m, kind);
-        if (kind == 0) tot += __popcll(m & colm);
-        else if (kind == 2) tot += __popc((unsigned)(m >> (8 * i)) & 0xFFu);
-        else tot += __popcll(m & colm & ((1ull << (8 * i)) - 1ull)) + __popc((unsigned)(m >> (9 * i)) & (0xFFu >> i));
-      }
-    }
-    tot = __shfl_sync(FULL_MASK, warp_sum(tot), 0);  // warp_sum reduces into lane 0
-    unsigned long long off = 0;
-    if (lane == 0) off = atomicAdd(a.pool_used, (unsigned long long)tot);
-    off = __shfl_sync(FULL_MASK, off, 0);
-    const bool okp = (long long)off + tot <= a.pool_cap;
+    // the row's kept entries at its scanned offset (K3s counted them), in column order
+    const long long tot = so.rowcnt[r];
+    const int64_t off = so.rowoff[r];
+    const bool okp = off + tot <= a.pool_cap;
     double q1 = 0.0;
     long long c1 = 0;
-    if (okp) {  // pass 2: the kept values, in column order
+    if (okp) {
       long long pos = (long long)off;
       for (int q0 = 0; q0 < nj; q0 += 32) {
         const int q = q0 + lane;
@@ -2798,25 +2815,30 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
           const int y = __shfl_up_sync(FULL_MASK, x, o);
           if (lane >= o) x += y;
         }
-        if (c > 0) {
-          long long p = pos + x - c;
+        if (c > 0) {  // all of the block's loads in flight at once (predicated, unrolled)
           const int J = cj[q];
           const double *slot = so.bstore + (size_t)b * 64;
-          while (rb) {
-            const int j = __ffs(rb) - 1;
-            rb &= rb - 1;
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
             const int e = bit_of(kind, j);
-            const double v = __ldg(slot + __popcll(m & ((1ull << e) - 1ull)));
-            const double av = fabs(v);
-            if (av <= a.eps_g) q1 += v * v;
-            else c1++;
-            a.pool_col[p] = 8 * J + j;
-            a.pool_val[p] = v;
-            p++;
+            v[j] = ((rb >> j) & 1u) ? __ldg(slot + __popcll(m & ((1ull << e) - 1ull))) : 0.0;
           }
+          long long p = pos + x - c;
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            if ((rb >> j) & 1u) {
+              const double av = fabs(v[j]);
+              if (av <= a.eps_g) q1 += v[j] * v[j];
+              else c1++;
+              a.pool_col[p] = 8 * J + j;
+              a.pool_val[p] = v[j];
+              p++;
+            }
         }
         pos += __shfl_sync(FULL_MASK, x, 31);
       }
+      if (lane == 0 && pos != off + tot) atomicOr(so.flag, 16);  // K3s's count disagrees
     }
     q1 = warp_sum(q1);
     c1 = warp_sum(c1);

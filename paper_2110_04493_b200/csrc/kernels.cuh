@@ -264,13 +264,15 @@ struct SymOut {
   unsigned long long *bmask = nullptr;    // per upper block: kept elements (bit 8 row + col)
   double *fsI = nullptr;                  // per block row: dropped sum x^2 (mirrors counted)
   int64_t *nzI = nullptr;                 // per block row: distinct nonzeros (mirrors counted)
+  int64_t *rowcnt = nullptr;              // per row: kept entries (K3s, atomics; zeroed before)
+  const int64_t *rowoff = nullptr;        // its exclusive scan: the row's pool offset (K3a)
   int32_t *cj = nullptr;
   const int64_t *ob_off = nullptr, *cj_off = nullptr;  // scans of K3c's counts
   const int64_t *nj = nullptr, *nup = nullptr;         // K3c: |cand(I)|, |cand(I) >= I|
   const int32_t *wlo = nullptr, *whi = nullptr;        // K3c: the union's block-column extent
   int *flag = nullptr;  // 1: a block row K3s or K3c could not hold, 2: K3s's list differs from
                         // K3c's count, 4: pattern not symmetric (a lower block missing from its
-                        // mirror's list), 8: K3a's lower-list cap
+                        // mirror's list), 8: K3a's lower-list cap, 16: a row's count
 };
 // K3c: nj[I] = |cand(I)|, nup[I] = |cand(I) >= I| over the view's block rows (A = B)
 // and the union's block-column extent [wlo, whi] (K3s's window: cand(I) is then the exact block
