@@ -548,7 +548,12 @@ def main():
     # ---------------- roofline of the dominant kernel ----------------
     import math
     sq_ms = [float(st["sq_kernel_ms"][i]) for i in range(1, N + 1)]
-    sq_fl = [2.0 * float(st["sq_fmas"][i]) for i in range(1, N + 1)]
+    sym = int(st["sq_sym_used"]) == N and N > 0
+    # algorithmic flops of the squaring kernel: 2 per product of T T (sq_fmas = products +
+    # nnz(T)); the symmetric kernel K3s computes the products with j >= r only -- for a
+    # symmetric pattern exactly (products + nnz(T)) / 2 = sq_fmas / 2 of them
+    sq_fl = [(1.0 if sym else 2.0) * float(st["sq_fmas"][i]) for i in range(1, N + 1)]
+    sq_asm = [float(st["sq_assemble_ms"][i]) for i in range(1, N + 1)]
     ty_idx = [i for i in range(2, int(st["M"]) + 1) if st["taylor_numeric_ms"][i] > 0]
     ty_ms = [float(st["taylor_numeric_ms"][i]) for i in ty_idx]
     ty_by = [float(st["taylor_numeric_bytes"][i]) for i in ty_idx]
@@ -563,8 +568,11 @@ def main():
         dur = sum(sq_ms) / len(sq_ms) / 1e3
         ach = sum(sq_fl) / len(sq_fl) / dur / 1e12
         kname = "k_numeric_bsrm" if int(st["sq_bsr_blocks"][1]) > 0 else "k_numeric_paged"
+        if sym:
+            kname = "k_numeric_bsrm_sym"
         tr = traffic_db.get(kname)
-        roof = {"kernel": f"{kname} (squaring SpGEMM + 2T + filter classify)", "bound": "alu",
+        roof = {"kernel": f"{kname} (squaring SpGEMM + 2T + filter classify"
+                          + (", output blocks J >= I of the symmetric T~)" if sym else ")"), "bound": "alu",
                 "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP64_PEAK_TFLOPS,
                 "traffic": tr["dram_bytes"] if tr and args.config == 5 else None,
@@ -579,6 +587,12 @@ def main():
                                "the instruction the kernel issues)",
                 "dmma_peak": fp64_peak["dmma_tflops"],
                 "launches_per_step": len(sq_ms), "avg_launch_ms": dur * 1e3,
+                "symmetric_path": sym,
+                # the full product's flops (2 sq_fmas) over K3s + K3c + K3a: the rate the
+                # symmetric path delivers T~ at, for comparison with the full kernel
+                "full_product_equiv_tflops": (sum(2.0 * float(st["sq_fmas"][i]) for i in range(1, N + 1))
+                                              / (sum(sq_ms) + sum(sq_asm)) / 1e9) if sym else None,
+                "assemble_ms": sq_asm if sym else None,
                 "hbm_gbs_compulsory": sum(float(st["sq_numeric_bytes"][i]) for i in range(1, N + 1)) / len(sq_ms) / dur / 1e9}
     elif ty_ms:
         dur = sum(ty_ms) / len(ty_ms) / 1e3
