@@ -1502,14 +1502,29 @@ __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t
   __syncwarp();
   // ranks of each word for the scatter: recompute the prefix in place (word -> rank)
   // (bm[w] keeps its bits; the rank of block b = popc of the words before + bits below)
+  // scatter: 4 entries' loads in flight per lane before their stores (bval does not alias A,
+  // which the compiler cannot know)
   for (int64_t r = r0; r < r1; r++) {
     const int ri = (int)(r - r0);
-    for (int64_t p = A.rp[r] + lane; p < A.rp[r + 1]; p += 32) {
-      const int c = A.col[p];
-      const int b = (c >> 3) - jmin;
-      const int rank = pref[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
-      const int e = FRAG ? 2 * (4 * ri + (c & 3)) + ((c & 7) >> 2) : ri * 8 + (c & 7);
-      bval[(base + rank) * 64 + e] = A.val[p];
+    const int64_t pe = A.rp[r + 1];
+    for (int64_t p0 = A.rp[r] + lane; p0 < pe; p0 += 128) {
+      int cc[4];
+      double vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t p = p0 + 32 * u;
+        cc[u] = p < pe ? __ldg(A.col + p) : -1;
+        vv[u] = p < pe ? __ldg(A.val + p) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (cc[u] >= 0) {
+          const int c = cc[u];
+          const int b = (c >> 3) - jmin;
+          const int rank = pref[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
+          const int e = FRAG ? 2 * (4 * ri + (c & 3)) + ((c & 7) >> 2) : ri * 8 + (c & 7);
+          bval[(base + rank) * 64 + e] = vv[u];
+        }
     }
   }
 }
@@ -3310,7 +3325,7 @@ __device__ __forceinline__ void row_stat_finish(int lane, int64_t w, double s, i
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 6) k_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
+__global__ void __launch_bounds__(kThreads, 4) k_compact_write(int64_t nrows, int64_t row0, const int64_t *row_off,
                                 const int64_t *row_cnt, const int32_t *pool_col,
                                 const double *pool_val, double tau, const int64_t *rp_out,
                                 int32_t *col_out, double *val_out, double *rs, int64_t *l1r,
@@ -3327,28 +3342,35 @@ __global__ void __launch_bounds__(kThreads, 6) k_compact_write(int64_t nrows, in
   int have_diag = 0;
   long long l1 = 0, l2 = 0;
   long long nlt = 0;  // kept entries left of the diagonal (insert position, idg == 0)
-  for (int64_t base = 0; base < c; base += 32) {
-    int64_t t = base + lane;
-    bool k = false;
-    double x = 0.0;
-    int32_t cc = 0;
-    if (t < c) {
-      x = pool_val[o + t];
-      cc = pool_col[o + t];
-      k = fabs(x) > tau;
+  // 4 chunks' loads in flight before their stores (the outputs do not alias the pool)
+  for (int64_t base0 = 0; base0 < c; base0 += 128) {
+    double xb[4];
+    int32_t cb[4];
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      const int64_t tv = base0 + 32 * v + lane;
+      xb[v] = tv < c ? __ldg(pool_val + o + tv) : 0.0;
+      cb[v] = tv < c ? __ldg(pool_col + o + tv) : 0;
     }
-    if (k) row_stat_accum(grow, cc, x, s, have_diag, l1, l2);  // statistics of T^ itself
-    const bool isd = k && cc == grow;
-    const bool wr = k && !(isd && idg == 2);
-    unsigned m = __ballot_sync(FULL_MASK, wr);
-    if (wr) {
-      int64_t q = dst + __popc(m & lanemask_lt());
-      if (idg == 0 && cc > grow) q += 1;  // room for the inserted diagonal
-      col_out[q] = cc;
-      val_out[q] = (isd && idg == 1) ? 1.0 + x : x;
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+      const int64_t t = base0 + 32 * v + lane;
+      const double x = xb[v];
+      const int32_t cc = cb[v];
+      const bool k = t < c && fabs(x) > tau;
+      if (k) row_stat_accum(grow, cc, x, s, have_diag, l1, l2);  // statistics of T^ itself
+      const bool isd = k && cc == grow;
+      const bool wr = k && !(isd && idg == 2);
+      unsigned m = __ballot_sync(FULL_MASK, wr);
+      if (wr) {
+        int64_t q = dst + __popc(m & lanemask_lt());
+        if (idg == 0 && cc > grow) q += 1;  // room for the inserted diagonal
+        col_out[q] = cc;
+        val_out[q] = (isd && idg == 1) ? 1.0 + x : x;
+      }
+      dst += __popc(m);
+      if (idg == 0) nlt += __popc(__ballot_sync(FULL_MASK, k && cc < grow));
     }
-    dst += __popc(m);
-    if (idg == 0) nlt += __popc(__ballot_sync(FULL_MASK, k && cc < grow));
   }
   if (idg == 0 && lane == 0) {
     col_out[dst0 + nlt] = (int32_t)grow;
@@ -4048,14 +4070,26 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_sort_rows(const int64_t *rp
         run += __popc(bits[w]);
       }
       __syncwarp();
+      // values in groups of 8 loads in flight before their stores (vin / vout do not alias,
+      // but the compiler cannot know: one load -> store chain per entry otherwise)
 #pragma unroll
-      for (int t = 0; t < kSortCap / 32; t++)
-        if (lane + 32 * t < len) {
-          const int k = kr[t], d = k - kmin;
-          const int pos = pref[d >> 5] + __popc(bits[d >> 5] & ((1u << (d & 31)) - 1u));
-          kout[p0 + pos] = k;
-          vout[p0 + pos] = vin[q0 + lane + 32 * t];
+      for (int t0 = 0; t0 < kSortCap / 32; t0 += 8) {
+        if (32 * t0 >= len) break;
+        double vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int e = lane + 32 * (t0 + u);
+          vv[u] = e < len ? __ldg(vin + q0 + e) : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (lane + 32 * (t0 + u) < len) {
+            const int k = kr[t0 + u], d = k - kmin;
+            const int pos = pref[d >> 5] + __popc(bits[d >> 5] & ((1u << (d & 31)) - 1u));
+            kout[p0 + pos] = k;
+            vout[p0 + pos] = vv[u];
+          }
+      }
       __syncwarp();
       continue;
     }
