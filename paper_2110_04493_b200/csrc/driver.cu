@@ -537,7 +537,7 @@ struct Workspace {
   // symmetric squaring (K3c / K3s / K3a): per block row |cand(I)|, |cand(I) >= I| and their
   // scans, the candidate lists and the upper output blocks
   DBuf<int64_t> sym_nj, sym_nup, sym_cjoff, sym_oboff;
-  DBuf<int32_t> sym_cj, sym_wlo, sym_whi;
+  DBuf<int32_t> sym_cj, sym_wlo, sym_whi, sym_lidx;
   DBuf<unsigned long long> sym_bmask;
   DBuf<double> sym_fsI;
   DBuf<int64_t> sym_nzI, sym_rowcnt, sym_rowoff;
@@ -851,8 +851,8 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
   CK(cudaStreamSynchronize(st));
   bool ok = flag == 0 && tot[1] < ((int64_t)1 << 31);  // K3a's block indices are int32
   if (ok) {  // the stores must fit beside the live buffers (else: the full product)
-    const double need = 4.0 * (double)tot[0] + 520.0 * (double)tot[1];
-    const double have_now = (double)(w.sym_cj.n * 4 + w.sym_bstore.n * 8 + w.sym_bmask.n * 8);
+    const double need = 8.0 * (double)tot[0] + 520.0 * (double)tot[1];
+    const double have_now = (double)(w.sym_cj.n * 4 + w.sym_lidx.n * 4 + w.sym_bstore.n * 8 + w.sym_bmask.n * 8);
     std::lock_guard<std::mutex> lk(cache::mu);
     if (cache::budget == 0) {
       size_t fr = 0, tt = 0;
@@ -865,6 +865,7 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
   if (ok) {
     w.sym_cj.ensure((size_t)std::max<int64_t>(tot[0], 1), st);
     w.sym_bstore.ensure((size_t)std::max<int64_t>(tot[1], 1) * 64, st);
+    w.sym_lidx.ensure((size_t)std::max<int64_t>(tot[0], 1), st);
     SymOut so;
     so.bstore = w.sym_bstore.p;
     so.cj = w.sym_cj.p;
@@ -883,6 +884,7 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
     w.sym_rowoff.ensure((size_t)nr + 1, st);
     w.scan_tmp.ensure((size_t)scan_tmp_elems(nr) + 1, st);
     so.rowcnt = w.sym_rowcnt.p;
+    so.lidx = w.sym_lidx.p;
     so.rowoff = w.sym_rowoff.p;
     CK(cudaMemsetAsync(w.sym_rowcnt.p, 0, (size_t)nr * sizeof(int64_t), st));
     so.whi = w.sym_whi.p;
@@ -908,6 +910,7 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
     }
     if (ok) {  // K3a only over K3s's complete lists
       CK(cudaMemcpyAsync(w.pool_used.p, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      launch_sym_lidx(so, nbr, st);
       launch_sym_assemble(nh, so, nbr, nr, P.sm_count * 4, st);
       CK(cudaEventRecord(a1, st));
       CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -2211,6 +2211,7 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
           if (s_fail || so.nj[I] != 0) atomicOr(so.flag, s_fail ? 1 : 2);
           so.fsI[I] = 0.0;
           so.nzI[I] = 0;
+
         }
         continue;
       }
@@ -2755,37 +2756,46 @@ void launch_sym_count(const BsrView &Bv, int64_t *nj, int64_t *nup, int32_t *wlo
 // classified as in the product kernels' flush (Algorithm 4.1 floor and fused first pass);
 // the row is counted, reserved in the pool, then staged in a second pass over its values.
 // ------------------------------------------------------------------------------------
-constexpr int kAsmThreads = 256, kAsmLowCap = 4096;
+// K3a's lower blocks: per block row I and lower candidate J < I (position p in cand(I)), the
+// global index of the upper block (J, I) -- a binary search of I in J's ascending list -- to
+// lidx[cj_off[I] + p] (warp per block row; flag 4 when absent: the pattern is not symmetric)
+__global__ void k_sym_lidx(SymOut so, int64_t nbr) {
+  const int64_t I = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (I >= nbr) return;
+  const int nlow = (int)(so.nj[I] - so.nup[I]);
+  const int64_t c0 = so.cj_off[I];
+  for (int p = lane; p < nlow; p += 32) {
+    const int J = so.cj[c0 + p];
+    const int32_t *lj = so.cj + so.cj_off[J];
+    const int njJ = (int)so.nj[J], nlJ = (int)(so.nj[J] - so.nup[J]);
+    int lo = nlJ, hi = njJ;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (lj[mid] < (int)I) lo = mid + 1;
+      else hi = mid;
+    }
+    int idx = -1;
+    if (lo < njJ && lj[lo] == (int)I) idx = (int)(so.ob_off[J] + (lo - nlJ));
+    else atomicOr(so.flag, 4);
+    so.lidx[c0 + p] = idx;
+  }
+}
+void launch_sym_lidx(const SymOut &so, int64_t nbr, cudaStream_t st) {
+  if (nbr == 0) return;
+  KL;
+  k_sym_lidx<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr);
+}
+constexpr int kAsmThreads = 256;
 __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, SymOut so, int64_t nbr,
                                                                  int64_t nrows) {
-  __shared__ int32_t s_lidx[kAsmLowCap];
   const int tid = threadIdx.x, lane = tid & 31, i = tid >> 5;
   const unsigned long long colm = 0x0101010101010101ull << i;  // column i of a block
   for (int64_t I = blockIdx.x; I < nbr; I += gridDim.x) {
     const int nj = (int)so.nj[I], nlow = (int)(so.nj[I] - so.nup[I]);
-    const int32_t *cj = so.cj + so.cj_off[I];
+    const int64_t c0 = so.cj_off[I];
+    const int32_t *cj = so.cj + c0;
     const int64_t obo = so.ob_off[I];
-    if (nlow > kAsmLowCap) {
-      if (tid == 0) atomicOr(so.flag, 8);
-      continue;  // uniform per CTA; the host falls back to the full product
-    }
-    __syncthreads();  // the previous block row's s_lidx consumed
-    for (int p = tid; p < nlow; p += kAsmThreads) {
-      const int J = cj[p];
-      const int32_t *lj = so.cj + so.cj_off[J];
-      const int njJ = (int)so.nj[J], nlJ = (int)(so.nj[J] - so.nup[J]);
-      int lo = nlJ, hi = njJ;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (lj[mid] < (int)I) lo = mid + 1;
-        else hi = mid;
-      }
-      int idx = -1;
-      if (lo < njJ && lj[lo] == (int)I) idx = (int)(so.ob_off[J] + (lo - nlJ));
-      else atomicOr(so.flag, 4);
-      s_lidx[p] = idx;
-    }
-    __syncthreads();
     const int64_t r = 8 * I + i;
     if (r >= nrows) continue;
     const bool hasdiag = nlow < nj && cj[nlow] == (int)I;
@@ -2794,7 +2804,7 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
     auto blk_of = [&](int q, unsigned long long &m, int &kind) -> int64_t {
       int64_t b;
       if (q < nlow) {
-        b = s_lidx[q];
+        b = so.lidx[c0 + q];  // k_sym_lidx
         kind = 0;
       } else {
         b = obo + (q - nlow);
@@ -2808,18 +2818,29 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
     const long long tot = so.rowcnt[r];
     const int64_t off = so.rowoff[r];
     const bool okp = off + tot <= a.pool_cap;
-    double q1 = 0.0;
-    long long c1 = 0;
+    double q1 = 0.0;   // the fused first pass: x^2 of kept |x| <= eps_g
+    long long c1 = 0;  // kept |x| > eps_g (the compaction's count when one pass sufficed)
     if (okp) {
       long long pos = (long long)off;
+      // the next chunk's block index, mask and column are fetched before this chunk's stores
+      int64_t nb = 0;
+      unsigned long long nm = 0;
+      int nk = 2, nJ = 0;
+      if (lane < nj) {
+        nb = blk_of(lane, nm, nk);
+        nJ = cj[lane];
+      }
       for (int q0 = 0; q0 < nj; q0 += 32) {
         const int q = q0 + lane;
-        unsigned long long m = 0;
-        int kind = 2;
-        int64_t b = 0;
+        const unsigned long long m = nm;
+        const int kind = nk, J = nJ;
+        const int64_t b = nb;
+        if (q0 + 32 + lane < nj) {
+          nb = blk_of(q0 + 32 + lane, nm, nk);
+          nJ = cj[q0 + 32 + lane];
+        }
         unsigned rb = 0;  // row i's kept entries j (bits)
         if (q < nj) {
-          b = blk_of(q, m, kind);
 #pragma unroll
           for (int j = 0; j < 8; j++) rb |= (unsigned)((m >> bit_of(kind, j)) & 1ull) << j;
         }
@@ -2831,25 +2852,43 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
           if (lane >= o) x += y;
         }
         if (c > 0) {  // all of the block's loads in flight at once (predicated, unrolled)
-          const int J = cj[q];
           const double *slot = so.bstore + (size_t)b * 64;
           double v[8];
+          if (kind == 2) {  // row i of an upper block: its kept values are consecutive
+            const double *sv = slot + __popcll(m & ((1ull << (8 * i)) - 1ull));
 #pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const int e = bit_of(kind, j);
-            v[j] = ((rb >> j) & 1u) ? __ldg(slot + __popcll(m & ((1ull << e) - 1ull))) : 0.0;
+            for (int k = 0; k < 8; k++) v[k] = k < c ? __ldg(sv + k) : 0.0;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              const int e = bit_of(kind, j);
+              v[j] = ((rb >> j) & 1u) ? __ldg(slot + __popcll(m & ((1ull << e) - 1ull))) : 0.0;
+            }
           }
           long long p = pos + x - c;
+          if (kind == 2) {  // the k-th value is the k-th set bit's column
+            unsigned rbm = rb;
 #pragma unroll
-          for (int j = 0; j < 8; j++)
-            if ((rb >> j) & 1u) {
-              const double av = fabs(v[j]);
-              if (av <= a.eps_g) q1 += v[j] * v[j];
-              else c1++;
-              a.pool_col[p] = 8 * J + j;
-              a.pool_val[p] = v[j];
-              p++;
-            }
+            for (int k = 0; k < 8; k++)
+              if (k < c) {
+                const int j = __ffs(rbm) - 1;
+                rbm &= rbm - 1;
+                a.pool_col[p + k] = 8 * J + j;
+                a.pool_val[p + k] = v[k];
+                if (fabs(v[k]) <= a.eps_g) q1 += v[k] * v[k];
+                else c1++;
+              }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+              if ((rb >> j) & 1u) {
+                a.pool_col[p] = 8 * J + j;
+                a.pool_val[p] = v[j];
+                if (fabs(v[j]) <= a.eps_g) q1 += v[j] * v[j];
+                else c1++;
+                p++;
+              }
+          }
         }
         pos += __shfl_sync(FULL_MASK, x, 31);
       }
@@ -2864,7 +2903,7 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
       // Algorithm 4.1's floor sum and the distinct count per block row (K3s), on its first row
       a.row_fsum[r] = i == 0 ? so.fsI[I] : 0.0;
       a.row_nnz[r] = i == 0 ? so.nzI[I] : 0;
-      if (a.row_p1) {
+      if (a.row_p1) {  // the fused first pass per block row (K3s), on its first row
         a.row_p1[r] = q1;
         a.row_c1[r] = c1;
       }

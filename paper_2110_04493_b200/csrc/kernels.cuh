@@ -266,6 +266,7 @@ struct SymOut {
   int64_t *nzI = nullptr;                 // per block row: distinct nonzeros (mirrors counted)
   int64_t *rowcnt = nullptr;              // per row: kept entries (K3s, atomics; zeroed before)
   const int64_t *rowoff = nullptr;        // its exclusive scan: the row's pool offset (K3a)
+  int32_t *lidx = nullptr;                // per candidate (cj layout): a lower block's global index
   int32_t *cj = nullptr;
   const int64_t *ob_off = nullptr, *cj_off = nullptr;  // scans of K3c's counts
   const int64_t *nj = nullptr, *nup = nullptr;         // K3c: |cand(I)|, |cand(I) >= I|
@@ -281,6 +282,7 @@ void launch_sym_count(const BsrView &Bv, int64_t *nj, int64_t *nup, int32_t *wlo
                       cudaStream_t st);
 void launch_numeric_bsrm_sym(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                              const SymOut &so, cudaStream_t st, bool long_lists);
+void launch_sym_lidx(const SymOut &so, int64_t nbr, cudaStream_t st);
 void launch_sym_assemble(const NumericArgs &a, const SymOut &so, int64_t nbr, int64_t nrows, int grid,
                          cudaStream_t st);
 // T := the symmetric part read from the upper triangle: entry (r, c) kept iff (c, r) is
