@@ -2709,15 +2709,25 @@ __global__ void __launch_bounds__(kSymCntWarps * 32) k_sym_count(BsrView Bv, int
   }
   for (int w = lane; w < nw; w += 32) bm[w] = 0u;
   __syncwarp();
-  const int lim = nw * 32;
-  for (int64_t q = a0; q < a1; q++) {
-    const int K = Bv.bcol[q];
-    if (lane == 0 && K - jlo >= 0 && K - jlo < lim)
-      atomicOr(&bm[(K - jlo) >> 5], 1u << ((K - jlo) & 31));  // the 2T term
-    if (K < Bv.nbr)
-      for (int64_t b = Bv.brp[K] + lane; b < Bv.brp[K + 1]; b += 32) {
+  // the 2T term (row I's own blocks), then the block rows K of row I, 4 at a time (their
+  // extents loaded together)
+  for (int64_t q = a0 + lane; q < a1; q += 32) {
+    const int d = Bv.bcol[q] - jlo;
+    atomicOr(&bm[d >> 5], 1u << (d & 31));
+  }
+  for (int64_t q0 = a0; q0 < a1; q0 += 4) {
+    int64_t s0[4], s1[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int K = q0 + u < a1 ? Bv.bcol[q0 + u] : (int)Bv.nbr;
+      s0[u] = K < Bv.nbr ? Bv.brp[K] : 0;
+      s1[u] = K < Bv.nbr ? Bv.brp[K + 1] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      for (int64_t b = s0[u] + lane; b < s1[u]; b += 32) {
         const int d = Bv.bcol[b] - jlo;
-        if (d >= 0 && d < lim) atomicOr(&bm[d >> 5], 1u << (d & 31));
+        atomicOr(&bm[d >> 5], 1u << (d & 31));
       }
   }
   __syncwarp();
