@@ -819,7 +819,8 @@ static double alg41_threshold(sexpm_plan_s &P, double eps_g, double F, bool fuse
 // K3s (rep.kernel_ms) and the K3c + K3a time in rep.asm_ms.  Returns false (nothing staged;
 // the caller runs the full K3m) when a block row does not fit or the lists disagree.
 static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &Bv, int64_t nr,
-                               bool long_lists, cudaEvent_t k0, cudaEvent_t k1, StepReport &rep) {
+                               bool long_lists, cudaEvent_t k0, cudaEvent_t k1, StepReport &rep,
+                               double eps_g, double &floor_tau) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   const int64_t nbr = Bv.nbr;
@@ -850,6 +851,12 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
   CK(cudaEventRecord(c1, st));
   CK(cudaStreamSynchronize(st));
   bool ok = flag == 0 && tot[1] < ((int64_t)1 << 31);  // K3a's block indices are int32
+  if (floor_tau == 0.0 && eps_g > 0.0) {
+    // floor lemma: K = 64 x the candidate blocks of all block rows bounds the
+    // number of entries of T~ (every nonzero lies in a candidate block)
+    floor_tau = eps_g / sqrt(64.0 * (double)tot[0]);
+  }
+  nh.floor_tau = floor_tau;
   if (ok) {  // the stores must fit beside the live buffers (else: the full product)
     const double need = 8.0 * (double)tot[0] + 520.0 * (double)tot[1];
     const double have_now = (double)(w.sym_cj.n * 4 + w.sym_lidx.n * 4 + w.sym_bstore.n * 8 + w.sym_bmask.n * 8);
@@ -989,15 +996,25 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
     have_symbolic = true;
   };
   double Kglob;
+  // the symmetric squaring needs no K1: its K (floor lemma) is K3c's candidate-slot count and
+  // its products follow from the row lengths (symmetric pattern: sum_k nnz(row k)^2)
+  const bool sym_planned = P.sym_sq && self == 2.0 && B.rp == A.rp && nr == P.n && A.row0 == 0 &&
+                           (okern == 0 || okern == 13) && !P.o.exact_products;
   if (dia_path) {
     hstat[0] = (int64_t)P.dia_nd * A.nnz;
     Kglob = allsum(P, (double)hstat[0]);
+  } else if (sym_planned) {
+    launch_rowlen_sq(A.rp, nr, w.bound.p, st);
+    launch_reduce_sum_i64(w.bound.p, nr, w.i64tmp.p + 2, st);
+    hstat[2] = d2h(w.i64tmp.p + 2, st) + A.nnz;
+    hstat[0] = (int64_t)1 << 60;  // no bound on the staging pool (K3a's total is exact)
+    Kglob = 0.0;                  // set by the stage from K3c
   } else {
     run_symbolic();
     Kglob = allsum(P, (double)hstat[0]);
   }
   rep.fmas = (double)hstat[2];
-  const double floor_tau = (eps_g > 0.0 && Kglob > 0.0) ? eps_g / sqrt(Kglob) : 0.0;
+  double floor_tau = (eps_g > 0.0 && Kglob > 0.0) ? eps_g / sqrt(Kglob) : 0.0;
 
   // K2 scheduling order: the plan's locality (cluster) order when it covers these rows,
   // else longest-processing-time-first bins
@@ -1108,7 +1125,8 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
       // the paged (5) and diagonal (7) kernels fuse Algorithm 4.1's first pass into their flush
       fused_p1 = eps_g > 0.0 && (kern == 5 || kern == 7 || kern == 11 || kern == 13);
       while (nlist > 0) {
-        if (stage != 7 && !have_symbolic) {  // rows left by K5d: the other kernels need K1
+        if (stage != 7 && !have_symbolic && !(sym_planned && stage == 13 && !sym_failed)) {
+          // rows left by K5d: the other kernels need K1 (the symmetric squaring does not)
           run_symbolic();
           rep.fmas = (double)hstat[2];
           na.cursor_cap = std::max<int64_t>(hstat[6], 1);
@@ -1197,10 +1215,16 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           // symmetric squaring: one GPU, T exactly symmetric (do_run), A = B
           bool sym_done = false;
           if (sym_try) {
-            sym_done = sym_squaring_stage(P, nh, Bv, nr, long_lists, k0, k1, rep);
+            sym_done = sym_squaring_stage(P, nh, Bv, nr, long_lists, k0, k1, rep, eps_g, floor_tau);
             rep.sym = sym_done;
-            if (!sym_done) {  // the full K3m: it needs the block transpose
+            if (!sym_done) {  // the full K3m: it needs the block transpose and K1's spans
               sym_failed = true;
+              if (!have_symbolic) {
+                run_symbolic();
+                nh.lo = w.lo.p;
+                nh.hi = w.hi.p;
+              }
+              nh.floor_tau = floor_tau;
               bsr_transpose(P, w.bsrB);
               Bv.tp = w.bsrB.tp.p;
               Bv.tk = w.bsrB.tk.p;

@@ -343,6 +343,18 @@ void launch_scale_pow2(double *v, int64_t cnt, int e, cudaStream_t st) {
   k_scale_pow2<<<grid_for(cnt, kThreads, 148 * 16), kThreads, 0, st>>>(v, cnt, e);
 }
 
+__global__ void k_rowlen_sq(const int64_t *rp, int64_t nrows, int64_t *out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nrows) {
+    const int64_t l = rp[r + 1] - rp[r];
+    out[r] = l * l;
+  }
+}
+void launch_rowlen_sq(const int64_t *rp, int64_t nrows, int64_t *out, cudaStream_t st) {
+  if (nrows == 0) return;
+  KL;
+  k_rowlen_sq<<<grid_for(nrows, kThreads), kThreads, 0, st>>>(rp, nrows, out);
+}
 __global__ void k_row_lengths(const int64_t *rp, int64_t nrows, int64_t *out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nrows) out[i] = rp[i + 1] - rp[i];

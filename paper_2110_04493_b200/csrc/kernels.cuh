@@ -47,6 +47,7 @@ void launch_reduce_max_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStre
 void launch_reduce_sum_i64(const int64_t *x, int64_t cnt, int64_t *out, cudaStream_t st);
 void launch_scale_pow2(double *v, int64_t cnt, int e, cudaStream_t st);
 void launch_row_lengths(const int64_t *rp, int64_t nrows, int64_t *out, cudaStream_t st);
+void launch_rowlen_sq(const int64_t *rp, int64_t nrows, int64_t *out, cudaStream_t st);  // out[r] = len(r)^2
 void launch_copy_i64_offset(const int64_t *src, int64_t cnt, int64_t off, int64_t *dst,
                             cudaStream_t st);
 
