@@ -370,6 +370,12 @@ static void park(int role, void *p, size_t bytes) {  // idle blocks only (plan d
     bytes_allocated -= (double)other.bytes;
   }
 }
+// bytes parked for a role (reused by its next ensure when large enough); caller holds mu
+static size_t parked_bytes(int role) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return (role >= 0 && parked[role].p && parked[role].dev == dev) ? parked[role].bytes : 0;
+}
 static void *unpark(int role, size_t bytes, size_t *got) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -492,6 +498,7 @@ struct StepReport {
   unsigned long long prof[12] = {0};  // grouped kernel phase clocks
   float asm_ms = 0.f;  // symmetric path: K3c + K3a
   bool sym = false;    // the product ran on the symmetric path
+  bool relabel_needed = false;  // T^_0 in index order could not take the symmetric path
 };
 
 // BSR-8 view of a CSR matrix (k_bsr_build) and, optionally, its block transpose
@@ -607,6 +614,7 @@ struct sexpm_plan_s {
   DBuf<int32_t> block_order_t;  // the aggregates (block rows in that order) in locality order
   bool sq_tiled = false;
   bool h_sym = false;   // H bit-exactly symmetric (plan time)
+  bool t_index_pending = false;  // T^_0 kept in index order: the first squaring's BSR build relabels
   bool sym_sq = false;  // this run squares on the symmetric path (option sym_squaring)
   int agg_kind = 0;  // 0 none, 1 BFS aggregates, 2 compact aggregates, 3 lattice diamonds, 4 lattice cubes
   bool tperm_ready = false;  // tperm / tinv (/ _loc) hold the squarings' aggregate relabelling
@@ -728,7 +736,8 @@ static void wait_order(sexpm_plan_s &P) {
 // (nothing built) when a block row spans more block columns than k_bsr_build's bitmap, or
 // the view would not fit K3m's 32-bit block indices.
 static void bsr_transpose(sexpm_plan_s &P, BsrBufs &b);
-static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpose, BsrBufs &b) {
+static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpose, BsrBufs &b,
+                      RowColMap map = RowColMap{}) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   const int64_t nbr = (M.nrows + 7) / 8, nbc = (P.n + 7) / 8;
@@ -739,7 +748,7 @@ static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpo
   b.brp.ensure((size_t)nbr + 1, st);
   w.scan_tmp2.ensure((size_t)scan_tmp_elems(std::max(nbr, nbc)) + 1, st);
   CK(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
-  launch_bsr_count(M, nbr, b.bcnt.p, w.flags.p, st);
+  launch_bsr_count(M, nbr, b.bcnt.p, w.flags.p, st, map);
   launch_reduce_max_i64(b.bcnt.p, nbr, w.i64tmp.p + 7, st);
   launch_exclusive_scan(b.bcnt.p, nbr, b.brp.p, w.scan_tmp2.p, st);
   int bflags = 0;
@@ -751,7 +760,7 @@ static bool build_bsr(sexpm_plan_s &P, const CsrView &M, bool frag, bool transpo
   const size_t nb1 = (size_t)std::max<int64_t>(b.nb, 1);
   b.bcol.ensure(nb1, st);
   b.bval.ensure(nb1 * 64, st);
-  launch_bsr_fill(M, nbr, b.brp.p, b.bcol.p, b.bval.p, w.flags.p, st, frag);
+  launch_bsr_fill(M, nbr, b.brp.p, b.bcol.p, b.bval.p, w.flags.p, st, frag, map);
   if (transpose) bsr_transpose(P, b);
   return true;
 }
@@ -859,8 +868,11 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
   nh.floor_tau = floor_tau;
   if (ok) {  // the stores must fit beside the live buffers (else: the full product)
     const double need = 8.0 * (double)tot[0] + 520.0 * (double)tot[1];
-    const double have_now = (double)(w.sym_cj.n * 4 + w.sym_lidx.n * 4 + w.sym_bstore.n * 8 + w.sym_bmask.n * 8);
     std::lock_guard<std::mutex> lk(cache::mu);
+    // what the stores already hold, or will reuse from the previous plan's parked buffers
+    const double have_now = (double)(w.sym_cj.n * 4 + w.sym_lidx.n * 4 + w.sym_bmask.n * 8) +
+                            (double)std::max<size_t>(w.sym_bstore.n * 8, w.sym_bstore.p ? 0 : cache::parked_bytes(w.sym_bstore.role)) +
+                            (double)(w.sym_cj.p ? 0 : cache::parked_bytes(w.sym_cj.role));
     if (cache::budget == 0) {
       size_t fr = 0, tt = 0;
       cudaMemGetInfo(&fr, &tt);
@@ -1175,7 +1187,20 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           } else {
             // the symmetric kernel reads B_KJ as B_JK^T: no block transpose (built on fallback)
             sym_try = stage == 13 && P.sym_sq && same && nr == P.n && self == 2.0 && !sym_failed;
-            ok_view = build_bsr(P, B, stage == 13, !sym_try, w.bsrB);
+            // T^_0 still in index order (do_run): the relabelling into aggregates fused here
+            RowColMap map;
+            if (P.t_index_pending && sym_try) {
+              map.rowmap = P.tperm_loc.p;
+              map.colmap = P.tinv.p;
+            }
+            if (P.t_index_pending && !sym_try) {  // only the symmetric path takes it
+              rep.relabel_needed = true;
+              cudaEventDestroy(e0);
+              cudaEventDestroy(e1);
+              cudaEventDestroy(e_first);
+              return;
+            }
+            ok_view = build_bsr(P, B, stage == 13, !sym_try, w.bsrB, map);
             // K3b holds a row of A in shared memory
             if (ok_view && stage == 11 && w.bsrB.bmax > kBsrMaxRowBlocks) ok_view = false;
           }
@@ -1217,6 +1242,15 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           if (sym_try) {
             sym_done = sym_squaring_stage(P, nh, Bv, nr, long_lists, k0, k1, rep, eps_g, floor_tau);
             rep.sym = sym_done;
+            if (!sym_done && P.t_index_pending) {  // do_run relabels T^_0 and runs the product again
+              rep.relabel_needed = true;
+              cudaEventDestroy(k0);
+              cudaEventDestroy(k1);
+              cudaEventDestroy(e0);
+              cudaEventDestroy(e1);
+              cudaEventDestroy(e_first);
+              return;
+            }
             if (!sym_done) {  // the full K3m: it needs the block transpose and K1's spans
               sym_failed = true;
               if (!have_symbolic) {
@@ -3212,8 +3246,12 @@ static void do_run(sexpm_plan_s &P) {
   if (P.o.sq_order == 1 && P.N >= 1 && !P.o.ssat && P.M >= 1) {
     wait_order(P);
     if (P.tperm_ready) {
-      permute_csr(P, T.view(), P.tperm_loc.p, P.tinv.p, Tn);  // row i <- row tperm[i], col c -> tinv[c]
-      swap_csr(T, Tn);
+      if (P.sym_sq && P.world == 1 && !getenv("SEXPM_NO_FUSED_RELABEL")) {
+        P.t_index_pending = true;  // the first squaring's BSR build relabels (no CSR pass)
+      } else {
+        permute_csr(P, T.view(), P.tperm_loc.p, P.tinv.p, Tn);  // row i <- row tperm[i], col c -> tinv[c]
+        swap_csr(T, Tn);
+      }
       P.sq_tiled = true;
       S.sq_order_used = P.agg_kind;
     }
@@ -3266,6 +3304,14 @@ static void do_run(sexpm_plan_s &P) {
     const double self = ssat ? 0.0 : 2.0;  // T~ = 2T + T^2 (Eq. 4.15), or E^2 (SSAT)
     if (P.world == 1) {
       filtered_product(P, T.view(), T.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
+      if (rep.relabel_needed) {  // relabel T^_0 after all, then the product as usual
+        P.t_index_pending = false;
+        permute_csr(P, T.view(), P.tperm_loc.p, P.tinv.p, Tn);
+        swap_csr(T, Tn);
+        rep = StepReport();
+        filtered_product(P, T.view(), T.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
+      }
+      P.t_index_pending = false;
     } else {
       const auto x0 = std::chrono::steady_clock::now();
       exchange_halo(P, T, l1, l2, P.Bhalo);

@@ -1438,10 +1438,12 @@ constexpr int kBsrSpanWords = 512;  // block-column span per block row: 16384 bl
 // block at 2 (4 r + c % 4) + c / 4, i.e. lane l = 4 r + c % 4 of a warp holds (r, c) and
 // (r, c + 4) as one 16-byte pair -- the A operand of mma.m8n8k4 for k = c % 4 and c % 4 + 4
 // in one load; otherwise row-major (K3b).
+// map (optional): view row r is A's row rowmap[r], column c of A is column colmap[c] of the
+// view -- the relabelling fused into the build (no relabelled CSR is written)
 template <bool FILL, bool FRAG = false>
 __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t nbr, int64_t *bcnt,
                                                               const int64_t *brp, int32_t *bcol,
-                                                              double *bval, int *flags) {
+                                                              double *bval, int *flags, RowColMap map) {
   __shared__ unsigned bits[kBsrWarps][kBsrSpanWords];
   __shared__ uint16_t prefs[kBsrWarps][kBsrSpanWords];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1450,13 +1452,28 @@ __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t
   unsigned *bm = bits[wib];
   uint16_t *pref = prefs[wib];
   const int64_t r0 = 8 * I, r1 = r0 + 8 < A.nrows ? r0 + 8 : A.nrows;
+  auto srow = [&](int64_t r) { return map.rowmap ? map.rowmap[r] : r; };
+  auto mcol = [&](int32_t c) { return map.colmap ? (int32_t)map.colmap[c] : c; };
   int32_t jmin = INT32_MAX, jmax = -1;
-  for (int64_t r = r0; r < r1; r++) {
-    const int64_t p0 = A.rp[r], p1 = A.rp[r + 1];
-    if (p1 > p0) {
-      jmin = min(jmin, A.col[p0] >> 3);
-      jmax = max(jmax, A.col[p1 - 1] >> 3);
+  if (!map.colmap) {
+    for (int64_t r = r0; r < r1; r++) {
+      const int64_t p0 = A.rp[srow(r)], p1 = A.rp[srow(r) + 1];
+      if (p1 > p0) {
+        jmin = min(jmin, A.col[p0] >> 3);
+        jmax = max(jmax, A.col[p1 - 1] >> 3);
+      }
     }
+  } else {  // mapped columns are not monotone: all entries
+    for (int64_t r = r0; r < r1; r++) {
+      const int64_t sr = srow(r);
+      for (int64_t p = A.rp[sr] + lane; p < A.rp[sr + 1]; p += 32) {
+        const int32_t b = mcol(A.col[p]) >> 3;
+        jmin = min(jmin, b);
+        jmax = max(jmax, b);
+      }
+    }
+    jmin = __shfl_sync(FULL_MASK, warp_min(jmin), 0);
+    jmax = __shfl_sync(FULL_MASK, warp_max(jmax), 0);
   }
   if (jmax < jmin) {
     if (!FILL && lane == 0) bcnt[I] = 0;
@@ -1473,8 +1490,9 @@ __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t
   for (int w = lane; w < nw; w += 32) bm[w] = 0u;
   __syncwarp();
   for (int64_t r = r0; r < r1; r++) {
-    for (int64_t p = A.rp[r] + lane; p < A.rp[r + 1]; p += 32) {
-      const int b = (A.col[p] >> 3) - jmin;
+    const int64_t sr = srow(r);
+    for (int64_t p = A.rp[sr] + lane; p < A.rp[sr + 1]; p += 32) {
+      const int b = (mcol(A.col[p]) >> 3) - jmin;
       atomicOr(&bm[b >> 5], 1u << (b & 31));
     }
   }
@@ -1518,14 +1536,15 @@ __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t
   // which the compiler cannot know)
   for (int64_t r = r0; r < r1; r++) {
     const int ri = (int)(r - r0);
-    const int64_t pe = A.rp[r + 1];
-    for (int64_t p0 = A.rp[r] + lane; p0 < pe; p0 += 128) {
+    const int64_t sr = srow(r);
+    const int64_t pe = A.rp[sr + 1];
+    for (int64_t p0 = A.rp[sr] + lane; p0 < pe; p0 += 128) {
       int cc[4];
       double vv[4];
 #pragma unroll
       for (int u = 0; u < 4; u++) {
         const int64_t p = p0 + 32 * u;
-        cc[u] = p < pe ? __ldg(A.col + p) : -1;
+        cc[u] = p < pe ? mcol(__ldg(A.col + p)) : -1;
         vv[u] = p < pe ? __ldg(A.val + p) : 0.0;
       }
 #pragma unroll
@@ -1540,22 +1559,23 @@ __global__ void __launch_bounds__(kBsrWarps * 32) k_bsr_build(CsrView A, int64_t
     }
   }
 }
-void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st) {
+void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st,
+                      RowColMap map) {
   if (nbr == 0) return;
   KL;
   k_bsr_build<false><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, bcnt, nullptr,
-                                                                           nullptr, nullptr, flags);
+                                                                           nullptr, nullptr, flags, map);
 }
 void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
-                     double *bval, int *flags, cudaStream_t st, bool frag) {
+                     double *bval, int *flags, cudaStream_t st, bool frag, RowColMap map) {
   if (nbr == 0) return;
   KL;
   if (frag)
     k_bsr_build<true, true><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, nullptr, brp,
-                                                                                bcol, bval, flags);
+                                                                                bcol, bval, flags, map);
   else
     k_bsr_build<true, false><<<grid_for(nbr, kBsrWarps), kBsrWarps * 32, 0, st>>>(A, nbr, nullptr, brp,
-                                                                                 bcol, bval, flags);
+                                                                                 bcol, bval, flags, map);
 }
 
 // block transpose: a stable radix sort of the blocks (enumerated block row by block row,

@@ -226,10 +226,17 @@ struct BsrView {
 };
 constexpr int kBsrScratchPerCta = 512 * 64;  // doubles of output-block scratch per CTA
 constexpr int kBsrMaxRowBlocks = 136;        // blocks of a block row the numeric kernel holds
-void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st);
+// optional relabelling fused into the BSR build: view row r = A's row rowmap[r], A's column c
+// = the view's column colmap[c] (null: identity)
+struct RowColMap {
+  const int64_t *rowmap = nullptr, *colmap = nullptr;
+};
+void launch_bsr_count(const CsrView &A, int64_t nbr, int64_t *bcnt, int *flags, cudaStream_t st,
+                      RowColMap map = RowColMap{});
 // frag = true: values in K3m's tensor-core fragment order (see kernels.cu), else row-major
 void launch_bsr_fill(const CsrView &A, int64_t nbr, const int64_t *brp, int32_t *bcol,
-                     double *bval, int *flags, cudaStream_t st, bool frag = false);
+                     double *bval, int *flags, cudaStream_t st, bool frag = false,
+                     RowColMap map = RowColMap{});
 // tk_tmp / tb_tmp: nb-sized scratch; keys_out: nb int32 scratch; sort_tmp: bytes from
 // bsr_transpose_temp_bytes(nb)
 size_t bsr_transpose_temp_bytes(int64_t nb);
