@@ -2831,6 +2831,8 @@ void launch_sym_lidx(const SymOut &so, int64_t nbr, cudaStream_t st) {
 constexpr int kAsmThreads = 256;
 __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, SymOut so, int64_t nbr,
                                                                  int64_t nrows) {
+  __shared__ int32_t s_col[kAsmThreads / 32][256];  // a chunk's entries (32 blocks x 8)
+  __shared__ double s_val[kAsmThreads / 32][256];
   const int tid = threadIdx.x, lane = tid & 31, i = tid >> 5;
   const unsigned long long colm = 0x0101010101010101ull << i;  // column i of a block
   for (int64_t I = blockIdx.x; I < nbr; I += gridDim.x) {
@@ -2907,7 +2909,8 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
               v[j] = ((rb >> j) & 1u) ? __ldg(slot + __popcll(m & ((1ull << e) - 1ull))) : 0.0;
             }
           }
-          long long p = pos + x - c;
+          // staged in shared memory at the chunk-local position, copied out coalesced below
+          int p = x - c;
           if (kind == 2) {  // the k-th value is the k-th set bit's column
             unsigned rbm = rb;
 #pragma unroll
@@ -2915,8 +2918,8 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
               if (k < c) {
                 const int j = __ffs(rbm) - 1;
                 rbm &= rbm - 1;
-                a.pool_col[p + k] = 8 * J + j;
-                a.pool_val[p + k] = v[k];
+                s_col[i][p + k] = 8 * J + j;
+                s_val[i][p + k] = v[k];
                 if (fabs(v[k]) <= a.eps_g) q1 += v[k] * v[k];
                 else c1++;
               }
@@ -2924,15 +2927,22 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_sym_assemble(NumericArgs a, 
 #pragma unroll
             for (int j = 0; j < 8; j++)
               if ((rb >> j) & 1u) {
-                a.pool_col[p] = 8 * J + j;
-                a.pool_val[p] = v[j];
+                s_col[i][p] = 8 * J + j;
+                s_val[i][p] = v[j];
                 if (fabs(v[j]) <= a.eps_g) q1 += v[j] * v[j];
                 else c1++;
                 p++;
               }
           }
         }
-        pos += __shfl_sync(FULL_MASK, x, 31);
+        const int ct = __shfl_sync(FULL_MASK, x, 31);  // the chunk's entries
+        __syncwarp();
+        for (int k = lane; k < ct; k += 32) {
+          a.pool_col[pos + k] = s_col[i][k];
+          a.pool_val[pos + k] = s_val[i][k];
+        }
+        __syncwarp();
+        pos += ct;
       }
       if (lane == 0 && pos != off + tot) atomicOr(so.flag, 16);  // K3s's count disagrees
     }
@@ -3027,7 +3037,10 @@ __global__ void k_mark_offsets(CsrView H, unsigned *bits, int64_t n) {
   const int64_t row = H.row0 + w;
   for (int64_t p = H.rp[w] + lane; p < H.rp[w + 1]; p += 32) {
     const int64_t b = (int64_t)H.col[p] - row + (n - 1);
-    atomicOr(&bits[b >> 5], 1u << (b & 31));
+    // a stencil has a handful of offsets: almost every bit is set already, so read first
+    // (the atomics on those few words would serialise)
+    const unsigned m = 1u << (b & 31);
+    if (!(*reinterpret_cast<volatile unsigned *>(&bits[b >> 5]) & m)) atomicOr(&bits[b >> 5], m);
   }
 }
 void launch_mark_offsets(const CsrView &H, unsigned *bits, int64_t n, cudaStream_t st) {
