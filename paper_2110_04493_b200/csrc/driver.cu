@@ -582,6 +582,14 @@ struct sexpm_plan_s {
     bool ok = false;
     int nU = 0, dzero = -1, rw = 0;
     int64_t pad = 0, npad = 0;
+    // half window (symmetric path): the terms are computed and stored over the offsets o >= 0
+    // only (lcnt_h planes of stride plane = rows + padr, padr zero rows in front for the
+    // mirrored reads of rows r + s, -padr <= s < 0); T^_0 over U_h; the FINAL tables map every
+    // offset o of cum_m to |o| (row shift o < 0 ? o : 0)
+    bool half = false;
+    int nUh = 0;
+    int64_t padr = 0;
+    std::vector<int> lcnt_h;
     std::vector<int> lcnt, ccnt;      // |W_j|, |cum_j| (index j; ccnt[0] = 0)
     std::vector<int64_t> woff, coff;  // per term: start of its W-indexed / cum-indexed tables
     DBuf<int32_t> rec;                // TERM records (k_taylor_win), rw int32 per position
@@ -2057,6 +2065,13 @@ static bool detect_lattice(const sexpm_plan_s &P, LatticeDesc &L) {
 // W_j and of the cumulative union (the support of T^_0 after term j), ascending.  The window is
 // used when U is small enough for shared memory (grid stencils in 1D / 2D; 3D octahedra of
 // radius M are not) with at least 8 resident warps per SM.
+// the symmetric path (option sym_squaring, reading R21): H bit-exactly symmetric, one GPU, the
+// tensor-core squarings
+static bool sym_path_enabled(const sexpm_plan_s &P) {
+  return P.o.sym_squaring != 0 && P.h_sym && P.world == 1 && !P.o.exact_products && !P.o.ssat &&
+         (P.o.kernel == 0 || P.o.kernel == 8 || P.o.kernel == 13) && P.N >= 1;
+}
+
 static void build_window(sexpm_plan_s &P) {
   auto &W = P.win;
   cudaStream_t st = P.st;
@@ -2092,6 +2107,22 @@ static void build_window(sexpm_plan_s &P) {
     cur.swap(nx);
   }
   const int nU = (int)U.size();
+  // half window: symmetric H, T^_0 fused into the terms (0 in D), at least two terms
+  int dz0 = -1;
+  for (size_t di = 0; di < D.size(); di++)
+    if (D[di] == 0) dz0 = (int)di;
+  const bool half = sym_path_enabled(P) && dz0 >= 0 && P.M >= 3 && !getenv("SEXPM_NO_HALF_WIN");
+  auto nonneg = [](const std::vector<int64_t> &v) {
+    std::vector<int64_t> h;
+    for (int64_t o : v)
+      if (o >= 0) h.push_back(o);
+    return h;
+  };
+  std::vector<std::vector<int64_t>> Wh((size_t)P.M + 1);
+  for (int j = 1; j <= P.M; j++) Wh[j] = nonneg(Wj[j]);
+  const std::vector<int64_t> Uh = nonneg(U);
+  int64_t padr = 0;
+  for (int64_t d : D) padr = std::max<int64_t>(padr, d);
   // positions: binary search in a sorted offset list
   auto pos = [](const std::vector<int64_t> &v, int64_t o) -> int {
     auto it = std::lower_bound(v.begin(), v.end(), o);
@@ -2121,7 +2152,9 @@ static void build_window(sexpm_plan_s &P) {
   if ((maxl + 1) * nl >= INT32_MAX || (int64_t)(U.size() + 1) * nl >= INT32_MAX || (int64_t)(nd + 1) * npad >= INT32_MAX)
     return;
   W.lcnt.assign((size_t)P.M + 1, 0);
+  W.lcnt_h.assign((size_t)P.M + 1, 0);
   W.ccnt.assign((size_t)P.M + 1, 0);
+  const int64_t nlp = half ? nl + padr : nl;  // plane stride of the S~ checkpoints
   W.woff.assign((size_t)P.M + 2, 0);
   W.coff.assign((size_t)P.M + 2, 0);
   std::vector<int32_t> hrec, hco;
@@ -2134,10 +2167,42 @@ static void build_window(sexpm_plan_s &P) {
     cum_prev = cum;  // cum_{j-1}
     cum.swap(un);    // cum_j
     W.lcnt[j] = (int)Wj[j].size();
+    W.lcnt_h[j] = (int)Wh[j].size();
     W.ccnt[j] = (int)cum.size();
     W.woff[j] = (int64_t)hrec.size();
     W.coff[j] = (int64_t)hco.size();
-    if (j >= 2) {  // TERM launch i = j: records over W_j
+    if (j >= 2 && half) {  // TERM launch i = j over W_j's offsets o >= 0
+      const int64_t zs = j == 2 ? (int64_t)nd * npad : (int64_t)W.lcnt_h[j - 1] * nlp;  // zero planes
+      const int64_t zt = (int64_t)Uh.size() * nl;
+      const std::vector<int64_t> cph = nonneg(cum_prev), cph2 = nonneg(cum_prev2);
+      for (int64_t o : Wh[j]) {
+        for (int di = 0; di < knd; di++) {
+          int64_t rv = zs;
+          if (di < nd) {
+            const int64_t sft = o - D[di];
+            if (j == 2) {  // S~_1 = H0: its diagonals exist for either sign
+              const int p = pos(Wj[1], sft);
+              if (p >= 0) rv = (int64_t)(nd - 1 - p) * npad;
+            } else if (sft >= 0) {
+              const int p = pos(Wh[j - 1], sft);
+              if (p >= 0) rv = (int64_t)p * nlp;
+            } else {  // S^_{j-1}(r, r + s) = S^_{j-1}(r + s, r): the mirror's row, shift s
+              const int p = pos(Wh[j - 1], -sft);
+              if (p >= 0) rv = (int64_t)p * nlp + sft;
+            }
+          }
+          hrec.push_back((int32_t)rv);
+        }
+        const int q = pos(cph, o);
+        const int pc = pos(cph2, o);
+        const int64_t uo = pos(Uh, o);
+        hrec.push_back((int32_t)(q < 0 ? -1 : uo * nl));
+        hrec.push_back((int32_t)(pc < 0 ? zt : uo * nl));
+        hrec.push_back((int32_t)o);
+        for (int w = knd + 3; w < rw; w++) hrec.push_back(0);
+      }
+      for (int64_t o : cph) REQUIRE(pos(Wh[j], o) >= 0, SEXPM_EINTERNAL, "window tables: cum not in W (half)");
+    } else if (j >= 2) {  // TERM launch i = j: records over W_j
       const int64_t zs = j == 2 ? (int64_t)nd * npad : (int64_t)W.lcnt[j - 1] * nl;  // zero planes
       const int64_t zt = (int64_t)nU * nl;  // T^_0's zero plane
       for (int64_t o : Wj[j]) {
@@ -2161,9 +2226,16 @@ static void build_window(sexpm_plan_s &P) {
     }
     for (int64_t o : cum) {
       hco.push_back((int32_t)o);
-      hmc.push_back((int16_t)(pos(cum_prev, o) >= 0 ? pos(U, o) : -1));
-      hmw.push_back((int16_t)pos(Wj[j], o));
-      hcu.push_back((int16_t)pos(U, o));
+      if (half) {  // the FINAL reads |o| (the mirror's row for o < 0)
+        const int64_t ao = o < 0 ? -o : o;
+        hmc.push_back((int16_t)(pos(cum_prev, ao) >= 0 ? pos(Uh, ao) : -1));
+        hmw.push_back((int16_t)pos(Wh[j], ao));
+        hcu.push_back((int16_t)pos(Uh, ao));
+      } else {
+        hmc.push_back((int16_t)(pos(cum_prev, o) >= 0 ? pos(U, o) : -1));
+        hmw.push_back((int16_t)pos(Wj[j], o));
+        hcu.push_back((int16_t)pos(U, o));
+      }
     }
   }
   int optin = 0;
@@ -2171,6 +2243,9 @@ static void build_window(sexpm_plan_s &P) {
   for (int j = 2; j <= P.M; j++)
     if (taylor_win_smem_bytes(nd, W.lcnt[j], W.ccnt[j - 1]) > optin - 1024) return;
   W.nU = nU;
+  W.half = half;
+  W.nUh = (int)Uh.size();
+  W.padr = half ? padr : 0;
   W.dzero = dzero;
   W.rw = rw;
   W.pad = pad;
@@ -2882,18 +2957,28 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
   const auto h_start = std::chrono::steady_clock::now();
   const int64_t nl = P.row_end - P.row_begin;
   const size_t nl1 = (size_t)std::max<int64_t>(nl, 1);
-  int maxl = 1, maxc = 1;
+  int maxl = 1, maxc = 1, maxlp = 1;
   for (int j = 1; j <= P.M; j++) {
     maxl = std::max(maxl, W.lcnt[j]);
     maxc = std::max(maxc, W.ccnt[j]);
+    maxlp = std::max(maxlp, W.half ? W.lcnt_h[j] : W.lcnt[j]);
   }
+  // half window (symmetric path): planes over the offsets o >= 0, padr zero rows in front
+  const int64_t plane = nl + W.padr;
+  const int nUs = W.half ? W.nUh : W.nU;
+  auto lc = [&](int j) { return W.half ? W.lcnt_h[j] : W.lcnt[j]; };
   DBuf<double> *ck_s[2] = {&P.Tn.val, &P.E.val};
   DBuf<double> &t0buf = w.bsrB.bval;
   // one extra (zero) plane each: the records' "absent" operand
   if (P.M >= 2)
-    for (int k = 0; k < 2; k++) ck_s[k]->ensure(nl1 * (size_t)(maxl + 1), st);
-  t0buf.ensure(nl1 * (size_t)(W.nU + 1), st);
-  CK(cudaMemsetAsync(t0buf.p + (size_t)W.nU * nl, 0, nl1 * sizeof(double), st));
+    for (int k = 0; k < 2; k++) {
+      ck_s[k]->ensure((size_t)std::max<int64_t>(plane, 1) * (size_t)(maxlp + 1), st);
+      if (W.padr > 0)  // the pad rows stay zero: the kernels never write them
+        CK(cudaMemset2DAsync(ck_s[k]->p, (size_t)plane * sizeof(double), 0, (size_t)W.padr * sizeof(double),
+                             (size_t)(maxlp + 1), st));
+    }
+  t0buf.ensure(nl1 * (size_t)(nUs + 1), st);
+  CK(cudaMemsetAsync(t0buf.p + (size_t)nUs * nl, 0, nl1 * sizeof(double), st));
   // band values staged in the staging pool (position-major, band_cap per row)
   // (a row of S~_i has at most |W_i| <= maxl values: sized for that, no term ever re-runs; the
   // pool is the squarings' staging pool, which is larger anyway)
@@ -2928,6 +3013,9 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
   base.row_c1 = w.row_c1.p;
   base.row_fsum = w.row_fsum.p;
   base.row_p1 = w.row_p1.p;
+  base.half = W.half ? 1 : 0;
+  base.plane = plane;
+  base.padr = W.padr;
   // CTAs (4 warps) per SM of the term kernel (default: one CTA per tile of 128 rows)
   const int win_ctas = getenv("SEXPM_WIN_CTAS") ? std::max(1, atoi(getenv("SEXPM_WIN_CTAS"))) : 1 << 20;
   cudaEvent_t k0, k1;
@@ -2953,11 +3041,11 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
     a.mapC = W.mapC.p + W.coff[i - 1];
     a.mapW = W.mapW.p + W.coff[i - 1];
     a.cumU = W.cumU.p + W.coff[i - 1];
-    a.ncnt = W.lcnt[i];
+    a.ncnt = lc(i);
     a.rec = W.rec.p + W.woff[i];
     a.nS = ck_s[sa ^ 1]->p;
     // zero planes of the inputs (absent operands)
-    if (i > 2) CK(cudaMemsetAsync(ck_s[sa]->p + (size_t)W.lcnt[i - 1] * nl, 0, nl1 * sizeof(double), st));
+    if (i > 2) CK(cudaMemsetAsync(ck_s[sa]->p + (size_t)lc(i - 1) * plane, 0, (size_t)plane * sizeof(double), st));
     if (W.dzero < 0) launch_taylor_win_t0(a, st);  // T^_0 update not fused
     a.divisor = (double)i;
     // floor lemma: K = n |W_i| bounds the entries of S~_i
@@ -3013,7 +3101,8 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
         if (passes == 0 && tau_d == eps_g) {
           Sp = allsum(P, hs[3]);
         } else {
-          launch_win_band_pass(nl, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p, nullptr, st);
+          launch_win_band_pass(nl, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p, nullptr, st, base.half,
+                               w.pool_col.p, P.row_begin);
           launch_reduce_sum(w.passrow.p, nl, w.partial.p, w.scal.p + 1, st);
           Sp = allsum(P, d2h(w.scal.p + 1, st));
         }
@@ -3027,7 +3116,8 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
     // nnz(S^_i) = sure keeps + band values above tau
     int64_t kept = hi[1];
     if (eps_g > 0.0 && !(passes == 1 && tau == eps_g) && hi[2] > 0) {
-      launch_win_band_pass(nl, w.row_cnt.p, w.pool_val.p, tau, nullptr, w.cnt2.p, st);
+      launch_win_band_pass(nl, w.row_cnt.p, w.pool_val.p, tau, nullptr, w.cnt2.p, st, base.half, w.pool_col.p,
+                           P.row_begin);
       launch_reduce_sum_i64(w.cnt2.p, nl, w.i64tmp.p + 6, st);
       kept += d2h(w.i64tmp.p + 6, st);
     }
@@ -3035,7 +3125,8 @@ static int taylor_window(sexpm_plan_s &P, DCsr &T, const std::function<double()>
     const int64_t kept_local = kept;
     float kms = 0.f;
     CK(cudaEventElapsedTime(&kms, k0, k1));
-    const double bytes = 8.0 * (double)nl * (W.lcnt[i - 1] + W.ccnt[i - 2] + W.ccnt[i - 1] + W.lcnt[i]) +
+    const double hw = W.half ? 0.5 : 1.0;  // the half window moves about half the planes
+    const double bytes = 8.0 * hw * (double)nl * (W.lcnt[i - 1] + W.ccnt[i - 2] + W.ccnt[i - 1] + W.lcnt[i]) +
                          12.0 * (double)hi[2] + 40.0 * (double)nl;
     if (i < SEXPM_MAXSTEP) {
       S.taylor_nnz_unf[i] = (int64_t)allsum(P, (double)hi[0]);
@@ -3144,8 +3235,7 @@ static void do_run(sexpm_plan_s &P) {
   const int64_t nl = P.row_end - P.row_begin;
   // symmetric squarings (option sym_squaring, reading R21): H bit-exactly symmetric, one GPU,
   // the tensor-core block kernel
-  P.sym_sq = P.o.sym_squaring != 0 && P.h_sym && P.world == 1 && !P.o.exact_products && !P.o.ssat &&
-             (P.o.kernel == 0 || P.o.kernel == 8 || P.o.kernel == 13) && P.N >= 1;
+  P.sym_sq = sym_path_enabled(P);
   DCsr &H0loc = P.H0loc;
   DCsr &T = P.T, &Tn = P.Tn, &Sc = P.S, &Sn = P.Sn;
   // ---- Taylor phase ----

@@ -4436,10 +4436,11 @@ __global__ void __launch_bounds__(kWinThreads) k_taylor_win(WinArgs a) {
     if (l >= nl) break;
     const int64_t r = a.row0 + l;
     const double *hb = a.dpad - a.hpad + r;         // h_d(r + o - d) = hb[hoff[di] + o]
-    const double *xb = H0PREV ? a.dpad + r : a.pS + l;  // S~_{i-1}(r, r + o') = xb[rec]
+    const double *xb = H0PREV ? a.dpad + r : a.pS + a.padr + l;  // S~_{i-1}(r, r + o') = xb[rec]
     const double *t0ob = a.T0old + l;
     double *t0nb = a.T0new + l;
-    double *nsb = a.nS + l;
+    double *nsb = a.nS + a.padr + l;
+    const uint32_t pstride = (uint32_t)(a.plane ? a.plane : nl);
     auto load = [&](int t, Ops &op) {
       int rc[RW];
 #pragma unroll
@@ -4454,7 +4455,7 @@ __global__ void __launch_bounds__(kWinThreads) k_taylor_win(WinArgs a) {
       op.t0n = rc[ND];
 #pragma unroll
       for (int di = 0; di < ND; di++) {
-        op.x[di] = __ldg(xb + (uint32_t)rc[di]);
+        op.x[di] = __ldg(xb + rc[di]);  // signed: a mirrored read is a row shift s < 0
         op.h[di] = __ldg(hb + (hoff[di] + (uint32_t)op.o));
       }
       op.t0 = t0ob[(uint32_t)rc[ND + 1]];  // plain load: T^_0 is updated in place
@@ -4478,21 +4479,23 @@ __global__ void __launch_bounds__(kWinThreads) k_taylor_win(WinArgs a) {
       if (cur.t0n >= 0) t0nb[(uint32_t)cur.t0n] = cur.t0 + v0;  // fused T^_0 update (d = 0 operand)
       const double x = acc / div;  // acc = +0 gives +0
       nsb[nso] = x;
-      nso += (uint32_t)nl;
+      nso += pstride;
       if (x != 0.0) {
-        nnzu++;
+        // half window: an off-diagonal value stands for itself and its mirror
+        const int mult = (a.half && cur.o != 0) ? 2 : 1;
+        nnzu += mult;
         const double ax = fabs(x);
         if (ax <= floor_tau) {
-          fs += x * x;
+          fs += mult * (x * x);
         } else if (ax <= eps_g) {
-          q1 += x * x;
+          q1 += mult * (x * x);
           if (nb < a.band_cap) {
             a.band_val[(int64_t)nb * nl + l] = x;
             a.band_col[(int64_t)nb * nl + l] = (int32_t)(r + cur.o);
           }
           nb++;
         } else {
-          c1++;
+          c1 += mult;
         }
       }
       cur = nxt;
@@ -4568,7 +4571,8 @@ void launch_taylor_win(const WinArgs &a, int ctas_per_sm, int sms, cudaStream_t 
 // Algorithm 4.1 pass over the staged band values (position-major, row_cnt per row):
 // rowsum[l] = sum over k < cnt of x^2 with |x| <= tau (k order), count[l] = |x| > tau
 __global__ void k_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val, double tau,
-                                double *rowsum, int64_t *rowcnt) {
+                                double *rowsum, int64_t *rowcnt, int half, const int32_t *band_col,
+                                int64_t row0) {
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= nl) return;
   const int64_t c = cnt[l];
@@ -4576,17 +4580,19 @@ __global__ void k_win_band_pass(int64_t nl, const int64_t *cnt, const double *ba
   int64_t k = 0;
   for (int64_t j = 0; j < c; j++) {
     const double x = band_val[(size_t)j * nl + l];
-    if (fabs(x) <= tau) s += x * x;
-    else k++;
+    const int mult = (half && band_col[(size_t)j * nl + l] != row0 + l) ? 2 : 1;
+    if (fabs(x) <= tau) s += mult * (x * x);
+    else k += mult;
   }
   if (rowsum) rowsum[l] = s;
   if (rowcnt) rowcnt[l] = k;
 }
 void launch_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val, double tau, double *rowsum,
-                          int64_t *rowcnt, cudaStream_t st) {
+                          int64_t *rowcnt, cudaStream_t st, int half, const int32_t *band_col, int64_t row0) {
   if (nl == 0) return;
   KL;
-  k_win_band_pass<<<grid_for(nl, kThreads), kThreads, 0, st>>>(nl, cnt, band_val, tau, rowsum, rowcnt);
+  k_win_band_pass<<<grid_for(nl, kThreads), kThreads, 0, st>>>(nl, cnt, band_val, tau, rowsum, rowcnt, half,
+                                                               band_col, row0);
 }
 // FINAL: T^_0 = T^_0^(m-1) + S^_m over cum_m.  Count pass (thread per row), then the write
 // pass: a CTA takes 32 rows, computes 32 positions x 32 rows per round into a shared tile
@@ -4594,7 +4600,7 @@ void launch_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val
 // contiguously (columns ascending) at rp_out[l] + the row's running count.
 __device__ __forceinline__ double win_prev(const WinArgs &a, int p, int64_t l, int64_t r, int nd) {
   if (a.prev_is_h0) return __ldg(a.dia + (size_t)(nd - 1 - p) * (size_t)a.n + (size_t)r);
-  const double x = __ldg(a.pS + (size_t)p * (size_t)a.nrows + (size_t)l);
+  const double x = __ldg(a.pS + (size_t)p * (size_t)(a.plane ? a.plane : a.nrows) + (size_t)a.padr + (size_t)l);
   return fabs(x) > a.tau_prev ? x : 0.0;
 }
 __device__ __forceinline__ double win_t0(const WinArgs &a, const int16_t *mc, const int16_t *mw, int q,
@@ -4608,7 +4614,10 @@ __device__ __forceinline__ double win_t0(const WinArgs &a, const int16_t *mc, co
 // read as its mirror (r + o, -o), position ccnt - 1 - q: T^_0 exactly symmetric (K3s input)
 __device__ __forceinline__ double win_t0s(const WinArgs &a, const int16_t *mc, const int16_t *mw,
                                           const int32_t *offs, int q, int64_t l, int64_t r, int nd) {
-  if (a.sym) {
+  if (a.half) {  // the maps point at |o|: an entry below the diagonal is its mirror's, row r + o
+    const int32_t o = offs[q];
+    if (o < 0) return l + o < 0 ? 0.0 : win_t0(a, mc, mw, q, l + o, r + o, nd);
+  } else if (a.sym) {
     const int32_t o = offs[q];
     if (o < 0) return l + o < 0 ? 0.0 : win_t0(a, mc, mw, a.c1cnt - 1 - q, l + o, r + o, nd);
   }

@@ -153,6 +153,10 @@ struct WinArgs {
   const int16_t *cumU = nullptr;   // per cum position: its U-index (T^_0 is stored over U)
   const int32_t *coffs = nullptr;  // per cum position: its offset (FINAL)
   int sym = 0;                     // FINAL: lower entries read as their mirrors (K3s input)
+  int half = 0;                    // half window (symmetric path): offsets o >= 0 only; each
+                                   // off-diagonal value counted twice in the filter's sums
+  int64_t plane = 0;               // S~ plane stride (rows + padr); 0: nrows
+  int64_t padr = 0;                // zero rows in front of each S~ plane (mirrored reads)
   int ncnt = 0;                    // |W_i| (TERM)
   const int32_t *rec = nullptr;    // TERM: per position t of W_i a record of element offsets
                                    // (kernels.cu k_taylor_win; taylor_win_rec_words(nd) int32)
@@ -178,8 +182,10 @@ int taylor_win_rec_words(int nd);
 void launch_taylor_win_t0(const WinArgs &a, cudaStream_t st);  // T^_0 update when 0 is not in D
 // persistent grid of ctas_per_sm CTAs per SM over tiles of 128 rows
 void launch_taylor_win(const WinArgs &a, int ctas_per_sm, int sms, cudaStream_t st);
+// half: each staged value whose column is not its row's counted twice (its mirror)
 void launch_win_band_pass(int64_t nl, const int64_t *cnt, const double *band_val, double tau, double *rowsum,
-                          int64_t *rowcnt, cudaStream_t st);
+                          int64_t *rowcnt, cudaStream_t st, int half = 0, const int32_t *band_col = nullptr,
+                          int64_t row0 = 0);
 // FINAL: rp_out null -> per-row counts of T^_0 into cnt; else write T^_0's rows (CSR)
 void launch_taylor_win_final(const WinArgs &a, int64_t *cnt, const int64_t *rp_out, int32_t *col_out,
                              double *val_out, cudaStream_t st);
