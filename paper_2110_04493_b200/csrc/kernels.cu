@@ -2415,6 +2415,10 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
               wb[pos] = bidx;
             }
             nm += __popc(m);
+            if (SYM) {  // row J's block columns ascend: none after this chunk's last can match
+              const int64_t tl = tb0 + 31 < t1 ? tb0 + 31 : t1 - 1;
+              if (Bv.bcol[tl] - kmin >= nkw * 32) tb0 = t1 - 32;  // (tb0 += 32 ends the scan)
+            }
           }
           __syncwarp();
           nbp += nm;
