@@ -499,6 +499,7 @@ struct StepReport {
   float asm_ms = 0.f;  // symmetric path: K3c + K3a
   bool sym = false;    // the product ran on the symmetric path
   bool relabel_needed = false;  // T^_0 in index order could not take the symmetric path
+  bool need_csr = false;        // T^ in block form could not take the symmetric path
 };
 
 // BSR-8 view of a CSR matrix (k_bsr_build) and, optionally, its block transpose
@@ -548,6 +549,8 @@ struct Workspace {
   DBuf<unsigned long long> sym_bmask;
   DBuf<double> sym_fsI;
   DBuf<int64_t> sym_nzI, sym_rowcnt, sym_rowoff;
+  DBuf<int64_t> fin_nnzI, fin_sqI, fin_l1I, fin_l2I;
+  DBuf<double> fin_rsI, sym_psum;
   DBuf<double> sym_bstore;
   DBuf<int> sym_flag;
 };
@@ -623,6 +626,11 @@ struct sexpm_plan_s {
   bool sq_tiled = false;
   bool h_sym = false;   // H bit-exactly symmetric (plan time)
   bool t_index_pending = false;  // T^_0 kept in index order: the first squaring's BSR build relabels
+  // the symmetric path hands the iterate between squarings on in block form: blk_out asks the
+  // product for it (sym_finish_blocks writes ws.bsrB), blk_valid says ws.bsrB holds T^
+  bool blk_out = false, blk_valid = false;
+  int64_t blk_nnz = 0;
+  double blk_fmas = 0.0;
   bool sym_sq = false;  // this run squares on the symmetric path (option sym_squaring)
   int agg_kind = 0;  // 0 none, 1 BFS aggregates, 2 compact aggregates, 3 lattice diamonds, 4 lattice cubes
   bool tperm_ready = false;  // tperm / tinv (/ _loc) hold the squarings' aggregate relabelling
@@ -801,7 +809,7 @@ static void bsr_transpose(sexpm_plan_s &P, BsrBufs &b) {
 // for sure), p1 = the first pass's sum when the product kernel fused it (tau_1 = eps_g).
 // Returns the final threshold tau (keep |x| > tau) and the number of passes.
 static double alg41_threshold(sexpm_plan_s &P, double eps_g, double F, bool fused_p1, double p1_local,
-                              int64_t nr, int &passes) {
+                              int64_t nr, int &passes, const SymOut *sym = nullptr, int64_t nbr = 0) {
   Workspace &w = P.ws;
   cudaStream_t st = P.st;
   passes = 0;
@@ -819,8 +827,13 @@ static double alg41_threshold(sexpm_plan_s &P, double eps_g, double F, bool fuse
     if (passes == 0 && fused_p1 && tau_d == eps_g) {
       S = allsum(P, p1_local);  // tau_1 = eps_g: summed in the product kernel's flush
     } else {
-      launch_alg41_pass_rows(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p,
-                             w.partial.p, w.scal.p + 1, st);
+      if (sym) {  // over the symmetric path's block store (per block row, rows in order)
+        launch_sym_pass(*sym, nbr, tau_d, w.sym_psum.p, st);
+        launch_reduce_sum(w.sym_psum.p, nbr, w.partial.p, w.scal.p + 1, st);
+      } else {
+        launch_alg41_pass_rows(nr, w.row_off.p, w.row_cnt.p, w.pool_val.p, tau_d, w.passrow.p,
+                               w.partial.p, w.scal.p + 1, st);
+      }
       S = allsum(P, d2h(w.scal.p + 1, st));
     }
     b = sqrtl((long double)F + (long double)S);
@@ -938,7 +951,7 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
     if (ok) {  // K3a only over K3s's complete lists
       CK(cudaMemcpyAsync(w.pool_used.p, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
       launch_sym_lidx(so, nbr, st);
-      launch_sym_assemble(nh, so, nbr, nr, P.sm_count * 4, st);
+      if (!P.blk_out) launch_sym_assemble(nh, so, nbr, nr, P.sm_count * 4, st);
       CK(cudaEventRecord(a1, st));
       CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -959,6 +972,104 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
   }
   for (cudaEvent_t e : {c0, c1, a0, a1}) cudaEventDestroy(e);
   return ok;
+}
+
+static SymOut sym_out_of(Workspace &w) {
+  SymOut so;
+  so.bstore = w.sym_bstore.p;
+  so.bmask = w.sym_bmask.p;
+  so.fsI = w.sym_fsI.p;
+  so.nzI = w.sym_nzI.p;
+  so.cj = w.sym_cj.p;
+  so.ob_off = w.sym_oboff.p;
+  so.cj_off = w.sym_cjoff.p;
+  so.nj = w.sym_nj.p;
+  so.nup = w.sym_nup.p;
+  so.wlo = w.sym_wlo.p;
+  so.whi = w.sym_whi.p;
+  so.flag = w.sym_flag.p;
+  so.rowcnt = w.sym_rowcnt.p;
+  so.rowoff = w.sym_rowoff.p;
+  so.lidx = w.sym_lidx.p;
+  return so;
+}
+
+// The symmetric product's result handed on in block form (no staging, no CSR): Algorithm 4.1
+// over the block store (passes k_sym_pass), then the next squaring's BSR-8 view written from
+// the store with |x| > tau into ws.bsrB (k_sym_fin count / scan / write), with the iterate's
+// statistics (nnz, ||I + T^||_F, bandwidths, and sum_r nnz_r^2 + nnz: the next product count)
+static void sym_finish_blocks(sexpm_plan_s &P, double eps_g, int64_t nr, StepReport &rep) {
+  Workspace &w = P.ws;
+  cudaStream_t st = P.st;
+  const int64_t nbr = (nr + 7) / 8;
+  const size_t nb1 = (size_t)std::max<int64_t>(nbr, 1);
+  const SymOut so = sym_out_of(w);
+  w.sym_psum.ensure(nb1, st);
+  launch_reduce_sum(w.sym_fsI.p, nbr, w.partial.p, w.scal.p + 0, st);
+  launch_reduce_sum_i64(w.sym_nzI.p, nbr, w.i64tmp.p + 3, st);
+  launch_reduce_sum_i64(w.sym_rowcnt.p, nr, w.i64tmp.p + 4, st);
+  double F = 0.0;
+  int64_t hz[2];
+  CK(cudaMemcpyAsync(&F, w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hz, w.i64tmp.p + 3, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  rep.nnz_unf = hz[0];
+  rep.staged = hz[1];
+  rep.fsum = F;
+  int passes = 0;
+  const double tau = alg41_threshold(P, eps_g, F, false, 0.0, nr, passes, &so, nbr);
+  rep.passes = passes;
+  rep.tau = tau;
+  // the next view: counts and statistics, scan, blocks
+  BsrBufs &b = w.bsrB;
+  b.nbr = nbr;
+  b.frag = true;
+  b.transposed = false;
+  b.bcnt.ensure(nb1 + 1, st);
+  b.brp.ensure(nb1 + 1, st);
+  w.fin_nnzI.ensure(nb1, st);
+  w.fin_sqI.ensure(nb1, st);
+  w.fin_l1I.ensure(nb1, st);
+  w.fin_l2I.ensure(nb1, st);
+  w.fin_rsI.ensure(nb1, st);
+  w.scan_tmp2.ensure((size_t)scan_tmp_elems(nbr) + 1, st);
+  SymFin f;
+  f.bcnt = b.bcnt.p;
+  f.nnzI = w.fin_nnzI.p;
+  f.sqI = w.fin_sqI.p;
+  f.rsI = w.fin_rsI.p;
+  f.l1I = w.fin_l1I.p;
+  f.l2I = w.fin_l2I.p;
+  launch_sym_fin(so, nbr, nr, tau, f, false, st);
+  launch_exclusive_scan(b.bcnt.p, nbr, b.brp.p, w.scan_tmp2.p, st);
+  launch_reduce_sum_i64(w.fin_nnzI.p, nbr, w.i64tmp.p + 0, st);
+  launch_reduce_sum_i64(w.fin_sqI.p, nbr, w.i64tmp.p + 1, st);
+  launch_reduce_max_i64(w.fin_l1I.p, nbr, w.i64tmp.p + 2, st);
+  launch_reduce_max_i64(w.fin_l2I.p, nbr, w.i64tmp.p + 5, st);
+  launch_reduce_max_i64(b.bcnt.p, nbr, w.i64tmp.p + 6, st);
+  launch_reduce_sum(w.fin_rsI.p, nbr, w.partial.p, w.scal.p + 2, st);
+  int64_t hs[7];
+  double rs = 0.0;
+  CK(cudaMemcpyAsync(hs, w.i64tmp.p, 7 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&rs, w.scal.p + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&b.nb, b.brp.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  b.bmax = hs[6];
+  const size_t nbb = (size_t)std::max<int64_t>(b.nb, 1);
+  b.bcol.ensure(nbb, st);
+  b.bval.ensure(nbb * 64, st);
+  f.brp = b.brp.p;
+  f.bcol = b.bcol.p;
+  f.bval = b.bval.p;
+  launch_sym_fin(so, nbr, nr, tau, f, true, st);
+  CK(cudaGetLastError());
+  rep.nnz = hs[0];
+  rep.normIT2 = rs;
+  rep.l1 = hs[2];
+  rep.l2 = hs[5];
+  P.blk_valid = true;
+  P.blk_nnz = hs[0];
+  P.blk_fmas = (double)hs[1] + (double)hs[0];  // sum_k nnz(row k)^2 + nnz (the 2T term)
 }
 
 static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B, double self,
@@ -1023,6 +1134,10 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
   if (dia_path) {
     hstat[0] = (int64_t)P.dia_nd * A.nnz;
     Kglob = allsum(P, (double)hstat[0]);
+  } else if (sym_planned && P.blk_valid) {  // the iterate in block form (sym_finish_blocks)
+    hstat[2] = (int64_t)P.blk_fmas;
+    hstat[0] = (int64_t)1 << 60;
+    Kglob = 0.0;
   } else if (sym_planned) {
     launch_rowlen_sq(A.rp, nr, w.bound.p, st);
     launch_reduce_sum_i64(w.bound.p, nr, w.i64tmp.p + 2, st);
@@ -1201,14 +1316,15 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
               map.rowmap = P.tperm_loc.p;
               map.colmap = P.tinv.p;
             }
-            if (P.t_index_pending && !sym_try) {  // only the symmetric path takes it
-              rep.relabel_needed = true;
+            if ((P.t_index_pending || P.blk_valid) && !sym_try) {  // only the symmetric path takes it
+              rep.relabel_needed = P.t_index_pending;
+              rep.need_csr = P.blk_valid;
               cudaEventDestroy(e0);
               cudaEventDestroy(e1);
               cudaEventDestroy(e_first);
               return;
             }
-            ok_view = build_bsr(P, B, stage == 13, !sym_try, w.bsrB, map);
+            ok_view = P.blk_valid ? true : build_bsr(P, B, stage == 13, !sym_try, w.bsrB, map);
             // K3b holds a row of A in shared memory
             if (ok_view && stage == 11 && w.bsrB.bmax > kBsrMaxRowBlocks) ok_view = false;
           }
@@ -1250,8 +1366,9 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
           if (sym_try) {
             sym_done = sym_squaring_stage(P, nh, Bv, nr, long_lists, k0, k1, rep, eps_g, floor_tau);
             rep.sym = sym_done;
-            if (!sym_done && P.t_index_pending) {  // do_run relabels T^_0 and runs the product again
-              rep.relabel_needed = true;
+            if (!sym_done && (P.t_index_pending || P.blk_valid)) {  // do_run re-runs on the CSR
+              rep.relabel_needed = P.t_index_pending;
+              rep.need_csr = P.blk_valid;
               cudaEventDestroy(k0);
               cudaEventDestroy(k1);
               cudaEventDestroy(e0);
@@ -1389,6 +1506,12 @@ static void filtered_product(sexpm_plan_s &P, const CsrView &A, const CsrView &B
                         12.0 * (double)used + 32.0 * (double)nr;
   }
 
+  if (rep.sym && P.blk_out) {  // handed on in block form: no staging, no CSR
+    P.blk_valid = false;       // the input view is consumed; sym_finish_blocks writes the next
+    sym_finish_blocks(P, eps_g, nr, rep);
+    return;
+  }
+  P.blk_valid = false;
   // Algorithm 4.1: scalar recurrence on the host, sums on the device (one
   // read-back for the floor sum, the distinct count and the fused first pass)
   launch_reduce_sum(w.row_fsum.p, nr, w.partial.p, w.scal.p + 0, st);
@@ -3392,16 +3515,46 @@ static void do_run(sexpm_plan_s &P) {
     const bool fuse_I = (i == P.N) && !P.o.output_T && !ssat;
     DCsr &dst = fuse_I ? P.E : Tn;
     const double self = ssat ? 0.0 : 2.0;  // T~ = 2T + T^2 (Eq. 4.15), or E^2 (SSAT)
+    const int64_t nnz_in = P.blk_valid ? P.blk_nnz : T.nnz;
     if (P.world == 1) {
-      filtered_product(P, T.view(), T.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
-      if (rep.relabel_needed) {  // relabel T^_0 after all, then the product as usual
-        P.t_index_pending = false;
-        permute_csr(P, T.view(), P.tperm_loc.p, P.tinv.p, Tn);
-        swap_csr(T, Tn);
+      // the symmetric path hands the iterate on in block form up to the last squaring
+      P.blk_out = P.sym_sq && i < P.N && !ssat && !getenv("SEXPM_NO_BLOCK_ITER");
+      CsrView Tv = T.view();
+      if (P.blk_valid) {  // T^ lives in ws.bsrB: no CSR of it exists
+        Tv = CsrView();
+        Tv.nrows = nl;
+        Tv.row0 = P.row_begin;
+        Tv.nnz = P.blk_nnz;
+      }
+      filtered_product(P, Tv, Tv, self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
+      if (rep.relabel_needed || rep.need_csr) {  // back to the CSR path, then the product again
+        if (rep.need_csr) {  // T^ from its block view
+          Workspace &w = P.ws;
+          w.cnt.ensure((size_t)std::max<int64_t>(nl, 1), st);
+          w.scan_tmp.ensure((size_t)scan_tmp_elems(nl) + 1, st);
+          const BsrView V = w.bsrB.view();
+          launch_bsr_to_csr(V, nl, w.cnt.p, nullptr, nullptr, nullptr, st);
+          T.nrows = nl;
+          T.row0 = P.row_begin;
+          T.padded = false;
+          T.rp.ensure((size_t)nl + 1, st);
+          launch_exclusive_scan(w.cnt.p, nl, T.rp.p, w.scan_tmp.p, st);
+          T.nnz = d2h(T.rp.p + nl, st);
+          T.col.ensure((size_t)std::max<int64_t>(T.nnz, 1), st);
+          T.val.ensure((size_t)std::max<int64_t>(T.nnz, 1), st);
+          launch_bsr_to_csr(V, nl, nullptr, T.rp.p, T.col.p, T.val.p, st);
+          P.blk_valid = false;
+        } else {  // relabel T^_0 after all
+          P.t_index_pending = false;
+          permute_csr(P, T.view(), P.tperm_loc.p, P.tinv.p, Tn);
+          swap_csr(T, Tn);
+        }
+        P.blk_out = false;
         rep = StepReport();
         filtered_product(P, T.view(), T.view(), self, 1.0, eps_g, dst, rep, nullptr, fuse_I);
       }
       P.t_index_pending = false;
+      P.blk_out = false;
     } else {
       const auto x0 = std::chrono::steady_clock::now();
       exchange_halo(P, T, l1, l2, P.Bhalo);
@@ -3431,7 +3584,7 @@ static void do_run(sexpm_plan_s &P) {
       S.sq_block_products[i] = rep.block_products;
       S.sq_assemble_ms[i] = rep.asm_ms;
       S.sq_sym_used += rep.sym ? 1 : 0;
-      S.sq_bytes[i] = 12.0 * (double)T.nnz + 12.0 * (double)dst.nnz + 16.0 * (double)nl;
+      S.sq_bytes[i] = 12.0 * (double)nnz_in + 12.0 * (double)rep.nnz + 16.0 * (double)nl;
     }
     if (getenv("SEXPM_STEP_LOG"))
       fprintf(stderr, "[sexpm run] squaring %d: nnz %lld passes %d numeric %.1f ms (first kernel %.1f) fallback %lld\n",
@@ -3439,8 +3592,9 @@ static void do_run(sexpm_plan_s &P) {
     normIT = sqrt(rep.normIT2);
     l1 = rep.l1;
     l2 = rep.l2;
-    if (!fuse_I) swap_csr(T, Tn);
+    if (!fuse_I && !P.blk_valid) swap_csr(T, Tn);  // (block form: T^ lives in ws.bsrB)
   }
+  P.blk_valid = false;
   CK(cudaEventRecord(ev_sq, st));
   // ---- e^H = I + T^_N ----
   if (ssat && P.N >= 1) {

@@ -2973,6 +2973,225 @@ void launch_sym_assemble(const NumericArgs &a, const SymOut &so, int64_t nbr, in
   k_sym_assemble<<<grid, kAsmThreads, 0, st>>>(a, so, nbr, nrows);
 }
 
+
+// ------------------------------------------------------------------------------------
+// The symmetric path between two squarings: the filtered iterate handed on in block form.
+//  k_sym_pass: Algorithm 4.1's pass sum over K3s's kept values (each entry and its mirror),
+//    sum x^2 over |x| <= tau, per block row (warp per block row, fixed order).
+//  k_sym_fin<WRITE>: the next squaring's BSR-8 view (fragment order) straight from the block
+//    store: per block row I the candidate blocks J (lower ones as the transposes of (J, I), the
+//    diagonal one mirrored from its upper triangle) keeping |x| > tau; COUNT: non-empty blocks
+//    per block row and the iterate's statistics (nnz, sum_r nnz_r^2 for the next product count,
+//    ||I + T^||_F^2, bandwidths); WRITE: block columns and values.  Warp per block row, the
+//    whole warp on one block at a time (lane l: elements 2l, 2l + 1), the next block's mask
+//    fetched ahead.
+//  k_bsr_to_csr<WRITE>: CSR rows of a fragment-order BSR view (the fallback when the next
+//    symmetric product cannot run on the view).
+// ------------------------------------------------------------------------------------
+__global__ void k_sym_pass(SymOut so, int64_t nbr, double tau, double *psum) {
+  const int64_t I = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (I >= nbr) return;
+  const int nup = (int)so.nup[I], nlow = (int)(so.nj[I] - so.nup[I]);
+  const int32_t *cj = so.cj + so.cj_off[I] + nlow;
+  const int64_t obo = so.ob_off[I];
+  double sacc = 0.0;
+  for (int u = 0; u < nup; u++) {  // the warp on one block: lane l holds kept values l, l + 32
+    const unsigned long long m = __ldg(so.bmask + obo + u);
+    const int c = __popcll(m);
+    const bool dg = cj[u] == (int)I;
+    const double *slot = so.bstore + (size_t)(obo + u) * 64;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int e = lane + 32 * h;
+      if (e < c) {
+        const double x = __ldg(slot + e);
+        if (fabs(x) <= tau) {
+          double mult = 2.0;
+          if (dg) {  // the e-th set bit's element: on the diagonal it counts once
+            unsigned long long mm = m;
+            for (int k = 0; k < e; k++) mm &= mm - 1;
+            if ((__ffsll((long long)mm) - 1) % 9 == 0) mult = 1.0;
+          }
+          sacc += mult * (x * x);
+        }
+      }
+    }
+  }
+  sacc = warp_sum(sacc);
+  if (lane == 0) psum[I] = sacc;
+}
+void launch_sym_pass(const SymOut &so, int64_t nbr, double tau, double *psum, cudaStream_t st) {
+  if (nbr == 0) return;
+  KL;
+  k_sym_pass<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, tau, psum);
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(kThreads) k_sym_fin(SymOut so, int64_t nbr, int64_t nrows, double tau,
+                                                      SymFin f) {
+  const int64_t I = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (I >= nbr) return;
+  const int nj = (int)so.nj[I], nlow = (int)(so.nj[I] - so.nup[I]);
+  const int64_t c0 = so.cj_off[I];
+  const int32_t *cj = so.cj + c0;
+  const int64_t obo = so.ob_off[I];
+  const bool hasdiag = nlow < nj && cj[nlow] == (int)I;
+  const int r = lane >> 2, t = lane & 3;  // this lane's output elements (r, 2t), (r, 2t + 1)
+  const bool rowok = 8 * I + r < nrows;
+  const int64_t grow = 8 * I + r;
+  // fragment-order positions of (r, 2t), (r, 2t + 1)
+  const int f0 = 2 * (4 * r + ((2 * t) & 3)) + ((2 * t) >> 2);
+  const int f1 = 2 * (4 * r + ((2 * t + 1) & 3)) + ((2 * t + 1) >> 2);
+  auto blk = [&](int q, int &kind) -> int64_t {
+    if (q < nlow) {
+      kind = 0;
+      return so.lidx[c0 + q];
+    }
+    kind = (q == nlow && hasdiag) ? 1 : 2;
+    return obo + (q - nlow);
+  };
+  int64_t wbase = WRITE ? f.brp[I] : 0;
+  int nblk = 0, rc = 0, havediag = 0;
+  double s2 = 0.0;
+  long long l1 = 0, l2 = 0;
+  int kind_n = 2;
+  int64_t b_n = nj > 0 ? blk(0, kind_n) : 0;
+  unsigned long long m_n = (nj > 0 && b_n >= 0) ? __ldg(so.bmask + b_n) : 0ull;
+  for (int q = 0; q < nj; q++) {
+    const int kind = kind_n;
+    const int64_t b = b_n;
+    const unsigned long long m = m_n;
+    if (q + 1 < nj) {  // the next block's mask in flight
+      b_n = blk(q + 1, kind_n);
+      m_n = b_n >= 0 ? __ldg(so.bmask + b_n) : 0ull;
+    }
+    const int J = cj[q];
+    const double *slot = so.bstore + (size_t)(b >= 0 ? b : 0) * 64;
+    double v[2];
+    bool k[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int c = 2 * t + h;
+      const int se = (kind == 0 || (kind == 1 && c < r)) ? 8 * c + r : 8 * r + c;
+      const bool present = (m >> se) & 1ull;
+      v[h] = present ? __ldg(slot + __popcll(m & ((1ull << se) - 1ull))) : 0.0;
+      k[h] = present && rowok && fabs(v[h]) > tau;
+    }
+    const unsigned any = __ballot_sync(FULL_MASK, k[0] || k[1]);
+    if (!any) continue;
+    if (!WRITE) {
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        if (k[h]) {
+          const int64_t col = 8 * (int64_t)J + 2 * t + h;
+          rc++;
+          if (col == grow) {
+            s2 += (1.0 + v[h]) * (1.0 + v[h]);
+            havediag = 1;
+          } else {
+            s2 += v[h] * v[h];
+          }
+          l1 = max(l1, (long long)(col - grow));
+          l2 = max(l2, (long long)(grow - col));
+        }
+    } else {
+      double *dst = f.bval + (size_t)(wbase + nblk) * 64;
+      dst[f0] = k[0] ? v[0] : 0.0;
+      dst[f1] = k[1] ? v[1] : 0.0;
+      if (lane == 0) f.bcol[wbase + nblk] = J;
+    }
+    nblk++;
+  }
+  if (WRITE) return;
+  // per row (its 4 lanes): nnz and the diagonal; then the block row's sums in lane order
+  int rn = rc;
+  rn += __shfl_xor_sync(FULL_MASK, rn, 1);
+  rn += __shfl_xor_sync(FULL_MASK, rn, 2);
+  int hd = havediag;
+  hd |= __shfl_xor_sync(FULL_MASK, hd, 1);
+  hd |= __shfl_xor_sync(FULL_MASK, hd, 2);
+  long long sq = (t == 0 && rowok) ? (long long)rn * rn : 0;
+  const long long nn = warp_sum((long long)rc);
+  sq = warp_sum(sq);
+  double s = warp_sum(s2);
+  const int nodiag = __popc(__ballot_sync(FULL_MASK, t == 0 && rowok && !hd));
+  l1 = warp_max(l1);
+  l2 = warp_max(l2);
+  if (lane == 0) {
+    f.bcnt[I] = nblk;
+    f.nnzI[I] = nn;
+    f.sqI[I] = sq;
+    f.rsI[I] = s + (double)nodiag;  // ||I + T^||_F^2: a missing diagonal contributes 1
+    f.l1I[I] = l1;
+    f.l2I[I] = l2;
+  }
+}
+void launch_sym_fin(const SymOut &so, int64_t nbr, int64_t nrows, double tau, const SymFin &f, bool write,
+                    cudaStream_t st) {
+  if (nbr == 0) return;
+  KL;
+  if (write)
+    k_sym_fin<true><<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, nrows, tau, f);
+  else
+    k_sym_fin<false><<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, nrows, tau, f);
+}
+
+template <bool WRITE>
+__global__ void k_bsr_to_csr(BsrView V, int64_t nrows, int64_t *cnt, const int64_t *rp, int32_t *col,
+                             double *val) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= nrows) return;
+  const int64_t I = r >> 3;
+  const int i = (int)(r & 7);
+  const int64_t b0 = V.brp[I], b1 = V.brp[I + 1];
+  int64_t pos = WRITE ? rp[r] : 0;
+  for (int64_t bb = b0; bb < b1; bb += 32) {
+    const int64_t b = bb + lane;
+    double x[8];
+    unsigned nzm = 0;
+    if (b < b1) {
+      const double *blkv = V.bval + (size_t)b * 64;
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        x[c] = __ldg(blkv + 2 * (4 * i + (c & 3)) + (c >> 2));
+        if (x[c] != 0.0) nzm |= 1u << c;
+      }
+    }
+    const int cntb = __popc(nzm);
+    int xs = cntb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL_MASK, xs, o);
+      if (lane >= o) xs += y;
+    }
+    if (WRITE && cntb) {
+      int64_t p = pos + xs - cntb;
+      const int J = V.bcol[b];
+#pragma unroll
+      for (int c = 0; c < 8; c++)
+        if ((nzm >> c) & 1u) {
+          col[p] = 8 * J + c;
+          val[p] = x[c];
+          p++;
+        }
+    }
+    pos += __shfl_sync(FULL_MASK, xs, 31);
+  }
+  if (!WRITE && lane == 0) cnt[r] = pos;
+}
+void launch_bsr_to_csr(const BsrView &V, int64_t nrows, int64_t *cnt, const int64_t *rp, int32_t *col,
+                       double *val, cudaStream_t st) {
+  if (nrows == 0) return;
+  KL;
+  if (rp)
+    k_bsr_to_csr<true><<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(V, nrows, cnt, rp, col, val);
+  else
+    k_bsr_to_csr<false><<<grid_for(nrows * 32, kThreads), kThreads, 0, st>>>(V, nrows, cnt, rp, col, val);
+}
+
 // symmetric part from the upper triangle (kernels.cuh launch_sym_intersect); warp per row
 __device__ __forceinline__ int64_t csr_find(const CsrView &A, int64_t row, int32_t c) {
   int64_t lo = A.rp[row], hi = A.rp[row + 1];

@@ -297,6 +297,23 @@ void launch_sym_count(const BsrView &Bv, int64_t *nj, int64_t *nup, int32_t *wlo
 void launch_numeric_bsrm_sym(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                              const SymOut &so, cudaStream_t st, bool long_lists);
 void launch_sym_lidx(const SymOut &so, int64_t nbr, cudaStream_t st);
+// after K3s (+ lidx): Algorithm 4.1's pass over the store (psum per block row, x 2 mirrors)
+void launch_sym_pass(const SymOut &so, int64_t nbr, double tau, double *psum, cudaStream_t st);
+// the next squaring's BSR-8 view (fragment order) from the store, |x| > tau (kernels.cu)
+struct SymFin {
+  int64_t *bcnt = nullptr;                    // COUNT: non-empty blocks per block row
+  int64_t *nnzI = nullptr, *sqI = nullptr;    // COUNT: entries; sum over rows of nnz_r^2
+  double *rsI = nullptr;                      // COUNT: ||I + T^||_F^2 of the block row's rows
+  int64_t *l1I = nullptr, *l2I = nullptr;     // COUNT: bandwidths
+  const int64_t *brp = nullptr;               // WRITE: the scan of bcnt
+  int32_t *bcol = nullptr;                    // WRITE
+  double *bval = nullptr;                     // WRITE
+};
+void launch_sym_fin(const SymOut &so, int64_t nbr, int64_t nrows, double tau, const SymFin &f, bool write,
+                    cudaStream_t st);
+// CSR rows of a fragment-order BSR view: counts (rp null) or the rows
+void launch_bsr_to_csr(const BsrView &V, int64_t nrows, int64_t *cnt, const int64_t *rp, int32_t *col,
+                       double *val, cudaStream_t st);
 void launch_sym_assemble(const NumericArgs &a, const SymOut &so, int64_t nbr, int64_t nrows, int grid,
                          cudaStream_t st);
 // T := the symmetric part read from the upper triangle: entry (r, c) kept iff (c, r) is
