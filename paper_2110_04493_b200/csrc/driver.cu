@@ -629,6 +629,7 @@ struct sexpm_plan_s {
   // the symmetric path hands the iterate between squarings on in block form: blk_out asks the
   // product for it (sym_finish_blocks writes ws.bsrB), blk_valid says ws.bsrB holds T^
   bool blk_out = false, blk_valid = false;
+  int sq_index = 0;  // the squaring being computed (1..N; 0 in the Taylor phase)
   int64_t blk_nnz = 0;
   double blk_fmas = 0.0;
   bool sym_sq = false;  // this run squares on the symmetric path (option sym_squaring)
@@ -881,6 +882,10 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
   CK(cudaEventRecord(c1, st));
   CK(cudaStreamSynchronize(st));
   bool ok = flag == 0 && tot[1] < ((int64_t)1 << 31);  // K3a's block indices are int32
+  // test hook (tests/test_gpu_symmetric.py): SEXPM_SYM_FAIL = a bitmask of squarings (bit i-1 for
+  // squaring i) whose symmetric product is refused, exercising the fall-backs
+  if (const char *fe = getenv("SEXPM_SYM_FAIL"))
+    if ((atoll(fe) >> (P.sq_index - 1)) & 1) ok = false;
   if (floor_tau == 0.0 && eps_g > 0.0) {
     // floor lemma: K = 64 x the candidate blocks of all block rows bounds the
     // number of entries of T~ (every nonzero lies in a candidate block)
@@ -3516,6 +3521,7 @@ static void do_run(sexpm_plan_s &P) {
     DCsr &dst = fuse_I ? P.E : Tn;
     const double self = ssat ? 0.0 : 2.0;  // T~ = 2T + T^2 (Eq. 4.15), or E^2 (SSAT)
     const int64_t nnz_in = P.blk_valid ? P.blk_nnz : T.nnz;
+    P.sq_index = i;
     if (P.world == 1) {
       // the symmetric path hands the iterate on in block form up to the last squaring
       P.blk_out = P.sym_sq && i < P.N && !ssat && !getenv("SEXPM_NO_BLOCK_ITER");

@@ -142,3 +142,21 @@ def test_symmetric_option_off(B):
     H = make_config(1)
     _, st = run(B, H, sym_squaring=0)
     assert st["sq_sym_used"] == 0
+
+
+@pytest.mark.parametrize("fail", [1, 2, 4, 6])
+def test_symmetric_fallbacks(B, fail, monkeypatch):
+    """The symmetric product refused at chosen squarings (test hook SEXPM_SYM_FAIL, a bitmask):
+    squaring 1 with T^_0 still in index order relabels it and runs the full product; a later
+    squaring whose input is in block form converts the view to CSR (k_bsr_to_csr) first.  The
+    result keeps parity with the oracle and the other squarings stay on the symmetric path."""
+    H = make_config(2)  # N = 4: three block-form hand-offs
+    monkeypatch.setenv("SEXPM_SYM_FAIL", str(fail))
+    Eg, st = run(B, H)
+    monkeypatch.delenv("SEXPM_SYM_FAIL")
+    N = int(st["N"])
+    assert N == 4
+    assert st["sq_sym_used"] == N - bin(fail).count("1")
+    Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS)
+    ok, res = parity(Eg, Eo, last_tau(tr, st))
+    assert ok, (fail, res)
