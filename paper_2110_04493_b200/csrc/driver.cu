@@ -549,7 +549,8 @@ struct Workspace {
   DBuf<unsigned long long> sym_bmask;
   DBuf<double> sym_fsI;
   DBuf<int64_t> sym_nzI, sym_rowcnt, sym_rowoff;
-  DBuf<int64_t> fin_nnzI, fin_sqI, fin_l1I, fin_l2I;
+  DBuf<int64_t> fin_rowcnt, fin_sq, fin_l1I;
+  DBuf<uint8_t> fin_flag;
   DBuf<double> fin_rsI, sym_psum;
   DBuf<double> sym_bstore;
   DBuf<int> sym_flag;
@@ -999,6 +1000,10 @@ static SymOut sym_out_of(Workspace &w) {
   return so;
 }
 
+static int64_t so_nup_total(Workspace &w, int64_t nbr, cudaStream_t st) {
+  return d2h(w.sym_oboff.p + nbr, st);  // the scan of K3c's upper counts
+}
+
 // The symmetric product's result handed on in block form (no staging, no CSR): Algorithm 4.1
 // over the block store (passes k_sym_pass), then the next squaring's BSR-8 view written from
 // the store with |x| > tau into ws.bsrB (k_sym_fin count / scan / write), with the iterate's
@@ -1032,25 +1037,27 @@ static void sym_finish_blocks(sexpm_plan_s &P, double eps_g, int64_t nr, StepRep
   b.transposed = false;
   b.bcnt.ensure(nb1 + 1, st);
   b.brp.ensure(nb1 + 1, st);
-  w.fin_nnzI.ensure(nb1, st);
-  w.fin_sqI.ensure(nb1, st);
+  const size_t nr1 = (size_t)std::max<int64_t>(nr, 1);
+  w.fin_rowcnt.ensure(nr1, st);
+  w.fin_sq.ensure(nr1, st);
+  w.fin_flag.ensure((size_t)std::max<int64_t>(so_nup_total(w, nbr, st), 1), st);
   w.fin_l1I.ensure(nb1, st);
-  w.fin_l2I.ensure(nb1, st);
   w.fin_rsI.ensure(nb1, st);
-  w.scan_tmp2.ensure((size_t)scan_tmp_elems(nbr) + 1, st);
+  w.scan_tmp2.ensure((size_t)scan_tmp_elems(std::max<int64_t>(nbr, nr)) + 1, st);
+  CK(cudaMemsetAsync(b.bcnt.p, 0, nb1 * sizeof(int64_t), st));
+  CK(cudaMemsetAsync(w.fin_rowcnt.p, 0, nr1 * sizeof(int64_t), st));
   SymFin f;
   f.bcnt = b.bcnt.p;
-  f.nnzI = w.fin_nnzI.p;
-  f.sqI = w.fin_sqI.p;
+  f.rowcnt = w.fin_rowcnt.p;
+  f.flag = w.fin_flag.p;
   f.rsI = w.fin_rsI.p;
   f.l1I = w.fin_l1I.p;
-  f.l2I = w.fin_l2I.p;
   launch_sym_fin(so, nbr, nr, tau, f, false, st);
   launch_exclusive_scan(b.bcnt.p, nbr, b.brp.p, w.scan_tmp2.p, st);
-  launch_reduce_sum_i64(w.fin_nnzI.p, nbr, w.i64tmp.p + 0, st);
-  launch_reduce_sum_i64(w.fin_sqI.p, nbr, w.i64tmp.p + 1, st);
+  launch_rowcnt_sq(w.fin_rowcnt.p, nr, w.fin_sq.p, st);
+  launch_reduce_sum_i64(w.fin_rowcnt.p, nr, w.i64tmp.p + 0, st);
+  launch_reduce_sum_i64(w.fin_sq.p, nr, w.i64tmp.p + 1, st);
   launch_reduce_max_i64(w.fin_l1I.p, nbr, w.i64tmp.p + 2, st);
-  launch_reduce_max_i64(w.fin_l2I.p, nbr, w.i64tmp.p + 5, st);
   launch_reduce_max_i64(b.bcnt.p, nbr, w.i64tmp.p + 6, st);
   launch_reduce_sum(w.fin_rsI.p, nbr, w.partial.p, w.scal.p + 2, st);
   int64_t hs[7];
@@ -1071,7 +1078,7 @@ static void sym_finish_blocks(sexpm_plan_s &P, double eps_g, int64_t nr, StepRep
   rep.nnz = hs[0];
   rep.normIT2 = rs;
   rep.l1 = hs[2];
-  rep.l2 = hs[5];
+  rep.l2 = hs[2];  // symmetric
   P.blk_valid = true;
   P.blk_nnz = hs[0];
   P.blk_fmas = (double)hs[1] + (double)hs[0];  // sum_k nnz(row k)^2 + nnz (the 2T term)

@@ -3027,9 +3027,95 @@ void launch_sym_pass(const SymOut &so, int64_t nbr, double tau, double *psum, cu
   k_sym_pass<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, tau, psum);
 }
 
-template <bool WRITE>
-__global__ void __launch_bounds__(kThreads) k_sym_fin(SymOut so, int64_t nbr, int64_t nrows, double tau,
-                                                      SymFin f) {
+// COUNT: warp per block row I over its upper blocks only (each entry with its mirror): the
+// block's elements kept after tau, a flag per upper block (non-empty), the non-empty block
+// counts of I and of J (the mirror, atomics), kept counts per row (own rows summed per warp,
+// mirror rows by atomics), the block row's ||I + T^||_F^2 share (x^2 twice off the diagonal,
+// (1 + x)^2 on it, 1 per row without a kept diagonal) and bandwidth
+__global__ void __launch_bounds__(kThreads) k_sym_fin_count(SymOut so, int64_t nbr, int64_t nrows, double tau,
+                                                            SymFin f) {
+  const int64_t I = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (I >= nbr) return;
+  const int nup = (int)so.nup[I], nlow = (int)(so.nj[I] - so.nup[I]);
+  const int32_t *cj = so.cj + so.cj_off[I] + nlow;
+  const int64_t obo = so.ob_off[I];
+  const int r = lane >> 2, t = lane & 3;  // stored elements (r, 2t), (r, 2t + 1)
+  int rown = 0, nblk = 0, diagk = 0;
+  double s2 = 0.0;
+  long long l1 = 0;
+  for (int u = 0; u < nup; u++) {
+    const unsigned long long m = __ldg(so.bmask + obo + u);
+    if (m == 0ull) {
+      if (lane == 0) f.flag[obo + u] = 0;
+      continue;
+    }
+    const int J = cj[u];
+    const bool dg = J == (int)I;
+    const double *slot = so.bstore + (size_t)(obo + u) * 64;
+    bool k[2];
+    double v[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int c = 2 * t + h, se = 8 * r + c;
+      const bool present = (m >> se) & 1ull;
+      v[h] = present ? __ldg(slot + __popcll(m & ((1ull << se) - 1ull))) : 0.0;
+      k[h] = present && fabs(v[h]) > tau;  // (the diagonal block stores only c >= r)
+    }
+    const unsigned any = __ballot_sync(FULL_MASK, k[0] || k[1]);
+    if (lane == 0) f.flag[obo + u] = any ? 1 : 0;
+    if (!any) continue;
+    nblk++;
+    int mc[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+      if (k[h]) {
+        const int c = 2 * t + h;
+        rown++;
+        if (dg && c == r) {
+          s2 += (1.0 + v[h]) * (1.0 + v[h]);
+          diagk = 1;
+        } else {
+          s2 += 2.0 * (v[h] * v[h]);  // the entry and its mirror
+          mc[h] = 1;
+          l1 = max(l1, (long long)(8 * (int64_t)J + c - (8 * I + r)));
+        }
+      }
+    // mirrors: column c of (I, J) is row 8J + c's (the 8 lanes of a column pair summed)
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      mc[0] += __shfl_xor_sync(FULL_MASK, mc[0], o);
+      mc[1] += __shfl_xor_sync(FULL_MASK, mc[1], o);
+    }
+    if (r == 0) {
+      if (mc[0]) atomicAdd(reinterpret_cast<unsigned long long *>(f.rowcnt + 8 * (int64_t)J + 2 * t), (unsigned long long)mc[0]);
+      if (mc[1]) atomicAdd(reinterpret_cast<unsigned long long *>(f.rowcnt + 8 * (int64_t)J + 2 * t + 1), (unsigned long long)mc[1]);
+    }
+    if (!dg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(f.bcnt + J), 1ull);
+  }
+  // own rows: the 4 lanes of each row
+  rown += __shfl_xor_sync(FULL_MASK, rown, 1);
+  rown += __shfl_xor_sync(FULL_MASK, rown, 2);
+  diagk |= __shfl_xor_sync(FULL_MASK, diagk, 1);
+  diagk |= __shfl_xor_sync(FULL_MASK, diagk, 2);
+  const bool rowok = 8 * I + r < nrows;
+  if (t == 0 && rowok && rown)
+    atomicAdd(reinterpret_cast<unsigned long long *>(f.rowcnt + 8 * I + r), (unsigned long long)rown);
+  const int nodiag = __popc(__ballot_sync(FULL_MASK, t == 0 && rowok && !diagk));
+  s2 = warp_sum(s2);
+  l1 = warp_max(l1);
+  if (lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long *>(f.bcnt + I), (unsigned long long)nblk);
+    f.rsI[I] = s2 + (double)nodiag;
+    f.l1I[I] = l1;
+  }
+}
+
+// WRITE: warp per block row I over its candidates in column order; the non-empty ones (the
+// upper block's flag, a lower block's mirror's flag) are written, the warp on one block at a
+// time: lane l writes elements (r, 2t), (r, 2t + 1) in fragment order, zeros where dropped
+__global__ void __launch_bounds__(kThreads) k_sym_fin_write(SymOut so, int64_t nbr, int64_t nrows, double tau,
+                                                            SymFin f) {
   const int64_t I = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (I >= nbr) return;
@@ -3038,94 +3124,43 @@ __global__ void __launch_bounds__(kThreads) k_sym_fin(SymOut so, int64_t nbr, in
   const int32_t *cj = so.cj + c0;
   const int64_t obo = so.ob_off[I];
   const bool hasdiag = nlow < nj && cj[nlow] == (int)I;
-  const int r = lane >> 2, t = lane & 3;  // this lane's output elements (r, 2t), (r, 2t + 1)
+  const int r = lane >> 2, t = lane & 3;
   const bool rowok = 8 * I + r < nrows;
-  const int64_t grow = 8 * I + r;
-  // fragment-order positions of (r, 2t), (r, 2t + 1)
   const int f0 = 2 * (4 * r + ((2 * t) & 3)) + ((2 * t) >> 2);
   const int f1 = 2 * (4 * r + ((2 * t + 1) & 3)) + ((2 * t + 1) >> 2);
-  auto blk = [&](int q, int &kind) -> int64_t {
-    if (q < nlow) {
-      kind = 0;
-      return so.lidx[c0 + q];
+  int64_t pos = f.brp[I];
+  for (int q0 = 0; q0 < nj; q0 += 32) {
+    const int q = q0 + lane;
+    int64_t b = -1;
+    int fl = 0;
+    if (q < nj) {
+      b = q < nlow ? (int64_t)so.lidx[c0 + q] : obo + (q - nlow);
+      fl = b >= 0 ? f.flag[b] : 0;
     }
-    kind = (q == nlow && hasdiag) ? 1 : 2;
-    return obo + (q - nlow);
-  };
-  int64_t wbase = WRITE ? f.brp[I] : 0;
-  int nblk = 0, rc = 0, havediag = 0;
-  double s2 = 0.0;
-  long long l1 = 0, l2 = 0;
-  int kind_n = 2;
-  int64_t b_n = nj > 0 ? blk(0, kind_n) : 0;
-  unsigned long long m_n = (nj > 0 && b_n >= 0) ? __ldg(so.bmask + b_n) : 0ull;
-  for (int q = 0; q < nj; q++) {
-    const int kind = kind_n;
-    const int64_t b = b_n;
-    const unsigned long long m = m_n;
-    if (q + 1 < nj) {  // the next block's mask in flight
-      b_n = blk(q + 1, kind_n);
-      m_n = b_n >= 0 ? __ldg(so.bmask + b_n) : 0ull;
-    }
-    const int J = cj[q];
-    const double *slot = so.bstore + (size_t)(b >= 0 ? b : 0) * 64;
-    double v[2];
-    bool k[2];
+    unsigned nem = __ballot_sync(FULL_MASK, fl != 0);
+    while (nem) {  // the chunk's non-empty blocks, in order, the whole warp on each
+      const int src = __ffs(nem) - 1;
+      nem &= nem - 1;
+      const int qq = q0 + src;
+      const int64_t bb = __shfl_sync(FULL_MASK, b, src);
+      const int kind = qq < nlow ? 0 : ((qq == nlow && hasdiag) ? 1 : 2);
+      const unsigned long long m = __ldg(so.bmask + bb);
+      const double *slot = so.bstore + (size_t)bb * 64;
+      double v[2];
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int c = 2 * t + h;
-      const int se = (kind == 0 || (kind == 1 && c < r)) ? 8 * c + r : 8 * r + c;
-      const bool present = (m >> se) & 1ull;
-      v[h] = present ? __ldg(slot + __popcll(m & ((1ull << se) - 1ull))) : 0.0;
-      k[h] = present && rowok && fabs(v[h]) > tau;
+      for (int h = 0; h < 2; h++) {
+        const int c = 2 * t + h;
+        const int se = (kind == 0 || (kind == 1 && c < r)) ? 8 * c + r : 8 * r + c;
+        const bool present = (m >> se) & 1ull;
+        const double x = present ? __ldg(slot + __popcll(m & ((1ull << se) - 1ull))) : 0.0;
+        v[h] = (present && rowok && fabs(x) > tau) ? x : 0.0;
+      }
+      double *dst = f.bval + (size_t)pos * 64;
+      dst[f0] = v[0];
+      dst[f1] = v[1];
+      if (lane == 0) f.bcol[pos] = cj[qq];
+      pos++;
     }
-    const unsigned any = __ballot_sync(FULL_MASK, k[0] || k[1]);
-    if (!any) continue;
-    if (!WRITE) {
-#pragma unroll
-      for (int h = 0; h < 2; h++)
-        if (k[h]) {
-          const int64_t col = 8 * (int64_t)J + 2 * t + h;
-          rc++;
-          if (col == grow) {
-            s2 += (1.0 + v[h]) * (1.0 + v[h]);
-            havediag = 1;
-          } else {
-            s2 += v[h] * v[h];
-          }
-          l1 = max(l1, (long long)(col - grow));
-          l2 = max(l2, (long long)(grow - col));
-        }
-    } else {
-      double *dst = f.bval + (size_t)(wbase + nblk) * 64;
-      dst[f0] = k[0] ? v[0] : 0.0;
-      dst[f1] = k[1] ? v[1] : 0.0;
-      if (lane == 0) f.bcol[wbase + nblk] = J;
-    }
-    nblk++;
-  }
-  if (WRITE) return;
-  // per row (its 4 lanes): nnz and the diagonal; then the block row's sums in lane order
-  int rn = rc;
-  rn += __shfl_xor_sync(FULL_MASK, rn, 1);
-  rn += __shfl_xor_sync(FULL_MASK, rn, 2);
-  int hd = havediag;
-  hd |= __shfl_xor_sync(FULL_MASK, hd, 1);
-  hd |= __shfl_xor_sync(FULL_MASK, hd, 2);
-  long long sq = (t == 0 && rowok) ? (long long)rn * rn : 0;
-  const long long nn = warp_sum((long long)rc);
-  sq = warp_sum(sq);
-  double s = warp_sum(s2);
-  const int nodiag = __popc(__ballot_sync(FULL_MASK, t == 0 && rowok && !hd));
-  l1 = warp_max(l1);
-  l2 = warp_max(l2);
-  if (lane == 0) {
-    f.bcnt[I] = nblk;
-    f.nnzI[I] = nn;
-    f.sqI[I] = sq;
-    f.rsI[I] = s + (double)nodiag;  // ||I + T^||_F^2: a missing diagonal contributes 1
-    f.l1I[I] = l1;
-    f.l2I[I] = l2;
   }
 }
 void launch_sym_fin(const SymOut &so, int64_t nbr, int64_t nrows, double tau, const SymFin &f, bool write,
@@ -3133,9 +3168,19 @@ void launch_sym_fin(const SymOut &so, int64_t nbr, int64_t nrows, double tau, co
   if (nbr == 0) return;
   KL;
   if (write)
-    k_sym_fin<true><<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, nrows, tau, f);
+    k_sym_fin_write<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, nrows, tau, f);
   else
-    k_sym_fin<false><<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, nrows, tau, f);
+    k_sym_fin_count<<<grid_for(nbr * 32, kThreads), kThreads, 0, st>>>(so, nbr, nrows, tau, f);
+}
+// sum and sum of squares of the rows' counts (the next product count)
+__global__ void k_rowcnt_sums(const int64_t *rc, int64_t n, int64_t *sq) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) sq[r] = rc[r] * rc[r];
+}
+void launch_rowcnt_sq(const int64_t *rc, int64_t n, int64_t *sq, cudaStream_t st) {
+  if (n == 0) return;
+  KL;
+  k_rowcnt_sums<<<grid_for(n, kThreads), kThreads, 0, st>>>(rc, n, sq);
 }
 
 template <bool WRITE>

@@ -301,16 +301,18 @@ void launch_sym_lidx(const SymOut &so, int64_t nbr, cudaStream_t st);
 void launch_sym_pass(const SymOut &so, int64_t nbr, double tau, double *psum, cudaStream_t st);
 // the next squaring's BSR-8 view (fragment order) from the store, |x| > tau (kernels.cu)
 struct SymFin {
-  int64_t *bcnt = nullptr;                    // COUNT: non-empty blocks per block row
-  int64_t *nnzI = nullptr, *sqI = nullptr;    // COUNT: entries; sum over rows of nnz_r^2
-  double *rsI = nullptr;                      // COUNT: ||I + T^||_F^2 of the block row's rows
-  int64_t *l1I = nullptr, *l2I = nullptr;     // COUNT: bandwidths
+  int64_t *bcnt = nullptr;                    // COUNT: non-empty blocks per block row (zeroed before)
+  int64_t *rowcnt = nullptr;                  // COUNT: kept entries per row (zeroed before)
+  uint8_t *flag = nullptr;                    // COUNT: per upper block, non-empty after tau
+  double *rsI = nullptr;                      // COUNT: ||I + T^||_F^2 share of the block row
+  int64_t *l1I = nullptr;                     // COUNT: bandwidth (symmetric: l1 = l2)
   const int64_t *brp = nullptr;               // WRITE: the scan of bcnt
   int32_t *bcol = nullptr;                    // WRITE
   double *bval = nullptr;                     // WRITE
 };
 void launch_sym_fin(const SymOut &so, int64_t nbr, int64_t nrows, double tau, const SymFin &f, bool write,
                     cudaStream_t st);
+void launch_rowcnt_sq(const int64_t *rc, int64_t n, int64_t *sq, cudaStream_t st);  // sq[r] = rc[r]^2
 // CSR rows of a fragment-order BSR view: counts (rp null) or the rows
 void launch_bsr_to_csr(const BsrView &V, int64_t nrows, int64_t *cnt, const int64_t *rp, int32_t *col,
                        double *val, cudaStream_t st);
