@@ -929,10 +929,10 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
     w.sym_rowcnt.ensure((size_t)std::max<int64_t>(nr, 1), st);
     w.sym_rowoff.ensure((size_t)nr + 1, st);
     w.scan_tmp.ensure((size_t)scan_tmp_elems(nr) + 1, st);
-    so.rowcnt = w.sym_rowcnt.p;
+    so.rowcnt = P.blk_out ? nullptr : w.sym_rowcnt.p;  // K3a's row counts: the last squaring
     so.lidx = w.sym_lidx.p;
     so.rowoff = w.sym_rowoff.p;
-    CK(cudaMemsetAsync(w.sym_rowcnt.p, 0, (size_t)nr * sizeof(int64_t), st));
+    if (!P.blk_out) CK(cudaMemsetAsync(w.sym_rowcnt.p, 0, (size_t)nr * sizeof(int64_t), st));
     so.whi = w.sym_whi.p;
     so.flag = w.sym_flag.p;
     CK(cudaMemsetAsync(w.row_counter.p, 0, sizeof(int), st));
@@ -941,10 +941,12 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
     CK(cudaEventRecord(k1, st));
     // the rows' pool offsets: a scan of K3s's kept counts (deterministic layout)
     CK(cudaEventRecord(a0, st));
-    launch_exclusive_scan(w.sym_rowcnt.p, nr, w.sym_rowoff.p, w.scan_tmp.p, st);
     int64_t total = 0;
+    if (!P.blk_out) {  // (handed on in block form: no rows are staged)
+      launch_exclusive_scan(w.sym_rowcnt.p, nr, w.sym_rowoff.p, w.scan_tmp.p, st);
+      CK(cudaMemcpyAsync(&total, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaMemcpyAsync(&flag, w.sym_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&total, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     ok = flag == 0;
     if (ok && total > nh.pool_cap) {  // exact size known: grow the pool, no re-run
@@ -955,7 +957,8 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
       nh.pool_cap = (int64_t)std::min(w.pool_col.n, w.pool_val.n);
     }
     if (ok) {  // K3a only over K3s's complete lists
-      CK(cudaMemcpyAsync(w.pool_used.p, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      if (!P.blk_out)
+        CK(cudaMemcpyAsync(w.pool_used.p, w.sym_rowoff.p + nr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
       launch_sym_lidx(so, nbr, st);
       if (!P.blk_out) launch_sym_assemble(nh, so, nbr, nr, P.sm_count * 4, st);
       CK(cudaEventRecord(a1, st));
@@ -1017,7 +1020,7 @@ static void sym_finish_blocks(sexpm_plan_s &P, double eps_g, int64_t nr, StepRep
   w.sym_psum.ensure(nb1, st);
   launch_reduce_sum(w.sym_fsI.p, nbr, w.partial.p, w.scal.p + 0, st);
   launch_reduce_sum_i64(w.sym_nzI.p, nbr, w.i64tmp.p + 3, st);
-  launch_reduce_sum_i64(w.sym_rowcnt.p, nr, w.i64tmp.p + 4, st);
+  CK(cudaMemsetAsync(w.i64tmp.p + 4, 0, sizeof(int64_t), st));  // (no rows staged)
   double F = 0.0;
   int64_t hz[2];
   CK(cudaMemcpyAsync(&F, w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));

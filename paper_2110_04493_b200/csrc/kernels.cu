@@ -2508,16 +2508,18 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
           if (lane == 0) so.bmask[blk] = msk;
           // kept counts of the rows: row g of I here (summed per CTA below), column c's
           // mirrors (strictly above the diagonal of a diagonal block) to row 8J + c now
-          rkept += (k0 ? 1 : 0) + (k1 ? 1 : 0);
-          int mc0 = (k0 && (!dg || 2 * t > g)) ? 1 : 0, mc1 = (k1 && (!dg || 2 * t + 1 > g)) ? 1 : 0;
+          if (so.rowcnt) {  // K3a's row counts (the last squaring only; warp-uniform)
+            rkept += (k0 ? 1 : 0) + (k1 ? 1 : 0);
+            int mc0 = (k0 && (!dg || 2 * t > g)) ? 1 : 0, mc1 = (k1 && (!dg || 2 * t + 1 > g)) ? 1 : 0;
 #pragma unroll
-          for (int o = 4; o < 32; o <<= 1) {
-            mc0 += __shfl_xor_sync(FULL_MASK, mc0, o);
-            mc1 += __shfl_xor_sync(FULL_MASK, mc1, o);
-          }
-          if (g == 0) {
-            if (mc0) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * (int64_t)J + 2 * t), (unsigned long long)mc0);
-            if (mc1) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * (int64_t)J + 2 * t + 1), (unsigned long long)mc1);
+            for (int o = 4; o < 32; o <<= 1) {
+              mc0 += __shfl_xor_sync(FULL_MASK, mc0, o);
+              mc1 += __shfl_xor_sync(FULL_MASK, mc1, o);
+            }
+            if (g == 0) {
+              if (mc0) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * (int64_t)J + 2 * t), (unsigned long long)mc0);
+              if (mc1) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * (int64_t)J + 2 * t + 1), (unsigned long long)mc1);
+            }
           }
           continue;
         }
@@ -2569,7 +2571,7 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
       }
       if (t == 0) s_c1[warp][g] = rkept;
       __syncthreads();
-      if (tid < 8 && 8 * I + tid < nrows) {
+      if (so.rowcnt && tid < 8 && 8 * I + tid < nrows) {
         long long c = 0;
         for (int w = 0; w < kMWarps; w++) c += s_c1[w][tid];
         if (c) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * I + tid), (unsigned long long)c);
