@@ -2169,7 +2169,7 @@ __device__ __forceinline__ unsigned spread4(unsigned m) {
 // short match lists (2D: more warps), <4, 2> for long ones (3D: more loads per warp)
 // SYM (K3s, see kernels.cuh SymOut): only the output blocks J >= I, written raw to the block
 // store; cand(I) to the J store; classification and staging are left to K3a
-template <int kMPF, int kMinB, bool SYM = false>
+template <int kMPF, int kMinB, bool SYM = false, bool ROWCNT = true>
 __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a, BsrView Bv, int64_t nrows,
                                                               double *scratch, int32_t *fail_rows,
                                                               int *fail_count, SymOut so) {
@@ -2508,7 +2508,7 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
           if (lane == 0) so.bmask[blk] = msk;
           // kept counts of the rows: row g of I here (summed per CTA below), column c's
           // mirrors (strictly above the diagonal of a diagonal block) to row 8J + c now
-          if (so.rowcnt) {  // K3a's row counts (the last squaring only; warp-uniform)
+          if (ROWCNT && so.rowcnt) {  // K3a's row counts (the last squaring only)
             rkept += (k0 ? 1 : 0) + (k1 ? 1 : 0);
             int mc0 = (k0 && (!dg || 2 * t > g)) ? 1 : 0, mc1 = (k1 && (!dg || 2 * t + 1 > g)) ? 1 : 0;
 #pragma unroll
@@ -2563,15 +2563,17 @@ __global__ void __launch_bounds__(kMThreads, kMinB) k_numeric_bsrm(NumericArgs a
     if constexpr (SYM) {  // the block row's dropped sum x^2 and nonzero count (warps in order)
       fs = warp_sum(fs);
       nz = warp_sum(nz);
-      rkept += __shfl_xor_sync(FULL_MASK, rkept, 1);  // row g: its 4 lanes
-      rkept += __shfl_xor_sync(FULL_MASK, rkept, 2);
+      if (ROWCNT) {
+        rkept += __shfl_xor_sync(FULL_MASK, rkept, 1);  // row g: its 4 lanes
+        rkept += __shfl_xor_sync(FULL_MASK, rkept, 2);
+      }
       if (lane == 0) {
         s_fs[warp][0] = fs;
         s_nz[warp][0] = nz;
       }
       if (t == 0) s_c1[warp][g] = rkept;
       __syncthreads();
-      if (so.rowcnt && tid < 8 && 8 * I + tid < nrows) {
+      if (ROWCNT && so.rowcnt && tid < 8 && 8 * I + tid < nrows) {
         long long c = 0;
         for (int w = 0; w < kMWarps; w++) c += s_c1[w][tid];
         if (c) atomicAdd(reinterpret_cast<unsigned long long *>(so.rowcnt + 8 * I + tid), (unsigned long long)c);
@@ -2690,13 +2692,11 @@ void launch_numeric_bsrm_sym(const NumericArgs &a, const BsrView &Bv, int64_t nr
   if (Bv.nbr_a == 0) return;
   const int smem = bsrm_numeric_smem_bytes();
   KL;
-  if (long_lists) {
-    cudaFuncSetAttribute(k_numeric_bsrm<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_numeric_bsrm<4, 2, true><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, nullptr, nullptr, so);
-  } else {
-    cudaFuncSetAttribute(k_numeric_bsrm<2, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_numeric_bsrm<2, 4, true><<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, nullptr, nullptr, so);
-  }
+  // (no row counts when the product is handed on in block form: a leaner epilogue)
+  auto kf = long_lists ? (so.rowcnt ? k_numeric_bsrm<4, 2, true, true> : k_numeric_bsrm<4, 2, true, false>)
+                       : (so.rowcnt ? k_numeric_bsrm<2, 4, true, true> : k_numeric_bsrm<2, 4, true, false>);
+  cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kf<<<a.grid, kMThreads, smem, st>>>(a, Bv, nrows, scratch, nullptr, nullptr, so);
 }
 
 // K3c: per block row I of the symmetric squaring, |cand(I)| (the union of the block rows K of
