@@ -4676,7 +4676,7 @@ int taylor_win_smem_bytes(int nd, int ncnt, int ccnt) {
   return ncnt * taylor_win_rec_words(nd) * 4 + 16;
 }
 template <int ND, bool H0PREV>  // H0PREV: S~_{i-1} = H0 (i = 2)
-__global__ void __launch_bounds__(kWinThreads) k_taylor_win(WinArgs a) {
+__global__ void __launch_bounds__(kWinThreads, 7) k_taylor_win(WinArgs a) {
   extern __shared__ int4 wsm4[];
   constexpr int RW = ((ND + 3) + 3) / 4 * 4;
   const int tid = threadIdx.x;
