@@ -873,6 +873,10 @@ static bool sym_squaring_stage(sexpm_plan_s &P, NumericArgs nh, const BsrView &B
   CK(cudaEventRecord(c0, st));
   CK(cudaMemsetAsync(w.sym_flag.p, 0, sizeof(int), st));
   launch_sym_count(Bv, w.sym_nj.p, w.sym_nup.p, w.sym_wlo.p, w.sym_whi.p, w.sym_flag.p, st);
+  if (d2h(w.sym_flag.p, st) & 32) {  // a block row's union wider than the small bitmaps
+    CK(cudaMemsetAsync(w.sym_flag.p, 0, sizeof(int), st));
+    launch_sym_count(Bv, w.sym_nj.p, w.sym_nup.p, w.sym_wlo.p, w.sym_whi.p, w.sym_flag.p, st, true);
+  }
   launch_exclusive_scan(w.sym_nj.p, nbr, w.sym_cjoff.p, w.scan_tmp2.p, st);
   launch_exclusive_scan(w.sym_nup.p, nbr, w.sym_oboff.p, w.scan_tmp2.p, st);
   int64_t tot[2];

@@ -2705,10 +2705,10 @@ void launch_numeric_bsrm_sym(const NumericArgs &a, const BsrView &Bv, int64_t nr
 // Warp per block row, a 65536-block-column bitmap per warp; wider unions -> flag 1.
 constexpr int kSymCntWarps = 8, kSymCntWords = 2048;
 __global__ void __launch_bounds__(kSymCntWarps * 32) k_sym_count(BsrView Bv, int64_t *nj, int64_t *nup,
-                                                                 int32_t *wlo, int32_t *whi, int *flag) {
+                                                                 int32_t *wlo, int32_t *whi, int *flag, int words) {
   extern __shared__ unsigned scw[];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  unsigned *bm = scw + wi * kSymCntWords;
+  unsigned *bm = scw + wi * words;
   const int64_t I = (int64_t)blockIdx.x * kSymCntWarps + wi;
   if (I >= Bv.nbr) return;
   const int64_t a0 = Bv.brp[I], a1 = Bv.brp[I + 1];
@@ -2737,9 +2737,9 @@ __global__ void __launch_bounds__(kSymCntWarps * 32) k_sym_count(BsrView Bv, int
     return;
   }
   const int nw = ((jhi - jlo) >> 5) + 1;
-  if (nw > kSymCntWords) {
+  if (nw > words) {  // wider than this launch's bitmaps: 32 asks for a launch with the largest
     if (lane == 0) {
-      atomicOr(flag, 1);
+      atomicOr(flag, words < kSymCntWords ? 32 : 1);
       nj[I] = 0;
       nup[I] = 0;
     }
@@ -2786,13 +2786,18 @@ __global__ void __launch_bounds__(kSymCntWarps * 32) k_sym_count(BsrView Bv, int
   }
 }
 void launch_sym_count(const BsrView &Bv, int64_t *nj, int64_t *nup, int32_t *wlo, int32_t *whi, int *flag,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool wide) {
   if (Bv.nbr == 0) return;
-  const int smem = kSymCntWarps * kSymCntWords * 4;
+  // 512-word bitmaps first (16 KB per CTA: occupancy); rows wider set flag 32 and the driver
+  // runs the count again with the largest
+  // (test hook: SEXPM_K3C_WORDS sets the first launch's bitmap words)
+  const int words = wide ? kSymCntWords
+                         : (getenv("SEXPM_K3C_WORDS") ? std::max(1, std::min(kSymCntWords, atoi(getenv("SEXPM_K3C_WORDS")))) : 512);
+  const int smem = kSymCntWarps * words * 4;
   cudaFuncSetAttribute(k_sym_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   KL;
   k_sym_count<<<(unsigned)((Bv.nbr + kSymCntWarps - 1) / kSymCntWarps), kSymCntWarps * 32, smem, st>>>(Bv, nj, nup, wlo,
-                                                                                                   whi, flag);
+                                                                                                   whi, flag, words);
 }
 
 // ------------------------------------------------------------------------------------

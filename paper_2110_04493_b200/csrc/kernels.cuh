@@ -293,7 +293,7 @@ struct SymOut {
 // and the union's block-column extent [wlo, whi] (K3s's window: cand(I) is then the exact block
 // union, symmetric for a symmetric block pattern)
 void launch_sym_count(const BsrView &Bv, int64_t *nj, int64_t *nup, int32_t *wlo, int32_t *whi, int *flag,
-                      cudaStream_t st);
+                      cudaStream_t st, bool wide = false);
 void launch_numeric_bsrm_sym(const NumericArgs &a, const BsrView &Bv, int64_t nrows, double *scratch,
                              const SymOut &so, cudaStream_t st, bool long_lists);
 void launch_sym_lidx(const SymOut &so, int64_t nbr, cudaStream_t st);

@@ -160,3 +160,18 @@ def test_symmetric_fallbacks(B, fail, monkeypatch):
     Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS)
     ok, res = parity(Eg, Eo, last_tau(tr, st))
     assert ok, (fail, res)
+
+
+def test_symmetric_wide_union(B, monkeypatch):
+    """K3c's first launch uses small candidate bitmaps; block rows whose union is wider set flag
+    32 and the count runs again with the widest (test hook SEXPM_K3C_WORDS shrinks the first
+    bitmaps to 2 words so that every 2D block row takes that path).  Parity with the oracle."""
+    H = make_config(5, scale_down=96)
+    monkeypatch.setenv("SEXPM_K3C_WORDS", "2")
+    Eg, st = run(B, H)
+    monkeypatch.delenv("SEXPM_K3C_WORDS")
+    assert st["sq_sym_used"] == int(st["N"]) >= 1
+    Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS)
+    ok, res = parity(Eg, Eo, last_tau(tr, st))
+    assert ok, res
+    assert exactly_symmetric(Eg)
