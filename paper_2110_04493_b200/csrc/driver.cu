@@ -2891,6 +2891,11 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
       P.agg_kind = Ld.dims == 2 ? 3 : 4;
       P.order_pending = false;
       mark("lattice order (device)");
+    } else if (P.dia_nd > 0 && std::max<int64_t>(-(int64_t)P.dia_dmin, (int64_t)P.dia_dmax) <= 4) {
+      // a band of half-width <= 4 (1D stencils) is best in index order: no host ordering
+      launch_iota_i32(nl, P.proc_order.p, st);
+      launch_iota_i32((nl + 7) / 8, P.block_order.p, st);
+      mark("index order (narrow band)");
     } else {
     CK(cudaEventCreateWithFlags(&P.ev_pattern, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&P.ev_order, cudaEventDisableTiming));
