@@ -4,7 +4,7 @@ import os, sys, json
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 from paper_2110_04493_b200 import binding as B
-ns = 1 << 25
+ns = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 25)
 dev = torch.device("cuda", 0)
 r_ = torch.arange(ns, device=dev, dtype=torch.int64)
 cnt_ = torch.full((ns,), 3, dtype=torch.int64, device=dev)
