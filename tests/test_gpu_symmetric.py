@@ -175,3 +175,22 @@ def test_symmetric_wide_union(B, monkeypatch):
     ok, res = parity(Eg, Eo, last_tau(tr, st))
     assert ok, res
     assert exactly_symmetric(Eg)
+
+
+@pytest.mark.parametrize("opts", [dict(output_T=True), dict(filter=0), dict(threshold_mode=1),
+                                  dict(plan_norm="fro")],
+                         ids=["output_T", "unfiltered", "abs_threshold", "fro_plan"])
+def test_symmetric_path_options(B, opts):
+    """The symmetric path (with its block-form hand-offs: config 2 squares 4+ times) under the
+    options that change what the squarings filter or return: T^_N instead of E, the unfiltered
+    PIM, the printed absolute budget, the Frobenius plan -- all against the oracle."""
+    # (the unfiltered oracle is slow on config 2: a 40 x 40 grid of the same law there)
+    H = laplacian_2d(40, 40, 1.0, "pm10", 5) if opts.get("filter") == 0 else make_config(2)
+    Eg, st = run(B, H, **opts)
+    N = int(st["N"])
+    assert N >= 3 and st["sq_sym_used"] == N
+    Eo, tr = O.expm(H, 1e-16, nthreads=NTHREADS, **opts)
+    assert (st["M"], st["N"]) == (tr["M"], tr["N"])
+    ok, res = parity(Eg, Eo, last_tau(tr, st))
+    assert ok, res
+    assert exactly_symmetric(Eg)
