@@ -67,6 +67,7 @@ typedef enum {
 } sexpm_status;
 
 typedef struct sexpm_plan_s *sexpm_plan_t;
+typedef struct sexpm_copy_s *sexpm_copy_t; /* a result copy in flight (sexpm_result_copy_async) */
 
 typedef struct {
   int64_t n;                  /* global dimension (n >= 1) */
@@ -256,6 +257,21 @@ int sexpm_run(sexpm_plan_t p, sexpm_csr_out *E);
 /* Copy the last result (rows+1 rowptr, nnz cols, nnz vals) into caller-owned arrays,
  * HOST (D2H, pinned or pageable) or DEVICE (D2D) pointers alike; synchronises the stream. */
 int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *vals);
+
+/* The same copy without waiting for it: E = I + T^_N (Algorithm 4.2 step 5) is DETACHED
+ * from the plan (which then has no result: sexpm_apply / sexpm_result_copy return
+ * SEXPM_ESTATE until the next sexpm_run) and copied on the library's own copy stream, ordered
+ * after the plan's stream; returns at once with *ticket.  The plan may be destroyed and the
+ * next plan created and run on any stream while the copy is in flight: with results larger
+ * than the link can move in one e^H (config 5: 14.6 GB over PCIe), consecutive e^H overlap
+ * their copy-out with the next computation.  The caller's arrays (HOST, pinned for overlap,
+ * or DEVICE) must not be read before sexpm_result_wait(ticket) returns; every ticket must
+ * be waited for exactly once (it frees the detached device blocks: they go back to the
+ * library's cache for the next plan's result).  sexpm_result_wait(NULL) is a no-op.
+ * Errors: SEXPM_ESTATE (no result), SEXPM_EINVAL (null arrays / ticket), SEXPM_ECUDA. */
+int sexpm_result_copy_async(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *vals,
+                            sexpm_copy_t *ticket);
+int sexpm_result_wait(sexpm_copy_t ticket);
 
 /* N1 apply: Y = R^steps X, R the last result (E = I + T^_N, or T^_N
  * with output_T), i.e. `steps` steps of the discretised system u_{k+1} = e^H u_k (Eq. 2.2,

@@ -27,6 +27,7 @@ EXPORTED = [
     "sexpm_filtered_product", "sexpm_alg41", "sexpm_halo_ranges", "sexpm_partition_rows",
     "sexpm_abi_sizes", "sexpm_kernel_launches", "sexpm_release_cache", "sexpm_apply",
     "sexpm_spmm", "sexpm_rcm", "sexpm_plan_scalars", "sexpm_fp64_peak", "sexpm_virtual_comm_create",
+    "sexpm_result_copy_async", "sexpm_result_wait",
 ]
 
 
@@ -110,6 +111,8 @@ def lib():
         L.sexpm_plan_host.argtypes = L.sexpm_plan.argtypes
         L.sexpm_run.argtypes = [P, C.POINTER(CsrOut)]
         L.sexpm_result_copy.argtypes = [P, P, P, P]
+        L.sexpm_result_copy_async.argtypes = [P, P, P, P, C.POINTER(C.c_void_p)]
+        L.sexpm_result_wait.argtypes = [P]
         L.sexpm_stats_get.argtypes = [P, C.POINTER(Stats)]
         L.sexpm_destroy.argtypes = [P]
         L.sexpm_filtered_product.argtypes = [P, C.POINTER(CsrIn), C.POINTER(CsrIn), C.c_double,
@@ -189,6 +192,18 @@ def sexpm_run(h) -> CsrOut:
 
 def sexpm_result_copy(h, rowptr_ptr: int, col_ptr: int, val_ptr: int):
     _check(lib().sexpm_result_copy(h, C.c_void_p(rowptr_ptr), C.c_void_p(col_ptr), C.c_void_p(val_ptr)))
+
+
+def sexpm_result_copy_async(h, rowptr_ptr: int, col_ptr: int, val_ptr: int):
+    """Detaches the result and starts its copy; returns the ticket for sexpm_result_wait."""
+    t = C.c_void_p()
+    _check(lib().sexpm_result_copy_async(h, C.c_void_p(rowptr_ptr), C.c_void_p(col_ptr),
+                                         C.c_void_p(val_ptr), C.byref(t)))
+    return t
+
+
+def sexpm_result_wait(ticket):
+    _check(lib().sexpm_result_wait(ticket))
 
 
 def sexpm_stats_get(h) -> dict:
@@ -284,6 +299,17 @@ def _torch():
     return torch
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the handle that names the legacy default stream
+
+
+def stream_handle(stream) -> int:
+    """cudaStream_t of a torch stream for sexpm_options.stream.  torch's default stream is the
+    legacy default stream, whose handle 0 would read as "NULL = a stream created by the plan":
+    pass cudaStreamLegacy instead, so the plan runs on the caller's stream."""
+    h = int(stream.cuda_stream)
+    return h if h != 0 else CUDA_STREAM_LEGACY
+
+
 class Plan:
     """One e^H computation (Algorithm 4.2) bound to the current CUDA device and stream."""
 
@@ -294,7 +320,7 @@ class Plan:
         if stream is None:
             stream = torch.cuda.current_stream()
         o = sexpm_options_init(**opts)
-        o.stream = stream.cuda_stream
+        o.stream = stream_handle(stream)
         if nccl_comm is not None:
             o.nccl_comm = nccl_comm
         self.n = int(n)
@@ -354,7 +380,7 @@ def expm_host(n, rowptr: np.ndarray, col: np.ndarray, val: np.ndarray, eps_tol=1
     the result inside sexpm_result_copy.  Returns numpy arrays (or fills `out`)."""
     torch = _torch()
     o = sexpm_options_init(**opts)
-    o.stream = torch.cuda.current_stream().cuda_stream
+    o.stream = stream_handle(torch.cuda.current_stream())
     rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
     col = np.ascontiguousarray(col, dtype=np.int32)
     val = np.ascontiguousarray(val, dtype=np.float64)
@@ -393,7 +419,7 @@ def _context(kernel=0):
     ci = torch.zeros(1, dtype=torch.int32, device=dev)
     va = torch.zeros(1, dtype=torch.float64, device=dev)
     o = sexpm_options_init(kernel=kernel)
-    o.stream = torch.cuda.current_stream().cuda_stream
+    o.stream = stream_handle(torch.cuda.current_stream())
     h = sexpm_plan(_csr_in(1, rp, ci, va), 1e-16, o)
     if kernel == 0:
         _ctx = h

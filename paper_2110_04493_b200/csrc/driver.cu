@@ -342,9 +342,11 @@ static void *alloc(size_t bytes, cudaStream_t st, size_t *got) {
             bytes_allocated / 1e9, bytes_cached / 1e9);
   return p;
 }
-// large blocks that are not parked (growth trails of a cold plan) go back to the CUDA pool
-// at once: only the parked final blocks and small blocks are kept
-constexpr size_t kKeepMax = (size_t)64 << 20;
+// very large blocks that are not parked (growth trails of a cold plan) go back to the CUDA
+// pool at once: only the parked final blocks and blocks under 1 GiB are kept (config 5 takes
+// eight 80-370 MB work buffers per plan: re-allocating them every plan cost 8 misses and an
+// occasional 100+ ms stall in cudaMallocAsync at 136 GB allocated)
+constexpr size_t kKeepMax = (size_t)1 << 30;
 static void free(void *p, size_t bytes, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -2737,6 +2739,7 @@ static void do_plan(sexpm_plan_s &P, const sexpm_csr_in *H, double eps_tol) {
   CK(cudaMemcpyAsync(&rp01[0], L.rp, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&rp01[1], L.rp + L.nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  mark("input + rowptr ends");
   REQUIRE(rp01[0] == 0 && rp01[1] == L.nnz, SEXPM_EINVAL, "rowptr[0] must be 0 and rowptr[rows] == nnz");
   launch_validate(L, P.n, w.flags.p, st);
   int vf = d2h(w.flags.p, st);
@@ -3848,8 +3851,19 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
     sexpm_options_init(&P->o);
   }
   CK(cudaGetDevice(&P->dev));
+  static std::mutex prop_mu;
+  static std::map<int, cudaDeviceProp> props;  // cudaGetDeviceProperties is slow: once per device
   cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, P->dev));
+  {
+    std::lock_guard<std::mutex> lk(prop_mu);
+    auto it = props.find(P->dev);
+    if (it == props.end()) {
+      CK(cudaGetDeviceProperties(&prop, P->dev));
+      props[P->dev] = prop;
+    } else {
+      prop = it->second;
+    }
+  }
   P->sm_count = prop.multiProcessorCount;
   P->smem_per_sm = prop.sharedMemPerMultiprocessor;
   {
@@ -3894,10 +3908,17 @@ static sexpm_plan_s *new_plan(const sexpm_options *o) {
     CK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
     P->own_stream = true;
   }
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, P->dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  {  // once per device: the pool keeps freed memory (no trimming at synchronisation points)
+    static std::mutex pool_mu;
+    static bool pool_set[64] = {};
+    std::lock_guard<std::mutex> lk(pool_mu);
+    cudaMemPool_t pool;
+    if (P->dev >= 0 && P->dev < 64 && !pool_set[P->dev] &&
+        cudaDeviceGetDefaultMemPool(&pool, P->dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      pool_set[P->dev] = true;
+    }
   }
   if (P->o.nccl_comm) {
     SxComm *c = as_comm(P->o.nccl_comm);
@@ -3925,7 +3946,11 @@ static int plan_common(const sexpm_csr_in *H, double eps_tol, const sexpm_option
   *out = nullptr;
   sexpm_plan_s *P = nullptr;
   try {
+    const auto tnp = std::chrono::steady_clock::now();
     P = new_plan(o);
+    if (getenv("SEXPM_PLAN_LOG"))
+      fprintf(stderr, "[sexpm plan] %-28s %8.2f ms\n", "new_plan",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tnp).count());
     if (host) {
       // copy the host CSR in (H2D inside the call, for end-to-end timing)
       sexpm_csr_in D = *H;
@@ -3998,6 +4023,125 @@ int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *
     CK(cudaMemcpyAsync(vals, p->E.val.p, p->E.nnz * sizeof(double), cudaMemcpyDefault, p->st));
   }
   CK(cudaStreamSynchronize(p->st));
+  ABI_END
+}
+
+// A result detached from its plan while its copy to the caller's arrays is in flight
+// (sexpm_result_copy_async / sexpm_result_wait).
+//
+// The copy engine serves the copies queued on it in order, whatever their stream: behind one
+// 14.6 GB copy (or behind its chunks, once they are all queued) every scalar the next plan
+// reads back (Algorithm 4.1's sums, counts: ~100 small D2H copies per e^H) waits for the whole
+// transfer (measured: the next sexpm_plan blocked for 265 ms).  So a host thread feeds the
+// engine: chunks of kCopyChunk bytes, at most kCopyDepth of them queued; a scalar read-back
+// of the running plan then waits for kCopyDepth chunks at most (~0.15 ms).
+struct sexpm_copy_s {
+  DBuf<int64_t> rp;
+  DBuf<int32_t> col;
+  DBuf<double> val;
+  int dev = 0;
+  cudaEvent_t ready = nullptr;  // the plan's stream has produced E
+  std::thread th;
+  cudaError_t err = cudaSuccess;
+  struct Seg {
+    char *dst;
+    const char *src;
+    size_t bytes;
+  } seg[3] = {};
+};
+static size_t env_size(const char *name, size_t dflt) {
+  const char *e = getenv(name);
+  return e && atoll(e) > 0 ? (size_t)atoll(e) : dflt;
+}
+static void copy_worker(sexpm_copy_s *c) {
+  const size_t chunk = env_size("SEXPM_COPY_CHUNK_KB", 4096) << 10;
+  const int depth = (int)std::min<size_t>(env_size("SEXPM_COPY_DEPTH", 2), 8);
+  // one copy stream per device for the life of the process (copies of consecutive results
+  // queue on it in order)
+  static std::mutex cs_mu;
+  static cudaStream_t cs_dev[64] = {};
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev[8] = {};
+  cudaError_t e = cudaSetDevice(c->dev);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(cs_mu);
+    if (!cs_dev[c->dev & 63]) {  // lowest priority: the running plan's read-backs go first
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      e = cudaStreamCreateWithPriority(&cs_dev[c->dev & 63], cudaStreamNonBlocking, lo);
+    }
+    cs = cs_dev[c->dev & 63];
+  }
+  for (int k = 0; k < depth && e == cudaSuccess; k++)
+    e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventSynchronize(c->ready);
+  long long q = 0;
+  for (int sgi = 0; sgi < 3 && e == cudaSuccess; sgi++) {
+    const sexpm_copy_s::Seg &sg = c->seg[sgi];
+    for (size_t o = 0; o < sg.bytes && e == cudaSuccess; o += chunk, q++) {
+      if (q >= depth) e = cudaEventSynchronize(ev[q % depth]);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(sg.dst + o, sg.src + o, std::min(chunk, sg.bytes - o), cudaMemcpyDefault, cs);
+      if (e == cudaSuccess) e = cudaEventRecord(ev[q % depth], cs);
+    }
+  }
+  if (cs) {
+    cudaError_t e2 = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = e2;
+  }
+  for (int k = 0; k < depth; k++)
+    if (ev[k]) cudaEventDestroy(ev[k]);
+  c->err = e;
+}
+
+int sexpm_result_copy_async(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *vals,
+                            sexpm_copy_t *ticket) {
+  ABI_BEGIN
+  REQUIRE(ticket, SEXPM_EINVAL, "null ticket");
+  *ticket = nullptr;
+  REQUIRE(p && p->have_result, SEXPM_ESTATE, "no result: call sexpm_run first");
+  REQUIRE(rowptr && (p->E.nnz == 0 || (colidx && vals)), SEXPM_EINVAL, "null host arrays");
+  sexpm_plan_s &P = *p;
+  std::unique_ptr<sexpm_copy_s> c(new sexpm_copy_s());
+  c->dev = P.dev;
+  CK(cudaEventCreateWithFlags(&c->ready, cudaEventDisableTiming));
+  cudaError_t e = cudaEventRecord(c->ready, P.st);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(c->ready);
+    CK(e);
+  }
+  const int64_t nrows = P.E.nrows, nnz = P.E.nnz;
+  // detach E: the copy reads it after the plan is gone; its blocks keep their cache roles, so
+  // sexpm_result_wait parks them for the next plan's result
+  const int r_rp = P.E.rp.role, r_col = P.E.col.role, r_val = P.E.val.role;
+  c->rp = std::move(P.E.rp);
+  c->col = std::move(P.E.col);
+  c->val = std::move(P.E.val);
+  c->rp.role = r_rp;
+  c->col.role = r_col;
+  c->val.role = r_val;
+  P.E.nnz = 0;
+  P.have_result = false;
+  c->seg[0] = {(char *)rowptr, (const char *)c->rp.p, (size_t)(nrows + 1) * sizeof(int64_t)};
+  c->seg[1] = {(char *)colidx, (const char *)c->col.p, (size_t)nnz * sizeof(int32_t)};
+  c->seg[2] = {(char *)vals, (const char *)c->val.p, (size_t)nnz * sizeof(double)};
+  c->th = std::thread(copy_worker, c.get());
+  *ticket = c.release();
+  ABI_END
+}
+
+int sexpm_result_wait(sexpm_copy_t t) {
+  ABI_BEGIN
+  if (!t) return SEXPM_OK;
+  std::unique_ptr<sexpm_copy_s> c(t);
+  if (c->th.joinable()) c->th.join();  // the worker has synchronised its stream
+  if (c->ready) cudaEventDestroy(c->ready);
+  const cudaError_t e = c->err;
+  if (e != cudaSuccess) cudaDeviceSynchronize();  // nothing may still read the blocks
+  cache::freeing_idle = true;  // the copy is complete: E's blocks are idle, park them
+  c.reset();
+  cache::freeing_idle = false;
+  CK(e);
   ABI_END
 }
 

@@ -7,7 +7,7 @@ H = make_config(5)
 dev = torch.device("cuda", 0)
 rp, ci, va = (torch.from_numpy(x).to(dev) for x in (H.rowptr, H.col, H.val))
 stream = torch.cuda.current_stream()
-for it in range(5):
+for it in range(int(os.environ.get("STEPS", "5"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     p = B.Plan(H.n, rp, ci, va, 1e-16, stream=stream)
