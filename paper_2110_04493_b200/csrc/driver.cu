@@ -4029,12 +4029,15 @@ int sexpm_result_copy(sexpm_plan_t p, int64_t *rowptr, int32_t *colidx, double *
 // A result detached from its plan while its copy to the caller's arrays is in flight
 // (sexpm_result_copy_async / sexpm_result_wait).
 //
-// The copy engine serves the copies queued on it in order, whatever their stream: behind one
-// 14.6 GB copy (or behind its chunks, once they are all queued) every scalar the next plan
-// reads back (Algorithm 4.1's sums, counts: ~100 small D2H copies per e^H) waits for the whole
-// transfer (measured: the next sexpm_plan blocked for 265 ms).  So a host thread feeds the
-// engine: chunks of kCopyChunk bytes, at most kCopyDepth of them queued; a scalar read-back
-// of the running plan then waits for kCopyDepth chunks at most (~0.15 ms).
+// A host thread waits for the plan's stream and then moves the three arrays on the library's
+// copy stream.  Destinations a kernel can write (pinned or registered host memory, device
+// memory) are written by k_copy_out, a few resident CTAs storing over the link; the copy
+// engines are left to the running plan.  Measured at config 5 with the copy engine instead:
+// behind one 14.6 GB copy the next plan's first scalar read-back waited for the whole
+// transfer (265 ms); in 4 MB chunks, 2 queued at a time, read-backs on the legacy default
+// stream got through, but one read-back per array still waited for that array's whole
+// transfer (85 + 180 ms inside the Taylor phase), and on created streams every one did: no
+// overlap either way (tools/ce_probe*.py).  Pageable destinations take that chunked path.
 struct sexpm_copy_s {
   DBuf<int64_t> rp;
   DBuf<int32_t> col;
@@ -4065,10 +4068,10 @@ static void copy_worker(sexpm_copy_s *c) {
   cudaError_t e = cudaSetDevice(c->dev);
   if (e == cudaSuccess) {
     std::lock_guard<std::mutex> lk(cs_mu);
-    if (!cs_dev[c->dev & 63]) {  // lowest priority: the running plan's read-backs go first
+    if (!cs_dev[c->dev & 63]) {  // highest priority: its few CTAs become resident at once
       int lo = 0, hi = 0;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      e = cudaStreamCreateWithPriority(&cs_dev[c->dev & 63], cudaStreamNonBlocking, lo);
+      e = cudaStreamCreateWithPriority(&cs_dev[c->dev & 63], cudaStreamNonBlocking, hi);
     }
     cs = cs_dev[c->dev & 63];
   }
@@ -4076,8 +4079,22 @@ static void copy_worker(sexpm_copy_s *c) {
     e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventSynchronize(c->ready);
   long long q = 0;
+  // config 5 (14.6 GB over PCIe 5 x16): 4 CTAs fall short of the link (the next e^H waits 25 ms
+  // for the copy), 6 keep up with it (~50 GB/s) and slow the running e^H by 35 ms, 32 by 115 ms
+  const int ctas = (int)env_size("SEXPM_COPY_CTAS", 6);
   for (int sgi = 0; sgi < 3 && e == cudaSuccess; sgi++) {
     const sexpm_copy_s::Seg &sg = c->seg[sgi];
+    // destinations a kernel can write (pinned / registered host memory, device memory): one
+    // kernel of a few resident CTAs per array; pageable host memory: the copy engine
+    cudaPointerAttributes pa;
+    const bool sm_path = !getenv("SEXPM_COPY_ENGINE") && sg.bytes > 0 &&
+                         cudaPointerGetAttributes(&pa, sg.dst) == cudaSuccess &&
+                         pa.type != cudaMemoryTypeUnregistered && pa.devicePointer != nullptr;
+    cudaGetLastError();
+    if (sm_path && launch_copy_out(pa.devicePointer, sg.src, sg.bytes, ctas, cs)) {
+      e = cudaGetLastError();
+      continue;
+    }
     for (size_t o = 0; o < sg.bytes && e == cudaSuccess; o += chunk, q++) {
       if (q >= depth) e = cudaEventSynchronize(ev[q % depth]);
       if (e == cudaSuccess)

@@ -4116,6 +4116,38 @@ void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, doub
   else if (m > 1) k_spmm<2, 1><<<grid, 256, 0, st>>>(A, m, X, ldx, Y, ldy);
   else k_spmv<<<grid, 256, 0, st>>>(A, X, ldx, Y, ldy);
 }
+
+// ------------------------------------------------------------------------------------
+// Result copy-out by the SMs (sexpm_result_copy_async): a few resident CTAs stream a
+// detached result to the caller's mapped pinned host (or device) memory with 16-byte stores
+// over the link.  The copy engines are left alone: a small read-back of the plan running
+// meanwhile was measured to wait behind a whole buffer's copy-engine transfer, however
+// finely that was chunked.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_copy_out(const uint4 *__restrict__ src, uint4 *__restrict__ dst,
+                                                  size_t n16, size_t tail_bytes) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+                d = __ldcs(src + i + 3 * stride);
+    __stcs(dst + i, a);
+    __stcs(dst + i + stride, b);
+    __stcs(dst + i + 2 * stride, c);
+    __stcs(dst + i + 3 * stride, d);
+  }
+  for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
+  if (blockIdx.x == 0 && threadIdx.x < tail_bytes)
+    ((unsigned char *)(dst + n16))[threadIdx.x] = ((const unsigned char *)(src + n16))[threadIdx.x];
+}
+
+bool launch_copy_out(void *dst, const void *src, size_t bytes, int ctas, cudaStream_t st) {
+  if ((((uintptr_t)dst) | ((uintptr_t)src)) & 15) return false;  // caller copies another way
+  if (bytes == 0) return true;
+  KL;
+  k_copy_out<<<std::max(1, ctas), 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, bytes / 16, bytes % 16);
+  return true;
+}
 }  // namespace sx
 
 namespace sx {

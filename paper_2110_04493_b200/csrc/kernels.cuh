@@ -373,6 +373,8 @@ void launch_merge_staged_write(const CsrView &A, const int64_t *alen, const int6
                                cudaStream_t st);
 // N1 apply: Y = A X, A CSR (rows A.nrows, global columns), X dense row-major (rows = A's
 // column range, ldx >= m), Y row-major (A.nrows x m, ldy >= m)
+// result copy-out by resident CTAs (false: pointers not 16-byte aligned, nothing launched)
+bool launch_copy_out(void *dst, const void *src, size_t bytes, int ctas, cudaStream_t st);
 void launch_spmm(const CsrView &A, int64_t m, const double *X, int64_t ldx, double *Y, int64_t ldy,
                  cudaStream_t st);
 // N3 reverse Cuthill-McKee (driver.cu compute_rcm runs the level loop)

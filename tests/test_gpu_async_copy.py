@@ -111,3 +111,36 @@ def test_async_copy_errors_and_device_destination(B):
     B.sexpm_result_wait(t)
     for a, b in zip(ref, out):
         assert torch.equal(a, b)
+
+
+def test_async_copy_pageable_and_unaligned_destinations(B):
+    """Pageable host arrays (copy-engine path) and pinned arrays that are not 16-byte aligned
+    (k_copy_out refuses them: copy-engine path) receive the result of sexpm_result_copy."""
+    import torch
+    H = make_config(2)
+    d = to_dev(H)
+    res = []
+    for kind in ("sync", "pageable", "unaligned"):
+        h, E = _plan_run(B, H, d)
+        if kind == "sync":
+            bufs = _pinned(H.n, E.nnz)
+            B.sexpm_result_copy(h, *(b.data_ptr() for b in bufs))
+            out = [bufs[0].numpy().copy(), bufs[1][:E.nnz].numpy().copy(), bufs[2][:E.nnz].numpy().copy()]
+        elif kind == "pageable":
+            out = [np.full(H.n + 1, -1, np.int64), np.full(E.nnz, -1, np.int32), np.full(E.nnz, -1.0)]
+            t = B.sexpm_result_copy_async(h, *(a.ctypes.data for a in out))
+            B.sexpm_result_wait(t)
+        else:
+            raw = (torch.empty(H.n + 2, dtype=torch.int64).pin_memory(),
+                   torch.empty(E.nnz + 1, dtype=torch.int32).pin_memory(),
+                   torch.empty(E.nnz + 1, dtype=torch.float64).pin_memory())
+            views = [r[1:] for r in raw]  # offsets of 8, 4 and 8 bytes
+            assert all(v.data_ptr() % 16 != 0 for v in views)
+            t = B.sexpm_result_copy_async(h, *(v.data_ptr() for v in views))
+            B.sexpm_result_wait(t)
+            out = [v.numpy().copy() for v in views]
+        B.sexpm_destroy(h)
+        res.append(out)
+    for out in res[1:]:
+        for a, b in zip(res[0], out):
+            assert np.array_equal(a, b)
