@@ -141,7 +141,9 @@ typedef struct {
                              T^_0 by rounding only).  Falls back to the full product when a
                              block row does not fit.  0 = off (the full product). */
   double e_r;             /* Algorithm 4.1 tolerance e_r > 0 (default 0.1, R6) */
-  void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan) */
+  void *stream;           /* cudaStream_t to run on (NULL = a stream created by the plan; to run
+                             on the legacy default stream pass cudaStreamLegacy, as the Python
+                             binding does for torch's default stream) */
   void *nccl_comm;        /* communicator handle from sexpm_nccl_comm_init (NCCL) or
                              sexpm_virtual_comm_create (virtual ranks), or NULL for one GPU */
 } sexpm_options;
