@@ -315,7 +315,7 @@ def main():
             # landed.  The one-shot figure above stays as `serial_value`.
             if 2 * est_out_bytes <= 0.5 * avail:
                 sets = [outbufs, tuple(torch.empty_like(t).pin_memory() for t in outbufs)]
-                ke, kw = max(4, min(args.steps, 10)), 3
+                ke, kw = max(8, min(args.steps, 16)), 3
 
                 def pipelined(k, mark_at):
                     """k consecutive e^H; returns the wall time from the start of step mark_at
