@@ -87,3 +87,11 @@ def test_compute_without_gpu_fails_loudly():
     H = B._csr_in(1, rp, ci, va, host=True)
     with pytest.raises(B.SexpmError):
         B.sexpm_plan_host(H, 1e-16, o)
+
+
+def test_stream_handle_maps_default_stream_to_legacy_handle():
+    """torch's default stream has handle 0, which sexpm_options.stream reads as "create a
+    stream": the binding passes cudaStreamLegacy (1) instead; other handles pass through."""
+    from types import SimpleNamespace
+    assert B.stream_handle(SimpleNamespace(cuda_stream=0)) == B.CUDA_STREAM_LEGACY == 1
+    assert B.stream_handle(SimpleNamespace(cuda_stream=0x7F00DEAD)) == 0x7F00DEAD
